@@ -1,0 +1,264 @@
+"""Pins for the CPU oracle (oracle/) against what the paper and mathematics fix.
+
+None of these compares the oracle with itself: every expected value is a
+closed form of the paper (identity, FFT-multiply-iFFT propagator, lattice
+shift), a library routine the definition reduces to (numpy FFT), an exact
+invariant (Parseval, partition of unity, adjoint pairing, linearity) or a
+printed/worked value (tests/golden/spec_examples.json).  Each test names the
+mistake it would catch.
+"""
+import json
+import os
+
+import numpy as np
+import pytest
+
+import oracle
+import workloads as wl
+
+GOLD = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "spec_examples.json")))
+rng = np.random.default_rng(1234)
+
+
+def crandn(*shape):
+    return rng.standard_normal(shape) + 1j * rng.standard_normal(shape)
+
+
+def multiplier(N, m):
+    """N * ifft2(m * fhat): (1/N) sum_xi e^{2 pi i x.xi} m(xi) fhat(xi) for a Fourier multiplier."""
+    return lambda fhat: N * np.fft.ifft2(m * fhat)
+
+
+# ------------------------------------------------------------------ DFT (eq. dft)
+def test_dft_impulse_golden():
+    g = GOLD["dft_impulse_N4"]
+    f = np.zeros((g["N"], g["N"]), complex)
+    f[0, 0] = 1
+    np.testing.assert_allclose(oracle.dft2(f), g["value"], atol=1e-15)
+
+
+def test_dft_constant_golden():
+    g = GOLD["dft_constant_N8"]
+    N = g["N"]
+    fh = oracle.dft2(np.ones((N, N), complex))
+    assert abs(fh[0, 0] - g["dc"]) < 1e-13
+    fh[0, 0] = 0
+    assert np.abs(fh).max() < 1e-13
+
+
+@pytest.mark.parametrize("N", [6, 16, 30])
+def test_dft_matches_library_fft_and_parseval(N):
+    # catches: sign of the exponent, 1/N normalisation, transposed axes, index wrap
+    f = crandn(N, N)
+    fh = oracle.dft2(f)
+    np.testing.assert_allclose(fh, np.fft.fft2(f) / N, atol=1e-12)
+    assert abs(np.linalg.norm(fh) / np.linalg.norm(f) - 1) < 1e-13
+    f2 = np.zeros((N, N), complex)
+    f2[1, 0] = 1.0  # x = (1/N, 0): fhat(xi) = e^{-2 pi i xi1/N}/N depends on k1 only
+    k = np.arange(N)
+    np.testing.assert_allclose(oracle.dft2(f2)[:, 3], np.exp(-2j * np.pi * k / N) / N, atol=1e-14)
+
+
+# ------------------------------------------------------------------ eq. dfio closed forms
+@pytest.mark.parametrize("N", [8, 16, 22])
+def test_identity_phase_is_inverse_dft(N):
+    # Phi = x.xi makes L the inverse DFT, so L(f) = f
+    f = crandn(N, N)
+    np.testing.assert_allclose(oracle.fio(wl.identity_operator(N), f), f, atol=1e-12)
+
+
+@pytest.mark.parametrize("c1,c2", [(0.7, 0.7), (0.3, 1.7)])
+def test_constant_radii_is_fourier_multiplier(c1, c2):
+    # PAPER.md:109-119 (c1 = c2 = c t is the wave propagator); c1 != c2 pins xi1 <-> axis 0
+    N = 16
+    f = crandn(N, N)
+    fh = np.fft.fft2(f) / N
+    xi1, xi2 = wl.freqs(N)
+    m = np.exp(2j * np.pi * np.sqrt(c1 ** 2 * xi1 ** 2 + c2 ** 2 * xi2 ** 2))
+    np.testing.assert_allclose(oracle.fio(wl.const_ellipse_operator(N, c1, c2), f),
+                               multiplier(N, m)(fh), atol=1e-11)
+
+
+def test_constant_shift_is_roll():
+    # Phi = (x + d).xi, d = k/N: Lf[n] = f[n + k] exactly (reading R12)
+    N = 16
+    f = crandn(N, N)
+    out = oracle.fio(wl.shift_operator(N, 3, -5), f)
+    np.testing.assert_allclose(out, np.roll(f, (-3, 5), axis=(0, 1)), atol=1e-12)
+
+
+def test_pointwise_shift_pins_spatial_indexing():
+    # b(x) varies with x: Lf[n1,n2] = f[n1 + k1(n), n2 + k2(n)] -- catches a transposed or
+    # mis-indexed spatial coefficient array
+    N = 12
+    f = crandn(N, N)
+    n1, n2 = np.meshgrid(np.arange(N), np.arange(N), indexing="ij")
+    k1 = (n1 + 2 * n2) % 3 - 1
+    k2 = (n1 * n2) % 5 - 2
+    out = oracle.fio(wl.shift_operator(N, k1, k2), f)
+    np.testing.assert_allclose(out, f[(n1 + k1) % N, (n2 + k2) % N], atol=1e-12)
+
+
+def test_piecewise_radii_pins_c1_c2_indexing():
+    # c1, c2 piecewise constant in x: at each x, Lf(x) is the constant-radius multiplier
+    # with the radii of that x (the sum over xi is local in x) -- catches c1/c2 swapped,
+    # a transposed c array, or a dropped square
+    N = 16
+    f = crandn(N, N)
+    fh = np.fft.fft2(f) / N
+    n1, n2 = np.meshgrid(np.arange(N), np.arange(N), indexing="ij")
+    ma = (n1 < 5)
+    mb = ((n1 + 3 * n2) % 4 == 0)
+    A1, B1, A2, B2 = 0.3, 1.1, 0.9, 0.45
+    c1 = np.where(ma, A1, B1)
+    c2 = np.where(mb, A2, B2)
+    op = wl.Operator(N, c1, c2)
+    xi1, xi2 = wl.freqs(N)
+    exp_ = np.zeros((N, N), complex)
+    for v1 in (A1, B1):
+        for v2 in (A2, B2):
+            P = multiplier(N, np.exp(2j * np.pi * np.sqrt(v1 ** 2 * xi1 ** 2 + v2 ** 2 * xi2 ** 2)))(fh)
+            sel = (c1 == v1) & (c2 == v2)
+            exp_[sel] = P[sel]
+    np.testing.assert_allclose(oracle.fio(op, f), exp_, atol=1e-11)
+
+
+def test_wave_amplitude_closed_form():
+    # config 2's amplitude a = 1 + 0.1 cos(2 pi x1) xi1/|xi| with constant c: L = M0 + 0.1 cos(2 pi x1) M1
+    # (a complex spatial factor is used so that a dropped conj/imag part shows)
+    N = 16
+    t = 0.1
+    f = crandn(N, N)
+    fh = np.fft.fft2(f) / N
+    base = wl.wave_operator(N, t)
+    c = 1.37 * t
+    px = base.px.copy()
+    px[1] = px[1] * np.exp(0.4j)
+    op = wl.Operator(N, np.full((N, N), c), np.full((N, N), c), px=px, pxi=base.pxi)
+    xi1, xi2 = wl.freqs(N)
+    r = np.sqrt(xi1 ** 2 + xi2 ** 2)
+    m0 = np.exp(2j * np.pi * c * r)
+    ratio = np.where(r > 0, xi1 / np.where(r > 0, r, 1), 0)
+    x1, _ = wl.grid(N)
+    exp_ = multiplier(N, m0)(fh) + 0.1 * np.exp(0.4j) * np.cos(2 * np.pi * x1) * multiplier(N, m0 * ratio)(fh)
+    np.testing.assert_allclose(oracle.fio(op, f), exp_, atol=1e-11)
+
+
+def test_single_mode():
+    # fhat = delta_{xi0}: (Lf)(x) = (1/N) a(x,xi0) e^{2 pi i Phi(x, xi0)} -- the GRT phase at
+    # one frequency; checks the per-term phase reduction against numpy at large |xi|
+    N = 32
+    op = wl.grt_operator(N)
+    fh = np.zeros((N, N), complex)
+    xi0 = (-16, 11)
+    fh[xi0[0] % N, xi0[1] % N] = 1.0
+    x1, x2 = wl.grid(N)
+    phi = x1 * xi0[0] + x2 * xi0[1] + np.sqrt(op.c1 ** 2 * xi0[0] ** 2 + op.c2 ** 2 * xi0[1] ** 2)
+    np.testing.assert_allclose(oracle.fio(op, fhat=fh), np.exp(2j * np.pi * phi) / N, atol=1e-13)
+
+
+# ------------------------------------------------------------------ invariants
+def test_linearity_and_sampling_consistency():
+    N = 16
+    op = wl.grt_operator(N)
+    f, g = crandn(N, N), crandn(N, N)
+    a, b = 0.3 - 1.2j, 2.1
+    Lf, Lg = oracle.fio(op, f), oracle.fio(op, g)
+    np.testing.assert_allclose(oracle.fio(op, a * f + b * g), a * Lf + b * Lg, atol=1e-12)
+    pts = wl.sample_points(N, 40, seed=3)
+    # sampled mode must equal the full grid bit for bit (same sum order)
+    assert np.array_equal(oracle.fio(op, f, pts=pts), Lf.ravel()[pts])
+
+
+def test_partition_of_unity():
+    # sum_l chi_l = 1: sum of per-wedge partial operators + DC = L
+    N, W = 16, 8
+    op = wl.grt_operator(N)
+    f = crandn(N, N)
+    full = oracle.fio(op, f)
+    acc = oracle.fio(op, f, wedges=[], W=W, include_dc=True)
+    parts = []
+    for l in range(W):
+        p = oracle.fio(op, f, wedges=[l], W=W, include_dc=False)
+        parts.append(np.linalg.norm(p))
+        acc = acc + p
+    np.testing.assert_allclose(acc, full, atol=1e-12)
+    assert min(parts) > 1e-3 * max(parts)
+
+
+def test_adjoint_pairing():
+    # <L f, g>_X = <fhat, widehat(L* g)>_Omega (DFT unitary)
+    N = 12
+    op = wl.wave_operator(N)
+    f, g = crandn(N, N), crandn(N, N)
+    lhs = np.vdot(g, oracle.fio(op, f))
+    rhs = np.vdot(oracle.fio_adjoint_hat(op, g), oracle.dft2(f))
+    assert abs(lhs - rhs) < 1e-11 * abs(lhs)
+
+
+# ------------------------------------------------------------------ wedges
+def test_wedge_golden_examples():
+    g = GOLD["wedges_N64"]
+    for xi1, xi2, l in g["members"]:
+        assert oracle.wedge_of(g["W"], xi1, xi2) == l
+    assert oracle.wedge_of(8, 0, 0) == -1
+
+
+@pytest.mark.parametrize("N,W", [(16, 8), (64, 8), (32, 12)])
+def test_wedge_membership_by_cross_products(N, W):
+    # independent check of arg-interval membership with long-double boundary rays
+    xi1, xi2 = wl.freqs(N)
+    pi = np.longdouble(np.pi)
+    count = np.zeros(W, int)
+    for a, b in zip(xi1.ravel(), xi2.ravel()):
+        l = oracle.wedge_of(W, int(a), int(b))
+        if a == 0 and b == 0:
+            assert l == -1
+            continue
+        count[l] += 1
+        lo = (2 * l - 1) * pi / W
+        hi = (2 * l + 1) * pi / W
+        A, B = np.longdouble(a), np.longdouble(b)
+        assert np.cos(lo) * B - np.sin(lo) * A >= 0
+        assert np.cos(hi) * B - np.sin(hi) * A < 0
+    assert count.sum() == N * N - 1 and count.min() > 0
+
+
+# ------------------------------------------------------------------ NUDFT component oracle
+def test_nudft_single_coefficient_and_uniform_targets():
+    n1, n2 = 6, 10
+    c = np.zeros((n1, n2), complex)
+    c[1, 7] = 2 - 1j  # k = (1 - 3, 7 - 5) = (-2, 2)
+    y = rng.random((50, 2)) * 3 - 1
+    np.testing.assert_allclose(oracle.nudft2(c, y), (2 - 1j) * np.exp(2j * np.pi * (-2 * y[:, 0] + 2 * y[:, 1])),
+                               atol=1e-13)
+    # uniform targets y = j/n reduce to an (un-normalised) inverse FFT
+    c = crandn(n1, n2)
+    j1, j2 = np.meshgrid(np.arange(n1), np.arange(n2), indexing="ij")
+    y = np.stack([j1.ravel() / n1, j2.ravel() / n2], axis=1)
+    ref = np.fft.ifft2(np.fft.ifftshift(c)) * n1 * n2
+    np.testing.assert_allclose(oracle.nudft2(c, y).reshape(n1, n2), ref, atol=1e-11)
+
+
+# ------------------------------------------------------------------ workloads
+def test_workload_radii_golden():
+    g = GOLD["grt_radii"]
+    N = 64
+    op = wl.grt_operator(N)
+    for x1, x2, c1, c2 in g["points"]:
+        i, j = int(round(x1 * N)), int(round(x2 * N))
+        assert abs(op.c1[i, j] - c1) < 1e-15 and abs(op.c2[i, j] - c2) < 1e-15
+    p = wl.paper_ellipse_operator(N)
+    assert abs(p.c1[0, 0] - GOLD["paper_radii_at_origin"]["r1"]) < 1e-15
+    assert abs(p.c2[0, 0] - GOLD["paper_radii_at_origin"]["r2"]) < 1e-15
+
+
+def test_workload_inputs_deterministic():
+    a = wl.white_noise(32, 0)
+    assert np.array_equal(a, wl.white_noise(32, 0)) and np.all(a.imag == 0)
+    b = wl.white_noise(32, 0, "c64")
+    assert np.array_equal(b.real.astype(np.float32).astype(np.float64), b.real)
+    g = wl.gaussian_bumps(64, 0)
+    assert g.shape == (64, 64) and np.abs(g).max() > 0.1
+    p = wl.sample_points(1024, 4096, 1)
+    assert len(np.unique(p)) == 4096 and np.all(np.diff(p) > 0)
