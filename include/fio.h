@@ -1,0 +1,165 @@
+/*
+ * fio.h -- C ABI of the B200-native fast Fourier integral operator apply
+ * (Candes, Demanet, Ying, "Fast computation of Fourier integral operators",
+ * arXiv math/0610051; the paper text is cited as PAPER.md:<line>).
+ *
+ * The library evaluates the discrete FIO of eq. (dfio), PAPER.md:165-168,
+ *
+ *     (Lf)(x) = (1/N) sum_{xi in Omega} a(x,xi) e^{2 pi i Phi(x,xi)} fhat(xi),
+ *     fhat(xi) = (1/N) sum_{x in X} e^{-2 pi i x.xi} f(x)      (eq. dft)
+ *
+ * on the grid X = {(n1/N, n2/N)}, Omega = [-N/2, N/2)^2
+ * (PAPER.md:172-174), with the wedge-decomposed algorithm of PAPER.md:332-378:
+ * W angular wedges, per wedge a residual kernel separated
+ * to rank q_l by a randomized skeleton, and per (l,t) a
+ * type-2 NUFFT at the warped points (M_l^{-T} grad_xi Phi(x, xihat_l))
+ * whose result is multiplied by alpha_lt(x) and summed
+ * (PAPER.md:1296-1302).
+ *
+ * Preprocessing (fio_plan) is done once per (Phi, a, eps) and reused for many
+ * f.  Evaluation (fio_apply) runs entirely in this
+ * library's sm_100a CUDA kernels; there is no CPU fallback.
+ *
+ * Conventions used by every entry point
+ *  - complex arrays are interleaved (re, im); C64 = 2 x float, C128 = 2 x double.
+ *  - spatial arrays are row-major N x N over (n1, n2), x = (n1/N, n2/N); axis 0
+ *    is x1 <-> xi1 (reading R14).
+ *  - frequency arrays are N x N in FFT-natural order: index k stands for
+ *    xi = k - N [k >= N/2].
+ *  - every call returns fio_status: 0 ok, < 0 error (nothing was done, the
+ *    message is in fio_last_error()), > 0 warning (the call did its work).
+ *  - the library never frees caller memory; handles own their device memory
+ *    and release it in fio_destroy.
+ */
+#ifndef FIO_B200_H
+#define FIO_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct fio_plan_s* fio_handle; /* opaque, owned by the library */
+
+typedef enum { FIO_C64 = 1, FIO_C128 = 2 } fio_dtype;
+
+typedef enum {
+  FIO_OK = 0,
+  FIO_WNOTCERT = 1,   /* plan built, but a wedge's sampled separation error
+                          exceeded eps; it still evaluates */
+  FIO_EINVAL = -1,    /* bad argument (message says which) */
+  FIO_ENOMEM = -2,    /* device or host allocation failed */
+  FIO_ECUDA = -3,     /* CUDA runtime error (launch or sync) */
+  FIO_ENCCL = -4,     /* reserved: collective failure */
+  FIO_ENOTHOMOG = -5, /* reserved: phase failed the degree-1 homogeneity check */
+  FIO_EINTERNAL = -6  /* internal invariant violated (a bug) */
+} fio_status;
+
+/* The phase, PAPER.md:54-61 (homogeneous of degree 1 in xi), given as data on X:
+ *     Phi(x,xi) = x.xi + b(x).xi + sqrt(c1(x)^2 xi1^2 + c2(x)^2 xi2^2).
+ * This family contains the identity (c = b = 0), the wave
+ * propagator x.xi +- c|xi|t (c1 = c2 = c t), the paper's
+ * ellipse phases (eq. nrphase) and every BASELINE config.
+ * c1, c2: host arrays of N*N doubles (required).  b1, b2: N*N doubles or NULL (0).
+ * The library copies them during fio_plan. */
+typedef struct {
+  const double* c1;
+  const double* c2;
+  const double* b1;
+  const double* b2;
+} fio_phase;
+
+/* The amplitude (order-0 symbol), rank-K separable on the grids:
+ *     a(x,xi) = sum_{k<K} px_k(x) pxi_k(xi).
+ * K = 0 (px = pxi = NULL) is a == 1, the Egorov operator of PAPER.md:972-977.
+ * px: K*N*N interleaved complex doubles over X; pxi: K*N*N over Omega in FFT
+ * order.  Copied during fio_plan.  The amplitude is folded into the separated
+ * kernel (reading R9). */
+typedef struct {
+  int K;
+  const double* px;
+  const double* pxi;
+} fio_amplitude;
+
+/* Options; fio_default_opts() fills the defaults shown. */
+typedef struct {
+  fio_dtype dtype;    /* FIO_C128 */
+  int n_wedges;       /* 0 -> W = 8 round(sqrt(N)/8), >= 8 (reading R1) */
+  int nufft_w;        /* 0 -> taps per dimension chosen from eps (reading R10) */
+  double nufft_beta;  /* 0 -> 2.30 w (exponential-of-semicircle kernel) */
+  uint64_t seed;      /* 0x5EED: seed of the randomized separation */
+  int device;         /* CUDA device ordinal; -1 -> current device */
+  int rank, nranks;   /* 0, 1: this process owns the wedges assigned to `rank`
+                         among `nranks` (BASELINE north_star (3)) */
+  int r_init;         /* 32: initial skeleton size r of PAPER.md:1211-1221 */
+  int r_max;          /* 512: cap of the doubling */
+  int certify;        /* 1: compute the sampled error of PAPER.md:1464-1477 */
+} fio_opts;
+
+void fio_default_opts(fio_opts* opts);
+
+/* Build a plan for the N x N operator (N even, 5-smooth, 8 <= N <= 8192) at
+ * separation accuracy eps in (0, 1) (the relative singular
+ * value cutoff, reading R6).  opts may be NULL (defaults).  Runs on the device
+ * (kernel-entry evaluation, Gram products, factor expansion) and the host
+ * (partition, pivoting, small Jacobi SVDs).  Synchronous.
+ * Returns FIO_OK, FIO_WNOTCERT, or an error (*out is then NULL). */
+fio_status fio_plan(fio_handle* out, int N, const fio_phase* phase, const fio_amplitude* amp,
+                    double eps, const fio_opts* opts);
+
+/* Evaluate L f.  f_dev: device N x N complex of the plan dtype (caller-owned,
+ * read-only).  Lf_dev: device N x N complex of the plan dtype (caller-owned,
+ * fully overwritten; must not alias f_dev).  With nranks > 1, Lf_dev receives
+ * this rank's partial sum over its own wedges (the DC term is added on rank
+ * 0 only); the caller sums the partials across ranks (reduce-scatter).
+ * stream: a cudaStream_t (NULL = legacy default stream).  Asynchronous on
+ * `stream`; one apply in flight per handle (the workspace is per handle). */
+fio_status fio_apply(fio_handle h, const void* f_dev, void* Lf_dev, void* stream);
+
+/* End-to-end variant: f_host / Lf_host are HOST buffers (pinned for overlap);
+ * the host->device copy, the apply and the device->host copy are enqueued on
+ * `stream`, which is synchronized before return. */
+fio_status fio_apply_host(fio_handle h, const void* f_host, void* Lf_host, void* stream);
+
+fio_status fio_destroy(fio_handle h);
+
+typedef struct {
+  int N, W, nufft_w, dtype, rank, nranks;
+  int n_owned;            /* wedges owned by this rank */
+  int sum_q;              /* sum of q_l over owned wedges */
+  int certified;          /* 1 if every owned wedge passed the sampled check */
+  double nufft_beta;
+  double max_sep_err;     /* max sampled relative Frobenius error */
+  double plan_seconds;
+  size_t alpha_bytes, beta_bytes, workspace_bytes, fine_elems, p1_elems;
+  int launches_per_apply; /* kernels one fio_apply enqueues */
+} fio_info;
+
+fio_status fio_plan_info(fio_handle h, fio_info* info);
+
+/* Per owned wedge: l, q_l, n1, n2, n1f, n2f, M (4 ints, row-major), xi_c (2 ints),
+ * r (final skeleton size) and the sampled error; arrays of length >= n_owned
+ * (any pointer may be NULL). */
+fio_status fio_plan_wedges(fio_handle h, int* l, int* q, int* box /* 4 per wedge */,
+                           int* M /* 4 per wedge */, int* xc /* 2 per wedge */, int* r,
+                           double* sep_err);
+
+/* Host-only geometry of the partition (no GPU needed; used by the CPU tests):
+ * wedge_of[k1*N+k2] = wedge of xi(k) in [0,W) or -1 for xi = 0 (PAPER.md:214-217,
+ * readings R3/R4); for each wedge: M (4 ints), xi_c (2), box n1,n2 and fine n1f,n2f
+ * (4) as chosen by the plan (reading R5). */
+fio_status fio_geometry(int N, int W, int* wedge_of, int* M, int* xc, int* box);
+
+/* Wedge -> rank assignment used for nranks > 1 (owner[l] in [0, nranks)), from
+ * per-wedge costs (longest-processing-time greedy, deterministic). Host-only. */
+fio_status fio_assign_wedges(int W, const double* cost, int nranks, int* owner);
+
+const char* fio_last_error(void); /* thread-local message of the last error */
+const char* fio_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* FIO_B200_H */

@@ -1,0 +1,249 @@
+"""paper_math_0610051_b200 -- B200-native fast Fourier integral operator apply.
+
+Thin ctypes binding over the C ABI of include/fio.h (libfio_b200.so, built
+in-tree for sm_100a by paper_math_0610051_b200/build.py).  This module only
+marshals arguments: the plan's heavy steps and every step of fio_apply run in
+the library's CUDA kernels.  There is no CPU fallback -- if the library or a
+CUDA device is missing, calls raise.
+
+    Plan(N, c1, c2, ...)      fio_plan
+    Plan.apply(f)             fio_apply, device tensors
+    Plan.apply_host(f, out)   fio_apply_host (host buffers, copies included)
+    Plan.apply_sharded(f, g)  per-rank partial + reduce-scatter over NCCL
+    geometry(N, W)            fio_geometry (host only)
+    assign_wedges(cost, R)    fio_assign_wedges (host only)
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from typing import Optional
+
+import numpy as np
+
+__all__ = ["FioError", "Plan", "geometry", "assign_wedges", "library_path", "load_library", "SYMBOLS"]
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_LIB_PATH = os.path.join(_HERE, "libfio_b200.so")
+_lib = None
+
+FIO_C64, FIO_C128 = 1, 2
+FIO_OK, FIO_WNOTCERT = 0, 1
+
+# every entry point declared in include/fio.h
+SYMBOLS = ["fio_default_opts", "fio_plan", "fio_apply", "fio_apply_host", "fio_destroy", "fio_plan_info",
+           "fio_plan_wedges", "fio_geometry", "fio_assign_wedges", "fio_last_error", "fio_version"]
+
+
+class FioError(RuntimeError):
+    def __init__(self, code: int, msg: str):
+        super().__init__(f"fio error {code}: {msg}")
+        self.code = code
+
+
+class _Phase(ctypes.Structure):
+    _fields_ = [("c1", ctypes.c_void_p), ("c2", ctypes.c_void_p), ("b1", ctypes.c_void_p), ("b2", ctypes.c_void_p)]
+
+
+class _Amp(ctypes.Structure):
+    _fields_ = [("K", ctypes.c_int), ("px", ctypes.c_void_p), ("pxi", ctypes.c_void_p)]
+
+
+class _Opts(ctypes.Structure):
+    _fields_ = [("dtype", ctypes.c_int), ("n_wedges", ctypes.c_int), ("nufft_w", ctypes.c_int),
+                ("nufft_beta", ctypes.c_double), ("seed", ctypes.c_uint64), ("device", ctypes.c_int),
+                ("rank", ctypes.c_int), ("nranks", ctypes.c_int), ("r_init", ctypes.c_int),
+                ("r_max", ctypes.c_int), ("certify", ctypes.c_int)]
+
+
+class _Info(ctypes.Structure):
+    _fields_ = [("N", ctypes.c_int), ("W", ctypes.c_int), ("nufft_w", ctypes.c_int), ("dtype", ctypes.c_int),
+                ("rank", ctypes.c_int), ("nranks", ctypes.c_int), ("n_owned", ctypes.c_int),
+                ("sum_q", ctypes.c_int), ("certified", ctypes.c_int), ("nufft_beta", ctypes.c_double),
+                ("max_sep_err", ctypes.c_double), ("plan_seconds", ctypes.c_double),
+                ("alpha_bytes", ctypes.c_size_t), ("beta_bytes", ctypes.c_size_t),
+                ("workspace_bytes", ctypes.c_size_t), ("fine_elems", ctypes.c_size_t),
+                ("p1_elems", ctypes.c_size_t), ("launches_per_apply", ctypes.c_int)]
+
+
+def library_path() -> str:
+    return _LIB_PATH
+
+
+def load_library():
+    """Load libfio_b200.so (building it first if its sources are newer).  Raises if it cannot."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    from . import build as _build
+    if not _build.up_to_date():
+        _build.build()
+    lib = ctypes.CDLL(_LIB_PATH)
+    P, I = ctypes.c_void_p, ctypes.c_int
+    lib.fio_default_opts.argtypes = [ctypes.POINTER(_Opts)]
+    lib.fio_default_opts.restype = None
+    lib.fio_plan.argtypes = [ctypes.POINTER(P), I, ctypes.POINTER(_Phase), ctypes.POINTER(_Amp), ctypes.c_double,
+                             ctypes.POINTER(_Opts)]
+    lib.fio_apply.argtypes = [P, P, P, P]
+    lib.fio_apply_host.argtypes = [P, P, P, P]
+    lib.fio_destroy.argtypes = [P]
+    lib.fio_plan_info.argtypes = [P, ctypes.POINTER(_Info)]
+    lib.fio_plan_wedges.argtypes = [P, P, P, P, P, P, P, P]
+    lib.fio_geometry.argtypes = [I, I, P, P, P, P]
+    lib.fio_assign_wedges.argtypes = [I, P, I, P]
+    lib.fio_last_error.restype = ctypes.c_char_p
+    lib.fio_version.restype = ctypes.c_char_p
+    for name in ["fio_plan", "fio_apply", "fio_apply_host", "fio_destroy", "fio_plan_info", "fio_plan_wedges",
+                 "fio_geometry", "fio_assign_wedges"]:
+        getattr(lib, name).restype = ctypes.c_int
+    _lib = lib
+    return lib
+
+
+def _check(code: int) -> int:
+    if code < 0:
+        raise FioError(code, load_library().fio_last_error().decode())
+    return code
+
+
+def _ptr(a: Optional[np.ndarray]):
+    return None if a is None else a.ctypes.data_as(ctypes.c_void_p)
+
+
+def _f64(a) -> Optional[np.ndarray]:
+    return None if a is None else np.ascontiguousarray(a, dtype=np.float64)
+
+
+def _c128(a) -> Optional[np.ndarray]:
+    return None if a is None else np.ascontiguousarray(a, dtype=np.complex128)
+
+
+def geometry(N: int, W: int) -> dict:
+    """Wedge partition and lattice boxes chosen by the plan (host only, no GPU)."""
+    lib = load_library()
+    wo = np.empty(N * N, np.int32)
+    M = np.empty((W, 4), np.int32)
+    xc = np.empty((W, 2), np.int32)
+    box = np.empty((W, 4), np.int32)
+    _check(lib.fio_geometry(N, W, _ptr(wo), _ptr(M), _ptr(xc), _ptr(box)))
+    return {"wedge_of": wo.reshape(N, N), "M": M.reshape(W, 2, 2), "xc": xc, "box": box[:, :2],
+            "fine": box[:, 2:]}
+
+
+def assign_wedges(cost, nranks: int) -> np.ndarray:
+    lib = load_library()
+    cost = _f64(cost)
+    owner = np.empty(cost.shape[0], np.int32)
+    _check(lib.fio_assign_wedges(cost.shape[0], _ptr(cost), int(nranks), _ptr(owner)))
+    return owner
+
+
+class Plan:
+    """fio_plan: preprocessing of Phi(x,xi) = x.xi + b(x).xi + sqrt(c1(x)^2 xi1^2 + c2(x)^2 xi2^2)
+    and a(x,xi) = sum_k px[k](x) pxi[k](xi) at accuracy eps (include/fio.h)."""
+
+    def __init__(self, N: int, c1, c2, b1=None, b2=None, px=None, pxi=None, eps: float = 1e-6,
+                 dtype: str = "c128", n_wedges: int = 0, nufft_w: int = 0, nufft_beta: float = 0.0,
+                 seed: int = 0x5EED, device: Optional[int] = None, rank: int = 0, nranks: int = 1,
+                 r_init: int = 32, r_max: int = 512, certify: bool = True):
+        import torch
+        if not torch.cuda.is_available():
+            raise FioError(-3, "no CUDA device: the FIO apply runs only on the GPU (no CPU fallback)")
+        lib = load_library()
+        self._lib = lib
+        self.N = int(N)
+        self.dtype = dtype
+        self.c64 = dtype == "c64"
+        if device is None:
+            device = torch.cuda.current_device()
+        self.device = int(device)
+        keep = [_f64(c1), _f64(c2), _f64(b1), _f64(b2)]
+        for k in keep:
+            if k is not None and k.size != N * N:
+                raise FioError(-1, "phase arrays must have N*N entries")
+        ph = _Phase(*[_ptr(k) for k in keep])
+        pxa, pxia = _c128(px), _c128(pxi)
+        K = 0 if pxa is None else int(pxa.reshape(-1, N * N).shape[0])
+        amp = _Amp(K, _ptr(pxa), _ptr(pxia))
+        o = _Opts()
+        lib.fio_default_opts(ctypes.byref(o))
+        o.dtype = FIO_C64 if self.c64 else FIO_C128
+        o.n_wedges, o.nufft_w, o.nufft_beta, o.seed = int(n_wedges), int(nufft_w), float(nufft_beta), int(seed)
+        o.device, o.rank, o.nranks = self.device, int(rank), int(nranks)
+        o.r_init, o.r_max, o.certify = int(r_init), int(r_max), int(bool(certify))
+        h = ctypes.c_void_p()
+        with torch.cuda.device(self.device):
+            self.status = _check(lib.fio_plan(ctypes.byref(h), self.N, ctypes.byref(ph), ctypes.byref(amp),
+                                              float(eps), ctypes.byref(o)))
+        self._h = h
+        self.eps = eps
+        self.rank, self.nranks = int(rank), int(nranks)
+        self.torch_dtype = torch.complex64 if self.c64 else torch.complex128
+
+    # ------------------------------------------------------------ evaluation
+    def apply(self, f, out=None, stream=None):
+        """Lf for a device tensor f (N x N, complex64/complex128 matching the plan dtype)."""
+        import torch
+        if not (f.is_cuda and f.dtype == self.torch_dtype and tuple(f.shape) == (self.N, self.N)):
+            raise FioError(-1, f"f must be a CUDA {self.torch_dtype} tensor of shape ({self.N}, {self.N})")
+        f = f.contiguous()
+        if out is None:
+            out = torch.empty_like(f)
+        if stream is None:
+            stream = torch.cuda.current_stream(f.device)
+        _check(self._lib.fio_apply(self._h, ctypes.c_void_p(f.data_ptr()), ctypes.c_void_p(out.data_ptr()),
+                                   ctypes.c_void_p(stream.cuda_stream)))
+        return out
+
+    def apply_host(self, f_host, out_host, stream=None):
+        """End-to-end apply from host (pinned) tensors; copies in both directions inside the call."""
+        import torch
+        if stream is None:
+            stream = torch.cuda.current_stream(self.device)
+        _check(self._lib.fio_apply_host(self._h, ctypes.c_void_p(f_host.data_ptr()),
+                                        ctypes.c_void_p(out_host.data_ptr()), ctypes.c_void_p(stream.cuda_stream)))
+        return out_host
+
+    def apply_sharded(self, f, group=None, out=None):
+        """Wedge-sharded apply: this rank's partial over its wedges, then a reduce-scatter (sum) over
+        the process group.  Returns this rank's (N/nranks) x N row slab of Lf."""
+        import torch
+        import torch.distributed as dist
+        part = self.apply(f)
+        R = self.nranks
+        if R == 1:
+            return part
+        rows = self.N // R
+        real = torch.view_as_real(part).reshape(R, rows * self.N * 2)
+        slab = torch.empty(rows * self.N * 2, dtype=real.dtype, device=real.device) if out is None else \
+            torch.view_as_real(out).reshape(-1)
+        dist.reduce_scatter_tensor(slab, real.reshape(-1), op=dist.ReduceOp.SUM, group=group)
+        return torch.view_as_complex(slab.reshape(rows, self.N, 2))
+
+    # ------------------------------------------------------------ introspection
+    @property
+    def info(self) -> dict:
+        i = _Info()
+        _check(self._lib.fio_plan_info(self._h, ctypes.byref(i)))
+        return {k: getattr(i, k) for k, _ in _Info._fields_}
+
+    def wedges(self) -> dict:
+        n = self.info["n_owned"]
+        l, q, r = (np.zeros(n, np.int32) for _ in range(3))
+        box, M = np.zeros((n, 4), np.int32), np.zeros((n, 4), np.int32)
+        xc, err = np.zeros((n, 2), np.int32), np.zeros(n, np.float64)
+        _check(self._lib.fio_plan_wedges(self._h, _ptr(l), _ptr(q), _ptr(box), _ptr(M), _ptr(xc), _ptr(r),
+                                         _ptr(err)))
+        return {"l": l, "q": q, "box": box[:, :2], "fine": box[:, 2:], "M": M.reshape(n, 2, 2), "xc": xc,
+                "r": r, "sep_err": err}
+
+    def close(self):
+        if getattr(self, "_h", None) is not None and self._h.value:
+            self._lib.fio_destroy(self._h)
+            self._h = ctypes.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass

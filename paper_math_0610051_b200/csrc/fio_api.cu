@@ -1,0 +1,741 @@
+// fio_api.cu -- the C ABI (include/fio.h): plan construction (PAPER.md:981-1008,
+// 1111-1250) and the apply orchestration.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstring>
+#include <map>
+#include <string>
+#include <vector>
+
+#include "fio_internal.h"
+#include "fio_kernels.h"
+
+namespace fio {
+const char* last_error_cstr();
+}
+
+using namespace fio;
+
+namespace {
+
+constexpr size_t kSmemBudget = 96 * 1024;   // per-CTA FFT pass target (2 CTAs / SM)
+constexpr size_t kSmemMax = 200 * 1024;     // opt-in maximum for one long sequence
+constexpr int kCertSamples = 200;           // s of PAPER.md:1464-1477
+
+struct Status {
+  fio_status code = FIO_OK;
+};
+
+#define FIO_CUDA(expr)                                                                               \
+  do {                                                                                               \
+    cudaError_t e_ = (expr);                                                                         \
+    if (e_ != cudaSuccess) {                                                                         \
+      set_error(std::string("CUDA error at " #expr ": ") + cudaGetErrorString(e_));                  \
+      return FIO_ECUDA;                                                                              \
+    }                                                                                                \
+  } while (0)
+
+struct DevBuf {
+  void* p = nullptr;
+  size_t bytes = 0;
+  DevBuf() = default;
+  DevBuf(const DevBuf&) = delete;
+  DevBuf& operator=(const DevBuf&) = delete;
+  ~DevBuf() { release(); }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    bytes = 0;
+  }
+  cudaError_t ensure(size_t b) {
+    if (b <= bytes && p) return cudaSuccess;
+    release();
+    cudaError_t e = cudaMalloc(&p, std::max<size_t>(b, 16));
+    if (e == cudaSuccess) bytes = b;
+    return e;
+  }
+  template <typename T>
+  T* as() const {
+    return reinterpret_cast<T*>(p);
+  }
+};
+
+}  // namespace
+
+struct fio_plan_s {
+  int N = 0, W = 0, taps = 0, c64 = 0, device = 0;
+  double eps = 0, es_beta = 0;
+  fio_opts opts{};
+  std::vector<WedgeGeom> geom;
+  std::vector<int> owned;
+  std::vector<WedgeDev> wd;
+  std::vector<int> r_final;
+  std::vector<double> sep_err;
+  std::vector<void*> allocs;
+  std::vector<void*> alpha_ptrs, beta_ptrs;
+  OperatorDev op{};
+  double2* a0 = nullptr;
+  WedgeDev* d_wedges = nullptr;
+  FftLen* d_ffts = nullptr;
+  void* d_tw = nullptr;
+  void** d_alpha = nullptr;
+  void** d_beta = nullptr;
+  void *fhat = nullptr, *tmp = nullptr, *p1 = nullptr, *g = nullptr;
+  FftJob *jobs_row = nullptr, *jobs_col = nullptr;
+  int njobs_row = 0, njobs_col = 0, smem_row = 0, smem_col = 0;
+  int rows_per_cta_N = 1, cols_per_cta_N = 1, fft_N = 0;
+  void *e2e_in = nullptr, *e2e_out = nullptr;
+  size_t alpha_bytes = 0, beta_bytes = 0, ws_bytes = 0, fine_elems = 0, p1_elems = 0;
+  double plan_seconds = 0, max_err = 0;
+  int certified = 1;
+  int launches = 0;
+
+  cudaError_t alloc(void** p, size_t bytes) {
+    cudaError_t e = cudaMalloc(p, std::max<size_t>(bytes, 16));
+    if (e == cudaSuccess) allocs.push_back(*p);
+    return e;
+  }
+  template <typename T>
+  cudaError_t upload(T** dst, const T* src, size_t n) {
+    cudaError_t e = alloc(reinterpret_cast<void**>(dst), n * sizeof(T));
+    if (e != cudaSuccess) return e;
+    if (n) e = cudaMemcpy(*dst, src, n * sizeof(T), cudaMemcpyHostToDevice);
+    return e;
+  }
+  ~fio_plan_s() {
+    for (void* p : allocs) cudaFree(p);
+  }
+};
+
+extern "C" {
+
+const char* fio_last_error(void) { return last_error_cstr(); }
+const char* fio_version(void) { return "fio-b200 0.1 (sm_100a)"; }
+
+void fio_default_opts(fio_opts* o) {
+  if (!o) return;
+  std::memset(o, 0, sizeof(*o));
+  o->dtype = FIO_C128;
+  o->n_wedges = 0;
+  o->nufft_w = 0;
+  o->nufft_beta = 0.0;
+  o->seed = 0x5EEDull;
+  o->device = -1;
+  o->rank = 0;
+  o->nranks = 1;
+  o->r_init = 32;
+  o->r_max = 512;
+  o->certify = 1;
+}
+
+fio_status fio_geometry(int N, int W, int* wedge_of_out, int* M, int* xc, int* box) {
+  if (N < 4 || N % 2 || W < 1) {
+    set_error("fio_geometry: N must be even >= 4 and W >= 1");
+    return FIO_EINVAL;
+  }
+  std::vector<WedgeGeom> g;
+  build_geometry(N, W, g);
+  if (wedge_of_out) {
+    for (int k = 0; k < N * N; ++k) wedge_of_out[k] = -1;
+    for (int l = 0; l < W; ++l)
+      for (int k : g[l].members) wedge_of_out[k] = l;
+  }
+  for (int l = 0; l < W; ++l) {
+    if (M) std::memcpy(M + 4 * l, g[l].M, 4 * sizeof(int));
+    if (xc) { xc[2 * l] = g[l].xc1; xc[2 * l + 1] = g[l].xc2; }
+    if (box) { box[4 * l] = g[l].n1; box[4 * l + 1] = g[l].n2; box[4 * l + 2] = g[l].n1f; box[4 * l + 3] = g[l].n2f; }
+  }
+  return FIO_OK;
+}
+
+fio_status fio_assign_wedges(int W, const double* cost, int nranks, int* owner) {
+  if (W < 1 || nranks < 1 || !cost || !owner) {
+    set_error("fio_assign_wedges: bad arguments");
+    return FIO_EINVAL;
+  }
+  lpt_assign(W, cost, nranks, owner);
+  return FIO_OK;
+}
+
+}  // extern "C"
+
+namespace {
+
+// Randomized separation of the residual kernel of one wedge (PAPER.md:1111-1221,
+// DESIGN.md reading R8: skeleton columns chosen by column pivoting on a random
+// row sample, rows by pivoting on U; the paper's doubling of r and relative
+// threshold eps are kept).  Produces U (m x q, device, FP64), beta (q x n,
+// device, FP64), q, the final r and the sampled error.
+fio_status separate_wedge(fio_plan_s& P, const WedgeGeom& g, Rng& rng, cudaStream_t s, DevBuf& dU, DevBuf& dBeta,
+                          int& q_out, int& r_out, double& err_out) {
+  const int N = P.N;
+  const int m = N * N;
+  const int n = (int)g.members.size();
+  const double eps = P.eps;
+  DevBuf dMembers, dRows, dCols, dAC, dWork, dGram, dY, dAR, dZ, dTmp;
+  FIO_CUDA(dMembers.ensure(sizeof(int) * n));
+  FIO_CUDA(cudaMemcpy(dMembers.p, g.members.data(), sizeof(int) * n, cudaMemcpyHostToDevice));
+
+  int r = std::min(std::max(P.opts.r_init, 4), n);
+  std::vector<int> C;
+  std::vector<cplx> V;
+  std::vector<double> lam;
+  int q = 0;
+  for (;;) {
+    // (1) random row sample R0, candidate columns, A(R0, cand) -> host
+    std::vector<int> R0 = sample_distinct(rng, m, r);
+    std::vector<int> candIdx = sample_distinct(rng, n, std::min(n, 64 * r));
+    std::vector<int> candCols(candIdx.size());
+    for (size_t j = 0; j < candIdx.size(); ++j) candCols[j] = g.members[candIdx[j]];
+    const int nr0 = (int)R0.size(), nc0 = (int)candCols.size();
+    FIO_CUDA(dRows.ensure(sizeof(int) * nr0));
+    FIO_CUDA(dCols.ensure(sizeof(int) * nc0));
+    FIO_CUDA(cudaMemcpy(dRows.p, R0.data(), sizeof(int) * nr0, cudaMemcpyHostToDevice));
+    FIO_CUDA(cudaMemcpy(dCols.p, candCols.data(), sizeof(int) * nc0, cudaMemcpyHostToDevice));
+    FIO_CUDA(dTmp.ensure(sizeof(double2) * (size_t)nr0 * nc0));
+    FIO_CUDA(launch_eval_entries(P.op, g.u1, g.u2, dRows.as<int>(), nr0, dCols.as<int>(), nc0, dTmp.as<double2>(), 1,
+                                 nr0, s));
+    std::vector<cplx> B((size_t)nr0 * nc0);
+    FIO_CUDA(cudaMemcpyAsync(B.data(), dTmp.p, sizeof(cplx) * B.size(), cudaMemcpyDeviceToHost, s));
+    FIO_CUDA(cudaStreamSynchronize(s));
+    // (2) column pivoting -> skeleton columns C
+    std::vector<int> piv = pivoted_columns(nr0, nc0, B, r);
+    C.clear();
+    for (int p : piv) C.push_back(candCols[p]);
+    const int rc = (int)C.size();
+    if (rc == 0) {
+      q = 0;
+      break;
+    }
+    // (3) A_C = A(all x, C) on the device, Gram = A_C^H A_C, eigen-decomposition
+    FIO_CUDA(dCols.ensure(sizeof(int) * rc));
+    FIO_CUDA(cudaMemcpy(dCols.p, C.data(), sizeof(int) * rc, cudaMemcpyHostToDevice));
+    FIO_CUDA(dAC.ensure(sizeof(double2) * (size_t)m * rc));
+    FIO_CUDA(launch_eval_entries(P.op, g.u1, g.u2, nullptr, m, dCols.as<int>(), rc, dAC.as<double2>(), 1, m, s));
+    int nsplit = std::max(1, std::min(256, m / 8192));
+    FIO_CUDA(dWork.ensure(sizeof(double2) * (size_t)nsplit * rc * rc));
+    FIO_CUDA(dGram.ensure(sizeof(double2) * (size_t)rc * rc));
+    FIO_CUDA(launch_zgemm(rc, rc, m, dAC.as<double2>(), m, 1, true, dAC.as<double2>(), 1, m, dGram.as<double2>(), 1,
+                          rc, nsplit, dWork.as<double2>(), s));
+    std::vector<cplx> G((size_t)rc * rc);
+    FIO_CUDA(cudaMemcpyAsync(G.data(), dGram.p, sizeof(cplx) * G.size(), cudaMemcpyDeviceToHost, s));
+    FIO_CUDA(cudaStreamSynchronize(s));
+    jacobi_svd(rc, rc, G, V, lam);  // G PSD: singular values = eigenvalues, V = eigenvectors
+    const double s1 = std::sqrt(std::max(lam[0], 0.0));
+    q = 0;
+    for (int k = 0; k < rc; ++k)
+      if (std::sqrt(std::max(lam[k], 0.0)) > eps * s1) ++q;
+    // accept when q is small against r, else double r and resample
+    if (4 * q <= 3 * rc || rc < r || r >= n || r >= P.opts.r_max) break;
+    r = std::min(std::min(2 * r, n), P.opts.r_max);
+  }
+  r_out = r;
+  q_out = q;
+  if (q == 0) {
+    err_out = 0.0;
+    return FIO_OK;
+  }
+  const int rc = (int)C.size();
+  // (4) U = A_C V_q S_q^{-1}
+  std::vector<cplx> Y((size_t)rc * q);
+  for (int t = 0; t < q; ++t) {
+    double sg = std::sqrt(lam[t]);
+    for (int i = 0; i < rc; ++i) Y[i + (size_t)t * rc] = {V[i + (size_t)t * rc].re / sg, V[i + (size_t)t * rc].im / sg};
+  }
+  FIO_CUDA(dY.ensure(sizeof(double2) * Y.size()));
+  FIO_CUDA(cudaMemcpy(dY.p, Y.data(), sizeof(double2) * Y.size(), cudaMemcpyHostToDevice));
+  FIO_CUDA(dU.ensure(sizeof(double2) * (size_t)m * q));
+  FIO_CUDA(launch_zgemm(m, q, rc, dAC.as<double2>(), 1, m, false, dY.as<double2>(), 1, rc, dU.as<double2>(), 1, m, 1,
+                        nullptr, s));
+  dAC.release();
+  // (5) rows: pivoting on a random row sample of U, plus r uniform rows
+  std::vector<int> R1 = sample_distinct(rng, m, std::min(m, 8 * r));
+  const int n1r = (int)R1.size();
+  FIO_CUDA(dRows.ensure(sizeof(int) * std::max(n1r, kCertSamples)));
+  FIO_CUDA(cudaMemcpy(dRows.p, R1.data(), sizeof(int) * n1r, cudaMemcpyHostToDevice));
+  FIO_CUDA(dTmp.ensure(sizeof(double2) * (size_t)std::max(n1r, kCertSamples) * q));
+  FIO_CUDA(launch_gather_rows(dU.as<double2>(), m, q, dRows.as<int>(), n1r, dTmp.as<double2>(), s));
+  std::vector<cplx> UR1((size_t)n1r * q);
+  FIO_CUDA(cudaMemcpyAsync(UR1.data(), dTmp.p, sizeof(cplx) * UR1.size(), cudaMemcpyDeviceToHost, s));
+  FIO_CUDA(cudaStreamSynchronize(s));
+  std::vector<cplx> Bt((size_t)q * n1r);
+  for (int i = 0; i < n1r; ++i)
+    for (int t = 0; t < q; ++t) Bt[t + (size_t)i * q] = UR1[i + (size_t)t * n1r];
+  std::vector<int> piv2 = pivoted_columns(q, n1r, Bt, q);
+  std::vector<int> R;
+  for (int p : piv2) R.push_back(R1[p]);
+  for (int x : sample_distinct(rng, m, r)) R.push_back(x);
+  std::sort(R.begin(), R.end());
+  R.erase(std::unique(R.begin(), R.end()), R.end());
+  const int nR = (int)R.size();
+  // U_R and its pseudo-inverse (cutoff 1e-12 sigma_max, reading R8)
+  std::vector<cplx> UR((size_t)nR * q);
+  FIO_CUDA(dRows.ensure(sizeof(int) * std::max(nR, std::max(n1r, kCertSamples))));
+  FIO_CUDA(cudaMemcpy(dRows.p, R.data(), sizeof(int) * nR, cudaMemcpyHostToDevice));
+  FIO_CUDA(dTmp.ensure(sizeof(double2) * (size_t)std::max(nR, kCertSamples) * q));
+  FIO_CUDA(launch_gather_rows(dU.as<double2>(), m, q, dRows.as<int>(), nR, dTmp.as<double2>(), s));
+  FIO_CUDA(cudaMemcpyAsync(UR.data(), dTmp.p, sizeof(cplx) * UR.size(), cudaMemcpyDeviceToHost, s));
+  FIO_CUDA(cudaStreamSynchronize(s));
+  std::vector<cplx> Vr;
+  std::vector<double> sr;
+  jacobi_svd(nR, q, UR, Vr, sr);
+  std::vector<cplx> Z((size_t)q * nR, cplx{0, 0});
+  for (int k = 0; k < q; ++k) {
+    if (!(sr[k] > 1e-12 * sr[0])) continue;
+    const double inv2 = 1.0 / (sr[k] * sr[k]);
+    for (int i = 0; i < nR; ++i) {
+      cplx a = UR[i + (size_t)k * nR];  // = u_k sigma_k
+      for (int t = 0; t < q; ++t) {
+        cplx v = Vr[t + (size_t)k * q];
+        // Z(t, i) += v_t conj(a_i) / sigma^2
+        Z[t + (size_t)i * q].re += (v.re * a.re + v.im * a.im) * inv2;
+        Z[t + (size_t)i * q].im += (v.im * a.re - v.re * a.im) * inv2;
+      }
+    }
+  }
+  // (6) beta = T = U_R^+ A_R
+  FIO_CUDA(dAR.ensure(sizeof(double2) * (size_t)nR * n));
+  FIO_CUDA(launch_eval_entries(P.op, g.u1, g.u2, dRows.as<int>(), nR, dMembers.as<int>(), n, dAR.as<double2>(), 1, nR,
+                               s));
+  FIO_CUDA(dZ.ensure(sizeof(double2) * Z.size()));
+  FIO_CUDA(cudaMemcpy(dZ.p, Z.data(), sizeof(double2) * Z.size(), cudaMemcpyHostToDevice));
+  FIO_CUDA(dBeta.ensure(sizeof(double2) * (size_t)q * n));
+  FIO_CUDA(launch_zgemm(q, n, nR, dZ.as<double2>(), 1, q, false, dAR.as<double2>(), 1, nR, dBeta.as<double2>(), 1, q,
+                        1, nullptr, s));
+  dAR.release();
+  // (7) certification: sampled relative Frobenius error on s x s entries
+  err_out = 0.0;
+  if (P.opts.certify) {
+    std::vector<int> Gam = sample_distinct(rng, m, kCertSamples);
+    std::vector<int> Del = sample_distinct(rng, n, kCertSamples);
+    const int ng = (int)Gam.size(), nd = (int)Del.size();
+    std::vector<int> delCols(nd);
+    for (int j = 0; j < nd; ++j) delCols[j] = g.members[Del[j]];
+    FIO_CUDA(cudaMemcpy(dRows.p, Gam.data(), sizeof(int) * ng, cudaMemcpyHostToDevice));
+    FIO_CUDA(dCols.ensure(sizeof(int) * nd));
+    FIO_CUDA(cudaMemcpy(dCols.p, delCols.data(), sizeof(int) * nd, cudaMemcpyHostToDevice));
+    DevBuf dA;
+    FIO_CUDA(dA.ensure(sizeof(double2) * (size_t)ng * nd));
+    FIO_CUDA(launch_eval_entries(P.op, g.u1, g.u2, dRows.as<int>(), ng, dCols.as<int>(), nd, dA.as<double2>(), 1, ng,
+                                 s));
+    std::vector<cplx> Aref((size_t)ng * nd), UG((size_t)ng * q), Bh((size_t)q * n);
+    FIO_CUDA(cudaMemcpyAsync(Aref.data(), dA.p, sizeof(cplx) * Aref.size(), cudaMemcpyDeviceToHost, s));
+    FIO_CUDA(launch_gather_rows(dU.as<double2>(), m, q, dRows.as<int>(), ng, dTmp.as<double2>(), s));
+    FIO_CUDA(cudaMemcpyAsync(UG.data(), dTmp.p, sizeof(cplx) * UG.size(), cudaMemcpyDeviceToHost, s));
+    FIO_CUDA(cudaMemcpyAsync(Bh.data(), dBeta.p, sizeof(cplx) * Bh.size(), cudaMemcpyDeviceToHost, s));
+    FIO_CUDA(cudaStreamSynchronize(s));
+    double num = 0, den = 0;
+    for (int j = 0; j < nd; ++j)
+      for (int i = 0; i < ng; ++i) {
+        double ar = 0, ai = 0;
+        for (int t = 0; t < q; ++t) {
+          cplx u = UG[i + (size_t)t * ng], b = Bh[t + (size_t)Del[j] * q];
+          ar += u.re * b.re - u.im * b.im;
+          ai += u.re * b.im + u.im * b.re;
+        }
+        cplx e = Aref[i + (size_t)j * ng];
+        num += (e.re - ar) * (e.re - ar) + (e.im - ai) * (e.im - ai);
+        den += e.re * e.re + e.im * e.im;
+      }
+    err_out = den > 0 ? std::sqrt(num / den) : 0.0;
+  }
+  return FIO_OK;
+}
+
+int fft_index(std::map<int, int>& lens, std::vector<FftLen>& tab, int L) {
+  auto it = lens.find(L);
+  if (it != lens.end()) return it->second;
+  FftLen f{};
+  f.L = L;
+  std::vector<int8_t> r = radix_plan(L);
+  f.nst = (int)r.size();
+  for (int i = 0; i < f.nst; ++i) f.radix[i] = r[i];
+  int idx = (int)tab.size();
+  tab.push_back(f);
+  lens[L] = idx;
+  return idx;
+}
+
+fio_status build_plan(fio_plan_s& P, const fio_phase* phase, const fio_amplitude* amp) {
+  const int N = P.N;
+  const long long NN = (long long)N * N;
+  const bool c64 = P.c64;
+  const size_t cs = c64 ? sizeof(float2) : sizeof(double2);
+  cudaStream_t s = 0;
+  // operator data on the device
+  FIO_CUDA(P.upload(const_cast<double**>(&P.op.c1), phase->c1, NN));
+  FIO_CUDA(P.upload(const_cast<double**>(&P.op.c2), phase->c2, NN));
+  if (phase->b1) FIO_CUDA(P.upload(const_cast<double**>(&P.op.b1), phase->b1, NN));
+  if (phase->b2) FIO_CUDA(P.upload(const_cast<double**>(&P.op.b2), phase->b2, NN));
+  P.op.N = N;
+  P.op.K = amp ? amp->K : 0;
+  std::vector<double2> a0(NN);
+  if (P.op.K > 0) {
+    const double2* px = reinterpret_cast<const double2*>(amp->px);
+    const double2* pxi = reinterpret_cast<const double2*>(amp->pxi);
+    FIO_CUDA(P.upload(const_cast<double2**>(&P.op.px), px, (size_t)P.op.K * NN));
+    FIO_CUDA(P.upload(const_cast<double2**>(&P.op.pxi), pxi, (size_t)P.op.K * NN));
+    for (long long x = 0; x < NN; ++x) {
+      double re = 0, im = 0;
+      for (int k = 0; k < P.op.K; ++k) {  // a(x, 0) = sum_k px_k(x) pxi_k(0)
+        double2 u = px[k * NN + x], v = pxi[k * NN];
+        re += u.x * v.x - u.y * v.y;
+        im += u.x * v.y + u.y * v.x;
+      }
+      a0[x] = make_double2(re / N, im / N);
+    }
+  } else {
+    for (long long x = 0; x < NN; ++x) a0[x] = make_double2(1.0 / N, 0.0);
+  }
+  FIO_CUDA(P.upload(&P.a0, a0.data(), NN));
+
+  // geometry and ownership
+  build_geometry(N, P.W, P.geom);
+  std::vector<int> owner(P.W, 0);
+  if (P.opts.nranks > 1) {
+    std::vector<double> cost(P.W);
+    for (int l = 0; l < P.W; ++l)  // interpolation (N^2 w^2) + FFT volume, per term
+      cost[l] = (double)NN * P.taps * P.taps + 8.0 * P.geom[l].n1f * P.geom[l].n2f * std::log2((double)P.geom[l].n1f * P.geom[l].n2f);
+    lpt_assign(P.W, cost.data(), P.opts.nranks, owner.data());
+  }
+  for (int l = 0; l < P.W; ++l)
+    if (owner[l] == P.opts.rank && !P.geom[l].members.empty()) P.owned.push_back(l);
+
+  // FFT length table
+  std::map<int, int> lens;
+  std::vector<FftLen> ffts;
+  P.fft_N = fft_index(lens, ffts, N);
+
+  // per owned wedge: separation, folding of alpha' and beta'
+  for (size_t wi = 0; wi < P.owned.size(); ++wi) {
+    const WedgeGeom& g = P.geom[P.owned[wi]];
+    Rng rng(P.opts.seed ^ (0x9E3779B97F4A7C15ull * (uint64_t)(g.l + 1)));
+    DevBuf dU, dBeta;
+    int q = 0, r = 0;
+    double err = 0;
+    fio_status st = separate_wedge(P, g, rng, s, dU, dBeta, q, r, err);
+    if (st != FIO_OK) return st;
+    WedgeDev w{};
+    w.l = g.l;
+    w.q = q;
+    w.n1 = g.n1; w.n2 = g.n2; w.n1f = g.n1f; w.n2f = g.n2f;
+    std::memcpy(w.M, g.M, sizeof(w.M));
+    std::memcpy(w.Mi, g.Mi, sizeof(w.Mi));
+    w.xc1 = g.xc1; w.xc2 = g.xc2;
+    w.u1 = g.u1; w.u2 = g.u2;
+    w.fft1 = fft_index(lens, ffts, g.n1f);
+    w.fft2 = fft_index(lens, ffts, g.n2f);
+    void* alpha = nullptr;
+    void* betap = nullptr;
+    FIO_CUDA(P.alloc(&alpha, cs * (size_t)q * NN));
+    FIO_CUDA(P.alloc(&betap, cs * (size_t)q * g.n1 * g.n2));
+    if (q > 0) {
+      FIO_CUDA(launch_fold_alpha(P.op, w, dU.as<double2>(), q, alpha, c64, s));
+      FIO_CUDA(cudaMemsetAsync(betap, 0, cs * (size_t)q * g.n1 * g.n2, s));
+      std::vector<double> d1(g.n1), d2(g.n2);
+      for (int i = 0; i < g.n1; ++i) d1[i] = 1.0 / es_fourier((double)(i - g.n1 / 2) / g.n1f, P.taps, P.es_beta);
+      for (int i = 0; i < g.n2; ++i) d2[i] = 1.0 / es_fourier((double)(i - g.n2 / 2) / g.n2f, P.taps, P.es_beta);
+      DevBuf dd1, dd2, dMem;
+      FIO_CUDA(dd1.ensure(sizeof(double) * g.n1));
+      FIO_CUDA(dd2.ensure(sizeof(double) * g.n2));
+      FIO_CUDA(dMem.ensure(sizeof(int) * g.members.size()));
+      FIO_CUDA(cudaMemcpy(dd1.p, d1.data(), sizeof(double) * g.n1, cudaMemcpyHostToDevice));
+      FIO_CUDA(cudaMemcpy(dd2.p, d2.data(), sizeof(double) * g.n2, cudaMemcpyHostToDevice));
+      FIO_CUDA(cudaMemcpy(dMem.p, g.members.data(), sizeof(int) * g.members.size(), cudaMemcpyHostToDevice));
+      FIO_CUDA(launch_fold_beta(N, w, dMem.as<int>(), (int)g.members.size(), dBeta.as<double2>(), q, dd1.as<double>(),
+                                dd2.as<double>(), betap, c64, s));
+      FIO_CUDA(cudaStreamSynchronize(s));
+    }
+    P.alpha_bytes += cs * (size_t)q * NN;
+    P.beta_bytes += cs * (size_t)q * g.n1 * g.n2;
+    P.alpha_ptrs.push_back(alpha);
+    P.beta_ptrs.push_back(betap);
+    P.wd.push_back(w);
+    P.r_final.push_back(r);
+    P.sep_err.push_back(err);
+    P.max_err = std::max(P.max_err, err);
+    if (err > P.eps) P.certified = 0;
+  }
+
+  // twiddle tables
+  std::vector<double2> twd;
+  for (auto& f : ffts) {
+    f.tw_off = (int)twd.size();
+    for (int mm = 0; mm < f.L; ++mm) {
+      const double ang = 6.283185307179586476925286766559 * (double)mm / (double)f.L;
+      twd.push_back(make_double2(std::cos(ang), std::sin(ang)));
+    }
+    if (f.nst == 0 && f.L != 1) {
+      set_error("internal: FFT length " + std::to_string(f.L) + " is not 5-smooth");
+      return FIO_EINTERNAL;
+    }
+  }
+  if (c64) {
+    std::vector<float2> twf(twd.size());
+    for (size_t i = 0; i < twd.size(); ++i) twf[i] = make_float2((float)twd[i].x, (float)twd[i].y);
+    FIO_CUDA(P.upload(reinterpret_cast<float2**>(&P.d_tw), twf.data(), twf.size()));
+  } else {
+    FIO_CUDA(P.upload(reinterpret_cast<double2**>(&P.d_tw), twd.data(), twd.size()));
+  }
+
+  // workspace offsets and FFT job lists
+  long long p1_off = 0, g_off = 0;
+  std::vector<FftJob> jr, jc;
+  size_t smem_row = 0, smem_col = 0;
+  for (size_t wi = 0; wi < P.wd.size(); ++wi) {
+    WedgeDev& w = P.wd[wi];
+    w.p1_off = p1_off;
+    w.g_off = g_off;
+    p1_off += (long long)w.q * w.n1 * w.n2f;
+    g_off += (long long)w.q * w.n1f * w.n2f;
+    size_t sr = fft_seq_bytes(w.n2f, c64), sc = fft_seq_bytes(w.n1f, c64);
+    int rows = (int)std::max<size_t>(1, kSmemBudget / sr);
+    int cols = (int)std::max<size_t>(1, kSmemBudget / sc);
+    cols = std::min(cols, w.n2f);
+    rows = std::min(rows, w.n1);
+    for (int t = 0; t < w.q; ++t) {
+      for (int i = 0; i < w.n1; i += rows) {
+        jr.push_back({(int)wi, t, i, std::min(rows, w.n1 - i)});
+        smem_row = std::max(smem_row, sr * std::min(rows, w.n1 - i));
+      }
+      for (int c = 0; c < w.n2f; c += cols) {
+        jc.push_back({(int)wi, t, c, std::min(cols, w.n2f - c)});
+        smem_col = std::max(smem_col, sc * std::min(cols, w.n2f - c));
+      }
+    }
+  }
+  if (smem_row > kSmemMax || smem_col > kSmemMax || fft_seq_bytes(N, c64) > kSmemMax) {
+    set_error("fine grid too large for the shared-memory FFT (N too large for this dtype)");
+    return FIO_EINVAL;
+  }
+  P.smem_row = (int)smem_row;
+  P.smem_col = (int)smem_col;
+  P.njobs_row = (int)jr.size();
+  P.njobs_col = (int)jc.size();
+  P.p1_elems = (size_t)p1_off;
+  P.fine_elems = (size_t)g_off;
+  P.rows_per_cta_N = (int)std::max<size_t>(1, kSmemBudget / fft_seq_bytes(N, c64));
+  P.cols_per_cta_N = std::min(N, (int)std::max<size_t>(1, kSmemBudget / fft_seq_bytes(N, c64)));
+  FIO_CUDA(configure_kernels(kSmemMax));
+  if (!jr.empty()) FIO_CUDA(P.upload(&P.jobs_row, jr.data(), jr.size()));
+  if (!jc.empty()) FIO_CUDA(P.upload(&P.jobs_col, jc.data(), jc.size()));
+  FIO_CUDA(P.upload(&P.d_ffts, ffts.data(), ffts.size()));
+  FIO_CUDA(P.upload(&P.d_wedges, P.wd.data(), std::max<size_t>(P.wd.size(), 1)));
+  FIO_CUDA(P.upload(&P.d_alpha, P.alpha_ptrs.data(), std::max<size_t>(P.alpha_ptrs.size(), 1)));
+  FIO_CUDA(P.upload(&P.d_beta, P.beta_ptrs.data(), std::max<size_t>(P.beta_ptrs.size(), 1)));
+  FIO_CUDA(P.alloc(&P.fhat, cs * NN));
+  FIO_CUDA(P.alloc(&P.tmp, cs * NN));
+  FIO_CUDA(P.alloc(&P.p1, cs * std::max<size_t>(P.p1_elems, 1)));
+  FIO_CUDA(P.alloc(&P.g, cs * std::max<size_t>(P.fine_elems, 1)));
+  P.ws_bytes = cs * (2 * NN + P.p1_elems + P.fine_elems);
+  FIO_CUDA(cudaDeviceSynchronize());
+  return FIO_OK;
+}
+
+ApplyArgs make_args(const fio_plan_s& P) {
+  ApplyArgs a{};
+  a.N = P.N;
+  a.nw = (int)P.wd.size();
+  a.wedges = P.d_wedges;
+  a.ffts = P.d_ffts;
+  a.fft_N = P.fft_N;
+  a.tw = P.d_tw;
+  a.alpha = const_cast<const void* const*>(P.d_alpha);
+  a.beta = const_cast<const void* const*>(P.d_beta);
+  a.op = P.op;
+  a.a0 = P.a0;
+  a.add_dc = P.opts.rank == 0 ? 1 : 0;
+  a.taps = P.taps;
+  a.es_beta = P.es_beta;
+  a.fhat = P.fhat;
+  a.tmp = P.tmp;
+  a.p1 = P.p1;
+  a.g = P.g;
+  a.jobs_row = P.jobs_row;
+  a.njobs_row = P.njobs_row;
+  a.smem_row = P.smem_row;
+  a.jobs_col = P.jobs_col;
+  a.njobs_col = P.njobs_col;
+  a.smem_col = P.smem_col;
+  a.rows_per_cta_N = P.rows_per_cta_N;
+  a.cols_per_cta_N = P.cols_per_cta_N;
+  return a;
+}
+
+}  // namespace
+
+extern "C" {
+
+fio_status fio_plan(fio_handle* out, int N, const fio_phase* phase, const fio_amplitude* amp, double eps,
+                    const fio_opts* opts) {
+  if (!out) {
+    set_error("fio_plan: out is NULL");
+    return FIO_EINVAL;
+  }
+  *out = nullptr;
+  if (N < 8 || N > 4096 || N % 2 != 0 || !is_smooth5(N)) {
+    set_error("fio_plan: N must be even, 5-smooth and in [8, 4096] (got " + std::to_string(N) + ")");
+    return FIO_EINVAL;
+  }
+  if (!(eps > 0.0 && eps < 1.0)) {
+    set_error("fio_plan: eps must lie in (0, 1)");
+    return FIO_EINVAL;
+  }
+  if (!phase || !phase->c1 || !phase->c2) {
+    set_error("fio_plan: phase->c1 and phase->c2 are required");
+    return FIO_EINVAL;
+  }
+  if (amp && amp->K < 0) {
+    set_error("fio_plan: amplitude rank K must be >= 0");
+    return FIO_EINVAL;
+  }
+  if (amp && amp->K > 0 && (!amp->px || !amp->pxi)) {
+    set_error("fio_plan: amplitude K > 0 needs px and pxi");
+    return FIO_EINVAL;
+  }
+  fio_opts o;
+  fio_default_opts(&o);
+  if (opts) o = *opts;
+  if (o.dtype != FIO_C64 && o.dtype != FIO_C128) {
+    set_error("fio_plan: dtype must be FIO_C64 or FIO_C128");
+    return FIO_EINVAL;
+  }
+  if (o.nranks < 1 || o.rank < 0 || o.rank >= o.nranks) {
+    set_error("fio_plan: need 0 <= rank < nranks");
+    return FIO_EINVAL;
+  }
+  if (o.nufft_w != 0 && (o.nufft_w < 3 || o.nufft_w > kMaxTaps)) {
+    set_error("fio_plan: nufft_w must be 0 or in [3, 12]");
+    return FIO_EINVAL;
+  }
+  if (o.n_wedges < 0 || o.r_init < 0 || o.r_max < 0) {
+    set_error("fio_plan: negative option");
+    return FIO_EINVAL;
+  }
+  if (o.r_init == 0) o.r_init = 32;
+  if (o.r_max == 0) o.r_max = 512;
+  if (o.device >= 0) {
+    cudaError_t e = cudaSetDevice(o.device);
+    if (e != cudaSuccess) {
+      set_error(std::string("fio_plan: cudaSetDevice: ") + cudaGetErrorString(e));
+      return FIO_ECUDA;
+    }
+  }
+  auto t0 = std::chrono::steady_clock::now();
+  fio_plan_s* P = new (std::nothrow) fio_plan_s();
+  if (!P) {
+    set_error("fio_plan: out of host memory");
+    return FIO_ENOMEM;
+  }
+  cudaGetDevice(&P->device);
+  P->N = N;
+  P->eps = eps;
+  P->opts = o;
+  P->c64 = o.dtype == FIO_C64;
+  P->W = o.n_wedges > 0 ? o.n_wedges : default_wedges(N);
+  P->taps = o.nufft_w > 0 ? o.nufft_w : taps_for_eps(eps);
+  P->es_beta = o.nufft_beta > 0 ? o.nufft_beta : 2.30 * P->taps;
+  fio_status st = build_plan(*P, phase, amp);
+  if (st < 0) {
+    delete P;
+    return st;
+  }
+  P->plan_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+  P->launches = 5;
+  *out = P;
+  return P->certified ? FIO_OK : FIO_WNOTCERT;
+}
+
+fio_status fio_apply(fio_handle h, const void* f_dev, void* Lf_dev, void* stream) {
+  if (!h || !f_dev || !Lf_dev) {
+    set_error("fio_apply: NULL argument");
+    return FIO_EINVAL;
+  }
+  if (f_dev == Lf_dev) {
+    set_error("fio_apply: f and Lf must not alias");
+    return FIO_EINVAL;
+  }
+  int dev = -1;
+  cudaGetDevice(&dev);
+  if (dev != h->device) FIO_CUDA(cudaSetDevice(h->device));
+  ApplyArgs a = make_args(*h);
+  int launches = 0;
+  FIO_CUDA(enqueue_apply(a, h->c64, f_dev, Lf_dev, (cudaStream_t)stream, &launches));
+  h->launches = launches;
+  return FIO_OK;
+}
+
+fio_status fio_apply_host(fio_handle h, const void* f_host, void* Lf_host, void* stream) {
+  if (!h || !f_host || !Lf_host) {
+    set_error("fio_apply_host: NULL argument");
+    return FIO_EINVAL;
+  }
+  const size_t bytes = (size_t)h->N * h->N * (h->c64 ? sizeof(float2) : sizeof(double2));
+  if (!h->e2e_in) {
+    FIO_CUDA(h->alloc(&h->e2e_in, bytes));
+    FIO_CUDA(h->alloc(&h->e2e_out, bytes));
+  }
+  cudaStream_t s = (cudaStream_t)stream;
+  FIO_CUDA(cudaMemcpyAsync(h->e2e_in, f_host, bytes, cudaMemcpyHostToDevice, s));
+  fio_status st = fio_apply(h, h->e2e_in, h->e2e_out, stream);
+  if (st != FIO_OK) return st;
+  FIO_CUDA(cudaMemcpyAsync(Lf_host, h->e2e_out, bytes, cudaMemcpyDeviceToHost, s));
+  FIO_CUDA(cudaStreamSynchronize(s));
+  return FIO_OK;
+}
+
+fio_status fio_destroy(fio_handle h) {
+  if (!h) return FIO_OK;
+  delete h;
+  return FIO_OK;
+}
+
+fio_status fio_plan_info(fio_handle h, fio_info* info) {
+  if (!h || !info) {
+    set_error("fio_plan_info: NULL argument");
+    return FIO_EINVAL;
+  }
+  std::memset(info, 0, sizeof(*info));
+  info->N = h->N;
+  info->W = h->W;
+  info->nufft_w = h->taps;
+  info->dtype = h->c64 ? FIO_C64 : FIO_C128;
+  info->rank = h->opts.rank;
+  info->nranks = h->opts.nranks;
+  info->n_owned = (int)h->wd.size();
+  for (const auto& w : h->wd) info->sum_q += w.q;
+  info->certified = h->certified;
+  info->nufft_beta = h->es_beta;
+  info->max_sep_err = h->max_err;
+  info->plan_seconds = h->plan_seconds;
+  info->alpha_bytes = h->alpha_bytes;
+  info->beta_bytes = h->beta_bytes;
+  info->workspace_bytes = h->ws_bytes;
+  info->fine_elems = h->fine_elems;
+  info->p1_elems = h->p1_elems;
+  info->launches_per_apply = h->launches;
+  return FIO_OK;
+}
+
+fio_status fio_plan_wedges(fio_handle h, int* l, int* q, int* box, int* M, int* xc, int* r, double* sep_err) {
+  if (!h) {
+    set_error("fio_plan_wedges: NULL handle");
+    return FIO_EINVAL;
+  }
+  for (size_t i = 0; i < h->wd.size(); ++i) {
+    const WedgeDev& w = h->wd[i];
+    if (l) l[i] = w.l;
+    if (q) q[i] = w.q;
+    if (box) { box[4 * i] = w.n1; box[4 * i + 1] = w.n2; box[4 * i + 2] = w.n1f; box[4 * i + 3] = w.n2f; }
+    if (M) std::memcpy(M + 4 * i, w.M, 4 * sizeof(int));
+    if (xc) { xc[2 * i] = w.xc1; xc[2 * i + 1] = w.xc2; }
+    if (r) r[i] = h->r_final[i];
+    if (sep_err) sep_err[i] = h->sep_err[i];
+  }
+  return FIO_OK;
+}
+
+}  // extern "C"

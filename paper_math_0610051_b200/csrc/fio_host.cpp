@@ -1,0 +1,339 @@
+// fio_host.cpp -- host-side plan logic of the product library: the wedge
+// partition and lattice boxes, FFT radix plans, the NUFFT kernel and its
+// Fourier transform, small dense linear algebra (Jacobi SVD, column-pivoted
+// Gram-Schmidt), the counter-based RNG and the wedge->rank assignment.
+// Shares no code with oracle/.  Citations are PAPER.md line numbers.
+#include <algorithm>
+#include <array>
+#include <cmath>
+#include <cstring>
+#include <numeric>
+#include <unordered_set>
+
+#include "fio_internal.h"
+
+namespace fio {
+
+static thread_local std::string g_err;
+void set_error(const std::string& msg) { g_err = msg; }
+const char* last_error_cstr() { return g_err.c_str(); }
+
+// Reading R1: W = 8 round(sqrt(N)/8), at least 8.  A multiple of 8
+// makes every boundary ray (2l+1) pi / W irrational-sloped, so no lattice point
+// is ever on a wedge boundary.
+int default_wedges(int N) {
+  int w = 8 * (int)std::lround(std::sqrt((double)N) / 8.0);
+  return std::max(8, w);
+}
+
+bool is_smooth5(int n) {
+  if (n <= 0) return false;
+  for (int p : {2, 3, 5})
+    while (n % p == 0) n /= p;
+  return n == 1;
+}
+
+// Smallest even 5-smooth nf >= 2 * extent: oversampling sigma >= 2 (PAPER.md:1305-1325,
+// reading R10), sizes the hand-written mixed-radix FFT supports.
+int next_fine_size(int extent) {
+  int nf = std::max(2 * extent, 8);
+  while (!(is_smooth5(nf) && nf % 2 == 0)) ++nf;
+  return nf;
+}
+
+// Wedge W_l = {xi : (2l-1) pi/W <= arg xi < (2l+1) pi/W}, arg
+// measured from (1,0) and wrapped to [-pi/W, 2 pi - pi/W) (readings R4, R14);
+// xi = 0 belongs to no wedge (reading R3).
+int wedge_of(int W, int xi1, int xi2) {
+  if (xi1 == 0 && xi2 == 0) return -1;
+  const double pi = 3.14159265358979323846;
+  double th = std::atan2((double)xi2, (double)xi1);
+  double lo = -pi / W;
+  if (th < lo) th += 2.0 * pi;
+  int l = (int)std::floor((th - lo) / (2.0 * pi / W));
+  return std::min(std::max(l, 0), W - 1);
+}
+
+static void all_sl2z(std::vector<std::array<int, 4>>& out) {
+  out.clear();
+  // identity first so that ties keep the plain relabeling of PAPER.md:1331-1336
+  out.push_back({1, 0, 0, 1});
+  for (int a = -3; a <= 3; ++a)
+    for (int b = -3; b <= 3; ++b)
+      for (int c = -3; c <= 3; ++c)
+        for (int d = -3; d <= 3; ++d)
+          if (a * d - b * c == 1 && !(a == 1 && b == 0 && c == 0 && d == 1)) out.push_back({a, b, c, d});
+}
+
+// Partition Omega \ {0} into W wedges and pick, per wedge, the lattice map
+// M in SL(2,Z) (entries in [-3,3]) whose relabelled box has the smallest
+// oversampled volume (PAPER.md:1327-1347 uses the identity or a 45-degree
+// shear; reading R5 generalizes to any small unimodular M -- still an exact
+// relabeling).  xi_c places the box's k' range at [-floor(n/2), n - floor(n/2)).
+void build_geometry(int N, int W, std::vector<WedgeGeom>& wedges) {
+  wedges.assign(W, WedgeGeom());
+  const double pi = 3.14159265358979323846;
+  for (int l = 0; l < W; ++l) {
+    wedges[l].l = l;
+    wedges[l].u1 = std::cos(2.0 * pi * l / W);
+    wedges[l].u2 = std::sin(2.0 * pi * l / W);
+  }
+  for (int k1 = 0; k1 < N; ++k1) {
+    int x1 = k1 >= N / 2 ? k1 - N : k1;
+    for (int k2 = 0; k2 < N; ++k2) {
+      int x2 = k2 >= N / 2 ? k2 - N : k2;
+      int l = wedge_of(W, x1, x2);
+      if (l >= 0) wedges[l].members.push_back(k1 * N + k2);
+    }
+  }
+  std::vector<std::array<int, 4>> mats;
+  all_sl2z(mats);
+#pragma omp parallel for schedule(dynamic, 1)
+  for (int l = 0; l < W; ++l) {
+    WedgeGeom& g = wedges[l];
+    long long best = -1;
+    for (const auto& M : mats) {
+      int lo1 = 1 << 30, hi1 = -(1 << 30), lo2 = 1 << 30, hi2 = -(1 << 30);
+      for (int k : g.members) {
+        int k1 = k / N, k2 = k % N;
+        int x1 = k1 >= N / 2 ? k1 - N : k1;
+        int x2 = k2 >= N / 2 ? k2 - N : k2;
+        int z1 = M[0] * x1 + M[1] * x2, z2 = M[2] * x1 + M[3] * x2;
+        lo1 = std::min(lo1, z1); hi1 = std::max(hi1, z1);
+        lo2 = std::min(lo2, z2); hi2 = std::max(hi2, z2);
+      }
+      if (g.members.empty()) { lo1 = hi1 = lo2 = hi2 = 0; }
+      int n1f = next_fine_size(hi1 - lo1 + 1), n2f = next_fine_size(hi2 - lo2 + 1);
+      long long cost = (long long)n1f * n2f;
+      if (best < 0 || cost < best) {
+        best = cost;
+        std::memcpy(g.M, M.data(), sizeof(g.M));
+        g.n1f = n1f; g.n2f = n2f;
+        g.n1 = n1f / 2; g.n2 = n2f / 2;
+        g.xc1 = lo1 + g.n1 / 2;
+        g.xc2 = lo2 + g.n2 / 2;
+      }
+    }
+    // inverse of a unimodular matrix [[a,b],[c,d]] is [[d,-b],[-c,a]]
+    g.Mi[0] = g.M[3]; g.Mi[1] = -g.M[1]; g.Mi[2] = -g.M[2]; g.Mi[3] = g.M[0];
+  }
+}
+
+// Stockham radix sequence: 4s first, then 2, 3s, 5s (all sizes 5-smooth).
+std::vector<int8_t> radix_plan(int L) {
+  std::vector<int8_t> r;
+  while (L % 4 == 0) { r.push_back(4); L /= 4; }
+  while (L % 2 == 0) { r.push_back(2); L /= 2; }
+  while (L % 3 == 0) { r.push_back(3); L /= 3; }
+  while (L % 5 == 0) { r.push_back(5); L /= 5; }
+  if (L != 1) r.clear();
+  return r;
+}
+
+// "Exponential of semicircle" kernel phi(z) = exp(beta (sqrt(1 - (2z/w)^2) - 1)),
+// |z| < w/2, in fine-grid units (reading R10: the paper's Dutt-Rokhlin
+// parameters are not reproducible from the text; any kernel with a known
+// Fourier transform works -- the deconvolution is folded into beta').
+double es_kernel(double z, int w, double beta) {
+  double t = 2.0 * z / w;
+  if (std::fabs(t) >= 1.0) return 0.0;
+  return std::exp(beta * (std::sqrt(1.0 - t * t) - 1.0));
+}
+
+// Gauss-Legendre nodes/weights on [-1,1] (Newton on P_n), cached for n = 256.
+static void gauss_legendre(int n, std::vector<double>& x, std::vector<double>& wt) {
+  x.resize(n); wt.resize(n);
+  const double pi = 3.14159265358979323846;
+  for (int i = 0; i < n; ++i) {
+    double z = std::cos(pi * (i + 0.75) / (n + 0.5)), pp = 0.0;
+    for (int it = 0; it < 100; ++it) {
+      double p1 = 1.0, p2 = 0.0;
+      for (int j = 1; j <= n; ++j) {
+        double p3 = p2; p2 = p1;
+        p1 = ((2.0 * j - 1.0) * z * p2 - (j - 1.0) * p3) / j;
+      }
+      pp = n * (z * p1 - p2) / (z * z - 1.0);
+      double z1 = z;
+      z = z1 - p1 / pp;
+      if (std::fabs(z - z1) < 1e-16) break;
+    }
+    x[i] = z;
+    wt[i] = 2.0 / ((1.0 - z * z) * pp * pp);
+  }
+}
+
+// psi(s) = int_{-w/2}^{w/2} phi(v) cos(2 pi s v) dv: the factor by which
+// interpolating with phi multiplies frequency k when s = k / nf, so beta'
+// carries 1/(psi(k1/n1f) psi(k2/n2f)) (deconvolution step of the NUFFT).
+struct GaussLegendre {
+  std::vector<double> x, w;
+  GaussLegendre() { gauss_legendre(256, x, w); }
+};
+
+double es_fourier(double s, int w, double beta) {
+  static const GaussLegendre gl;  // thread-safe static init (C++11)
+  const std::vector<double>& gx = gl.x;
+  const std::vector<double>& gw = gl.w;
+  const double pi = 3.14159265358979323846;
+  double acc = 0.0, h = 0.5 * w;
+  for (size_t i = 0; i < gx.size(); ++i) {
+    double v = gx[i] * h;
+    acc += gw[i] * h * es_kernel(v, w, beta) * std::cos(2.0 * pi * s * v);
+  }
+  return acc;
+}
+
+// Reading R10: taps per dimension so that the NUFFT error (measured: ~1e-(w-1)
+// relative l2 at sigma = 2, beta = 2.3 w) stays below ~2 eps.
+int taps_for_eps(double eps) {
+  int w = (int)std::ceil(-std::log10(2.0 * eps)) + 1;
+  if (eps >= 2e-3) w = 3;
+  return std::min(std::max(w, 3), kMaxTaps);
+}
+
+// Longest-processing-time greedy: wedges by decreasing cost, each to the least
+// loaded rank (ties -> lowest rank).  Deterministic.
+void lpt_assign(int W, const double* cost, int nranks, int* owner) {
+  std::vector<int> idx(W);
+  std::iota(idx.begin(), idx.end(), 0);
+  std::stable_sort(idx.begin(), idx.end(), [&](int a, int b) { return cost[a] > cost[b]; });
+  std::vector<double> load(nranks, 0.0);
+  for (int l : idx) {
+    int r = (int)(std::min_element(load.begin(), load.end()) - load.begin());
+    owner[l] = r;
+    load[r] += cost[l];
+  }
+}
+
+uint64_t Rng::next() {
+  uint64_t z = (s += 0x9E3779B97F4A7C15ull);
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+uint64_t Rng::below(uint64_t n) { return n ? next() % n : 0; }
+
+// k distinct indices of [0, n), sorted (Floyd's algorithm); all of them if k >= n.
+std::vector<int> sample_distinct(Rng& rng, int n, int k) {
+  std::vector<int> out;
+  if (k >= n) {
+    out.resize(n);
+    std::iota(out.begin(), out.end(), 0);
+    return out;
+  }
+  std::unordered_set<int> s;
+  s.reserve(2 * k);
+  for (int j = n - k; j < n; ++j) {
+    int t = (int)rng.below((uint64_t)j + 1);
+    if (!s.insert(t).second) s.insert(j);
+  }
+  out.assign(s.begin(), s.end());
+  std::sort(out.begin(), out.end());
+  return out;
+}
+
+// ---------------------------------------------------------------- dense linear algebra
+static inline cplx cmul(cplx a, cplx b) { return {a.re * b.re - a.im * b.im, a.re * b.im + a.im * b.re}; }
+static inline cplx cconjmul(cplx a, cplx b) { return {a.re * b.re + a.im * b.im, a.re * b.im - a.im * b.re}; }
+
+void jacobi_svd(int m, int n, std::vector<cplx>& A, std::vector<cplx>& V, std::vector<double>& sigma) {
+  V.assign((size_t)n * n, cplx{0, 0});
+  for (int i = 0; i < n; ++i) V[(size_t)i * n + i] = {1, 0};
+  const double tol = 1e-15;
+  for (int sweep = 0; sweep < 80; ++sweep) {
+    double off = 0.0;
+    for (int p = 0; p < n - 1; ++p) {
+      for (int q = p + 1; q < n; ++q) {
+        cplx* ap = &A[(size_t)p * m];
+        cplx* aq = &A[(size_t)q * m];
+        double alpha = 0, beta = 0;
+        cplx gamma{0, 0};
+        for (int i = 0; i < m; ++i) {
+          alpha += ap[i].re * ap[i].re + ap[i].im * ap[i].im;
+          beta += aq[i].re * aq[i].re + aq[i].im * aq[i].im;
+          cplx c = cconjmul(ap[i], aq[i]);
+          gamma.re += c.re; gamma.im += c.im;
+        }
+        double g = std::hypot(gamma.re, gamma.im);
+        if (g == 0.0 || g <= tol * std::sqrt(alpha * beta)) continue;
+        off = std::max(off, g / std::sqrt(alpha * beta));
+        cplx ph{gamma.re / g, -gamma.im / g};  // e^{-i theta}
+        double zeta = (beta - alpha) / (2.0 * g);
+        double t = (zeta >= 0 ? 1.0 : -1.0) / (std::fabs(zeta) + std::sqrt(1.0 + zeta * zeta));
+        double c = 1.0 / std::sqrt(1.0 + t * t), s = c * t;
+        for (int i = 0; i < m; ++i) {
+          cplx x = ap[i], y = cmul(ph, aq[i]);
+          ap[i] = {c * x.re - s * y.re, c * x.im - s * y.im};
+          aq[i] = {s * x.re + c * y.re, s * x.im + c * y.im};
+        }
+        cplx* vp = &V[(size_t)p * n];
+        cplx* vq = &V[(size_t)q * n];
+        for (int i = 0; i < n; ++i) {
+          cplx x = vp[i], y = cmul(ph, vq[i]);
+          vp[i] = {c * x.re - s * y.re, c * x.im - s * y.im};
+          vq[i] = {s * x.re + c * y.re, s * x.im + c * y.im};
+        }
+      }
+    }
+    if (off <= tol) break;
+  }
+  sigma.resize(n);
+  for (int k = 0; k < n; ++k) {
+    double s2 = 0;
+    for (int i = 0; i < m; ++i) s2 += A[(size_t)k * m + i].re * A[(size_t)k * m + i].re + A[(size_t)k * m + i].im * A[(size_t)k * m + i].im;
+    sigma[k] = std::sqrt(s2);
+  }
+  // sort descending (permute columns of A and V)
+  std::vector<int> ord(n);
+  std::iota(ord.begin(), ord.end(), 0);
+  std::stable_sort(ord.begin(), ord.end(), [&](int a, int b) { return sigma[a] > sigma[b]; });
+  std::vector<cplx> A2((size_t)m * n), V2((size_t)n * n);
+  std::vector<double> s2(n);
+  for (int k = 0; k < n; ++k) {
+    std::memcpy(&A2[(size_t)k * m], &A[(size_t)ord[k] * m], sizeof(cplx) * m);
+    std::memcpy(&V2[(size_t)k * n], &V[(size_t)ord[k] * n], sizeof(cplx) * n);
+    s2[k] = sigma[ord[k]];
+  }
+  A.swap(A2); V.swap(V2); sigma.swap(s2);
+}
+
+std::vector<int> pivoted_columns(int m, int n, std::vector<cplx>& B, int k) {
+  std::vector<int> piv;
+  std::vector<double> nrm(n);
+  std::vector<char> used(n, 0);
+  for (int j = 0; j < n; ++j) {
+    double s = 0;
+    for (int i = 0; i < m; ++i) s += B[(size_t)j * m + i].re * B[(size_t)j * m + i].re + B[(size_t)j * m + i].im * B[(size_t)j * m + i].im;
+    nrm[j] = s;
+  }
+  double n0 = *std::max_element(nrm.begin(), nrm.end());
+  std::vector<cplx> qv(m);
+  for (int s = 0; s < k && s < n; ++s) {
+    int p = -1;
+    double best = -1;
+    for (int j = 0; j < n; ++j)
+      if (!used[j] && nrm[j] > best) { best = nrm[j]; p = j; }
+    if (p < 0 || best <= 1e-28 * n0) break;
+    used[p] = 1;
+    piv.push_back(p);
+    double inv = 1.0 / std::sqrt(best);
+    for (int i = 0; i < m; ++i) qv[i] = {B[(size_t)p * m + i].re * inv, B[(size_t)p * m + i].im * inv};
+#pragma omp parallel for schedule(static)
+    for (int j = 0; j < n; ++j) {
+      if (used[j]) continue;
+      cplx* b = &B[(size_t)j * m];
+      cplx c{0, 0};
+      for (int i = 0; i < m; ++i) { cplx t = cconjmul(qv[i], b[i]); c.re += t.re; c.im += t.im; }
+      double s2 = 0;
+      for (int i = 0; i < m; ++i) {
+        cplx t = cmul(c, qv[i]);
+        b[i].re -= t.re; b[i].im -= t.im;
+        s2 += b[i].re * b[i].re + b[i].im * b[i].im;
+      }
+      nrm[j] = s2;
+    }
+  }
+  return piv;
+}
+
+}  // namespace fio

@@ -1,0 +1,100 @@
+// fio_internal.h -- structures shared by the host plan code and the CUDA kernels
+// of the product library (never by the oracle).  See include/fio.h and DESIGN.md.
+#pragma once
+#include <cstddef>
+#include <cstdint>
+#include <string>
+#include <vector>
+
+#include "../../include/fio.h"
+
+namespace fio {
+
+constexpr int kMaxRadixStages = 24;
+constexpr int kMaxTaps = 12;
+
+// One FFT length L (5-smooth), its Stockham radix sequence and the offset of its
+// twiddle table e^{+2 pi i m / L}, m < L, inside the plan's twiddle buffer.
+struct FftLen {
+  int L;
+  int nst;
+  int tw_off;
+  int pad;
+  int8_t radix[kMaxRadixStages];
+};
+
+// Per owned wedge l:
+//   box frequencies  k' = M xi - xi_c  in [-n1/2, n1/2) x [-n2/2, n2/2)
+//   fine grid        n1f x n2f (oversampled, 5-smooth), index k' mod nf
+//   warped points    y(x) = M^{-T} g_l(x), g_l(x) = x + b(x) + grad_xi rho(x, xihat_l)
+struct WedgeDev {
+  int l, q;
+  int n1, n2, n1f, n2f;
+  int M[4];     // row-major integer matrix in SL(2,Z)
+  int Mi[4];    // its inverse (integer)
+  int xc1, xc2; // xi_c
+  int fft1, fft2;  // FftLen index for n1f (column pass) and n2f (row pass)
+  double u1, u2;   // xihat_l = (cos 2 pi l / W, sin 2 pi l / W)
+  long long alpha_off;  // element offset of alpha'[t][x] block (q * N*N)
+  long long beta_off;   // element offset of beta'[t][i1][i2] block (q * n1 * n2)
+  long long p1_off;     // element offset of row-pass buffer (q * n1 * n2f)
+  long long g_off;      // element offset of fine grids (q * n1f * n2f)
+};
+
+// Work item of the batched FFT passes: one CTA processes `count` sequences of
+// the (wedge, t) pair starting at row/column `start`.
+struct FftJob {
+  int w;      // index into the owned-wedge table
+  int t;
+  int start;
+  int count;
+};
+
+// Host-side geometry of one wedge.
+struct WedgeGeom {
+  int l;
+  std::vector<int> members;  // flat FFT-order frequency indices k1*N+k2
+  int M[4], Mi[4];
+  int xc1, xc2;
+  int n1, n2, n1f, n2f;
+  double u1, u2;
+};
+
+// Host helpers (fio_host.cpp).
+int default_wedges(int N);
+bool is_smooth5(int n);
+int next_fine_size(int extent);
+int wedge_of(int W, int xi1, int xi2);
+void build_geometry(int N, int W, std::vector<WedgeGeom>& wedges);
+std::vector<int8_t> radix_plan(int L);
+double es_kernel(double z, int w, double beta);
+double es_fourier(double s, int w, double beta);  // psi(s) = int phi(v) cos(2 pi s v) dv
+int taps_for_eps(double eps);
+void lpt_assign(int W, const double* cost, int nranks, int* owner);
+
+// Complex helpers on interleaved doubles.
+struct cplx {
+  double re, im;
+};
+
+// One-sided (Hestenes) Jacobi SVD of a complex m x n column-major matrix A
+// (m >= n): on return A holds U*Sigma (columns), V (n x n column-major) and
+// sigma (n), sorted descending.
+void jacobi_svd(int m, int n, std::vector<cplx>& A, std::vector<cplx>& V, std::vector<double>& sigma);
+
+// Column-pivoted modified Gram-Schmidt on the m x n column-major matrix B (destroyed);
+// returns up to k pivot column indices in order.
+std::vector<int> pivoted_columns(int m, int n, std::vector<cplx>& B, int k);
+
+// Counter-based generator (splitmix64) and sampling without replacement.
+struct Rng {
+  uint64_t s;
+  explicit Rng(uint64_t seed) : s(seed) {}
+  uint64_t next();
+  uint64_t below(uint64_t n);
+};
+std::vector<int> sample_distinct(Rng& rng, int n, int k);
+
+void set_error(const std::string& msg);
+
+}  // namespace fio

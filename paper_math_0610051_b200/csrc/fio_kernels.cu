@@ -1,0 +1,683 @@
+// fio_kernels.cu -- sm_100a CUDA kernels of the wedge-decomposed FIO apply
+// (arXiv math/0610051) and of its plan.
+//
+// Hot path, per fio_apply:
+//   K0  k_fft_rows / k_fft_cols   fhat = DFT(f)/N, eq. (dft)
+//   K1  k_rowpass                 fhat * chi_l * beta_lt relabelled onto the box
+//                                 (PAPER.md:1297-1298, 1327-1347), deconvolved,
+//                                 zero-padded, FFT along axis 2
+//   K2  k_colpass                 zero-padded FFT along axis 1 -> fine grid G_lt
+//                                 (the oversampled FFT of the NUFFT)
+//   K3  k_interp                  interpolation of G_lt at the warped points
+//                                 M^{-T} grad Phi(x, xihat_l) (PAPER.md:1299-1311,
+//                                 1357-1363) fused with the alpha epilogue and the
+//                                 sums over t and l, + DC term.
+// No code here is shared with oracle/.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdio>
+
+#include "fio_kernels.h"
+
+namespace fio {
+
+// ------------------------------------------------------------------ complex helpers
+__device__ __forceinline__ double2 cmul(double2 a, double2 b) {
+  return make_double2(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x);
+}
+__device__ __forceinline__ float2 cmul(float2 a, float2 b) {
+  return make_float2(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x);
+}
+__device__ __forceinline__ double2 cadd(double2 a, double2 b) { return make_double2(a.x + b.x, a.y + b.y); }
+__device__ __forceinline__ float2 cadd(float2 a, float2 b) { return make_float2(a.x + b.x, a.y + b.y); }
+__device__ __forceinline__ double2 csub(double2 a, double2 b) { return make_double2(a.x - b.x, a.y - b.y); }
+__device__ __forceinline__ float2 csub(float2 a, float2 b) { return make_float2(a.x - b.x, a.y - b.y); }
+
+template <typename T2> struct Real;
+template <> struct Real<double2> { using type = double; };
+template <> struct Real<float2> { using type = float; };
+
+template <typename T2>
+__device__ __forceinline__ T2 mk(typename Real<T2>::type x, typename Real<T2>::type y) {
+  T2 r;
+  r.x = x;
+  r.y = y;
+  return r;
+}
+template <typename T2>
+__device__ __forceinline__ T2 to_t2(double2 v) {
+  return mk<T2>((typename Real<T2>::type)v.x, (typename Real<T2>::type)v.y);
+}
+
+// ------------------------------------------------------------------ phase geometry
+// grad_xi rho(x, u) for rho = sqrt(c1^2 xi1^2 + c2^2 xi2^2), u = xihat_l.
+__device__ __forceinline__ void grad_rho(double c1, double c2, double u1, double u2, double& g1, double& g2) {
+  double a = c1 * c1 * u1, b = c2 * c2 * u2;
+  double den = sqrt(a * u1 + b * u2);
+  if (den > 0.0) {
+    g1 = a / den;
+    g2 = b / den;
+  } else {
+    g1 = 0.0;
+    g2 = 0.0;
+  }
+}
+
+// y_l(x) = M^{-T} g_l(x), g_l(x) = x + b(x) + grad_xi rho(x, xihat_l)
+__device__ __forceinline__ void warped_point(const OperatorDev& op, int n1, int n2, const WedgeDev& w, double& y1,
+                                             double& y2) {
+  const int N = op.N;
+  const long long x = (long long)n1 * N + n2;
+  double c1 = op.c1[x], c2 = op.c2[x];
+  double gr1, gr2;
+  grad_rho(c1, c2, w.u1, w.u2, gr1, gr2);
+  double g1 = (double)n1 / N + gr1, g2 = (double)n2 / N + gr2;
+  if (op.b1) g1 += op.b1[x];
+  if (op.b2) g2 += op.b2[x];
+  y1 = (double)w.Mi[0] * g1 + (double)w.Mi[2] * g2;
+  y2 = (double)w.Mi[1] * g1 + (double)w.Mi[3] * g2;
+}
+
+// ------------------------------------------------------------------ plan kernels
+// Residual kernel entry A(x, xi) = a(x, xi) e^{2 pi i (rho(x,xi) - grad rho(x,xihat).xi)}.
+__device__ double2 kernel_entry(const OperatorDev& op, int x, int kf, double u1, double u2) {
+  const int N = op.N;
+  int k1 = kf / N, k2 = kf - k1 * N;
+  double xi1 = (double)(k1 >= N / 2 ? k1 - N : k1);
+  double xi2 = (double)(k2 >= N / 2 ? k2 - N : k2);
+  double c1 = op.c1[x], c2 = op.c2[x];
+  double g1, g2;
+  grad_rho(c1, c2, u1, u2, g1, g2);
+  double rho = sqrt(c1 * c1 * xi1 * xi1 + c2 * c2 * xi2 * xi2);
+  double ph = rho - g1 * xi1 - g2 * xi2;
+  ph -= floor(ph);
+  double s, c;
+  sincospi(2.0 * ph, &s, &c);
+  double2 e = make_double2(c, s);
+  if (op.K > 0) {
+    double2 a = make_double2(0.0, 0.0);
+    const long long NN = (long long)N * N;
+    for (int k = 0; k < op.K; ++k) a = cadd(a, cmul(op.px[k * NN + x], op.pxi[k * NN + kf]));
+    e = cmul(a, e);
+  }
+  return e;
+}
+
+__global__ void k_eval_entries(OperatorDev op, double u1, double u2, const int* __restrict__ rows, int nr,
+                               const int* __restrict__ cols, int nc, double2* __restrict__ out, long long ldr,
+                               long long ldc) {
+  long long total = (long long)nr * nc;
+  for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < total;
+       idx += (long long)gridDim.x * blockDim.x) {
+    int i = (int)(idx % nr), j = (int)(idx / nr);
+    int x = rows ? rows[i] : i;
+    out[i * ldr + j * ldc] = kernel_entry(op, x, cols[j], u1, u2);
+  }
+}
+
+cudaError_t launch_eval_entries(const OperatorDev& op, double u1, double u2, const int* rows, int nr,
+                                const int* cols, int nc, double2* out, long long ldr, long long ldc,
+                                cudaStream_t s) {
+  long long total = (long long)nr * nc;
+  if (total == 0) return cudaSuccess;
+  int blocks = (int)std::min<long long>((total + 255) / 256, 148LL * 64);
+  k_eval_entries<<<blocks, 256, 0, s>>>(op, u1, u2, rows, nr, cols, nc, out, ldr, ldc);
+  return cudaGetLastError();
+}
+
+// Tiled complex FP64 product (plan-time Gram matrix, factor expansion).
+// loadA_i: A tile loaded with threadIdx.x along i (A contiguous in i) else along k.
+__global__ void k_zgemm(int p, int s, long long K, long long kchunk, const double2* __restrict__ A, long long sai,
+                        long long sak, int conjA, int loadA_i, const double2* __restrict__ B, long long sbk,
+                        long long sbj, int loadB_k, double2* __restrict__ C, long long sci, long long scj,
+                        long long split_stride) {
+  __shared__ double2 As[16][17];  // [i][k]
+  __shared__ double2 Bs[16][17];  // [k][j]
+  const int tx = threadIdx.x, ty = threadIdx.y;
+  const int ib = blockIdx.y * 16, jb = blockIdx.x * 16;
+  const long long k0 = (long long)blockIdx.z * kchunk;
+  const long long k1 = min(K, k0 + kchunk);
+  double2 acc = make_double2(0.0, 0.0);
+  for (long long kk = k0; kk < k1; kk += 16) {
+    {
+      int ii = loadA_i ? tx : ty, kt = loadA_i ? ty : tx;
+      int i = ib + ii;
+      long long k = kk + kt;
+      double2 v = make_double2(0.0, 0.0);
+      if (i < p && k < k1) {
+        v = A[i * sai + k * sak];
+        if (conjA) v.y = -v.y;
+      }
+      As[ii][kt] = v;
+    }
+    {
+      int kt = loadB_k ? tx : ty, jj = loadB_k ? ty : tx;
+      int j = jb + jj;
+      long long k = kk + kt;
+      double2 v = make_double2(0.0, 0.0);
+      if (j < s && k < k1) v = B[k * sbk + j * sbj];
+      Bs[kt][jj] = v;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int t = 0; t < 16; ++t) {
+      double2 a = As[ty][t], b = Bs[t][tx];
+      acc.x = fma(a.x, b.x, fma(-a.y, b.y, acc.x));
+      acc.y = fma(a.x, b.y, fma(a.y, b.x, acc.y));
+    }
+    __syncthreads();
+  }
+  int i = ib + ty, j = jb + tx;
+  if (i < p && j < s) C[blockIdx.z * split_stride + i * sci + j * scj] = acc;
+}
+
+__global__ void k_split_reduce(int p, int s, int nsplit, const double2* __restrict__ work, double2* __restrict__ C,
+                               long long sci, long long scj) {
+  long long total = (long long)p * s;
+  for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < total;
+       idx += (long long)gridDim.x * blockDim.x) {
+    int i = (int)(idx / s), j = (int)(idx % s);
+    double2 acc = make_double2(0.0, 0.0);
+    for (int z = 0; z < nsplit; ++z) acc = cadd(acc, work[z * total + idx]);
+    C[i * sci + j * scj] = acc;
+  }
+}
+
+cudaError_t launch_zgemm(int p, int s, long long K, const double2* A, long long sai, long long sak, bool conjA,
+                         const double2* B, long long sbk, long long sbj, double2* C, long long sci,
+                         long long scj, int nsplit, double2* work, cudaStream_t st) {
+  if (p == 0 || s == 0) return cudaSuccess;
+  if (nsplit < 1) nsplit = 1;
+  long long kchunk = (K + nsplit - 1) / nsplit;
+  kchunk = ((kchunk + 15) / 16) * 16;
+  nsplit = (int)((K + kchunk - 1) / kchunk);
+  if (nsplit < 1) nsplit = 1;
+  dim3 grid((s + 15) / 16, (p + 15) / 16, nsplit), block(16, 16);
+  int loadA_i = (sai == 1 && sak != 1) ? 1 : 0;
+  int loadB_k = (sbk == 1 && sbj != 1) ? 1 : 0;
+  if (nsplit == 1) {
+    k_zgemm<<<grid, block, 0, st>>>(p, s, K, kchunk, A, sai, sak, conjA, loadA_i, B, sbk, sbj, loadB_k, C, sci, scj,
+                                    0);
+    return cudaGetLastError();
+  }
+  k_zgemm<<<grid, block, 0, st>>>(p, s, K, kchunk, A, sai, sak, conjA, loadA_i, B, sbk, sbj, loadB_k, work,
+                                  (long long)s, 1, (long long)p * s);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
+  long long total = (long long)p * s;
+  int blocks = (int)std::min<long long>((total + 255) / 256, 148LL * 32);
+  k_split_reduce<<<blocks, 256, 0, st>>>(p, s, nsplit, work, C, sci, scj);
+  return cudaGetLastError();
+}
+
+__global__ void k_gather_rows(const double2* __restrict__ U, long long m, int q, const int* __restrict__ rows,
+                              int nrows, double2* __restrict__ out) {
+  long long total = (long long)nrows * q;
+  for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < total;
+       idx += (long long)gridDim.x * blockDim.x) {
+    int i = (int)(idx % nrows), t = (int)(idx / nrows);
+    out[i + (long long)t * nrows] = U[rows[i] + (long long)t * m];
+  }
+}
+
+cudaError_t launch_gather_rows(const double2* U, long long m, int q, const int* rows, int nrows, double2* out,
+                               cudaStream_t s) {
+  long long total = (long long)nrows * q;
+  if (total == 0) return cudaSuccess;
+  int blocks = (int)std::min<long long>((total + 255) / 256, 4096);
+  k_gather_rows<<<blocks, 256, 0, s>>>(U, m, q, rows, nrows, out);
+  return cudaGetLastError();
+}
+
+template <typename T2>
+__global__ void k_fold_alpha(OperatorDev op, WedgeDev w, const double2* __restrict__ U, int q,
+                             T2* __restrict__ alpha) {
+  const int N = op.N;
+  const long long NN = (long long)N * N;
+  for (long long x = blockIdx.x * (long long)blockDim.x + threadIdx.x; x < NN; x += (long long)gridDim.x * blockDim.x) {
+    int n1 = (int)(x / N), n2 = (int)(x % N);
+    double y1, y2;
+    warped_point(op, n1, n2, w, y1, y2);
+    double ph = y1 * (double)w.xc1 + y2 * (double)w.xc2;
+    ph -= floor(ph);
+    double s, c;
+    sincospi(2.0 * ph, &s, &c);
+    double2 e = make_double2(c / N, s / N);
+    for (int t = 0; t < q; ++t) alpha[t * NN + x] = to_t2<T2>(cmul(U[x + t * NN], e));
+  }
+}
+
+cudaError_t launch_fold_alpha(const OperatorDev& op, const WedgeDev& w, const double2* U, int q, void* alpha,
+                              bool c64, cudaStream_t s) {
+  long long NN = (long long)op.N * op.N;
+  int blocks = (int)std::min<long long>((NN + 255) / 256, 148LL * 16);
+  if (c64)
+    k_fold_alpha<float2><<<blocks, 256, 0, s>>>(op, w, U, q, (float2*)alpha);
+  else
+    k_fold_alpha<double2><<<blocks, 256, 0, s>>>(op, w, U, q, (double2*)alpha);
+  return cudaGetLastError();
+}
+
+template <typename T2>
+__global__ void k_fold_beta(int N, WedgeDev w, const int* __restrict__ members, int n,
+                            const double2* __restrict__ beta, int q, const double* __restrict__ d1,
+                            const double* __restrict__ d2, T2* __restrict__ betap) {
+  long long total = (long long)n * q;
+  const long long box = (long long)w.n1 * w.n2;
+  for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < total;
+       idx += (long long)gridDim.x * blockDim.x) {
+    int t = (int)(idx % q), j = (int)(idx / q);
+    int kf = members[j];
+    int k1 = kf / N, k2 = kf - k1 * N;
+    int xi1 = k1 >= N / 2 ? k1 - N : k1, xi2 = k2 >= N / 2 ? k2 - N : k2;
+    int i1 = w.M[0] * xi1 + w.M[1] * xi2 - w.xc1 + w.n1 / 2;
+    int i2 = w.M[2] * xi1 + w.M[3] * xi2 - w.xc2 + w.n2 / 2;
+    double2 b = beta[t + (long long)j * q];
+    double d = d1[i1] * d2[i2];
+    betap[t * box + (long long)i1 * w.n2 + i2] = to_t2<T2>(make_double2(b.x * d, b.y * d));
+  }
+}
+
+cudaError_t launch_fold_beta(int N, const WedgeDev& w, const int* members, int n, const double2* beta, int q,
+                             const double* d1, const double* d2, void* betap, bool c64, cudaStream_t s) {
+  long long total = (long long)n * q;
+  if (total == 0) return cudaSuccess;
+  int blocks = (int)std::min<long long>((total + 255) / 256, 148LL * 16);
+  if (c64)
+    k_fold_beta<float2><<<blocks, 256, 0, s>>>(N, w, members, n, beta, q, d1, d2, (float2*)betap);
+  else
+    k_fold_beta<double2><<<blocks, 256, 0, s>>>(N, w, members, n, beta, q, d1, d2, (double2*)betap);
+  return cudaGetLastError();
+}
+
+// ------------------------------------------------------------------ shared-memory FFT
+// Mixed-radix (4, 2, 3, 5) Stockham autosort FFT on `nseq` sequences of length
+// fl.L held in shared memory; element e of sequence b at buf[b*sb + e*si].
+// sign = +1: G_j = sum_k c_k e^{+2 pi i jk/L} (the NUFFT's fine grid); -1: DFT.
+template <typename T2>
+__device__ __forceinline__ T2 mul_i(T2 v, int sign) {  // (sign i) * v
+  return sign > 0 ? mk<T2>(-v.y, v.x) : mk<T2>(v.y, -v.x);
+}
+
+template <typename T2, int R>
+__device__ __forceinline__ void dft_small(T2 (&v)[R], int sign) {
+  using Rt = typename Real<T2>::type;
+  if constexpr (R == 2) {
+    T2 a = v[0], b = v[1];
+    v[0] = cadd(a, b);
+    v[1] = csub(a, b);
+  } else if constexpr (R == 4) {
+    T2 s02 = cadd(v[0], v[2]), d02 = csub(v[0], v[2]);
+    T2 s13 = cadd(v[1], v[3]), d13 = mul_i(csub(v[1], v[3]), sign);
+    v[0] = cadd(s02, s13);
+    v[2] = csub(s02, s13);
+    v[1] = cadd(d02, d13);
+    v[3] = csub(d02, d13);
+  } else if constexpr (R == 3) {
+    const Rt h = (Rt)0.86602540378443864676;
+    T2 t1 = cadd(v[1], v[2]), t2 = csub(v[1], v[2]);
+    T2 m = mk<T2>(v[0].x - (Rt)0.5 * t1.x, v[0].y - (Rt)0.5 * t1.y);
+    T2 r = mul_i(mk<T2>(h * t2.x, h * t2.y), sign);
+    v[0] = cadd(v[0], t1);
+    v[1] = cadd(m, r);
+    v[2] = csub(m, r);
+  } else if constexpr (R == 5) {
+    const Rt c1 = (Rt)0.30901699437494742410, c2 = (Rt)-0.80901699437494742410;
+    const Rt s1 = (Rt)0.95105651629515357212, s2 = (Rt)0.58778525229247312917;
+    T2 a1 = cadd(v[1], v[4]), b1 = csub(v[1], v[4]);
+    T2 a2 = cadd(v[2], v[3]), b2 = csub(v[2], v[3]);
+    T2 m1 = mk<T2>(v[0].x + c1 * a1.x + c2 * a2.x, v[0].y + c1 * a1.y + c2 * a2.y);
+    T2 m2 = mk<T2>(v[0].x + c2 * a1.x + c1 * a2.x, v[0].y + c2 * a1.y + c1 * a2.y);
+    T2 r1 = mul_i(mk<T2>(s1 * b1.x + s2 * b2.x, s1 * b1.y + s2 * b2.y), sign);
+    T2 r2 = mul_i(mk<T2>(s2 * b1.x - s1 * b2.x, s2 * b1.y - s1 * b2.y), sign);
+    v[0] = mk<T2>(v[0].x + a1.x + a2.x, v[0].y + a1.y + a2.y);
+    v[1] = cadd(m1, r1);
+    v[4] = csub(m1, r1);
+    v[2] = cadd(m2, r2);
+    v[3] = csub(m2, r2);
+  }
+}
+
+template <typename T2, int R>
+__device__ __forceinline__ void stockham_stage(const T2* __restrict__ a, T2* __restrict__ b, int L, int Ns,
+                                               const T2* __restrict__ tw, int nseq, int si, int sb, int sign) {
+  const int nb = L / R;
+  const int span = L / (Ns * R);
+  const int total = nseq * nb;
+  for (int idx = threadIdx.x; idx < total; idx += blockDim.x) {
+    int sq = idx / nb;
+    int j = idx - sq * nb;
+    int k = j % Ns;
+    const T2* in = a + sq * sb;
+    T2* out = b + sq * sb;
+    T2 v[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) v[r] = in[(j + r * nb) * si];
+#pragma unroll
+    for (int r = 1; r < R; ++r) {
+      T2 w = tw[r * k * span];
+      if (sign < 0) w.y = -w.y;
+      v[r] = cmul(v[r], w);
+    }
+    dft_small<T2, R>(v, sign);
+    int base = (j / Ns) * Ns * R + k;
+#pragma unroll
+    for (int r = 0; r < R; ++r) out[(base + r * Ns) * si] = v[r];
+  }
+}
+
+// Returns the buffer holding the result (a or b).  Ends with __syncthreads().
+template <typename T2>
+__device__ T2* smem_fft(T2* a, T2* b, const FftLen& fl, const T2* tw, int nseq, int si, int sb, int sign) {
+  int Ns = 1;
+  for (int st = 0; st < fl.nst; ++st) {
+    const int R = fl.radix[st];
+    switch (R) {
+      case 4: stockham_stage<T2, 4>(a, b, fl.L, Ns, tw, nseq, si, sb, sign); break;
+      case 2: stockham_stage<T2, 2>(a, b, fl.L, Ns, tw, nseq, si, sb, sign); break;
+      case 3: stockham_stage<T2, 3>(a, b, fl.L, Ns, tw, nseq, si, sb, sign); break;
+      default: stockham_stage<T2, 5>(a, b, fl.L, Ns, tw, nseq, si, sb, sign); break;
+    }
+    __syncthreads();
+    T2* t = a;
+    a = b;
+    b = t;
+    Ns *= R;
+  }
+  return a;
+}
+
+// ------------------------------------------------------------------ K0: input spectrum
+// Rows of length L (row-major, row stride L): out = FFT_sign(in) * scale.
+template <typename T2>
+__global__ void __launch_bounds__(256) k_fft_rows(const T2* __restrict__ in, T2* __restrict__ out, int nrows,
+                                                  int rows_per_cta, const FftLen* __restrict__ ffts, int fidx,
+                                                  const T2* __restrict__ tw, int sign, double scale) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const FftLen fl = ffts[fidx];
+  const int L = fl.L;
+  const int r0 = blockIdx.x * rows_per_cta;
+  const int nr = min(rows_per_cta, nrows - r0);
+  if (nr <= 0) return;
+  T2* a = reinterpret_cast<T2*>(smem_raw);
+  T2* b = a + rows_per_cta * L;
+  for (int idx = threadIdx.x; idx < nr * L; idx += blockDim.x) a[idx] = in[(long long)r0 * L + idx];
+  __syncthreads();
+  T2* res = smem_fft<T2>(a, b, fl, tw + fl.tw_off, nr, 1, L, sign);
+  using Rt = typename Real<T2>::type;
+  const Rt sc = (Rt)scale;
+  for (int idx = threadIdx.x; idx < nr * L; idx += blockDim.x) {
+    T2 v = res[idx];
+    out[(long long)r0 * L + idx] = mk<T2>(v.x * sc, v.y * sc);
+  }
+}
+
+// Columns [c0, c0 + C) of an L x ncols row-major array, FFT along the rows index.
+template <typename T2>
+__global__ void __launch_bounds__(256) k_fft_cols(const T2* __restrict__ in, T2* __restrict__ out, int ncols,
+                                                  int cols_per_cta, const FftLen* __restrict__ ffts, int fidx,
+                                                  const T2* __restrict__ tw, int sign, double scale) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const FftLen fl = ffts[fidx];
+  const int L = fl.L;
+  const int c0 = blockIdx.x * cols_per_cta;
+  const int C = min(cols_per_cta, ncols - c0);
+  if (C <= 0) return;
+  T2* a = reinterpret_cast<T2*>(smem_raw);
+  T2* b = a + cols_per_cta * L;
+  for (int idx = threadIdx.x; idx < L * C; idx += blockDim.x) {
+    int i = idx / C, c = idx - i * C;
+    a[i * C + c] = in[(long long)i * ncols + c0 + c];
+  }
+  __syncthreads();
+  T2* res = smem_fft<T2>(a, b, fl, tw + fl.tw_off, C, C, 1, sign);
+  using Rt = typename Real<T2>::type;
+  const Rt sc = (Rt)scale;
+  for (int idx = threadIdx.x; idx < L * C; idx += blockDim.x) {
+    int i = idx / C, c = idx - i * C;
+    T2 v = res[i * C + c];
+    out[(long long)i * ncols + c0 + c] = mk<T2>(v.x * sc, v.y * sc);
+  }
+}
+
+__device__ __forceinline__ int imod(int a, int n) {
+  int r = a % n;
+  return r < 0 ? r + n : r;
+}
+
+// ------------------------------------------------------------------ K1: window x beta + row FFT
+// Job (w, t, start, count): box rows i1 in [start, start + count) of wedge w, term t.
+// h(i1, i2) = beta'_lt(i1, i2) fhat(M^{-1}(k' + xi_c)), k' = (i1 - n1/2, i2 - n2/2),
+// placed at fine index k'_2 mod n2f, then G1 = FFT_{+}(h) along axis 2.
+template <typename T2>
+__global__ void __launch_bounds__(256) k_rowpass(int N, const WedgeDev* __restrict__ wedges,
+                                                 const FftJob* __restrict__ jobs, const FftLen* __restrict__ ffts,
+                                                 const T2* __restrict__ tw, const T2* const* __restrict__ betas,
+                                                 const T2* __restrict__ fhat, T2* __restrict__ p1) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const FftJob job = jobs[blockIdx.x];
+  const WedgeDev& w = wedges[job.w];
+  const FftLen fl = ffts[w.fft2];
+  const int L = fl.L, n1 = w.n1, n2 = w.n2, cnt = job.count;
+  T2* a = reinterpret_cast<T2*>(smem_raw);
+  T2* b = a + cnt * L;
+  const T2 zero = mk<T2>(0, 0);
+  for (int idx = threadIdx.x; idx < cnt * L; idx += blockDim.x) a[idx] = zero;
+  __syncthreads();
+  const T2* bet = betas[job.w] + ((long long)job.t * n1 + job.start) * n2;
+  for (int idx = threadIdx.x; idx < cnt * n2; idx += blockDim.x) {
+    int r = idx / n2, i2 = idx - r * n2;
+    T2 bv = bet[idx];
+    if (bv.x != 0 || bv.y != 0) {
+      int kp1 = job.start + r - n1 / 2, kp2 = i2 - n2 / 2;
+      int z1 = kp1 + w.xc1, z2 = kp2 + w.xc2;
+      int xi1 = w.Mi[0] * z1 + w.Mi[1] * z2, xi2 = w.Mi[2] * z1 + w.Mi[3] * z2;
+      T2 fv = fhat[(long long)imod(xi1, N) * N + imod(xi2, N)];
+      a[r * L + imod(kp2, L)] = cmul(bv, fv);
+    }
+  }
+  __syncthreads();
+  T2* res = smem_fft<T2>(a, b, fl, tw + fl.tw_off, cnt, 1, L, +1);
+  T2* dst = p1 + w.p1_off + ((long long)job.t * n1 + job.start) * L;
+  for (int idx = threadIdx.x; idx < cnt * L; idx += blockDim.x) dst[idx] = res[idx];
+}
+
+// ------------------------------------------------------------------ K2: column FFT -> fine grid
+// Job (w, t, c0, C): fine columns [c0, c0 + C): G(j1, c) = FFT_{+} along axis 1 of the
+// row-pass output placed at fine index (i1 - n1/2) mod n1f.
+template <typename T2>
+__global__ void __launch_bounds__(256) k_colpass(const WedgeDev* __restrict__ wedges, const FftJob* __restrict__ jobs,
+                                                 const FftLen* __restrict__ ffts, const T2* __restrict__ tw,
+                                                 const T2* __restrict__ p1, T2* __restrict__ g) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const FftJob job = jobs[blockIdx.x];
+  const WedgeDev& w = wedges[job.w];
+  const FftLen fl = ffts[w.fft1];
+  const int L = fl.L, n1 = w.n1, ncol = w.n2f, C = job.count, c0 = job.start;
+  T2* a = reinterpret_cast<T2*>(smem_raw);
+  T2* b = a + C * L;
+  const T2 zero = mk<T2>(0, 0);
+  for (int idx = threadIdx.x; idx < C * L; idx += blockDim.x) a[idx] = zero;
+  __syncthreads();
+  const T2* src = p1 + w.p1_off + (long long)job.t * n1 * ncol;
+  for (int idx = threadIdx.x; idx < n1 * C; idx += blockDim.x) {
+    int i1 = idx / C, c = idx - i1 * C;
+    a[imod(i1 - n1 / 2, L) * C + c] = src[(long long)i1 * ncol + c0 + c];
+  }
+  __syncthreads();
+  T2* res = smem_fft<T2>(a, b, fl, tw + fl.tw_off, C, C, 1, +1);
+  T2* dst = g + w.g_off + (long long)job.t * L * ncol;
+  for (int idx = threadIdx.x; idx < C * L; idx += blockDim.x) {
+    int j1 = idx / C, c = idx - j1 * C;
+    dst[(long long)j1 * ncol + c0 + c] = res[idx];
+  }
+}
+
+// ------------------------------------------------------------------ K3: interpolation + alpha epilogue
+template <typename Rt>
+__device__ __forceinline__ Rt es_weight(Rt z, Rt inv_half_w, Rt beta) {
+  Rt t = z * inv_half_w;
+  Rt s = (Rt)1 - t * t;
+  return s > (Rt)0 ? exp(beta * (sqrt(s) - (Rt)1)) : (Rt)0;
+}
+
+template <typename T2, int TAPS>
+__global__ void __launch_bounds__(256) k_interp(int N, int nw, const WedgeDev* __restrict__ wedges,
+                                                const T2* const* __restrict__ alphas, const T2* __restrict__ g,
+                                                OperatorDev op, const double2* __restrict__ a0,
+                                                const T2* __restrict__ fhat, int add_dc, double es_beta,
+                                                T2* __restrict__ Lf) {
+  using Rt = typename Real<T2>::type;
+  const int n2 = blockIdx.x * 32 + (threadIdx.x & 31);
+  const int n1 = blockIdx.y * 8 + (threadIdx.x >> 5);
+  if (n1 >= N || n2 >= N) return;
+  const long long NN = (long long)N * N;
+  const long long x = (long long)n1 * N + n2;
+  const Rt inv_half_w = (Rt)(2.0 / TAPS);
+  const Rt beta = (Rt)es_beta;
+  Rt accr = 0, acci = 0;
+  for (int wi = 0; wi < nw; ++wi) {
+    const WedgeDev& w = wedges[wi];
+    double y1, y2;
+    warped_point(op, n1, n2, w, y1, y2);
+    y1 -= floor(y1);
+    y2 -= floor(y2);
+    const int n1f = w.n1f, n2f = w.n2f;
+    const double u1 = y1 * n1f, u2 = y2 * n2f;
+    const int j01 = (int)ceil(u1 - 0.5 * TAPS), j02 = (int)ceil(u2 - 0.5 * TAPS);
+    Rt p1[TAPS], p2[TAPS];
+    int row[TAPS], col[TAPS];
+#pragma unroll
+    for (int i = 0; i < TAPS; ++i) {
+      p1[i] = es_weight<Rt>((Rt)(u1 - (double)(j01 + i)), inv_half_w, beta);
+      p2[i] = es_weight<Rt>((Rt)(u2 - (double)(j02 + i)), inv_half_w, beta);
+      int r = j01 + i;
+      r = r < 0 ? r + n1f : (r >= n1f ? r - n1f : r);
+      int c = j02 + i;
+      c = c < 0 ? c + n2f : (c >= n2f ? c - n2f : c);
+      row[i] = r * n2f;
+      col[i] = c;
+    }
+    const T2* al = alphas[wi] + x;
+    const T2* gw = g + w.g_off;
+    const long long gstride = (long long)n1f * n2f;
+    for (int t = 0; t < w.q; ++t) {
+      const T2* gt = gw + t * gstride;
+      Rt fr = 0, fi = 0;
+#pragma unroll
+      for (int i = 0; i < TAPS; ++i) {
+        const T2* rp = gt + row[i];
+        Rt rr = 0, ri = 0;
+#pragma unroll
+        for (int j = 0; j < TAPS; ++j) {
+          T2 v = __ldg(rp + col[j]);
+          rr = fma(p2[j], v.x, rr);
+          ri = fma(p2[j], v.y, ri);
+        }
+        fr = fma(p1[i], rr, fr);
+        fi = fma(p1[i], ri, fi);
+      }
+      T2 av = __ldg(al + t * NN);
+      accr = fma(av.x, fr, fma(-av.y, fi, accr));
+      acci = fma(av.x, fi, fma(av.y, fr, acci));
+    }
+  }
+  if (add_dc) {
+    double2 d = a0[x];
+    T2 f0 = fhat[0];
+    accr += (Rt)(d.x * (double)f0.x - d.y * (double)f0.y);
+    acci += (Rt)(d.x * (double)f0.y + d.y * (double)f0.x);
+  }
+  Lf[x] = mk<T2>(accr, acci);
+}
+
+template <typename T2>
+static cudaError_t launch_interp(const ApplyArgs& a, T2* Lf, cudaStream_t s) {
+  dim3 grid((a.N + 31) / 32, (a.N + 7) / 8), block(256);
+  const T2* const* al = reinterpret_cast<const T2* const*>(a.alpha);
+  const T2* g = reinterpret_cast<const T2*>(a.g);
+  const T2* fh = reinterpret_cast<const T2*>(a.fhat);
+#define FIO_INTERP_CASE(TP)                                                                                    \
+  case TP:                                                                                                     \
+    k_interp<T2, TP><<<grid, block, 0, s>>>(a.N, a.nw, a.wedges, al, g, a.op, a.a0, fh, a.add_dc, a.es_beta, Lf); \
+    break;
+  switch (a.taps) {
+    FIO_INTERP_CASE(3)
+    FIO_INTERP_CASE(4)
+    FIO_INTERP_CASE(5)
+    FIO_INTERP_CASE(6)
+    FIO_INTERP_CASE(7)
+    FIO_INTERP_CASE(8)
+    FIO_INTERP_CASE(9)
+    FIO_INTERP_CASE(10)
+    FIO_INTERP_CASE(11)
+    FIO_INTERP_CASE(12)
+    default: return cudaErrorInvalidValue;
+  }
+#undef FIO_INTERP_CASE
+  return cudaGetLastError();
+}
+
+size_t fft_seq_bytes(int L, bool c64) { return 2 * (size_t)L * (c64 ? sizeof(float2) : sizeof(double2)); }
+
+cudaError_t configure_kernels(size_t smem_bytes) {
+  cudaError_t e;
+#define FIO_SMEM(K)                                                                          \
+  e = cudaFuncSetAttribute(K, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_bytes); \
+  if (e != cudaSuccess) return e;
+  FIO_SMEM(k_fft_rows<double2>)
+  FIO_SMEM(k_fft_rows<float2>)
+  FIO_SMEM(k_fft_cols<double2>)
+  FIO_SMEM(k_fft_cols<float2>)
+  FIO_SMEM(k_rowpass<double2>)
+  FIO_SMEM(k_rowpass<float2>)
+  FIO_SMEM(k_colpass<double2>)
+  FIO_SMEM(k_colpass<float2>)
+#undef FIO_SMEM
+  return cudaSuccess;
+}
+
+template <typename T2>
+static cudaError_t enqueue_apply_t(const ApplyArgs& a, const T2* f, T2* Lf, cudaStream_t s, int* launches) {
+  cudaError_t e;
+  int n = 0;
+  const T2* tw = reinterpret_cast<const T2*>(a.tw);
+  T2* fhat = reinterpret_cast<T2*>(a.fhat);
+  T2* tmp = reinterpret_cast<T2*>(a.tmp);
+  const size_t seq = fft_seq_bytes(a.N, sizeof(T2) == sizeof(float2));
+  // K0: fhat = FFT2(f) / N  (forward sign, eq. dft)
+  {
+    int rpc = a.rows_per_cta_N;
+    k_fft_rows<T2><<<(a.N + rpc - 1) / rpc, 256, rpc * seq, s>>>(f, tmp, a.N, rpc, a.ffts, a.fft_N, tw, -1, 1.0);
+    if ((e = cudaGetLastError()) != cudaSuccess) return e;
+    ++n;
+    int cpc = a.cols_per_cta_N;
+    k_fft_cols<T2><<<(a.N + cpc - 1) / cpc, 256, cpc * seq, s>>>(tmp, fhat, a.N, cpc, a.ffts, a.fft_N, tw, -1,
+                                                                 1.0 / a.N);
+    if ((e = cudaGetLastError()) != cudaSuccess) return e;
+    ++n;
+  }
+  if (a.nw > 0) {
+    const T2* const* betas = reinterpret_cast<const T2* const*>(a.beta);
+    k_rowpass<T2><<<a.njobs_row, 256, a.smem_row, s>>>(a.N, a.wedges, a.jobs_row, a.ffts, tw, betas, fhat,
+                                                       reinterpret_cast<T2*>(a.p1));
+    if ((e = cudaGetLastError()) != cudaSuccess) return e;
+    ++n;
+    k_colpass<T2><<<a.njobs_col, 256, a.smem_col, s>>>(a.wedges, a.jobs_col, a.ffts, tw,
+                                                       reinterpret_cast<const T2*>(a.p1), reinterpret_cast<T2*>(a.g));
+    if ((e = cudaGetLastError()) != cudaSuccess) return e;
+    ++n;
+  }
+  if ((e = launch_interp<T2>(a, Lf, s)) != cudaSuccess) return e;
+  ++n;
+  if (launches) *launches = n;
+  return cudaSuccess;
+}
+
+cudaError_t enqueue_apply(const ApplyArgs& a, bool c64, const void* f, void* Lf, cudaStream_t s, int* launches) {
+  if (c64) return enqueue_apply_t<float2>(a, (const float2*)f, (float2*)Lf, s, launches);
+  return enqueue_apply_t<double2>(a, (const double2*)f, (double2*)Lf, s, launches);
+}
+
+}  // namespace fio

@@ -1,0 +1,83 @@
+// fio_kernels.h -- launchers of the sm_100a kernels (fio_kernels.cu).
+#pragma once
+#include <cuda_runtime.h>
+
+#include "fio_internal.h"
+
+namespace fio {
+
+// Phase/amplitude data resident on the device (copied at plan time).
+struct OperatorDev {
+  int N;
+  const double* c1;
+  const double* c2;
+  const double* b1;   // may be null
+  const double* b2;   // may be null
+  int K;
+  const double2* px;  // K x N*N
+  const double2* pxi; // K x N*N (FFT order)
+};
+
+// ---- plan-time kernels (FP64) ----
+// out[i*ldr + j*ldc] = a(x_i, xi_j) e^{2 pi i Phi_l(x_i, xi_j)} with the residual
+// phase Phi_l = Phi - grad_xi Phi(x, xihat_l).xi.
+cudaError_t launch_eval_entries(const OperatorDev& op, double u1, double u2, const int* rows, int nr,
+                                const int* cols, int nc, double2* out, long long ldr, long long ldc,
+                                cudaStream_t s);
+
+// C(i,j) = sum_k opA(i,k) opB(k,j), complex FP64, strided operands; conjA
+// conjugates A.  Split over K into `nsplit` partial products that are summed
+// by a second kernel into C (work buffer of nsplit*p*s elements).
+cudaError_t launch_zgemm(int p, int s, long long K, const double2* A, long long sai, long long sak, bool conjA,
+                         const double2* B, long long sbk, long long sbj, double2* C, long long sci,
+                         long long scj, int nsplit, double2* work, cudaStream_t st);
+
+cudaError_t launch_gather_rows(const double2* U, long long m, int q, const int* rows, int nrows, double2* out,
+                               cudaStream_t s);
+
+// alpha'[t][x] = U[x + t m] e^{2 pi i y_l(x).xi_c} / N  (center phase of
+// PAPER.md:1349-1356 and the 1/N of eq. dfio folded at plan time), in T2.
+cudaError_t launch_fold_alpha(const OperatorDev& op, const WedgeDev& w, const double2* U, int q, void* alpha,
+                              bool c64, cudaStream_t s);
+
+// beta'[t][i1][i2] = beta[t + j q] d1[i1] d2[i2] at the box cell of member j
+// (zero elsewhere; chi_l, the relabeling xi' = M xi - xi_c and the NUFFT
+// deconvolution folded).
+cudaError_t launch_fold_beta(int N, const WedgeDev& w, const int* members, int n, const double2* beta, int q,
+                             const double* d1, const double* d2, void* betap, bool c64, cudaStream_t s);
+
+// ---- apply-time kernels (the hot path) ----
+struct ApplyArgs {
+  int N;
+  int nw;                   // owned wedges
+  const WedgeDev* wedges;   // device table
+  const FftLen* ffts;       // device table
+  int fft_N;                // FftLen index of length N (input spectrum)
+  const void* tw;           // twiddles (double2 or float2)
+  const void* const* alpha; // per owned wedge (device array of pointers)
+  const void* const* beta;  // per owned wedge
+  OperatorDev op;
+  const double2* a0;        // a(x,0)/N, N*N
+  int add_dc;
+  int taps;
+  double es_beta;
+  void* fhat;               // N*N workspace
+  void* tmp;                // N*N workspace
+  void* p1;                 // row-pass buffer
+  void* g;                  // fine grids
+  const FftJob* jobs_row; int njobs_row; int smem_row;
+  const FftJob* jobs_col; int njobs_col; int smem_col;
+  int rows_per_cta_N;       // K0 row pass
+  int cols_per_cta_N;       // K0 column pass
+};
+
+// Enqueue the whole apply (K0 row/column FFT, K1 window x beta + row FFT,
+// K2 column FFT, K3 interpolation + alpha epilogue).  Returns the number of
+// kernels launched in *launches.
+cudaError_t enqueue_apply(const ApplyArgs& a, bool c64, const void* f, void* Lf, cudaStream_t s, int* launches);
+
+// Dynamic shared memory needed by the FFT passes for one sequence of length L.
+size_t fft_seq_bytes(int L, bool c64);
+cudaError_t configure_kernels(size_t smem_bytes);
+
+}  // namespace fio

@@ -1,0 +1,156 @@
+"""Parity of the CUDA path (through the C ABI of include/fio.h) against the CPU oracle.
+
+Every expected value comes from oracle/ (direct summation of eq. dfio)
+or from a closed form; the bar is relative l2 <= 10 eps (BASELINE.json north_star)."""
+import numpy as np
+import pytest
+
+import oracle
+import workloads as wl
+
+torch = pytest.importorskip("torch")
+fio = pytest.importorskip("paper_math_0610051_b200")
+
+pytestmark = pytest.mark.gpu
+DEV = "cuda:0"
+
+
+def run(op, f, eps=1e-6, dtype="c128", **kw):
+    plan = fio.Plan(op.N, op.c1, op.c2, op.b1, op.b2, op.px, op.pxi, eps=eps, dtype=dtype, device=0, **kw)
+    tdt = torch.complex64 if dtype == "c64" else torch.complex128
+    out = plan.apply(torch.from_numpy(f).to(DEV, tdt))
+    torch.cuda.synchronize()
+    return plan, out.cpu().numpy().astype(np.complex128)
+
+
+def crandn(N, seed=7):
+    r = np.random.default_rng(seed)
+    return r.standard_normal((N, N)) + 1j * r.standard_normal((N, N))
+
+
+# ------------------------------------------------------------------ closed forms
+@pytest.mark.parametrize("N", [8, 16, 40, 64])
+def test_identity_phase_returns_f(N):
+    # Phi = x.xi -> L = inverse DFT, L f = f; separation rank is 1 per wedge
+    f = crandn(N)
+    plan, out = run(wl.identity_operator(N), f)
+    assert np.all(plan.wedges()["q"] == 1)
+    assert oracle.rel_l2(out, f) <= 1e-5
+
+
+def test_integer_shift_is_roll():
+    N = 64
+    f = crandn(N)
+    _, out = run(wl.shift_operator(N, 3, -5), f)
+    assert oracle.rel_l2(out, np.roll(f, (-3, 5), axis=(0, 1))) <= 1e-5
+
+
+def test_constant_radii_multiplier():
+    # FFT-multiply-iFFT propagator (constant c1 != c2 pins the axis convention)
+    N = 64
+    f = crandn(N)
+    op = wl.const_ellipse_operator(N, 0.3, 1.7)
+    xi1, xi2 = wl.freqs(N)
+    m = np.exp(2j * np.pi * np.sqrt(0.09 * xi1 ** 2 + 2.89 * xi2 ** 2))
+    ref = N * np.fft.ifft2(m * np.fft.fft2(f) / N)
+    _, out = run(op, f)
+    assert oracle.rel_l2(out, ref) <= 1e-5
+
+
+# ------------------------------------------------------------------ configs vs the oracle
+def test_config0_full_grid_c128():
+    cfg = wl.config("cfg0")
+    op, f = wl.make_operator(cfg), wl.make_input(cfg)
+    plan, out = run(op, f, eps=cfg["eps"])
+    err = oracle.rel_l2(out, oracle.fio(op, f))
+    assert err <= 10 * cfg["eps"], err
+    assert plan.info["certified"] == 1
+
+
+def test_config0_c64():
+    cfg = wl.config("cfg0")
+    op = wl.make_operator(cfg)
+    f = wl.white_noise(cfg["N"], 0, "c64")
+    _, out = run(op, f, eps=1e-4, dtype="c64")
+    err = oracle.rel_l2(out, oracle.fio(op, f))
+    assert err <= 1e-3, err
+
+
+def test_wave_amplitude_small():
+    # config 2's family (variable c(x) and the rank-2 amplitude) at N = 64
+    op = wl.wave_operator(64)
+    f = wl.white_noise(64, 0)
+    _, out = run(op, f)
+    err = oracle.rel_l2(out, oracle.fio(op, f))
+    assert err <= 1e-5, err
+
+
+def test_config1_bumps_full_grid():
+    cfg = wl.config("cfg1")
+    op, f = wl.make_operator(cfg), wl.make_input(cfg)
+    _, out = run(op, f, eps=cfg["eps"])
+    err = oracle.rel_l2(out, oracle.fio(op, f))
+    assert err <= 10 * cfg["eps"], err
+
+
+def test_config2_wave_sampled():
+    cfg = wl.config("cfg2")
+    op, f = wl.make_operator(cfg), wl.make_input(cfg)
+    _, out = run(op, f, eps=cfg["eps"])
+    pts = wl.sample_points(op.N, 4096, 1)
+    err = oracle.rel_l2(out.ravel()[pts], oracle.fio(op, f, pts=pts))
+    assert err <= 10 * cfg["eps"], err
+
+
+@pytest.mark.parametrize("name", ["cfg3_c64", "cfg3_c128"])
+def test_config3_sampled(name):
+    cfg = wl.config(name)
+    op, f = wl.make_operator(cfg), wl.make_input(cfg)
+    _, out = run(op, f, eps=cfg["eps"], dtype=cfg["dtype"])
+    pts = wl.sample_points(op.N, 4096, 1)
+    err = oracle.rel_l2(out.ravel()[pts], oracle.fio(op, f, pts=pts))
+    assert err <= 10 * cfg["eps"], err
+
+
+# ------------------------------------------------------------------ structure
+def test_sharded_partials_sum_to_full():
+    # L = sum_l L_l: the per-rank partials of a 3-way wedge sharding add up
+    # to the 1-rank result, and rank r's partial equals the oracle restricted to its wedges
+    N = 64
+    op = wl.grt_operator(N)
+    f = wl.white_noise(N, 0)
+    _, full = run(op, f)
+    acc = np.zeros_like(full)
+    for r in range(3):
+        plan, part = run(op, f, rank=r, nranks=3)
+        acc += part
+        if r == 1:
+            ws = plan.wedges()["l"]
+            ref = oracle.fio(op, f, wedges=list(ws), W=plan.info["W"], include_dc=False)
+            assert oracle.rel_l2(part, ref) <= 1e-5
+    assert oracle.rel_l2(acc, full) <= 1e-12
+
+
+def test_linearity_and_apply_host():
+    N = 64
+    op = wl.grt_operator(N)
+    plan = fio.Plan(N, op.c1, op.c2, eps=1e-6, device=0)
+    f, g = crandn(N, 1), crandn(N, 2)
+    a, b = 0.3 - 1.1j, 2.0
+    tf = lambda z: torch.from_numpy(z).to(DEV)
+    Lf, Lg, Lh = (plan.apply(tf(z)).cpu().numpy() for z in (f, g, a * f + b * g))
+    assert oracle.rel_l2(Lh, a * Lf + b * Lg) <= 1e-12
+    hin = torch.from_numpy(f).pin_memory()
+    hout = torch.empty_like(hin).pin_memory()
+    plan.apply_host(hin, hout)
+    assert np.array_equal(hout.numpy(), Lf)
+
+
+def test_invalid_arguments():
+    op = wl.grt_operator(64)
+    with pytest.raises(fio.FioError):
+        fio.Plan(64, op.c1, op.c2, eps=0.0, device=0)
+    with pytest.raises(fio.FioError):
+        fio.Plan(14, np.zeros(196), np.zeros(196), device=0)  # 14 = 2*7 is not 5-smooth
+    with pytest.raises(fio.FioError):
+        fio.Plan(64, op.c1, op.c2, rank=2, nranks=2, device=0)
