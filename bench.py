@@ -1,0 +1,309 @@
+"""bench.py -- FIO applies/s at N=1024 on 1..8 B200s (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config cfg3_c128] [--impl fio|reference]
+
+A step is one full fio_apply (K0 input FFT, K1 window x beta + row FFT, K2 column
+FFT, K3 interpolation + alpha epilogue; + the reduce-scatter over NCCL when the
+wedges are sharded over N ranks) of one synthetic N x N input already resident
+in HBM.  Default workload: BASELINE config 3 (N=1024 generalized-Radon FIO) in
+complex128 at eps = 1e-6; the complex64 / eps = 1e-4 variant of the same config
+is timed in the same run and reported under "variants".  Rank 0 prints ONE
+JSON line.  `--impl reference` times the CPU oracle (direct summation, eq. dfio)
+on a bounded sample of the same workload -- the only other place bench.py runs
+oracle/.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import workloads as wl  # noqa: E402  (input generators only)
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=20)
+    p.add_argument("--warmup", type=int, default=5)
+    p.add_argument("--config", default="cfg3_c128")
+    p.add_argument("--variant", default="cfg3_c64", help="second config timed in the same run ('' = none)")
+    p.add_argument("--impl", default="fio", choices=["fio", "reference"])
+    p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--cpu-points", type=int, default=2048, help="oracle sample size (output points)")
+    return p.parse_args()
+
+
+def dist_env():
+    return int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)), int(os.environ.get("LOCAL_RANK", 0))
+
+
+# ---------------------------------------------------------------- clocks
+class Clocks:
+    """nvidia-smi sampled every 200 ms during the timed region (B200_PROFILING.md clocks line)."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.p = None
+
+    def __enter__(self):
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}",
+                                       "--format=csv,noheader,nounits", "-lms", "200"],
+                                      stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.p = None
+        return self
+
+    def __exit__(self, *a):
+        self.rows = []
+        if self.p is None:
+            return
+        time.sleep(0.25)
+        self.p.terminate()
+        try:
+            out, _ = self.p.communicate(timeout=5)
+        except Exception:
+            self.p.kill()
+            out = ""
+        for line in out.strip().splitlines():
+            f = [x.strip() for x in line.split(",")]
+            if len(f) >= 9:
+                self.rows.append(f)
+
+    def summary(self):
+        rows = getattr(self, "rows", [])
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in rows if r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({n for r in rows for n, v in zip(names, r[5:9]) if v.lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(rows)}
+
+
+# ---------------------------------------------------------------- roofline model
+def k3_algorithmic_bytes(info, N, c64):
+    """Algorithmic HBM bytes of one K3 launch: alpha' (N^2 sum_q), every fine grid
+    read once, the phase data c1, c2 (8 B each per x), a(x,0)/N (16 B per x) and the Lf write."""
+    cs = 8 if c64 else 16
+    return info["alpha_bytes"] + info["fine_elems"] * cs + N * N * (8 + 8 + 16 + cs)
+
+
+def apply_algorithmic_bytes(info, N, c64):
+    """Whole apply: K0 (read f, write+read tmp, write fhat), K1 (beta', fhat gather, write P1),
+    K2 (read P1, write G) and K3."""
+    cs = 8 if c64 else 16
+    k0 = 4 * N * N * cs
+    k12 = info["beta_bytes"] + N * N * cs + 2 * info["p1_elems"] * cs + info["fine_elems"] * cs
+    return k0 + k12 + k3_algorithmic_bytes(info, N, c64)
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            mp = json.load(fh)
+        return float(mp["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+# ---------------------------------------------------------------- CPU oracle baseline
+def cpu_oracle_rate(cfg, npts, seed=1):
+    import oracle
+    op = wl.make_operator(cfg)
+    f = wl.make_input(cfg)
+    N = cfg["N"]
+    fh = oracle.dft2(f)
+    pts = wl.sample_points(N, npts, seed)
+    t0 = time.perf_counter()
+    oracle.fio(op, fhat=fh, pts=pts)
+    dt = time.perf_counter() - t0
+    pps = len(pts) / dt
+    return {"value": pps / (N * N), "unit": "applies/s", "points_per_s": pps, "cores": oracle.num_threads(),
+            "kind": "oracle",
+            "sample": f"{len(pts)} seeded output points of the N={N} grid (direct sum over all N^2 frequencies, "
+                      f"fhat precomputed), {dt:.1f} s; applies/s = points/s / N^2"}
+
+
+def run_reference(args):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return
+    cfg = wl.config(args.config)
+    N = cfg["N"]
+    times = []
+    npts = max(64, args.cpu_points // 4)
+    for i in range(args.warmup + args.steps):
+        r = cpu_oracle_rate(cfg, npts, seed=1 + i)
+        if i >= args.warmup:
+            times.append(r)
+    pps = statistics.median([t["points_per_s"] for t in times])
+    val = pps / (N * N)
+    line = {"metric": "fio_applies_per_s", "value": val, "unit": "applies/s", "n_gpus": 0, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": 1e3 / val, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic", "impl": "reference",
+            "config": {"workload": args.config, "N": N, "eps": cfg["eps"]},
+            "points_per_s": pps,
+            "cpu_baseline": {"value": val, "unit": "applies/s", "cores": times[0]["cores"], "kind": "oracle",
+                             "sample": f"each step: {npts} seeded output points (direct sum), median over steps"},
+            "e2e": {"value": val, "unit": "applies/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------- GPU arm
+def time_config(name, args, rank, world, local, group):
+    import torch
+    import torch.distributed as dist
+    import paper_math_0610051_b200 as fio
+
+    cfg = wl.config(name)
+    N = cfg["N"]
+    c64 = cfg["dtype"] == "c64"
+    op = wl.make_operator(cfg)
+    f_np = wl.make_input(cfg)
+    dev = torch.device("cuda", local)
+    plan = fio.Plan(N, op.c1, op.c2, op.b1, op.b2, op.px, op.pxi, eps=cfg["eps"], dtype=cfg["dtype"],
+                    device=local, rank=rank, nranks=world)
+    info = plan.info
+    tdt = torch.complex64 if c64 else torch.complex128
+    f = torch.from_numpy(f_np).to(dev, tdt)
+    stream = torch.cuda.current_stream(dev)
+
+    def step():
+        if world > 1:
+            return plan.apply_sharded(f, group=group)
+        return plan.apply(f, out=out)
+
+    out = torch.empty_like(f)
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize(dev)
+    if world > 1:
+        dist.barrier(group=group)
+    plan.profile_begin(args.steps)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with Clocks(local) as clk:
+        torch.cuda.synchronize(dev)
+        if world > 1:
+            dist.barrier(group=group)
+        e0.record(stream)
+        for _ in range(args.steps):
+            step()
+        e1.record(stream)
+        torch.cuda.synchronize(dev)
+        if world > 1:
+            dist.barrier(group=group)
+    ms = e0.elapsed_time(e1)
+    stages = plan.profile_end()
+    if world > 1:
+        t = torch.tensor([ms], device=dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX, group=group)
+        ms = float(t.item())
+    ms_step = ms / args.steps
+    applies_per_s = 1e3 / ms_step
+    # e2e through the public API with host buffers (pinned), copies inside the timed region
+    hin = torch.from_numpy(f_np.astype(np.complex64 if c64 else np.complex128)).pin_memory()
+    hout = torch.empty_like(hin).pin_memory()
+    e2e = None
+    if world == 1:
+        for _ in range(2):
+            plan.apply_host(hin, hout)
+        t0 = time.perf_counter()
+        for _ in range(args.steps):
+            plan.apply_host(hin, hout)
+        e2e_s = (time.perf_counter() - t0) / args.steps
+        e2e = {"value": 1.0 / e2e_s, "unit": "applies/s", "h2d_bytes_per_step": hin.numel() * hin.element_size(),
+               "d2h_bytes_per_step": hout.numel() * hout.element_size()}
+    n = max(stages["n"], 1)
+    k3_ms = stages["K3_interp"] / n
+    hbm, src = peaks()
+    k3_bytes = k3_algorithmic_bytes(info, N, c64)
+    ach = k3_bytes / (k3_ms * 1e-3) / 1e9
+    total_stage = sum(stages[k] for k in fio.STAGES) / n
+    res = {
+        "name": name, "N": N, "eps": cfg["eps"], "dtype": "c64" if c64 else "c128",
+        "ms_per_step": ms_step, "applies_per_s": applies_per_s, "points_per_s": applies_per_s * N * N,
+        "stage_ms": {k: stages[k] / n for k in fio.STAGES},
+        "k3_share": k3_ms / total_stage if total_stage > 0 else None,
+        "roofline": {"bound": "hbm", "achieved": ach, "peak": hbm, "unit": "GB/s", "frac": ach / hbm,
+                     "traffic": None, "kernel": "k_interp (K3)", "peak_source": src,
+                     "algorithmic_bytes": k3_bytes},
+        "apply_hbm_gbs": apply_algorithmic_bytes(info, N, c64) / (ms_step * 1e-3) / 1e9,
+        "plan": {"W": info["W"], "sum_q": info["sum_q"], "nufft_w": info["nufft_w"],
+                 "plan_seconds": info["plan_seconds"], "max_sep_err": info["max_sep_err"],
+                 "alpha_GB": info["alpha_bytes"] / 1e9, "fine_elems": info["fine_elems"]},
+        "launches_per_step": info["launches_per_apply"],
+        "clocks": clk.summary(), "e2e": e2e,
+    }
+    plan.close()
+    del f, out
+    torch.cuda.empty_cache()
+    return res
+
+
+def run_gpu(args):
+    import torch
+    import torch.distributed as dist
+    rank, world, local = dist_env()
+    group = None
+    if world > 1:
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        group = dist.group.WORLD
+    else:
+        torch.cuda.set_device(local)
+    main = time_config(args.config, args, rank, world, local, group)
+    variants = {}
+    if args.variant:
+        v = time_config(args.variant, args, rank, world, local, group)
+        variants[args.variant] = {k: v[k] for k in ("dtype", "eps", "applies_per_s", "points_per_s", "ms_per_step",
+                                                    "roofline", "stage_ms", "k3_share", "plan", "e2e")}
+    if rank == 0:
+        cpu = None
+        if world == 1 and not args.no_cpu_baseline:
+            cpu = cpu_oracle_rate(wl.config(args.config), args.cpu_points)
+        line = {
+            "metric": "fio_applies_per_s", "value": main["applies_per_s"], "unit": "applies/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": main["ms_per_step"],
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+            "dtype": main["dtype"], "data": "synthetic",
+            "config": {"workload": args.config, "N": main["N"], "eps": main["eps"],
+                       "parallelism": f"wedge-sharded x{world}" if world > 1 else "single GPU",
+                       "l2": "inputs larger than L2 (alpha' streams %.1f GB per step)" % main["plan"]["alpha_GB"]},
+            "points_per_s": main["points_per_s"],
+            "roofline": main["roofline"], "apply_hbm_gbs": main["apply_hbm_gbs"], "stage_ms": main["stage_ms"],
+            "k3_share": main["k3_share"], "plan": main["plan"],
+            "clocks": main["clocks"], "e2e": main["e2e"],
+            "gpu_launches": main["launches_per_step"] * args.steps,
+            "cpu_baseline": cpu, "variants": variants,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_gpu(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -48,7 +48,7 @@ typedef enum { FIO_C64 = 1, FIO_C128 = 2 } fio_dtype;
 typedef enum {
   FIO_OK = 0,
   FIO_WNOTCERT = 1,   /* plan built, but a wedge's sampled separation error
-                          exceeded eps; it still evaluates */
+                          exceeded 10 eps; it still evaluates */
   FIO_EINVAL = -1,    /* bad argument (message says which) */
   FIO_ENOMEM = -2,    /* device or host allocation failed */
   FIO_ECUDA = -3,     /* CUDA runtime error (launch or sync) */
@@ -100,7 +100,7 @@ typedef struct {
 
 void fio_default_opts(fio_opts* opts);
 
-/* Build a plan for the N x N operator (N even, 5-smooth, 8 <= N <= 8192) at
+/* Build a plan for the N x N operator (N even, 5-smooth, 8 <= N <= 4096) at
  * separation accuracy eps in (0, 1) (the relative singular
  * value cutoff, reading R6).  opts may be NULL (defaults).  Runs on the device
  * (kernel-entry evaluation, Gram products, factor expansion) and the host
@@ -155,6 +155,14 @@ fio_status fio_geometry(int N, int W, int* wedge_of, int* M, int* xc, int* box);
 /* Wedge -> rank assignment used for nranks > 1 (owner[l] in [0, nranks)), from
  * per-wedge costs (longest-processing-time greedy, deterministic). Host-only. */
 fio_status fio_assign_wedges(int W, const double* cost, int nranks, int* owner);
+
+/* Live per-stage timing for bench.py: after fio_profile_begin(h, S), each of the
+ * next S applies records CUDA events between its kernels on its stream;
+ * fio_profile_end synchronizes and writes, per stage (K0 rows, K0 cols, K1, K2,
+ * K3 -- 5 entries), the SUM of the stage durations in milliseconds over the
+ * recorded applies, and the number of applies recorded. */
+fio_status fio_profile_begin(fio_handle h, int max_applies);
+fio_status fio_profile_end(fio_handle h, double* stage_ms /* 5 */, int* n_applies);
 
 const char* fio_last_error(void); /* thread-local message of the last error */
 const char* fio_version(void);

@@ -32,7 +32,9 @@ FIO_OK, FIO_WNOTCERT = 0, 1
 
 # every entry point declared in include/fio.h
 SYMBOLS = ["fio_default_opts", "fio_plan", "fio_apply", "fio_apply_host", "fio_destroy", "fio_plan_info",
-           "fio_plan_wedges", "fio_geometry", "fio_assign_wedges", "fio_last_error", "fio_version"]
+           "fio_plan_wedges", "fio_geometry", "fio_assign_wedges", "fio_profile_begin", "fio_profile_end",
+           "fio_last_error", "fio_version"]
+STAGES = ["K0_rows", "K0_cols", "K1_rowpass", "K2_colpass", "K3_interp"]
 
 
 class FioError(RuntimeError):
@@ -91,10 +93,12 @@ def load_library():
     lib.fio_plan_wedges.argtypes = [P, P, P, P, P, P, P, P]
     lib.fio_geometry.argtypes = [I, I, P, P, P, P]
     lib.fio_assign_wedges.argtypes = [I, P, I, P]
+    lib.fio_profile_begin.argtypes = [P, I]
+    lib.fio_profile_end.argtypes = [P, P, P]
     lib.fio_last_error.restype = ctypes.c_char_p
     lib.fio_version.restype = ctypes.c_char_p
     for name in ["fio_plan", "fio_apply", "fio_apply_host", "fio_destroy", "fio_plan_info", "fio_plan_wedges",
-                 "fio_geometry", "fio_assign_wedges"]:
+                 "fio_geometry", "fio_assign_wedges", "fio_profile_begin", "fio_profile_end"]:
         getattr(lib, name).restype = ctypes.c_int
     _lib = lib
     return lib
@@ -219,6 +223,19 @@ class Plan:
             torch.view_as_real(out).reshape(-1)
         dist.reduce_scatter_tensor(slab, real.reshape(-1), op=dist.ReduceOp.SUM, group=group)
         return torch.view_as_complex(slab.reshape(rows, self.N, 2))
+
+    def profile_begin(self, max_applies: int):
+        """Record per-stage CUDA events for the next max_applies applies (on their stream)."""
+        _check(self._lib.fio_profile_begin(self._h, int(max_applies)))
+
+    def profile_end(self) -> dict:
+        """Synchronize and return {stage: total ms} over the recorded applies, plus 'n'."""
+        ms = np.zeros(len(STAGES), np.float64)
+        n = ctypes.c_int(0)
+        _check(self._lib.fio_profile_end(self._h, _ptr(ms), ctypes.byref(n)))
+        out = {k: float(v) for k, v in zip(STAGES, ms)}
+        out["n"] = n.value
+        return out
 
     # ------------------------------------------------------------ introspection
     @property

@@ -135,7 +135,7 @@ __global__ void k_zgemm(int p, int s, long long K, long long kchunk, const doubl
   __shared__ double2 As[16][17];  // [i][k]
   __shared__ double2 Bs[16][17];  // [k][j]
   const int tx = threadIdx.x, ty = threadIdx.y;
-  const int ib = blockIdx.y * 16, jb = blockIdx.x * 16;
+  const int ib = blockIdx.x * 16, jb = blockIdx.y * 16;
   const long long k0 = (long long)blockIdx.z * kchunk;
   const long long k1 = min(K, k0 + kchunk);
   double2 acc = make_double2(0.0, 0.0);
@@ -193,7 +193,7 @@ cudaError_t launch_zgemm(int p, int s, long long K, const double2* A, long long 
   kchunk = ((kchunk + 15) / 16) * 16;
   nsplit = (int)((K + kchunk - 1) / kchunk);
   if (nsplit < 1) nsplit = 1;
-  dim3 grid((s + 15) / 16, (p + 15) / 16, nsplit), block(16, 16);
+  dim3 grid((p + 15) / 16, (s + 15) / 16, nsplit), block(16, 16);
   int loadA_i = (sai == 1 && sak != 1) ? 1 : 0;
   int loadB_k = (sbk == 1 && sbj != 1) ? 1 : 0;
   if (nsplit == 1) {
@@ -639,9 +639,16 @@ cudaError_t configure_kernels(size_t smem_bytes) {
 }
 
 template <typename T2>
-static cudaError_t enqueue_apply_t(const ApplyArgs& a, const T2* f, T2* Lf, cudaStream_t s, int* launches) {
+static cudaError_t enqueue_apply_t(const ApplyArgs& a, const T2* f, T2* Lf, cudaStream_t s, int* launches,
+                                   cudaEvent_t* ev) {
   cudaError_t e;
   int n = 0;
+  int stage = 0;
+  auto mark = [&]() {
+    if (ev) cudaEventRecord(ev[stage], s);
+    ++stage;
+  };
+  mark();
   const T2* tw = reinterpret_cast<const T2*>(a.tw);
   T2* fhat = reinterpret_cast<T2*>(a.fhat);
   T2* tmp = reinterpret_cast<T2*>(a.tmp);
@@ -652,11 +659,13 @@ static cudaError_t enqueue_apply_t(const ApplyArgs& a, const T2* f, T2* Lf, cuda
     k_fft_rows<T2><<<(a.N + rpc - 1) / rpc, 256, rpc * seq, s>>>(f, tmp, a.N, rpc, a.ffts, a.fft_N, tw, -1, 1.0);
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
     ++n;
+    mark();
     int cpc = a.cols_per_cta_N;
     k_fft_cols<T2><<<(a.N + cpc - 1) / cpc, 256, cpc * seq, s>>>(tmp, fhat, a.N, cpc, a.ffts, a.fft_N, tw, -1,
                                                                  1.0 / a.N);
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
     ++n;
+    mark();
   }
   if (a.nw > 0) {
     const T2* const* betas = reinterpret_cast<const T2* const*>(a.beta);
@@ -664,20 +673,27 @@ static cudaError_t enqueue_apply_t(const ApplyArgs& a, const T2* f, T2* Lf, cuda
                                                        reinterpret_cast<T2*>(a.p1));
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
     ++n;
+    mark();
     k_colpass<T2><<<a.njobs_col, 256, a.smem_col, s>>>(a.wedges, a.jobs_col, a.ffts, tw,
                                                        reinterpret_cast<const T2*>(a.p1), reinterpret_cast<T2*>(a.g));
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
     ++n;
+    mark();
+  } else {
+    mark();
+    mark();
   }
   if ((e = launch_interp<T2>(a, Lf, s)) != cudaSuccess) return e;
   ++n;
+  mark();
   if (launches) *launches = n;
   return cudaSuccess;
 }
 
-cudaError_t enqueue_apply(const ApplyArgs& a, bool c64, const void* f, void* Lf, cudaStream_t s, int* launches) {
-  if (c64) return enqueue_apply_t<float2>(a, (const float2*)f, (float2*)Lf, s, launches);
-  return enqueue_apply_t<double2>(a, (const double2*)f, (double2*)Lf, s, launches);
+cudaError_t enqueue_apply(const ApplyArgs& a, bool c64, const void* f, void* Lf, cudaStream_t s, int* launches,
+                          cudaEvent_t* ev) {
+  if (c64) return enqueue_apply_t<float2>(a, (const float2*)f, (float2*)Lf, s, launches, ev);
+  return enqueue_apply_t<double2>(a, (const double2*)f, (double2*)Lf, s, launches, ev);
 }
 
 }  // namespace fio

@@ -74,7 +74,10 @@ struct ApplyArgs {
 // Enqueue the whole apply (K0 row/column FFT, K1 window x beta + row FFT,
 // K2 column FFT, K3 interpolation + alpha epilogue).  Returns the number of
 // kernels launched in *launches.
-cudaError_t enqueue_apply(const ApplyArgs& a, bool c64, const void* f, void* Lf, cudaStream_t s, int* launches);
+// ev (optional): 6 events recorded before K0 and after each of the 5 stages.
+cudaError_t enqueue_apply(const ApplyArgs& a, bool c64, const void* f, void* Lf, cudaStream_t s, int* launches,
+                          cudaEvent_t* ev = nullptr);
+constexpr int kStages = 5;
 
 // Dynamic shared memory needed by the FFT passes for one sequence of length L.
 size_t fft_seq_bytes(int L, bool c64);
