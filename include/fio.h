@@ -135,6 +135,8 @@ typedef struct {
   double plan_seconds;
   size_t alpha_bytes, beta_bytes, workspace_bytes, fine_elems, p1_elems;
   int launches_per_apply; /* kernels one fio_apply enqueues */
+  size_t meta_bytes;      /* K3 point-group tables (anchors, slot indices, offsets) */
+  long long slots;        /* sum over owned wedges of the padded K3 group slots */
 } fio_info;
 
 fio_status fio_plan_info(fio_handle h, fio_info* info);

@@ -65,7 +65,8 @@ class _Info(ctypes.Structure):
                 ("max_sep_err", ctypes.c_double), ("plan_seconds", ctypes.c_double),
                 ("alpha_bytes", ctypes.c_size_t), ("beta_bytes", ctypes.c_size_t),
                 ("workspace_bytes", ctypes.c_size_t), ("fine_elems", ctypes.c_size_t),
-                ("p1_elems", ctypes.c_size_t), ("launches_per_apply", ctypes.c_int)]
+                ("p1_elems", ctypes.c_size_t), ("launches_per_apply", ctypes.c_int),
+                ("meta_bytes", ctypes.c_size_t), ("slots", ctypes.c_longlong)]
 
 
 def library_path() -> str:

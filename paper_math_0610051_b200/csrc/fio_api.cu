@@ -76,6 +76,7 @@ struct fio_plan_s {
   std::vector<double> sep_err;
   std::vector<void*> allocs;
   std::vector<void*> alpha_ptrs, beta_ptrs;
+  std::vector<InterpWedge> iw;
   OperatorDev op{};
   double2* a0 = nullptr;
   WedgeDev* d_wedges = nullptr;
@@ -88,7 +89,8 @@ struct fio_plan_s {
   int njobs_row = 0, njobs_col = 0, smem_row = 0, smem_col = 0;
   int rows_per_cta_N = 1, cols_per_cta_N = 1, fft_N = 0;
   void *e2e_in = nullptr, *e2e_out = nullptr;
-  size_t alpha_bytes = 0, beta_bytes = 0, ws_bytes = 0, fine_elems = 0, p1_elems = 0;
+  size_t alpha_bytes = 0, beta_bytes = 0, ws_bytes = 0, fine_elems = 0, p1_elems = 0, meta_bytes = 0;
+  long long slots = 0;
   double plan_seconds = 0, max_err = 0;
   int certified = 1;
   int launches = 0;
@@ -436,12 +438,49 @@ fio_status build_plan(fio_plan_s& P, const fio_phase* phase, const fio_amplitude
     w.u1 = g.u1; w.u2 = g.u2;
     w.fft1 = fft_index(lens, ffts, g.n1f);
     w.fft2 = fft_index(lens, ffts, g.n2f);
+    // K3 point groups (plan time): fine coordinates -> host grouping -> device tables
+    InterpWedge iw{};
+    iw.q = q;
+    iw.n1f = g.n1f;
+    iw.n2f = g.n2f;
+    iw.n2p = g.n2f + 2 * kHalo;
+    {
+      DevBuf du;
+      FIO_CUDA(du.ensure(sizeof(double2) * NN));
+      FIO_CUDA(launch_fine_coords(P.op, w, du.as<double2>(), s));
+      std::vector<double> uh(2 * NN);
+      FIO_CUDA(cudaMemcpyAsync(uh.data(), du.p, sizeof(double2) * NN, cudaMemcpyDeviceToHost, s));
+      FIO_CUDA(cudaStreamSynchronize(s));
+      std::vector<int> anchor, slot_x;
+      std::vector<double> off;
+      group_points(uh.data(), NN, P.taps, kGroupP, g.n1f, g.n2f, anchor, slot_x, off);
+      iw.ngroups = (int)(anchor.size() / 2);
+      int* d_anchor = nullptr;
+      int* d_slot = nullptr;
+      FIO_CUDA(P.upload(&d_anchor, anchor.data(), anchor.size()));
+      FIO_CUDA(P.upload(&d_slot, slot_x.data(), slot_x.size()));
+      if (c64) {
+        std::vector<float> offf(off.begin(), off.end());
+        float* d_off = nullptr;
+        FIO_CUDA(P.upload(&d_off, offf.data(), offf.size()));
+        iw.slot_off = d_off;
+      } else {
+        double* d_off = nullptr;
+        FIO_CUDA(P.upload(&d_off, off.data(), off.size()));
+        iw.slot_off = d_off;
+      }
+      iw.anchor = d_anchor;
+      iw.slot_x = d_slot;
+      P.meta_bytes += anchor.size() * 4 + slot_x.size() * 4 + off.size() * (c64 ? 4 : 8);
+    }
+    const long long nslots = (long long)iw.ngroups * kGroupP;
     void* alpha = nullptr;
     void* betap = nullptr;
-    FIO_CUDA(P.alloc(&alpha, cs * (size_t)q * NN));
+    FIO_CUDA(P.alloc(&alpha, cs * (size_t)q * nslots));
     FIO_CUDA(P.alloc(&betap, cs * (size_t)q * g.n1 * g.n2));
+    iw.alpha = alpha;
     if (q > 0) {
-      FIO_CUDA(launch_fold_alpha(P.op, w, dU.as<double2>(), q, alpha, c64, s));
+      FIO_CUDA(launch_fold_alpha(P.op, w, dU.as<double2>(), q, iw.slot_x, nslots, alpha, c64, s));
       FIO_CUDA(cudaMemsetAsync(betap, 0, cs * (size_t)q * g.n1 * g.n2, s));
       std::vector<double> d1(g.n1), d2(g.n2);
       for (int i = 0; i < g.n1; ++i) d1[i] = 1.0 / es_fourier((double)(i - g.n1 / 2) / g.n1f, P.taps, P.es_beta);
@@ -457,7 +496,9 @@ fio_status build_plan(fio_plan_s& P, const fio_phase* phase, const fio_amplitude
                                 dd2.as<double>(), betap, c64, s));
       FIO_CUDA(cudaStreamSynchronize(s));
     }
-    P.alpha_bytes += cs * (size_t)q * NN;
+    P.alpha_bytes += cs * (size_t)q * nslots;
+    P.slots += nslots;
+    P.iw.push_back(iw);
     P.beta_bytes += cs * (size_t)q * g.n1 * g.n2;
     P.alpha_ptrs.push_back(alpha);
     P.beta_ptrs.push_back(betap);
@@ -497,8 +538,9 @@ fio_status build_plan(fio_plan_s& P, const fio_phase* phase, const fio_amplitude
     WedgeDev& w = P.wd[wi];
     w.p1_off = p1_off;
     w.g_off = g_off;
+    P.iw[wi].g_off = g_off;
     p1_off += (long long)w.q * w.n1 * w.n2f;
-    g_off += (long long)w.q * w.n1f * w.n2f;
+    g_off += (long long)w.q * w.n1f * (w.n2f + 2 * kHalo);
     size_t sr = fft_seq_bytes(w.n2f, c64), sc = fft_seq_bytes(w.n1f, c64);
     int rows = (int)std::max<size_t>(1, kSmemBudget / sr);
     int cols = (int)std::max<size_t>(1, kSmemBudget / sc);
@@ -532,7 +574,6 @@ fio_status build_plan(fio_plan_s& P, const fio_phase* phase, const fio_amplitude
   if (!jc.empty()) FIO_CUDA(P.upload(&P.jobs_col, jc.data(), jc.size()));
   FIO_CUDA(P.upload(&P.d_ffts, ffts.data(), ffts.size()));
   FIO_CUDA(P.upload(&P.d_wedges, P.wd.data(), std::max<size_t>(P.wd.size(), 1)));
-  FIO_CUDA(P.upload(&P.d_alpha, P.alpha_ptrs.data(), std::max<size_t>(P.alpha_ptrs.size(), 1)));
   FIO_CUDA(P.upload(&P.d_beta, P.beta_ptrs.data(), std::max<size_t>(P.beta_ptrs.size(), 1)));
   FIO_CUDA(P.alloc(&P.fhat, cs * NN));
   FIO_CUDA(P.alloc(&P.tmp, cs * NN));
@@ -551,7 +592,7 @@ ApplyArgs make_args(const fio_plan_s& P) {
   a.ffts = P.d_ffts;
   a.fft_N = P.fft_N;
   a.tw = P.d_tw;
-  a.alpha = const_cast<const void* const*>(P.d_alpha);
+  a.iw = P.iw.data();
   a.beta = const_cast<const void* const*>(P.d_beta);
   a.op = P.op;
   a.a0 = P.a0;
@@ -616,7 +657,7 @@ fio_status fio_plan(fio_handle* out, int N, const fio_phase* phase, const fio_am
     return FIO_EINVAL;
   }
   if (o.nufft_w != 0 && (o.nufft_w < 3 || o.nufft_w > kMaxTaps)) {
-    set_error("fio_plan: nufft_w must be 0 or in [3, 12]");
+    set_error("fio_plan: nufft_w must be 0 or in [3, 10]");
     return FIO_EINVAL;
   }
   if (o.n_wedges < 0 || o.r_init < 0 || o.r_max < 0) {
@@ -652,7 +693,7 @@ fio_status fio_plan(fio_handle* out, int N, const fio_phase* phase, const fio_am
     return st;
   }
   P->plan_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
-  P->launches = 5;
+  P->launches = 4 + std::max<int>(1, (int)P->wd.size());
   *out = P;
   return P->certified ? FIO_OK : FIO_WNOTCERT;
 }
@@ -757,6 +798,8 @@ fio_status fio_plan_info(fio_handle h, fio_info* info) {
   info->max_sep_err = h->max_err;
   info->plan_seconds = h->plan_seconds;
   info->alpha_bytes = h->alpha_bytes;
+  info->meta_bytes = h->meta_bytes;
+  info->slots = h->slots;
   info->beta_bytes = h->beta_bytes;
   info->workspace_bytes = h->ws_bytes;
   info->fine_elems = h->fine_elems;

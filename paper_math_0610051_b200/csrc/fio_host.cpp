@@ -205,6 +205,59 @@ void lpt_assign(int W, const double* cost, int nranks, int* owner) {
   }
 }
 
+static inline long long floor_div2(long long b) { return b >= 0 ? b / 2 : -((-b + 1) / 2); }
+
+// K3 grouping: base cell b = ceil(u - w/2) per axis, supercell
+// s = floor(b / 2); points are counting-sorted by supercell (row-major, then by
+// x) and each supercell's list is cut into groups of P.  The (w+1)^2 window
+// anchored at 2 s covers the w x w taps of every point of the group.
+void group_points(const double* u, long long NN, int taps, int P, int n1f, int n2f, std::vector<int>& anchor,
+                  std::vector<int>& slot_x, std::vector<double>& off) {
+  const long long lo = -((taps + 3) / 2) - 1;  // smallest possible supercell index
+  const long long n1s = n1f / 2 + 8, n2s = n2f / 2 + 8;
+  const long long nkeys = n1s * n2s;
+  std::vector<int> key(NN);
+  std::vector<long long> cnt(nkeys + 1, 0);
+  for (long long x = 0; x < NN; ++x) {
+    long long b1 = (long long)std::ceil(u[2 * x] - 0.5 * taps);
+    long long b2 = (long long)std::ceil(u[2 * x + 1] - 0.5 * taps);
+    long long s1 = floor_div2(b1) - lo, s2 = floor_div2(b2) - lo;
+    long long k = s1 * n2s + s2;
+    key[x] = (int)k;
+    cnt[k + 1]++;
+  }
+  for (long long k = 0; k < nkeys; ++k) cnt[k + 1] += cnt[k];
+  std::vector<int> order(NN);
+  {
+    std::vector<long long> pos(cnt.begin(), cnt.end() - 1);
+    for (long long x = 0; x < NN; ++x) order[pos[key[x]]++] = (int)x;
+  }
+  anchor.clear();
+  slot_x.clear();
+  off.clear();
+  for (long long k = 0; k < nkeys; ++k) {
+    const long long b = cnt[k], e = cnt[k + 1];
+    if (b == e) continue;
+    const int a1 = (int)(2 * (k / n2s + lo)), a2 = (int)(2 * (k % n2s + lo));
+    for (long long i = b; i < e; i += P) {
+      anchor.push_back(a1);
+      anchor.push_back(a2);
+      for (int j = 0; j < P; ++j) {
+        if (i + j < e) {
+          const int x = order[i + j];
+          slot_x.push_back(x);
+          off.push_back(u[2 * (long long)x] - a1);
+          off.push_back(u[2 * (long long)x + 1] - a2);
+        } else {
+          slot_x.push_back(-1);
+          off.push_back(0.5 * taps);
+          off.push_back(0.5 * taps);
+        }
+      }
+    }
+  }
+}
+
 uint64_t Rng::next() {
   uint64_t z = (s += 0x9E3779B97F4A7C15ull);
   z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;

@@ -11,7 +11,9 @@
 namespace fio {
 
 constexpr int kMaxRadixStages = 24;
-constexpr int kMaxTaps = 12;
+constexpr int kMaxTaps = 10;
+constexpr int kGroupP = 4;  // points per K3 group
+constexpr int kHalo = 8;    // periodic column halo on each side of a fine-grid row (K2 writes, K3 reads)
 
 // One FFT length L (5-smooth), its Stockham radix sequence and the offset of its
 // twiddle table e^{+2 pi i m / L}, m < L, inside the plan's twiddle buffer.
@@ -38,7 +40,21 @@ struct WedgeDev {
   long long alpha_off;  // element offset of alpha'[t][x] block (q * N*N)
   long long beta_off;   // element offset of beta'[t][i1][i2] block (q * n1 * n2)
   long long p1_off;     // element offset of row-pass buffer (q * n1 * n2f)
-  long long g_off;      // element offset of fine grids (q * n1f * n2f)
+  long long g_off;      // element offset of fine grids (q * n1f * (n2f + 2 kHalo), haloed rows)
+};
+
+// K3 (interpolation + alpha epilogue) data of one owned wedge.  Points are
+// grouped at plan time: the P points of a group have their base fine cells
+// b = ceil(u - w/2) in the same 2 x 2 "supercell", so one (w+1) x (w+1) window
+// of the fine grid anchored at `anchor` covers all their taps.
+struct InterpWedge {
+  int q, n1f, n2f, ngroups;
+  int n2p;                  // fine row stride n2f + 2 kHalo; column c is stored at kHalo + c
+  long long g_off;          // element offset of this wedge's fine grids
+  const int* anchor;        // 2 ints per group (a1, a2), may be negative (wrapped in K3)
+  const int* slot_x;        // P per group: flat output index, -1 = padding
+  const void* slot_off;     // P per group: (u1 - a1, u2 - a2) as float2 (c64) / double2 (c128)
+  const void* alpha;        // alpha'[t][group*P + k], plan dtype
 };
 
 // Work item of the batched FFT passes: one CTA processes `count` sequences of
@@ -71,6 +87,12 @@ double es_kernel(double z, int w, double beta);
 double es_fourier(double s, int w, double beta);  // psi(s) = int phi(v) cos(2 pi s v) dv
 int taps_for_eps(double eps);
 void lpt_assign(int W, const double* cost, int nranks, int* owner);
+
+// Group the output points of one wedge for K3 (see InterpWedge).  u: 2*NN doubles
+// (fine coordinates in [0, n1f) x [0, n2f)).  Outputs: anchor (2 per group),
+// slot_x (P per group, -1 padding), off (2 per slot: u - anchor).
+void group_points(const double* u, long long NN, int taps, int P, int n1f, int n2f, std::vector<int>& anchor,
+                  std::vector<int>& slot_x, std::vector<double>& off);
 
 // Complex helpers on interleaved doubles.
 struct cplx {

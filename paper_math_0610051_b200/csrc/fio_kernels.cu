@@ -232,30 +232,54 @@ cudaError_t launch_gather_rows(const double2* U, long long m, int q, const int* 
 
 template <typename T2>
 __global__ void k_fold_alpha(OperatorDev op, WedgeDev w, const double2* __restrict__ U, int q,
-                             T2* __restrict__ alpha) {
+                             const int* __restrict__ slot_x, long long nslots, T2* __restrict__ alpha) {
   const int N = op.N;
   const long long NN = (long long)N * N;
-  for (long long x = blockIdx.x * (long long)blockDim.x + threadIdx.x; x < NN; x += (long long)gridDim.x * blockDim.x) {
-    int n1 = (int)(x / N), n2 = (int)(x % N);
+  for (long long sl = blockIdx.x * (long long)blockDim.x + threadIdx.x; sl < nslots;
+       sl += (long long)gridDim.x * blockDim.x) {
+    const int x = slot_x[sl];
+    if (x < 0) {
+      for (int t = 0; t < q; ++t) alpha[t * nslots + sl] = to_t2<T2>(make_double2(0.0, 0.0));
+      continue;
+    }
     double y1, y2;
-    warped_point(op, n1, n2, w, y1, y2);
+    warped_point(op, x / N, x % N, w, y1, y2);
     double ph = y1 * (double)w.xc1 + y2 * (double)w.xc2;
     ph -= floor(ph);
     double s, c;
     sincospi(2.0 * ph, &s, &c);
     double2 e = make_double2(c / N, s / N);
-    for (int t = 0; t < q; ++t) alpha[t * NN + x] = to_t2<T2>(cmul(U[x + t * NN], e));
+    for (int t = 0; t < q; ++t) alpha[t * nslots + sl] = to_t2<T2>(cmul(U[x + t * NN], e));
   }
 }
 
-cudaError_t launch_fold_alpha(const OperatorDev& op, const WedgeDev& w, const double2* U, int q, void* alpha,
-                              bool c64, cudaStream_t s) {
+cudaError_t launch_fold_alpha(const OperatorDev& op, const WedgeDev& w, const double2* U, int q, const int* slot_x,
+                              long long nslots, void* alpha, bool c64, cudaStream_t s) {
+  int blocks = (int)std::min<long long>((nslots + 255) / 256, 148LL * 16);
+  if (c64)
+    k_fold_alpha<float2><<<blocks, 256, 0, s>>>(op, w, U, q, slot_x, nslots, (float2*)alpha);
+  else
+    k_fold_alpha<double2><<<blocks, 256, 0, s>>>(op, w, U, q, slot_x, nslots, (double2*)alpha);
+  return cudaGetLastError();
+}
+
+// Fine-grid coordinates u = frac(y_l(x)) (n1f, n2f) of every output point (plan time, FP64).
+__global__ void k_fine_coords(OperatorDev op, WedgeDev w, double2* __restrict__ u) {
+  const int N = op.N;
+  const long long NN = (long long)N * N;
+  for (long long x = blockIdx.x * (long long)blockDim.x + threadIdx.x; x < NN; x += (long long)gridDim.x * blockDim.x) {
+    double y1, y2;
+    warped_point(op, (int)(x / N), (int)(x % N), w, y1, y2);
+    y1 -= floor(y1);
+    y2 -= floor(y2);
+    u[x] = make_double2(y1 * w.n1f, y2 * w.n2f);
+  }
+}
+
+cudaError_t launch_fine_coords(const OperatorDev& op, const WedgeDev& w, double2* u, cudaStream_t s) {
   long long NN = (long long)op.N * op.N;
   int blocks = (int)std::min<long long>((NN + 255) / 256, 148LL * 16);
-  if (c64)
-    k_fold_alpha<float2><<<blocks, 256, 0, s>>>(op, w, U, q, (float2*)alpha);
-  else
-    k_fold_alpha<double2><<<blocks, 256, 0, s>>>(op, w, U, q, (double2*)alpha);
+  k_fine_coords<<<blocks, 256, 0, s>>>(op, w, u);
   return cudaGetLastError();
 }
 
@@ -507,10 +531,17 @@ __global__ void __launch_bounds__(256) k_colpass(const WedgeDev* __restrict__ we
   }
   __syncthreads();
   T2* res = smem_fft<T2>(a, b, fl, tw + fl.tw_off, C, C, 1, +1);
-  T2* dst = g + w.g_off + (long long)job.t * L * ncol;
+  // haloed row layout: fine column c at kHalo + c, plus periodic copies in the halos
+  const int n2p = ncol + 2 * kHalo;
+  T2* dst = g + w.g_off + (long long)job.t * L * n2p + kHalo;
   for (int idx = threadIdx.x; idx < C * L; idx += blockDim.x) {
     int j1 = idx / C, c = idx - j1 * C;
-    dst[(long long)j1 * ncol + c0 + c] = res[idx];
+    const int col = c0 + c;
+    T2* rowp = dst + (long long)j1 * n2p;
+    const T2 v = res[idx];
+    rowp[col] = v;
+    if (col < kHalo) rowp[ncol + col] = v;
+    if (col >= ncol - kHalo) rowp[col - ncol] = v;
   }
 }
 
@@ -521,102 +552,271 @@ __device__ __forceinline__ Rt es_weight(Rt z, Rt inv_half_w, Rt beta) {
   Rt s = (Rt)1 - t * t;
   return s > (Rt)0 ? exp(beta * (sqrt(s) - (Rt)1)) : (Rt)0;
 }
+template <>
+__device__ __forceinline__ float es_weight<float>(float z, float inv_half_w, float beta) {
+  float t = z * inv_half_w;
+  float s = 1.f - t * t;
+  return s > 0.f ? __expf(beta * (sqrtf(s) - 1.f)) : 0.f;
+}
 
-template <typename T2, int TAPS>
-__global__ void __launch_bounds__(256) k_interp(int N, int nw, const WedgeDev* __restrict__ wedges,
-                                                const T2* const* __restrict__ alphas, const T2* __restrict__ g,
-                                                OperatorDev op, const double2* __restrict__ a0,
-                                                const T2* __restrict__ fhat, int add_dc, double es_beta,
-                                                T2* __restrict__ Lf) {
+// c + a * (b.x, b.y) as one packed FFMA2 (sm_100 fma.rn.f32x2)
+__device__ __forceinline__ float2 ffma2(float a, float2 b, float2 c) {
+  float2 r;
+  asm("{\n\t.reg .b64 ra, rb, rc, rd;\n\t"
+      "mov.b64 ra, {%2, %2};\n\tmov.b64 rb, {%3, %4};\n\tmov.b64 rc, {%5, %6};\n\t"
+      "fma.rn.f32x2 rd, ra, rb, rc;\n\tmov.b64 {%0, %1}, rd;\n\t}"
+      : "=f"(r.x), "=f"(r.y)
+      : "f"(a), "f"(b.x), "f"(b.y), "f"(c.x), "f"(c.y));
+  return r;
+}
+__device__ __forceinline__ float2 cfma_real(float a, float2 b, float2 c) { return ffma2(a, b, c); }
+__device__ __forceinline__ double2 cfma_real(double a, double2 b, double2 c) {
+  return make_double2(fma(a, b.x, c.x), fma(a, b.y, c.y));
+}
+
+template <typename T2> struct OffT;
+template <> struct OffT<float2> { using type = float2; };
+template <> struct OffT<double2> { using type = double2; };
+
+// One thread = one group of P points sharing a (TAPS+1)^2 window of each fine grid
+// G_lt.  For every term t: F_k = sum_i phi1_k[i] sum_j phi2_k[j] G_lt[a1+i][a2+j]
+// (PAPER.md:1305-1311, 1357-1363), acc_k += alpha'_lt(x_k) F_k.
+// The window is loaded once per (group, t) and reused by the P points.
+// Persistent grid-stride loop over the wedge's groups; Lf[x_k] is written (first
+// wedge, + the DC term of rank 0) or read-modify-written: each point occurs in
+// exactly one group per wedge, so one launch per wedge is race-free and the
+// summation order over wedges is fixed (deterministic).
+template <typename T2> struct K3Cfg;
+template <> struct K3Cfg<float2> { static constexpr int BLOCK = 256, MINB = 2; };
+template <> struct K3Cfg<double2> { static constexpr int BLOCK = 128, MINB = 2; };
+constexpr int kAlphaStages = 4;  // depth of the per-thread cp.async ring that streams alpha'
+
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+  unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory"); }
+__device__ __forceinline__ void prefetch_l2(const void* p) { asm volatile("prefetch.global.L2 [%0];" ::"l"(p)); }
+
+template <typename T2, int TAPS, int P>
+__global__ void __launch_bounds__(K3Cfg<T2>::BLOCK, K3Cfg<T2>::MINB)
+    k_interp_groups(InterpWedge iw, const T2* __restrict__ gbase, const double2* __restrict__ a0,
+                    const T2* __restrict__ fhat, int first, int add_dc, double es_beta, T2* __restrict__ Lf) {
   using Rt = typename Real<T2>::type;
-  const int n2 = blockIdx.x * 32 + (threadIdx.x & 31);
-  const int n1 = blockIdx.y * 8 + (threadIdx.x >> 5);
-  if (n1 >= N || n2 >= N) return;
-  const long long NN = (long long)N * N;
-  const long long x = (long long)n1 * N + n2;
+  using O2 = typename OffT<T2>::type;
+  constexpr int WIN = TAPS + 1;            // window columns
+  constexpr int WINR = (WIN + 1) & ~1;     // window rows, even for the paired row loop (extra row weight = 0)
+  constexpr int BLOCK = K3Cfg<T2>::BLOCK;
+  constexpr int S = kAlphaStages;
+  constexpr int CHUNKS = P * (int)sizeof(T2) / 16;  // 16-byte cp.async chunks per (group, t)
+  // dynamic shared memory (k3_smem_bytes):
+  //   alpha' ring [stage][thread][P] (each thread reads back only what it copied), then
+  //   phi1 (row weights) [k*WIN + i][thread] (used once per row)
+  extern __shared__ __align__(16) unsigned char k3_smem[];
+  T2* aring = reinterpret_cast<T2*>(k3_smem);
+  Rt* p1s = reinterpret_cast<Rt*>(k3_smem + sizeof(T2) * S * BLOCK * P);
   const Rt inv_half_w = (Rt)(2.0 / TAPS);
   const Rt beta = (Rt)es_beta;
-  Rt accr = 0, acci = 0;
-  for (int wi = 0; wi < nw; ++wi) {
-    const WedgeDev& w = wedges[wi];
-    double y1, y2;
-    warped_point(op, n1, n2, w, y1, y2);
-    y1 -= floor(y1);
-    y2 -= floor(y2);
-    const int n1f = w.n1f, n2f = w.n2f;
-    const double u1 = y1 * n1f, u2 = y2 * n2f;
-    const int j01 = (int)ceil(u1 - 0.5 * TAPS), j02 = (int)ceil(u2 - 0.5 * TAPS);
-    Rt p1[TAPS], p2[TAPS];
-    int row[TAPS], col[TAPS];
+  const int n1f = iw.n1f, n2p = iw.n2p, q = iw.q;
+  const long long gstride = (long long)n1f * n2p;
+  const long long nslots = (long long)iw.ngroups * P;
+  const T2* __restrict__ G = gbase + iw.g_off + kHalo;
+  const T2* __restrict__ alpha = reinterpret_cast<const T2*>(iw.alpha);
+  const O2* __restrict__ offs = reinterpret_cast<const O2*>(iw.slot_off);
+  T2* myring = aring + threadIdx.x * P;
+  T2 f0 = mk<T2>(0, 0);
+  if (add_dc) f0 = fhat[0];
+  for (int g = blockIdx.x * BLOCK + threadIdx.x; g < iw.ngroups; g += gridDim.x * BLOCK) {
+    const T2* __restrict__ al = alpha + (long long)g * P;
+    // prologue: alpha'(t) for t < S-1 in flight
 #pragma unroll
-    for (int i = 0; i < TAPS; ++i) {
-      p1[i] = es_weight<Rt>((Rt)(u1 - (double)(j01 + i)), inv_half_w, beta);
-      p2[i] = es_weight<Rt>((Rt)(u2 - (double)(j02 + i)), inv_half_w, beta);
-      int r = j01 + i;
-      r = r < 0 ? r + n1f : (r >= n1f ? r - n1f : r);
-      int c = j02 + i;
-      c = c < 0 ? c + n2f : (c >= n2f ? c - n2f : c);
-      row[i] = r * n2f;
-      col[i] = c;
-    }
-    const T2* al = alphas[wi] + x;
-    const T2* gw = g + w.g_off;
-    const long long gstride = (long long)n1f * n2f;
-    for (int t = 0; t < w.q; ++t) {
-      const T2* gt = gw + t * gstride;
-      Rt fr = 0, fi = 0;
+    for (int st = 0; st < S - 1; ++st) {
+      if (st < q) {
 #pragma unroll
-      for (int i = 0; i < TAPS; ++i) {
-        const T2* rp = gt + row[i];
-        Rt rr = 0, ri = 0;
-#pragma unroll
-        for (int j = 0; j < TAPS; ++j) {
-          T2 v = __ldg(rp + col[j]);
-          rr = fma(p2[j], v.x, rr);
-          ri = fma(p2[j], v.y, ri);
-        }
-        fr = fma(p1[i], rr, fr);
-        fi = fma(p1[i], ri, fi);
+        for (int c = 0; c < CHUNKS; ++c)
+          cp_async16(reinterpret_cast<char*>(myring + st * BLOCK * P) + 16 * c,
+                     reinterpret_cast<const char*>(al + st * nslots) + 16 * c);
       }
-      T2 av = __ldg(al + t * NN);
-      accr = fma(av.x, fr, fma(-av.y, fi, accr));
-      acci = fma(av.x, fi, fma(av.y, fr, acci));
+      cp_async_commit();
+    }
+    const int a1 = iw.anchor[2 * g], a2 = iw.anchor[2 * g + 1];
+    int xs[P];
+    Rt p2[P][WIN];
+#pragma unroll
+    for (int k = 0; k < P; ++k) {
+      xs[k] = iw.slot_x[g * P + k];
+      O2 o = offs[g * P + k];
+#pragma unroll
+      for (int i = 0; i < WINR; ++i) p1s[(k * WINR + i) * BLOCK + threadIdx.x] = es_weight<Rt>((Rt)o.x - (Rt)i, inv_half_w, beta);
+#pragma unroll
+      for (int i = 0; i < WIN; ++i) p2[k][i] = es_weight<Rt>((Rt)o.y - (Rt)i, inv_half_w, beta);
+    }
+    // window origin: row r0 (wrapped), column a2 (the row halos make a2 .. a2+WIN-1 contiguous)
+    const int r0 = a1 < 0 ? a1 + n1f : a1;
+    const long long wstep_wrap = -(long long)(n1f - 1) * n2p;
+    T2 acc[P];
+#pragma unroll
+    for (int k = 0; k < P; ++k) acc[k] = mk<T2>(0, 0);
+    for (int t = 0; t < q; ++t) {
+      // keep S-1 copies in flight: issue alpha'(t + S - 1)
+      {
+        const int tn = t + S - 1;
+        if (tn < q) {
+#pragma unroll
+          for (int c = 0; c < CHUNKS; ++c)
+            cp_async16(reinterpret_cast<char*>(myring + (tn % S) * BLOCK * P) + 16 * c,
+                       reinterpret_cast<const char*>(al + tn * nslots) + 16 * c);
+        }
+        cp_async_commit();
+      }
+      const bool pf = t + 1 < q;
+      T2 F[P];
+#pragma unroll
+      for (int k = 0; k < P; ++k) F[k] = mk<T2>(0, 0);
+      const T2* __restrict__ rp = G + t * gstride + (long long)r0 * n2p + a2;
+      int r = r0;
+      T2 va[WIN], vb[WIN];
+#pragma unroll
+      for (int j = 0; j < WIN; ++j) va[j] = __ldg(rp + j);
+#pragma unroll 1
+      for (int i = 0; i < WINR; i += 2) {
+        // row i in va; fetch row i+1 into vb, then row i+2 into va while computing
+        if (pf) prefetch_l2(rp + gstride);
+        rp += (r + 1 == n1f) ? wstep_wrap : (long long)n2p;
+        r = (r + 1 == n1f) ? 0 : r + 1;
+#pragma unroll
+        for (int j = 0; j < WIN; ++j) vb[j] = __ldg(rp + j);
+#pragma unroll
+        for (int k = 0; k < P; ++k) {
+          T2 rr = mk<T2>(0, 0);
+#pragma unroll
+          for (int j = 0; j < WIN; ++j) rr = cfma_real(p2[k][j], va[j], rr);
+          F[k] = cfma_real(p1s[(k * WINR + i) * BLOCK + threadIdx.x], rr, F[k]);
+        }
+        if (pf) prefetch_l2(rp + gstride);
+        if (i + 2 < WINR) {
+          rp += (r + 1 == n1f) ? wstep_wrap : (long long)n2p;
+          r = (r + 1 == n1f) ? 0 : r + 1;
+#pragma unroll
+          for (int j = 0; j < WIN; ++j) va[j] = __ldg(rp + j);
+        }
+#pragma unroll
+        for (int k = 0; k < P; ++k) {
+          T2 rr = mk<T2>(0, 0);
+#pragma unroll
+          for (int j = 0; j < WIN; ++j) rr = cfma_real(p2[k][j], vb[j], rr);
+          F[k] = cfma_real(p1s[(k * WINR + i + 1) * BLOCK + threadIdx.x], rr, F[k]);
+        }
+      }
+      cp_async_wait<S - 1>();  // alpha'(t) has landed
+      const T2* ring = myring + (t % S) * BLOCK * P;
+#pragma unroll
+      for (int k = 0; k < P; ++k) {
+        T2 av = ring[k];
+        acc[k].x = fma(av.x, F[k].x, fma(-av.y, F[k].y, acc[k].x));
+        acc[k].y = fma(av.x, F[k].y, fma(av.y, F[k].x, acc[k].y));
+      }
+    }
+    cp_async_wait<0>();
+#pragma unroll
+    for (int k = 0; k < P; ++k) {
+      const int x = xs[k];
+      if (x < 0) continue;
+      T2 base;
+      if (first) {
+        base = mk<T2>(0, 0);
+        if (add_dc) {
+          double2 d = a0[x];
+          base = mk<T2>((Rt)(d.x * (double)f0.x - d.y * (double)f0.y), (Rt)(d.x * (double)f0.y + d.y * (double)f0.x));
+        }
+      } else {
+        base = Lf[x];
+      }
+      Lf[x] = mk<T2>(base.x + acc[k].x, base.y + acc[k].y);
     }
   }
-  if (add_dc) {
-    double2 d = a0[x];
-    T2 f0 = fhat[0];
-    accr += (Rt)(d.x * (double)f0.x - d.y * (double)f0.y);
-    acci += (Rt)(d.x * (double)f0.y + d.y * (double)f0.x);
+}
+
+// Lf = a(x,0) fhat(0) / N (rank 0) or 0: used only when this rank owns no wedge.
+template <typename T2>
+__global__ void k_dc_only(int N, const double2* __restrict__ a0, const T2* __restrict__ fhat, int add_dc,
+                          T2* __restrict__ Lf) {
+  using Rt = typename Real<T2>::type;
+  const long long NN = (long long)N * N;
+  for (long long x = blockIdx.x * (long long)blockDim.x + threadIdx.x; x < NN; x += (long long)gridDim.x * blockDim.x) {
+    T2 v = mk<T2>(0, 0);
+    if (add_dc) {
+      double2 d = a0[x];
+      T2 f0 = fhat[0];
+      v = mk<T2>((Rt)(d.x * (double)f0.x - d.y * (double)f0.y), (Rt)(d.x * (double)f0.y + d.y * (double)f0.x));
+    }
+    Lf[x] = v;
   }
-  Lf[x] = mk<T2>(accr, acci);
+}
+
+template <typename T2, int TAPS, int P>
+constexpr size_t k3_smem_bytes() {
+  return sizeof(T2) * kAlphaStages * K3Cfg<T2>::BLOCK * P +
+         sizeof(typename Real<T2>::type) * P * ((TAPS + 2) & ~1) * K3Cfg<T2>::BLOCK;
+}
+
+template <typename T2, int TAPS, int P>
+static cudaError_t launch_groups_tp(const ApplyArgs& a, int wi, T2* Lf, cudaStream_t s) {
+  constexpr int BLOCK = K3Cfg<T2>::BLOCK;
+  constexpr size_t SMEM = k3_smem_bytes<T2, TAPS, P>();
+  static int blocks_per_sm = -1, sms = 0;
+  if (blocks_per_sm < 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaError_t e = cudaFuncSetAttribute(k_interp_groups<T2, TAPS, P>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)SMEM);
+    if (e != cudaSuccess) return e;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, k_interp_groups<T2, TAPS, P>, BLOCK, SMEM);
+    if (blocks_per_sm < 1) blocks_per_sm = 1;
+  }
+  const InterpWedge& iw = a.iw[wi];
+  int need = (iw.ngroups + BLOCK - 1) / BLOCK;
+  int blocks = std::max(1, std::min(need, blocks_per_sm * sms));
+  k_interp_groups<T2, TAPS, P><<<blocks, BLOCK, SMEM, s>>>(iw, reinterpret_cast<const T2*>(a.g), a.a0,
+                                                        reinterpret_cast<const T2*>(a.fhat), wi == 0 ? 1 : 0,
+                                                        (wi == 0 && a.add_dc) ? 1 : 0, a.es_beta, Lf);
+  return cudaGetLastError();
 }
 
 template <typename T2>
-static cudaError_t launch_interp(const ApplyArgs& a, T2* Lf, cudaStream_t s) {
-  dim3 grid((a.N + 31) / 32, (a.N + 7) / 8), block(256);
-  const T2* const* al = reinterpret_cast<const T2* const*>(a.alpha);
-  const T2* g = reinterpret_cast<const T2*>(a.g);
-  const T2* fh = reinterpret_cast<const T2*>(a.fhat);
-#define FIO_INTERP_CASE(TP)                                                                                    \
-  case TP:                                                                                                     \
-    k_interp<T2, TP><<<grid, block, 0, s>>>(a.N, a.nw, a.wedges, al, g, a.op, a.a0, fh, a.add_dc, a.es_beta, Lf); \
-    break;
-  switch (a.taps) {
-    FIO_INTERP_CASE(3)
-    FIO_INTERP_CASE(4)
-    FIO_INTERP_CASE(5)
-    FIO_INTERP_CASE(6)
-    FIO_INTERP_CASE(7)
-    FIO_INTERP_CASE(8)
-    FIO_INTERP_CASE(9)
-    FIO_INTERP_CASE(10)
-    FIO_INTERP_CASE(11)
-    FIO_INTERP_CASE(12)
-    default: return cudaErrorInvalidValue;
+static cudaError_t launch_interp(const ApplyArgs& a, T2* Lf, cudaStream_t s, int* n) {
+  if (a.nw == 0) {
+    long long NN = (long long)a.N * a.N;
+    int blocks = (int)std::min<long long>((NN + 255) / 256, 148LL * 8);
+    k_dc_only<T2><<<blocks, 256, 0, s>>>(a.N, a.a0, reinterpret_cast<const T2*>(a.fhat), a.add_dc, Lf);
+    ++*n;
+    return cudaGetLastError();
   }
-#undef FIO_INTERP_CASE
-  return cudaGetLastError();
+  for (int wi = 0; wi < a.nw; ++wi) {
+    cudaError_t e;
+#define FIO_GROUPS_CASE(TP)                                            \
+  case TP:                                                             \
+    e = launch_groups_tp<T2, TP, kGroupP>(a, wi, Lf, s);               \
+    break;
+    switch (a.taps) {
+      FIO_GROUPS_CASE(3)
+      FIO_GROUPS_CASE(4)
+      FIO_GROUPS_CASE(5)
+      FIO_GROUPS_CASE(6)
+      FIO_GROUPS_CASE(7)
+      FIO_GROUPS_CASE(8)
+      FIO_GROUPS_CASE(9)
+      FIO_GROUPS_CASE(10)
+      default: return cudaErrorInvalidValue;
+    }
+#undef FIO_GROUPS_CASE
+    if (e != cudaSuccess) return e;
+    ++*n;
+  }
+  return cudaSuccess;
 }
 
 size_t fft_seq_bytes(int L, bool c64) { return 2 * (size_t)L * (c64 ? sizeof(float2) : sizeof(double2)); }
@@ -683,8 +883,7 @@ static cudaError_t enqueue_apply_t(const ApplyArgs& a, const T2* f, T2* Lf, cuda
     mark();
     mark();
   }
-  if ((e = launch_interp<T2>(a, Lf, s)) != cudaSuccess) return e;
-  ++n;
+  if ((e = launch_interp<T2>(a, Lf, s, &n)) != cudaSuccess) return e;
   mark();
   if (launches) *launches = n;
   return cudaSuccess;

@@ -37,8 +37,12 @@ cudaError_t launch_gather_rows(const double2* U, long long m, int q, const int* 
 
 // alpha'[t][x] = U[x + t m] e^{2 pi i y_l(x).xi_c} / N  (center phase of
 // PAPER.md:1349-1356 and the 1/N of eq. dfio folded at plan time), in T2.
-cudaError_t launch_fold_alpha(const OperatorDev& op, const WedgeDev& w, const double2* U, int q, void* alpha,
-                              bool c64, cudaStream_t s);
+// in group-slot order: alpha'[t][s] for slot s with output point slot_x[s] (0 for padding)
+cudaError_t launch_fold_alpha(const OperatorDev& op, const WedgeDev& w, const double2* U, int q, const int* slot_x,
+                              long long nslots, void* alpha, bool c64, cudaStream_t s);
+
+// u[x] = frac(y_l(x)) * (n1f, n2f), FP64 (plan-time input of the point grouping)
+cudaError_t launch_fine_coords(const OperatorDev& op, const WedgeDev& w, double2* u, cudaStream_t s);
 
 // beta'[t][i1][i2] = beta[t + j q] d1[i1] d2[i2] at the box cell of member j
 // (zero elsewhere; chi_l, the relabeling xi' = M xi - xi_c and the NUFFT
@@ -54,12 +58,12 @@ struct ApplyArgs {
   const FftLen* ffts;       // device table
   int fft_N;                // FftLen index of length N (input spectrum)
   const void* tw;           // twiddles (double2 or float2)
-  const void* const* alpha; // per owned wedge (device array of pointers)
+  const InterpWedge* iw;    // host array, one per owned wedge (passed by value to K3)
   const void* const* beta;  // per owned wedge
   OperatorDev op;
   const double2* a0;        // a(x,0)/N, N*N
   int add_dc;
-  int taps;
+  int taps;                 // w (K3 template), groups of kGroupP points
   double es_beta;
   void* fhat;               // N*N workspace
   void* tmp;                // N*N workspace
