@@ -246,7 +246,9 @@ def time_config(name, args, rank, world, local, group):
         "apply_hbm_gbs": apply_algorithmic_bytes(info, N, c64) / (ms_step * 1e-3) / 1e9,
         "plan": {"W": info["W"], "sum_q": info["sum_q"], "nufft_w": info["nufft_w"],
                  "plan_seconds": info["plan_seconds"], "max_sep_err": info["max_sep_err"],
-                 "alpha_GB": info["alpha_bytes"] / 1e9, "fine_elems": info["fine_elems"]},
+                 "alpha_GB": info["alpha_bytes"] / 1e9, "fine_elems": info["fine_elems"],
+                 "slots": info["slots"], "max_tile_cap": info["max_tile_cap"],
+                 "k3_thread_fill": info["slots"] / 4 / max(info["k3_thread_slots"], 1)},
         "launches_per_step": info["launches_per_apply"],
         "clocks": clk.summary(), "e2e": e2e,
     }

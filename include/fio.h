@@ -137,6 +137,8 @@ typedef struct {
   int launches_per_apply; /* kernels one fio_apply enqueues */
   size_t meta_bytes;      /* K3 point-group tables (anchors, slot indices, offsets) */
   long long slots;        /* sum over owned wedges of the padded K3 group slots */
+  long long max_tile_cap; /* largest K3 chunk footprint (fine-grid elements) */
+  long long k3_thread_slots; /* K3 chunks x threads per CTA (slots / P / this = thread fill) */
 } fio_info;
 
 fio_status fio_plan_info(fio_handle h, fio_info* info);

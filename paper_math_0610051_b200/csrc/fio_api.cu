@@ -91,6 +91,8 @@ struct fio_plan_s {
   void *e2e_in = nullptr, *e2e_out = nullptr;
   size_t alpha_bytes = 0, beta_bytes = 0, ws_bytes = 0, fine_elems = 0, p1_elems = 0, meta_bytes = 0;
   long long slots = 0;
+  long long max_tile_cap = 0;
+  long long chunk_threads = 0;  // K3 thread slots (chunks x BLOCK): groups / this = thread fill
   double plan_seconds = 0, max_err = 0;
   int certified = 1;
   int launches = 0;
@@ -471,6 +473,17 @@ fio_status build_plan(fio_plan_s& P, const fio_phase* phase, const fio_amplitude
       }
       iw.anchor = d_anchor;
       iw.slot_x = d_slot;
+      std::vector<int> box;
+      const int blk = c64 ? kK3BlockC64 : kK3BlockC128;
+      const long long cap = chunk_boxes(anchor, blk, (P.taps + 2) & ~1, P.taps + 1,
+                                        c64 ? kK3TileCapC64 : kK3TileCapC128, box);
+      iw.nchunks = (int)(box.size() / 6);
+      P.chunk_threads += (long long)iw.nchunks * blk;
+      iw.tile_cap = (int)cap;
+      int* d_box = nullptr;
+      FIO_CUDA(P.upload(&d_box, box.data(), std::max<size_t>(box.size(), 4)));
+      iw.box = d_box;
+      P.max_tile_cap = std::max(P.max_tile_cap, cap);
       P.meta_bytes += anchor.size() * 4 + slot_x.size() * 4 + off.size() * (c64 ? 4 : 8);
     }
     const long long nslots = (long long)iw.ngroups * kGroupP;
@@ -800,6 +813,8 @@ fio_status fio_plan_info(fio_handle h, fio_info* info) {
   info->alpha_bytes = h->alpha_bytes;
   info->meta_bytes = h->meta_bytes;
   info->slots = h->slots;
+  info->max_tile_cap = h->max_tile_cap;
+  info->k3_thread_slots = h->chunk_threads;
   info->beta_bytes = h->beta_bytes;
   info->workspace_bytes = h->ws_bytes;
   info->fine_elems = h->fine_elems;

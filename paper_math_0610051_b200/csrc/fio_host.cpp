@@ -235,27 +235,76 @@ void group_points(const double* u, long long NN, int taps, int P, int n1f, int n
   anchor.clear();
   slot_x.clear();
   off.clear();
-  for (long long k = 0; k < nkeys; ++k) {
-    const long long b = cnt[k], e = cnt[k + 1];
-    if (b == e) continue;
-    const int a1 = (int)(2 * (k / n2s + lo)), a2 = (int)(2 * (k % n2s + lo));
-    for (long long i = b; i < e; i += P) {
-      anchor.push_back(a1);
-      anchor.push_back(a2);
-      for (int j = 0; j < P; ++j) {
-        if (i + j < e) {
-          const int x = order[i + j];
-          slot_x.push_back(x);
-          off.push_back(u[2 * (long long)x] - a1);
-          off.push_back(u[2 * (long long)x + 1] - a2);
-        } else {
-          slot_x.push_back(-1);
-          off.push_back(0.5 * taps);
-          off.push_back(0.5 * taps);
+  // supercells in serpentine order of 8 x 8 blocks, so that any run of consecutive groups
+  // (one K3 CTA chunk) has a compact footprint on the fine grid
+  const long long BS = 8;
+  const long long nb1 = (n1s + BS - 1) / BS, nb2 = (n2s + BS - 1) / BS;
+  for (long long bb1 = 0; bb1 < nb1; ++bb1) {
+    for (long long jb = 0; jb < nb2; ++jb) {
+      const long long bb2 = (bb1 % 2 == 0) ? jb : nb2 - 1 - jb;
+      for (long long s1 = bb1 * BS; s1 < std::min(n1s, (bb1 + 1) * BS); ++s1) {
+        for (long long s2 = bb2 * BS; s2 < std::min(n2s, (bb2 + 1) * BS); ++s2) {
+          const long long k = s1 * n2s + s2;
+          const long long b = cnt[k], e = cnt[k + 1];
+          if (b == e) continue;
+          const int a1 = (int)(2 * (s1 + lo)), a2 = (int)(2 * (s2 + lo));
+          for (long long i = b; i < e; i += P) {
+            anchor.push_back(a1);
+            anchor.push_back(a2);
+            for (int j = 0; j < P; ++j) {
+              if (i + j < e) {
+                const int x = order[i + j];
+                slot_x.push_back(x);
+                off.push_back(u[2 * (long long)x] - a1);
+                off.push_back(u[2 * (long long)x + 1] - a2);
+              } else {
+                slot_x.push_back(-1);
+                off.push_back(0.5 * taps);
+                off.push_back(0.5 * taps);
+              }
+            }
+          }
         }
       }
     }
   }
+}
+
+// K3 chunks: runs of at most `block` consecutive groups whose windows' bounding box
+// has at most `cap` cells.  Per chunk: {first group, row origin, column origin, rows,
+// columns (even), groups}; returns the largest rows*cols.
+long long chunk_boxes(const std::vector<int>& anchor, int block, int win_rows, int win_cols, long long cap,
+                      std::vector<int>& box) {
+  const long long ng = (long long)anchor.size() / 2;
+  box.clear();
+  long long maxcap = 0;
+  long long c0 = 0;
+  while (c0 < ng) {
+    int rlo = anchor[2 * c0], rhi = rlo, clo = anchor[2 * c0 + 1], chi = clo;
+    long long c1 = c0 + 1;
+    while (c1 < ng && c1 - c0 < block) {
+      const int r = anchor[2 * c1], c = anchor[2 * c1 + 1];
+      const int nrlo = std::min(rlo, r), nrhi = std::max(rhi, r), nclo = std::min(clo, c), nchi = std::max(chi, c);
+      const long long nr = nrhi - nrlo + win_rows;
+      long long nc = nchi - nclo + win_cols;
+      nc += nc & 1;
+      if (nr * nc > cap) break;
+      rlo = nrlo; rhi = nrhi; clo = nclo; chi = nchi;
+      ++c1;
+    }
+    const int nr = rhi - rlo + win_rows;
+    int nc = chi - clo + win_cols;
+    nc += nc & 1;
+    box.push_back((int)c0);
+    box.push_back(rlo);
+    box.push_back(clo);
+    box.push_back(nr);
+    box.push_back(nc);
+    box.push_back((int)(c1 - c0));
+    maxcap = std::max(maxcap, (long long)nr * nc);
+    c0 = c1;
+  }
+  return maxcap;
 }
 
 uint64_t Rng::next() {

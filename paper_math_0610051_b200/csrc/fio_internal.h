@@ -13,6 +13,11 @@ namespace fio {
 constexpr int kMaxRadixStages = 24;
 constexpr int kMaxTaps = 10;
 constexpr int kGroupP = 4;  // points per K3 group
+constexpr int kK3BlockC64 = 256;   // K3 threads per CTA (= groups per chunk), complex64
+constexpr int kK3BlockC128 = 128;  // complex128
+constexpr int kK3Stages = 3;       // cp.async pipeline depth of K3 (fine-grid tiles + alpha')
+constexpr int kK3TileCapC64 = 2048;   // max cells of a K3 chunk footprint, complex64
+constexpr int kK3TileCapC128 = 1024;  // complex128
 constexpr int kHalo = 8;    // periodic column halo on each side of a fine-grid row (K2 writes, K3 reads)
 
 // One FFT length L (5-smooth), its Stockham radix sequence and the offset of its
@@ -55,6 +60,9 @@ struct InterpWedge {
   const int* slot_x;        // P per group: flat output index, -1 = padding
   const void* slot_off;     // P per group: (u1 - a1, u2 - a2) as float2 (c64) / double2 (c128)
   const void* alpha;        // alpha'[t][group*P + k], plan dtype
+  int nchunks;              // chunks of K3 BLOCK consecutive groups
+  int tile_cap;             // max rows*cols of a chunk's window footprint (elements)
+  const int* box;           // 6 per chunk: first group, row origin, column origin, rows, columns, groups
 };
 
 // Work item of the batched FFT passes: one CTA processes `count` sequences of
@@ -93,6 +101,8 @@ void lpt_assign(int W, const double* cost, int nranks, int* owner);
 // slot_x (P per group, -1 padding), off (2 per slot: u - anchor).
 void group_points(const double* u, long long NN, int taps, int P, int n1f, int n2f, std::vector<int>& anchor,
                   std::vector<int>& slot_x, std::vector<double>& off);
+long long chunk_boxes(const std::vector<int>& anchor, int block, int win_rows, int win_cols, long long cap,
+                      std::vector<int>& box);
 
 // Complex helpers on interleaved doubles.
 struct cplx {

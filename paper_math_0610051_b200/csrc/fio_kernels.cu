@@ -587,9 +587,8 @@ template <> struct OffT<double2> { using type = double2; };
 // exactly one group per wedge, so one launch per wedge is race-free and the
 // summation order over wedges is fixed (deterministic).
 template <typename T2> struct K3Cfg;
-template <> struct K3Cfg<float2> { static constexpr int BLOCK = 256, MINB = 2; };
-template <> struct K3Cfg<double2> { static constexpr int BLOCK = 128, MINB = 2; };
-constexpr int kAlphaStages = 4;  // depth of the per-thread cp.async ring that streams alpha'
+template <> struct K3Cfg<float2> { static constexpr int BLOCK = kK3BlockC64, MINB = 2; };
+template <> struct K3Cfg<double2> { static constexpr int BLOCK = kK3BlockC128, MINB = 2; };
 
 __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
   unsigned s = (unsigned)__cvta_generic_to_shared(smem);
@@ -598,25 +597,41 @@ __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
 template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory"); }
-__device__ __forceinline__ void prefetch_l2(const void* p) { asm volatile("prefetch.global.L2 [%0];" ::"l"(p)); }
 
+// Dynamic shared memory of K3: alpha' ring [S][BLOCK][P], phi1 [P*WINR][BLOCK], tile ring [S][tile_cap].
+template <typename T2, int TAPS, int P>
+__host__ __device__ constexpr size_t k3_fixed_smem() {
+  return sizeof(T2) * kK3Stages * K3Cfg<T2>::BLOCK * P +
+         sizeof(typename Real<T2>::type) * P * ((TAPS + 2) & ~1) * K3Cfg<T2>::BLOCK;
+}
+
+// K3: one CTA processes chunks of BLOCK consecutive groups (one group of P points per
+// thread).  For every term t the CTA stages, with cp.async, the footprint tile of the
+// chunk's windows on G_lt (rows wrap mod n1f; columns use the haloed row layout) and
+// each thread's alpha'(t) into a kK3Stages-deep ring, so global latency overlaps the
+// arithmetic of earlier terms.  Per group and term:
+//   F_k = sum_i phi1_k[i] sum_j phi2_k[j] G_lt[a1+i][a2+j]
+//   acc_k += alpha'_lt(x_k) F_k
+// Lf[x_k] is written (first wedge, + the DC term of rank 0) or read-modify-written:
+// each point occurs in exactly one group per wedge, so one launch per wedge is
+// race-free and the summation order over wedges is fixed (deterministic).
 template <typename T2, int TAPS, int P>
 __global__ void __launch_bounds__(K3Cfg<T2>::BLOCK, K3Cfg<T2>::MINB)
     k_interp_groups(InterpWedge iw, const T2* __restrict__ gbase, const double2* __restrict__ a0,
                     const T2* __restrict__ fhat, int first, int add_dc, double es_beta, T2* __restrict__ Lf) {
   using Rt = typename Real<T2>::type;
   using O2 = typename OffT<T2>::type;
-  constexpr int WIN = TAPS + 1;            // window columns
-  constexpr int WINR = (WIN + 1) & ~1;     // window rows, even for the paired row loop (extra row weight = 0)
+  constexpr int WIN = TAPS + 1;         // window columns
+  constexpr int WINR = (WIN + 1) & ~1;  // window rows (even; the extra row has weight 0)
   constexpr int BLOCK = K3Cfg<T2>::BLOCK;
-  constexpr int S = kAlphaStages;
-  constexpr int CHUNKS = P * (int)sizeof(T2) / 16;  // 16-byte cp.async chunks per (group, t)
-  // dynamic shared memory (k3_smem_bytes):
-  //   alpha' ring [stage][thread][P] (each thread reads back only what it copied), then
-  //   phi1 (row weights) [k*WIN + i][thread] (used once per row)
+  constexpr int S = kK3Stages;
+  constexpr int ACH = P * (int)sizeof(T2) / 16;  // 16-byte alpha' chunks per (group, t)
+  constexpr int EPC = 16 / (int)sizeof(T2);      // elements per 16-byte chunk
   extern __shared__ __align__(16) unsigned char k3_smem[];
   T2* aring = reinterpret_cast<T2*>(k3_smem);
   Rt* p1s = reinterpret_cast<Rt*>(k3_smem + sizeof(T2) * S * BLOCK * P);
+  T2* tring = reinterpret_cast<T2*>(k3_smem + k3_fixed_smem<T2, TAPS, P>());
+  const int cap = iw.tile_cap;
   const Rt inv_half_w = (Rt)(2.0 / TAPS);
   const Rt beta = (Rt)es_beta;
   const int n1f = iw.n1f, n2p = iw.n2p, q = iw.q;
@@ -628,89 +643,91 @@ __global__ void __launch_bounds__(K3Cfg<T2>::BLOCK, K3Cfg<T2>::MINB)
   T2* myring = aring + threadIdx.x * P;
   T2 f0 = mk<T2>(0, 0);
   if (add_dc) f0 = fhat[0];
-  for (int g = blockIdx.x * BLOCK + threadIdx.x; g < iw.ngroups; g += gridDim.x * BLOCK) {
+  for (int ch = blockIdx.x; ch < iw.nchunks; ch += gridDim.x) {
+    const int* cb = iw.box + 6 * ch;  // first group, r_lo, c_lo, nr, nc, groups
+    const int g = cb[0] + threadIdx.x;
+    const bool valid = threadIdx.x < cb[5];
+    const int4 bx = make_int4(cb[1], cb[2], cb[3], cb[4]);
+    const int tchunks = bx.z * (bx.w / EPC);                    // 16-byte chunks of one tile
+    const int cpr = bx.w / EPC;
     const T2* __restrict__ al = alpha + (long long)g * P;
-    // prologue: alpha'(t) for t < S-1 in flight
+    // stage term t into ring slot t % S: this thread's alpha'(t) and its share of the tile
+    auto issue = [&](int t) {
+      if (t < q) {
+        const int st = t % S;
+        if (valid) {
 #pragma unroll
-    for (int st = 0; st < S - 1; ++st) {
-      if (st < q) {
-#pragma unroll
-        for (int c = 0; c < CHUNKS; ++c)
-          cp_async16(reinterpret_cast<char*>(myring + st * BLOCK * P) + 16 * c,
-                     reinterpret_cast<const char*>(al + st * nslots) + 16 * c);
+          for (int c = 0; c < ACH; ++c)
+            cp_async16(reinterpret_cast<char*>(myring + st * BLOCK * P) + 16 * c,
+                       reinterpret_cast<const char*>(al + t * nslots) + 16 * c);
+        }
+        const T2* __restrict__ gt = G + t * gstride;
+        T2* tile = tring + st * cap;
+        for (int idx = threadIdx.x; idx < tchunks; idx += BLOCK) {
+          const int rr = idx / cpr, cc = idx - rr * cpr;
+          int r = bx.x + rr;
+          r = r < 0 ? r + n1f : (r >= n1f ? r - n1f : r);
+          cp_async16(tile + rr * bx.w + cc * EPC, gt + (long long)r * n2p + bx.y + cc * EPC);
+        }
       }
       cp_async_commit();
-    }
-    const int a1 = iw.anchor[2 * g], a2 = iw.anchor[2 * g + 1];
+    };
+    __syncthreads();  // the previous chunk is done with every ring slot
+#pragma unroll
+    for (int st = 0; st < S - 1; ++st) issue(st);
+    int a1 = 0, a2 = 0;
     int xs[P];
     Rt p2[P][WIN];
+    T2 base[P];
+    if (valid) {
+      a1 = iw.anchor[2 * g] - bx.x;
+      a2 = iw.anchor[2 * g + 1] - bx.y;
+    }
 #pragma unroll
     for (int k = 0; k < P; ++k) {
-      xs[k] = iw.slot_x[g * P + k];
-      O2 o = offs[g * P + k];
+      O2 o;
+      o.x = (Rt)0;
+      o.y = (Rt)0;
+      xs[k] = -1;
+      if (valid) {
+        xs[k] = iw.slot_x[g * P + k];
+        o = offs[g * P + k];
+      }
 #pragma unroll
-      for (int i = 0; i < WINR; ++i) p1s[(k * WINR + i) * BLOCK + threadIdx.x] = es_weight<Rt>((Rt)o.x - (Rt)i, inv_half_w, beta);
+      for (int i = 0; i < WINR; ++i)
+        p1s[(k * WINR + i) * BLOCK + threadIdx.x] = es_weight<Rt>((Rt)o.x - (Rt)i, inv_half_w, beta);
 #pragma unroll
       for (int i = 0; i < WIN; ++i) p2[k][i] = es_weight<Rt>((Rt)o.y - (Rt)i, inv_half_w, beta);
+      // start the read of the running sum early (latency hidden by the term loop)
+      base[k] = mk<T2>(0, 0);
+      if (xs[k] >= 0 && !first) base[k] = Lf[xs[k]];
     }
-    // window origin: row r0 (wrapped), column a2 (the row halos make a2 .. a2+WIN-1 contiguous)
-    const int r0 = a1 < 0 ? a1 + n1f : a1;
-    const long long wstep_wrap = -(long long)(n1f - 1) * n2p;
+    const int woff = a1 * bx.w + a2;
     T2 acc[P];
 #pragma unroll
     for (int k = 0; k < P; ++k) acc[k] = mk<T2>(0, 0);
     for (int t = 0; t < q; ++t) {
-      // keep S-1 copies in flight: issue alpha'(t + S - 1)
-      {
-        const int tn = t + S - 1;
-        if (tn < q) {
-#pragma unroll
-          for (int c = 0; c < CHUNKS; ++c)
-            cp_async16(reinterpret_cast<char*>(myring + (tn % S) * BLOCK * P) + 16 * c,
-                       reinterpret_cast<const char*>(al + tn * nslots) + 16 * c);
-        }
-        cp_async_commit();
-      }
-      const bool pf = t + 1 < q;
+      cp_async_wait<S - 2>();
+      __syncthreads();  // term t staged by every thread; every thread is done with term t-1
+      issue(t + S - 1);
+      const T2* __restrict__ win = tring + (t % S) * cap + woff;
       T2 F[P];
 #pragma unroll
       for (int k = 0; k < P; ++k) F[k] = mk<T2>(0, 0);
-      const T2* __restrict__ rp = G + t * gstride + (long long)r0 * n2p + a2;
-      int r = r0;
-      T2 va[WIN], vb[WIN];
+#pragma unroll 2
+      for (int i = 0; i < WINR; ++i) {
+        const T2* rowp = win + i * bx.w;
+        T2 v[WIN];
 #pragma unroll
-      for (int j = 0; j < WIN; ++j) va[j] = __ldg(rp + j);
-#pragma unroll 1
-      for (int i = 0; i < WINR; i += 2) {
-        // row i in va; fetch row i+1 into vb, then row i+2 into va while computing
-        if (pf) prefetch_l2(rp + gstride);
-        rp += (r + 1 == n1f) ? wstep_wrap : (long long)n2p;
-        r = (r + 1 == n1f) ? 0 : r + 1;
-#pragma unroll
-        for (int j = 0; j < WIN; ++j) vb[j] = __ldg(rp + j);
+        for (int j = 0; j < WIN; ++j) v[j] = rowp[j];
 #pragma unroll
         for (int k = 0; k < P; ++k) {
           T2 rr = mk<T2>(0, 0);
 #pragma unroll
-          for (int j = 0; j < WIN; ++j) rr = cfma_real(p2[k][j], va[j], rr);
+          for (int j = 0; j < WIN; ++j) rr = cfma_real(p2[k][j], v[j], rr);
           F[k] = cfma_real(p1s[(k * WINR + i) * BLOCK + threadIdx.x], rr, F[k]);
         }
-        if (pf) prefetch_l2(rp + gstride);
-        if (i + 2 < WINR) {
-          rp += (r + 1 == n1f) ? wstep_wrap : (long long)n2p;
-          r = (r + 1 == n1f) ? 0 : r + 1;
-#pragma unroll
-          for (int j = 0; j < WIN; ++j) va[j] = __ldg(rp + j);
-        }
-#pragma unroll
-        for (int k = 0; k < P; ++k) {
-          T2 rr = mk<T2>(0, 0);
-#pragma unroll
-          for (int j = 0; j < WIN; ++j) rr = cfma_real(p2[k][j], vb[j], rr);
-          F[k] = cfma_real(p1s[(k * WINR + i + 1) * BLOCK + threadIdx.x], rr, F[k]);
-        }
       }
-      cp_async_wait<S - 1>();  // alpha'(t) has landed
       const T2* ring = myring + (t % S) * BLOCK * P;
 #pragma unroll
       for (int k = 0; k < P; ++k) {
@@ -724,17 +741,12 @@ __global__ void __launch_bounds__(K3Cfg<T2>::BLOCK, K3Cfg<T2>::MINB)
     for (int k = 0; k < P; ++k) {
       const int x = xs[k];
       if (x < 0) continue;
-      T2 base;
-      if (first) {
-        base = mk<T2>(0, 0);
-        if (add_dc) {
-          double2 d = a0[x];
-          base = mk<T2>((Rt)(d.x * (double)f0.x - d.y * (double)f0.y), (Rt)(d.x * (double)f0.y + d.y * (double)f0.x));
-        }
-      } else {
-        base = Lf[x];
+      T2 b0 = base[k];
+      if (first && add_dc) {
+        double2 d = a0[x];
+        b0 = mk<T2>((Rt)(d.x * (double)f0.x - d.y * (double)f0.y), (Rt)(d.x * (double)f0.y + d.y * (double)f0.x));
       }
-      Lf[x] = mk<T2>(base.x + acc[k].x, base.y + acc[k].y);
+      Lf[x] = mk<T2>(b0.x + acc[k].x, b0.y + acc[k].y);
     }
   }
 }
@@ -757,32 +769,30 @@ __global__ void k_dc_only(int N, const double2* __restrict__ a0, const T2* __res
 }
 
 template <typename T2, int TAPS, int P>
-constexpr size_t k3_smem_bytes() {
-  return sizeof(T2) * kAlphaStages * K3Cfg<T2>::BLOCK * P +
-         sizeof(typename Real<T2>::type) * P * ((TAPS + 2) & ~1) * K3Cfg<T2>::BLOCK;
-}
-
-template <typename T2, int TAPS, int P>
 static cudaError_t launch_groups_tp(const ApplyArgs& a, int wi, T2* Lf, cudaStream_t s) {
   constexpr int BLOCK = K3Cfg<T2>::BLOCK;
-  constexpr size_t SMEM = k3_smem_bytes<T2, TAPS, P>();
-  static int blocks_per_sm = -1, sms = 0;
-  if (blocks_per_sm < 0) {
+  const InterpWedge& iw = a.iw[wi];
+  const size_t smem = k3_fixed_smem<T2, TAPS, P>() + sizeof(T2) * kK3Stages * (size_t)iw.tile_cap;
+  static int sms = 0;
+  static size_t configured = 0;
+  if (sms == 0) {
     int dev = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaError_t e = cudaFuncSetAttribute(k_interp_groups<T2, TAPS, P>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)SMEM);
-    if (e != cudaSuccess) return e;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, k_interp_groups<T2, TAPS, P>, BLOCK, SMEM);
-    if (blocks_per_sm < 1) blocks_per_sm = 1;
   }
-  const InterpWedge& iw = a.iw[wi];
-  int need = (iw.ngroups + BLOCK - 1) / BLOCK;
-  int blocks = std::max(1, std::min(need, blocks_per_sm * sms));
-  k_interp_groups<T2, TAPS, P><<<blocks, BLOCK, SMEM, s>>>(iw, reinterpret_cast<const T2*>(a.g), a.a0,
-                                                        reinterpret_cast<const T2*>(a.fhat), wi == 0 ? 1 : 0,
-                                                        (wi == 0 && a.add_dc) ? 1 : 0, a.es_beta, Lf);
+  if (smem > configured) {
+    cudaError_t e = cudaFuncSetAttribute(k_interp_groups<T2, TAPS, P>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)smem);
+    if (e != cudaSuccess) return e;
+    configured = smem;
+  }
+  int per_sm = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_interp_groups<T2, TAPS, P>, BLOCK, smem);
+  per_sm = std::max(per_sm, 1);
+  int blocks = std::max(1, std::min(iw.nchunks, per_sm * sms));
+  k_interp_groups<T2, TAPS, P><<<blocks, BLOCK, smem, s>>>(iw, reinterpret_cast<const T2*>(a.g), a.a0,
+                                                          reinterpret_cast<const T2*>(a.fhat), wi == 0 ? 1 : 0,
+                                                          (wi == 0 && a.add_dc) ? 1 : 0, a.es_beta, Lf);
   return cudaGetLastError();
 }
 
