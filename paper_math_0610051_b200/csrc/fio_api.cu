@@ -443,9 +443,9 @@ fio_status build_plan(fio_plan_s& P, const fio_phase* phase, const fio_amplitude
     // K3 point groups (plan time): fine coordinates -> host grouping -> device tables
     InterpWedge iw{};
     iw.q = q;
-    iw.n1f = g.n1f;
-    iw.n2f = g.n2f;
-    iw.n2p = g.n2f + 2 * kHalo;
+    iw.nrow = g.n2f;                 // K3 rows = j2
+    iw.ncol = g.n1f;                 // K3 columns = j1 (haloed)
+    iw.ncolp = g.n1f + 2 * kHalo;
     {
       DevBuf du;
       FIO_CUDA(du.ensure(sizeof(double2) * NN));
@@ -453,9 +453,10 @@ fio_status build_plan(fio_plan_s& P, const fio_phase* phase, const fio_amplitude
       std::vector<double> uh(2 * NN);
       FIO_CUDA(cudaMemcpyAsync(uh.data(), du.p, sizeof(double2) * NN, cudaMemcpyDeviceToHost, s));
       FIO_CUDA(cudaStreamSynchronize(s));
+      for (long long x = 0; x < NN; ++x) std::swap(uh[2 * x], uh[2 * x + 1]);  // (K3 row, column) = (u2, u1)
       std::vector<int> anchor, slot_x;
       std::vector<double> off;
-      group_points(uh.data(), NN, P.taps, kGroupP, g.n1f, g.n2f, anchor, slot_x, off);
+      group_points(uh.data(), NN, P.taps, kGroupP, g.n2f, g.n1f, anchor, slot_x, off);
       iw.ngroups = (int)(anchor.size() / 2);
       int* d_anchor = nullptr;
       int* d_slot = nullptr;
@@ -553,10 +554,10 @@ fio_status build_plan(fio_plan_s& P, const fio_phase* phase, const fio_amplitude
     w.g_off = g_off;
     P.iw[wi].g_off = g_off;
     p1_off += (long long)w.q * w.n1 * w.n2f;
-    g_off += (long long)w.q * w.n1f * (w.n2f + 2 * kHalo);
+    g_off += (long long)w.q * w.n2f * (w.n1f + 2 * kHalo);
     size_t sr = fft_seq_bytes(w.n2f, c64), sc = fft_seq_bytes(w.n1f, c64);
-    int rows = (int)std::max<size_t>(1, kSmemBudget / sr);
-    int cols = (int)std::max<size_t>(1, kSmemBudget / sc);
+    int rows = (int)std::max<size_t>(1, std::min<size_t>(32, kSmemBudget / sr));
+    int cols = (int)std::max<size_t>(1, std::min<size_t>(16, kSmemBudget / sc));
     cols = std::min(cols, w.n2f);
     rows = std::min(rows, w.n1);
     for (int t = 0; t < w.q; ++t) {

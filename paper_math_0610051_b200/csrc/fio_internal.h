@@ -44,17 +44,19 @@ struct WedgeDev {
   double u1, u2;   // xihat_l = (cos 2 pi l / W, sin 2 pi l / W)
   long long alpha_off;  // element offset of alpha'[t][x] block (q * N*N)
   long long beta_off;   // element offset of beta'[t][i1][i2] block (q * n1 * n2)
-  long long p1_off;     // element offset of row-pass buffer (q * n1 * n2f)
-  long long g_off;      // element offset of fine grids (q * n1f * (n2f + 2 kHalo), haloed rows)
+  long long p1_off;     // element offset of the row-pass buffer, [t][j2][i1] (q * n2f * n1)
+  long long g_off;      // element offset of the fine grids, [t][j2][kHalo + j1] (q * n2f * (n1f + 2 kHalo))
 };
 
 // K3 (interpolation + alpha epilogue) data of one owned wedge.  Points are
 // grouped at plan time: the P points of a group have their base fine cells
 // b = ceil(u - w/2) in the same 2 x 2 "supercell", so one (w+1) x (w+1) window
 // of the fine grid anchored at `anchor` covers all their taps.
+// The fine grid is stored [j2][kHalo + j1]: K3's "rows" are j2 (nrow = n2f, wrapped) and
+// its "columns" are j1 (ncol = n1f, haloed row stride ncolp = n1f + 2 kHalo).
 struct InterpWedge {
-  int q, n1f, n2f, ngroups;
-  int n2p;                  // fine row stride n2f + 2 kHalo; column c is stored at kHalo + c
+  int q, nrow, ncol, ngroups;
+  int ncolp;
   long long g_off;          // element offset of this wedge's fine grids
   const int* anchor;        // 2 ints per group (a1, a2), may be negative (wrapped in K3)
   const int* slot_x;        // P per group: flat output index, -1 = padding
@@ -97,7 +99,7 @@ int taps_for_eps(double eps);
 void lpt_assign(int W, const double* cost, int nranks, int* owner);
 
 // Group the output points of one wedge for K3 (see InterpWedge).  u: 2*NN doubles
-// (fine coordinates in [0, n1f) x [0, n2f)).  Outputs: anchor (2 per group),
+// (K3 row / column fine coordinates in [0, n1f) x [0, n2f)).  Outputs: anchor (2 per group),
 // slot_x (P per group, -1 padding), off (2 per slot: u - anchor).
 void group_points(const double* u, long long NN, int taps, int P, int n1f, int n2f, std::vector<int>& anchor,
                   std::vector<int>& slot_x, std::vector<double>& off);

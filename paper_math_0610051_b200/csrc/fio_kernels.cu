@@ -5,9 +5,9 @@
 //   K0  k_fft_rows / k_fft_cols   fhat = DFT(f)/N, eq. (dft)
 //   K1  k_rowpass                 fhat * chi_l * beta_lt relabelled onto the box
 //                                 (PAPER.md:1297-1298, 1327-1347), deconvolved,
-//                                 zero-padded, FFT along axis 2
-//   K2  k_colpass                 zero-padded FFT along axis 1 -> fine grid G_lt
-//                                 (the oversampled FFT of the NUFFT)
+//                                 zero-padded, FFT along axis 2, written transposed
+//   K2  k_colpass                 zero-padded FFT along axis 1 -> fine grid G_lt, stored
+//                                 [j2][j1] (the oversampled FFT of the NUFFT)
 //   K3  k_interp                  interpolation of G_lt at the warped points
 //                                 M^{-T} grad Phi(x, xihat_l) (PAPER.md:1299-1311,
 //                                 1357-1363) fused with the alpha epilogue and the
@@ -473,7 +473,8 @@ __device__ __forceinline__ int imod(int a, int n) {
 // ------------------------------------------------------------------ K1: window x beta + row FFT
 // Job (w, t, start, count): box rows i1 in [start, start + count) of wedge w, term t.
 // h(i1, i2) = beta'_lt(i1, i2) fhat(M^{-1}(k' + xi_c)), k' = (i1 - n1/2, i2 - n2/2),
-// placed at fine index k'_2 mod n2f, then G1 = FFT_{+}(h) along axis 2.
+// placed at fine index k'_2 mod n2f, then H = FFT_{+}(h) along axis 2.  The result is
+// written TRANSPOSED, p1[t][j2][i1] (row length n1), so that K2 reads contiguous columns.
 template <typename T2>
 __global__ void __launch_bounds__(256) k_rowpass(int N, const WedgeDev* __restrict__ wedges,
                                                  const FftJob* __restrict__ jobs, const FftLen* __restrict__ ffts,
@@ -503,13 +504,19 @@ __global__ void __launch_bounds__(256) k_rowpass(int N, const WedgeDev* __restri
   }
   __syncthreads();
   T2* res = smem_fft<T2>(a, b, fl, tw + fl.tw_off, cnt, 1, L, +1);
-  T2* dst = p1 + w.p1_off + ((long long)job.t * n1 + job.start) * L;
-  for (int idx = threadIdx.x; idx < cnt * L; idx += blockDim.x) dst[idx] = res[idx];
+  T2* dst = p1 + w.p1_off + (long long)job.t * L * n1 + job.start;
+  for (int idx = threadIdx.x; idx < cnt * L; idx += blockDim.x) {
+    const int j2 = idx / cnt, r = idx - j2 * cnt;
+    dst[(long long)j2 * n1 + r] = res[r * L + j2];
+  }
 }
 
 // ------------------------------------------------------------------ K2: column FFT -> fine grid
-// Job (w, t, c0, C): fine columns [c0, c0 + C): G(j1, c) = FFT_{+} along axis 1 of the
-// row-pass output placed at fine index (i1 - n1/2) mod n1f.
+// Job (w, t, c0, C): fine columns j2 in [c0, c0 + C).  Column j2 of the row-pass output
+// (contiguous in p1) is placed at fine index (i1 - n1/2) mod n1f and transformed
+// (FFT_{+}, length n1f).  The fine grid is stored TRANSPOSED with a periodic halo on
+// its contiguous axis: G_lt[j2][kHalo + j1] (row length n1f + 2 kHalo), the layout K3
+// reads (K3's rows are j2, its columns j1).
 template <typename T2>
 __global__ void __launch_bounds__(256) k_colpass(const WedgeDev* __restrict__ wedges, const FftJob* __restrict__ jobs,
                                                  const FftLen* __restrict__ ffts, const T2* __restrict__ tw,
@@ -518,30 +525,28 @@ __global__ void __launch_bounds__(256) k_colpass(const WedgeDev* __restrict__ we
   const FftJob job = jobs[blockIdx.x];
   const WedgeDev& w = wedges[job.w];
   const FftLen fl = ffts[w.fft1];
-  const int L = fl.L, n1 = w.n1, ncol = w.n2f, C = job.count, c0 = job.start;
+  const int L = fl.L, n1 = w.n1, C = job.count, c0 = job.start;
   T2* a = reinterpret_cast<T2*>(smem_raw);
   T2* b = a + C * L;
   const T2 zero = mk<T2>(0, 0);
   for (int idx = threadIdx.x; idx < C * L; idx += blockDim.x) a[idx] = zero;
   __syncthreads();
-  const T2* src = p1 + w.p1_off + (long long)job.t * n1 * ncol;
-  for (int idx = threadIdx.x; idx < n1 * C; idx += blockDim.x) {
-    int i1 = idx / C, c = idx - i1 * C;
-    a[imod(i1 - n1 / 2, L) * C + c] = src[(long long)i1 * ncol + c0 + c];
+  const T2* src = p1 + w.p1_off + ((long long)job.t * w.n2f + c0) * n1;
+  for (int idx = threadIdx.x; idx < C * n1; idx += blockDim.x) {
+    const int c = idx / n1, i1 = idx - c * n1;
+    a[c * L + imod(i1 - n1 / 2, L)] = src[idx];
   }
   __syncthreads();
-  T2* res = smem_fft<T2>(a, b, fl, tw + fl.tw_off, C, C, 1, +1);
-  // haloed row layout: fine column c at kHalo + c, plus periodic copies in the halos
-  const int n2p = ncol + 2 * kHalo;
-  T2* dst = g + w.g_off + (long long)job.t * L * n2p + kHalo;
+  T2* res = smem_fft<T2>(a, b, fl, tw + fl.tw_off, C, 1, L, +1);
+  const int rowp = L + 2 * kHalo;
+  T2* dst = g + w.g_off + ((long long)job.t * w.n2f + c0) * rowp + kHalo;
   for (int idx = threadIdx.x; idx < C * L; idx += blockDim.x) {
-    int j1 = idx / C, c = idx - j1 * C;
-    const int col = c0 + c;
-    T2* rowp = dst + (long long)j1 * n2p;
+    const int c = idx / L, j1 = idx - c * L;
+    T2* rp = dst + (long long)c * rowp;
     const T2 v = res[idx];
-    rowp[col] = v;
-    if (col < kHalo) rowp[ncol + col] = v;
-    if (col >= ncol - kHalo) rowp[col - ncol] = v;
+    rp[j1] = v;
+    if (j1 < kHalo) rp[L + j1] = v;
+    if (j1 >= L - kHalo) rp[j1 - L] = v;
   }
 }
 
@@ -634,7 +639,7 @@ __global__ void __launch_bounds__(K3Cfg<T2>::BLOCK, K3Cfg<T2>::MINB)
   const int cap = iw.tile_cap;
   const Rt inv_half_w = (Rt)(2.0 / TAPS);
   const Rt beta = (Rt)es_beta;
-  const int n1f = iw.n1f, n2p = iw.n2p, q = iw.q;
+  const int n1f = iw.nrow, n2p = iw.ncolp, q = iw.q;  // K3 rows / haloed row length of G_lt
   const long long gstride = (long long)n1f * n2p;
   const long long nslots = (long long)iw.ngroups * P;
   const T2* __restrict__ G = gbase + iw.g_off + kHalo;
@@ -651,6 +656,27 @@ __global__ void __launch_bounds__(K3Cfg<T2>::BLOCK, K3Cfg<T2>::MINB)
     const int tchunks = bx.z * (bx.w / EPC);                    // 16-byte chunks of one tile
     const int cpr = bx.w / EPC;
     const T2* __restrict__ al = alpha + (long long)g * P;
+    // this thread's share of a tile copy, fixed for the chunk: source offsets within G_lt
+    // (row wrapped mod n1f) and destination offsets within the tile
+    constexpr int MAXC = 8;  // >= tile_cap / EPC / BLOCK for both dtypes
+    static_assert(kK3TileCapC64 / 2 <= 8 * kK3BlockC64 && kK3TileCapC128 <= 8 * kK3BlockC128, "K3 copy slots");
+    long long csrc[MAXC];
+    int cdst[MAXC];
+    int ncp = 0;
+#pragma unroll
+    for (int u = 0; u < MAXC; ++u) {
+      const int idx = threadIdx.x + u * BLOCK;
+      csrc[u] = 0;
+      cdst[u] = 0;
+      if (idx < tchunks) {
+        const int rr = idx / cpr, cc = idx - rr * cpr;
+        int r = bx.x + rr;
+        r = r < 0 ? r + n1f : (r >= n1f ? r - n1f : r);
+        csrc[u] = (long long)r * n2p + bx.y + cc * EPC;
+        cdst[u] = rr * bx.w + cc * EPC;
+        ncp = u + 1;
+      }
+    }
     // stage term t into ring slot t % S: this thread's alpha'(t) and its share of the tile
     auto issue = [&](int t) {
       if (t < q) {
@@ -663,12 +689,9 @@ __global__ void __launch_bounds__(K3Cfg<T2>::BLOCK, K3Cfg<T2>::MINB)
         }
         const T2* __restrict__ gt = G + t * gstride;
         T2* tile = tring + st * cap;
-        for (int idx = threadIdx.x; idx < tchunks; idx += BLOCK) {
-          const int rr = idx / cpr, cc = idx - rr * cpr;
-          int r = bx.x + rr;
-          r = r < 0 ? r + n1f : (r >= n1f ? r - n1f : r);
-          cp_async16(tile + rr * bx.w + cc * EPC, gt + (long long)r * n2p + bx.y + cc * EPC);
-        }
+#pragma unroll
+        for (int u = 0; u < MAXC; ++u)
+          if (u < ncp) cp_async16(tile + cdst[u], gt + csrc[u]);
       }
       cp_async_commit();
     };
