@@ -39,7 +39,7 @@ def parse():
     p.add_argument("--variant", default="cfg3_c64", help="second config timed in the same run ('' = none)")
     p.add_argument("--impl", default="fio", choices=["fio", "reference"])
     p.add_argument("--no-cpu-baseline", action="store_true")
-    p.add_argument("--cpu-points", type=int, default=2048, help="oracle sample size (output points)")
+    p.add_argument("--cpu-points", type=int, default=8192, help="oracle sample size (output points)")
     return p.parse_args()
 
 

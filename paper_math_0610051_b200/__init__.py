@@ -21,7 +21,8 @@ from typing import Optional
 
 import numpy as np
 
-__all__ = ["FioError", "Plan", "geometry", "assign_wedges", "library_path", "load_library", "SYMBOLS"]
+__all__ = ["FioError", "Plan", "geometry", "assign_wedges", "reduce_scatter_rows", "library_path", "load_library",
+           "SYMBOLS", "STAGES"]
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 _LIB_PATH = os.path.join(_HERE, "libfio_b200.so")
@@ -144,6 +145,32 @@ def assign_wedges(cost, nranks: int) -> np.ndarray:
     return owner
 
 
+def reduce_scatter_rows(part, nranks: int, group=None, out=None):
+    """Sum the N x N complex partials of all ranks and return this rank's row slab
+    [r N/R, (r+1) N/R).  NCCL: one reduce_scatter_tensor on the real view (NCCL has no complex
+    type).  Backends without reduce_scatter (gloo, used by the CPU tests): all_reduce + slice."""
+    import torch
+    import torch.distributed as dist
+    N = part.shape[0]
+    if N % nranks:
+        raise FioError(-1, "nranks must divide N")
+    rows = N // nranks
+    real = torch.view_as_real(part.contiguous()).reshape(-1)
+    if dist.get_backend(group) == "nccl":
+        slab = torch.empty(rows * N * 2, dtype=real.dtype, device=real.device) if out is None else \
+            torch.view_as_real(out).reshape(-1)
+        dist.reduce_scatter_tensor(slab, real, op=dist.ReduceOp.SUM, group=group)
+        return torch.view_as_complex(slab.reshape(rows, N, 2))
+    full = real.clone()
+    dist.all_reduce(full, op=dist.ReduceOp.SUM, group=group)
+    r = dist.get_rank(group)
+    slab = torch.view_as_complex(full.reshape(N, N, 2))[r * rows:(r + 1) * rows].clone()
+    if out is not None:
+        out.copy_(slab)
+        return out
+    return slab
+
+
 class Plan:
     """fio_plan: preprocessing of Phi(x,xi) = x.xi + b(x).xi + sqrt(c1(x)^2 xi1^2 + c2(x)^2 xi2^2)
     and a(x,xi) = sum_k px[k](x) pxi[k](xi) at accuracy eps (include/fio.h)."""
@@ -211,20 +238,13 @@ class Plan:
         return out_host
 
     def apply_sharded(self, f, group=None, out=None):
-        """Wedge-sharded apply: this rank's partial over its wedges, then a reduce-scatter (sum) over
-        the process group.  Returns this rank's (N/nranks) x N row slab of Lf."""
-        import torch
-        import torch.distributed as dist
+        """Wedge-sharded apply (BASELINE north_star (3)): this rank's partial sum over its own
+        wedges, then a sum-reduce-scatter over the process group.  Returns this rank's
+        (N/nranks) x N row slab of Lf."""
         part = self.apply(f)
-        R = self.nranks
-        if R == 1:
+        if self.nranks == 1:
             return part
-        rows = self.N // R
-        real = torch.view_as_real(part).reshape(R, rows * self.N * 2)
-        slab = torch.empty(rows * self.N * 2, dtype=real.dtype, device=real.device) if out is None else \
-            torch.view_as_real(out).reshape(-1)
-        dist.reduce_scatter_tensor(slab, real.reshape(-1), op=dist.ReduceOp.SUM, group=group)
-        return torch.view_as_complex(slab.reshape(rows, self.N, 2))
+        return reduce_scatter_rows(part, self.nranks, group=group, out=out)
 
     def profile_begin(self, max_applies: int):
         """Record per-stage CUDA events for the next max_applies applies (on their stream)."""
