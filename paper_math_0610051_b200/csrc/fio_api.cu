@@ -94,6 +94,8 @@ struct fio_plan_s {
   long long max_tile_cap = 0;
   long long chunk_threads = 0;  // K3 thread slots (chunks x BLOCK): groups / this = thread fill
   double plan_seconds = 0, max_err = 0;
+  EsPoly poly{};
+  double poly_err = 0;
   int certified = 1;
   int launches = 0;
   std::vector<cudaEvent_t> prof_ev;  // (kStages + 1) per recorded apply
@@ -613,6 +615,7 @@ ApplyArgs make_args(const fio_plan_s& P) {
   a.add_dc = P.opts.rank == 0 ? 1 : 0;
   a.taps = P.taps;
   a.es_beta = P.es_beta;
+  a.poly = &P.poly;
   a.fhat = P.fhat;
   a.tmp = P.tmp;
   a.p1 = P.p1;
@@ -701,6 +704,8 @@ fio_status fio_plan(fio_handle* out, int N, const fio_phase* phase, const fio_am
   P->W = o.n_wedges > 0 ? o.n_wedges : default_wedges(N);
   P->taps = o.nufft_w > 0 ? o.nufft_w : taps_for_eps(eps);
   P->es_beta = o.nufft_beta > 0 ? o.nufft_beta : 2.30 * P->taps;
+  // polynomial kernel for the c128 K3 weights: error ~1.5 e^{-beta}, the kernel's own edge value
+  P->poly_err = es_poly_fit(P->taps, P->es_beta, 2.0 * std::exp(-P->es_beta), P->poly);
   fio_status st = build_plan(*P, phase, amp);
   if (st < 0) {
     delete P;

@@ -183,6 +183,61 @@ double es_fourier(double s, int w, double beta) {
   return acc;
 }
 
+// Chebyshev interpolation of phi(s - j) on s in (w/2 - 1, w/2] at deg+1 nodes, converted to
+// monomial coefficients in x = 2 (s - w/2) + 1; the degree grows until the error measured
+// on a fine grid is below tol.
+double es_poly_fit(int w, double beta, double tol, EsPoly& out) {
+  const double pi = 3.14159265358979323846;
+  double err = 1.0;
+  for (int deg = 6; deg <= kPolyMaxDeg; ++deg) {
+    std::memset(&out, 0, sizeof(out));
+    out.deg = deg;
+    const int n = deg + 1;
+    err = 0.0;
+    for (int j = 0; j < w; ++j) {
+      std::vector<double> f(n), a(n, 0.0);
+      for (int k = 0; k < n; ++k) {
+        double x = std::cos(pi * (k + 0.5) / n);
+        double sv = 0.5 * w + 0.5 * (x - 1.0);
+        f[k] = es_kernel(sv - j, w, beta);
+      }
+      for (int m = 0; m < n; ++m) {
+        double acc = 0;
+        for (int k = 0; k < n; ++k) acc += f[k] * std::cos(pi * m * (k + 0.5) / n);
+        a[m] = acc * (m == 0 ? 1.0 : 2.0) / n;
+      }
+      // sum_m a_m T_m(x) -> monomials
+      std::vector<double> tprev(n, 0.0), tcur(n, 0.0), coef(n, 0.0);
+      tprev[0] = 1.0;                 // T_0
+      if (n > 1) tcur[1] = 1.0;       // T_1
+      for (int i = 0; i < n; ++i) coef[i] += a[0] * tprev[i];
+      if (n > 1)
+        for (int i = 0; i < n; ++i) coef[i] += a[1] * tcur[i];
+      for (int m = 2; m < n; ++m) {
+        std::vector<double> tnext(n, 0.0);
+        for (int i = 0; i < n; ++i) {
+          if (i > 0) tnext[i] += 2.0 * tcur[i - 1];
+          tnext[i] -= tprev[i];
+        }
+        for (int i = 0; i < n; ++i) coef[i] += a[m] * tnext[i];
+        tprev.swap(tcur);
+        tcur.swap(tnext);
+      }
+      for (int m = 0; m < n; ++m) out.c[j][m] = coef[m];
+      for (int k = 0; k <= 400; ++k) {
+        double x = -1.0 + 2.0 * k / 400.0;
+        if (k == 0) x += 1e-12;
+        double sv = 0.5 * w + 0.5 * (x - 1.0);
+        double p = 0;
+        for (int m = n - 1; m >= 0; --m) p = p * x + coef[m];
+        err = std::max(err, std::fabs(p - es_kernel(sv - j, w, beta)));
+      }
+    }
+    if (err <= tol) return err;
+  }
+  return err;
+}
+
 // Reading R10: taps per dimension so that the NUFFT error (measured: ~1e-(w-1)
 // relative l2 at sigma = 2, beta = 2.3 w) stays below ~2 eps.
 int taps_for_eps(double eps) {

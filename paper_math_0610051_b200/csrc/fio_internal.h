@@ -86,6 +86,15 @@ struct WedgeGeom {
   double u1, u2;
 };
 
+// Piecewise-polynomial form of the NUFFT kernel for K3 (c128): tap j of a point whose base
+// cell is b and fractional offset s = u - b in (w/2 - 1, w/2] has weight
+// phi(s - j) = sum_m c[j][m] x^m, x = 2 (s - w/2) + 1 in (-1, 1].
+constexpr int kPolyMaxDeg = 20;
+struct EsPoly {
+  int deg;
+  double c[kMaxTaps][kPolyMaxDeg + 1];
+};
+
 // Host helpers (fio_host.cpp).
 int default_wedges(int N);
 bool is_smooth5(int n);
@@ -96,6 +105,8 @@ std::vector<int8_t> radix_plan(int L);
 double es_kernel(double z, int w, double beta);
 double es_fourier(double s, int w, double beta);  // psi(s) = int phi(v) cos(2 pi s v) dv
 int taps_for_eps(double eps);
+// Fit EsPoly for (w, beta) to absolute accuracy tol (degree chosen <= kPolyMaxDeg); returns max error.
+double es_poly_fit(int w, double beta, double tol, EsPoly& out);
 void lpt_assign(int W, const double* cost, int nranks, int* owner);
 
 // Group the output points of one wedge for K3 (see InterpWedge).  u: 2*NN doubles

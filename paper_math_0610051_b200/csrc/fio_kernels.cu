@@ -561,7 +561,8 @@ template <>
 __device__ __forceinline__ float es_weight<float>(float z, float inv_half_w, float beta) {
   float t = z * inv_half_w;
   float s = 1.f - t * t;
-  return s > 0.f ? __expf(beta * (sqrtf(s) - 1.f)) : 0.f;
+  // s * rsqrt(s) (MUFU.RSQ) and ex2.approx: ~1e-7 relative, far below the c64 NUFFT error
+  return s > 0.f ? __expf(beta * (s * rsqrtf(s) - 1.f)) : 0.f;
 }
 
 // c + a * (b.x, b.y) as one packed FFMA2 (sm_100 fma.rn.f32x2)
@@ -579,6 +580,69 @@ __device__ __forceinline__ double2 cfma_real(double a, double2 b, double2 c) {
   return make_double2(fma(a, b.x, c.x), fma(a, b.y, c.y));
 }
 
+// Weights of the window positions i = 0..NW-1 for a point at offset o = u - anchor
+// (o in (w/2 - 1, w/2 + 1]).  float: exact ES kernel with fast intrinsics.  double: the
+// plan's piecewise polynomials (EsPoly) -- the point's base b = anchor + d, d = ceil(o - w/2)
+// in {0, 1}, s = o - d, taps j = i - d.
+template <typename Rt, int TAPS, int NW>
+__device__ __forceinline__ void window_weights(Rt o, Rt inv_half_w, Rt beta, const EsPoly& poly, Rt (&w)[NW]) {
+  if constexpr (sizeof(Rt) == 4) {
+#pragma unroll
+    for (int i = 0; i < NW; ++i) w[i] = es_weight<Rt>(o - (Rt)i, inv_half_w, beta);
+  } else {
+    const int d = (o > (Rt)(0.5 * TAPS)) ? 1 : 0;
+    const Rt x = (Rt)2 * (o - (Rt)d - (Rt)(0.5 * TAPS)) + (Rt)1;
+    Rt qv[TAPS];
+#pragma unroll
+    for (int j = 0; j < TAPS; ++j) qv[j] = (Rt)poly.c[j][poly.deg];
+    for (int m = poly.deg - 1; m >= 0; --m) {
+#pragma unroll
+      for (int j = 0; j < TAPS; ++j) qv[j] = fma(qv[j], x, (Rt)poly.c[j][m]);
+    }
+#pragma unroll
+    for (int i = 0; i < NW; ++i) {
+      Rt a = (i < TAPS) ? qv[i < TAPS ? i : 0] : (Rt)0;
+      Rt b = (i >= 1 && i - 1 < TAPS) ? qv[(i >= 1 && i - 1 < TAPS) ? i - 1 : 0] : (Rt)0;
+      w[i] = d ? b : a;
+    }
+  }
+}
+
+// Window row of WIN elements from shared memory (float2 rows start 16-byte aligned:
+// anchors and tile origins are even) and the P row weights of one thread.
+template <typename T2, int WIN>
+__device__ __forceinline__ void load_row(const T2* p, T2 (&v)[WIN]) {
+  if constexpr (sizeof(T2) == 8) {
+    const float4* q = reinterpret_cast<const float4*>(p);
+#pragma unroll
+    for (int j = 0; j < WIN / 2; ++j) {
+      float4 a = q[j];
+      v[2 * j] = mk<T2>(a.x, a.y);
+      v[2 * j + 1] = mk<T2>(a.z, a.w);
+    }
+    if constexpr (WIN % 2) v[WIN - 1] = p[WIN - 1];
+  } else {
+#pragma unroll
+    for (int j = 0; j < WIN; ++j) v[j] = p[j];
+  }
+}
+template <typename Rt, int P>
+__device__ __forceinline__ void load_p1(const Rt* p, Rt (&w)[P]) {
+  if constexpr (sizeof(Rt) == 4 && P == 4) {
+    float4 a = *reinterpret_cast<const float4*>(p);
+    w[0] = a.x; w[1] = a.y; w[2] = a.z; w[3] = a.w;
+  } else if constexpr (sizeof(Rt) == 8 && P % 2 == 0) {
+#pragma unroll
+    for (int k = 0; k < P; k += 2) {
+      double2 a = *reinterpret_cast<const double2*>(p + k);
+      w[k] = a.x; w[k + 1] = a.y;
+    }
+  } else {
+#pragma unroll
+    for (int k = 0; k < P; ++k) w[k] = p[k];
+  }
+}
+
 template <typename T2> struct OffT;
 template <> struct OffT<float2> { using type = float2; };
 template <> struct OffT<double2> { using type = double2; };
@@ -592,8 +656,14 @@ template <> struct OffT<double2> { using type = double2; };
 // exactly one group per wedge, so one launch per wedge is race-free and the
 // summation order over wedges is fixed (deterministic).
 template <typename T2> struct K3Cfg;
-template <> struct K3Cfg<float2> { static constexpr int BLOCK = kK3BlockC64, MINB = 2; };
-template <> struct K3Cfg<double2> { static constexpr int BLOCK = kK3BlockC128, MINB = 2; };
+template <> struct K3Cfg<float2> {
+  static constexpr int BLOCK = kK3BlockC64, MINB = 2;
+  static constexpr int MAXC = kK3TileCapC64 / 2 / kK3BlockC64;  // 16-B tile-copy slots per thread
+};
+template <> struct K3Cfg<double2> {
+  static constexpr int BLOCK = kK3BlockC128, MINB = 2;
+  static constexpr int MAXC = kK3TileCapC128 / 1 / kK3BlockC128;
+};
 
 __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
   unsigned s = (unsigned)__cvta_generic_to_shared(smem);
@@ -623,7 +693,8 @@ __host__ __device__ constexpr size_t k3_fixed_smem() {
 template <typename T2, int TAPS, int P>
 __global__ void __launch_bounds__(K3Cfg<T2>::BLOCK, K3Cfg<T2>::MINB)
     k_interp_groups(InterpWedge iw, const T2* __restrict__ gbase, const double2* __restrict__ a0,
-                    const T2* __restrict__ fhat, int first, int add_dc, double es_beta, T2* __restrict__ Lf) {
+                    const T2* __restrict__ fhat, int first, int add_dc, double es_beta, EsPoly poly,
+                    T2* __restrict__ Lf) {
   using Rt = typename Real<T2>::type;
   using O2 = typename OffT<T2>::type;
   constexpr int WIN = TAPS + 1;         // window columns
@@ -658,9 +729,8 @@ __global__ void __launch_bounds__(K3Cfg<T2>::BLOCK, K3Cfg<T2>::MINB)
     const T2* __restrict__ al = alpha + (long long)g * P;
     // this thread's share of a tile copy, fixed for the chunk: source offsets within G_lt
     // (row wrapped mod n1f) and destination offsets within the tile
-    constexpr int MAXC = 8;  // >= tile_cap / EPC / BLOCK for both dtypes
-    static_assert(kK3TileCapC64 / 2 <= 8 * kK3BlockC64 && kK3TileCapC128 <= 8 * kK3BlockC128, "K3 copy slots");
-    long long csrc[MAXC];
+    constexpr int MAXC = K3Cfg<T2>::MAXC;  // = tile_cap / EPC / BLOCK
+    int csrc[MAXC];
     int cdst[MAXC];
     int ncp = 0;
 #pragma unroll
@@ -672,7 +742,7 @@ __global__ void __launch_bounds__(K3Cfg<T2>::BLOCK, K3Cfg<T2>::MINB)
         const int rr = idx / cpr, cc = idx - rr * cpr;
         int r = bx.x + rr;
         r = r < 0 ? r + n1f : (r >= n1f ? r - n1f : r);
-        csrc[u] = (long long)r * n2p + bx.y + cc * EPC;
+        csrc[u] = r * n2p + bx.y + cc * EPC;
         cdst[u] = rr * bx.w + cc * EPC;
         ncp = u + 1;
       }
@@ -709,18 +779,18 @@ __global__ void __launch_bounds__(K3Cfg<T2>::BLOCK, K3Cfg<T2>::MINB)
 #pragma unroll
     for (int k = 0; k < P; ++k) {
       O2 o;
-      o.x = (Rt)0;
-      o.y = (Rt)0;
+      o.x = (Rt)(0.5 * TAPS);
+      o.y = (Rt)(0.5 * TAPS);
       xs[k] = -1;
       if (valid) {
         xs[k] = iw.slot_x[g * P + k];
         o = offs[g * P + k];
       }
+      Rt w1[WINR];
+      window_weights<Rt, TAPS, WINR>(o.x, inv_half_w, beta, poly, w1);
+      window_weights<Rt, TAPS, WIN>(o.y, inv_half_w, beta, poly, p2[k]);
 #pragma unroll
-      for (int i = 0; i < WINR; ++i)
-        p1s[(k * WINR + i) * BLOCK + threadIdx.x] = es_weight<Rt>((Rt)o.x - (Rt)i, inv_half_w, beta);
-#pragma unroll
-      for (int i = 0; i < WIN; ++i) p2[k][i] = es_weight<Rt>((Rt)o.y - (Rt)i, inv_half_w, beta);
+      for (int i = 0; i < WINR; ++i) p1s[(i * BLOCK + threadIdx.x) * P + k] = w1[i];
       // start the read of the running sum early (latency hidden by the term loop)
       base[k] = mk<T2>(0, 0);
       if (xs[k] >= 0 && !first) base[k] = Lf[xs[k]];
@@ -737,18 +807,19 @@ __global__ void __launch_bounds__(K3Cfg<T2>::BLOCK, K3Cfg<T2>::MINB)
       T2 F[P];
 #pragma unroll
       for (int k = 0; k < P; ++k) F[k] = mk<T2>(0, 0);
-#pragma unroll 2
+#pragma unroll
       for (int i = 0; i < WINR; ++i) {
         const T2* rowp = win + i * bx.w;
         T2 v[WIN];
-#pragma unroll
-        for (int j = 0; j < WIN; ++j) v[j] = rowp[j];
+        load_row<T2, WIN>(rowp, v);
+        Rt w1[P];
+        load_p1<Rt, P>(p1s + (i * BLOCK + threadIdx.x) * P, w1);
 #pragma unroll
         for (int k = 0; k < P; ++k) {
           T2 rr = mk<T2>(0, 0);
 #pragma unroll
           for (int j = 0; j < WIN; ++j) rr = cfma_real(p2[k][j], v[j], rr);
-          F[k] = cfma_real(p1s[(k * WINR + i) * BLOCK + threadIdx.x], rr, F[k]);
+          F[k] = cfma_real(w1[k], rr, F[k]);
         }
       }
       const T2* ring = myring + (t % S) * BLOCK * P;
@@ -815,7 +886,7 @@ static cudaError_t launch_groups_tp(const ApplyArgs& a, int wi, T2* Lf, cudaStre
   int blocks = std::max(1, std::min(iw.nchunks, per_sm * sms));
   k_interp_groups<T2, TAPS, P><<<blocks, BLOCK, smem, s>>>(iw, reinterpret_cast<const T2*>(a.g), a.a0,
                                                           reinterpret_cast<const T2*>(a.fhat), wi == 0 ? 1 : 0,
-                                                          (wi == 0 && a.add_dc) ? 1 : 0, a.es_beta, Lf);
+                                                          (wi == 0 && a.add_dc) ? 1 : 0, a.es_beta, *a.poly, Lf);
   return cudaGetLastError();
 }
 

@@ -65,6 +65,7 @@ struct ApplyArgs {
   int add_dc;
   int taps;                 // w (K3 template), groups of kGroupP points
   double es_beta;
+  const EsPoly* poly;       // host pointer: piecewise-polynomial kernel (c128 K3 weights)
   void* fhat;               // N*N workspace
   void* tmp;                // N*N workspace
   void* p1;                 // row-pass buffer
