@@ -5,6 +5,7 @@
 #include <algorithm>
 #include <chrono>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <string>
@@ -21,7 +22,7 @@ using namespace fio;
 
 namespace {
 
-constexpr size_t kSmemBudget = 96 * 1024;   // per-CTA FFT pass target (2 CTAs / SM)
+constexpr size_t kSmemBudgetDefault = 48 * 1024;  // per-CTA FFT pass target (FIO_FFT_SMEM_KB overrides)
 constexpr size_t kSmemMax = 200 * 1024;     // opt-in maximum for one long sequence
 constexpr int kCertSamples = 200;           // s of PAPER.md:1464-1477
 
@@ -547,6 +548,10 @@ fio_status build_plan(fio_plan_s& P, const fio_phase* phase, const fio_amplitude
   }
 
   // workspace offsets and FFT job lists
+  size_t kSmemBudget = kSmemBudgetDefault;
+  if (const char* e = std::getenv("FIO_FFT_SMEM_KB")) kSmemBudget = (size_t)std::max(8, std::atoi(e)) * 1024;
+  int max_rows = 32, max_cols = 16;
+  if (const char* e = std::getenv("FIO_FFT_MAXSEQ")) max_rows = max_cols = std::max(1, std::atoi(e));
   long long p1_off = 0, g_off = 0;
   std::vector<FftJob> jr, jc;
   size_t smem_row = 0, smem_col = 0;
@@ -558,8 +563,8 @@ fio_status build_plan(fio_plan_s& P, const fio_phase* phase, const fio_amplitude
     p1_off += (long long)w.q * w.n1 * w.n2f;
     g_off += (long long)w.q * w.n2f * (w.n1f + 2 * kHalo);
     size_t sr = fft_seq_bytes(w.n2f, c64), sc = fft_seq_bytes(w.n1f, c64);
-    int rows = (int)std::max<size_t>(1, std::min<size_t>(32, kSmemBudget / sr));
-    int cols = (int)std::max<size_t>(1, std::min<size_t>(16, kSmemBudget / sc));
+    int rows = (int)std::max<size_t>(1, std::min<size_t>(max_rows, kSmemBudget / sr));
+    int cols = (int)std::max<size_t>(1, std::min<size_t>(max_cols, kSmemBudget / sc));
     cols = std::min(cols, w.n2f);
     rows = std::min(rows, w.n1);
     for (int t = 0; t < w.q; ++t) {
@@ -585,6 +590,7 @@ fio_status build_plan(fio_plan_s& P, const fio_phase* phase, const fio_amplitude
   P.fine_elems = (size_t)g_off;
   P.rows_per_cta_N = (int)std::max<size_t>(1, kSmemBudget / fft_seq_bytes(N, c64));
   P.cols_per_cta_N = std::min(N, (int)std::max<size_t>(1, kSmemBudget / fft_seq_bytes(N, c64)));
+  (void)kSmemBudgetDefault;
   FIO_CUDA(configure_kernels(kSmemMax));
   if (!jr.empty()) FIO_CUDA(P.upload(&P.jobs_row, jr.data(), jr.size()));
   if (!jc.empty()) FIO_CUDA(P.upload(&P.jobs_col, jc.data(), jc.size()));
