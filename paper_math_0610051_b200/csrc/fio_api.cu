@@ -367,7 +367,13 @@ int fft_index(std::map<int, int>& lens, std::vector<FftLen>& tab, int L) {
   f.L = L;
   std::vector<int8_t> r = radix_plan(L);
   f.nst = (int)r.size();
-  for (int i = 0; i < f.nst; ++i) f.radix[i] = r[i];
+  int ns = 1;
+  for (int i = 0; i < f.nst; ++i) {
+    f.radix[i] = r[i];
+    f.div_nb[i] = make_fastdiv((uint32_t)(L / r[i]));
+    f.div_ns[i] = make_fastdiv((uint32_t)ns);
+    ns *= r[i];
+  }
   int idx = (int)tab.size();
   tab.push_back(f);
   lens[L] = idx;
@@ -551,7 +557,7 @@ fio_status build_plan(fio_plan_s& P, const fio_phase* phase, const fio_amplitude
   size_t kSmemBudget = kSmemBudgetDefault;
   if (const char* e = std::getenv("FIO_FFT_SMEM_KB")) kSmemBudget = (size_t)std::max(8, std::atoi(e)) * 1024;
   int max_rows = 32, max_cols = 16;
-  if (const char* e = std::getenv("FIO_FFT_MAXSEQ")) max_rows = max_cols = std::max(1, std::atoi(e));
+  if (const char* e = std::getenv("FIO_FFT_MAXSEQ")) max_rows = max_cols = std::min(32, std::max(1, std::atoi(e)));
   long long p1_off = 0, g_off = 0;
   std::vector<FftJob> jr, jc;
   size_t smem_row = 0, smem_col = 0;

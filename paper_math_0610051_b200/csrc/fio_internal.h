@@ -20,14 +20,28 @@ constexpr int kK3TileCapC64 = 2048;   // max cells of a K3 chunk footprint, comp
 constexpr int kK3TileCapC128 = 1024;  // complex128
 constexpr int kHalo = 8;    // periodic column halo on each side of a fine-grid row (K2 writes, K3 reads)
 
-// One FFT length L (5-smooth), its Stockham radix sequence and the offset of its
-// twiddle table e^{+2 pi i m / L}, m < L, inside the plan's twiddle buffer.
+// Division by a runtime constant d via multiply-high (Granlund-Montgomery), exact for
+// numerators n < 2^31: q = (umulhi(m, n) + n) >> l.
+struct FastDiv {
+  uint32_t m, l, d;
+};
+inline FastDiv make_fastdiv(uint32_t d) {
+  uint32_t l = 0;
+  while ((1ull << l) < d) ++l;
+  uint64_t m = ((((1ull << l) - d) << 32) / d) + 1;
+  return FastDiv{(uint32_t)m, l, d};
+}
+
+// One FFT length L (5-smooth), its Stockham radix sequence, per-stage divisors (butterflies
+// per sequence nb = L/R and span Ns) and the offset of its twiddle table e^{+2 pi i m / L}.
 struct FftLen {
   int L;
   int nst;
   int tw_off;
   int pad;
   int8_t radix[kMaxRadixStages];
+  FastDiv div_nb[kMaxRadixStages];
+  FastDiv div_ns[kMaxRadixStages];
 };
 
 // Per owned wedge l:

@@ -363,16 +363,28 @@ __device__ __forceinline__ void dft_small(T2 (&v)[R], int sign) {
   }
 }
 
+__device__ __forceinline__ int fdiv(int n, const FastDiv& f) {
+  return (int)((__umulhi(f.m, (unsigned)n) + (unsigned)n) >> f.l);
+}
+__device__ __forceinline__ FastDiv make_fastdiv_dev(unsigned d) {
+  unsigned l = 0;
+  while ((1ull << l) < d) ++l;
+  unsigned long long m = ((((1ull << l) - d) << 32) / d) + 1;
+  return FastDiv{(unsigned)m, l, d};
+}
+
 template <typename T2, int R>
 __device__ __forceinline__ void stockham_stage(const T2* __restrict__ a, T2* __restrict__ b, int L, int Ns,
+                                               const FastDiv& dnb, const FastDiv& dns,
                                                const T2* __restrict__ tw, int nseq, int si, int sb, int sign) {
   const int nb = L / R;
   const int span = L / (Ns * R);
   const int total = nseq * nb;
   for (int idx = threadIdx.x; idx < total; idx += blockDim.x) {
-    int sq = idx / nb;
+    int sq = fdiv(idx, dnb);
     int j = idx - sq * nb;
-    int k = j % Ns;
+    int jq = fdiv(j, dns);
+    int k = j - jq * Ns;
     const T2* in = a + sq * sb;
     T2* out = b + sq * sb;
     T2 v[R];
@@ -385,7 +397,7 @@ __device__ __forceinline__ void stockham_stage(const T2* __restrict__ a, T2* __r
       v[r] = cmul(v[r], w);
     }
     dft_small<T2, R>(v, sign);
-    int base = (j / Ns) * Ns * R + k;
+    int base = jq * Ns * R + k;
 #pragma unroll
     for (int r = 0; r < R; ++r) out[(base + r * Ns) * si] = v[r];
   }
@@ -397,11 +409,13 @@ __device__ T2* smem_fft(T2* a, T2* b, const FftLen& fl, const T2* tw, int nseq, 
   int Ns = 1;
   for (int st = 0; st < fl.nst; ++st) {
     const int R = fl.radix[st];
+    const FastDiv& dnb = fl.div_nb[st];
+    const FastDiv& dns = fl.div_ns[st];
     switch (R) {
-      case 4: stockham_stage<T2, 4>(a, b, fl.L, Ns, tw, nseq, si, sb, sign); break;
-      case 2: stockham_stage<T2, 2>(a, b, fl.L, Ns, tw, nseq, si, sb, sign); break;
-      case 3: stockham_stage<T2, 3>(a, b, fl.L, Ns, tw, nseq, si, sb, sign); break;
-      default: stockham_stage<T2, 5>(a, b, fl.L, Ns, tw, nseq, si, sb, sign); break;
+      case 4: stockham_stage<T2, 4>(a, b, fl.L, Ns, dnb, dns, tw, nseq, si, sb, sign); break;
+      case 2: stockham_stage<T2, 2>(a, b, fl.L, Ns, dnb, dns, tw, nseq, si, sb, sign); break;
+      case 3: stockham_stage<T2, 3>(a, b, fl.L, Ns, dnb, dns, tw, nseq, si, sb, sign); break;
+      default: stockham_stage<T2, 5>(a, b, fl.L, Ns, dnb, dns, tw, nseq, si, sb, sign); break;
     }
     __syncthreads();
     T2* t = a;
@@ -419,7 +433,7 @@ __global__ void __launch_bounds__(256) k_fft_rows(const T2* __restrict__ in, T2*
                                                   int rows_per_cta, const FftLen* __restrict__ ffts, int fidx,
                                                   const T2* __restrict__ tw, int sign, double scale) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  const FftLen fl = ffts[fidx];
+  const FftLen& fl = ffts[fidx];
   const int L = fl.L;
   const int r0 = blockIdx.x * rows_per_cta;
   const int nr = min(rows_per_cta, nrows - r0);
@@ -443,7 +457,7 @@ __global__ void __launch_bounds__(256) k_fft_cols(const T2* __restrict__ in, T2*
                                                   int cols_per_cta, const FftLen* __restrict__ ffts, int fidx,
                                                   const T2* __restrict__ tw, int sign, double scale) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  const FftLen fl = ffts[fidx];
+  const FftLen& fl = ffts[fidx];
   const int L = fl.L;
   const int c0 = blockIdx.x * cols_per_cta;
   const int C = min(cols_per_cta, ncols - c0);
@@ -483,7 +497,7 @@ __global__ void __launch_bounds__(256) k_rowpass(int N, const WedgeDev* __restri
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const FftJob job = jobs[blockIdx.x];
   const WedgeDev& w = wedges[job.w];
-  const FftLen fl = ffts[w.fft2];
+  const FftLen& fl = ffts[w.fft2];
   const int L = fl.L, n1 = w.n1, n2 = w.n2, cnt = job.count;
   T2* a = reinterpret_cast<T2*>(smem_raw);
   T2* b = a + cnt * L;
@@ -491,9 +505,9 @@ __global__ void __launch_bounds__(256) k_rowpass(int N, const WedgeDev* __restri
   for (int idx = threadIdx.x; idx < cnt * L; idx += blockDim.x) a[idx] = zero;
   __syncthreads();
   const T2* bet = betas[job.w] + ((long long)job.t * n1 + job.start) * n2;
-  for (int idx = threadIdx.x; idx < cnt * n2; idx += blockDim.x) {
-    int r = idx / n2, i2 = idx - r * n2;
-    T2 bv = bet[idx];
+  for (int r = 0; r < cnt; ++r)
+  for (int i2 = threadIdx.x; i2 < n2; i2 += blockDim.x) {
+    T2 bv = bet[r * n2 + i2];
     if (bv.x != 0 || bv.y != 0) {
       int kp1 = job.start + r - n1 / 2, kp2 = i2 - n2 / 2;
       int z1 = kp1 + w.xc1, z2 = kp2 + w.xc2;
@@ -505,8 +519,9 @@ __global__ void __launch_bounds__(256) k_rowpass(int N, const WedgeDev* __restri
   __syncthreads();
   T2* res = smem_fft<T2>(a, b, fl, tw + fl.tw_off, cnt, 1, L, +1);
   T2* dst = p1 + w.p1_off + (long long)job.t * L * n1 + job.start;
-  for (int idx = threadIdx.x; idx < cnt * L; idx += blockDim.x) {
-    const int j2 = idx / cnt, r = idx - j2 * cnt;
+  const FastDiv dc = make_fastdiv_dev((unsigned)cnt);
+  for (int idx = threadIdx.x; idx < cnt * L; idx += blockDim.x) {  // consecutive threads: consecutive i1
+    const int j2 = fdiv(idx, dc), r = idx - j2 * cnt;
     dst[(long long)j2 * n1 + r] = res[r * L + j2];
   }
 }
@@ -524,7 +539,7 @@ __global__ void __launch_bounds__(256) k_colpass(const WedgeDev* __restrict__ we
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const FftJob job = jobs[blockIdx.x];
   const WedgeDev& w = wedges[job.w];
-  const FftLen fl = ffts[w.fft1];
+  const FftLen& fl = ffts[w.fft1];
   const int L = fl.L, n1 = w.n1, C = job.count, c0 = job.start;
   T2* a = reinterpret_cast<T2*>(smem_raw);
   T2* b = a + C * L;
@@ -532,21 +547,24 @@ __global__ void __launch_bounds__(256) k_colpass(const WedgeDev* __restrict__ we
   for (int idx = threadIdx.x; idx < C * L; idx += blockDim.x) a[idx] = zero;
   __syncthreads();
   const T2* src = p1 + w.p1_off + ((long long)job.t * w.n2f + c0) * n1;
-  for (int idx = threadIdx.x; idx < C * n1; idx += blockDim.x) {
-    const int c = idx / n1, i1 = idx - c * n1;
-    a[c * L + imod(i1 - n1 / 2, L)] = src[idx];
-  }
+  for (int c = 0; c < C; ++c)
+    for (int i1 = threadIdx.x; i1 < n1; i1 += blockDim.x) {
+      int pos = i1 - n1 / 2;
+      pos = pos < 0 ? pos + L : pos;
+      a[c * L + pos] = src[(long long)c * n1 + i1];
+    }
   __syncthreads();
   T2* res = smem_fft<T2>(a, b, fl, tw + fl.tw_off, C, 1, L, +1);
   const int rowp = L + 2 * kHalo;
   T2* dst = g + w.g_off + ((long long)job.t * w.n2f + c0) * rowp + kHalo;
-  for (int idx = threadIdx.x; idx < C * L; idx += blockDim.x) {
-    const int c = idx / L, j1 = idx - c * L;
+  for (int c = 0; c < C; ++c) {
     T2* rp = dst + (long long)c * rowp;
-    const T2 v = res[idx];
-    rp[j1] = v;
-    if (j1 < kHalo) rp[L + j1] = v;
-    if (j1 >= L - kHalo) rp[j1 - L] = v;
+    for (int j1 = threadIdx.x; j1 < L; j1 += blockDim.x) {
+      const T2 v = res[c * L + j1];
+      rp[j1] = v;
+      if (j1 < kHalo) rp[L + j1] = v;
+      if (j1 >= L - kHalo) rp[j1 - L] = v;
+    }
   }
 }
 
