@@ -156,3 +156,15 @@ def test_invalid_arguments():
         fio.Plan(14, np.zeros(196), np.zeros(196), device=0)  # 14 = 2*7 is not 5-smooth
     with pytest.raises(fio.FioError):
         fio.Plan(64, op.c1, op.c2, rank=2, nranks=2, device=0)
+
+
+@pytest.mark.slow
+def test_config4_sampled():
+    # N = 2048, complex128, eps = 1e-6: direct sum at 4096 seeded output points (BASELINE configs[4])
+    cfg = wl.config("cfg4")
+    op, f = wl.make_operator(cfg), wl.make_input(cfg)
+    plan, out = run(op, f, eps=cfg["eps"])
+    pts = wl.sample_points(op.N, 4096, 1)
+    err = oracle.rel_l2(out.ravel()[pts], oracle.fio(op, f, pts=pts))
+    print("config4: W", plan.info["W"], "sum_q", plan.info["sum_q"], "plan s", plan.info["plan_seconds"], "err", err)
+    assert err <= 10 * cfg["eps"], err
