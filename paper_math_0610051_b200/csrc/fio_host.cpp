@@ -6,6 +6,7 @@
 #include <algorithm>
 #include <array>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <numeric>
 #include <unordered_set>
@@ -119,9 +120,15 @@ void build_geometry(int N, int W, std::vector<WedgeGeom>& wedges) {
   }
 }
 
-// Stockham radix sequence: 4s first, then 2, 3s, 5s (all sizes 5-smooth).
+// Stockham radix sequence: 4s, then 2, 3s, 5s (all sizes 5-smooth).  Radix-8/16 butterflies
+// exist in the kernels but measured slower on B200 for these lengths (fewer butterflies per
+// stage than threads, higher register use); FIO_FFT_RADIX16=1 selects them.
 std::vector<int8_t> radix_plan(int L) {
   std::vector<int8_t> r;
+  if (const char* e = std::getenv("FIO_FFT_RADIX16"); e && std::atoi(e) == 1) {
+    while (L % 16 == 0) { r.push_back(16); L /= 16; }
+    while (L % 8 == 0) { r.push_back(8); L /= 8; }
+  }
   while (L % 4 == 0) { r.push_back(4); L /= 4; }
   while (L % 2 == 0) { r.push_back(2); L /= 2; }
   while (L % 3 == 0) { r.push_back(3); L /= 3; }

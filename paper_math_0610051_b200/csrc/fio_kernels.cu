@@ -360,6 +360,54 @@ __device__ __forceinline__ void dft_small(T2 (&v)[R], int sign) {
     v[4] = csub(m1, r1);
     v[2] = cadd(m2, r2);
     v[3] = csub(m2, r2);
+  } else if constexpr (R == 8) {
+    const Rt r2 = (Rt)0.70710678118654752440;
+    const Rt sg = (Rt)sign;
+    T2 a[4] = {v[0], v[2], v[4], v[6]};
+    T2 b[4] = {v[1], v[3], v[5], v[7]};
+    dft_small<T2, 4>(a, sign);
+    dft_small<T2, 4>(b, sign);
+    // b_k *= e^{sign 2 pi i k / 8}
+    b[1] = mk<T2>((b[1].x - sg * b[1].y) * r2, (b[1].y + sg * b[1].x) * r2);
+    b[2] = mul_i(b[2], sign);
+    b[3] = mk<T2>((-b[3].x - sg * b[3].y) * r2, (-b[3].y + sg * b[3].x) * r2);
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      v[k] = cadd(a[k], b[k]);
+      v[k + 4] = csub(a[k], b[k]);
+    }
+  } else if constexpr (R == 16) {
+    // 16 = 4 x 4: inner DFT-4 over r1 (stride 4), twiddle w16^{r2 o1}, outer DFT-4 over r2
+    T2 y[4][4];
+#pragma unroll
+    for (int r2 = 0; r2 < 4; ++r2) {
+      T2 t[4] = {v[r2], v[4 + r2], v[8 + r2], v[12 + r2]};
+      dft_small<T2, 4>(t, sign);
+#pragma unroll
+      for (int o1 = 0; o1 < 4; ++o1) y[r2][o1] = t[o1];
+    }
+    const Rt C[10] = {(Rt)1, (Rt)0.92387953251128675613, (Rt)0.70710678118654752440, (Rt)0.38268343236508977173,
+                      (Rt)0, (Rt)-0.38268343236508977173, (Rt)-0.70710678118654752440,
+                      (Rt)-0.92387953251128675613, (Rt)-1, (Rt)-0.92387953251128675613};
+    const Rt S[10] = {(Rt)0, (Rt)0.38268343236508977173, (Rt)0.70710678118654752440, (Rt)0.92387953251128675613,
+                      (Rt)1, (Rt)0.92387953251128675613, (Rt)0.70710678118654752440, (Rt)0.38268343236508977173,
+                      (Rt)0, (Rt)-0.38268343236508977173};
+#pragma unroll
+    for (int r2 = 1; r2 < 4; ++r2)
+#pragma unroll
+      for (int o1 = 1; o1 < 4; ++o1) {
+        const int m = r2 * o1;
+        const Rt c = C[m], sn = (Rt)sign * S[m];
+        T2 u = y[r2][o1];
+        y[r2][o1] = mk<T2>(u.x * c - u.y * sn, u.x * sn + u.y * c);
+      }
+#pragma unroll
+    for (int o1 = 0; o1 < 4; ++o1) {
+      T2 t[4] = {y[0][o1], y[1][o1], y[2][o1], y[3][o1]};
+      dft_small<T2, 4>(t, sign);
+#pragma unroll
+      for (int o2 = 0; o2 < 4; ++o2) v[o1 + 4 * o2] = t[o2];
+    }
   }
 }
 
@@ -412,6 +460,8 @@ __device__ T2* smem_fft(T2* a, T2* b, const FftLen& fl, const T2* tw, int nseq, 
     const FastDiv& dnb = fl.div_nb[st];
     const FastDiv& dns = fl.div_ns[st];
     switch (R) {
+      case 16: stockham_stage<T2, 16>(a, b, fl.L, Ns, dnb, dns, tw, nseq, si, sb, sign); break;
+      case 8: stockham_stage<T2, 8>(a, b, fl.L, Ns, dnb, dns, tw, nseq, si, sb, sign); break;
       case 4: stockham_stage<T2, 4>(a, b, fl.L, Ns, dnb, dns, tw, nseq, si, sb, sign); break;
       case 2: stockham_stage<T2, 2>(a, b, fl.L, Ns, dnb, dns, tw, nseq, si, sb, sign); break;
       case 3: stockham_stage<T2, 3>(a, b, fl.L, Ns, dnb, dns, tw, nseq, si, sb, sign); break;
