@@ -726,10 +726,12 @@ template <> struct OffT<double2> { using type = double2; };
 template <typename T2> struct K3Cfg;
 template <> struct K3Cfg<float2> {
   static constexpr int BLOCK = kK3BlockC64, MINB = 2;
+  static constexpr bool P1REG = false;  // row weights in registers measured slower (4.28 vs 3.69 ms)
   static constexpr int MAXC = kK3TileCapC64 / 2 / kK3BlockC64;  // 16-B tile-copy slots per thread
 };
 template <> struct K3Cfg<double2> {
   static constexpr int BLOCK = kK3BlockC128, MINB = 2;
+  static constexpr bool P1REG = false;  // 64 more FP64 registers would not fit
   static constexpr int MAXC = kK3TileCapC128 / 1 / kK3BlockC128;
 };
 
@@ -745,7 +747,7 @@ __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_gr
 template <typename T2, int TAPS, int P>
 __host__ __device__ constexpr size_t k3_fixed_smem() {
   return sizeof(T2) * kK3Stages * K3Cfg<T2>::BLOCK * P +
-         sizeof(typename Real<T2>::type) * P * ((TAPS + 2) & ~1) * K3Cfg<T2>::BLOCK;
+         (K3Cfg<T2>::P1REG ? 0 : sizeof(typename Real<T2>::type) * P * ((TAPS + 2) & ~1) * K3Cfg<T2>::BLOCK);
 }
 
 // K3: one CTA processes chunks of BLOCK consecutive groups (one group of P points per
@@ -839,6 +841,8 @@ __global__ void __launch_bounds__(K3Cfg<T2>::BLOCK, K3Cfg<T2>::MINB)
     int a1 = 0, a2 = 0;
     int xs[P];
     Rt p2[P][WIN];
+    constexpr bool P1REG = K3Cfg<T2>::P1REG;
+    Rt p1r[P][P1REG ? WINR : 1];
     T2 base[P];
     if (valid) {
       a1 = iw.anchor[2 * g] - bx.x;
@@ -857,11 +861,16 @@ __global__ void __launch_bounds__(K3Cfg<T2>::BLOCK, K3Cfg<T2>::MINB)
       Rt w1[WINR];
       window_weights<Rt, TAPS, WINR>(o.x, inv_half_w, beta, poly, w1);
       window_weights<Rt, TAPS, WIN>(o.y, inv_half_w, beta, poly, p2[k]);
+      if constexpr (P1REG) {
 #pragma unroll
-      for (int i = 0; i < WINR; ++i) p1s[(i * BLOCK + threadIdx.x) * P + k] = w1[i];
-      // start the read of the running sum early (latency hidden by the term loop)
-      base[k] = mk<T2>(0, 0);
-      if (xs[k] >= 0 && !first) base[k] = Lf[xs[k]];
+        for (int i = 0; i < WINR; ++i) p1r[k][i] = w1[i];
+      } else {
+#pragma unroll
+        for (int i = 0; i < WINR; ++i) p1s[(i * BLOCK + threadIdx.x) * P + k] = w1[i];
+        // start the read of the running sum early (latency hidden by the term loop)
+        base[k] = mk<T2>(0, 0);
+        if (xs[k] >= 0 && !first) base[k] = Lf[xs[k]];
+      }
     }
     const int woff = a1 * bx.w + a2;
     T2 acc[P];
@@ -881,7 +890,12 @@ __global__ void __launch_bounds__(K3Cfg<T2>::BLOCK, K3Cfg<T2>::MINB)
         T2 v[WIN];
         load_row<T2, WIN>(rowp, v);
         Rt w1[P];
-        load_p1<Rt, P>(p1s + (i * BLOCK + threadIdx.x) * P, w1);
+        if constexpr (P1REG) {
+#pragma unroll
+          for (int k = 0; k < P; ++k) w1[k] = p1r[k][i];
+        } else {
+          load_p1<Rt, P>(p1s + (i * BLOCK + threadIdx.x) * P, w1);
+        }
 #pragma unroll
         for (int k = 0; k < P; ++k) {
           T2 rr = mk<T2>(0, 0);
@@ -903,7 +917,12 @@ __global__ void __launch_bounds__(K3Cfg<T2>::BLOCK, K3Cfg<T2>::MINB)
     for (int k = 0; k < P; ++k) {
       const int x = xs[k];
       if (x < 0) continue;
-      T2 b0 = base[k];
+      T2 b0;
+      if constexpr (P1REG) {
+        b0 = first ? mk<T2>(0, 0) : Lf[x];
+      } else {
+        b0 = base[k];
+      }
       if (first && add_dc) {
         double2 d = a0[x];
         b0 = mk<T2>((Rt)(d.x * (double)f0.x - d.y * (double)f0.y), (Rt)(d.x * (double)f0.y + d.y * (double)f0.x));
