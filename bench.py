@@ -216,6 +216,21 @@ def time_config(name, args, rank, world, local, group):
         ms = float(t.item())
     ms_step = ms / args.steps
     applies_per_s = 1e3 / ms_step
+    # adjoint (NEXT-1), same input, device-timed
+    adj_ms = None
+    if world == 1:
+        g = torch.empty_like(f)
+        for _ in range(2):
+            plan.apply_adjoint(f, out=g)
+        a0e, a1e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize(dev)
+        a0e.record(stream)
+        for _ in range(args.steps):
+            plan.apply_adjoint(f, out=g)
+        a1e.record(stream)
+        torch.cuda.synchronize(dev)
+        adj_ms = a0e.elapsed_time(a1e) / args.steps
+        del g
     # e2e through the public API with host buffers (pinned), copies inside the timed region
     hin = torch.from_numpy(f_np.astype(np.complex64 if c64 else np.complex128)).pin_memory()
     hout = torch.empty_like(hin).pin_memory()
@@ -250,6 +265,7 @@ def time_config(name, args, rank, world, local, group):
                  "slots": info["slots"], "max_tile_cap": info["max_tile_cap"],
                  "k3_thread_fill": info["slots"] / 4 / max(info["k3_thread_slots"], 1)},
         "launches_per_step": info["launches_per_apply"],
+        "adjoint_ms_per_step": adj_ms,
         "clocks": clk.summary(), "e2e": e2e,
     }
     plan.close()
@@ -274,7 +290,8 @@ def run_gpu(args):
     if args.variant:
         v = time_config(args.variant, args, rank, world, local, group)
         variants[args.variant] = {k: v[k] for k in ("dtype", "eps", "applies_per_s", "points_per_s", "ms_per_step",
-                                                    "roofline", "stage_ms", "k3_share", "plan", "e2e")}
+                                                    "roofline", "stage_ms", "k3_share", "plan", "e2e",
+                                                    "adjoint_ms_per_step")}
     if rank == 0:
         cpu = None
         if world == 1 and not args.no_cpu_baseline:
@@ -289,7 +306,7 @@ def run_gpu(args):
                        "l2": "inputs larger than L2 (alpha' streams %.1f GB per step)" % main["plan"]["alpha_GB"]},
             "points_per_s": main["points_per_s"],
             "roofline": main["roofline"], "apply_hbm_gbs": main["apply_hbm_gbs"], "stage_ms": main["stage_ms"],
-            "k3_share": main["k3_share"], "plan": main["plan"],
+            "k3_share": main["k3_share"], "plan": main["plan"], "adjoint_ms_per_step": main["adjoint_ms_per_step"],
             "clocks": main["clocks"], "e2e": main["e2e"],
             "gpu_launches": main["launches_per_step"] * args.steps,
             "cpu_baseline": cpu, "variants": variants,

@@ -118,6 +118,15 @@ fio_status fio_plan(fio_handle* out, int N, const fio_phase* phase, const fio_am
  * `stream`; one apply in flight per handle (the workspace is per handle). */
 fio_status fio_apply(fio_handle h, const void* f_dev, void* Lf_dev, void* stream);
 
+/* The adjoint: out = L~* g, the exact conjugate transpose of the fast
+ * operator fio_apply evaluates (so <L~f, g> = <f, L~* g> to rounding), approximating
+ * (L* g)(x) = (1/N) sum_xi e^{2 pi i x.xi} (1/N) sum_y conj(a(y,xi)) e^{-2 pi i Phi(y,xi)} g(y).
+ * g_dev, out_dev: device N x N complex of the plan dtype (no aliasing).  With nranks > 1 the
+ * result is this rank's partial (its wedges; the DC term on rank 0).  Asynchronous on stream;
+ * shares the handle's workspace with fio_apply (one call in flight per handle).  The type-1
+ * spreading step accumulates with atomics: the last bits may vary between runs. */
+fio_status fio_apply_adjoint(fio_handle h, const void* g_dev, void* out_dev, void* stream);
+
 /* End-to-end variant: f_host / Lf_host are HOST buffers (pinned for overlap);
  * the host->device copy, the apply and the device->host copy are enqueued on
  * `stream`, which is synchronized before return. */

@@ -32,7 +32,7 @@ FIO_C64, FIO_C128 = 1, 2
 FIO_OK, FIO_WNOTCERT = 0, 1
 
 # every entry point declared in include/fio.h
-SYMBOLS = ["fio_default_opts", "fio_plan", "fio_apply", "fio_apply_host", "fio_destroy", "fio_plan_info",
+SYMBOLS = ["fio_default_opts", "fio_plan", "fio_apply", "fio_apply_adjoint", "fio_apply_host", "fio_destroy", "fio_plan_info",
            "fio_plan_wedges", "fio_geometry", "fio_assign_wedges", "fio_profile_begin", "fio_profile_end",
            "fio_last_error", "fio_version"]
 STAGES = ["K0_rows", "K0_cols", "K1_rowpass", "K2_colpass", "K3_interp"]
@@ -91,6 +91,7 @@ def load_library():
                              ctypes.POINTER(_Opts)]
     lib.fio_apply.argtypes = [P, P, P, P]
     lib.fio_apply_host.argtypes = [P, P, P, P]
+    lib.fio_apply_adjoint.argtypes = [P, P, P, P]
     lib.fio_destroy.argtypes = [P]
     lib.fio_plan_info.argtypes = [P, ctypes.POINTER(_Info)]
     lib.fio_plan_wedges.argtypes = [P, P, P, P, P, P, P, P]
@@ -100,7 +101,7 @@ def load_library():
     lib.fio_profile_end.argtypes = [P, P, P]
     lib.fio_last_error.restype = ctypes.c_char_p
     lib.fio_version.restype = ctypes.c_char_p
-    for name in ["fio_plan", "fio_apply", "fio_apply_host", "fio_destroy", "fio_plan_info", "fio_plan_wedges",
+    for name in ["fio_plan", "fio_apply", "fio_apply_adjoint", "fio_apply_host", "fio_destroy", "fio_plan_info", "fio_plan_wedges",
                  "fio_geometry", "fio_assign_wedges", "fio_profile_begin", "fio_profile_end"]:
         getattr(lib, name).restype = ctypes.c_int
     _lib = lib
@@ -226,6 +227,20 @@ class Plan:
             stream = torch.cuda.current_stream(f.device)
         _check(self._lib.fio_apply(self._h, ctypes.c_void_p(f.data_ptr()), ctypes.c_void_p(out.data_ptr()),
                                    ctypes.c_void_p(stream.cuda_stream)))
+        return out
+
+    def apply_adjoint(self, g, out=None, stream=None):
+        """L~* g for a device tensor g (N x N, plan dtype)."""
+        import torch
+        if not (g.is_cuda and g.dtype == self.torch_dtype and tuple(g.shape) == (self.N, self.N)):
+            raise FioError(-1, f"g must be a CUDA {self.torch_dtype} tensor of shape ({self.N}, {self.N})")
+        g = g.contiguous()
+        if out is None:
+            out = torch.empty_like(g)
+        if stream is None:
+            stream = torch.cuda.current_stream(g.device)
+        _check(self._lib.fio_apply_adjoint(self._h, ctypes.c_void_p(g.data_ptr()), ctypes.c_void_p(out.data_ptr()),
+                                           ctypes.c_void_p(stream.cuda_stream)))
         return out
 
     def apply_host(self, f_host, out_host, stream=None):

@@ -86,7 +86,10 @@ struct fio_plan_s {
   void** d_alpha = nullptr;
   void** d_beta = nullptr;
   void *fhat = nullptr, *tmp = nullptr, *p1 = nullptr, *g = nullptr;
-  FftJob *jobs_row = nullptr, *jobs_col = nullptr;
+  FftJob *jobs_row = nullptr, *jobs_col = nullptr, *jobs_rowadj = nullptr;
+  int njobs_rowadj = 0, smem_rowadj = 0;
+  std::vector<void*> mask_ptrs;
+  unsigned char** d_masks = nullptr;
   int njobs_row = 0, njobs_col = 0, smem_row = 0, smem_col = 0;
   int rows_per_cta_N = 1, cols_per_cta_N = 1, fft_N = 0;
   void *e2e_in = nullptr, *e2e_out = nullptr;
@@ -525,6 +528,19 @@ fio_status build_plan(fio_plan_s& P, const fio_phase* phase, const fio_amplitude
     P.beta_bytes += cs * (size_t)q * g.n1 * g.n2;
     P.alpha_ptrs.push_back(alpha);
     P.beta_ptrs.push_back(betap);
+    {  // box mask of the wedge's members (adjoint K1* writes fhat* only there)
+      std::vector<unsigned char> mask((size_t)g.n1 * g.n2, 0);
+      for (int kf : g.members) {
+        int k1 = kf / N, k2 = kf % N;
+        int x1 = k1 >= N / 2 ? k1 - N : k1, x2 = k2 >= N / 2 ? k2 - N : k2;
+        int i1 = g.M[0] * x1 + g.M[1] * x2 - g.xc1 + g.n1 / 2;
+        int i2 = g.M[2] * x1 + g.M[3] * x2 - g.xc2 + g.n2 / 2;
+        mask[(size_t)i1 * g.n2 + i2] = 1;
+      }
+      unsigned char* dm = nullptr;
+      FIO_CUDA(P.upload(&dm, mask.data(), mask.size()));
+      P.mask_ptrs.push_back(dm);
+    }
     P.wd.push_back(w);
     P.r_final.push_back(r);
     P.sep_err.push_back(err);
@@ -559,8 +575,8 @@ fio_status build_plan(fio_plan_s& P, const fio_phase* phase, const fio_amplitude
   int max_rows = 32, max_cols = 16;
   if (const char* e = std::getenv("FIO_FFT_MAXSEQ")) max_rows = max_cols = std::min(32, std::max(1, std::atoi(e)));
   long long p1_off = 0, g_off = 0;
-  std::vector<FftJob> jr, jc;
-  size_t smem_row = 0, smem_col = 0;
+  std::vector<FftJob> jr, jc, jra;
+  size_t smem_row = 0, smem_col = 0, smem_rowadj = 0;
   for (size_t wi = 0; wi < P.wd.size(); ++wi) {
     WedgeDev& w = P.wd[wi];
     w.p1_off = p1_off;
@@ -573,6 +589,11 @@ fio_status build_plan(fio_plan_s& P, const fio_phase* phase, const fio_amplitude
     int cols = (int)std::max<size_t>(1, std::min<size_t>(max_cols, kSmemBudget / sc));
     cols = std::min(cols, w.n2f);
     rows = std::min(rows, w.n1);
+    for (int i = 0; i < w.n1; i += rows) {
+      const int cnt = std::min(rows, w.n1 - i);
+      jra.push_back({(int)wi, 0, i, cnt});
+      smem_rowadj = std::max(smem_rowadj, sr * cnt + (size_t)cnt * w.n2 * (c64 ? sizeof(float2) : sizeof(double2)));
+    }
     for (int t = 0; t < w.q; ++t) {
       for (int i = 0; i < w.n1; i += rows) {
         jr.push_back({(int)wi, t, i, std::min(rows, w.n1 - i)});
@@ -584,7 +605,7 @@ fio_status build_plan(fio_plan_s& P, const fio_phase* phase, const fio_amplitude
       }
     }
   }
-  if (smem_row > kSmemMax || smem_col > kSmemMax || fft_seq_bytes(N, c64) > kSmemMax) {
+  if (smem_row > kSmemMax || smem_col > kSmemMax || smem_rowadj > kSmemMax || fft_seq_bytes(N, c64) > kSmemMax) {
     set_error("fine grid too large for the shared-memory FFT (N too large for this dtype)");
     return FIO_EINVAL;
   }
@@ -600,6 +621,10 @@ fio_status build_plan(fio_plan_s& P, const fio_phase* phase, const fio_amplitude
   FIO_CUDA(configure_kernels(kSmemMax));
   if (!jr.empty()) FIO_CUDA(P.upload(&P.jobs_row, jr.data(), jr.size()));
   if (!jc.empty()) FIO_CUDA(P.upload(&P.jobs_col, jc.data(), jc.size()));
+  if (!jra.empty()) FIO_CUDA(P.upload(&P.jobs_rowadj, jra.data(), jra.size()));
+  P.njobs_rowadj = (int)jra.size();
+  P.smem_rowadj = (int)smem_rowadj;
+  FIO_CUDA(P.upload(reinterpret_cast<void***>(&P.d_masks), P.mask_ptrs.data(), std::max<size_t>(P.mask_ptrs.size(), 1)));
   FIO_CUDA(P.upload(&P.d_ffts, ffts.data(), ffts.size()));
   FIO_CUDA(P.upload(&P.d_wedges, P.wd.data(), std::max<size_t>(P.wd.size(), 1)));
   FIO_CUDA(P.upload(&P.d_beta, P.beta_ptrs.data(), std::max<size_t>(P.beta_ptrs.size(), 1)));
@@ -639,6 +664,11 @@ ApplyArgs make_args(const fio_plan_s& P) {
   a.njobs_col = P.njobs_col;
   a.smem_col = P.smem_col;
   a.rows_per_cta_N = P.rows_per_cta_N;
+  a.jobs_rowadj = P.jobs_rowadj;
+  a.njobs_rowadj = P.njobs_rowadj;
+  a.smem_rowadj = P.smem_rowadj;
+  a.masks = const_cast<const unsigned char* const*>(P.d_masks);
+  a.fine_elems = P.fine_elems;
   a.cols_per_cta_N = P.cols_per_cta_N;
   return a;
 }
@@ -747,6 +777,24 @@ fio_status fio_apply(fio_handle h, const void* f_dev, void* Lf_dev, void* stream
   if (h->prof_n < h->prof_cap) ev = &h->prof_ev[(size_t)h->prof_n++ * (kStages + 1)];
   FIO_CUDA(enqueue_apply(a, h->c64, f_dev, Lf_dev, (cudaStream_t)stream, &launches, ev));
   h->launches = launches;
+  return FIO_OK;
+}
+
+fio_status fio_apply_adjoint(fio_handle h, const void* g_dev, void* out_dev, void* stream) {
+  if (!h || !g_dev || !out_dev) {
+    set_error("fio_apply_adjoint: NULL argument");
+    return FIO_EINVAL;
+  }
+  if (g_dev == out_dev) {
+    set_error("fio_apply_adjoint: g and out must not alias");
+    return FIO_EINVAL;
+  }
+  int dev = -1;
+  cudaGetDevice(&dev);
+  if (dev != h->device) FIO_CUDA(cudaSetDevice(h->device));
+  ApplyArgs a = make_args(*h);
+  int launches = 0;
+  FIO_CUDA(enqueue_adjoint(a, h->c64, g_dev, out_dev, (cudaStream_t)stream, &launches));
   return FIO_OK;
 }
 

@@ -125,7 +125,7 @@ void build_geometry(int N, int W, std::vector<WedgeGeom>& wedges) {
 // stage than threads, higher register use); FIO_FFT_RADIX16=1 selects them.
 std::vector<int8_t> radix_plan(int L) {
   std::vector<int8_t> r;
-  if (const char* e = std::getenv("FIO_FFT_RADIX16"); e && std::atoi(e) == 1) {
+  if (const char* e = std::getenv("FIO_FFT_RADIX16"); e && std::atoi(e) == 1) {  // needs FIO_FFT_BIG_RADIX=1 build
     while (L % 16 == 0) { r.push_back(16); L /= 16; }
     while (L % 8 == 0) { r.push_back(8); L /= 8; }
   }

@@ -411,6 +411,12 @@ __device__ __forceinline__ void dft_small(T2 (&v)[R], int sign) {
   }
 }
 
+// Radix-8/16 stages (compiled in with -DFIO_FFT_BIG_RADIX=1 and selected by FIO_FFT_RADIX16=1):
+// measured slower on B200 and their register footprint slows every FFT kernel, so off by default.
+#ifndef FIO_FFT_BIG_RADIX
+#define FIO_FFT_BIG_RADIX 0
+#endif
+
 __device__ __forceinline__ int fdiv(int n, const FastDiv& f) {
   return (int)((__umulhi(f.m, (unsigned)n) + (unsigned)n) >> f.l);
 }
@@ -460,8 +466,10 @@ __device__ T2* smem_fft(T2* a, T2* b, const FftLen& fl, const T2* tw, int nseq, 
     const FastDiv& dnb = fl.div_nb[st];
     const FastDiv& dns = fl.div_ns[st];
     switch (R) {
+#if FIO_FFT_BIG_RADIX
       case 16: stockham_stage<T2, 16>(a, b, fl.L, Ns, dnb, dns, tw, nseq, si, sb, sign); break;
       case 8: stockham_stage<T2, 8>(a, b, fl.L, Ns, dnb, dns, tw, nseq, si, sb, sign); break;
+#endif
       case 4: stockham_stage<T2, 4>(a, b, fl.L, Ns, dnb, dns, tw, nseq, si, sb, sign); break;
       case 2: stockham_stage<T2, 2>(a, b, fl.L, Ns, dnb, dns, tw, nseq, si, sb, sign); break;
       case 3: stockham_stage<T2, 3>(a, b, fl.L, Ns, dnb, dns, tw, nseq, si, sb, sign); break;
@@ -1010,6 +1018,266 @@ static cudaError_t launch_interp(const ApplyArgs& a, T2* Lf, cudaStream_t s, int
   return cudaSuccess;
 }
 
+// ================================================================== adjoint
+// The exact conjugate transpose of the discrete fast forward operator above:
+//   K3*  spread: G*_lt[cell] += sum_points phi(x, cell) conj(alpha'_lt(x)) g(x)   (NUFFT type 1)
+//   K2*  per fine row j2: fold halos, FFT_{-} (length n1f), keep box indices -> P1*[t][j2][i1]
+//   K1*  per box row i1: FFT_{-} (length n2f) of P1*[t][.][i1], keep box indices,
+//        fhat*(xi) = sum_t conj(beta'_lt) h*_t  (each xi belongs to one wedge and one box cell)
+//   DC   fhat*(0) = sum_x conj(a(x,0)/N) g(x)
+//   K0*  L* g = (1/N) sum_xi e^{+2 pi i x.xi} fhat*(xi)
+// K3* accumulates with global RED atomics (native on sm_100a; the shared-memory float atomic
+// is a CAS loop), so its summation order -- and the last bits of the adjoint -- can vary
+// from run to run.
+template <typename T2, int TAPS, int P>
+__global__ void __launch_bounds__(128) k_spread_groups(InterpWedge iw, T2* __restrict__ gstar,
+                                                       const T2* __restrict__ g, double es_beta, EsPoly poly) {
+  using Rt = typename Real<T2>::type;
+  using O2 = typename OffT<T2>::type;
+  constexpr int WIN = TAPS + 1;
+  constexpr int WINR = (WIN + 1) & ~1;
+  const Rt inv_half_w = (Rt)(2.0 / TAPS);
+  const Rt beta = (Rt)es_beta;
+  const int n1f = iw.nrow, n2p = iw.ncolp, q = iw.q;
+  const long long gstride = (long long)n1f * n2p;
+  const long long nslots = (long long)iw.ngroups * P;
+  T2* __restrict__ G = gstar + iw.g_off + kHalo;
+  const T2* __restrict__ alpha = reinterpret_cast<const T2*>(iw.alpha);
+  const O2* __restrict__ offs = reinterpret_cast<const O2*>(iw.slot_off);
+  for (int grp = blockIdx.x * blockDim.x + threadIdx.x; grp < iw.ngroups; grp += gridDim.x * blockDim.x) {
+    const int a1 = iw.anchor[2 * grp], a2 = iw.anchor[2 * grp + 1];
+    const int r0 = a1 < 0 ? a1 + n1f : a1;
+    Rt p1[P][WINR], p2[P][WIN];
+    T2 gx[P];
+#pragma unroll
+    for (int k = 0; k < P; ++k) {
+      const int x = iw.slot_x[grp * P + k];
+      const O2 o = offs[grp * P + k];
+      gx[k] = x >= 0 ? g[x] : mk<T2>(0, 0);
+      window_weights<Rt, TAPS, WINR>((Rt)o.x, inv_half_w, beta, poly, p1[k]);
+      window_weights<Rt, TAPS, WIN>((Rt)o.y, inv_half_w, beta, poly, p2[k]);
+    }
+    for (int t = 0; t < q; ++t) {
+      T2 c[P];
+#pragma unroll
+      for (int k = 0; k < P; ++k) {
+        const T2 av = alpha[t * nslots + (long long)grp * P + k];  // conj(alpha') g
+        c[k] = mk<T2>(av.x * gx[k].x + av.y * gx[k].y, av.x * gx[k].y - av.y * gx[k].x);
+      }
+      T2* __restrict__ rp = G + t * gstride + (long long)r0 * n2p + a2;
+      int r = r0;
+#pragma unroll 1
+      for (int i = 0; i < WINR; ++i) {
+        T2 e[P];
+#pragma unroll
+        for (int k = 0; k < P; ++k) e[k] = mk<T2>(p1[k][i] * c[k].x, p1[k][i] * c[k].y);
+#pragma unroll
+        for (int j = 0; j < WIN; ++j) {
+          T2 v = mk<T2>(0, 0);
+#pragma unroll
+          for (int k = 0; k < P; ++k) v = cfma_real(p2[k][j], e[k], v);
+          atomicAdd(&rp[j].x, v.x);
+          atomicAdd(&rp[j].y, v.y);
+        }
+        rp += (r + 1 == n1f) ? -(long long)(n1f - 1) * n2p : (long long)n2p;
+        r = (r + 1 == n1f) ? 0 : r + 1;
+      }
+    }
+  }
+}
+
+// K2*: job (w, t, c0, C) over fine rows j2 in [c0, c0 + C) of G*_lt.
+template <typename T2>
+__global__ void __launch_bounds__(256) k_colpass_adj(const WedgeDev* __restrict__ wedges,
+                                                     const FftJob* __restrict__ jobs, const FftLen* __restrict__ ffts,
+                                                     const T2* __restrict__ tw, const T2* __restrict__ g,
+                                                     T2* __restrict__ p1) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const FftJob job = jobs[blockIdx.x];
+  const WedgeDev& w = wedges[job.w];
+  const FftLen& fl = ffts[w.fft1];
+  const int L = fl.L, n1 = w.n1, C = job.count, c0 = job.start;
+  T2* a = reinterpret_cast<T2*>(smem_raw);
+  T2* b = a + C * L;
+  const int rowp = L + 2 * kHalo;
+  const T2* src = g + w.g_off + ((long long)job.t * w.n2f + c0) * rowp + kHalo;
+  for (int c = 0; c < C; ++c) {
+    const T2* rp = src + (long long)c * rowp;
+    for (int j1 = threadIdx.x; j1 < L; j1 += blockDim.x) {
+      T2 v = rp[j1];
+      if (j1 < kHalo) v = cadd(v, rp[L + j1]);        // right halo holds columns 0..kHalo-1
+      if (j1 >= L - kHalo) v = cadd(v, rp[j1 - L]);   // left halo holds columns L-kHalo..L-1
+      a[c * L + j1] = v;
+    }
+  }
+  __syncthreads();
+  T2* res = smem_fft<T2>(a, b, fl, tw + fl.tw_off, C, 1, L, -1);
+  T2* dst = p1 + w.p1_off + ((long long)job.t * w.n2f + c0) * n1;
+  for (int c = 0; c < C; ++c)
+    for (int i1 = threadIdx.x; i1 < n1; i1 += blockDim.x) {
+      int pos = i1 - n1 / 2;
+      pos = pos < 0 ? pos + L : pos;
+      dst[(long long)c * n1 + i1] = res[c * L + pos];
+    }
+}
+
+// K1*: job (w, -, start, count) over box rows i1, all terms t in-CTA (deterministic sum over t).
+template <typename T2>
+__global__ void __launch_bounds__(256) k_rowpass_adj(int N, const WedgeDev* __restrict__ wedges,
+                                                     const FftJob* __restrict__ jobs, const FftLen* __restrict__ ffts,
+                                                     const T2* __restrict__ tw, const T2* const* __restrict__ betas,
+                                                     const unsigned char* const* __restrict__ masks,
+                                                     const T2* __restrict__ p1, T2* __restrict__ fhat) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const FftJob job = jobs[blockIdx.x];
+  const WedgeDev& w = wedges[job.w];
+  const FftLen& fl = ffts[w.fft2];
+  const int L = fl.L, n1 = w.n1, n2 = w.n2, cnt = job.count;
+  T2* a = reinterpret_cast<T2*>(smem_raw);
+  T2* b = a + cnt * L;
+  T2* acc = b + cnt * L;
+  for (int idx = threadIdx.x; idx < cnt * n2; idx += blockDim.x) acc[idx] = mk<T2>(0, 0);
+  const FastDiv dc = make_fastdiv_dev((unsigned)cnt);
+  for (int t = 0; t < w.q; ++t) {
+    const T2* src = p1 + w.p1_off + (long long)t * L * n1 + job.start;
+    __syncthreads();
+    for (int idx = threadIdx.x; idx < cnt * L; idx += blockDim.x) {
+      const int j2 = fdiv(idx, dc), r = idx - j2 * cnt;
+      a[r * L + j2] = src[(long long)j2 * n1 + r];
+    }
+    __syncthreads();
+    T2* res = smem_fft<T2>(a, b, fl, tw + fl.tw_off, cnt, 1, L, -1);
+    const T2* bet = betas[job.w] + ((long long)t * n1 + job.start) * n2;
+    for (int r = 0; r < cnt; ++r)
+      for (int i2 = threadIdx.x; i2 < n2; i2 += blockDim.x) {
+        const T2 bv = bet[r * n2 + i2];
+        int pos = i2 - n2 / 2;
+        pos = pos < 0 ? pos + L : pos;
+        const T2 h = res[r * L + pos];
+        T2 v = acc[r * n2 + i2];
+        v.x += bv.x * h.x + bv.y * h.y;  // conj(beta') h
+        v.y += bv.x * h.y - bv.y * h.x;
+        acc[r * n2 + i2] = v;
+      }
+  }
+  __syncthreads();
+  const unsigned char* mk_ = masks[job.w] + (long long)job.start * n2;
+  for (int r = 0; r < cnt; ++r)
+    for (int i2 = threadIdx.x; i2 < n2; i2 += blockDim.x) {
+      if (!mk_[r * n2 + i2]) continue;
+      const int kp1 = job.start + r - n1 / 2, kp2 = i2 - n2 / 2;
+      const int z1 = kp1 + w.xc1, z2 = kp2 + w.xc2;
+      const int xi1 = w.Mi[0] * z1 + w.Mi[1] * z2, xi2 = w.Mi[2] * z1 + w.Mi[3] * z2;
+      fhat[(long long)imod(xi1, N) * N + imod(xi2, N)] = acc[r * n2 + i2];
+    }
+}
+
+// fhat*(0) = sum_x conj(a0(x)) g(x): one CTA, fixed-order tree reduction in FP64.
+template <typename T2>
+__global__ void __launch_bounds__(1024) k_dc_adj(long long NN, const double2* __restrict__ a0,
+                                                 const T2* __restrict__ g, T2* __restrict__ fhat) {
+  __shared__ double sr[1024], si[1024];
+  double r = 0, im = 0;
+  for (long long x = threadIdx.x; x < NN; x += blockDim.x) {
+    const double2 d = a0[x];
+    const double gr = (double)g[x].x, gi = (double)g[x].y;
+    r += d.x * gr + d.y * gi;
+    im += d.x * gi - d.y * gr;
+  }
+  sr[threadIdx.x] = r;
+  si[threadIdx.x] = im;
+  __syncthreads();
+  for (int h = blockDim.x / 2; h > 0; h >>= 1) {
+    if (threadIdx.x < h) {
+      sr[threadIdx.x] += sr[threadIdx.x + h];
+      si[threadIdx.x] += si[threadIdx.x + h];
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) fhat[0] = mk<T2>((typename Real<T2>::type)sr[0], (typename Real<T2>::type)si[0]);
+}
+
+template <typename T2, int TAPS, int P>
+static cudaError_t launch_spread_tp(const ApplyArgs& a, int wi, const T2* g, cudaStream_t s) {
+  static int sms = 0;
+  if (sms == 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  }
+  const InterpWedge& iw = a.iw[wi];
+  int blocks = std::max(1, std::min((iw.ngroups + 127) / 128, sms * 8));
+  k_spread_groups<T2, TAPS, P><<<blocks, 128, 0, s>>>(iw, reinterpret_cast<T2*>(a.g), g, a.es_beta, *a.poly);
+  return cudaGetLastError();
+}
+
+template <typename T2>
+static cudaError_t enqueue_adjoint_t(const ApplyArgs& a, const T2* g, T2* out, cudaStream_t s, int* launches) {
+  cudaError_t e;
+  int n = 0;
+  const bool c64 = sizeof(T2) == sizeof(float2);
+  const T2* tw = reinterpret_cast<const T2*>(a.tw);
+  T2* fhat = reinterpret_cast<T2*>(a.fhat);
+  T2* tmp = reinterpret_cast<T2*>(a.tmp);
+  const long long NN = (long long)a.N * a.N;
+  if ((e = cudaMemsetAsync(fhat, 0, sizeof(T2) * NN, s)) != cudaSuccess) return e;
+  if (a.nw > 0) {
+    if ((e = cudaMemsetAsync(a.g, 0, sizeof(T2) * a.fine_elems, s)) != cudaSuccess) return e;
+    for (int wi = 0; wi < a.nw; ++wi) {
+#define FIO_SPREAD_CASE(TP)                                   \
+  case TP:                                                    \
+    e = launch_spread_tp<T2, TP, kGroupP>(a, wi, g, s);       \
+    break;
+      switch (a.taps) {
+        FIO_SPREAD_CASE(3)
+        FIO_SPREAD_CASE(4)
+        FIO_SPREAD_CASE(5)
+        FIO_SPREAD_CASE(6)
+        FIO_SPREAD_CASE(7)
+        FIO_SPREAD_CASE(8)
+        FIO_SPREAD_CASE(9)
+        FIO_SPREAD_CASE(10)
+        default: return cudaErrorInvalidValue;
+      }
+#undef FIO_SPREAD_CASE
+      if (e != cudaSuccess) return e;
+      ++n;
+    }
+    k_colpass_adj<T2><<<a.njobs_col, 256, a.smem_col, s>>>(a.wedges, a.jobs_col, a.ffts, tw,
+                                                           reinterpret_cast<const T2*>(a.g),
+                                                           reinterpret_cast<T2*>(a.p1));
+    if ((e = cudaGetLastError()) != cudaSuccess) return e;
+    ++n;
+    const T2* const* betas = reinterpret_cast<const T2* const*>(a.beta);
+    k_rowpass_adj<T2><<<a.njobs_rowadj, 256, a.smem_rowadj, s>>>(a.N, a.wedges, a.jobs_rowadj, a.ffts, tw, betas,
+                                                                a.masks, reinterpret_cast<const T2*>(a.p1), fhat);
+    if ((e = cudaGetLastError()) != cudaSuccess) return e;
+    ++n;
+  }
+  if (a.add_dc) {
+    k_dc_adj<T2><<<1, 1024, 0, s>>>(NN, a.a0, g, fhat);
+    if ((e = cudaGetLastError()) != cudaSuccess) return e;
+    ++n;
+  }
+  // K0*: out = (1/N) sum_xi e^{+2 pi i x.xi} fhat*(xi)
+  const size_t seq = fft_seq_bytes(a.N, c64);
+  int rpc = a.rows_per_cta_N;
+  k_fft_rows<T2><<<(a.N + rpc - 1) / rpc, 256, rpc * seq, s>>>(fhat, tmp, a.N, rpc, a.ffts, a.fft_N, tw, +1, 1.0);
+  if ((e = cudaGetLastError()) != cudaSuccess) return e;
+  int cpc = a.cols_per_cta_N;
+  k_fft_cols<T2><<<(a.N + cpc - 1) / cpc, 256, cpc * seq, s>>>(tmp, out, a.N, cpc, a.ffts, a.fft_N, tw, +1,
+                                                               1.0 / a.N);
+  if ((e = cudaGetLastError()) != cudaSuccess) return e;
+  n += 2;
+  if (launches) *launches = n;
+  return cudaSuccess;
+}
+
+cudaError_t enqueue_adjoint(const ApplyArgs& a, bool c64, const void* g, void* out, cudaStream_t s, int* launches) {
+  if (c64) return enqueue_adjoint_t<float2>(a, (const float2*)g, (float2*)out, s, launches);
+  return enqueue_adjoint_t<double2>(a, (const double2*)g, (double2*)out, s, launches);
+}
+
 size_t fft_seq_bytes(int L, bool c64) { return 2 * (size_t)L * (c64 ? sizeof(float2) : sizeof(double2)); }
 
 cudaError_t configure_kernels(size_t smem_bytes) {
@@ -1025,6 +1293,10 @@ cudaError_t configure_kernels(size_t smem_bytes) {
   FIO_SMEM(k_rowpass<float2>)
   FIO_SMEM(k_colpass<double2>)
   FIO_SMEM(k_colpass<float2>)
+  FIO_SMEM(k_rowpass_adj<double2>)
+  FIO_SMEM(k_rowpass_adj<float2>)
+  FIO_SMEM(k_colpass_adj<double2>)
+  FIO_SMEM(k_colpass_adj<float2>)
 #undef FIO_SMEM
   return cudaSuccess;
 }

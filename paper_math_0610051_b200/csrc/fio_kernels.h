@@ -72,6 +72,9 @@ struct ApplyArgs {
   void* g;                  // fine grids
   const FftJob* jobs_row; int njobs_row; int smem_row;
   const FftJob* jobs_col; int njobs_col; int smem_col;
+  const FftJob* jobs_rowadj; int njobs_rowadj; int smem_rowadj;  // K1* (all t per job)
+  const unsigned char* const* masks;  // per owned wedge: n1 x n2 box mask (cell is a member)
+  size_t fine_elems;        // elements of the fine-grid workspace (G, reused as G* by the adjoint)
   int rows_per_cta_N;       // K0 row pass
   int cols_per_cta_N;       // K0 column pass
 };
@@ -83,6 +86,9 @@ struct ApplyArgs {
 cudaError_t enqueue_apply(const ApplyArgs& a, bool c64, const void* f, void* Lf, cudaStream_t s, int* launches,
                           cudaEvent_t* ev = nullptr);
 constexpr int kStages = 5;
+
+// Enqueue the exact adjoint of the fast operator: out = L~* g.
+cudaError_t enqueue_adjoint(const ApplyArgs& a, bool c64, const void* g, void* out, cudaStream_t s, int* launches);
 
 // Dynamic shared memory needed by the FFT passes for one sequence of length L.
 size_t fft_seq_bytes(int L, bool c64);

@@ -168,3 +168,58 @@ def test_config4_sampled():
     err = oracle.rel_l2(out.ravel()[pts], oracle.fio(op, f, pts=pts))
     print("config4: W", plan.info["W"], "sum_q", plan.info["sum_q"], "plan s", plan.info["plan_seconds"], "err", err)
     assert err <= 10 * cfg["eps"], err
+
+
+# ------------------------------------------------------------------ adjoint
+def adjoint_ref(op, g):
+    """(L* g)(x) = (1/N) sum_xi e^{2 pi i x.xi} widehat(L* g)(xi), the hat from the oracle."""
+    return op.N * np.fft.ifft2(oracle.fio_adjoint_hat(op, g))
+
+
+def run_adj(op, g, eps=1e-6, dtype="c128", **kw):
+    plan = fio.Plan(op.N, op.c1, op.c2, op.b1, op.b2, op.px, op.pxi, eps=eps, dtype=dtype, device=0, **kw)
+    tdt = torch.complex64 if dtype == "c64" else torch.complex128
+    out = plan.apply_adjoint(torch.from_numpy(g).to(DEV, tdt))
+    torch.cuda.synchronize()
+    return plan, out.cpu().numpy().astype(np.complex128)
+
+
+@pytest.mark.parametrize("name", ["grt", "wave"])
+def test_adjoint_matches_oracle(name):
+    N = 64
+    op = wl.grt_operator(N) if name == "grt" else wl.wave_operator(N)
+    g = crandn(N, 11)
+    _, out = run_adj(op, g)
+    err = oracle.rel_l2(out, adjoint_ref(op, g))
+    assert err <= 1e-5, err
+
+
+def test_adjoint_c64_and_identity():
+    N = 64
+    op = wl.grt_operator(N)
+    g = crandn(N, 12).astype(np.complex64).astype(np.complex128)
+    _, out = run_adj(op, g, eps=1e-4, dtype="c64")
+    assert oracle.rel_l2(out, adjoint_ref(op, g)) <= 1e-3
+    _, out = run_adj(wl.identity_operator(32), crandn(32, 13))
+    assert oracle.rel_l2(out, crandn(32, 13)) <= 1e-5
+
+
+def test_adjoint_pairing_is_exact():
+    # <L~ f, g> = <f, L~* g>: the GPU adjoint is the conjugate transpose of the GPU forward
+    N = 64
+    op = wl.wave_operator(N)
+    plan = fio.Plan(N, op.c1, op.c2, px=op.px, pxi=op.pxi, eps=1e-6, device=0)
+    f, g = crandn(N, 21), crandn(N, 22)
+    Lf = plan.apply(torch.from_numpy(f).to(DEV)).cpu().numpy()
+    Lsg = plan.apply_adjoint(torch.from_numpy(g).to(DEV)).cpu().numpy()
+    lhs, rhs = np.vdot(g, Lf), np.vdot(Lsg, f)
+    assert abs(lhs - rhs) <= 1e-12 * np.linalg.norm(f) * np.linalg.norm(g) * N, (lhs, rhs)
+
+
+def test_adjoint_sharded_partials():
+    N = 64
+    op = wl.grt_operator(N)
+    g = crandn(N, 31)
+    _, full = run_adj(op, g)
+    acc = sum(run_adj(op, g, rank=r, nranks=2)[1] for r in range(2))
+    assert oracle.rel_l2(acc, full) <= 1e-12
