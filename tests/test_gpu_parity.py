@@ -223,3 +223,14 @@ def test_adjoint_sharded_partials():
     _, full = run_adj(op, g)
     acc = sum(run_adj(op, g, rank=r, nranks=2)[1] for r in range(2))
     assert oracle.rel_l2(acc, full) <= 1e-12
+
+
+@pytest.mark.parametrize("N,dtype,eps", [(96, "c128", 1e-6), (120, "c64", 1e-4), (8, "c128", 1e-6), (30, "c128", 1e-6)])
+def test_ragged_sizes_full_grid(N, dtype, eps):
+    # non-power-of-2 grids (5-smooth N, ragged K3 chunks and FFT batches, W = 8 wedges
+    # of a few cells at N = 8) against the direct sum
+    op = wl.grt_operator(N)
+    f = wl.white_noise(N, 3, dtype)
+    _, out = run(op, f, eps=eps, dtype=dtype)
+    err = oracle.rel_l2(out, oracle.fio(op, f))
+    assert err <= 10 * eps, err
