@@ -489,7 +489,7 @@ fio_status build_plan(fio_plan_s& P, const fio_phase* phase, const fio_amplitude
       std::vector<int> box;
       const int blk = c64 ? kK3BlockC64 : kK3BlockC128;
       const long long cap = chunk_boxes(anchor, blk, (P.taps + 2) & ~1, P.taps + 1,
-                                        c64 ? kK3TileCapC64 : kK3TileCapC128, box);
+                                        c64 ? kK3TileCapC64 : kK3TileCapC128, box, c64 ? 8 : 16);
       iw.nchunks = (int)(box.size() / 6);
       P.chunk_threads += (long long)iw.nchunks * blk;
       iw.tile_cap = (int)cap;

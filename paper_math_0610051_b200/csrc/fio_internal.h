@@ -129,7 +129,7 @@ void lpt_assign(int W, const double* cost, int nranks, int* owner);
 void group_points(const double* u, long long NN, int taps, int P, int n1f, int n2f, std::vector<int>& anchor,
                   std::vector<int>& slot_x, std::vector<double>& off);
 long long chunk_boxes(const std::vector<int>& anchor, int block, int win_rows, int win_cols, long long cap,
-                      std::vector<int>& box);
+                      std::vector<int>& box, int elem_bytes);
 
 // Complex helpers on interleaved doubles.
 struct cplx {
