@@ -9,7 +9,9 @@ OpenMP over output points); this module only marshals numpy arrays.
 Functions and the passages they restate:
   dft2            eq. (dft)
   fio             eq. (dfio) PAPER.md:165-168 (full grid or sampled points;
-                  optionally restricted to a wedge set = sum of L_l)
+                  optionally restricted to a wedge set = sum of L_l, PAPER.md:236-241);
+                  phases Phi_+- (op.sign) and the Bessel amplitude of eq. ellipses_amp
+                  (op.amp == "bessel", PAPER.md:1596-1603)
   wedge_of        wedges W_l PAPER.md:210-217 (W wedges, reading R1)
   nudft2          the Fourier series of evaluation step 3, PAPER.md:1299-1311
   fio_adjoint_hat widehat(L* g)(xi)
@@ -48,10 +50,10 @@ def _load():
         lib.oracle_wedge_of.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_int]
         lib.oracle_wedge_of.restype = ctypes.c_int
         lib.oracle_fio_points.argtypes = [ctypes.c_int, P, P, P, P, ctypes.c_int, P, P, P, I64, P,
-                                          ctypes.c_int, P, ctypes.c_int, P]
+                                          ctypes.c_int, P, ctypes.c_int, ctypes.c_int, ctypes.c_int, P]
         lib.oracle_nudft2.argtypes = [ctypes.c_int, ctypes.c_int, P, I64, P, P]
         lib.oracle_fio_adjoint_freq.argtypes = [ctypes.c_int, P, P, P, P, ctypes.c_int, P, P, P, I64,
-                                                P, P]
+                                                P, ctypes.c_int, ctypes.c_int, P]
         lib.oracle_num_threads.restype = ctypes.c_int
         _lib = lib
     return _lib
@@ -63,6 +65,10 @@ def _c(a, dtype):
 
 def _ptr(a):
     return None if a is None else a.ctypes.data_as(ctypes.c_void_p)
+
+
+def _amp_kind(op) -> int:
+    return 1 if getattr(op, "amp", "separable") == "bessel" else 0
 
 
 def num_threads() -> int:
@@ -110,7 +116,7 @@ def fio(op, f: Optional[np.ndarray] = None, pts: Optional[np.ndarray] = None,
     out = np.empty(pts.shape[0], dtype=np.complex128)
     _load().oracle_fio_points(N, _ptr(c1), _ptr(c2), _ptr(b1), _ptr(b2), K, _ptr(px), _ptr(pxi),
                               _ptr(fhat), pts.shape[0], _ptr(pts), int(W), _ptr(sel),
-                              int(bool(include_dc)), _ptr(out))
+                              int(bool(include_dc)), int(getattr(op, "sign", 1)), _amp_kind(op), _ptr(out))
     return out.reshape(N, N) if full else out
 
 
@@ -130,7 +136,8 @@ def fio_adjoint_hat(op, g: np.ndarray, fidx: Optional[np.ndarray] = None) -> np.
     pxi = None if K == 0 else _c(op.pxi, np.complex128)
     out = np.empty(fidx.shape[0], dtype=np.complex128)
     _load().oracle_fio_adjoint_freq(N, _ptr(c1), _ptr(c2), _ptr(b1), _ptr(b2), K, _ptr(px),
-                                    _ptr(pxi), _ptr(g), fidx.shape[0], _ptr(fidx), _ptr(out))
+                                    _ptr(pxi), _ptr(g), fidx.shape[0], _ptr(fidx),
+                                    int(getattr(op, "sign", 1)), _amp_kind(op), _ptr(out))
     return out.reshape(N, N) if full else out
 
 

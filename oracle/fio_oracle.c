@@ -26,9 +26,14 @@
  *                      widehat(L* g)(xi) = (1/N) sum_y conj(a(y,xi)) e^{-2 pi i Phi(y,xi)} g(y).
  *
  * The operator family (the phase and amplitude are DATA, given on the grids):
- *     Phi(x,xi) = x.xi + b(x).xi + sqrt(c1(x)^2 xi1^2 + c2(x)^2 xi2^2)
- *     a(x,xi)   = sum_k px_k(x) pxi_k(xi)      (K = 0  ->  a == 1, the Egorov
+ *     Phi(x,xi) = x.xi + b(x).xi + s rho(x,xi),  rho = sqrt(c1(x)^2 xi1^2 + c2(x)^2 xi2^2),
+ *                 s = +1 or -1 (Phi_+- of PAPER.md:1600-1603)
+ *     a(x,xi)   = sum_k px_k(x) pxi_k(xi)      (amp_kind 0; K = 0  ->  a == 1, the Egorov
  *                                                operator of PAPER.md:972-977)
+ *     a(x,xi)   = (1/4pi) (J0(2 pi rho_e) + s i Y0(2 pi rho_e)) e^{-s 2 pi i rho_e}
+ *                 (amp_kind 1: eq. ellipses_amp, the Appendix
+ *                  split 2 J0 = (J0 + iY0) + (J0 - iY0)), with the
+ *                  regularisation rho_e = max(rho, 1/2) (reading R22)
  * This covers every phase used by the paper's experiments with elliptic radii
  * (eq. nrphase; the wave phase x.xi +- c|xi|t,
  * PAPER.md:94-97) and all five BASELINE.json configurations.
@@ -43,6 +48,7 @@
  * fractional part before the multiplication by 2 pi.  Sums are plain FP64 in
  * a fixed order (xi1 outer, xi2 inner) per output point.
  */
+#define _DEFAULT_SOURCE 1
 #include <math.h>
 #include <stdint.h>
 #include <stdlib.h>
@@ -51,6 +57,18 @@
 #endif
 
 static const double TWO_PI = 6.283185307179586476925286766559;
+
+/* amplitude of eq. ellipses_amp at radius rho, phase sign s */
+static void bessel_amp(double rho, int s, double* ar, double* ai) {
+    const double PI = 3.14159265358979323846264338327950288;
+    double re = rho < 0.5 ? 0.5 : rho;
+    double J = j0(TWO_PI * re), Y = y0(TWO_PI * re);
+    double fr = re - floor(re);
+    double c = cos(TWO_PI * fr), sn = -(double)s * sin(TWO_PI * fr); /* e^{-s 2 pi i re} */
+    /* (J + s i Y)(c + i sn) / (4 pi) */
+    *ar = (J * c - (double)s * Y * sn) / (4.0 * PI);
+    *ai = (J * sn + (double)s * Y * c) / (4.0 * PI);
+}
 
 static inline int freq_of_index(int k, int N) { return k >= N / 2 ? k - N : k; }
 
@@ -131,7 +149,8 @@ int oracle_wedge_of(int W, int xi1, int xi2) {
 void oracle_fio_points(int N, const double* c1, const double* c2, const double* b1,
                        const double* b2, int K, const double* px, const double* pxi,
                        const double* fhat, int64_t npts, const int64_t* pts, int W,
-                       const int* wedge_sel, int include_dc, double* out) {
+                       const int* wedge_sel, int include_dc, int rho_sign, int amp_kind,
+                       double* out) {
     int* wsel = NULL;
     if (wedge_sel) {
         /* per-frequency selection mask, FFT-natural order */
@@ -161,14 +180,16 @@ void oracle_fio_points(int N, const double* c1, const double* c2, const double* 
                 if (m < 0) m += N;
                 /* b(x).xi + rho(x,xi), reduced to its fractional part */
                 double rho = sqrt(C1 * C1 * (double)x1 * (double)x1 + C2 * C2 * (double)x2 * (double)x2);
-                double s = B1 * (double)x1 + B2 * (double)x2 + rho;
+                double s = B1 * (double)x1 + B2 * (double)x2 + (double)rho_sign * rho;
                 s -= floor(s);
                 double ph = (double)m / (double)N + s;
                 ph -= floor(ph);
                 double cr = cos(TWO_PI * ph), ci = sin(TWO_PI * ph);
                 /* amplitude a(x,xi) = sum_k px_k(x) pxi_k(xi) */
                 double ar = 1.0, ai = 0.0;
-                if (K > 0) {
+                if (amp_kind == 1) {
+                    bessel_amp(rho, rho_sign, &ar, &ai);
+                } else if (K > 0) {
                     ar = 0.0;
                     for (int k = 0; k < K; ++k) {
                         const double* pxk = px + 2 * (size_t)k * N * N;
@@ -225,7 +246,8 @@ void oracle_nudft2(int n1, int n2, const double* coeffs, int64_t npts, const dou
  * at the FFT-natural frequency indices fidx[p] = k1*N+k2. */
 void oracle_fio_adjoint_freq(int N, const double* c1, const double* c2, const double* b1,
                              const double* b2, int K, const double* px, const double* pxi,
-                             const double* g, int64_t nfreq, const int64_t* fidx, double* out) {
+                             const double* g, int64_t nfreq, const int64_t* fidx, int rho_sign,
+                             int amp_kind, double* out) {
 #pragma omp parallel for schedule(dynamic, 1)
     for (int64_t p = 0; p < nfreq; ++p) {
         int64_t fi = fidx[p];
@@ -239,13 +261,15 @@ void oracle_fio_adjoint_freq(int N, const double* c1, const double* c2, const do
                 double C1 = c1[idx], C2 = c2[idx];
                 double B1 = b1 ? b1[idx] : 0.0, B2 = b2 ? b2[idx] : 0.0;
                 double rho = sqrt(C1 * C1 * (double)x1 * (double)x1 + C2 * C2 * (double)x2 * (double)x2);
-                double s = B1 * (double)x1 + B2 * (double)x2 + rho;
+                double s = B1 * (double)x1 + B2 * (double)x2 + (double)rho_sign * rho;
                 s -= floor(s);
                 double ph = (double)m / (double)N + s;
                 ph -= floor(ph);
                 double cr = cos(TWO_PI * ph), ci = -sin(TWO_PI * ph); /* e^{-2 pi i Phi} */
                 double ar = 1.0, ai = 0.0;
-                if (K > 0) {
+                if (amp_kind == 1) {
+                    bessel_amp(rho, rho_sign, &ar, &ai);
+                } else if (K > 0) {
                     ar = 0.0;
                     for (int k = 0; k < K; ++k) {
                         const double* pxk = px + 2 * (size_t)k * N * N;

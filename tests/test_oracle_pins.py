@@ -262,3 +262,63 @@ def test_workload_inputs_deterministic():
     assert g.shape == (64, 64) and np.abs(g).max() > 0.1
     p = wl.sample_points(1024, 4096, 1)
     assert len(np.unique(p)) == 4096 and np.all(np.diff(p) > 0)
+
+
+# ------------------------------------------------------------------ Bessel amplitude (Appendix)
+def circle_average_kernel(rho, nth=256):
+    """(1/4 pi^2) int_0^{2 pi} e^{2 pi i rho cos th} d th by the trapezoid rule (spectrally accurate):
+    the Appendix kernel (1/2 pi) J0(2 pi rho) obtained WITHOUT a Bessel routine."""
+    th = 2 * np.pi * np.arange(nth) / nth
+    rho = np.asarray(rho, float)
+    return np.exp(2j * np.pi * rho[..., None] * np.cos(th)).mean(-1) * (2 * np.pi) / (4 * np.pi ** 2)
+
+
+def test_bessel_pair_sums_to_circle_average():
+    # Appendix: a_+ e^{2 pi i rho} + a_- e^{-2 pi i rho} = (1/2 pi) J0(2 pi rho), so L_+ + L_- is the
+    # circle-average operator for every frequency with rho >= 1/2 (reading R22 clamps below 1/2).
+    # catches: wrong Y0 sign, wrong e^{-+2 pi i rho} factor, wrong 1/4 pi, wrong J0 argument
+    N = 24
+    f = crandn(N, N)
+    fh = np.fft.fft2(f) / N
+    xi1, xi2 = wl.freqs(N)
+    fh[np.hypot(xi1, xi2) < 3] = 0          # r >= 1/4 below: rho >= 3/4 on the support
+    lp, lm = wl.bessel_grt_operator(N, +1), wl.bessel_grt_operator(N, -1)
+    out = oracle.fio(lp, fhat=fh) + oracle.fio(lm, fhat=fh)
+    x1, x2 = wl.grid(N)
+    ref = np.zeros((N, N), complex)
+    for i in range(N):
+        for j in range(N):
+            rho = lp.c1[i, j] * np.hypot(xi1, xi2)
+            ker = circle_average_kernel(rho) * np.exp(2j * np.pi * (x1[i, j] * xi1 + x2[i, j] * xi2))
+            ref[i, j] = (ker * fh).sum() / N
+    np.testing.assert_allclose(out, ref, atol=1e-12 * np.abs(ref).max())
+
+
+def test_bessel_single_mode_asymptotics():
+    # f_hat = delta_xi0 with rho = r |xi0| large: a_+(rho) -> (1/4 pi) sqrt(1/(pi^2 rho)) e^{-i pi/4}
+    # (H0^(1)(z) ~ sqrt(2/(pi z)) e^{i(z - pi/4)}, PAPER.md:1926-1933); checks the sign of Y0 and of
+    # the demodulating exponential separately from the pair identity
+    N = 64
+    op = wl.bessel_grt_operator(N, +1)
+    fh = np.zeros((N, N), complex)
+    xi0 = (24, -17)
+    fh[xi0[0] % N, xi0[1] % N] = 1.0
+    out = oracle.fio(op, fhat=fh)
+    x1, x2 = wl.grid(N)
+    rho = op.c1 * np.hypot(*xi0)
+    amp = N * out * np.exp(-2j * np.pi * (x1 * xi0[0] + x2 * xi0[1] + rho))
+    asym = np.exp(-1j * np.pi / 4) / (4 * np.pi * np.pi * np.sqrt(rho))
+    assert np.max(np.abs(amp / asym - 1)) < 2e-2      # leading term, rho in [7, 30]
+    om = wl.bessel_grt_operator(N, -1)
+    out_m = oracle.fio(om, fhat=fh)
+    amp_m = N * out_m * np.exp(-2j * np.pi * (x1 * xi0[0] + x2 * xi0[1] - rho))
+    np.testing.assert_allclose(amp_m, np.conj(amp), rtol=1e-12)   # a_- = conj(a_+) for real rho
+
+
+def test_bessel_dc_term_uses_clamped_radius():
+    # reading R22: rho_e = max(rho, 1/2); at xi = 0 the pair sums to -(1/2 pi) J0(pi) / N
+    N = 16
+    fh = np.zeros((N, N), complex)
+    fh[0, 0] = 1.0
+    s = oracle.fio(wl.bessel_grt_operator(N, +1), fhat=fh) + oracle.fio(wl.bessel_grt_operator(N, -1), fhat=fh)
+    np.testing.assert_allclose(s, -circle_average_kernel(0.5) / N * np.ones((N, N)), rtol=1e-12)

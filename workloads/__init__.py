@@ -29,7 +29,7 @@ import numpy as np
 __all__ = [
     "Operator", "CONFIGS", "config", "grid", "freqs", "grt_operator", "wave_operator",
     "identity_operator", "const_ellipse_operator", "shift_operator", "paper_ellipse_operator",
-    "white_noise", "gaussian_bumps", "sample_points", "make_operator", "make_input",
+    "white_noise", "gaussian_bumps", "sample_points", "make_operator", "make_input", "bessel_grt_operator",
 ]
 
 
@@ -45,6 +45,8 @@ class Operator:
     px: Optional[np.ndarray] = None   # (K, N, N) complex128, spatial factors
     pxi: Optional[np.ndarray] = None  # (K, N, N) complex128, frequency factors, FFT order
     name: str = ""
+    sign: int = 1                     # Phi = x.xi + b.xi + sign * rho (Phi_+- of PAPER.md:1600-1603)
+    amp: str = "separable"            # "separable" (px, pxi) or "bessel" (eq. ellipses_amp)
 
     @property
     def K(self) -> int:
@@ -135,6 +137,14 @@ def paper_ellipse_operator(N: int) -> Operator:
     r1 = (2 + np.sin(4 * np.pi * x1)) * (2 + np.sin(4 * np.pi * x2)) / 9.0
     r2 = (2 + np.cos(4 * np.pi * x1)) * (2 + np.cos(4 * np.pi * x2)) / 9.0
     return Operator(N, r1, r2, name="paper_ellipse")
+
+
+def bessel_grt_operator(N: int, sign: int = 1) -> Operator:
+    """L_+ (sign = 1) or L_- of the circle-averaging GRT: Phi_+- = x.xi +- r(x)|xi|,
+    r = (3 + sin 4pi x1)(3 + sin 4pi x2)/16 (eq. circlerad), amplitude a_+- of eq. ellipses_amp."""
+    x1, x2 = grid(N)
+    r = (3 + np.sin(4 * np.pi * x1)) * (3 + np.sin(4 * np.pi * x2)) / 16.0
+    return Operator(N, r, r.copy(), name=f"bessel_grt{'+' if sign > 0 else '-'}", sign=int(sign), amp="bessel")
 
 
 def make_operator(cfg: dict) -> Operator:
