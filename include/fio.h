@@ -58,7 +58,8 @@ typedef enum {
 } fio_status;
 
 /* The phase, PAPER.md:54-61 (homogeneous of degree 1 in xi), given as data on X:
- *     Phi(x,xi) = x.xi + b(x).xi + sqrt(c1(x)^2 xi1^2 + c2(x)^2 xi2^2).
+ *     Phi(x,xi) = x.xi + b(x).xi + s rho(x,xi),  rho = sqrt(c1(x)^2 xi1^2 + c2(x)^2 xi2^2),
+ * s = rho_sign in {+1, -1} (0 means +1): Phi_+- of PAPER.md:1600-1603.
  * This family contains the identity (c = b = 0), the wave
  * propagator x.xi +- c|xi|t (c1 = c2 = c t), the paper's
  * ellipse phases (eq. nrphase) and every BASELINE config.
@@ -69,10 +70,17 @@ typedef struct {
   const double* c2;
   const double* b1;
   const double* b2;
+  int rho_sign;
 } fio_phase;
 
-/* The amplitude (order-0 symbol), rank-K separable on the grids:
- *     a(x,xi) = sum_{k<K} px_k(x) pxi_k(xi).
+typedef enum { FIO_AMP_SEPARABLE = 0, FIO_AMP_BESSEL_GRT = 1 } fio_amp_kind;
+
+/* The amplitude (order-0 symbol).
+ * kind FIO_AMP_SEPARABLE: rank-K separable on the grids, a(x,xi) = sum_{k<K} px_k(x) pxi_k(xi).
+ * kind FIO_AMP_BESSEL_GRT (K = 0): the ellipse-GRT amplitude of eq. ellipses_amp
+ *     a(x,xi) = (1/4 pi)(J0(2 pi rho_e) + s i Y0(2 pi rho_e)) e^{-s 2 pi i rho_e},
+ *     rho_e = max(rho(x,xi), 1/2) (reading R22), rho and s from the phase
+ *     (with r1 = r2 = r of eq. circlerad it is the paper's Table tbl:result_b).
  * K = 0 (px = pxi = NULL) is a == 1, the Egorov operator of PAPER.md:972-977.
  * px: K*N*N interleaved complex doubles over X; pxi: K*N*N over Omega in FFT
  * order.  Copied during fio_plan.  The amplitude is folded into the separated
@@ -81,6 +89,7 @@ typedef struct {
   int K;
   const double* px;
   const double* pxi;
+  int kind;
 } fio_amplitude;
 
 /* Options; fio_default_opts() fills the defaults shown. */

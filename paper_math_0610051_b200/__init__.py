@@ -45,11 +45,12 @@ class FioError(RuntimeError):
 
 
 class _Phase(ctypes.Structure):
-    _fields_ = [("c1", ctypes.c_void_p), ("c2", ctypes.c_void_p), ("b1", ctypes.c_void_p), ("b2", ctypes.c_void_p)]
+    _fields_ = [("c1", ctypes.c_void_p), ("c2", ctypes.c_void_p), ("b1", ctypes.c_void_p), ("b2", ctypes.c_void_p),
+                ("rho_sign", ctypes.c_int)]
 
 
 class _Amp(ctypes.Structure):
-    _fields_ = [("K", ctypes.c_int), ("px", ctypes.c_void_p), ("pxi", ctypes.c_void_p)]
+    _fields_ = [("K", ctypes.c_int), ("px", ctypes.c_void_p), ("pxi", ctypes.c_void_p), ("kind", ctypes.c_int)]
 
 
 class _Opts(ctypes.Structure):
@@ -179,7 +180,8 @@ class Plan:
     def __init__(self, N: int, c1, c2, b1=None, b2=None, px=None, pxi=None, eps: float = 1e-6,
                  dtype: str = "c128", n_wedges: int = 0, nufft_w: int = 0, nufft_beta: float = 0.0,
                  seed: int = 0x5EED, device: Optional[int] = None, rank: int = 0, nranks: int = 1,
-                 r_init: int = 32, r_max: int = 512, certify: bool = True):
+                 r_init: int = 32, r_max: int = 512, certify: bool = True, rho_sign: int = 1,
+                 amplitude: str = "separable"):
         import torch
         if not torch.cuda.is_available():
             raise FioError(-3, "no CUDA device: the FIO apply runs only on the GPU (no CPU fallback)")
@@ -195,10 +197,12 @@ class Plan:
         for k in keep:
             if k is not None and k.size != N * N:
                 raise FioError(-1, "phase arrays must have N*N entries")
-        ph = _Phase(*[_ptr(k) for k in keep])
+        ph = _Phase(*[_ptr(k) for k in keep], -1 if rho_sign < 0 else 1)
         pxa, pxia = _c128(px), _c128(pxi)
         K = 0 if pxa is None else int(pxa.reshape(-1, N * N).shape[0])
-        amp = _Amp(K, _ptr(pxa), _ptr(pxia))
+        if amplitude not in ("separable", "bessel"):
+            raise FioError(-1, "amplitude must be 'separable' or 'bessel'")
+        amp = _Amp(K, _ptr(pxa), _ptr(pxia), 1 if amplitude == "bessel" else 0)
         o = _Opts()
         lib.fio_default_opts(ctypes.byref(o))
         o.dtype = FIO_C64 if self.c64 else FIO_C128

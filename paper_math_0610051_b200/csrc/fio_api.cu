@@ -6,6 +6,7 @@
 #include <chrono>
 #include <cmath>
 #include <cstdlib>
+#include <math.h>
 #include <cstring>
 #include <map>
 #include <string>
@@ -396,8 +397,16 @@ fio_status build_plan(fio_plan_s& P, const fio_phase* phase, const fio_amplitude
   if (phase->b2) FIO_CUDA(P.upload(const_cast<double**>(&P.op.b2), phase->b2, NN));
   P.op.N = N;
   P.op.K = amp ? amp->K : 0;
+  P.op.sign = phase->rho_sign < 0 ? -1 : 1;
+  P.op.amp_kind = amp ? amp->kind : FIO_AMP_SEPARABLE;
   std::vector<double2> a0(NN);
-  if (P.op.K > 0) {
+  if (P.op.amp_kind == FIO_AMP_BESSEL_GRT) {
+    // a(x, 0) at rho_e = 1/2 (reading R22): (J0(pi) + s i Y0(pi)) e^{-s i pi} / (4 pi), x-independent
+    const double PI = 3.14159265358979323846;
+    const double J = ::j0(PI), Y = ::y0(PI), sg = P.op.sign;
+    const double re = -J / (4.0 * PI), im = -sg * Y / (4.0 * PI);
+    for (long long x = 0; x < NN; ++x) a0[x] = make_double2(re / N, im / N);
+  } else if (P.op.K > 0) {
     const double2* px = reinterpret_cast<const double2*>(amp->px);
     const double2* pxi = reinterpret_cast<const double2*>(amp->pxi);
     FIO_CUDA(P.upload(const_cast<double2**>(&P.op.px), px, (size_t)P.op.K * NN));
@@ -698,6 +707,14 @@ fio_status fio_plan(fio_handle* out, int N, const fio_phase* phase, const fio_am
   }
   if (amp && amp->K < 0) {
     set_error("fio_plan: amplitude rank K must be >= 0");
+    return FIO_EINVAL;
+  }
+  if (amp && amp->kind != FIO_AMP_SEPARABLE && amp->kind != FIO_AMP_BESSEL_GRT) {
+    set_error("fio_plan: unknown amplitude kind");
+    return FIO_EINVAL;
+  }
+  if (amp && amp->kind == FIO_AMP_BESSEL_GRT && amp->K != 0) {
+    set_error("fio_plan: the Bessel amplitude takes K = 0");
     return FIO_EINVAL;
   }
   if (amp && amp->K > 0 && (!amp->px || !amp->pxi)) {

@@ -249,8 +249,7 @@ double es_poly_fit(int w, double beta, double tol, EsPoly& out) {
 // relative l2 at sigma = 2, beta = 2.3 w) stays below ~2 eps.
 int taps_for_eps(double eps) {
   int w = (int)std::ceil(-std::log10(2.0 * eps)) + 1;
-  if (eps >= 2e-3) w = 3;
-  return std::min(std::max(w, 3), kMaxTaps);
+  return std::min(std::max(w, 4), kMaxTaps);  // w = 3 is ~1e-2 accurate: never chosen
 }
 
 // Longest-processing-time greedy: wedges by decreasing cost, each to the least

@@ -72,7 +72,7 @@ __device__ __forceinline__ void warped_point(const OperatorDev& op, int n1, int 
   double c1 = op.c1[x], c2 = op.c2[x];
   double gr1, gr2;
   grad_rho(c1, c2, w.u1, w.u2, gr1, gr2);
-  double g1 = (double)n1 / N + gr1, g2 = (double)n2 / N + gr2;
+  double g1 = (double)n1 / N + op.sign * gr1, g2 = (double)n2 / N + op.sign * gr2;
   if (op.b1) g1 += op.b1[x];
   if (op.b2) g2 += op.b2[x];
   y1 = (double)w.Mi[0] * g1 + (double)w.Mi[2] * g2;
@@ -90,12 +90,22 @@ __device__ double2 kernel_entry(const OperatorDev& op, int x, int kf, double u1,
   double g1, g2;
   grad_rho(c1, c2, u1, u2, g1, g2);
   double rho = sqrt(c1 * c1 * xi1 * xi1 + c2 * c2 * xi2 * xi2);
-  double ph = rho - g1 * xi1 - g2 * xi2;
+  double ph = op.sign * (rho - g1 * xi1 - g2 * xi2);
   ph -= floor(ph);
   double s, c;
   sincospi(2.0 * ph, &s, &c);
   double2 e = make_double2(c, s);
-  if (op.K > 0) {
+  if (op.amp_kind == FIO_AMP_BESSEL_GRT) {
+    // eq. ellipses_amp, rho_e = max(rho, 1/2) (reading R22)
+    const double re = rho < 0.5 ? 0.5 : rho;
+    const double J = j0(6.283185307179586476925286766559 * re), Y = y0(6.283185307179586476925286766559 * re);
+    double fr = re - floor(re), sn, cs;
+    sincospi(2.0 * fr, &sn, &cs);
+    sn = -op.sign * sn;  // e^{-s 2 pi i rho_e}
+    const double inv4pi = 0.079577471545947667884;
+    const double2 a = make_double2((J * cs - op.sign * Y * sn) * inv4pi, (J * sn + op.sign * Y * cs) * inv4pi);
+    e = cmul(a, e);
+  } else if (op.K > 0) {
     double2 a = make_double2(0.0, 0.0);
     const long long NN = (long long)N * N;
     for (int k = 0; k < op.K; ++k) a = cadd(a, cmul(op.px[k * NN + x], op.pxi[k * NN + kf]));

@@ -16,6 +16,8 @@ struct OperatorDev {
   int K;
   const double2* px;  // K x N*N
   const double2* pxi; // K x N*N (FFT order)
+  int sign;           // Phi = x.xi + b.xi + sign * rho
+  int amp_kind;       // FIO_AMP_SEPARABLE / FIO_AMP_BESSEL_GRT
 };
 
 // ---- plan-time kernels (FP64) ----
