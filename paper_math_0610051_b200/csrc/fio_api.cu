@@ -477,7 +477,7 @@ fio_status build_plan(fio_plan_s& P, const fio_phase* phase, const fio_amplitude
       for (long long x = 0; x < NN; ++x) std::swap(uh[2 * x], uh[2 * x + 1]);  // (K3 row, column) = (u2, u1)
       std::vector<int> anchor, slot_x;
       std::vector<double> off;
-      group_points(uh.data(), NN, P.taps, kGroupP, g.n2f, g.n1f, anchor, slot_x, off);
+      group_points(uh.data(), NN, P.taps, group_p(c64), g.n2f, g.n1f, anchor, slot_x, off);
       iw.ngroups = (int)(anchor.size() / 2);
       int* d_anchor = nullptr;
       int* d_slot = nullptr;
@@ -508,7 +508,7 @@ fio_status build_plan(fio_plan_s& P, const fio_phase* phase, const fio_amplitude
       P.max_tile_cap = std::max(P.max_tile_cap, cap);
       P.meta_bytes += anchor.size() * 4 + slot_x.size() * 4 + off.size() * (c64 ? 4 : 8);
     }
-    const long long nslots = (long long)iw.ngroups * kGroupP;
+    const long long nslots = (long long)iw.ngroups * group_p(c64);
     void* alpha = nullptr;
     void* betap = nullptr;
     FIO_CUDA(P.alloc(&alpha, cs * (size_t)q * nslots));

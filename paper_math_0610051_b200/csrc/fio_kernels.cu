@@ -726,9 +726,12 @@ __device__ __forceinline__ void load_row(const T2* p, T2 (&v)[WIN]) {
 }
 template <typename Rt, int P>
 __device__ __forceinline__ void load_p1(const Rt* p, Rt (&w)[P]) {
-  if constexpr (sizeof(Rt) == 4 && P == 4) {
-    float4 a = *reinterpret_cast<const float4*>(p);
-    w[0] = a.x; w[1] = a.y; w[2] = a.z; w[3] = a.w;
+  if constexpr (sizeof(Rt) == 4 && P % 4 == 0) {
+#pragma unroll
+    for (int k = 0; k < P; k += 4) {
+      float4 a = *reinterpret_cast<const float4*>(p + k);
+      w[k] = a.x; w[k + 1] = a.y; w[k + 2] = a.z; w[k + 3] = a.w;
+    }
   } else if constexpr (sizeof(Rt) == 8 && P % 2 == 0) {
 #pragma unroll
     for (int k = 0; k < P; k += 2) {
@@ -753,6 +756,10 @@ template <> struct OffT<double2> { using type = double2; };
 // wedge, + the DC term of rank 0) or read-modify-written: each point occurs in
 // exactly one group per wedge, so one launch per wedge is race-free and the
 // summation order over wedges is fixed (deterministic).
+template <typename T2> struct GroupP;
+template <> struct GroupP<float2> { static constexpr int value = kGroupPC64; };
+template <> struct GroupP<double2> { static constexpr int value = kGroupPC128; };
+
 template <typename T2> struct K3Cfg;
 template <> struct K3Cfg<float2> {
   static constexpr int BLOCK = kK3BlockC64, MINB = 2;
@@ -1020,7 +1027,7 @@ static cudaError_t launch_interp(const ApplyArgs& a, T2* Lf, cudaStream_t s, int
     cudaError_t e;
 #define FIO_GROUPS_CASE(TP)                                            \
   case TP:                                                             \
-    e = launch_groups_tp<T2, TP, kGroupP>(a, wi, Lf, s);               \
+    e = launch_groups_tp<T2, TP, GroupP<T2>::value>(a, wi, Lf, s);     \
     break;
     switch (a.taps) {
       FIO_GROUPS_CASE(3)
@@ -1248,7 +1255,7 @@ static cudaError_t enqueue_adjoint_t(const ApplyArgs& a, const T2* g, T2* out, c
     for (int wi = 0; wi < a.nw; ++wi) {
 #define FIO_SPREAD_CASE(TP)                                   \
   case TP:                                                    \
-    e = launch_spread_tp<T2, TP, kGroupP>(a, wi, g, s);       \
+    e = launch_spread_tp<T2, TP, GroupP<T2>::value>(a, wi, g, s); \
     break;
       switch (a.taps) {
         FIO_SPREAD_CASE(3)

@@ -65,7 +65,7 @@ struct ApplyArgs {
   OperatorDev op;
   const double2* a0;        // a(x,0)/N, N*N
   int add_dc;
-  int taps;                 // w (K3 template), groups of kGroupP points
+  int taps;                 // w (K3 template), groups of group_p(dtype) points
   double es_beta;
   const EsPoly* poly;       // host pointer: piecewise-polynomial kernel (c128 K3 weights)
   void* fhat;               // N*N workspace
