@@ -1058,6 +1058,13 @@ static cudaError_t launch_interp(const ApplyArgs& a, T2* Lf, cudaStream_t s, int
 // K3* accumulates with global RED atomics (native on sm_100a; the shared-memory float atomic
 // is a CAS loop), so its summation order -- and the last bits of the adjoint -- can vary
 // from run to run.
+// one vector RED (REDG.E.ADD.F32x2) for complex64; two FP64 REDs for complex128
+__device__ __forceinline__ void red_add(float2* p, float2 v) { atomicAdd(p, v); }
+__device__ __forceinline__ void red_add(double2* p, double2 v) {
+  atomicAdd(&p->x, v.x);
+  atomicAdd(&p->y, v.y);
+}
+
 template <typename T2, int TAPS, int P>
 __global__ void __launch_bounds__(128) k_spread_groups(InterpWedge iw, T2* __restrict__ gstar,
                                                        const T2* __restrict__ g, double es_beta, EsPoly poly) {
@@ -1105,8 +1112,7 @@ __global__ void __launch_bounds__(128) k_spread_groups(InterpWedge iw, T2* __res
           T2 v = mk<T2>(0, 0);
 #pragma unroll
           for (int k = 0; k < P; ++k) v = cfma_real(p2[k][j], e[k], v);
-          atomicAdd(&rp[j].x, v.x);
-          atomicAdd(&rp[j].y, v.y);
+          red_add(rp + j, v);
         }
         rp += (r + 1 == n1f) ? -(long long)(n1f - 1) * n2p : (long long)n2p;
         r = (r + 1 == n1f) ? 0 : r + 1;
