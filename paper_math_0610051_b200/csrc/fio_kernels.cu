@@ -764,11 +764,13 @@ template <typename T2> struct K3Cfg;
 template <> struct K3Cfg<float2> {
   static constexpr int BLOCK = kK3BlockC64, MINB = 2;
   static constexpr bool P1REG = false;  // row weights in registers measured slower (4.28 vs 3.69 ms)
+  static constexpr bool LEAN = false;   // lean-register variant measured slower (4.19 vs 3.68 ms)
   static constexpr int MAXC = kK3TileCapC64 / 2 / kK3BlockC64;  // 16-B tile-copy slots per thread
 };
 template <> struct K3Cfg<double2> {
   static constexpr int BLOCK = kK3BlockC128, MINB = 2;
   static constexpr bool P1REG = false;  // 64 more FP64 registers would not fit
+  static constexpr bool LEAN = false;
   static constexpr int MAXC = kK3TileCapC128 / 1 / kK3BlockC128;
 };
 
@@ -837,21 +839,25 @@ __global__ void __launch_bounds__(K3Cfg<T2>::BLOCK, K3Cfg<T2>::MINB)
     // this thread's share of a tile copy, fixed for the chunk: source offsets within G_lt
     // (row wrapped mod n1f) and destination offsets within the tile
     constexpr int MAXC = K3Cfg<T2>::MAXC;  // = tile_cap / EPC / BLOCK
-    int csrc[MAXC];
-    int cdst[MAXC];
+    constexpr bool LEAN = K3Cfg<T2>::LEAN;
+    int csrc[LEAN ? 1 : MAXC];
+    int cdst[LEAN ? 1 : MAXC];
     int ncp = 0;
+    const FastDiv dcpr = make_fastdiv_dev((unsigned)cpr);
+    if constexpr (!LEAN) {
 #pragma unroll
-    for (int u = 0; u < MAXC; ++u) {
-      const int idx = threadIdx.x + u * BLOCK;
-      csrc[u] = 0;
-      cdst[u] = 0;
-      if (idx < tchunks) {
-        const int rr = idx / cpr, cc = idx - rr * cpr;
-        int r = bx.x + rr;
-        r = r < 0 ? r + n1f : (r >= n1f ? r - n1f : r);
-        csrc[u] = r * n2p + bx.y + cc * EPC;
-        cdst[u] = rr * bx.w + cc * EPC;
-        ncp = u + 1;
+      for (int u = 0; u < MAXC; ++u) {
+        const int idx = threadIdx.x + u * BLOCK;
+        csrc[u] = 0;
+        cdst[u] = 0;
+        if (idx < tchunks) {
+          const int rr = idx / cpr, cc = idx - rr * cpr;
+          int r = bx.x + rr;
+          r = r < 0 ? r + n1f : (r >= n1f ? r - n1f : r);
+          csrc[u] = r * n2p + bx.y + cc * EPC;
+          cdst[u] = rr * bx.w + cc * EPC;
+          ncp = u + 1;
+        }
       }
     }
     // stage term t into ring slot t % S: this thread's alpha'(t) and its share of the tile
@@ -866,9 +872,18 @@ __global__ void __launch_bounds__(K3Cfg<T2>::BLOCK, K3Cfg<T2>::MINB)
         }
         const T2* __restrict__ gt = G + t * gstride;
         T2* tile = tring + st * cap;
+        if constexpr (LEAN) {
+          for (int idx = threadIdx.x; idx < tchunks; idx += BLOCK) {
+            const int rr = fdiv(idx, dcpr), cc = idx - rr * cpr;
+            int r = bx.x + rr;
+            r = r < 0 ? r + n1f : (r >= n1f ? r - n1f : r);
+            cp_async16(tile + rr * bx.w + cc * EPC, gt + (r * n2p + bx.y + cc * EPC));
+          }
+        } else {
 #pragma unroll
-        for (int u = 0; u < MAXC; ++u)
-          if (u < ncp) cp_async16(tile + cdst[u], gt + csrc[u]);
+          for (int u = 0; u < MAXC; ++u)
+            if (u < ncp) cp_async16(tile + cdst[u], gt + csrc[u]);
+        }
       }
       cp_async_commit();
     };
@@ -906,7 +921,8 @@ __global__ void __launch_bounds__(K3Cfg<T2>::BLOCK, K3Cfg<T2>::MINB)
         for (int i = 0; i < WINR; ++i) p1s[(i * BLOCK + threadIdx.x) * P + k] = w1[i];
         // start the read of the running sum early (latency hidden by the term loop)
         base[k] = mk<T2>(0, 0);
-        if (xs[k] >= 0 && !first) base[k] = Lf[xs[k]];
+        if constexpr (!K3Cfg<T2>::LEAN)
+          if (xs[k] >= 0 && !first) base[k] = Lf[xs[k]];
       }
     }
     const int woff = a1 * bx.w + a2;
@@ -952,10 +968,10 @@ __global__ void __launch_bounds__(K3Cfg<T2>::BLOCK, K3Cfg<T2>::MINB)
     cp_async_wait<0>();
 #pragma unroll
     for (int k = 0; k < P; ++k) {
-      const int x = xs[k];
+      const int x = K3Cfg<T2>::LEAN ? (valid ? iw.slot_x[g * P + k] : -1) : xs[k];
       if (x < 0) continue;
       T2 b0;
-      if constexpr (P1REG) {
+      if constexpr (P1REG || K3Cfg<T2>::LEAN) {
         b0 = first ? mk<T2>(0, 0) : Lf[x];
       } else {
         b0 = base[k];
