@@ -157,6 +157,7 @@ typedef struct {
   long long slots;        /* sum over owned wedges of the padded K3 group slots */
   long long max_tile_cap; /* largest K3 chunk footprint (fine-grid elements) */
   long long k3_thread_slots; /* K3 chunks x threads per CTA (slots / P / this = thread fill) */
+  double rank_balance;    /* predicted max/mean per-rank cost of the wedge assignment (1 if nranks = 1) */
 } fio_info;
 
 fio_status fio_plan_info(fio_handle h, fio_info* info);

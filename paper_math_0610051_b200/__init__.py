@@ -69,7 +69,8 @@ class _Info(ctypes.Structure):
                 ("workspace_bytes", ctypes.c_size_t), ("fine_elems", ctypes.c_size_t),
                 ("p1_elems", ctypes.c_size_t), ("launches_per_apply", ctypes.c_int),
                 ("meta_bytes", ctypes.c_size_t), ("slots", ctypes.c_longlong),
-                ("max_tile_cap", ctypes.c_longlong), ("k3_thread_slots", ctypes.c_longlong)]
+                ("max_tile_cap", ctypes.c_longlong), ("k3_thread_slots", ctypes.c_longlong),
+                ("rank_balance", ctypes.c_double)]
 
 
 def library_path() -> str:

@@ -97,7 +97,8 @@ struct fio_plan_s {
   size_t alpha_bytes = 0, beta_bytes = 0, ws_bytes = 0, fine_elems = 0, p1_elems = 0, meta_bytes = 0;
   long long slots = 0;
   long long max_tile_cap = 0;
-  long long chunk_threads = 0;  // K3 thread slots (chunks x BLOCK): groups / this = thread fill
+  long long chunk_threads = 0;
+  double balance = 1.0;  // predicted max/mean rank load of the wedge assignment  // K3 thread slots (chunks x BLOCK): groups / this = thread fill
   double plan_seconds = 0, max_err = 0;
   EsPoly poly{};
   double poly_err = 0;
@@ -364,6 +365,79 @@ fio_status separate_wedge(fio_plan_s& P, const WedgeGeom& g, Rng& rng, cudaStrea
   return FIO_OK;
 }
 
+// Cheap, rank-independent estimate of q_l for the wedge -> rank assignment: the number of
+// column pivots of A(R, C) (64 random rows x <= 4096 random members) above eps x the largest.
+// Its own RNG stream, so the separation's draws (and factors) do not depend on nranks.
+fio_status estimate_rank(fio_plan_s& P, const WedgeGeom& g, cudaStream_t s, int& q_est) {
+  const int m = P.N * P.N, n = (int)g.members.size();
+  Rng rng(P.opts.seed ^ 0xA5A5A5A5DEADBEEFull ^ (0x9E3779B97F4A7C15ull * (uint64_t)(g.l + 7)));
+  std::vector<int> R = sample_distinct(rng, m, 64);
+  std::vector<int> ci = sample_distinct(rng, n, std::min(n, 4096));
+  std::vector<int> C(ci.size());
+  for (size_t j = 0; j < ci.size(); ++j) C[j] = g.members[ci[j]];
+  const int nr = (int)R.size(), nc = (int)C.size();
+  DevBuf dR, dC, dB;
+  FIO_CUDA(dR.ensure(sizeof(int) * nr));
+  FIO_CUDA(dC.ensure(sizeof(int) * nc));
+  FIO_CUDA(dB.ensure(sizeof(double2) * (size_t)nr * nc));
+  FIO_CUDA(cudaMemcpy(dR.p, R.data(), sizeof(int) * nr, cudaMemcpyHostToDevice));
+  FIO_CUDA(cudaMemcpy(dC.p, C.data(), sizeof(int) * nc, cudaMemcpyHostToDevice));
+  FIO_CUDA(launch_eval_entries(P.op, g.u1, g.u2, dR.as<int>(), nr, dC.as<int>(), nc, dB.as<double2>(), 1, nr, s));
+  std::vector<cplx> B((size_t)nr * nc);
+  FIO_CUDA(cudaMemcpyAsync(B.data(), dB.p, sizeof(cplx) * B.size(), cudaMemcpyDeviceToHost, s));
+  FIO_CUDA(cudaStreamSynchronize(s));
+  // modified Gram-Schmidt with pivoting over the nr sampled rows (vectors of length nc); the
+  // eps-rank is the number of pivots whose residual norm exceeds eps x the largest row norm
+  std::vector<cplx> Bt2((size_t)nc * nr);
+  for (int j = 0; j < nc; ++j)
+    for (int i = 0; i < nr; ++i) Bt2[j + (size_t)i * nc] = B[i + (size_t)j * nr];
+  double mx = 0;
+  for (int i = 0; i < nr; ++i) {
+    double t = 0;
+    for (int j = 0; j < nc; ++j) t += Bt2[j + (size_t)i * nc].re * Bt2[j + (size_t)i * nc].re + Bt2[j + (size_t)i * nc].im * Bt2[j + (size_t)i * nc].im;
+    mx = std::max(mx, t);
+  }
+  q_est = 0;
+  {
+    std::vector<double> nr2(nr);
+    std::vector<char> used(nr, 0);
+    for (int i = 0; i < nr; ++i) {
+      double t = 0;
+      for (int j = 0; j < nc; ++j) t += Bt2[j + (size_t)i * nc].re * Bt2[j + (size_t)i * nc].re + Bt2[j + (size_t)i * nc].im * Bt2[j + (size_t)i * nc].im;
+      nr2[i] = t;
+    }
+    for (int stp = 0; stp < nr; ++stp) {
+      int p = -1;
+      double best = -1;
+      for (int i = 0; i < nr; ++i)
+        if (!used[i] && nr2[i] > best) { best = nr2[i]; p = i; }
+      if (p < 0 || best <= P.eps * P.eps * mx) break;
+      used[p] = 1;
+      ++q_est;
+      const double inv = 1.0 / std::sqrt(best);
+      cplx* qv = &Bt2[(size_t)p * nc];
+      for (int j = 0; j < nc; ++j) { qv[j].re *= inv; qv[j].im *= inv; }
+      for (int i = 0; i < nr; ++i) {
+        if (used[i]) continue;
+        cplx* b = &Bt2[(size_t)i * nc];
+        double cr = 0, ci2 = 0;
+        for (int j = 0; j < nc; ++j) {
+          cr += qv[j].re * b[j].re + qv[j].im * b[j].im;
+          ci2 += qv[j].re * b[j].im - qv[j].im * b[j].re;
+        }
+        double t = 0;
+        for (int j = 0; j < nc; ++j) {
+          b[j].re -= cr * qv[j].re - ci2 * qv[j].im;
+          b[j].im -= cr * qv[j].im + ci2 * qv[j].re;
+          t += b[j].re * b[j].re + b[j].im * b[j].im;
+        }
+        nr2[i] = t;
+      }
+    }
+  }
+  return FIO_OK;
+}
+
 int fft_index(std::map<int, int>& lens, std::vector<FftLen>& tab, int L) {
   auto it = lens.find(L);
   if (it != lens.end()) return it->second;
@@ -429,10 +503,25 @@ fio_status build_plan(fio_plan_s& P, const fio_phase* phase, const fio_amplitude
   build_geometry(N, P.W, P.geom);
   std::vector<int> owner(P.W, 0);
   if (P.opts.nranks > 1) {
+    // per-wedge cost = q_l (estimated, identical on every rank) x (interpolation N^2 w^2 + FFT volume)
     std::vector<double> cost(P.W);
-    for (int l = 0; l < P.W; ++l)  // interpolation (N^2 w^2) + FFT volume, per term
-      cost[l] = (double)NN * P.taps * P.taps + 8.0 * P.geom[l].n1f * P.geom[l].n2f * std::log2((double)P.geom[l].n1f * P.geom[l].n2f);
+    for (int l = 0; l < P.W; ++l) {
+      int qe = 1;
+      if (!P.geom[l].members.empty()) {
+        fio_status st = estimate_rank(P, P.geom[l], 0, qe);
+        if (st != FIO_OK) return st;
+      }
+      cost[l] = (double)std::max(qe, 1) *
+                ((double)NN * P.taps * P.taps +
+                 8.0 * P.geom[l].n1f * P.geom[l].n2f * std::log2((double)P.geom[l].n1f * P.geom[l].n2f));
+    }
     lpt_assign(P.W, cost.data(), P.opts.nranks, owner.data());
+    std::vector<double> load(P.opts.nranks, 0.0);
+    for (int l = 0; l < P.W; ++l) load[owner[l]] += cost[l];
+    double mean = 0, mxl = 0;
+    for (double v : load) { mean += v; mxl = std::max(mxl, v); }
+    mean /= P.opts.nranks;
+    P.balance = mean > 0 ? mxl / mean : 1.0;
   }
   for (int l = 0; l < P.W; ++l)
     if (owner[l] == P.opts.rank && !P.geom[l].members.empty()) P.owned.push_back(l);
@@ -898,6 +987,7 @@ fio_status fio_plan_info(fio_handle h, fio_info* info) {
   info->slots = h->slots;
   info->max_tile_cap = h->max_tile_cap;
   info->k3_thread_slots = h->chunk_threads;
+  info->rank_balance = h->balance;
   info->beta_bytes = h->beta_bytes;
   info->workspace_bytes = h->ws_bytes;
   info->fine_elems = h->fine_elems;
