@@ -429,6 +429,9 @@ __device__ __forceinline__ void dft_small(T2 (&v)[R], int sign) {
 #ifndef FIO_FFT_FAST_TWIDDLE
 #define FIO_FFT_FAST_TWIDDLE 1
 #endif
+#ifndef FIO_FFT_TW2
+#define FIO_FFT_TW2 0  // two-level shared twiddles for c128: measured no gain
+#endif
 
 __device__ __forceinline__ int fdiv(int n, const FastDiv& f) {
   return (int)((__umulhi(f.m, (unsigned)n) + (unsigned)n) >> f.l);
@@ -443,7 +446,8 @@ __device__ __forceinline__ FastDiv make_fastdiv_dev(unsigned d) {
 template <typename T2, int R>
 __device__ __forceinline__ void stockham_stage(const T2* __restrict__ a, T2* __restrict__ b, int L, int Ns,
                                                const FastDiv& dnb, const FastDiv& dns,
-                                               const T2* __restrict__ tw, int nseq, int si, int sb, int sign) {
+                                               const T2* __restrict__ tw, const T2* __restrict__ tlo,
+                                               const T2* __restrict__ thi, int nseq, int si, int sb, int sign) {
   const int nb = L / R;
   const int span = L / (Ns * R);
   const int total = nseq * nb;
@@ -466,6 +470,10 @@ __device__ __forceinline__ void stockham_stage(const T2* __restrict__ a, T2* __r
         float sn, cs;
         __sincosf(wscale * (float)(r * k * span), &sn, &cs);
         w = mk<T2>(cs, sn);
+      } else if constexpr (sizeof(T2) == 16 && FIO_FFT_TW2) {
+        // complex128: e^{2 pi i m/L} = lo[m mod 64] * hi[m / 64] from a shared two-level table
+        const int m = r * k * span;
+        w = cmul(tlo[m & 63], thi[m >> 6]);
       } else {
         w = tw[r * k * span];
       }
@@ -482,6 +490,15 @@ __device__ __forceinline__ void stockham_stage(const T2* __restrict__ a, T2* __r
 // Returns the buffer holding the result (a or b).  Ends with __syncthreads().
 template <typename T2>
 __device__ T2* smem_fft(T2* a, T2* b, const FftLen& fl, const T2* tw, int nseq, int si, int sb, int sign) {
+  // two-level twiddle tables (complex128): lo[j] = e^{2 pi i j/L}, hi[h] = e^{2 pi i 64 h/L}, L <= 4096
+  __shared__ T2 tw_lo[64], tw_hi[64];
+  if constexpr (sizeof(T2) == 16 && FIO_FFT_TW2) {
+    for (int j = threadIdx.x; j < 64; j += blockDim.x) {
+      if (j < fl.L) tw_lo[j] = tw[j];
+      if (64 * j < fl.L) tw_hi[j] = tw[64 * j];
+    }
+    __syncthreads();
+  }
   int Ns = 1;
   for (int st = 0; st < fl.nst; ++st) {
     const int R = fl.radix[st];
@@ -489,13 +506,13 @@ __device__ T2* smem_fft(T2* a, T2* b, const FftLen& fl, const T2* tw, int nseq, 
     const FastDiv& dns = fl.div_ns[st];
     switch (R) {
 #if FIO_FFT_BIG_RADIX
-      case 16: stockham_stage<T2, 16>(a, b, fl.L, Ns, dnb, dns, tw, nseq, si, sb, sign); break;
-      case 8: stockham_stage<T2, 8>(a, b, fl.L, Ns, dnb, dns, tw, nseq, si, sb, sign); break;
+      case 16: stockham_stage<T2, 16>(a, b, fl.L, Ns, dnb, dns, tw, tw_lo, tw_hi, nseq, si, sb, sign); break;
+      case 8: stockham_stage<T2, 8>(a, b, fl.L, Ns, dnb, dns, tw, tw_lo, tw_hi, nseq, si, sb, sign); break;
 #endif
-      case 4: stockham_stage<T2, 4>(a, b, fl.L, Ns, dnb, dns, tw, nseq, si, sb, sign); break;
-      case 2: stockham_stage<T2, 2>(a, b, fl.L, Ns, dnb, dns, tw, nseq, si, sb, sign); break;
-      case 3: stockham_stage<T2, 3>(a, b, fl.L, Ns, dnb, dns, tw, nseq, si, sb, sign); break;
-      default: stockham_stage<T2, 5>(a, b, fl.L, Ns, dnb, dns, tw, nseq, si, sb, sign); break;
+      case 4: stockham_stage<T2, 4>(a, b, fl.L, Ns, dnb, dns, tw, tw_lo, tw_hi, nseq, si, sb, sign); break;
+      case 2: stockham_stage<T2, 2>(a, b, fl.L, Ns, dnb, dns, tw, tw_lo, tw_hi, nseq, si, sb, sign); break;
+      case 3: stockham_stage<T2, 3>(a, b, fl.L, Ns, dnb, dns, tw, tw_lo, tw_hi, nseq, si, sb, sign); break;
+      default: stockham_stage<T2, 5>(a, b, fl.L, Ns, dnb, dns, tw, tw_lo, tw_hi, nseq, si, sb, sign); break;
     }
     __syncthreads();
     T2* t = a;
