@@ -443,7 +443,25 @@ __device__ __forceinline__ FastDiv make_fastdiv_dev(unsigned d) {
   return FastDiv{(unsigned)m, l, d};
 }
 
-template <typename T2, int R>
+// Bank-conflict padding of the shared FFT buffers of the wedge passes: one empty slot after
+// every 128 bytes (8 complex128 / 16 complex64), so the stride-R writes of the early Stockham
+// stages hit distinct banks.  Sequence s, element e -> s * padded_len(L) + pad_idx(e).
+template <typename T2> struct PadShift;
+template <> struct PadShift<float2> { static constexpr int value = 4; };
+template <> struct PadShift<double2> { static constexpr int value = 3; };
+#ifndef FIO_FFT_PAD
+#define FIO_FFT_PAD 0  // measured neutral-to-slower on B200 (K2 c128 3.38 vs 3.26 ms): off
+#endif
+template <typename T2, bool PAD>
+__host__ __device__ __forceinline__ int pad_idx(int i) {
+  return (PAD && FIO_FFT_PAD) ? i + (i >> PadShift<T2>::value) : i;
+}
+template <typename T2, bool PAD>
+__host__ __device__ __forceinline__ int padded_len(int L) {
+  return (PAD && FIO_FFT_PAD) ? L + (L >> PadShift<T2>::value) + 1 : L;
+}
+
+template <typename T2, int R, bool PAD>
 __device__ __forceinline__ void stockham_stage(const T2* __restrict__ a, T2* __restrict__ b, int L, int Ns,
                                                const FastDiv& dnb, const FastDiv& dns,
                                                const T2* __restrict__ tw, const T2* __restrict__ tlo,
@@ -461,7 +479,7 @@ __device__ __forceinline__ void stockham_stage(const T2* __restrict__ a, T2* __r
     T2* out = b + sq * sb;
     T2 v[R];
 #pragma unroll
-    for (int r = 0; r < R; ++r) v[r] = in[(j + r * nb) * si];
+    for (int r = 0; r < R; ++r) v[r] = in[pad_idx<T2, PAD>((j + r * nb) * si)];
 #pragma unroll
     for (int r = 1; r < R; ++r) {
       T2 w;
@@ -483,12 +501,12 @@ __device__ __forceinline__ void stockham_stage(const T2* __restrict__ a, T2* __r
     dft_small<T2, R>(v, sign);
     int base = jq * Ns * R + k;
 #pragma unroll
-    for (int r = 0; r < R; ++r) out[(base + r * Ns) * si] = v[r];
+    for (int r = 0; r < R; ++r) out[pad_idx<T2, PAD>((base + r * Ns) * si)] = v[r];
   }
 }
 
 // Returns the buffer holding the result (a or b).  Ends with __syncthreads().
-template <typename T2>
+template <typename T2, bool PAD = false>
 __device__ T2* smem_fft(T2* a, T2* b, const FftLen& fl, const T2* tw, int nseq, int si, int sb, int sign) {
   // two-level twiddle tables (complex128): lo[j] = e^{2 pi i j/L}, hi[h] = e^{2 pi i 64 h/L}, L <= 4096
   __shared__ T2 tw_lo[64], tw_hi[64];
@@ -506,13 +524,13 @@ __device__ T2* smem_fft(T2* a, T2* b, const FftLen& fl, const T2* tw, int nseq, 
     const FastDiv& dns = fl.div_ns[st];
     switch (R) {
 #if FIO_FFT_BIG_RADIX
-      case 16: stockham_stage<T2, 16>(a, b, fl.L, Ns, dnb, dns, tw, tw_lo, tw_hi, nseq, si, sb, sign); break;
-      case 8: stockham_stage<T2, 8>(a, b, fl.L, Ns, dnb, dns, tw, tw_lo, tw_hi, nseq, si, sb, sign); break;
+      case 16: stockham_stage<T2, 16, PAD>(a, b, fl.L, Ns, dnb, dns, tw, tw_lo, tw_hi, nseq, si, sb, sign); break;
+      case 8: stockham_stage<T2, 8, PAD>(a, b, fl.L, Ns, dnb, dns, tw, tw_lo, tw_hi, nseq, si, sb, sign); break;
 #endif
-      case 4: stockham_stage<T2, 4>(a, b, fl.L, Ns, dnb, dns, tw, tw_lo, tw_hi, nseq, si, sb, sign); break;
-      case 2: stockham_stage<T2, 2>(a, b, fl.L, Ns, dnb, dns, tw, tw_lo, tw_hi, nseq, si, sb, sign); break;
-      case 3: stockham_stage<T2, 3>(a, b, fl.L, Ns, dnb, dns, tw, tw_lo, tw_hi, nseq, si, sb, sign); break;
-      default: stockham_stage<T2, 5>(a, b, fl.L, Ns, dnb, dns, tw, tw_lo, tw_hi, nseq, si, sb, sign); break;
+      case 4: stockham_stage<T2, 4, PAD>(a, b, fl.L, Ns, dnb, dns, tw, tw_lo, tw_hi, nseq, si, sb, sign); break;
+      case 2: stockham_stage<T2, 2, PAD>(a, b, fl.L, Ns, dnb, dns, tw, tw_lo, tw_hi, nseq, si, sb, sign); break;
+      case 3: stockham_stage<T2, 3, PAD>(a, b, fl.L, Ns, dnb, dns, tw, tw_lo, tw_hi, nseq, si, sb, sign); break;
+      default: stockham_stage<T2, 5, PAD>(a, b, fl.L, Ns, dnb, dns, tw, tw_lo, tw_hi, nseq, si, sb, sign); break;
     }
     __syncthreads();
     T2* t = a;
@@ -596,10 +614,11 @@ __global__ void __launch_bounds__(256) k_rowpass(int N, const WedgeDev* __restri
   const WedgeDev& w = wedges[job.w];
   const FftLen& fl = ffts[w.fft2];
   const int L = fl.L, n1 = w.n1, n2 = w.n2, cnt = job.count;
+  const int Lp = padded_len<T2, true>(L);
   T2* a = reinterpret_cast<T2*>(smem_raw);
-  T2* b = a + cnt * L;
+  T2* b = a + cnt * Lp;
   const T2 zero = mk<T2>(0, 0);
-  for (int idx = threadIdx.x; idx < cnt * L; idx += blockDim.x) a[idx] = zero;
+  for (int idx = threadIdx.x; idx < cnt * Lp; idx += blockDim.x) a[idx] = zero;
   __syncthreads();
   const T2* bet = betas[job.w] + ((long long)job.t * n1 + job.start) * n2;
   for (int r = 0; r < cnt; ++r)
@@ -610,16 +629,16 @@ __global__ void __launch_bounds__(256) k_rowpass(int N, const WedgeDev* __restri
       int z1 = kp1 + w.xc1, z2 = kp2 + w.xc2;
       int xi1 = w.Mi[0] * z1 + w.Mi[1] * z2, xi2 = w.Mi[2] * z1 + w.Mi[3] * z2;
       T2 fv = fhat[(long long)imod(xi1, N) * N + imod(xi2, N)];
-      a[r * L + imod(kp2, L)] = cmul(bv, fv);
+      a[r * Lp + pad_idx<T2, true>(imod(kp2, L))] = cmul(bv, fv);
     }
   }
   __syncthreads();
-  T2* res = smem_fft<T2>(a, b, fl, tw + fl.tw_off, cnt, 1, L, +1);
+  T2* res = smem_fft<T2, true>(a, b, fl, tw + fl.tw_off, cnt, 1, Lp, +1);
   T2* dst = p1 + w.p1_off + (long long)job.t * L * n1 + job.start;
   const FastDiv dc = make_fastdiv_dev((unsigned)cnt);
   for (int idx = threadIdx.x; idx < cnt * L; idx += blockDim.x) {  // consecutive threads: consecutive i1
     const int j2 = fdiv(idx, dc), r = idx - j2 * cnt;
-    dst[(long long)j2 * n1 + r] = res[r * L + j2];
+    dst[(long long)j2 * n1 + r] = res[r * Lp + pad_idx<T2, true>(j2)];
   }
 }
 
@@ -638,26 +657,27 @@ __global__ void __launch_bounds__(256) k_colpass(const WedgeDev* __restrict__ we
   const WedgeDev& w = wedges[job.w];
   const FftLen& fl = ffts[w.fft1];
   const int L = fl.L, n1 = w.n1, C = job.count, c0 = job.start;
+  const int Lp = padded_len<T2, true>(L);
   T2* a = reinterpret_cast<T2*>(smem_raw);
-  T2* b = a + C * L;
+  T2* b = a + C * Lp;
   const T2 zero = mk<T2>(0, 0);
-  for (int idx = threadIdx.x; idx < C * L; idx += blockDim.x) a[idx] = zero;
+  for (int idx = threadIdx.x; idx < C * Lp; idx += blockDim.x) a[idx] = zero;
   __syncthreads();
   const T2* src = p1 + w.p1_off + ((long long)job.t * w.n2f + c0) * n1;
   for (int c = 0; c < C; ++c)
     for (int i1 = threadIdx.x; i1 < n1; i1 += blockDim.x) {
       int pos = i1 - n1 / 2;
       pos = pos < 0 ? pos + L : pos;
-      a[c * L + pos] = src[(long long)c * n1 + i1];
+      a[c * Lp + pad_idx<T2, true>(pos)] = src[(long long)c * n1 + i1];
     }
   __syncthreads();
-  T2* res = smem_fft<T2>(a, b, fl, tw + fl.tw_off, C, 1, L, +1);
+  T2* res = smem_fft<T2, true>(a, b, fl, tw + fl.tw_off, C, 1, Lp, +1);
   const int rowp = L + 2 * kHalo;
   T2* dst = g + w.g_off + ((long long)job.t * w.n2f + c0) * rowp + kHalo;
   for (int c = 0; c < C; ++c) {
     T2* rp = dst + (long long)c * rowp;
     for (int j1 = threadIdx.x; j1 < L; j1 += blockDim.x) {
-      const T2 v = res[c * L + j1];
+      const T2 v = res[c * Lp + pad_idx<T2, true>(j1)];
       rp[j1] = v;
       if (j1 < kHalo) rp[L + j1] = v;
       if (j1 >= L - kHalo) rp[j1 - L] = v;
@@ -1165,8 +1185,9 @@ __global__ void __launch_bounds__(256) k_colpass_adj(const WedgeDev* __restrict_
   const WedgeDev& w = wedges[job.w];
   const FftLen& fl = ffts[w.fft1];
   const int L = fl.L, n1 = w.n1, C = job.count, c0 = job.start;
+  const int Lp = padded_len<T2, true>(L);
   T2* a = reinterpret_cast<T2*>(smem_raw);
-  T2* b = a + C * L;
+  T2* b = a + C * Lp;
   const int rowp = L + 2 * kHalo;
   const T2* src = g + w.g_off + ((long long)job.t * w.n2f + c0) * rowp + kHalo;
   for (int c = 0; c < C; ++c) {
@@ -1175,17 +1196,17 @@ __global__ void __launch_bounds__(256) k_colpass_adj(const WedgeDev* __restrict_
       T2 v = rp[j1];
       if (j1 < kHalo) v = cadd(v, rp[L + j1]);        // right halo holds columns 0..kHalo-1
       if (j1 >= L - kHalo) v = cadd(v, rp[j1 - L]);   // left halo holds columns L-kHalo..L-1
-      a[c * L + j1] = v;
+      a[c * Lp + pad_idx<T2, true>(j1)] = v;
     }
   }
   __syncthreads();
-  T2* res = smem_fft<T2>(a, b, fl, tw + fl.tw_off, C, 1, L, -1);
+  T2* res = smem_fft<T2, true>(a, b, fl, tw + fl.tw_off, C, 1, Lp, -1);
   T2* dst = p1 + w.p1_off + ((long long)job.t * w.n2f + c0) * n1;
   for (int c = 0; c < C; ++c)
     for (int i1 = threadIdx.x; i1 < n1; i1 += blockDim.x) {
       int pos = i1 - n1 / 2;
       pos = pos < 0 ? pos + L : pos;
-      dst[(long long)c * n1 + i1] = res[c * L + pos];
+      dst[(long long)c * n1 + i1] = res[c * Lp + pad_idx<T2, true>(pos)];
     }
 }
 
@@ -1201,9 +1222,10 @@ __global__ void __launch_bounds__(256) k_rowpass_adj(int N, const WedgeDev* __re
   const WedgeDev& w = wedges[job.w];
   const FftLen& fl = ffts[w.fft2];
   const int L = fl.L, n1 = w.n1, n2 = w.n2, cnt = job.count;
+  const int Lp = padded_len<T2, true>(L);
   T2* a = reinterpret_cast<T2*>(smem_raw);
-  T2* b = a + cnt * L;
-  T2* acc = b + cnt * L;
+  T2* b = a + cnt * Lp;
+  T2* acc = b + cnt * Lp;
   for (int idx = threadIdx.x; idx < cnt * n2; idx += blockDim.x) acc[idx] = mk<T2>(0, 0);
   const FastDiv dc = make_fastdiv_dev((unsigned)cnt);
   for (int t = 0; t < w.q; ++t) {
@@ -1211,17 +1233,17 @@ __global__ void __launch_bounds__(256) k_rowpass_adj(int N, const WedgeDev* __re
     __syncthreads();
     for (int idx = threadIdx.x; idx < cnt * L; idx += blockDim.x) {
       const int j2 = fdiv(idx, dc), r = idx - j2 * cnt;
-      a[r * L + j2] = src[(long long)j2 * n1 + r];
+      a[r * Lp + pad_idx<T2, true>(j2)] = src[(long long)j2 * n1 + r];
     }
     __syncthreads();
-    T2* res = smem_fft<T2>(a, b, fl, tw + fl.tw_off, cnt, 1, L, -1);
+    T2* res = smem_fft<T2, true>(a, b, fl, tw + fl.tw_off, cnt, 1, Lp, -1);
     const T2* bet = betas[job.w] + ((long long)t * n1 + job.start) * n2;
     for (int r = 0; r < cnt; ++r)
       for (int i2 = threadIdx.x; i2 < n2; i2 += blockDim.x) {
         const T2 bv = bet[r * n2 + i2];
         int pos = i2 - n2 / 2;
         pos = pos < 0 ? pos + L : pos;
-        const T2 h = res[r * L + pos];
+        const T2 h = res[r * Lp + pad_idx<T2, true>(pos)];
         T2 v = acc[r * n2 + i2];
         v.x += bv.x * h.x + bv.y * h.y;  // conj(beta') h
         v.y += bv.x * h.y - bv.y * h.x;
@@ -1346,7 +1368,10 @@ cudaError_t enqueue_adjoint(const ApplyArgs& a, bool c64, const void* g, void* o
   return enqueue_adjoint_t<double2>(a, (const double2*)g, (double2*)out, s, launches);
 }
 
-size_t fft_seq_bytes(int L, bool c64) { return 2 * (size_t)L * (c64 ? sizeof(float2) : sizeof(double2)); }
+size_t fft_seq_bytes(int L, bool c64) {
+  return c64 ? 2 * (size_t)padded_len<float2, true>(L) * sizeof(float2)
+             : 2 * (size_t)padded_len<double2, true>(L) * sizeof(double2);
+}
 
 cudaError_t configure_kernels(size_t smem_bytes) {
   cudaError_t e;
