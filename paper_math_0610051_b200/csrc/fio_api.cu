@@ -27,16 +27,12 @@ constexpr size_t kSmemBudgetDefault = 48 * 1024;  // per-CTA FFT pass target (FI
 constexpr size_t kSmemMax = 200 * 1024;     // opt-in maximum for one long sequence
 constexpr int kCertSamples = 200;           // s of PAPER.md:1464-1477
 
-struct Status {
-  fio_status code = FIO_OK;
-};
-
 #define FIO_CUDA(expr)                                                                               \
   do {                                                                                               \
     cudaError_t e_ = (expr);                                                                         \
     if (e_ != cudaSuccess) {                                                                         \
       set_error(std::string("CUDA error at " #expr ": ") + cudaGetErrorString(e_));                  \
-      return FIO_ECUDA;                                                                              \
+      return e_ == cudaErrorMemoryAllocation ? FIO_ENOMEM : FIO_ECUDA;                               \
     }                                                                                                \
   } while (0)
 
@@ -77,14 +73,13 @@ struct fio_plan_s {
   std::vector<int> r_final;
   std::vector<double> sep_err;
   std::vector<void*> allocs;
-  std::vector<void*> alpha_ptrs, beta_ptrs;
+  std::vector<void*> beta_ptrs;
   std::vector<InterpWedge> iw;
   OperatorDev op{};
   double2* a0 = nullptr;
   WedgeDev* d_wedges = nullptr;
   FftLen* d_ffts = nullptr;
   void* d_tw = nullptr;
-  void** d_alpha = nullptr;
   void** d_beta = nullptr;
   void *fhat = nullptr, *tmp = nullptr, *p1 = nullptr, *g = nullptr;
   FftJob *jobs_row = nullptr, *jobs_col = nullptr, *jobs_rowadj = nullptr;
@@ -624,7 +619,6 @@ fio_status build_plan(fio_plan_s& P, const fio_phase* phase, const fio_amplitude
     P.slots += nslots;
     P.iw.push_back(iw);
     P.beta_bytes += cs * (size_t)q * g.n1 * g.n2;
-    P.alpha_ptrs.push_back(alpha);
     P.beta_ptrs.push_back(betap);
     {  // box mask of the wedge's members (adjoint K1* writes fhat* only there)
       std::vector<unsigned char> mask((size_t)g.n1 * g.n2, 0);

@@ -58,8 +58,6 @@ struct WedgeDev {
   int xc1, xc2; // xi_c
   int fft1, fft2;  // FftLen index for n1f (column pass) and n2f (row pass)
   double u1, u2;   // xihat_l = (cos 2 pi l / W, sin 2 pi l / W)
-  long long alpha_off;  // element offset of alpha'[t][x] block (q * N*N)
-  long long beta_off;   // element offset of beta'[t][i1][i2] block (q * n1 * n2)
   long long p1_off;     // element offset of the row-pass buffer, [t][j2][i1] (q * n2f * n1)
   long long g_off;      // element offset of the fine grids, [t][j2][kHalo + j1] (q * n2f * (n1f + 2 kHalo))
 };
