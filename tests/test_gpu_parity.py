@@ -276,3 +276,31 @@ def test_bessel_grt_paper_table_replay():
     err = oracle.rel_l2(out, oracle.fio(op, f))
     print("bessel L+ N=64 eps=%.3g err=%.3g (paper 7.30e-4)" % (eps, err))
     assert err <= 2 * eps
+
+
+# ------------------------------------------------------------------ separation (P3) vs dense SVD
+def test_separation_rank_matches_dense_svd():
+    # for each wedge the plan's q should be the eps-rank of the
+    # residual kernel A_l(x, xi) = e^{2 pi i (rho - grad rho(x, xihat_l).xi)}, computed here by a
+    # dense numpy SVD of the full N^2 x |W_l| matrix (no product or oracle code involved)
+    N, eps = 32, 1e-6
+    op = wl.grt_operator(N)
+    plan = make_plan(op, eps)
+    wd = plan.wedges()
+    W = plan.info["W"]
+    geo = fio.geometry(N, W)
+    xi1, xi2 = wl.freqs(N)
+    C1, C2 = op.c1.ravel(), op.c2.ravel()
+    for l, q in zip(wd["l"], wd["q"]):
+        m = geo["wedge_of"].ravel() == l
+        a1, a2 = xi1.ravel()[m].astype(float), xi2.ravel()[m].astype(float)
+        th = 2 * np.pi * l / W
+        u1, u2 = np.cos(th), np.sin(th)
+        den = np.sqrt(C1 ** 2 * u1 ** 2 + C2 ** 2 * u2 ** 2)
+        g1, g2 = C1 ** 2 * u1 / den, C2 ** 2 * u2 / den
+        rho = np.sqrt(np.outer(C1 ** 2, a1 ** 2) + np.outer(C2 ** 2, a2 ** 2))
+        A = np.exp(2j * np.pi * (rho - np.outer(g1, a1) - np.outer(g2, a2)))
+        s = np.linalg.svd(A, compute_uv=False)
+        rank = int((s > eps * s[0]).sum())
+        assert rank - 1 <= q <= rank + 8, (l, q, rank)
+    assert np.all(wd["sep_err"] <= 10 * eps)
