@@ -113,6 +113,27 @@ def apply_algorithmic_bytes(info, N, c64):
     return k0 + k12 + k3_algorithmic_bytes(info, N, c64)
 
 
+def k3_resource_model(info, c64, ms, sm_mhz):
+    """What binds K3: per group-term the thread reads its (w+1)^2 window
+    (rows rounded up to even) and the P row weights from shared memory and alpha'(t) from the ring,
+    and issues 2 real FMAs per (point, window cell) plus 2 per (point, row) plus the alpha product.
+    Returns achieved fractions of the SM load datapath (128 B/clk/SM) and of the FMA pipe
+    (128 FP32 or 64 FP64 FMA/clk/SM) at the measured SM clock."""
+    w = info["nufft_w"]
+    P = info["group_p"]
+    win, winr = w + 1, (w + 2) & ~1
+    cs, rs = (8, 4) if c64 else (16, 8)
+    gt = info["slot_terms"] / P
+    lsu_bytes = gt * (winr * win * cs + winr * P * rs + P * cs)
+    fmas = gt * (winr * (P * win * 2 + P * 2) + 4 * P)
+    clk = (sm_mhz or 1965.0) * 1e6
+    t = ms * 1e-3
+    sms = 148
+    return {"lsu_bytes": lsu_bytes, "lsu_frac": lsu_bytes / t / (sms * 128 * clk),
+            "fma": fmas, "fma_frac": fmas / t / (sms * (128 if c64 else 64) * clk),
+            "sm_mhz": sm_mhz, "model": "DESIGN.md section 7"}
+
+
 def peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
@@ -283,6 +304,7 @@ def time_config(name, args, rank, world, local, group):
                      "traffic": None, "kernel": "k_interp (K3)", "peak_source": src,
                      "algorithmic_bytes": k3_bytes},
         "apply_hbm_gbs": apply_algorithmic_bytes(info, N, c64) / (ms_step * 1e-3) / 1e9,
+        "k3_resources": k3_resource_model(info, c64, k3_ms, clk.summary().get("sm_mhz")),
         "plan": {"W": info["W"], "sum_q": info["sum_q"], "nufft_w": info["nufft_w"],
                  "plan_seconds": info["plan_seconds"], "max_sep_err": info["max_sep_err"],
                  "alpha_GB": info["alpha_bytes"] / 1e9, "fine_elems": info["fine_elems"],
@@ -316,7 +338,7 @@ def run_gpu(args):
         v = time_config(args.variant, args, rank, world, local, group)
         variants[args.variant] = {k: v[k] for k in ("dtype", "eps", "applies_per_s", "points_per_s", "ms_per_step",
                                                     "roofline", "stage_ms", "k3_share", "plan", "e2e",
-                                                    "adjoint_ms_per_step")}
+                                                    "adjoint_ms_per_step", "k3_resources")}
     if rank == 0:
         cpu = None
         if world == 1 and not args.no_cpu_baseline:
@@ -331,6 +353,7 @@ def run_gpu(args):
                        "l2": "inputs larger than L2 (alpha' streams %.1f GB per step)" % main["plan"]["alpha_GB"]},
             "points_per_s": main["points_per_s"],
             "roofline": main["roofline"], "apply_hbm_gbs": main["apply_hbm_gbs"], "stage_ms": main["stage_ms"],
+            "k3_resources": main["k3_resources"],
             "k3_share": main["k3_share"], "plan": main["plan"], "adjoint_ms_per_step": main["adjoint_ms_per_step"],
             "clocks": main["clocks"], "e2e": main["e2e"],
             "gpu_launches": main["launches_per_step"] * args.steps,

@@ -158,6 +158,8 @@ typedef struct {
   long long max_tile_cap; /* largest K3 chunk footprint (fine-grid elements) */
   long long k3_thread_slots; /* K3 chunks x threads per CTA (slots / P / this = thread fill) */
   double rank_balance;    /* predicted max/mean per-rank cost of the wedge assignment (1 if nranks = 1) */
+  long long slot_terms;   /* sum over owned wedges of K3 slots x q_l (K3 work units per apply) */
+  int group_p;            /* points per K3 group */
 } fio_info;
 
 fio_status fio_plan_info(fio_handle h, fio_info* info);

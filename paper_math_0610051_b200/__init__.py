@@ -70,7 +70,7 @@ class _Info(ctypes.Structure):
                 ("p1_elems", ctypes.c_size_t), ("launches_per_apply", ctypes.c_int),
                 ("meta_bytes", ctypes.c_size_t), ("slots", ctypes.c_longlong),
                 ("max_tile_cap", ctypes.c_longlong), ("k3_thread_slots", ctypes.c_longlong),
-                ("rank_balance", ctypes.c_double)]
+                ("rank_balance", ctypes.c_double), ("slot_terms", ctypes.c_longlong), ("group_p", ctypes.c_int)]
 
 
 def library_path() -> str:

@@ -91,6 +91,7 @@ struct fio_plan_s {
   void *e2e_in = nullptr, *e2e_out = nullptr;
   size_t alpha_bytes = 0, beta_bytes = 0, ws_bytes = 0, fine_elems = 0, p1_elems = 0, meta_bytes = 0;
   long long slots = 0;
+  long long slot_terms = 0;  // sum over owned wedges of padded K3 slots x q_l
   long long max_tile_cap = 0;
   long long chunk_threads = 0;
   double balance = 1.0;  // predicted max/mean rank load of the wedge assignment  // K3 thread slots (chunks x BLOCK): groups / this = thread fill
@@ -617,6 +618,7 @@ fio_status build_plan(fio_plan_s& P, const fio_phase* phase, const fio_amplitude
     }
     P.alpha_bytes += cs * (size_t)q * nslots;
     P.slots += nslots;
+    P.slot_terms += nslots * (long long)q;
     P.iw.push_back(iw);
     P.beta_bytes += cs * (size_t)q * g.n1 * g.n2;
     P.beta_ptrs.push_back(betap);
@@ -982,6 +984,8 @@ fio_status fio_plan_info(fio_handle h, fio_info* info) {
   info->max_tile_cap = h->max_tile_cap;
   info->k3_thread_slots = h->chunk_threads;
   info->rank_balance = h->balance;
+  info->slot_terms = h->slot_terms;
+  info->group_p = group_p(h->c64);
   info->beta_bytes = h->beta_bytes;
   info->workspace_bytes = h->ws_bytes;
   info->fine_elems = h->fine_elems;
