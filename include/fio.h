@@ -105,6 +105,10 @@ typedef struct {
   int r_init;         /* 32: initial skeleton size r of PAPER.md:1211-1221 */
   int r_max;          /* 512: cap of the doubling */
   int certify;        /* 1: compute the sampled error of PAPER.md:1464-1477 */
+  int skeleton;       /* 0: store alpha' (fast).  1: skeleton storage of PAPER.md:1223-1241 --
+                         keep only the skeleton columns C and V S^{-1} per wedge and rebuild
+                         alpha' = A_[C] V S^{-1} (with the center phase) before each wedge's
+                         interpolation; O(r q) storage per wedge, extra compute per apply */
 } fio_opts;
 
 void fio_default_opts(fio_opts* opts);
@@ -160,6 +164,8 @@ typedef struct {
   double rank_balance;    /* predicted max/mean per-rank cost of the wedge assignment (1 if nranks = 1) */
   long long slot_terms;   /* sum over owned wedges of K3 slots x q_l (K3 work units per apply) */
   int group_p;            /* points per K3 group */
+  size_t skeleton_bytes;  /* skeleton storage: C and V S^{-1} of every owned wedge (0 otherwise);
+                             alpha_bytes is then the size of the shared rebuild scratch */
 } fio_info;
 
 fio_status fio_plan_info(fio_handle h, fio_info* info);

@@ -57,7 +57,7 @@ class _Opts(ctypes.Structure):
     _fields_ = [("dtype", ctypes.c_int), ("n_wedges", ctypes.c_int), ("nufft_w", ctypes.c_int),
                 ("nufft_beta", ctypes.c_double), ("seed", ctypes.c_uint64), ("device", ctypes.c_int),
                 ("rank", ctypes.c_int), ("nranks", ctypes.c_int), ("r_init", ctypes.c_int),
-                ("r_max", ctypes.c_int), ("certify", ctypes.c_int)]
+                ("r_max", ctypes.c_int), ("certify", ctypes.c_int), ("skeleton", ctypes.c_int)]
 
 
 class _Info(ctypes.Structure):
@@ -70,7 +70,8 @@ class _Info(ctypes.Structure):
                 ("p1_elems", ctypes.c_size_t), ("launches_per_apply", ctypes.c_int),
                 ("meta_bytes", ctypes.c_size_t), ("slots", ctypes.c_longlong),
                 ("max_tile_cap", ctypes.c_longlong), ("k3_thread_slots", ctypes.c_longlong),
-                ("rank_balance", ctypes.c_double), ("slot_terms", ctypes.c_longlong), ("group_p", ctypes.c_int)]
+                ("rank_balance", ctypes.c_double), ("slot_terms", ctypes.c_longlong), ("group_p", ctypes.c_int),
+                ("skeleton_bytes", ctypes.c_size_t)]
 
 
 def library_path() -> str:
@@ -182,7 +183,7 @@ class Plan:
                  dtype: str = "c128", n_wedges: int = 0, nufft_w: int = 0, nufft_beta: float = 0.0,
                  seed: int = 0x5EED, device: Optional[int] = None, rank: int = 0, nranks: int = 1,
                  r_init: int = 32, r_max: int = 512, certify: bool = True, rho_sign: int = 1,
-                 amplitude: str = "separable"):
+                 amplitude: str = "separable", skeleton: bool = False):
         import torch
         if not torch.cuda.is_available():
             raise FioError(-3, "no CUDA device: the FIO apply runs only on the GPU (no CPU fallback)")
@@ -210,6 +211,7 @@ class Plan:
         o.n_wedges, o.nufft_w, o.nufft_beta, o.seed = int(n_wedges), int(nufft_w), float(nufft_beta), int(seed)
         o.device, o.rank, o.nranks = self.device, int(rank), int(nranks)
         o.r_init, o.r_max, o.certify = int(r_init), int(r_max), int(bool(certify))
+        o.skeleton = int(bool(skeleton))
         h = ctypes.c_void_p()
         with torch.cuda.device(self.device):
             self.status = _check(lib.fio_plan(ctypes.byref(h), self.N, ctypes.byref(ph), ctypes.byref(amp),

@@ -94,7 +94,9 @@ struct fio_plan_s {
   long long slot_terms = 0;  // sum over owned wedges of padded K3 slots x q_l
   long long max_tile_cap = 0;
   long long chunk_threads = 0;
-  double balance = 1.0;  // predicted max/mean rank load of the wedge assignment  // K3 thread slots (chunks x BLOCK): groups / this = thread fill
+  double balance = 1.0;  // predicted max/mean rank load of the wedge assignment
+  std::vector<SkelWedge> skel;  // skeleton storage (opts.skeleton)
+  size_t skel_bytes = 0, scratch_elems = 0;  // K3 thread slots (chunks x BLOCK): groups / this = thread fill
   double plan_seconds = 0, max_err = 0;
   EsPoly poly{};
   double poly_err = 0;
@@ -186,7 +188,8 @@ namespace {
 // threshold eps are kept).  Produces U (m x q, device, FP64), beta (q x n,
 // device, FP64), q, the final r and the sampled error.
 fio_status separate_wedge(fio_plan_s& P, const WedgeGeom& g, Rng& rng, cudaStream_t s, DevBuf& dU, DevBuf& dBeta,
-                          int& q_out, int& r_out, double& err_out) {
+                          int& q_out, int& r_out, double& err_out, std::vector<int>& C_out,
+                          std::vector<cplx>& Y_out) {
   const int N = P.N;
   const int m = N * N;
   const int n = (int)g.members.size();
@@ -267,6 +270,8 @@ fio_status separate_wedge(fio_plan_s& P, const WedgeGeom& g, Rng& rng, cudaStrea
   FIO_CUDA(launch_zgemm(m, q, rc, dAC.as<double2>(), 1, m, false, dY.as<double2>(), 1, rc, dU.as<double2>(), 1, m, 1,
                         nullptr, s));
   dAC.release();
+  C_out = C;  // skeleton storage keeps C and Y = V S^{-1}
+  Y_out = Y;
   // (5) rows: pivoting on a random row sample of U, plus r uniform rows
   std::vector<int> R1 = sample_distinct(rng, m, std::min(m, 8 * r));
   const int n1r = (int)R1.size();
@@ -534,7 +539,9 @@ fio_status build_plan(fio_plan_s& P, const fio_phase* phase, const fio_amplitude
     DevBuf dU, dBeta;
     int q = 0, r = 0;
     double err = 0;
-    fio_status st = separate_wedge(P, g, rng, s, dU, dBeta, q, r, err);
+    std::vector<int> Cs;
+    std::vector<cplx> Ys;
+    fio_status st = separate_wedge(P, g, rng, s, dU, dBeta, q, r, err, Cs, Ys);
     if (st != FIO_OK) return st;
     WedgeDev w{};
     w.l = g.l;
@@ -596,11 +603,26 @@ fio_status build_plan(fio_plan_s& P, const fio_phase* phase, const fio_amplitude
     const long long nslots = (long long)iw.ngroups * group_p(c64);
     void* alpha = nullptr;
     void* betap = nullptr;
-    FIO_CUDA(P.alloc(&alpha, cs * (size_t)q * nslots));
+    SkelWedge sk{};
+    if (P.opts.skeleton) {
+      // alpha' is rebuilt before every K3 launch into one shared scratch (allocated below)
+      sk.rc = q > 0 ? (int)Cs.size() : 0;
+      int* dC = nullptr;
+      double2* dYs = nullptr;
+      FIO_CUDA(P.upload(&dC, Cs.data(), std::max<size_t>(Cs.size(), 1)));
+      FIO_CUDA(P.upload(&dYs, reinterpret_cast<const double2*>(Ys.data()), std::max<size_t>(Ys.size(), 1)));
+      sk.C = dC;
+      sk.Y = dYs;
+      P.skel_bytes += Cs.size() * sizeof(int) + Ys.size() * sizeof(double2);
+      P.scratch_elems = std::max<size_t>(P.scratch_elems, (size_t)q * (size_t)nslots);
+    } else {
+      FIO_CUDA(P.alloc(&alpha, cs * (size_t)q * nslots));
+    }
+    P.skel.push_back(sk);
     FIO_CUDA(P.alloc(&betap, cs * (size_t)q * g.n1 * g.n2));
     iw.alpha = alpha;
     if (q > 0) {
-      FIO_CUDA(launch_fold_alpha(P.op, w, dU.as<double2>(), q, iw.slot_x, nslots, alpha, c64, s));
+      if (!P.opts.skeleton) FIO_CUDA(launch_fold_alpha(P.op, w, dU.as<double2>(), q, iw.slot_x, nslots, alpha, c64, s));
       FIO_CUDA(cudaMemsetAsync(betap, 0, cs * (size_t)q * g.n1 * g.n2, s));
       std::vector<double> d1(g.n1), d2(g.n2);
       for (int i = 0; i < g.n1; ++i) d1[i] = 1.0 / es_fourier((double)(i - g.n1 / 2) / g.n1f, P.taps, P.es_beta);
@@ -616,7 +638,7 @@ fio_status build_plan(fio_plan_s& P, const fio_phase* phase, const fio_amplitude
                                 dd2.as<double>(), betap, c64, s));
       FIO_CUDA(cudaStreamSynchronize(s));
     }
-    P.alpha_bytes += cs * (size_t)q * nslots;
+    if (!P.opts.skeleton) P.alpha_bytes += cs * (size_t)q * nslots;
     P.slots += nslots;
     P.slot_terms += nslots * (long long)q;
     P.iw.push_back(iw);
@@ -640,6 +662,13 @@ fio_status build_plan(fio_plan_s& P, const fio_phase* phase, const fio_amplitude
     P.sep_err.push_back(err);
     P.max_err = std::max(P.max_err, err);
     if (err > 10.0 * P.eps) P.certified = 0;  // reading R7: certify at the 10 eps apply budget
+  }
+
+  if (P.opts.skeleton) {  // one alpha' scratch shared by the wedges (rebuilt per wedge per apply)
+    void* scratch = nullptr;
+    FIO_CUDA(P.alloc(&scratch, cs * std::max<size_t>(P.scratch_elems, 1)));
+    for (auto& iw : P.iw) iw.alpha = scratch;
+    P.alpha_bytes = cs * P.scratch_elems;
   }
 
   // twiddle tables
@@ -740,6 +769,8 @@ ApplyArgs make_args(const fio_plan_s& P) {
   a.fft_N = P.fft_N;
   a.tw = P.d_tw;
   a.iw = P.iw.data();
+  a.wd_host = P.wd.data();
+  a.skel = P.opts.skeleton ? P.skel.data() : nullptr;
   a.beta = const_cast<const void* const*>(P.d_beta);
   a.op = P.op;
   a.a0 = P.a0;
@@ -856,7 +887,7 @@ fio_status fio_plan(fio_handle* out, int N, const fio_phase* phase, const fio_am
     return st;
   }
   P->plan_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
-  P->launches = 4 + std::max<int>(1, (int)P->wd.size());
+  P->launches = 4 + std::max<int>(1, (int)P->wd.size()) * (o.skeleton ? 2 : 1);
   *out = P;
   return P->certified ? FIO_OK : FIO_WNOTCERT;
 }
@@ -986,6 +1017,7 @@ fio_status fio_plan_info(fio_handle h, fio_info* info) {
   info->rank_balance = h->balance;
   info->slot_terms = h->slot_terms;
   info->group_p = group_p(h->c64);
+  info->skeleton_bytes = h->skel_bytes;
   info->beta_bytes = h->beta_bytes;
   info->workspace_bytes = h->ws_bytes;
   info->fine_elems = h->fine_elems;

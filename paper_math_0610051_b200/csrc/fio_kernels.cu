@@ -273,6 +273,57 @@ cudaError_t launch_fold_alpha(const OperatorDev& op, const WedgeDev& w, const do
   return cudaGetLastError();
 }
 
+// Skeleton storage (eq. probnewfac): U = A_[C] V S^{-1} is regenerated from
+// the kernel entries A(x, C_c) -- never stored -- folded with the center phase and 1/N.
+// Thread per slot; terms in chunks of 16 accumulators (entries recomputed per chunk).
+template <typename T2>
+__global__ void __launch_bounds__(128) k_rebuild_alpha(OperatorDev op, WedgeDev w, SkelWedge sk, int q,
+                                                       const int* __restrict__ slot_x, long long nslots,
+                                                       T2* __restrict__ alpha) {
+  const int N = op.N;
+  constexpr int TC = 16;
+  for (long long sl = blockIdx.x * (long long)blockDim.x + threadIdx.x; sl < nslots;
+       sl += (long long)gridDim.x * blockDim.x) {
+    const int x = slot_x[sl];
+    if (x < 0) {
+      for (int t = 0; t < q; ++t) alpha[t * nslots + sl] = to_t2<T2>(make_double2(0.0, 0.0));
+      continue;
+    }
+    double y1, y2;
+    warped_point(op, x / N, x % N, w, y1, y2);
+    double ph = y1 * (double)w.xc1 + y2 * (double)w.xc2;
+    ph -= floor(ph);
+    double sn, cs;
+    sincospi(2.0 * ph, &sn, &cs);
+    const double2 e = make_double2(cs / N, sn / N);
+    for (int t0 = 0; t0 < q; t0 += TC) {
+      double2 acc[TC];
+#pragma unroll
+      for (int k = 0; k < TC; ++k) acc[k] = make_double2(0.0, 0.0);
+      for (int c = 0; c < sk.rc; ++c) {
+        const double2 a = kernel_entry(op, x, sk.C[c], w.u1, w.u2);
+#pragma unroll
+        for (int k = 0; k < TC; ++k)
+          if (t0 + k < q) acc[k] = cadd(acc[k], cmul(a, sk.Y[c + (long long)(t0 + k) * sk.rc]));
+      }
+#pragma unroll
+      for (int k = 0; k < TC; ++k)
+        if (t0 + k < q) alpha[(t0 + k) * nslots + sl] = to_t2<T2>(cmul(acc[k], e));
+    }
+  }
+}
+
+cudaError_t launch_rebuild_alpha(const OperatorDev& op, const WedgeDev& w, const SkelWedge& sk, int q,
+                                 const int* slot_x, long long nslots, void* alpha, bool c64, cudaStream_t s) {
+  if (nslots == 0 || q == 0) return cudaSuccess;
+  int blocks = (int)std::min<long long>((nslots + 127) / 128, 148LL * 16);
+  if (c64)
+    k_rebuild_alpha<float2><<<blocks, 128, 0, s>>>(op, w, sk, q, slot_x, nslots, (float2*)alpha);
+  else
+    k_rebuild_alpha<double2><<<blocks, 128, 0, s>>>(op, w, sk, q, slot_x, nslots, (double2*)alpha);
+  return cudaGetLastError();
+}
+
 // Fine-grid coordinates u = frac(y_l(x)) (n1f, n2f) of every output point (plan time, FP64).
 __global__ void k_fine_coords(OperatorDev op, WedgeDev w, double2* __restrict__ u) {
   const int N = op.N;
@@ -1078,6 +1129,14 @@ static cudaError_t launch_interp(const ApplyArgs& a, T2* Lf, cudaStream_t s, int
   }
   for (int wi = 0; wi < a.nw; ++wi) {
     cudaError_t e;
+    if (a.skel) {  // skeleton storage: regenerate this wedge's alpha' into the shared scratch
+      const InterpWedge& iw = a.iw[wi];
+      e = launch_rebuild_alpha(a.op, a.wd_host[wi], a.skel[wi], iw.q, iw.slot_x,
+                               (long long)iw.ngroups * GroupP<T2>::value, const_cast<void*>(iw.alpha),
+                               sizeof(T2) == sizeof(float2), s);
+      if (e != cudaSuccess) return e;
+      ++*n;
+    }
 #define FIO_GROUPS_CASE(TP)                                            \
   case TP:                                                             \
     e = launch_groups_tp<T2, TP, GroupP<T2>::value>(a, wi, Lf, s);     \
@@ -1314,6 +1373,13 @@ static cudaError_t enqueue_adjoint_t(const ApplyArgs& a, const T2* g, T2* out, c
   if (a.nw > 0) {
     if ((e = cudaMemsetAsync(a.g, 0, sizeof(T2) * a.fine_elems, s)) != cudaSuccess) return e;
     for (int wi = 0; wi < a.nw; ++wi) {
+      if (a.skel) {
+        const InterpWedge& iw = a.iw[wi];
+        e = launch_rebuild_alpha(a.op, a.wd_host[wi], a.skel[wi], iw.q, iw.slot_x,
+                                 (long long)iw.ngroups * GroupP<T2>::value, const_cast<void*>(iw.alpha), c64, s);
+        if (e != cudaSuccess) return e;
+        ++n;
+      }
 #define FIO_SPREAD_CASE(TP)                                   \
   case TP:                                                    \
     e = launch_spread_tp<T2, TP, GroupP<T2>::value>(a, wi, g, s); \

@@ -52,6 +52,18 @@ cudaError_t launch_fine_coords(const OperatorDev& op, const WedgeDev& w, double2
 cudaError_t launch_fold_beta(int N, const WedgeDev& w, const int* members, int n, const double2* beta, int q,
                              const double* d1, const double* d2, void* betap, bool c64, cudaStream_t s);
 
+// Skeleton storage: per owned wedge the skeleton columns C (member
+// frequency indices) and Y = V S^{-1} (rc x q, column-major, FP64).
+struct SkelWedge {
+  int rc;
+  const int* C;
+  const double2* Y;
+};
+
+// alpha'[t][s] = e^{2 pi i y(x_s).xi_c} / N * sum_c A(x_s, C_c) Y[c + t rc]  (slot order; 0 for padding)
+cudaError_t launch_rebuild_alpha(const OperatorDev& op, const WedgeDev& w, const SkelWedge& sk, int q,
+                                 const int* slot_x, long long nslots, void* alpha, bool c64, cudaStream_t s);
+
 // ---- apply-time kernels (the hot path) ----
 struct ApplyArgs {
   int N;
@@ -61,6 +73,8 @@ struct ApplyArgs {
   int fft_N;                // FftLen index of length N (input spectrum)
   const void* tw;           // twiddles (double2 or float2)
   const InterpWedge* iw;    // host array, one per owned wedge (passed by value to K3)
+  const WedgeDev* wd_host;  // host copy of the wedge table
+  const SkelWedge* skel;    // host array (skeleton mode) or nullptr: alpha' rebuilt before each K3
   const void* const* beta;  // per owned wedge
   OperatorDev op;
   const double2* a0;        // a(x,0)/N, N*N
