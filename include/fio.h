@@ -140,6 +140,13 @@ fio_status fio_apply(fio_handle h, const void* f_dev, void* Lf_dev, void* stream
  * spreading step accumulates with atomics: the last bits may vary between runs. */
 fio_status fio_apply_adjoint(fio_handle h, const void* g_dev, void* out_dev, void* stream);
 
+/* Multi-RHS apply (NEXT-2): Lf_b = L f_b for b < nrhs; f_dev and Lf_dev hold nrhs contiguous
+ * N x N complex arrays of the plan dtype (device, no aliasing).  The FFT stages run per input;
+ * per wedge the interpolation then serves every input from one alpha' (in skeleton storage mode
+ * alpha' is rebuilt once per wedge for the whole batch).  The first call with a larger nrhs
+ * allocates (nrhs - 1) extra spectra and fine-grid workspaces (synchronizing `stream`). */
+fio_status fio_apply_batch(fio_handle h, int nrhs, const void* f_dev, void* Lf_dev, void* stream);
+
 /* End-to-end variant: f_host / Lf_host are HOST buffers (pinned for overlap);
  * the host->device copy, the apply and the device->host copy are enqueued on
  * `stream`, which is synchronized before return. */

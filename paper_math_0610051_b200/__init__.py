@@ -32,7 +32,7 @@ FIO_C64, FIO_C128 = 1, 2
 FIO_OK, FIO_WNOTCERT = 0, 1
 
 # every entry point declared in include/fio.h
-SYMBOLS = ["fio_default_opts", "fio_plan", "fio_apply", "fio_apply_adjoint", "fio_apply_host", "fio_destroy", "fio_plan_info",
+SYMBOLS = ["fio_default_opts", "fio_plan", "fio_apply", "fio_apply_batch", "fio_apply_adjoint", "fio_apply_host", "fio_destroy", "fio_plan_info",
            "fio_plan_wedges", "fio_geometry", "fio_assign_wedges", "fio_profile_begin", "fio_profile_end",
            "fio_last_error", "fio_version"]
 STAGES = ["K0_rows", "K0_cols", "K1_rowpass", "K2_colpass", "K3_interp"]
@@ -95,6 +95,7 @@ def load_library():
     lib.fio_apply.argtypes = [P, P, P, P]
     lib.fio_apply_host.argtypes = [P, P, P, P]
     lib.fio_apply_adjoint.argtypes = [P, P, P, P]
+    lib.fio_apply_batch.argtypes = [P, I, P, P, P]
     lib.fio_destroy.argtypes = [P]
     lib.fio_plan_info.argtypes = [P, ctypes.POINTER(_Info)]
     lib.fio_plan_wedges.argtypes = [P, P, P, P, P, P, P, P]
@@ -104,7 +105,7 @@ def load_library():
     lib.fio_profile_end.argtypes = [P, P, P]
     lib.fio_last_error.restype = ctypes.c_char_p
     lib.fio_version.restype = ctypes.c_char_p
-    for name in ["fio_plan", "fio_apply", "fio_apply_adjoint", "fio_apply_host", "fio_destroy", "fio_plan_info", "fio_plan_wedges",
+    for name in ["fio_plan", "fio_apply", "fio_apply_batch", "fio_apply_adjoint", "fio_apply_host", "fio_destroy", "fio_plan_info", "fio_plan_wedges",
                  "fio_geometry", "fio_assign_wedges", "fio_profile_begin", "fio_profile_end"]:
         getattr(lib, name).restype = ctypes.c_int
     _lib = lib
@@ -234,6 +235,20 @@ class Plan:
             stream = torch.cuda.current_stream(f.device)
         _check(self._lib.fio_apply(self._h, ctypes.c_void_p(f.data_ptr()), ctypes.c_void_p(out.data_ptr()),
                                    ctypes.c_void_p(stream.cuda_stream)))
+        return out
+
+    def apply_batch(self, f, out=None, stream=None):
+        """L f_b for a device tensor f of shape (B, N, N) (plan dtype): one fio_apply_batch call."""
+        import torch
+        if not (f.is_cuda and f.dtype == self.torch_dtype and f.dim() == 3 and tuple(f.shape[1:]) == (self.N, self.N)):
+            raise FioError(-1, f"f must be a CUDA {self.torch_dtype} tensor of shape (B, {self.N}, {self.N})")
+        f = f.contiguous()
+        if out is None:
+            out = torch.empty_like(f)
+        if stream is None:
+            stream = torch.cuda.current_stream(f.device)
+        _check(self._lib.fio_apply_batch(self._h, int(f.shape[0]), ctypes.c_void_p(f.data_ptr()),
+                                         ctypes.c_void_p(out.data_ptr()), ctypes.c_void_p(stream.cuda_stream)))
         return out
 
     def apply_adjoint(self, g, out=None, stream=None):

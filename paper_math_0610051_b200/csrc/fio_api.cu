@@ -89,6 +89,8 @@ struct fio_plan_s {
   int njobs_row = 0, njobs_col = 0, smem_row = 0, smem_col = 0;
   int rows_per_cta_N = 1, cols_per_cta_N = 1, fft_N = 0;
   void *e2e_in = nullptr, *e2e_out = nullptr;
+  void* batch_ws = nullptr;  // (nrhs - 1) x (fhat + fine grids) for fio_apply_batch
+  int batch_cap = 1;
   size_t alpha_bytes = 0, beta_bytes = 0, ws_bytes = 0, fine_elems = 0, p1_elems = 0, meta_bytes = 0;
   long long slots = 0;
   long long slot_terms = 0;  // sum over owned wedges of padded K3 slots x q_l
@@ -124,6 +126,7 @@ struct fio_plan_s {
   }
   ~fio_plan_s() {
     free_events();
+    if (batch_ws) cudaFree(batch_ws);
     for (void* p : allocs) cudaFree(p);
   }
 };
@@ -910,6 +913,41 @@ fio_status fio_apply(fio_handle h, const void* f_dev, void* Lf_dev, void* stream
   if (h->prof_n < h->prof_cap) ev = &h->prof_ev[(size_t)h->prof_n++ * (kStages + 1)];
   FIO_CUDA(enqueue_apply(a, h->c64, f_dev, Lf_dev, (cudaStream_t)stream, &launches, ev));
   h->launches = launches;
+  return FIO_OK;
+}
+
+fio_status fio_apply_batch(fio_handle h, int nrhs, const void* f_dev, void* Lf_dev, void* stream) {
+  if (!h || !f_dev || !Lf_dev || nrhs < 1) {
+    set_error("fio_apply_batch: bad arguments");
+    return FIO_EINVAL;
+  }
+  if (f_dev == Lf_dev) {
+    set_error("fio_apply_batch: f and Lf must not alias");
+    return FIO_EINVAL;
+  }
+  int dev = -1;
+  cudaGetDevice(&dev);
+  if (dev != h->device) FIO_CUDA(cudaSetDevice(h->device));
+  const size_t cs = h->c64 ? sizeof(float2) : sizeof(double2);
+  const size_t NN = (size_t)h->N * h->N;
+  const size_t per = NN + std::max<size_t>(h->fine_elems, 1);
+  if (nrhs > h->batch_cap) {
+    FIO_CUDA(cudaStreamSynchronize((cudaStream_t)stream));
+    if (h->batch_ws) {
+      cudaFree(h->batch_ws);
+      h->batch_ws = nullptr;
+    }
+    FIO_CUDA(cudaMalloc(&h->batch_ws, cs * per * (size_t)(nrhs - 1)));
+    h->batch_cap = nrhs;
+  }
+  std::vector<ApplyArgs> args(nrhs, make_args(*h));
+  for (int b = 1; b < nrhs; ++b) {
+    char* base = static_cast<char*>(h->batch_ws) + cs * per * (size_t)(b - 1);
+    args[b].fhat = base;
+    args[b].g = base + cs * NN;
+  }
+  int launches = 0;
+  FIO_CUDA(enqueue_apply_batch(args.data(), nrhs, h->c64, f_dev, Lf_dev, (cudaStream_t)stream, &launches));
   return FIO_OK;
 }
 

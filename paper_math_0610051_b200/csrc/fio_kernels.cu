@@ -1119,12 +1119,16 @@ static cudaError_t launch_groups_tp(const ApplyArgs& a, int wi, T2* Lf, cudaStre
 }
 
 template <typename T2>
-static cudaError_t launch_interp(const ApplyArgs& a, T2* Lf, cudaStream_t s, int* n) {
+static cudaError_t launch_interp(const ApplyArgs* args, int nrhs, T2* Lf0, cudaStream_t s, int* n) {
+  const ApplyArgs& a = args[0];
+  const long long NN = (long long)a.N * a.N;
   if (a.nw == 0) {
-    long long NN = (long long)a.N * a.N;
     int blocks = (int)std::min<long long>((NN + 255) / 256, 148LL * 8);
-    k_dc_only<T2><<<blocks, 256, 0, s>>>(a.N, a.a0, reinterpret_cast<const T2*>(a.fhat), a.add_dc, Lf);
-    ++*n;
+    for (int b = 0; b < nrhs; ++b) {
+      k_dc_only<T2><<<blocks, 256, 0, s>>>(a.N, a.a0, reinterpret_cast<const T2*>(args[b].fhat), a.add_dc,
+                                            Lf0 + b * NN);
+      ++*n;
+    }
     return cudaGetLastError();
   }
   for (int wi = 0; wi < a.nw; ++wi) {
@@ -1137,24 +1141,28 @@ static cudaError_t launch_interp(const ApplyArgs& a, T2* Lf, cudaStream_t s, int
       if (e != cudaSuccess) return e;
       ++*n;
     }
-#define FIO_GROUPS_CASE(TP)                                            \
-  case TP:                                                             \
-    e = launch_groups_tp<T2, TP, GroupP<T2>::value>(a, wi, Lf, s);     \
+    // one alpha' (rebuilt once in skeleton mode) serves every right-hand side (NEXT-2)
+    for (int b = 0; b < nrhs; ++b) {
+      T2* Lf = Lf0 + b * NN;
+#define FIO_GROUPS_CASE(TP)                                                  \
+  case TP:                                                                   \
+    e = launch_groups_tp<T2, TP, GroupP<T2>::value>(args[b], wi, Lf, s);     \
     break;
-    switch (a.taps) {
-      FIO_GROUPS_CASE(3)
-      FIO_GROUPS_CASE(4)
-      FIO_GROUPS_CASE(5)
-      FIO_GROUPS_CASE(6)
-      FIO_GROUPS_CASE(7)
-      FIO_GROUPS_CASE(8)
-      FIO_GROUPS_CASE(9)
-      FIO_GROUPS_CASE(10)
-      default: return cudaErrorInvalidValue;
-    }
+      switch (a.taps) {
+        FIO_GROUPS_CASE(3)
+        FIO_GROUPS_CASE(4)
+        FIO_GROUPS_CASE(5)
+        FIO_GROUPS_CASE(6)
+        FIO_GROUPS_CASE(7)
+        FIO_GROUPS_CASE(8)
+        FIO_GROUPS_CASE(9)
+        FIO_GROUPS_CASE(10)
+        default: return cudaErrorInvalidValue;
+      }
 #undef FIO_GROUPS_CASE
-    if (e != cudaSuccess) return e;
-    ++*n;
+      if (e != cudaSuccess) return e;
+      ++*n;
+    }
   }
   return cudaSuccess;
 }
@@ -1461,22 +1469,26 @@ cudaError_t configure_kernels(size_t smem_bytes) {
 }
 
 template <typename T2>
-static cudaError_t enqueue_apply_t(const ApplyArgs& a, const T2* f, T2* Lf, cudaStream_t s, int* launches,
-                                   cudaEvent_t* ev) {
+static cudaError_t enqueue_apply_t(const ApplyArgs* args, int nrhs, const T2* f0, T2* Lf, cudaStream_t s,
+                                   int* launches, cudaEvent_t* ev) {
   cudaError_t e;
   int n = 0;
   int stage = 0;
   auto mark = [&]() {
-    if (ev) cudaEventRecord(ev[stage], s);
+    if (ev && nrhs == 1) cudaEventRecord(ev[stage], s);
     ++stage;
   };
   mark();
-  const T2* tw = reinterpret_cast<const T2*>(a.tw);
-  T2* fhat = reinterpret_cast<T2*>(a.fhat);
-  T2* tmp = reinterpret_cast<T2*>(a.tmp);
-  const size_t seq = fft_seq_bytes(a.N, sizeof(T2) == sizeof(float2));
-  // K0: fhat = FFT2(f) / N  (forward sign, eq. dft)
-  {
+  const ApplyArgs& a0 = args[0];
+  const T2* tw = reinterpret_cast<const T2*>(a0.tw);
+  const size_t seq = fft_seq_bytes(a0.N, sizeof(T2) == sizeof(float2));
+  const long long NN = (long long)a0.N * a0.N;
+  for (int b = 0; b < nrhs; ++b) {
+    const ApplyArgs& a = args[b];
+    const T2* f = f0 + b * NN;
+    T2* fhat = reinterpret_cast<T2*>(a.fhat);
+    T2* tmp = reinterpret_cast<T2*>(a.tmp);
+    // K0: fhat = FFT2(f) / N  (forward sign, eq. dft)
     int rpc = a.rows_per_cta_N;
     k_fft_rows<T2><<<(a.N + rpc - 1) / rpc, 256, rpc * seq, s>>>(f, tmp, a.N, rpc, a.ffts, a.fft_N, tw, -1, 1.0);
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
@@ -1488,24 +1500,24 @@ static cudaError_t enqueue_apply_t(const ApplyArgs& a, const T2* f, T2* Lf, cuda
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
     ++n;
     mark();
+    if (a.nw > 0) {
+      const T2* const* betas = reinterpret_cast<const T2* const*>(a.beta);
+      k_rowpass<T2><<<a.njobs_row, 256, a.smem_row, s>>>(a.N, a.wedges, a.jobs_row, a.ffts, tw, betas, fhat,
+                                                         reinterpret_cast<T2*>(a.p1));
+      if ((e = cudaGetLastError()) != cudaSuccess) return e;
+      ++n;
+      mark();
+      k_colpass<T2><<<a.njobs_col, 256, a.smem_col, s>>>(a.wedges, a.jobs_col, a.ffts, tw,
+                                                         reinterpret_cast<const T2*>(a.p1), reinterpret_cast<T2*>(a.g));
+      if ((e = cudaGetLastError()) != cudaSuccess) return e;
+      ++n;
+      mark();
+    } else {
+      mark();
+      mark();
+    }
   }
-  if (a.nw > 0) {
-    const T2* const* betas = reinterpret_cast<const T2* const*>(a.beta);
-    k_rowpass<T2><<<a.njobs_row, 256, a.smem_row, s>>>(a.N, a.wedges, a.jobs_row, a.ffts, tw, betas, fhat,
-                                                       reinterpret_cast<T2*>(a.p1));
-    if ((e = cudaGetLastError()) != cudaSuccess) return e;
-    ++n;
-    mark();
-    k_colpass<T2><<<a.njobs_col, 256, a.smem_col, s>>>(a.wedges, a.jobs_col, a.ffts, tw,
-                                                       reinterpret_cast<const T2*>(a.p1), reinterpret_cast<T2*>(a.g));
-    if ((e = cudaGetLastError()) != cudaSuccess) return e;
-    ++n;
-    mark();
-  } else {
-    mark();
-    mark();
-  }
-  if ((e = launch_interp<T2>(a, Lf, s, &n)) != cudaSuccess) return e;
+  if ((e = launch_interp<T2>(args, nrhs, Lf, s, &n)) != cudaSuccess) return e;
   mark();
   if (launches) *launches = n;
   return cudaSuccess;
@@ -1513,8 +1525,14 @@ static cudaError_t enqueue_apply_t(const ApplyArgs& a, const T2* f, T2* Lf, cuda
 
 cudaError_t enqueue_apply(const ApplyArgs& a, bool c64, const void* f, void* Lf, cudaStream_t s, int* launches,
                           cudaEvent_t* ev) {
-  if (c64) return enqueue_apply_t<float2>(a, (const float2*)f, (float2*)Lf, s, launches, ev);
-  return enqueue_apply_t<double2>(a, (const double2*)f, (double2*)Lf, s, launches, ev);
+  if (c64) return enqueue_apply_t<float2>(&a, 1, (const float2*)f, (float2*)Lf, s, launches, ev);
+  return enqueue_apply_t<double2>(&a, 1, (const double2*)f, (double2*)Lf, s, launches, ev);
+}
+
+cudaError_t enqueue_apply_batch(const ApplyArgs* args, int nrhs, bool c64, const void* f, void* Lf, cudaStream_t s,
+                                int* launches) {
+  if (c64) return enqueue_apply_t<float2>(args, nrhs, (const float2*)f, (float2*)Lf, s, launches, nullptr);
+  return enqueue_apply_t<double2>(args, nrhs, (const double2*)f, (double2*)Lf, s, launches, nullptr);
 }
 
 }  // namespace fio

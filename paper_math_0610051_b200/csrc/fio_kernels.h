@@ -103,6 +103,11 @@ cudaError_t enqueue_apply(const ApplyArgs& a, bool c64, const void* f, void* Lf,
                           cudaEvent_t* ev = nullptr);
 constexpr int kStages = 5;
 
+// Multi-RHS apply (NEXT-2): args[b] differ only in the per-RHS workspace (fhat, fine grids);
+// f and Lf hold nrhs contiguous N x N arrays.  In skeleton mode alpha' is rebuilt once per wedge.
+cudaError_t enqueue_apply_batch(const ApplyArgs* args, int nrhs, bool c64, const void* f, void* Lf, cudaStream_t s,
+                                int* launches);
+
 // Enqueue the exact adjoint of the fast operator: out = L~* g.
 cudaError_t enqueue_adjoint(const ApplyArgs& a, bool c64, const void* g, void* out, cudaStream_t s, int* launches);
 

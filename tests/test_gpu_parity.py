@@ -326,3 +326,19 @@ def test_skeleton_storage_matches_stored_alpha(dtype, eps):
         Lsg = p_sk.apply_adjoint(torch.from_numpy(g).to(DEV)).cpu().numpy()
         Lf = p_sk.apply(torch.from_numpy(f).to(DEV)).cpu().numpy()
         assert abs(np.vdot(g, Lf) - np.vdot(Lsg, f)) <= 1e-12 * np.linalg.norm(f) * np.linalg.norm(g) * N
+
+
+# ------------------------------------------------------------------ multi-RHS (NEXT-2)
+@pytest.mark.parametrize("skeleton", [False, True])
+def test_apply_batch_equals_single_applies(skeleton):
+    N = 64
+    op = wl.grt_operator(N)
+    plan = make_plan(op, 1e-6, skeleton=skeleton)
+    fs = np.stack([crandn(N, 60 + b) for b in range(3)])
+    out = plan.apply_batch(torch.from_numpy(fs).to(DEV)).cpu().numpy()
+    for b in range(3):
+        single = plan.apply(torch.from_numpy(fs[b]).to(DEV)).cpu().numpy()
+        assert np.array_equal(out[b], single)
+    assert oracle.rel_l2(out[1], oracle.fio(op, fs[1])) <= 1e-5
+    out5 = plan.apply_batch(torch.from_numpy(np.concatenate([fs, fs[:2]])).to(DEV)).cpu().numpy()  # workspace grows
+    assert np.array_equal(out5[4], out[1])
