@@ -293,6 +293,14 @@ def time_config(name, args, rank, world, local, group):
     k3_ms = stages["K3_interp"] / n
     hbm, src = peaks()
     k3_bytes = k3_algorithmic_bytes(info, N, c64)
+    traffic = None  # DRAM bytes of all K3 launches of one apply, from the committed ncu capture
+    try:
+        with open(os.path.join(ROOT, "profiles", "r01_k3_traffic.json")) as fh:
+            tr = json.load(fh).get(name)
+        if tr and world == 1:
+            traffic = tr["dram_bytes"]
+    except Exception:
+        traffic = None
     ach = k3_bytes / (k3_ms * 1e-3) / 1e9
     total_stage = sum(stages[k] for k in fio.STAGES) / n
     res = {
@@ -301,7 +309,8 @@ def time_config(name, args, rank, world, local, group):
         "stage_ms": {k: stages[k] / n for k in fio.STAGES},
         "k3_share": k3_ms / total_stage if total_stage > 0 else None,
         "roofline": {"bound": "hbm", "achieved": ach, "peak": hbm, "unit": "GB/s", "frac": ach / hbm,
-                     "traffic": None, "kernel": "k_interp (K3)", "peak_source": src,
+                     "traffic": traffic, "kernel": "k_interp_groups (K3, all wedge launches of one apply)",
+                     "peak_source": src, "traffic_source": "profiles/r01_k3_traffic.json (ncu, cold cache)",
                      "algorithmic_bytes": k3_bytes},
         "apply_hbm_gbs": apply_algorithmic_bytes(info, N, c64) / (ms_step * 1e-3) / 1e9,
         "k3_resources": k3_resource_model(info, c64, k3_ms, clk.summary().get("sm_mhz")),
