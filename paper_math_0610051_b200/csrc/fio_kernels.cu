@@ -1185,6 +1185,18 @@ __device__ __forceinline__ void red_add(double2* p, double2 v) {
   atomicAdd(&p->y, v.y);
 }
 
+template <typename T2>
+__device__ __forceinline__ T2 shfl_down_t2(T2 v, int d) {
+  T2 r;
+  r.x = __shfl_down_sync(0xffffffffu, v.x, d);
+  r.y = __shfl_down_sync(0xffffffffu, v.y, d);
+  return r;
+}
+
+// K3*: one thread per group (persistent grid-stride loop, whole warps iterate together).  Lanes
+// whose groups share an anchor (same supercell: identical windows, consecutive in the sorted group
+// order) are summed with a segmented shuffle reduction first, so only the segment head issues the
+// RED atomics for each window cell.
 template <typename T2, int TAPS, int P>
 __global__ void __launch_bounds__(128) k_spread_groups(InterpWedge iw, T2* __restrict__ gstar,
                                                        const T2* __restrict__ g, double es_beta, EsPoly poly) {
@@ -1200,15 +1212,39 @@ __global__ void __launch_bounds__(128) k_spread_groups(InterpWedge iw, T2* __res
   T2* __restrict__ G = gstar + iw.g_off + kHalo;
   const T2* __restrict__ alpha = reinterpret_cast<const T2*>(iw.alpha);
   const O2* __restrict__ offs = reinterpret_cast<const O2*>(iw.slot_off);
-  for (int grp = blockIdx.x * blockDim.x + threadIdx.x; grp < iw.ngroups; grp += gridDim.x * blockDim.x) {
-    const int a1 = iw.anchor[2 * grp], a2 = iw.anchor[2 * grp + 1];
+  const int lane = threadIdx.x & 31;
+  const int stride = gridDim.x * blockDim.x;
+  // whole warps step through the groups so that the shuffles below see converged warps
+  for (int base = (blockIdx.x * blockDim.x + threadIdx.x) - lane; base < iw.ngroups; base += stride) {
+    const int grp = base + lane;
+    const bool valid = grp < iw.ngroups;
+    int a1 = 0, a2 = 0;
+    if (valid) {
+      a1 = iw.anchor[2 * grp];
+      a2 = iw.anchor[2 * grp + 1];
+    }
+    // segment = run of consecutive lanes with the same anchor; run_len = lanes from me to the run end
+    const unsigned long long key = valid ? (((unsigned long long)(unsigned)a1 << 32) | (unsigned)a2) : ~0ull;
+    const unsigned same = __match_any_sync(0xffffffffu, key);
+    const unsigned above = same >> lane;                   // bit 0 = me
+    const int run = __ffs(~above) - 1;                     // contiguous lanes from me with my key
+    const bool head = lane == 0 || !((same >> (lane - 1)) & 1u);
+    int maxrun = run;
+#pragma unroll
+    for (int d = 16; d > 0; d >>= 1) maxrun = max(maxrun, __shfl_xor_sync(0xffffffffu, maxrun, d));
     const int r0 = a1 < 0 ? a1 + n1f : a1;
     Rt p1[P][WINR], p2[P][WIN];
     T2 gx[P];
 #pragma unroll
     for (int k = 0; k < P; ++k) {
-      const int x = iw.slot_x[grp * P + k];
-      const O2 o = offs[grp * P + k];
+      int x = -1;
+      O2 o;
+      o.x = (Rt)(0.5 * TAPS);
+      o.y = (Rt)(0.5 * TAPS);
+      if (valid) {
+        x = iw.slot_x[grp * P + k];
+        o = offs[grp * P + k];
+      }
       gx[k] = x >= 0 ? g[x] : mk<T2>(0, 0);
       window_weights<Rt, TAPS, WINR>((Rt)o.x, inv_half_w, beta, poly, p1[k]);
       window_weights<Rt, TAPS, WIN>((Rt)o.y, inv_half_w, beta, poly, p2[k]);
@@ -1217,7 +1253,7 @@ __global__ void __launch_bounds__(128) k_spread_groups(InterpWedge iw, T2* __res
       T2 c[P];
 #pragma unroll
       for (int k = 0; k < P; ++k) {
-        const T2 av = alpha[t * nslots + (long long)grp * P + k];  // conj(alpha') g
+        const T2 av = valid ? alpha[t * nslots + (long long)grp * P + k] : mk<T2>(0, 0);  // conj(alpha') g
         c[k] = mk<T2>(av.x * gx[k].x + av.y * gx[k].y, av.x * gx[k].y - av.y * gx[k].x);
       }
       T2* __restrict__ rp = G + t * gstride + (long long)r0 * n2p + a2;
@@ -1232,7 +1268,12 @@ __global__ void __launch_bounds__(128) k_spread_groups(InterpWedge iw, T2* __res
           T2 v = mk<T2>(0, 0);
 #pragma unroll
           for (int k = 0; k < P; ++k) v = cfma_real(p2[k][j], e[k], v);
-          red_add(rp + j, v);
+          // segmented sum toward the run head: after the steps d < maxrun, the head holds the run total
+          for (int d = 1; d < maxrun; d <<= 1) {
+            const T2 u = shfl_down_t2(v, d);
+            if (d < run) v = cadd(v, u);
+          }
+          if (head && valid) red_add(rp + j, v);
         }
         rp += (r + 1 == n1f) ? -(long long)(n1f - 1) * n2p : (long long)n2p;
         r = (r + 1 == n1f) ? 0 : r + 1;
