@@ -609,6 +609,11 @@ fio_status build_plan(fio_plan_s& P, const fio_phase* phase, const fio_amplitude
     SkelWedge sk{};
     if (P.opts.skeleton) {
       // alpha' is rebuilt before every K3 launch into one shared scratch (allocated below)
+      if (q > 64) {
+        set_error("fio_plan: skeleton storage supports separation ranks q <= 64 (wedge " + std::to_string(g.l) +
+                  " has q = " + std::to_string(q) + ")");
+        return FIO_EINVAL;
+      }
       sk.rc = q > 0 ? (int)Cs.size() : 0;
       int* dC = nullptr;
       double2* dYs = nullptr;

@@ -80,15 +80,13 @@ __device__ __forceinline__ void warped_point(const OperatorDev& op, int n1, int 
 }
 
 // ------------------------------------------------------------------ plan kernels
-// Residual kernel entry A(x, xi) = a(x, xi) e^{2 pi i (rho(x,xi) - grad rho(x,xihat).xi)}.
-__device__ double2 kernel_entry(const OperatorDev& op, int x, int kf, double u1, double u2) {
+// Residual kernel entry A(x, xi) = a(x, xi) e^{2 pi i (rho(x,xi) - grad rho(x,xihat).xi)}; the
+// x-only quantities (c1, c2, grad rho(x, xihat)) are passed in.
+__device__ double2 kernel_entry_x(const OperatorDev& op, int x, double c1, double c2, double g1, double g2, int kf) {
   const int N = op.N;
   int k1 = kf / N, k2 = kf - k1 * N;
   double xi1 = (double)(k1 >= N / 2 ? k1 - N : k1);
   double xi2 = (double)(k2 >= N / 2 ? k2 - N : k2);
-  double c1 = op.c1[x], c2 = op.c2[x];
-  double g1, g2;
-  grad_rho(c1, c2, u1, u2, g1, g2);
   double rho = sqrt(c1 * c1 * xi1 * xi1 + c2 * c2 * xi2 * xi2);
   double ph = op.sign * (rho - g1 * xi1 - g2 * xi2);
   ph -= floor(ph);
@@ -112,6 +110,13 @@ __device__ double2 kernel_entry(const OperatorDev& op, int x, int kf, double u1,
     e = cmul(a, e);
   }
   return e;
+}
+
+__device__ double2 kernel_entry(const OperatorDev& op, int x, int kf, double u1, double u2) {
+  const double c1 = op.c1[x], c2 = op.c2[x];
+  double g1, g2;
+  grad_rho(c1, c2, u1, u2, g1, g2);
+  return kernel_entry_x(op, x, c1, c2, g1, g2, kf);
 }
 
 __global__ void k_eval_entries(OperatorDev op, double u1, double u2, const int* __restrict__ rows, int nr,
@@ -276,12 +281,18 @@ cudaError_t launch_fold_alpha(const OperatorDev& op, const WedgeDev& w, const do
 // Skeleton storage (eq. probnewfac): U = A_[C] V S^{-1} is regenerated from
 // the kernel entries A(x, C_c) -- never stored -- folded with the center phase and 1/N.
 // Thread per slot; terms in chunks of 16 accumulators (entries recomputed per chunk).
-template <typename T2>
+template <typename T2, int QMAX>
 __global__ void __launch_bounds__(128) k_rebuild_alpha(OperatorDev op, WedgeDev w, SkelWedge sk, int q,
                                                        const int* __restrict__ slot_x, long long nslots,
                                                        T2* __restrict__ alpha) {
+  // Y = V S^{-1} (rc x q) and the skeleton columns C staged once per CTA in shared memory
+  extern __shared__ __align__(16) unsigned char rb_smem[];
+  double2* Ys = reinterpret_cast<double2*>(rb_smem);
+  int* Cs = reinterpret_cast<int*>(Ys + (size_t)sk.rc * q);
+  for (int i = threadIdx.x; i < sk.rc * q; i += blockDim.x) Ys[i] = sk.Y[i];
+  for (int i = threadIdx.x; i < sk.rc; i += blockDim.x) Cs[i] = sk.C[i];
+  __syncthreads();
   const int N = op.N;
-  constexpr int TC = 16;
   for (long long sl = blockIdx.x * (long long)blockDim.x + threadIdx.x; sl < nslots;
        sl += (long long)gridDim.x * blockDim.x) {
     const int x = slot_x[sl];
@@ -296,32 +307,56 @@ __global__ void __launch_bounds__(128) k_rebuild_alpha(OperatorDev op, WedgeDev 
     double sn, cs;
     sincospi(2.0 * ph, &sn, &cs);
     const double2 e = make_double2(cs / N, sn / N);
-    for (int t0 = 0; t0 < q; t0 += TC) {
-      double2 acc[TC];
+    const double c1 = op.c1[x], c2 = op.c2[x];
+    double g1, g2;
+    grad_rho(c1, c2, w.u1, w.u2, g1, g2);
+    double2 acc[QMAX];
 #pragma unroll
-      for (int k = 0; k < TC; ++k) acc[k] = make_double2(0.0, 0.0);
-      for (int c = 0; c < sk.rc; ++c) {
-        const double2 a = kernel_entry(op, x, sk.C[c], w.u1, w.u2);
+    for (int k = 0; k < QMAX; ++k) acc[k] = make_double2(0.0, 0.0);
+    for (int c = 0; c < sk.rc; ++c) {
+      const double2 a = kernel_entry_x(op, x, c1, c2, g1, g2, Cs[c]);
+      const double2* yc = Ys + c;
 #pragma unroll
-        for (int k = 0; k < TC; ++k)
-          if (t0 + k < q) acc[k] = cadd(acc[k], cmul(a, sk.Y[c + (long long)(t0 + k) * sk.rc]));
-      }
-#pragma unroll
-      for (int k = 0; k < TC; ++k)
-        if (t0 + k < q) alpha[(t0 + k) * nslots + sl] = to_t2<T2>(cmul(acc[k], e));
+      for (int k = 0; k < QMAX; ++k)
+        if (k < q) {
+          const double2 yv = yc[(long long)k * sk.rc];
+          acc[k].x = fma(a.x, yv.x, fma(-a.y, yv.y, acc[k].x));
+          acc[k].y = fma(a.x, yv.y, fma(a.y, yv.x, acc[k].y));
+        }
     }
+#pragma unroll
+    for (int k = 0; k < QMAX; ++k)
+      if (k < q) alpha[k * nslots + sl] = to_t2<T2>(cmul(acc[k], e));
   }
+}
+
+template <typename T2, int QMAX>
+static cudaError_t launch_rebuild_q(const OperatorDev& op, const WedgeDev& w, const SkelWedge& sk, int q,
+                                    const int* slot_x, long long nslots, T2* alpha, cudaStream_t s) {
+  const size_t smem = sizeof(double2) * (size_t)sk.rc * q + sizeof(int) * (size_t)sk.rc;
+  static size_t configured = 0;
+  if (smem > 48 * 1024 && smem > configured) {
+    cudaError_t e = cudaFuncSetAttribute(k_rebuild_alpha<T2, QMAX>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)smem);
+    if (e != cudaSuccess) return e;
+    configured = smem;
+  }
+  int blocks = (int)std::min<long long>((nslots + 127) / 128, 148LL * 8);
+  k_rebuild_alpha<T2, QMAX><<<blocks, 128, smem, s>>>(op, w, sk, q, slot_x, nslots, alpha);
+  return cudaGetLastError();
 }
 
 cudaError_t launch_rebuild_alpha(const OperatorDev& op, const WedgeDev& w, const SkelWedge& sk, int q,
                                  const int* slot_x, long long nslots, void* alpha, bool c64, cudaStream_t s) {
   if (nslots == 0 || q == 0) return cudaSuccess;
-  int blocks = (int)std::min<long long>((nslots + 127) / 128, 148LL * 16);
-  if (c64)
-    k_rebuild_alpha<float2><<<blocks, 128, 0, s>>>(op, w, sk, q, slot_x, nslots, (float2*)alpha);
-  else
-    k_rebuild_alpha<double2><<<blocks, 128, 0, s>>>(op, w, sk, q, slot_x, nslots, (double2*)alpha);
-  return cudaGetLastError();
+  if (q > 64) return cudaErrorInvalidValue;  // plan caps the separation rank far below (r_max / 4 * 3)
+#define FIO_RB(QM)                                                                                        \
+  return c64 ? launch_rebuild_q<float2, QM>(op, w, sk, q, slot_x, nslots, (float2*)alpha, s)              \
+             : launch_rebuild_q<double2, QM>(op, w, sk, q, slot_x, nslots, (double2*)alpha, s);
+  if (q <= 16) { FIO_RB(16) }
+  if (q <= 32) { FIO_RB(32) }
+  FIO_RB(64)
+#undef FIO_RB
 }
 
 // Fine-grid coordinates u = frac(y_l(x)) (n1f, n2f) of every output point (plan time, FP64).
