@@ -342,3 +342,44 @@ def test_apply_batch_equals_single_applies(skeleton):
     assert oracle.rel_l2(out[1], oracle.fio(op, fs[1])) <= 1e-5
     out5 = plan.apply_batch(torch.from_numpy(np.concatenate([fs, fs[:2]])).to(DEV)).cpu().numpy()  # workspace grows
     assert np.array_equal(out5[4], out[1])
+
+
+# ------------------------------------------------------------------ options and argument checking
+@pytest.mark.parametrize("kw", [dict(n_wedges=16), dict(n_wedges=8, nufft_w=8), dict(r_init=16), dict(seed=7)])
+def test_plan_options_keep_parity(kw):
+    # L does not depend on W (sum chi_l = 1), the taps, the skeleton size or the seed
+    N = 64
+    op = wl.grt_operator(N)
+    f = wl.white_noise(N, 8)
+    plan, out = run(op, f, **kw)
+    assert oracle.rel_l2(out, oracle.fio(op, f)) <= 1e-5
+    info = plan.info
+    if "n_wedges" in kw:
+        assert info["W"] == kw["n_wedges"]
+    if "nufft_w" in kw:
+        assert info["nufft_w"] == kw["nufft_w"]
+
+
+def test_loose_eps_and_status():
+    N = 32
+    op = wl.grt_operator(N)
+    f = wl.white_noise(N, 9)
+    plan, out = run(op, f, eps=0.05)
+    assert plan.status in (fio.FIO_OK, fio.FIO_WNOTCERT)
+    assert oracle.rel_l2(out, oracle.fio(op, f)) <= 0.5
+    assert plan.info["nufft_w"] >= 4
+
+
+def test_more_invalid_arguments():
+    op = wl.grt_operator(64)
+    with pytest.raises(fio.FioError):
+        fio.Plan(64, op.c1, op.c2, amplitude="bogus", device=0)
+    with pytest.raises(fio.FioError):
+        fio.Plan(64, op.c1, op.c2, nufft_w=2, device=0)
+    with pytest.raises(fio.FioError):
+        fio.Plan(64, op.c1[:10], op.c2, device=0)
+    plan = fio.Plan(64, op.c1, op.c2, eps=1e-4, device=0)
+    with pytest.raises(fio.FioError):
+        plan.apply(torch.zeros((64, 64), dtype=torch.complex64, device=DEV))   # wrong dtype
+    with pytest.raises(fio.FioError):
+        plan.apply(torch.zeros((32, 32), dtype=torch.complex128, device=DEV))  # wrong shape
