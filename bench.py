@@ -121,7 +121,7 @@ def k3_resource_model(info, c64, ms, sm_mhz):
     (128 FP32 or 64 FP64 FMA/clk/SM) at the measured SM clock."""
     w = info["nufft_w"]
     P = info["group_p"]
-    win, winr = w + 1, (w + 2) & ~1
+    win, winr = w + 1, info.get("k3_window_rows") or w
     cs, rs = (8, 4) if c64 else (16, 8)
     gt = info["slot_terms"] / P
     lsu_bytes = gt * (winr * win * cs + winr * P * rs + P * cs)

@@ -171,6 +171,7 @@ typedef struct {
   double rank_balance;    /* predicted max/mean per-rank cost of the wedge assignment (1 if nranks = 1) */
   long long slot_terms;   /* sum over owned wedges of K3 slots x q_l (K3 work units per apply) */
   int group_p;            /* points per K3 group */
+  int k3_window_rows;     /* rows of the K3 interpolation window (w or w+1 rounded up to even) */
   size_t skeleton_bytes;  /* skeleton storage: C and V S^{-1} of every owned wedge (0 otherwise);
                              alpha_bytes is then the size of the shared rebuild scratch */
 } fio_info;

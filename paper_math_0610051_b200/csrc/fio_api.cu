@@ -572,7 +572,7 @@ fio_status build_plan(fio_plan_s& P, const fio_phase* phase, const fio_amplitude
       for (long long x = 0; x < NN; ++x) std::swap(uh[2 * x], uh[2 * x + 1]);  // (K3 row, column) = (u2, u1)
       std::vector<int> anchor, slot_x;
       std::vector<double> off;
-      group_points(uh.data(), NN, P.taps, group_p(c64), g.n2f, g.n1f, anchor, slot_x, off);
+      group_points(uh.data(), NN, P.taps, group_p(c64), g.n2f, g.n1f, super_rows(c64), anchor, slot_x, off);
       iw.ngroups = (int)(anchor.size() / 2);
       int* d_anchor = nullptr;
       int* d_slot = nullptr;
@@ -592,7 +592,7 @@ fio_status build_plan(fio_plan_s& P, const fio_phase* phase, const fio_amplitude
       iw.slot_x = d_slot;
       std::vector<int> box;
       const int blk = c64 ? kK3BlockC64 : kK3BlockC128;
-      const long long cap = chunk_boxes(anchor, blk, (P.taps + 2) & ~1, P.taps + 1,
+      const long long cap = chunk_boxes(anchor, blk, k3_window_rows(P.taps, c64), P.taps + 1,
                                         c64 ? kK3TileCapC64 : kK3TileCapC128, box, c64 ? 8 : 16);
       iw.nchunks = (int)(box.size() / 6);
       P.chunk_threads += (long long)iw.nchunks * blk;
@@ -1061,6 +1061,7 @@ fio_status fio_plan_info(fio_handle h, fio_info* info) {
   info->slot_terms = h->slot_terms;
   info->group_p = group_p(h->c64);
   info->skeleton_bytes = h->skel_bytes;
+  info->k3_window_rows = k3_window_rows(h->taps, h->c64);
   info->beta_bytes = h->beta_bytes;
   info->workspace_bytes = h->ws_bytes;
   info->fine_elems = h->fine_elems;

@@ -20,7 +20,22 @@ constexpr int kK3BlockC128 = 128;  // complex128
 constexpr int kK3Stages = 3;       // cp.async pipeline depth of K3 (fine-grid tiles + alpha')
 constexpr int kK3TileCapC64 = 2048;   // max cells of a K3 chunk footprint, complex64
 constexpr int kK3TileCapC128 = 1024;  // complex128
-constexpr int kHalo = 8;    // periodic column halo on each side of a fine-grid row (K2 writes, K3 reads)
+constexpr int kHalo = 8;
+// K3 supercell shape: super_rows x 2 base cells.  1 groups points with the same base row (window
+// w rows x (w+1) columns); 2 gives (w+1) x (w+1) windows (rounded up to even rows).  Measured on
+// B200: 1 is slightly faster for complex64 (3.64 vs 3.68 ms), 2 clearly faster for complex128
+// (17.6 vs 20.0 ms) at N = 1024.
+constexpr int kSuperRowsC64 = 1;
+constexpr int kSuperRowsC128 = 2;
+#ifdef __CUDACC__
+#define FIO_HD __host__ __device__
+#else
+#define FIO_HD
+#endif
+FIO_HD constexpr int super_rows(bool c64) { return c64 ? kSuperRowsC64 : kSuperRowsC128; }
+FIO_HD constexpr int k3_window_rows(int taps, bool c64) {
+  return super_rows(c64) == 1 ? taps : ((taps + 2) & ~1);
+}    // periodic column halo on each side of a fine-grid row (K2 writes, K3 reads)
 
 // Division by a runtime constant d via multiply-high (Granlund-Montgomery), exact for
 // numerators n < 2^31: q = (umulhi(m, n) + n) >> l.
@@ -126,8 +141,8 @@ void lpt_assign(int W, const double* cost, int nranks, int* owner);
 // Group the output points of one wedge for K3 (see InterpWedge).  u: 2*NN doubles
 // (K3 row / column fine coordinates in [0, n1f) x [0, n2f)).  Outputs: anchor (2 per group),
 // slot_x (P per group, -1 padding), off (2 per slot: u - anchor).
-void group_points(const double* u, long long NN, int taps, int P, int n1f, int n2f, std::vector<int>& anchor,
-                  std::vector<int>& slot_x, std::vector<double>& off);
+void group_points(const double* u, long long NN, int taps, int P, int n1f, int n2f, int super_rows,
+                  std::vector<int>& anchor, std::vector<int>& slot_x, std::vector<double>& off);
 long long chunk_boxes(const std::vector<int>& anchor, int block, int win_rows, int win_cols, long long cap,
                       std::vector<int>& box, int elem_bytes);
 

@@ -909,7 +909,7 @@ __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_gr
 template <typename T2, int TAPS, int P>
 __host__ __device__ constexpr size_t k3_fixed_smem() {
   return sizeof(T2) * kK3Stages * K3Cfg<T2>::BLOCK * P +
-         (K3Cfg<T2>::P1REG ? 0 : sizeof(typename Real<T2>::type) * P * ((TAPS + 2) & ~1) * K3Cfg<T2>::BLOCK);
+         (K3Cfg<T2>::P1REG ? 0 : sizeof(typename Real<T2>::type) * P * k3_window_rows(TAPS, sizeof(T2) == 8) * K3Cfg<T2>::BLOCK);
 }
 
 // K3: one CTA processes chunks of BLOCK consecutive groups (one group of P points per
@@ -930,7 +930,7 @@ __global__ void __launch_bounds__(K3Cfg<T2>::BLOCK, K3Cfg<T2>::MINB)
   using Rt = typename Real<T2>::type;
   using O2 = typename OffT<T2>::type;
   constexpr int WIN = TAPS + 1;         // window columns
-  constexpr int WINR = (WIN + 1) & ~1;  // window rows (even; the extra row has weight 0)
+  constexpr int WINR = k3_window_rows(TAPS, sizeof(T2) == 8);  // window rows (super_rows 2: even, extra row weight 0)
   constexpr int BLOCK = K3Cfg<T2>::BLOCK;
   constexpr int S = kK3Stages;
   constexpr int ACH = P * (int)sizeof(T2) / 16;  // 16-byte alpha' chunks per (group, t)
@@ -1238,7 +1238,7 @@ __global__ void __launch_bounds__(128) k_spread_groups(InterpWedge iw, T2* __res
   using Rt = typename Real<T2>::type;
   using O2 = typename OffT<T2>::type;
   constexpr int WIN = TAPS + 1;
-  constexpr int WINR = (WIN + 1) & ~1;
+  constexpr int WINR = k3_window_rows(TAPS, sizeof(T2) == 8);
   const Rt inv_half_w = (Rt)(2.0 / TAPS);
   const Rt beta = (Rt)es_beta;
   const int n1f = iw.nrow, n2p = iw.ncolp, q = iw.q;
