@@ -867,6 +867,21 @@ __device__ __forceinline__ void load_p1(const Rt* p, Rt (&w)[P]) {
   }
 }
 
+// P FP32 row weights (16-byte vector loads), widened to the compute type
+template <typename Rt, int P>
+__device__ __forceinline__ void load_p1_f(const float* p, Rt (&w)[P]) {
+  if constexpr (P % 4 == 0) {
+#pragma unroll
+    for (int k = 0; k < P; k += 4) {
+      float4 a = *reinterpret_cast<const float4*>(p + k);
+      w[k] = (Rt)a.x; w[k + 1] = (Rt)a.y; w[k + 2] = (Rt)a.z; w[k + 3] = (Rt)a.w;
+    }
+  } else {
+#pragma unroll
+    for (int k = 0; k < P; ++k) w[k] = (Rt)p[k];
+  }
+}
+
 template <typename T2> struct OffT;
 template <> struct OffT<float2> { using type = float2; };
 template <> struct OffT<double2> { using type = double2; };
@@ -909,7 +924,7 @@ __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_gr
 template <typename T2, int TAPS, int P>
 __host__ __device__ constexpr size_t k3_fixed_smem() {
   return sizeof(T2) * kK3Stages * K3Cfg<T2>::BLOCK * P +
-         (K3Cfg<T2>::P1REG ? 0 : sizeof(typename Real<T2>::type) * P * k3_window_rows(TAPS, sizeof(T2) == 8) * K3Cfg<T2>::BLOCK);
+         (K3Cfg<T2>::P1REG ? 0 : sizeof(float) * P * k3_window_rows(TAPS, sizeof(T2) == 8) * K3Cfg<T2>::BLOCK);
 }
 
 // K3: one CTA processes chunks of BLOCK consecutive groups (one group of P points per
@@ -937,7 +952,9 @@ __global__ void __launch_bounds__(K3Cfg<T2>::BLOCK, K3Cfg<T2>::MINB)
   constexpr int EPC = 16 / (int)sizeof(T2);      // elements per 16-byte chunk
   extern __shared__ __align__(16) unsigned char k3_smem[];
   T2* aring = reinterpret_cast<T2*>(k3_smem);
-  Rt* p1s = reinterpret_cast<Rt*>(k3_smem + sizeof(T2) * S * BLOCK * P);
+  // row weights phi1 in shared memory as FP32 for both dtypes: they are used once per row and
+  // point, and their own accuracy (ES polynomial, ~1.5 e^{-beta}) is below FP32 rounding anyway
+  float* p1s = reinterpret_cast<float*>(k3_smem + sizeof(T2) * S * BLOCK * P);
   T2* tring = reinterpret_cast<T2*>(k3_smem + k3_fixed_smem<T2, TAPS, P>());
   const int cap = iw.tile_cap;
   const Rt inv_half_w = (Rt)(2.0 / TAPS);
@@ -1041,7 +1058,7 @@ __global__ void __launch_bounds__(K3Cfg<T2>::BLOCK, K3Cfg<T2>::MINB)
         for (int i = 0; i < WINR; ++i) p1r[k][i] = w1[i];
       } else {
 #pragma unroll
-        for (int i = 0; i < WINR; ++i) p1s[(i * BLOCK + threadIdx.x) * P + k] = w1[i];
+        for (int i = 0; i < WINR; ++i) p1s[(i * BLOCK + threadIdx.x) * P + k] = (float)w1[i];
         // start the read of the running sum early (latency hidden by the term loop)
         base[k] = mk<T2>(0, 0);
         if constexpr (!K3Cfg<T2>::LEAN)
@@ -1070,7 +1087,7 @@ __global__ void __launch_bounds__(K3Cfg<T2>::BLOCK, K3Cfg<T2>::MINB)
 #pragma unroll
           for (int k = 0; k < P; ++k) w1[k] = p1r[k][i];
         } else {
-          load_p1<Rt, P>(p1s + (i * BLOCK + threadIdx.x) * P, w1);
+          load_p1_f<Rt, P>(p1s + (i * BLOCK + threadIdx.x) * P, w1);
         }
 #pragma unroll
         for (int k = 0; k < P; ++k) {
@@ -1160,7 +1177,7 @@ __global__ void __launch_bounds__(K3Cfg<T2>::BLOCK, K3Cfg<T2>::MINB)
   unsigned long long* full = reinterpret_cast<unsigned long long*>(k3_smem);
   unsigned long long* empty = full + S;
   T2* aring = reinterpret_cast<T2*>(k3_smem + 2 * sizeof(unsigned long long) * S);
-  Rt* p1s = reinterpret_cast<Rt*>(reinterpret_cast<unsigned char*>(aring) + sizeof(T2) * S * BLOCK * P);
+  float* p1s = reinterpret_cast<float*>(reinterpret_cast<unsigned char*>(aring) + sizeof(T2) * S * BLOCK * P);
   T2* tring = reinterpret_cast<T2*>(k3_smem + k3b_fixed_smem<T2, TAPS, P>());
   const int cap = iw.tile_cap;
   const Rt inv_half_w = (Rt)(2.0 / TAPS);
@@ -1242,7 +1259,7 @@ __global__ void __launch_bounds__(K3Cfg<T2>::BLOCK, K3Cfg<T2>::MINB)
       window_weights<Rt, TAPS, WINR>(o.x, inv_half_w, beta, poly, w1);
       window_weights<Rt, TAPS, WIN>(o.y, inv_half_w, beta, poly, p2[k]);
 #pragma unroll
-      for (int i = 0; i < WINR; ++i) p1s[(i * BLOCK + threadIdx.x) * P + k] = w1[i];
+      for (int i = 0; i < WINR; ++i) p1s[(i * BLOCK + threadIdx.x) * P + k] = (float)w1[i];
       base[k] = mk<T2>(0, 0);
       if (xs[k] >= 0 && !first) base[k] = Lf[xs[k]];
     }
@@ -1264,7 +1281,7 @@ __global__ void __launch_bounds__(K3Cfg<T2>::BLOCK, K3Cfg<T2>::MINB)
         T2 v[WIN];
         load_row<T2, WIN>(rowp, v);
         Rt w1[P];
-        load_p1<Rt, P>(p1s + (i * BLOCK + threadIdx.x) * P, w1);
+        load_p1_f<Rt, P>(p1s + (i * BLOCK + threadIdx.x) * P, w1);
 #pragma unroll
         for (int k = 0; k < P; ++k) {
           T2 rr = mk<T2>(0, 0);
