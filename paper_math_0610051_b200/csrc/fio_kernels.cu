@@ -627,6 +627,89 @@ __device__ T2* smem_fft(T2* a, T2* b, const FftLen& fl, const T2* tw, int nseq, 
   return a;
 }
 
+// Stockham FFT whose first stage reads its inputs through `load(seq, e)` (e.g. straight from
+// global memory, skipping the zero padding) and whose last stage writes through
+// `store(seq, e, v)` (e.g. straight to the fine grid); the stages in between ping-pong in shared
+// memory (a, b: nseq sequences of length L, stride L).  Same arithmetic as smem_fft.
+template <typename T2, int R, class Load, class Store>
+__device__ __forceinline__ void stockham_stage_io(int L, int Ns, const FastDiv& dnb, const FastDiv& dns,
+                                                  const T2* __restrict__ tw, int nseq, int sign, Load load,
+                                                  Store store) {
+  const int nb = L / R;
+  const int span = L / (Ns * R);
+  const int total = nseq * nb;
+  const float wscale = 6.283185307179586f / (float)L;
+  for (int idx = threadIdx.x; idx < total; idx += blockDim.x) {
+    const int sq = fdiv(idx, dnb);
+    const int j = idx - sq * nb;
+    const int jq = fdiv(j, dns);
+    const int k = j - jq * Ns;
+    T2 v[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) v[r] = load(sq, j + r * nb);
+    if (Ns > 1) {
+#pragma unroll
+      for (int r = 1; r < R; ++r) {
+        T2 w;
+        if constexpr (sizeof(T2) == 8 && FIO_FFT_FAST_TWIDDLE) {
+          float sn, cs;
+          __sincosf(wscale * (float)(r * k * span), &sn, &cs);
+          w = mk<T2>(cs, sn);
+        } else {
+          w = tw[r * k * span];
+        }
+        if (sign < 0) w.y = -w.y;
+        v[r] = cmul(v[r], w);
+      }
+    }
+    dft_small<T2, R>(v, sign);
+    const int base = jq * Ns * R + k;
+#pragma unroll
+    for (int r = 0; r < R; ++r) store(sq, base + r * Ns, v[r]);
+  }
+}
+
+template <typename T2, class Load, class Store>
+__device__ __forceinline__ void stage_dispatch(int R, int L, int Ns, const FastDiv& dnb, const FastDiv& dns,
+                                               const T2* tw, int nseq, int sign, Load load, Store store) {
+  switch (R) {
+    case 4: stockham_stage_io<T2, 4>(L, Ns, dnb, dns, tw, nseq, sign, load, store); break;
+    case 2: stockham_stage_io<T2, 2>(L, Ns, dnb, dns, tw, nseq, sign, load, store); break;
+    case 3: stockham_stage_io<T2, 3>(L, Ns, dnb, dns, tw, nseq, sign, load, store); break;
+    default: stockham_stage_io<T2, 5>(L, Ns, dnb, dns, tw, nseq, sign, load, store); break;
+  }
+}
+
+// Returns the shared buffer holding the result when the last stage writes to shared memory
+// (store_last_to_smem), else nullptr.  Ends with __syncthreads().
+template <typename T2, class LoadFirst, class StoreLast>
+__device__ T2* smem_fft_io(T2* a, T2* b, const FftLen& fl, const T2* tw, int nseq, int sign, LoadFirst load_first,
+                           StoreLast store_last, bool store_last_to_smem) {
+  const int L = fl.L;
+  int Ns = 1;
+  T2* in = a;   // unused by stage 0 (reads through load_first)
+  T2* out = b;
+  for (int st = 0; st < fl.nst; ++st) {
+    const int R = fl.radix[st];
+    const bool first = st == 0, last = st == fl.nst - 1;
+    auto sload = [&](int sq, int e) { return in[sq * L + e]; };
+    auto sstore = [&](int sq, int e, T2 v) { out[sq * L + e] = v; };
+    if (first && last && !store_last_to_smem)
+      stage_dispatch<T2>(R, L, Ns, fl.div_nb[st], fl.div_ns[st], tw, nseq, sign, load_first, store_last);
+    else if (first)
+      stage_dispatch<T2>(R, L, Ns, fl.div_nb[st], fl.div_ns[st], tw, nseq, sign, load_first, sstore);
+    else if (last && !store_last_to_smem)
+      stage_dispatch<T2>(R, L, Ns, fl.div_nb[st], fl.div_ns[st], tw, nseq, sign, sload, store_last);
+    else
+      stage_dispatch<T2>(R, L, Ns, fl.div_nb[st], fl.div_ns[st], tw, nseq, sign, sload, sstore);
+    __syncthreads();
+    in = out;
+    out = (out == b) ? a : b;
+    Ns *= R;
+  }
+  return store_last_to_smem ? in : nullptr;
+}
+
 // ------------------------------------------------------------------ K0: input spectrum
 // Rows of length L (row-major, row stride L): out = FFT_sign(in) * scale.
 template <typename T2>
@@ -700,31 +783,28 @@ __global__ void __launch_bounds__(256) k_rowpass(int N, const WedgeDev* __restri
   const WedgeDev& w = wedges[job.w];
   const FftLen& fl = ffts[w.fft2];
   const int L = fl.L, n1 = w.n1, n2 = w.n2, cnt = job.count;
-  const int Lp = padded_len<T2, true>(L);
   T2* a = reinterpret_cast<T2*>(smem_raw);
-  T2* b = a + cnt * Lp;
-  const T2 zero = mk<T2>(0, 0);
-  for (int idx = threadIdx.x; idx < cnt * Lp; idx += blockDim.x) a[idx] = zero;
-  __syncthreads();
+  T2* b = a + cnt * L;
   const T2* bet = betas[job.w] + ((long long)job.t * n1 + job.start) * n2;
-  for (int r = 0; r < cnt; ++r)
-  for (int i2 = threadIdx.x; i2 < n2; i2 += blockDim.x) {
-    T2 bv = bet[r * n2 + i2];
-    if (bv.x != 0 || bv.y != 0) {
-      int kp1 = job.start + r - n1 / 2, kp2 = i2 - n2 / 2;
-      int z1 = kp1 + w.xc1, z2 = kp2 + w.xc2;
-      int xi1 = w.Mi[0] * z1 + w.Mi[1] * z2, xi2 = w.Mi[2] * z1 + w.Mi[3] * z2;
-      T2 fv = fhat[(long long)imod(xi1, N) * N + imod(xi2, N)];
-      a[r * Lp + pad_idx<T2, true>(imod(kp2, L))] = cmul(bv, fv);
-    }
-  }
-  __syncthreads();
-  T2* res = smem_fft<T2, true>(a, b, fl, tw + fl.tw_off, cnt, 1, Lp, +1);
+  const int hi = n2 - n2 / 2;  // fine index pos = k'_2 mod L holds box column i2 = k'_2 + n2/2
+  // The first Stockham stage reads h straight from beta' and fhat (no zero fill / placement pass).
+  auto load_h = [&](int r, int pos) -> T2 {
+    int i2 = pos < hi ? pos + n2 / 2 : (pos >= L - n2 / 2 ? pos - L + n2 / 2 : -1);
+    if (i2 < 0) return mk<T2>(0, 0);
+    const T2 bv = bet[r * n2 + i2];
+    if (bv.x == 0 && bv.y == 0) return mk<T2>(0, 0);
+    const int kp1 = job.start + r - n1 / 2, kp2 = i2 - n2 / 2;
+    const int z1 = kp1 + w.xc1, z2 = kp2 + w.xc2;
+    const int xi1 = w.Mi[0] * z1 + w.Mi[1] * z2, xi2 = w.Mi[2] * z1 + w.Mi[3] * z2;
+    return cmul(bv, fhat[(long long)imod(xi1, N) * N + imod(xi2, N)]);
+  };
+  auto no_store = [](int, int, T2) {};
+  T2* res = smem_fft_io<T2>(a, b, fl, tw + fl.tw_off, cnt, +1, load_h, no_store, true);
   T2* dst = p1 + w.p1_off + (long long)job.t * L * n1 + job.start;
   const FastDiv dc = make_fastdiv_dev((unsigned)cnt);
   for (int idx = threadIdx.x; idx < cnt * L; idx += blockDim.x) {  // consecutive threads: consecutive i1
     const int j2 = fdiv(idx, dc), r = idx - j2 * cnt;
-    dst[(long long)j2 * n1 + r] = res[r * Lp + pad_idx<T2, true>(j2)];
+    dst[(long long)j2 * n1 + r] = res[r * L + j2];
   }
 }
 
@@ -743,32 +823,24 @@ __global__ void __launch_bounds__(256) k_colpass(const WedgeDev* __restrict__ we
   const WedgeDev& w = wedges[job.w];
   const FftLen& fl = ffts[w.fft1];
   const int L = fl.L, n1 = w.n1, C = job.count, c0 = job.start;
-  const int Lp = padded_len<T2, true>(L);
   T2* a = reinterpret_cast<T2*>(smem_raw);
-  T2* b = a + C * Lp;
-  const T2 zero = mk<T2>(0, 0);
-  for (int idx = threadIdx.x; idx < C * Lp; idx += blockDim.x) a[idx] = zero;
-  __syncthreads();
+  T2* b = a + C * L;
   const T2* src = p1 + w.p1_off + ((long long)job.t * w.n2f + c0) * n1;
-  for (int c = 0; c < C; ++c)
-    for (int i1 = threadIdx.x; i1 < n1; i1 += blockDim.x) {
-      int pos = i1 - n1 / 2;
-      pos = pos < 0 ? pos + L : pos;
-      a[c * Lp + pad_idx<T2, true>(pos)] = src[(long long)c * n1 + i1];
-    }
-  __syncthreads();
-  T2* res = smem_fft<T2, true>(a, b, fl, tw + fl.tw_off, C, 1, Lp, +1);
+  const int hi = n1 - n1 / 2;  // fine index pos = (i1 - n1/2) mod L
+  // First stage reads the row-pass output directly; last stage writes the haloed fine-grid row.
+  auto load_p = [&](int c, int pos) -> T2 {
+    int i1 = pos < hi ? pos + n1 / 2 : (pos >= L - n1 / 2 ? pos - L + n1 / 2 : -1);
+    return i1 < 0 ? mk<T2>(0, 0) : src[(long long)c * n1 + i1];
+  };
   const int rowp = L + 2 * kHalo;
   T2* dst = g + w.g_off + ((long long)job.t * w.n2f + c0) * rowp + kHalo;
-  for (int c = 0; c < C; ++c) {
+  auto store_g = [&](int c, int j1, T2 v) {
     T2* rp = dst + (long long)c * rowp;
-    for (int j1 = threadIdx.x; j1 < L; j1 += blockDim.x) {
-      const T2 v = res[c * Lp + pad_idx<T2, true>(j1)];
-      rp[j1] = v;
-      if (j1 < kHalo) rp[L + j1] = v;
-      if (j1 >= L - kHalo) rp[j1 - L] = v;
-    }
-  }
+    rp[j1] = v;
+    if (j1 < kHalo) rp[L + j1] = v;
+    if (j1 >= L - kHalo) rp[j1 - L] = v;
+  };
+  smem_fft_io<T2>(a, b, fl, tw + fl.tw_off, C, +1, load_p, store_g, false);
 }
 
 // ------------------------------------------------------------------ K3: interpolation + alpha epilogue
@@ -1522,6 +1594,10 @@ __global__ void __launch_bounds__(128) k_spread_groups(InterpWedge iw, T2* __res
       gx[k] = x >= 0 ? g[x] : mk<T2>(0, 0);
       window_weights<Rt, TAPS, WINR>((Rt)o.x, inv_half_w, beta, poly, p1[k]);
       window_weights<Rt, TAPS, WIN>((Rt)o.y, inv_half_w, beta, poly, p2[k]);
+      // K3 keeps its row weights in FP32 for both dtypes; round them the same way here so the
+      // adjoint stays the exact conjugate transpose of the forward operator
+#pragma unroll
+      for (int i = 0; i < WINR; ++i) p1[k][i] = (Rt)(float)p1[k][i];
     }
     for (int t = 0; t < q; ++t) {
       T2 c[P];
