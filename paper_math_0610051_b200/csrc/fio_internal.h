@@ -19,7 +19,10 @@ constexpr int kK3BlockC64 = 256;   // K3 threads per CTA (= groups per chunk), c
 constexpr int kK3BlockC128 = 128;  // complex128
 constexpr int kK3Stages = 3;       // cp.async pipeline depth of K3 (fine-grid tiles + alpha')
 constexpr int kK3TileCapC64 = 2048;   // max cells of a K3 chunk footprint, complex64
-constexpr int kK3TileCapC128 = 1024;  // complex128
+#ifndef FIO_K3_CAP128
+#define FIO_K3_CAP128 1024
+#endif
+constexpr int kK3TileCapC128 = FIO_K3_CAP128;  // complex128
 constexpr int kHalo = 8;
 // K3 supercell shape: super_rows x 2 base cells.  1 groups points with the same base row (window
 // w rows x (w+1) columns); 2 gives (w+1) x (w+1) windows (rounded up to even rows).  Measured on

@@ -970,6 +970,12 @@ template <typename T2> struct GroupP;
 template <> struct GroupP<float2> { static constexpr int value = kGroupPC64; };
 template <> struct GroupP<double2> { static constexpr int value = kGroupPC128; };
 
+#ifndef FIO_K3_SPLIT
+#define FIO_K3_SPLIT 0
+#endif
+#ifndef FIO_K3_MINB128
+#define FIO_K3_MINB128 2
+#endif
 template <typename T2> struct K3Cfg;
 template <> struct K3Cfg<float2> {
   static constexpr int BLOCK = kK3BlockC64, MINB = 2;
@@ -978,7 +984,7 @@ template <> struct K3Cfg<float2> {
   static constexpr int MAXC = kK3TileCapC64 / 2 / kK3BlockC64;  // 16-B tile-copy slots per thread
 };
 template <> struct K3Cfg<double2> {
-  static constexpr int BLOCK = kK3BlockC128, MINB = 2;
+  static constexpr int BLOCK = kK3BlockC128, MINB = FIO_K3_MINB128;
   static constexpr bool P1REG = false;  // 64 more FP64 registers would not fit
   static constexpr bool LEAN = false;
   static constexpr int MAXC = kK3TileCapC128 / 1 / kK3BlockC128;
@@ -1163,9 +1169,19 @@ __global__ void __launch_bounds__(K3Cfg<T2>::BLOCK, K3Cfg<T2>::MINB)
         }
 #pragma unroll
         for (int k = 0; k < P; ++k) {
+#if FIO_K3_SPLIT
+          T2 r0 = mk<T2>(0, 0), r1 = mk<T2>(0, 0);
+#pragma unroll
+          for (int j = 0; j < WIN; j += 2) {
+            r0 = cfma_real(p2[k][j], v[j], r0);
+            if (j + 1 < WIN) r1 = cfma_real(p2[k][j + 1], v[j + 1], r1);
+          }
+          const T2 rr = mk<T2>(r0.x + r1.x, r0.y + r1.y);
+#else
           T2 rr = mk<T2>(0, 0);
 #pragma unroll
           for (int j = 0; j < WIN; ++j) rr = cfma_real(p2[k][j], v[j], rr);
+#endif
           F[k] = cfma_real(w1[k], rr, F[k]);
         }
       }
