@@ -89,7 +89,9 @@ struct fio_plan_s {
   int njobs_row = 0, njobs_col = 0, smem_row = 0, smem_col = 0;
   int rows_per_cta_N = 1, cols_per_cta_N = 1, fft_N = 0;
   void *e2e_in = nullptr, *e2e_out = nullptr;
-  void* batch_ws = nullptr;  // (nrhs - 1) x (fhat + fine grids) for fio_apply_batch
+  void* batch_ws = nullptr;  // (nrhs - 1) x (fhat + fine grids + K3 accumulator) for fio_apply_batch
+  cudaStream_t side = nullptr;  // second K3 stream (odd wedges)
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   int batch_cap = 1;
   size_t alpha_bytes = 0, beta_bytes = 0, ws_bytes = 0, fine_elems = 0, p1_elems = 0, meta_bytes = 0;
   long long slots = 0;
@@ -126,6 +128,9 @@ struct fio_plan_s {
   }
   ~fio_plan_s() {
     free_events();
+    if (ev_fork) cudaEventDestroy(ev_fork);
+    if (ev_join) cudaEventDestroy(ev_join);
+    if (side) cudaStreamDestroy(side);
     if (batch_ws) cudaFree(batch_ws);
     for (void* p : allocs) cudaFree(p);
   }
@@ -761,6 +766,9 @@ fio_status build_plan(fio_plan_s& P, const fio_phase* phase, const fio_amplitude
   FIO_CUDA(P.upload(&P.d_beta, P.beta_ptrs.data(), std::max<size_t>(P.beta_ptrs.size(), 1)));
   FIO_CUDA(P.alloc(&P.fhat, cs * NN));
   FIO_CUDA(P.alloc(&P.tmp, cs * NN));
+  FIO_CUDA(cudaStreamCreateWithFlags(&P.side, cudaStreamNonBlocking));
+  FIO_CUDA(cudaEventCreateWithFlags(&P.ev_fork, cudaEventDisableTiming));
+  FIO_CUDA(cudaEventCreateWithFlags(&P.ev_join, cudaEventDisableTiming));
   FIO_CUDA(P.alloc(&P.p1, cs * std::max<size_t>(P.p1_elems, 1)));
   FIO_CUDA(P.alloc(&P.g, cs * std::max<size_t>(P.fine_elems, 1)));
   P.ws_bytes = cs * (2 * NN + P.p1_elems + P.fine_elems);
@@ -788,6 +796,10 @@ ApplyArgs make_args(const fio_plan_s& P) {
   a.poly = &P.poly;
   a.fhat = P.fhat;
   a.tmp = P.tmp;
+  a.acc2 = P.tmp;  // K0's scratch is free once K3 starts
+  a.side = P.side;
+  a.fork = P.ev_fork;
+  a.join = P.ev_join;
   a.p1 = P.p1;
   a.g = P.g;
   a.jobs_row = P.jobs_row;
@@ -935,7 +947,7 @@ fio_status fio_apply_batch(fio_handle h, int nrhs, const void* f_dev, void* Lf_d
   if (dev != h->device) FIO_CUDA(cudaSetDevice(h->device));
   const size_t cs = h->c64 ? sizeof(float2) : sizeof(double2);
   const size_t NN = (size_t)h->N * h->N;
-  const size_t per = NN + std::max<size_t>(h->fine_elems, 1);
+  const size_t per = NN + std::max<size_t>(h->fine_elems, 1) + NN;
   if (nrhs > h->batch_cap) {
     FIO_CUDA(cudaStreamSynchronize((cudaStream_t)stream));
     if (h->batch_ws) {
@@ -950,6 +962,7 @@ fio_status fio_apply_batch(fio_handle h, int nrhs, const void* f_dev, void* Lf_d
     char* base = static_cast<char*>(h->batch_ws) + cs * per * (size_t)(b - 1);
     args[b].fhat = base;
     args[b].g = base + cs * NN;
+    args[b].acc2 = base + cs * (NN + std::max<size_t>(h->fine_elems, 1));
   }
   int launches = 0;
   FIO_CUDA(enqueue_apply_batch(args.data(), nrhs, h->c64, f_dev, Lf_dev, (cudaStream_t)stream, &launches));

@@ -1419,12 +1419,25 @@ __global__ void k_dc_only(int N, const double2* __restrict__ a0, const T2* __res
   }
 }
 
+// Lf += acc2 (the odd-wedge partial sum of the two-stream K3)
+template <typename T2>
+__global__ void k_accum2(T2* __restrict__ Lf, const T2* __restrict__ acc2, long long NN) {
+  for (long long x = blockIdx.x * (long long)blockDim.x + threadIdx.x; x < NN; x += (long long)gridDim.x * blockDim.x) {
+    const T2 u = Lf[x], v = acc2[x];
+    Lf[x] = mk<T2>(u.x + v.x, u.y + v.y);
+  }
+}
+
+#ifndef FIO_K3_STREAMS
+#define FIO_K3_STREAMS 2
+#endif
 #ifndef FIO_K3_BULK
 #define FIO_K3_BULK 0  // bulk-copy + mbarrier pipeline: correct, measured no faster (c128 17.66 vs 17.56, c64 4.32 vs 3.64 ms)
 #endif
 
 template <typename T2, int TAPS, int P>
-static cudaError_t launch_groups_bulk_tp(const ApplyArgs& a, int wi, T2* Lf, cudaStream_t s) {
+static cudaError_t launch_groups_bulk_tp(const ApplyArgs& a, int wi, T2* Lf, int first, int add_dc,
+                                         cudaStream_t s) {
   constexpr int BLOCK = K3Cfg<T2>::BLOCK;
   const InterpWedge& iw = a.iw[wi];
   const size_t smem = k3b_fixed_smem<T2, TAPS, P>() + sizeof(T2) * kK3Stages * (size_t)iw.tile_cap;
@@ -1446,14 +1459,14 @@ static cudaError_t launch_groups_bulk_tp(const ApplyArgs& a, int wi, T2* Lf, cud
   per_sm = std::max(per_sm, 1);
   int blocks = std::max(1, std::min(iw.nchunks, per_sm * sms));
   k_interp_groups_bulk<T2, TAPS, P><<<blocks, BLOCK, smem, s>>>(iw, reinterpret_cast<const T2*>(a.g), a.a0,
-                                                               reinterpret_cast<const T2*>(a.fhat), wi == 0 ? 1 : 0,
-                                                               (wi == 0 && a.add_dc) ? 1 : 0, a.es_beta, *a.poly, Lf);
+                                                               reinterpret_cast<const T2*>(a.fhat), first,
+                                                               add_dc, a.es_beta, *a.poly, Lf);
   return cudaGetLastError();
 }
 
 template <typename T2, int TAPS, int P>
-static cudaError_t launch_groups_tp(const ApplyArgs& a, int wi, T2* Lf, cudaStream_t s) {
-  if (FIO_K3_BULK) return launch_groups_bulk_tp<T2, TAPS, P>(a, wi, Lf, s);
+static cudaError_t launch_groups_tp(const ApplyArgs& a, int wi, T2* Lf, int first, int add_dc, cudaStream_t s) {
+  if (FIO_K3_BULK) return launch_groups_bulk_tp<T2, TAPS, P>(a, wi, Lf, first, add_dc, s);
   constexpr int BLOCK = K3Cfg<T2>::BLOCK;
   const InterpWedge& iw = a.iw[wi];
   const size_t smem = k3_fixed_smem<T2, TAPS, P>() + sizeof(T2) * kK3Stages * (size_t)iw.tile_cap;
@@ -1475,8 +1488,8 @@ static cudaError_t launch_groups_tp(const ApplyArgs& a, int wi, T2* Lf, cudaStre
   per_sm = std::max(per_sm, 1);
   int blocks = std::max(1, std::min(iw.nchunks, per_sm * sms));
   k_interp_groups<T2, TAPS, P><<<blocks, BLOCK, smem, s>>>(iw, reinterpret_cast<const T2*>(a.g), a.a0,
-                                                          reinterpret_cast<const T2*>(a.fhat), wi == 0 ? 1 : 0,
-                                                          (wi == 0 && a.add_dc) ? 1 : 0, a.es_beta, *a.poly, Lf);
+                                                          reinterpret_cast<const T2*>(a.fhat), first,
+                                                          add_dc, a.es_beta, *a.poly, Lf);
   return cudaGetLastError();
 }
 
@@ -1493,22 +1506,36 @@ static cudaError_t launch_interp(const ApplyArgs* args, int nrhs, T2* Lf0, cudaS
     }
     return cudaGetLastError();
   }
+  // Two accumulators on two streams (FIO_K3_STREAMS): even wedges sum into Lf on s, odd wedges into
+  // acc2 on the plan's side stream, so one wedge's K3 tail overlaps the next wedge's start; the two
+  // partial sums are added at the end (fixed order: deterministic).  Skeleton mode shares one
+  // alpha' scratch between wedges and stays on one stream.
+  const bool dual = FIO_K3_STREAMS > 1 && a.side != nullptr && a.nw >= 2 && a.skel == nullptr;
+  if (dual) {
+    cudaError_t e = cudaEventRecord(a.fork, s);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(a.side, a.fork, 0);
+    if (e != cudaSuccess) return e;
+  }
   for (int wi = 0; wi < a.nw; ++wi) {
     cudaError_t e;
+    const bool odd = dual && (wi & 1);
+    cudaStream_t sw = odd ? a.side : s;
+    const int first = dual ? (wi < 2) : (wi == 0);
+    const int dc = (wi == 0 && a.add_dc) ? 1 : 0;
     if (a.skel) {  // skeleton storage: regenerate this wedge's alpha' into the shared scratch
       const InterpWedge& iw = a.iw[wi];
       e = launch_rebuild_alpha(a.op, a.wd_host[wi], a.skel[wi], iw.q, iw.slot_x,
                                (long long)iw.ngroups * GroupP<T2>::value, const_cast<void*>(iw.alpha),
-                               sizeof(T2) == sizeof(float2), s);
+                               sizeof(T2) == sizeof(float2), sw);
       if (e != cudaSuccess) return e;
       ++*n;
     }
     // one alpha' (rebuilt once in skeleton mode) serves every right-hand side (NEXT-2)
     for (int b = 0; b < nrhs; ++b) {
-      T2* Lf = Lf0 + b * NN;
+      T2* Lf = odd ? reinterpret_cast<T2*>(args[b].acc2) : Lf0 + b * NN;
 #define FIO_GROUPS_CASE(TP)                                                  \
   case TP:                                                                   \
-    e = launch_groups_tp<T2, TP, GroupP<T2>::value>(args[b], wi, Lf, s);     \
+    e = launch_groups_tp<T2, TP, GroupP<T2>::value>(args[b], wi, Lf, first, dc, sw); \
     break;
       switch (a.taps) {
         FIO_GROUPS_CASE(3)
@@ -1525,6 +1552,17 @@ static cudaError_t launch_interp(const ApplyArgs* args, int nrhs, T2* Lf0, cudaS
       if (e != cudaSuccess) return e;
       ++*n;
     }
+  }
+  if (dual) {
+    cudaError_t e = cudaEventRecord(a.join, a.side);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(s, a.join, 0);
+    if (e != cudaSuccess) return e;
+    const int blocks = (int)std::min<long long>((NN + 255) / 256, 148LL * 8);
+    for (int b = 0; b < nrhs; ++b) {
+      k_accum2<T2><<<blocks, 256, 0, s>>>(Lf0 + b * NN, reinterpret_cast<const T2*>(args[b].acc2), NN);
+      ++*n;
+    }
+    return cudaGetLastError();
   }
   return cudaSuccess;
 }

@@ -91,6 +91,9 @@ struct ApplyArgs {
   const FftJob* jobs_rowadj; int njobs_rowadj; int smem_rowadj;  // K1* (all t per job)
   const unsigned char* const* masks;  // per owned wedge: n1 x n2 box mask (cell is a member)
   size_t fine_elems;        // elements of the fine-grid workspace (G, reused as G* by the adjoint)
+  void* acc2;               // N*N second K3 accumulator (odd wedges, side stream)
+  cudaStream_t side;        // plan-owned stream for the odd wedges' K3 (nullptr: one stream)
+  cudaEvent_t fork, join;   // plan-owned events ordering the side stream
   int rows_per_cta_N;       // K0 row pass
   int cols_per_cta_N;       // K0 column pass
 };
