@@ -242,8 +242,10 @@ double es_poly_fit(int w, double beta, double tol, EsPoly& out) {
         err = std::max(err, std::fabs(p - es_kernel(sv - j, w, beta)));
       }
     }
-    if (err <= tol) return err;
+    if (err <= tol) break;
   }
+  for (int m = 0; m <= out.deg; ++m)
+    for (int j = 0; j < w; ++j) out.cf[m][j] = (float)out.c[j][m];
   return err;
 }
 

@@ -125,6 +125,9 @@ constexpr int kPolyMaxDeg = 20;
 struct EsPoly {
   int deg;
   double c[kMaxTaps][kPolyMaxDeg + 1];
+  // the same coefficients in FP32, coefficient-major with taps padded to an even count, so
+  // that taps (2i, 2i+1) are one float2 (packed FFMA2 Horner; c64 weights and the FP32 row weights)
+  float cf[kPolyMaxDeg + 1][kMaxTaps + 2];
 };
 
 // Host helpers (fio_host.cpp).

@@ -869,28 +869,80 @@ __device__ __forceinline__ float2 ffma2(float a, float2 b, float2 c) {
   return r;
 }
 __device__ __forceinline__ float2 cfma_real(float a, float2 b, float2 c) { return ffma2(a, b, c); }
+// a * (x, x) + c as one packed FFMA2
+__device__ __forceinline__ float2 ffma2_v(float2 a, float x, float2 c) { return ffma2(x, a, c); }
 __device__ __forceinline__ double2 cfma_real(double a, double2 b, double2 c) {
   return make_double2(fma(a, b.x, c.x), fma(a, b.y, c.y));
 }
 
 // Weights of the window positions i = 0..NW-1 for a point at offset o = u - anchor
-// (o in (w/2 - 1, w/2 + 1]).  float: exact ES kernel with fast intrinsics.  double: the
-// plan's piecewise polynomials (EsPoly) -- the point's base b = anchor + d, d = ceil(o - w/2)
-// in {0, 1}, s = o - d, taps j = i - d.
+// (o in (w/2 - 1, w/2 + 1]) from the plan's piecewise polynomials (EsPoly): the point's base
+// b = anchor + d, d = ceil(o - w/2) in {0, 1}, s = o - d, x = 2 (s - w/2) + 1, taps j = i - d.
+// float: FP32 coefficients, two taps per packed FFMA2 Horner step.  double: FP64 Horner.
+template <int TAPS, int NW>
+__device__ __forceinline__ void window_weights_f32(float o, const EsPoly& poly, float (&w)[NW]) {
+  constexpr int NP = (TAPS + 1) / 2;  // tap pairs
+  const int d = (o > 0.5f * TAPS) ? 1 : 0;
+  const float x = 2.f * (o - (float)d - 0.5f * TAPS) + 1.f;
+  float2 qv[NP];
+  constexpr int kDegF = 8;  // coefficients above the plan's degree are zero: fixed-length, unrolled Horner
+  if (poly.deg <= kDegF) {
+#pragma unroll
+    for (int p = 0; p < NP; ++p) qv[p] = make_float2(poly.cf[kDegF][2 * p], poly.cf[kDegF][2 * p + 1]);
+#pragma unroll
+    for (int m = kDegF - 1; m >= 0; --m) {
+#pragma unroll
+      for (int p = 0; p < NP; ++p) qv[p] = ffma2_v(qv[p], x, make_float2(poly.cf[m][2 * p], poly.cf[m][2 * p + 1]));
+    }
+  } else {
+    const int deg = poly.deg;
+#pragma unroll
+    for (int p = 0; p < NP; ++p) qv[p] = make_float2(poly.cf[deg][2 * p], poly.cf[deg][2 * p + 1]);
+    for (int m = deg - 1; m >= 0; --m) {
+#pragma unroll
+      for (int p = 0; p < NP; ++p) qv[p] = ffma2_v(qv[p], x, make_float2(poly.cf[m][2 * p], poly.cf[m][2 * p + 1]));
+    }
+  }
+  float q[2 * NP];
+#pragma unroll
+  for (int p = 0; p < NP; ++p) {
+    q[2 * p] = qv[p].x;
+    q[2 * p + 1] = qv[p].y;
+  }
+#pragma unroll
+  for (int i = 0; i < NW; ++i) {
+    const float a = (i < TAPS) ? q[i < TAPS ? i : 0] : 0.f;
+    const float b = (i >= 1 && i - 1 < TAPS) ? q[(i >= 1 && i - 1 < TAPS) ? i - 1 : 0] : 0.f;
+    w[i] = d ? b : a;
+  }
+}
+
 template <typename Rt, int TAPS, int NW>
 __device__ __forceinline__ void window_weights(Rt o, Rt inv_half_w, Rt beta, const EsPoly& poly, Rt (&w)[NW]) {
+  (void)inv_half_w;
+  (void)beta;
   if constexpr (sizeof(Rt) == 4) {
-#pragma unroll
-    for (int i = 0; i < NW; ++i) w[i] = es_weight<Rt>(o - (Rt)i, inv_half_w, beta);
+    window_weights_f32<TAPS, NW>(o, poly, w);
   } else {
     const int d = (o > (Rt)(0.5 * TAPS)) ? 1 : 0;
     const Rt x = (Rt)2 * (o - (Rt)d - (Rt)(0.5 * TAPS)) + (Rt)1;
     Rt qv[TAPS];
+    constexpr int kDegD = 8;  // as in window_weights_f32: zero coefficients above the plan's degree
+    if (poly.deg <= kDegD) {
 #pragma unroll
-    for (int j = 0; j < TAPS; ++j) qv[j] = (Rt)poly.c[j][poly.deg];
-    for (int m = poly.deg - 1; m >= 0; --m) {
+      for (int j = 0; j < TAPS; ++j) qv[j] = (Rt)poly.c[j][kDegD];
 #pragma unroll
-      for (int j = 0; j < TAPS; ++j) qv[j] = fma(qv[j], x, (Rt)poly.c[j][m]);
+      for (int m = kDegD - 1; m >= 0; --m) {
+#pragma unroll
+        for (int j = 0; j < TAPS; ++j) qv[j] = fma(qv[j], x, (Rt)poly.c[j][m]);
+      }
+    } else {
+#pragma unroll
+      for (int j = 0; j < TAPS; ++j) qv[j] = (Rt)poly.c[j][poly.deg];
+      for (int m = poly.deg - 1; m >= 0; --m) {
+#pragma unroll
+        for (int j = 0; j < TAPS; ++j) qv[j] = fma(qv[j], x, (Rt)poly.c[j][m]);
+      }
     }
 #pragma unroll
     for (int i = 0; i < NW; ++i) {
@@ -899,6 +951,12 @@ __device__ __forceinline__ void window_weights(Rt o, Rt inv_half_w, Rt beta, con
       w[i] = d ? b : a;
     }
   }
+}
+
+// Row weights phi1 (kept in FP32 for both dtypes): FP32 polynomial, as float.
+template <typename Rt, int TAPS, int NW>
+__device__ __forceinline__ void row_weights_f32(Rt o, const EsPoly& poly, float (&w)[NW]) {
+  window_weights_f32<TAPS, NW>((float)o, poly, w);
 }
 
 // Window row of WIN elements from shared memory (float2 rows start 16-byte aligned:
@@ -1128,15 +1186,15 @@ __global__ void __launch_bounds__(K3Cfg<T2>::BLOCK, K3Cfg<T2>::MINB)
         xs[k] = iw.slot_x[g * P + k];
         o = offs[g * P + k];
       }
-      Rt w1[WINR];
-      window_weights<Rt, TAPS, WINR>(o.x, inv_half_w, beta, poly, w1);
+      float w1[WINR];
+      row_weights_f32<Rt, TAPS, WINR>(o.x, poly, w1);
       window_weights<Rt, TAPS, WIN>(o.y, inv_half_w, beta, poly, p2[k]);
       if constexpr (P1REG) {
 #pragma unroll
-        for (int i = 0; i < WINR; ++i) p1r[k][i] = w1[i];
+        for (int i = 0; i < WINR; ++i) p1r[k][i] = (Rt)w1[i];
       } else {
 #pragma unroll
-        for (int i = 0; i < WINR; ++i) p1s[(i * BLOCK + threadIdx.x) * P + k] = (float)w1[i];
+        for (int i = 0; i < WINR; ++i) p1s[(i * BLOCK + threadIdx.x) * P + k] = w1[i];
         // start the read of the running sum early (latency hidden by the term loop)
         base[k] = mk<T2>(0, 0);
         if constexpr (!K3Cfg<T2>::LEAN)
@@ -1343,11 +1401,11 @@ __global__ void __launch_bounds__(K3Cfg<T2>::BLOCK, K3Cfg<T2>::MINB)
         xs[k] = iw.slot_x[g * P + k];
         o = offs[g * P + k];
       }
-      Rt w1[WINR];
-      window_weights<Rt, TAPS, WINR>(o.x, inv_half_w, beta, poly, w1);
+      float w1[WINR];
+      row_weights_f32<Rt, TAPS, WINR>(o.x, poly, w1);
       window_weights<Rt, TAPS, WIN>(o.y, inv_half_w, beta, poly, p2[k]);
 #pragma unroll
-      for (int i = 0; i < WINR; ++i) p1s[(i * BLOCK + threadIdx.x) * P + k] = (float)w1[i];
+      for (int i = 0; i < WINR; ++i) p1s[(i * BLOCK + threadIdx.x) * P + k] = w1[i];
       base[k] = mk<T2>(0, 0);
       if (xs[k] >= 0 && !first) base[k] = Lf[xs[k]];
     }
@@ -1419,18 +1477,29 @@ __global__ void k_dc_only(int N, const double2* __restrict__ a0, const T2* __res
   }
 }
 
-// Lf += acc2 (the odd-wedge partial sum of the two-stream K3)
+// Lf += acc[0] + ... + acc[n-1] (the other streams' partial sums of K3, fixed order)
 template <typename T2>
-__global__ void k_accum2(T2* __restrict__ Lf, const T2* __restrict__ acc2, long long NN) {
+__global__ void k_accum(T2* __restrict__ Lf, const T2* __restrict__ a0, const T2* __restrict__ a1,
+                        const T2* __restrict__ a2, int n, long long NN) {
   for (long long x = blockIdx.x * (long long)blockDim.x + threadIdx.x; x < NN; x += (long long)gridDim.x * blockDim.x) {
-    const T2 u = Lf[x], v = acc2[x];
-    Lf[x] = mk<T2>(u.x + v.x, u.y + v.y);
+    T2 u = Lf[x];
+    const T2 v = a0[x];
+    u.x += v.x;
+    u.y += v.y;
+    if (n > 1) {
+      const T2 w = a1[x];
+      u.x += w.x;
+      u.y += w.y;
+    }
+    if (n > 2) {
+      const T2 w = a2[x];
+      u.x += w.x;
+      u.y += w.y;
+    }
+    Lf[x] = u;
   }
 }
 
-#ifndef FIO_K3_STREAMS
-#define FIO_K3_STREAMS 2
-#endif
 #ifndef FIO_K3_BULK
 #define FIO_K3_BULK 0  // bulk-copy + mbarrier pipeline: correct, measured no faster (c128 17.66 vs 17.56, c64 4.32 vs 3.64 ms)
 #endif
@@ -1506,21 +1575,21 @@ static cudaError_t launch_interp(const ApplyArgs* args, int nrhs, T2* Lf0, cudaS
     }
     return cudaGetLastError();
   }
-  // Two accumulators on two streams (FIO_K3_STREAMS): even wedges sum into Lf on s, odd wedges into
-  // acc2 on the plan's side stream, so one wedge's K3 tail overlaps the next wedge's start; the two
-  // partial sums are added at the end (fixed order: deterministic).  Skeleton mode shares one
-  // alpha' scratch between wedges and stays on one stream.
-  const bool dual = FIO_K3_STREAMS > 1 && a.side != nullptr && a.nw >= 2 && a.skel == nullptr;
-  if (dual) {
+  // K3 of wedge wi runs on stream wi % ns with its own accumulator (stream 0: the caller's, into
+  // Lf), so one wedge's tail and prologue overlap other wedges' work; the partial sums are added at
+  // the end in a fixed order (deterministic).  Skeleton mode shares one alpha' scratch between
+  // wedges and stays on one stream.
+  const int ns = a.skel == nullptr ? std::max(1, std::min(a.k3_streams, a.nw)) : 1;
+  if (ns > 1) {
     cudaError_t e = cudaEventRecord(a.fork, s);
-    if (e == cudaSuccess) e = cudaStreamWaitEvent(a.side, a.fork, 0);
+    for (int j = 0; j + 1 < ns && e == cudaSuccess; ++j) e = cudaStreamWaitEvent(a.side[j], a.fork, 0);
     if (e != cudaSuccess) return e;
   }
   for (int wi = 0; wi < a.nw; ++wi) {
     cudaError_t e;
-    const bool odd = dual && (wi & 1);
-    cudaStream_t sw = odd ? a.side : s;
-    const int first = dual ? (wi < 2) : (wi == 0);
+    const int sj = wi % ns;
+    cudaStream_t sw = sj ? a.side[sj - 1] : s;
+    const int first = wi < ns;
     const int dc = (wi == 0 && a.add_dc) ? 1 : 0;
     if (a.skel) {  // skeleton storage: regenerate this wedge's alpha' into the shared scratch
       const InterpWedge& iw = a.iw[wi];
@@ -1532,7 +1601,7 @@ static cudaError_t launch_interp(const ApplyArgs* args, int nrhs, T2* Lf0, cudaS
     }
     // one alpha' (rebuilt once in skeleton mode) serves every right-hand side (NEXT-2)
     for (int b = 0; b < nrhs; ++b) {
-      T2* Lf = odd ? reinterpret_cast<T2*>(args[b].acc2) : Lf0 + b * NN;
+      T2* Lf = sj ? reinterpret_cast<T2*>(args[b].acc[sj - 1]) : Lf0 + b * NN;
 #define FIO_GROUPS_CASE(TP)                                                  \
   case TP:                                                                   \
     e = launch_groups_tp<T2, TP, GroupP<T2>::value>(args[b], wi, Lf, first, dc, sw); \
@@ -1553,13 +1622,18 @@ static cudaError_t launch_interp(const ApplyArgs* args, int nrhs, T2* Lf0, cudaS
       ++*n;
     }
   }
-  if (dual) {
-    cudaError_t e = cudaEventRecord(a.join, a.side);
-    if (e == cudaSuccess) e = cudaStreamWaitEvent(s, a.join, 0);
+  if (ns > 1) {
+    cudaError_t e = cudaSuccess;
+    for (int j = 0; j + 1 < ns && e == cudaSuccess; ++j) {
+      e = cudaEventRecord(a.join[j], a.side[j]);
+      if (e == cudaSuccess) e = cudaStreamWaitEvent(s, a.join[j], 0);
+    }
     if (e != cudaSuccess) return e;
     const int blocks = (int)std::min<long long>((NN + 255) / 256, 148LL * 8);
     for (int b = 0; b < nrhs; ++b) {
-      k_accum2<T2><<<blocks, 256, 0, s>>>(Lf0 + b * NN, reinterpret_cast<const T2*>(args[b].acc2), NN);
+      const T2* const* acc = reinterpret_cast<const T2* const*>(args[b].acc);
+      k_accum<T2><<<blocks, 256, 0, s>>>(Lf0 + b * NN, acc[0], ns > 2 ? acc[1] : acc[0], ns > 3 ? acc[2] : acc[0],
+                                          ns - 1, NN);
       ++*n;
     }
     return cudaGetLastError();
@@ -1646,12 +1720,12 @@ __global__ void __launch_bounds__(128) k_spread_groups(InterpWedge iw, T2* __res
         o = offs[grp * P + k];
       }
       gx[k] = x >= 0 ? g[x] : mk<T2>(0, 0);
-      window_weights<Rt, TAPS, WINR>((Rt)o.x, inv_half_w, beta, poly, p1[k]);
-      window_weights<Rt, TAPS, WIN>((Rt)o.y, inv_half_w, beta, poly, p2[k]);
-      // K3 keeps its row weights in FP32 for both dtypes; round them the same way here so the
-      // adjoint stays the exact conjugate transpose of the forward operator
+      // the same FP32 row weights as K3, so the adjoint stays the exact conjugate transpose
+      float w1[WINR];
+      row_weights_f32<Rt, TAPS, WINR>((Rt)o.x, poly, w1);
 #pragma unroll
-      for (int i = 0; i < WINR; ++i) p1[k][i] = (Rt)(float)p1[k][i];
+      for (int i = 0; i < WINR; ++i) p1[k][i] = (Rt)w1[i];
+      window_weights<Rt, TAPS, WIN>((Rt)o.y, inv_half_w, beta, poly, p2[k]);
     }
     for (int t = 0; t < q; ++t) {
       T2 c[P];

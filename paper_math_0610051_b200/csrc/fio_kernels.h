@@ -65,6 +65,8 @@ cudaError_t launch_rebuild_alpha(const OperatorDev& op, const WedgeDev& w, const
                                  const int* slot_x, long long nslots, void* alpha, bool c64, cudaStream_t s);
 
 // ---- apply-time kernels (the hot path) ----
+constexpr int kMaxK3Streams = 4;
+constexpr int kDefaultK3Streams = 2;  // env FIO_K3_STREAMS overrides (1..4)
 struct ApplyArgs {
   int N;
   int nw;                   // owned wedges
@@ -91,9 +93,12 @@ struct ApplyArgs {
   const FftJob* jobs_rowadj; int njobs_rowadj; int smem_rowadj;  // K1* (all t per job)
   const unsigned char* const* masks;  // per owned wedge: n1 x n2 box mask (cell is a member)
   size_t fine_elems;        // elements of the fine-grid workspace (G, reused as G* by the adjoint)
-  void* acc2;               // N*N second K3 accumulator (odd wedges, side stream)
-  cudaStream_t side;        // plan-owned stream for the odd wedges' K3 (nullptr: one stream)
-  cudaEvent_t fork, join;   // plan-owned events ordering the side stream
+  // K3 runs wedge wi on stream wi % k3_streams: stream 0 is the caller's and accumulates into Lf,
+  // stream j > 0 is plan-owned (side[j-1]) and accumulates into acc[j-1] (N*N each, per RHS)
+  int k3_streams;
+  void* acc[kMaxK3Streams - 1];
+  cudaStream_t side[kMaxK3Streams - 1];
+  cudaEvent_t fork, join[kMaxK3Streams - 1];
   int rows_per_cta_N;       // K0 row pass
   int cols_per_cta_N;       // K0 column pass
 };
