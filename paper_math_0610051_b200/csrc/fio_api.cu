@@ -568,6 +568,7 @@ fio_status build_plan(fio_plan_s& P, const fio_phase* phase, const fio_amplitude
     // K3 point groups (plan time): fine coordinates -> host grouping -> device tables
     InterpWedge iw{};
     iw.q = q;
+    long long real_groups = 0;
     iw.nrow = g.n2f;                 // K3 rows = j2
     iw.ncol = g.n1f;                 // K3 columns = j1 (haloed)
     iw.ncolp = g.n1f + 2 * kHalo;
@@ -582,6 +583,37 @@ fio_status build_plan(fio_plan_s& P, const fio_phase* phase, const fio_amplitude
       std::vector<int> anchor, slot_x;
       std::vector<double> off;
       group_points(uh.data(), NN, P.taps, group_p(c64), g.n2f, g.n1f, super_rows(c64), anchor, slot_x, off);
+      const int gp = group_p(c64);
+      real_groups = (long long)(anchor.size() / 2);
+      std::vector<int> box;
+      const int blk = c64 ? kK3BlockC64 : kK3BlockC128;
+      const long long cap = chunk_boxes(anchor, blk, k3_window_rows(P.taps, c64), P.taps + 1,
+                                        c64 ? kK3TileCapC64 : kK3TileCapC128, box, c64 ? 8 : 16);
+      iw.nchunks = (int)(box.size() / 6);
+      {  // pad every chunk to exactly blk groups, so that chunk c's groups are [c blk, (c+1) blk): K3
+         // can then prefetch a chunk's per-thread data without reading its box first.  Padding groups
+         // repeat the chunk's first anchor (inside the box), have no points (slot -1) and alpha' = 0.
+        std::vector<int> pa((size_t)iw.nchunks * blk * 2), ps((size_t)iw.nchunks * blk * gp, -1);
+        std::vector<double> po((size_t)iw.nchunks * blk * gp * 2, 0.5 * P.taps);
+        for (int c = 0; c < iw.nchunks; ++c) {
+          const long long g0 = box[6 * c], n = box[6 * c + 5];
+          for (long long i = 0; i < blk; ++i) {
+            const long long src = g0 + (i < n ? i : 0), dst = (long long)c * blk + i;
+            pa[2 * dst] = anchor[2 * src];
+            pa[2 * dst + 1] = anchor[2 * src + 1];
+            if (i < n)
+              for (int k = 0; k < gp; ++k) {
+                ps[dst * gp + k] = slot_x[src * gp + k];
+                po[2 * (dst * gp + k)] = off[2 * (src * gp + k)];
+                po[2 * (dst * gp + k) + 1] = off[2 * (src * gp + k) + 1];
+              }
+          }
+          box[6 * c] = c * blk;
+        }
+        anchor.swap(pa);
+        slot_x.swap(ps);
+        off.swap(po);
+      }
       iw.ngroups = (int)(anchor.size() / 2);
       int* d_anchor = nullptr;
       int* d_slot = nullptr;
@@ -599,11 +631,6 @@ fio_status build_plan(fio_plan_s& P, const fio_phase* phase, const fio_amplitude
       }
       iw.anchor = d_anchor;
       iw.slot_x = d_slot;
-      std::vector<int> box;
-      const int blk = c64 ? kK3BlockC64 : kK3BlockC128;
-      const long long cap = chunk_boxes(anchor, blk, k3_window_rows(P.taps, c64), P.taps + 1,
-                                        c64 ? kK3TileCapC64 : kK3TileCapC128, box, c64 ? 8 : 16);
-      iw.nchunks = (int)(box.size() / 6);
       P.chunk_threads += (long long)iw.nchunks * blk;
       iw.tile_cap = (int)cap;
       int* d_box = nullptr;
@@ -656,7 +683,7 @@ fio_status build_plan(fio_plan_s& P, const fio_phase* phase, const fio_amplitude
       FIO_CUDA(cudaStreamSynchronize(s));
     }
     if (!P.opts.skeleton) P.alpha_bytes += cs * (size_t)q * nslots;
-    P.slots += nslots;
+    P.slots += real_groups * group_p(c64);  // point slots before the chunk padding
     P.slot_terms += nslots * (long long)q;
     P.iw.push_back(iw);
     P.beta_bytes += cs * (size_t)q * g.n1 * g.n2;

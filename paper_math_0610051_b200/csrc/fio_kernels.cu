@@ -1052,15 +1052,27 @@ __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
   unsigned s = (unsigned)__cvta_generic_to_shared(smem);
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem) : "memory");
 }
+__device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
+  unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(s), "l"(gmem) : "memory");
+}
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
 template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory"); }
 
 // Dynamic shared memory of K3: alpha' ring [S][BLOCK][P], phi1 [P*WINR][BLOCK], tile ring [S][tile_cap].
 template <typename T2, int TAPS, int P>
+__host__ __device__ constexpr size_t k3_p1_smem() {
+  return K3Cfg<T2>::P1REG ? 0 : sizeof(float) * P * k3_window_rows(TAPS, sizeof(T2) == 8) * K3Cfg<T2>::BLOCK;
+}
+// prefetched per-chunk data: anchors (int2), slots (P ints), offsets (P x O2) per thread + 2 boxes
+template <typename T2, int P>
+__host__ __device__ constexpr size_t k3_meta_smem() {
+  return (size_t)K3Cfg<T2>::BLOCK * (8 + 4 * P + P * sizeof(T2)) + 64;
+}
+template <typename T2, int TAPS, int P>
 __host__ __device__ constexpr size_t k3_fixed_smem() {
-  return sizeof(T2) * kK3Stages * K3Cfg<T2>::BLOCK * P +
-         (K3Cfg<T2>::P1REG ? 0 : sizeof(float) * P * k3_window_rows(TAPS, sizeof(T2) == 8) * K3Cfg<T2>::BLOCK);
+  return sizeof(T2) * kK3Stages * K3Cfg<T2>::BLOCK * P + k3_p1_smem<T2, TAPS, P>() + k3_meta_smem<T2, P>();
 }
 
 // K3: one CTA processes chunks of BLOCK consecutive groups (one group of P points per
@@ -1091,6 +1103,13 @@ __global__ void __launch_bounds__(K3Cfg<T2>::BLOCK, K3Cfg<T2>::MINB)
   // row weights phi1 in shared memory as FP32 for both dtypes: they are used once per row and
   // point, and their own accuracy (ES polynomial, ~1.5 e^{-beta}) is below FP32 rounding anyway
   float* p1s = reinterpret_cast<float*>(k3_smem + sizeof(T2) * S * BLOCK * P);
+  // per-chunk data of the NEXT chunk, prefetched with cp.async while the current chunk runs
+  // (chunks are padded to BLOCK groups at plan time: chunk c's groups are [c BLOCK, (c+1) BLOCK))
+  unsigned char* meta = k3_smem + sizeof(T2) * S * BLOCK * P + k3_p1_smem<T2, TAPS, P>();
+  int2* m_anchor = reinterpret_cast<int2*>(meta);
+  int* m_slot = reinterpret_cast<int*>(meta + 8 * BLOCK);
+  O2* m_off = reinterpret_cast<O2*>(meta + (8 + 4 * P) * BLOCK);
+  int* sbox = reinterpret_cast<int*>(meta + (8 + 4 * P + P * sizeof(T2)) * BLOCK);  // [2][8]
   T2* tring = reinterpret_cast<T2*>(k3_smem + k3_fixed_smem<T2, TAPS, P>());
   const int cap = iw.tile_cap;
   const Rt inv_half_w = (Rt)(2.0 / TAPS);
@@ -1104,10 +1123,28 @@ __global__ void __launch_bounds__(K3Cfg<T2>::BLOCK, K3Cfg<T2>::MINB)
   T2* myring = aring + threadIdx.x * P;
   T2 f0 = mk<T2>(0, 0);
   if (add_dc) f0 = fhat[0];
-  for (int ch = blockIdx.x; ch < iw.nchunks; ch += gridDim.x) {
-    const int* cb = iw.box + 6 * ch;  // first group, r_lo, c_lo, nr, nc, groups
-    const int g = cb[0] + threadIdx.x;
-    const bool valid = threadIdx.x < cb[5];
+  static_assert((4 * P) % 16 == 0 && (P * sizeof(T2)) % 16 == 0, "K3 metadata rows must be 16-byte multiples");
+  auto prefetch_meta = [&](int chn, int bslot) {
+    if (chn < iw.nchunks) {
+      const long long gn = (long long)chn * BLOCK + threadIdx.x;
+      cp_async8(m_anchor + threadIdx.x, iw.anchor + 2 * gn);
+#pragma unroll
+      for (int c = 0; c < 4 * P / 16; ++c) cp_async16(m_slot + threadIdx.x * P + 4 * c, iw.slot_x + gn * P + 4 * c);
+      const char* so = reinterpret_cast<const char*>(offs + gn * P);
+      char* dofs = reinterpret_cast<char*>(m_off + threadIdx.x * P);
+#pragma unroll
+      for (int c = 0; c < (int)(P * sizeof(T2)) / 16; ++c) cp_async16(dofs + 16 * c, so + 16 * c);
+      if (threadIdx.x < 3) cp_async8(sbox + 8 * bslot + 2 * threadIdx.x, iw.box + 6 * (long long)chn + 2 * threadIdx.x);
+    }
+  };
+  prefetch_meta(blockIdx.x, 0);
+  cp_async_commit();
+  int it = 0;
+  for (int ch = blockIdx.x; ch < iw.nchunks; ch += gridDim.x, ++it) {
+    cp_async_wait<0>();
+    __syncthreads();  // this chunk's prefetched data is visible; the previous chunk is done with every ring slot
+    const int* cb = sbox + 8 * (it & 1);  // first group, r_lo, c_lo, nr, nc, groups
+    const int g = ch * BLOCK + threadIdx.x;
     const int4 bx = make_int4(cb[1], cb[2], cb[3], cb[4]);
     const int tchunks = bx.z * (bx.w / EPC);                    // 16-byte chunks of one tile
     const int cpr = bx.w / EPC;
@@ -1137,15 +1174,13 @@ __global__ void __launch_bounds__(K3Cfg<T2>::BLOCK, K3Cfg<T2>::MINB)
       }
     }
     // stage term t into ring slot t % S: this thread's alpha'(t) and its share of the tile
-    auto issue = [&](int t) {
+    auto issue = [&](int t, bool next_meta) {
       if (t < q) {
         const int st = t % S;
-        if (valid) {
 #pragma unroll
-          for (int c = 0; c < ACH; ++c)
-            cp_async16(reinterpret_cast<char*>(myring + st * BLOCK * P) + 16 * c,
-                       reinterpret_cast<const char*>(al + t * nslots) + 16 * c);
-        }
+        for (int c = 0; c < ACH; ++c)
+          cp_async16(reinterpret_cast<char*>(myring + st * BLOCK * P) + 16 * c,
+                     reinterpret_cast<const char*>(al + t * nslots) + 16 * c);
         const T2* __restrict__ gt = G + t * gstride;
         T2* tile = tring + st * cap;
         if constexpr (LEAN) {
@@ -1161,31 +1196,30 @@ __global__ void __launch_bounds__(K3Cfg<T2>::BLOCK, K3Cfg<T2>::MINB)
             if (u < ncp) cp_async16(tile + cdst[u], gt + csrc[u]);
         }
       }
+      // the next chunk's data, issued once this thread has consumed its copy of the current one
+      if (next_meta) prefetch_meta(ch + gridDim.x, (it + 1) & 1);
       cp_async_commit();
     };
-    __syncthreads();  // the previous chunk is done with every ring slot
 #pragma unroll
-    for (int st = 0; st < S - 1; ++st) issue(st);
+    for (int st = 0; st < S - 1; ++st) issue(st, false);
     int a1 = 0, a2 = 0;
     int xs[P];
     Rt p2[P][WIN];
     constexpr bool P1REG = K3Cfg<T2>::P1REG;
     Rt p1r[P][P1REG ? WINR : 1];
     T2 base[P];
-    if (valid) {
-      a1 = iw.anchor[2 * g] - bx.x;
-      a2 = iw.anchor[2 * g + 1] - bx.y;
+    {
+      const int2 an = m_anchor[threadIdx.x];
+      a1 = an.x - bx.x;
+      a2 = an.y - bx.y;
     }
 #pragma unroll
     for (int k = 0; k < P; ++k) {
       O2 o;
       o.x = (Rt)(0.5 * TAPS);
       o.y = (Rt)(0.5 * TAPS);
-      xs[k] = -1;
-      if (valid) {
-        xs[k] = iw.slot_x[g * P + k];
-        o = offs[g * P + k];
-      }
+      xs[k] = m_slot[threadIdx.x * P + k];
+      o = m_off[threadIdx.x * P + k];
       float w1[WINR];
       row_weights_f32<Rt, TAPS, WINR>(o.x, poly, w1);
       window_weights<Rt, TAPS, WIN>(o.y, inv_half_w, beta, poly, p2[k]);
@@ -1201,6 +1235,10 @@ __global__ void __launch_bounds__(K3Cfg<T2>::BLOCK, K3Cfg<T2>::MINB)
           if (xs[k] >= 0 && !first) base[k] = Lf[xs[k]];
       }
     }
+    if (q == 0) {  // no term loop: prefetch the next chunk's data here
+      prefetch_meta(ch + gridDim.x, (it + 1) & 1);
+      cp_async_commit();
+    }
     const int woff = a1 * bx.w + a2;
     T2 acc[P];
 #pragma unroll
@@ -1208,7 +1246,7 @@ __global__ void __launch_bounds__(K3Cfg<T2>::BLOCK, K3Cfg<T2>::MINB)
     for (int t = 0; t < q; ++t) {
       cp_async_wait<S - 2>();
       __syncthreads();  // term t staged by every thread; every thread is done with term t-1
-      issue(t + S - 1);
+      issue(t + S - 1, t == 0);
       const T2* __restrict__ win = tring + (t % S) * cap + woff;
       T2 F[P];
 #pragma unroll
@@ -1251,10 +1289,9 @@ __global__ void __launch_bounds__(K3Cfg<T2>::BLOCK, K3Cfg<T2>::MINB)
         acc[k].y = fma(av.x, F[k].y, fma(av.y, F[k].x, acc[k].y));
       }
     }
-    cp_async_wait<0>();
 #pragma unroll
     for (int k = 0; k < P; ++k) {
-      const int x = K3Cfg<T2>::LEAN ? (valid ? iw.slot_x[g * P + k] : -1) : xs[k];
+      const int x = xs[k];
       if (x < 0) continue;
       T2 b0;
       if constexpr (P1REG || K3Cfg<T2>::LEAN) {
