@@ -582,12 +582,13 @@ fio_status build_plan(fio_plan_s& P, const fio_phase* phase, const fio_amplitude
       for (long long x = 0; x < NN; ++x) std::swap(uh[2 * x], uh[2 * x + 1]);  // (K3 row, column) = (u2, u1)
       std::vector<int> anchor, slot_x;
       std::vector<double> off;
-      group_points(uh.data(), NN, P.taps, group_p(c64), g.n2f, g.n1f, super_rows(c64), anchor, slot_x, off);
+      group_points(uh.data(), NN, P.taps, group_p(c64), g.n2f, g.n1f, super_rows(c64), super_cols(c64), anchor, slot_x,
+                   off);
       const int gp = group_p(c64);
       real_groups = (long long)(anchor.size() / 2);
       std::vector<int> box;
       const int blk = c64 ? kK3BlockC64 : kK3BlockC128;
-      const long long cap = chunk_boxes(anchor, blk, k3_window_rows(P.taps, c64), P.taps + 1,
+      const long long cap = chunk_boxes(anchor, blk, k3_window_rows(P.taps, c64), k3_window_cols(P.taps, c64),
                                         c64 ? kK3TileCapC64 : kK3TileCapC128, box, c64 ? 8 : 16);
       iw.nchunks = (int)(box.size() / 6);
       {  // pad every chunk to exactly blk groups, so that chunk c's groups are [c blk, (c+1) blk): K3

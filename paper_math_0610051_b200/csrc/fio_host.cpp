@@ -276,18 +276,18 @@ static inline long long floor_div2(long long b) { return b >= 0 ? b / 2 : -((-b 
 // s = (floor(b1 / super_rows), floor(b2 / 2)); points are counting-sorted by supercell (row-major,
 // then by x) and each supercell's list is cut into groups of P.  The k3_window_rows(w) x (w+1)
 // window anchored at (kSuperRows s1, 2 s2) covers the w x w taps of every point of the group.
-void group_points(const double* u, long long NN, int taps, int P, int n1f, int n2f, int kSuperRows,
+void group_points(const double* u, long long NN, int taps, int P, int n1f, int n2f, int kSuperRows, int kSuperCols,
                   std::vector<int>& anchor, std::vector<int>& slot_x, std::vector<double>& off) {
   const long long lo = -((taps + 3) / 2) - 1;  // smallest possible supercell index (per axis, in units of 2)
-  const long long lo1 = kSuperRows == 1 ? 2 * lo : lo;
-  const long long n1s = kSuperRows == 1 ? n1f + 16 : n1f / 2 + 8, n2s = n2f / 2 + 8;
+  const long long lo1 = kSuperRows == 1 ? 2 * lo : lo, lo2 = kSuperCols == 1 ? 2 * lo : lo;
+  const long long n1s = kSuperRows == 1 ? n1f + 16 : n1f / 2 + 8, n2s = kSuperCols == 1 ? n2f + 16 : n2f / 2 + 8;
   const long long nkeys = n1s * n2s;
   std::vector<int> key(NN);
   std::vector<long long> cnt(nkeys + 1, 0);
   for (long long x = 0; x < NN; ++x) {
     long long b1 = (long long)std::ceil(u[2 * x] - 0.5 * taps);
     long long b2 = (long long)std::ceil(u[2 * x + 1] - 0.5 * taps);
-    long long s1 = (kSuperRows == 1 ? b1 : floor_div2(b1)) - lo1, s2 = floor_div2(b2) - lo;
+    long long s1 = (kSuperRows == 1 ? b1 : floor_div2(b1)) - lo1, s2 = (kSuperCols == 1 ? b2 : floor_div2(b2)) - lo2;
     long long k = s1 * n2s + s2;
     key[x] = (int)k;
     cnt[k + 1]++;
@@ -313,7 +313,7 @@ void group_points(const double* u, long long NN, int taps, int P, int n1f, int n
           const long long k = s1 * n2s + s2;
           const long long b = cnt[k], e = cnt[k + 1];
           if (b == e) continue;
-          const int a1 = (int)(kSuperRows * (s1 + lo1)), a2 = (int)(2 * (s2 + lo));
+          const int a1 = (int)(kSuperRows * (s1 + lo1)), a2 = (int)(kSuperCols * (s2 + lo2));
           for (long long i = b; i < e; i += P) {
             anchor.push_back(a1);
             anchor.push_back(a2);

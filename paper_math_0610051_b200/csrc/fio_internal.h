@@ -28,17 +28,29 @@ constexpr int kHalo = 8;
 // w rows x (w+1) columns); 2 gives (w+1) x (w+1) windows (rounded up to even rows).  Measured on
 // B200: 1 is slightly faster for complex64 (3.64 vs 3.68 ms), 2 clearly faster for complex128
 // (17.6 vs 20.0 ms) at N = 1024.
+#ifndef FIO_K3_SR128
+#define FIO_K3_SR128 2
+#endif
+#ifndef FIO_K3_SC128
+#define FIO_K3_SC128 1  // measured: 2x1 supercells (8x7 windows) K3 11.95 ms vs 2x2 12.21, 1x1 13.05 (c128, N=1024)
+#endif
 constexpr int kSuperRowsC64 = 1;
-constexpr int kSuperRowsC128 = 2;
+constexpr int kSuperRowsC128 = FIO_K3_SR128;
+// supercell columns: 2 (windows w+1 wide) or 1 (complex128 only: points share their base column,
+// windows exactly w wide; complex64 needs even anchors for 16-byte window rows)
+constexpr int kSuperColsC64 = 2;
+constexpr int kSuperColsC128 = FIO_K3_SC128;
 #ifdef __CUDACC__
 #define FIO_HD __host__ __device__
 #else
 #define FIO_HD
 #endif
 FIO_HD constexpr int super_rows(bool c64) { return c64 ? kSuperRowsC64 : kSuperRowsC128; }
+FIO_HD constexpr int super_cols(bool c64) { return c64 ? kSuperColsC64 : kSuperColsC128; }
 FIO_HD constexpr int k3_window_rows(int taps, bool c64) {
   return super_rows(c64) == 1 ? taps : ((taps + 2) & ~1);
-}    // periodic column halo on each side of a fine-grid row (K2 writes, K3 reads)
+}
+FIO_HD constexpr int k3_window_cols(int taps, bool c64) { return super_cols(c64) == 1 ? taps : taps + 1; }    // periodic column halo on each side of a fine-grid row (K2 writes, K3 reads)
 
 // Division by a runtime constant d via multiply-high (Granlund-Montgomery), exact for
 // numerators n < 2^31: q = (umulhi(m, n) + n) >> l.
@@ -147,7 +159,7 @@ void lpt_assign(int W, const double* cost, int nranks, int* owner);
 // Group the output points of one wedge for K3 (see InterpWedge).  u: 2*NN doubles
 // (K3 row / column fine coordinates in [0, n1f) x [0, n2f)).  Outputs: anchor (2 per group),
 // slot_x (P per group, -1 padding), off (2 per slot: u - anchor).
-void group_points(const double* u, long long NN, int taps, int P, int n1f, int n2f, int super_rows,
+void group_points(const double* u, long long NN, int taps, int P, int n1f, int n2f, int super_rows, int super_cols,
                   std::vector<int>& anchor, std::vector<int>& slot_x, std::vector<double>& off);
 long long chunk_boxes(const std::vector<int>& anchor, int block, int win_rows, int win_cols, long long cap,
                       std::vector<int>& box, int elem_bytes);

@@ -1092,7 +1092,7 @@ __global__ void __launch_bounds__(K3Cfg<T2>::BLOCK, K3Cfg<T2>::MINB)
                     T2* __restrict__ Lf) {
   using Rt = typename Real<T2>::type;
   using O2 = typename OffT<T2>::type;
-  constexpr int WIN = TAPS + 1;         // window columns
+  constexpr int WIN = k3_window_cols(TAPS, sizeof(T2) == 8);  // window columns
   constexpr int WINR = k3_window_rows(TAPS, sizeof(T2) == 8);  // window rows (super_rows 2: even, extra row weight 0)
   constexpr int BLOCK = K3Cfg<T2>::BLOCK;
   constexpr int S = kK3Stages;
@@ -1351,7 +1351,7 @@ __global__ void __launch_bounds__(K3Cfg<T2>::BLOCK, K3Cfg<T2>::MINB)
                          T2* __restrict__ Lf) {
   using Rt = typename Real<T2>::type;
   using O2 = typename OffT<T2>::type;
-  constexpr int WIN = TAPS + 1;
+  constexpr int WIN = k3_window_cols(TAPS, sizeof(T2) == 8);
   constexpr int WINR = k3_window_rows(TAPS, sizeof(T2) == 8);
   constexpr int BLOCK = K3Cfg<T2>::BLOCK;
   constexpr int NWARP = BLOCK / 32;
@@ -1713,7 +1713,7 @@ __global__ void __launch_bounds__(128) k_spread_groups(InterpWedge iw, T2* __res
                                                        const T2* __restrict__ g, double es_beta, EsPoly poly) {
   using Rt = typename Real<T2>::type;
   using O2 = typename OffT<T2>::type;
-  constexpr int WIN = TAPS + 1;
+  constexpr int WIN = k3_window_cols(TAPS, sizeof(T2) == 8);
   constexpr int WINR = k3_window_rows(TAPS, sizeof(T2) == 8);
   const Rt inv_half_w = (Rt)(2.0 / TAPS);
   const Rt beta = (Rt)es_beta;
