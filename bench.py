@@ -114,15 +114,15 @@ def apply_algorithmic_bytes(info, N, c64):
 
 
 def k3_resource_model(info, c64, ms, sm_mhz):
-    """What binds K3: per group-term the thread reads its (w+1)^2 window
-    (rows rounded up to even) and the P row weights from shared memory and alpha'(t) from the ring,
+    """What binds K3: per group-term the thread reads its window (k3_window_rows
+    x k3_window_cols) and the P FP32 row weights from shared memory and alpha'(t) from the ring,
     and issues 2 real FMAs per (point, window cell) plus 2 per (point, row) plus the alpha product.
     Returns achieved fractions of the SM load datapath (128 B/clk/SM) and of the FMA pipe
     (128 FP32 or 64 FP64 FMA/clk/SM) at the measured SM clock."""
     w = info["nufft_w"]
     P = info["group_p"]
-    win, winr = w + 1, info.get("k3_window_rows") or w
-    cs, rs = (8, 4) if c64 else (16, 8)
+    win, winr = info.get("k3_window_cols") or w + 1, info.get("k3_window_rows") or w
+    cs, rs = (8, 4) if c64 else (16, 4)
     gt = info["slot_terms"] / P
     lsu_bytes = gt * (winr * win * cs + winr * P * rs + P * cs)
     fmas = gt * (winr * (P * win * 2 + P * 2) + 4 * P)

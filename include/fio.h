@@ -174,6 +174,8 @@ typedef struct {
   int k3_window_rows;     /* rows of the K3 interpolation window (w or w+1 rounded up to even) */
   size_t skeleton_bytes;  /* skeleton storage: C and V S^{-1} of every owned wedge (0 otherwise);
                              alpha_bytes is then the size of the shared rebuild scratch */
+  int k3_window_cols;     /* columns of the K3 interpolation window (w or w+1) */
+  int k3_streams;         /* concurrent K3 streams of an apply (wedge l on stream l mod k3_streams) */
 } fio_info;
 
 fio_status fio_plan_info(fio_handle h, fio_info* info);

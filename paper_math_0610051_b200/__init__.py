@@ -71,7 +71,8 @@ class _Info(ctypes.Structure):
                 ("meta_bytes", ctypes.c_size_t), ("slots", ctypes.c_longlong),
                 ("max_tile_cap", ctypes.c_longlong), ("k3_thread_slots", ctypes.c_longlong),
                 ("rank_balance", ctypes.c_double), ("slot_terms", ctypes.c_longlong), ("group_p", ctypes.c_int),
-                ("k3_window_rows", ctypes.c_int), ("skeleton_bytes", ctypes.c_size_t)]
+                ("k3_window_rows", ctypes.c_int), ("skeleton_bytes", ctypes.c_size_t),
+                ("k3_window_cols", ctypes.c_int), ("k3_streams", ctypes.c_int)]
 
 
 def library_path() -> str:

@@ -1122,6 +1122,8 @@ fio_status fio_plan_info(fio_handle h, fio_info* info) {
   info->slot_terms = h->slot_terms;
   info->group_p = group_p(h->c64);
   info->skeleton_bytes = h->skel_bytes;
+  info->k3_window_cols = k3_window_cols(h->taps, h->c64);
+  info->k3_streams = h->k3_streams;
   info->k3_window_rows = k3_window_rows(h->taps, h->c64);
   info->beta_bytes = h->beta_bytes;
   info->workspace_bytes = h->ws_bytes;
