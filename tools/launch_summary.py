@@ -8,7 +8,7 @@ absolute times) are what compare with bench.py's stage_ms.
 import csv
 import sys
 
-APPLY = ("k_fft_rows", "k_fft_cols", "k_rowpass", "k_colpass", "k_interp_groups", "k_accum", "k_dc_only")
+APPLY = {"k_fft_rows", "k_fft_cols", "k_rowpass", "k_colpass", "k_interp_groups", "k_accum", "k_dc_only"}
 SCALE = {"ns": 1e-6, "nsecond": 1e-6, "us": 1e-3, "usecond": 1e-3, "ms": 1.0, "msecond": 1.0}
 
 
@@ -26,10 +26,10 @@ def main(path):
             order.append(name)
         agg[name][0] += 1
         agg[name][1] += ms
-    tot_apply = sum(v[1] for k, v in agg.items() if k.startswith(APPLY))
+    tot_apply = sum(v[1] for k, v in agg.items() if k in APPLY)
     for k in order:
         n, ms = agg[k]
-        share = f"  share_of_apply={ms / tot_apply:.3f}" if k.startswith(APPLY) and tot_apply > 0 else ""
+        share = f"  share_of_apply={ms / tot_apply:.3f}" if k in APPLY and tot_apply > 0 else ""
         print(f"{k:32s} launches={n:5d} total_ms={ms:10.3f}{share}")
 
 
