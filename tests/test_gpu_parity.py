@@ -221,6 +221,22 @@ def test_adjoint_pairing_is_exact():
     assert abs(lhs - rhs) <= 1e-12 * np.linalg.norm(f) * np.linalg.norm(g) * N, (lhs, rhs)
 
 
+@pytest.mark.parametrize("N,W,dtype,tol", [(128, 32, "c128", 1e-12), (128, 32, "c64", 1e-5), (512, 0, "c128", 1e-12)])
+def test_adjoint_pairing_dense_regions(N, W, dtype, tol):
+    # the GRT map folds: at N >= 128 with W >= 32 whole warps of K3 groups share one anchor, the case
+    # the segmented warp reduction of the spread must sum over all 32 lanes
+    op = wl.grt_operator(N)
+    tdt = torch.complex64 if dtype == "c64" else torch.complex128
+    plan = fio.Plan(N, op.c1, op.c2, eps=1e-6 if dtype == "c128" else 1e-4, dtype=dtype, device=0, n_wedges=W)
+    f, g = crandn(N, 41), crandn(N, 42)
+    Lf = plan.apply(torch.from_numpy(f).to(DEV, tdt)).cpu().numpy().astype(np.complex128)
+    Lsg = plan.apply_adjoint(torch.from_numpy(g).to(DEV, tdt)).cpu().numpy().astype(np.complex128)
+    if dtype == "c64":  # the GPU saw the rounded inputs
+        f, g = f.astype(np.complex64).astype(np.complex128), g.astype(np.complex64).astype(np.complex128)
+    lhs, rhs = np.vdot(g, Lf), np.vdot(Lsg, f)
+    assert abs(lhs - rhs) <= tol * np.linalg.norm(f) * np.linalg.norm(g), (lhs, rhs)
+
+
 def test_adjoint_sharded_partials():
     N = 64
     op = wl.grt_operator(N)
