@@ -15,12 +15,21 @@ constexpr int kMaxTaps = 10;
 constexpr int kGroupPC64 = 4;   // points per K3 group, complex64 (P = 8 measured slower: 4.63 vs 3.68 ms)
 constexpr int kGroupPC128 = 4;  // complex128 (register bound)
 inline int group_p(bool c64) { return c64 ? kGroupPC64 : kGroupPC128; }
-constexpr int kK3BlockC64 = 256;   // K3 threads per CTA (= groups per chunk), complex64
-constexpr int kK3BlockC128 = 128;  // complex128
+#ifndef FIO_K3_BLOCK64
+#define FIO_K3_BLOCK64 64  // measured (N=1024, K3 ms): 256x2 CTAs/SM 2.655, 128x4 2.484, 64x8 2.441, 32x16 2.447
+#endif
+#ifndef FIO_K3_CAP64
+#define FIO_K3_CAP64 512
+#endif
+constexpr int kK3BlockC64 = FIO_K3_BLOCK64;   // K3 threads per CTA (= groups per chunk), complex64
+#ifndef FIO_K3_BLOCK128
+#define FIO_K3_BLOCK128 64  // measured (N=1024, K3 ms): 128x2 CTAs/SM 11.95, 64x4 11.11, 32x8 11.42
+#endif
+constexpr int kK3BlockC128 = FIO_K3_BLOCK128;  // complex128
 constexpr int kK3Stages = 3;       // cp.async pipeline depth of K3 (fine-grid tiles + alpha')
-constexpr int kK3TileCapC64 = 2048;   // max cells of a K3 chunk footprint, complex64
+constexpr int kK3TileCapC64 = FIO_K3_CAP64;   // max cells of a K3 chunk footprint, complex64
 #ifndef FIO_K3_CAP128
-#define FIO_K3_CAP128 1024
+#define FIO_K3_CAP128 512
 #endif
 constexpr int kK3TileCapC128 = FIO_K3_CAP128;  // complex128
 constexpr int kHalo = 8;

@@ -1032,20 +1032,28 @@ template <> struct GroupP<double2> { static constexpr int value = kGroupPC128; }
 #define FIO_K3_SPLIT 0
 #endif
 #ifndef FIO_K3_MINB128
-#define FIO_K3_MINB128 2
+#define FIO_K3_MINB128 4
 #endif
 template <typename T2> struct K3Cfg;
 template <> struct K3Cfg<float2> {
-  static constexpr int BLOCK = kK3BlockC64, MINB = 2;
-  static constexpr bool P1REG = false;  // row weights in registers measured slower (4.28 vs 3.69 ms)
+#ifndef FIO_K3_MINB64
+#define FIO_K3_MINB64 8
+#endif
+#ifndef FIO_K3_P1REG64
+#define FIO_K3_P1REG64 false
+#endif
+  static constexpr int BLOCK = kK3BlockC64, MINB = FIO_K3_MINB64;
+  static constexpr bool P1REG = FIO_K3_P1REG64;  // row weights in registers measured slower (4.28 vs 3.69 ms)
   static constexpr bool LEAN = false;   // lean-register variant measured slower (4.19 vs 3.68 ms)
   static constexpr int MAXC = kK3TileCapC64 / 2 / kK3BlockC64;  // 16-B tile-copy slots per thread
+  static_assert(kK3TileCapC64 % (2 * kK3BlockC64) == 0, "tile cap must be a multiple of 2 BLOCK (copy slots)");
 };
 template <> struct K3Cfg<double2> {
   static constexpr int BLOCK = kK3BlockC128, MINB = FIO_K3_MINB128;
   static constexpr bool P1REG = false;  // 64 more FP64 registers would not fit
   static constexpr bool LEAN = false;
   static constexpr int MAXC = kK3TileCapC128 / 1 / kK3BlockC128;
+  static_assert(kK3TileCapC128 % kK3BlockC128 == 0, "tile cap must be a multiple of BLOCK (copy slots)");
 };
 
 __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
