@@ -1044,6 +1044,10 @@ template <> struct K3Cfg<float2> {
 #endif
   static constexpr int BLOCK = kK3BlockC64, MINB = FIO_K3_MINB64;
   static constexpr bool P1REG = FIO_K3_P1REG64;  // row weights in registers measured slower (4.28 vs 3.69 ms)
+#ifndef FIO_K3_AREG64
+#define FIO_K3_AREG64 false
+#endif
+  static constexpr bool AREG = FIO_K3_AREG64;
   static constexpr bool LEAN = false;   // lean-register variant measured slower (4.19 vs 3.68 ms)
   static constexpr int MAXC = kK3TileCapC64 / 2 / kK3BlockC64;  // 16-B tile-copy slots per thread
   static_assert(kK3TileCapC64 % (2 * kK3BlockC64) == 0, "tile cap must be a multiple of 2 BLOCK (copy slots)");
@@ -1052,6 +1056,7 @@ template <> struct K3Cfg<double2> {
   static constexpr int BLOCK = kK3BlockC128, MINB = FIO_K3_MINB128;
   static constexpr bool P1REG = false;  // 64 more FP64 registers would not fit
   static constexpr bool LEAN = false;
+  static constexpr bool AREG = false;
   static constexpr int MAXC = kK3TileCapC128 / 1 / kK3BlockC128;
   static_assert(kK3TileCapC128 % kK3BlockC128 == 0, "tile cap must be a multiple of BLOCK (copy slots)");
 };
@@ -1185,10 +1190,12 @@ __global__ void __launch_bounds__(K3Cfg<T2>::BLOCK, K3Cfg<T2>::MINB)
     auto issue = [&](int t, bool next_meta) {
       if (t < q) {
         const int st = t % S;
+        if constexpr (!K3Cfg<T2>::AREG) {
 #pragma unroll
-        for (int c = 0; c < ACH; ++c)
-          cp_async16(reinterpret_cast<char*>(myring + st * BLOCK * P) + 16 * c,
-                     reinterpret_cast<const char*>(al + t * nslots) + 16 * c);
+          for (int c = 0; c < ACH; ++c)
+            cp_async16(reinterpret_cast<char*>(myring + st * BLOCK * P) + 16 * c,
+                       reinterpret_cast<const char*>(al + t * nslots) + 16 * c);
+        }
         const T2* __restrict__ gt = G + t * gstride;
         T2* tile = tring + st * cap;
         if constexpr (LEAN) {
@@ -1251,7 +1258,17 @@ __global__ void __launch_bounds__(K3Cfg<T2>::BLOCK, K3Cfg<T2>::MINB)
     T2 acc[P];
 #pragma unroll
     for (int k = 0; k < P; ++k) acc[k] = mk<T2>(0, 0);
+    // AREG: alpha'(t) read straight into registers one term ahead (no shared-memory ring)
+    T2 acur[K3Cfg<T2>::AREG ? P : 1], anx[K3Cfg<T2>::AREG ? P : 1];
+    if constexpr (K3Cfg<T2>::AREG) {
+#pragma unroll
+      for (int k = 0; k < P; ++k) acur[k] = q > 0 ? al[k] : mk<T2>(0, 0);
+    }
     for (int t = 0; t < q; ++t) {
+      if constexpr (K3Cfg<T2>::AREG) {
+#pragma unroll
+        for (int k = 0; k < P; ++k) anx[k] = (t + 1 < q) ? al[(t + 1) * nslots + k] : mk<T2>(0, 0);
+      }
       cp_async_wait<S - 2>();
       __syncthreads();  // term t staged by every thread; every thread is done with term t-1
       issue(t + S - 1, t == 0);
@@ -1292,7 +1309,13 @@ __global__ void __launch_bounds__(K3Cfg<T2>::BLOCK, K3Cfg<T2>::MINB)
       const T2* ring = myring + (t % S) * BLOCK * P;
 #pragma unroll
       for (int k = 0; k < P; ++k) {
-        T2 av = ring[k];
+        T2 av;
+        if constexpr (K3Cfg<T2>::AREG) {
+          av = acur[k];
+          acur[k] = anx[k];
+        } else {
+          av = ring[k];
+        }
         acc[k].x = fma(av.x, F[k].x, fma(-av.y, F[k].y, acc[k].x));
         acc[k].y = fma(av.x, F[k].y, fma(av.y, F[k].x, acc[k].y));
       }
