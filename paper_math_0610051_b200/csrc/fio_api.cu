@@ -94,6 +94,11 @@ struct fio_plan_s {
   cudaStream_t side[kMaxK3Streams - 1] = {};
   cudaEvent_t ev_fork = nullptr, ev_join[kMaxK3Streams - 1] = {};
   void* acc_extra = nullptr;  // (k3_streams - 2) x N*N accumulators beyond tmp
+  int pipe_batches = 0;       // pipelined K1/K2 || K3 (0: off)
+  cudaStream_t fft_stream = nullptr;
+  cudaEvent_t ev_k0 = nullptr;
+  cudaEvent_t ev_batch[kMaxPipeBatches] = {};
+  std::vector<int> row_job_off, col_job_off;  // per owned wedge: first job in jobs_row / jobs_col
   int batch_cap = 1;
   size_t alpha_bytes = 0, beta_bytes = 0, ws_bytes = 0, fine_elems = 0, p1_elems = 0, meta_bytes = 0;
   long long slots = 0;
@@ -131,6 +136,10 @@ struct fio_plan_s {
   ~fio_plan_s() {
     free_events();
     if (ev_fork) cudaEventDestroy(ev_fork);
+    if (ev_k0) cudaEventDestroy(ev_k0);
+    for (cudaEvent_t e : ev_batch)
+      if (e) cudaEventDestroy(e);
+    if (fft_stream) cudaStreamDestroy(fft_stream);
     for (int j = 0; j + 1 < kMaxK3Streams; ++j) {
       if (ev_join[j]) cudaEventDestroy(ev_join[j]);
       if (side[j]) cudaStreamDestroy(side[j]);
@@ -757,6 +766,8 @@ fio_status build_plan(fio_plan_s& P, const fio_phase* phase, const fio_amplitude
     int cols = (int)std::max<size_t>(1, std::min<size_t>(max_cols, kSmemBudget / sc));
     cols = std::min(cols, w.n2f);
     rows = std::min(rows, w.n1);
+    P.row_job_off.push_back((int)jr.size());
+    P.col_job_off.push_back((int)jc.size());
     for (int i = 0; i < w.n1; i += rows) {
       const int cnt = std::min(rows, w.n1 - i);
       jra.push_back({(int)wi, 0, i, cnt});
@@ -777,6 +788,8 @@ fio_status build_plan(fio_plan_s& P, const fio_phase* phase, const fio_amplitude
     set_error("fine grid too large for the shared-memory FFT (N too large for this dtype)");
     return FIO_EINVAL;
   }
+  P.row_job_off.push_back((int)jr.size());
+  P.col_job_off.push_back((int)jc.size());
   P.smem_row = (int)smem_row;
   P.smem_col = (int)smem_col;
   P.njobs_row = (int)jr.size();
@@ -808,6 +821,14 @@ fio_status build_plan(fio_plan_s& P, const fio_phase* phase, const fio_amplitude
       FIO_CUDA(cudaEventCreateWithFlags(&P.ev_join[j], cudaEventDisableTiming));
     }
     if (P.k3_streams > 2) FIO_CUDA(P.alloc(&P.acc_extra, cs * NN * (P.k3_streams - 2)));
+    int nb = kDefaultPipeBatches;
+    if (const char* env = std::getenv("FIO_PIPE_BATCHES")) nb = std::atoi(env);
+    P.pipe_batches = std::max(0, std::min(nb, kMaxPipeBatches));
+    if (P.pipe_batches > 1) {
+      FIO_CUDA(cudaStreamCreateWithFlags(&P.fft_stream, cudaStreamNonBlocking));
+      FIO_CUDA(cudaEventCreateWithFlags(&P.ev_k0, cudaEventDisableTiming));
+      for (int b = 0; b < P.pipe_batches; ++b) FIO_CUDA(cudaEventCreateWithFlags(&P.ev_batch[b], cudaEventDisableTiming));
+    }
   }
   FIO_CUDA(P.alloc(&P.p1, cs * std::max<size_t>(P.p1_elems, 1)));
   FIO_CUDA(P.alloc(&P.g, cs * std::max<size_t>(P.fine_elems, 1)));
@@ -847,6 +868,12 @@ ApplyArgs make_args(const fio_plan_s& P) {
     a.join[j] = P.ev_join[j];
   }
   a.fork = P.ev_fork;
+  a.pipe_batches = P.pipe_batches;
+  a.fft_stream = P.fft_stream;
+  a.ev_k0 = P.ev_k0;
+  a.ev_batch = P.ev_batch;
+  a.row_job_off = P.row_job_off.empty() ? nullptr : P.row_job_off.data();
+  a.col_job_off = P.col_job_off.empty() ? nullptr : P.col_job_off.data();
   a.p1 = P.p1;
   a.g = P.g;
   a.jobs_row = P.jobs_row;

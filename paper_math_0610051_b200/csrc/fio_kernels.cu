@@ -13,6 +13,7 @@
 //                                 1357-1363) fused with the alpha epilogue and the
 //                                 sums over t and l, + DC term.
 // No code here is shared with oracle/.
+#include <vector>
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -1631,7 +1632,8 @@ static cudaError_t launch_groups_tp(const ApplyArgs& a, int wi, T2* Lf, int firs
 }
 
 template <typename T2>
-static cudaError_t launch_interp(const ApplyArgs* args, int nrhs, T2* Lf0, cudaStream_t s, int* n) {
+static cudaError_t launch_interp(const ApplyArgs* args, int nrhs, T2* Lf0, cudaStream_t s, int* n,
+                                 const int* wedge_batch = nullptr) {
   const ApplyArgs& a = args[0];
   const long long NN = (long long)a.N * a.N;
   if (a.nw == 0) {
@@ -1653,11 +1655,16 @@ static cudaError_t launch_interp(const ApplyArgs* args, int nrhs, T2* Lf0, cudaS
     for (int j = 0; j + 1 < ns && e == cudaSuccess; ++j) e = cudaStreamWaitEvent(a.side[j], a.fork, 0);
     if (e != cudaSuccess) return e;
   }
+  int waited[kMaxK3Streams] = {-1, -1, -1, -1};  // pipelined: last batch each K3 stream waited for
   for (int wi = 0; wi < a.nw; ++wi) {
     cudaError_t e;
     const int sj = wi % ns;
     cudaStream_t sw = sj ? a.side[sj - 1] : s;
     const int first = wi < ns;
+    if (wedge_batch && wedge_batch[wi] != waited[sj]) {  // this wedge's fine grids come from fft_stream
+      waited[sj] = wedge_batch[wi];
+      if ((e = cudaStreamWaitEvent(sw, a.ev_batch[waited[sj]], 0)) != cudaSuccess) return e;
+    }
     const int dc = (wi == 0 && a.add_dc) ? 1 : 0;
     if (a.skel) {  // skeleton storage: regenerate this wedge's alpha' into the shared scratch
       const InterpWedge& iw = a.iw[wi];
@@ -2210,6 +2217,19 @@ static cudaError_t enqueue_apply_t(const ApplyArgs* args, int nrhs, const T2* f0
   const T2* tw = reinterpret_cast<const T2*>(a0.tw);
   const size_t seq = fft_seq_bytes(a0.N, sizeof(T2) == sizeof(float2));
   const long long NN = (long long)a0.N * a0.N;
+  // pipelined K1/K2 || K3 (not with the per-stage profile, whose events need the stages in sequence)
+  const int nbat = std::min(a0.pipe_batches, kMaxPipeBatches);
+  const bool pipe = nbat > 1 && nrhs == 1 && ev == nullptr && a0.skel == nullptr && a0.nw >= 2 &&
+                    a0.fft_stream != nullptr && a0.row_job_off != nullptr;
+  std::vector<int> wedge_batch;
+  if (pipe) {
+    // the first batch is one wedge per K3 stream (only it is exposed), the rest split evenly
+    const int ns = std::max(1, std::min(a0.k3_streams, a0.nw));
+    wedge_batch.resize(a0.nw);
+    const int first = std::min(ns, a0.nw), rest = a0.nw - first, nb = std::max(1, std::min(nbat - 1, rest));
+    for (int wi = 0; wi < a0.nw; ++wi)
+      wedge_batch[wi] = wi < first ? 0 : 1 + (int)((long long)(wi - first) * nb / std::max(rest, 1));
+  }
   for (int b = 0; b < nrhs; ++b) {
     const ApplyArgs& a = args[b];
     const T2* f = f0 + b * NN;
@@ -2227,7 +2247,32 @@ static cudaError_t enqueue_apply_t(const ApplyArgs* args, int nrhs, const T2* f0
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
     ++n;
     mark();
-    if (a.nw > 0) {
+    if (pipe) {  // K1/K2 per wedge batch on fft_stream; K3 waits per batch (launch_interp)
+      const T2* const* betas = reinterpret_cast<const T2* const*>(a.beta);
+      if ((e = cudaEventRecord(a.ev_k0, s)) != cudaSuccess) return e;
+      if ((e = cudaStreamWaitEvent(a.fft_stream, a.ev_k0, 0)) != cudaSuccess) return e;
+      for (int bt = 0, w0 = 0; w0 < a.nw; ++bt) {
+        int w1 = w0;
+        while (w1 < a.nw && wedge_batch[w1] == bt) ++w1;
+        const int r0 = a.row_job_off[w0], r1 = a.row_job_off[w1], c0 = a.col_job_off[w0], c1 = a.col_job_off[w1];
+        if (r1 > r0) {
+          k_rowpass<T2><<<r1 - r0, 256, a.smem_row, a.fft_stream>>>(a.N, a.wedges, a.jobs_row + r0, a.ffts, tw, betas,
+                                                                    fhat, reinterpret_cast<T2*>(a.p1));
+          ++n;
+        }
+        if (c1 > c0) {
+          k_colpass<T2><<<c1 - c0, 256, a.smem_col, a.fft_stream>>>(a.wedges, a.jobs_col + c0, a.ffts, tw,
+                                                                    reinterpret_cast<const T2*>(a.p1),
+                                                                    reinterpret_cast<T2*>(a.g));
+          ++n;
+        }
+        if ((e = cudaGetLastError()) != cudaSuccess) return e;
+        if ((e = cudaEventRecord(a.ev_batch[bt], a.fft_stream)) != cudaSuccess) return e;
+        w0 = w1;
+      }
+      mark();
+      mark();
+    } else if (a.nw > 0) {
       const T2* const* betas = reinterpret_cast<const T2* const*>(a.beta);
       k_rowpass<T2><<<a.njobs_row, 256, a.smem_row, s>>>(a.N, a.wedges, a.jobs_row, a.ffts, tw, betas, fhat,
                                                          reinterpret_cast<T2*>(a.p1));
@@ -2244,7 +2289,10 @@ static cudaError_t enqueue_apply_t(const ApplyArgs* args, int nrhs, const T2* f0
       mark();
     }
   }
-  if ((e = launch_interp<T2>(args, nrhs, Lf, s, &n)) != cudaSuccess) return e;
+  if ((e = launch_interp<T2>(args, nrhs, Lf, s, &n, pipe ? wedge_batch.data() : nullptr)) != cudaSuccess) return e;
+  if (pipe) {  // join fft_stream (its last batch) back into s
+    if ((e = cudaStreamWaitEvent(s, a0.ev_batch[wedge_batch.back()], 0)) != cudaSuccess) return e;
+  }
   mark();
   if (launches) *launches = n;
   return cudaSuccess;

@@ -67,6 +67,8 @@ cudaError_t launch_rebuild_alpha(const OperatorDev& op, const WedgeDev& w, const
 // ---- apply-time kernels (the hot path) ----
 constexpr int kMaxK3Streams = 4;
 constexpr int kDefaultK3Streams = 2;  // env FIO_K3_STREAMS overrides (1..4)
+constexpr int kMaxPipeBatches = 16;
+constexpr int kDefaultPipeBatches = 0;  // env FIO_PIPE_BATCHES overrides; measured: 4/8/16 batches 14.46/14.51/14.56 ms vs 14.18 off (c128): K3 already fills the GPU
 struct ApplyArgs {
   int N;
   int nw;                   // owned wedges
@@ -99,6 +101,15 @@ struct ApplyArgs {
   void* acc[kMaxK3Streams - 1];
   cudaStream_t side[kMaxK3Streams - 1];
   cudaEvent_t fork, join[kMaxK3Streams - 1];
+  // pipelined apply (nrhs == 1, not skeleton): K1/K2 of wedge batch b run on fft_stream while K3 of
+  // batch b-1 runs; ev_batch[b] marks batch b's fine grids ready.  row/col_job_off: per owned wedge,
+  // its first job in jobs_row / jobs_col (nw + 1 entries, host).
+  int pipe_batches;                // 0/1: off
+  cudaStream_t fft_stream;
+  cudaEvent_t ev_k0;
+  const cudaEvent_t* ev_batch;     // kMaxPipeBatches
+  const int* row_job_off;
+  const int* col_job_off;
   int rows_per_cta_N;       // K0 row pass
   int cols_per_cta_N;       // K0 column pass
 };
