@@ -399,3 +399,22 @@ def test_more_invalid_arguments():
         plan.apply(torch.zeros((64, 64), dtype=torch.complex64, device=DEV))   # wrong dtype
     with pytest.raises(fio.FioError):
         plan.apply(torch.zeros((32, 32), dtype=torch.complex128, device=DEV))  # wrong shape
+
+
+# ------------------------------------------------------------------ stream / pipeline schedules
+@pytest.mark.parametrize("env,exact", [({"FIO_PIPE_BATCHES": "4"}, True), ({"FIO_K3_STREAMS": "1"}, False),
+                                       ({"FIO_K3_STREAMS": "3"}, False)])
+def test_apply_schedules_agree(env, exact, monkeypatch):
+    # the K3 stream count and the optional K1/K2 || K3 pipeline change only the schedule (and, for the
+    # stream count, the grouping of the per-wedge partial sums)
+    N = 256
+    op = wl.grt_operator(N)
+    f = wl.white_noise(N, 9)
+    _, ref = run(op, f)
+    for k, v in env.items():
+        monkeypatch.setenv(k, v)
+    _, out = run(op, f)
+    if exact:
+        assert np.array_equal(out, ref)
+    else:
+        assert oracle.rel_l2(out, ref) <= 1e-13
