@@ -637,7 +637,7 @@ __device__ __forceinline__ void stockham_stage_io(int L, int Ns, const FastDiv& 
                                                   const T2* __restrict__ tw, int nseq, int sign, Load load,
                                                   Store store) {
   const int nb = L / R;
-  const int span = L / (Ns * R);
+  const int span = fdiv(nb, dns);  // L / (Ns R), exact
   const int total = nseq * nb;
   const float wscale = 6.283185307179586f / (float)L;
   for (int idx = threadIdx.x; idx < total; idx += blockDim.x) {
@@ -789,15 +789,23 @@ __global__ void __launch_bounds__(256) k_rowpass(int N, const WedgeDev* __restri
   const T2* bet = betas[job.w] + ((long long)job.t * n1 + job.start) * n2;
   const int hi = n2 - n2 / 2;  // fine index pos = k'_2 mod L holds box column i2 = k'_2 + n2/2
   // The first Stockham stage reads h straight from beta' and fhat (no zero fill / placement pass).
+  const int h2 = n2 / 2, lo2 = L - h2;
+  const int m0 = w.Mi[0], m1 = w.Mi[1], m2 = w.Mi[2], m3 = w.Mi[3];
+  const int zb1 = job.start - n1 / 2 + w.xc1, zb2 = w.xc2 - h2;
+  const bool pow2 = (N & (N - 1)) == 0;
   auto load_h = [&](int r, int pos) -> T2 {
-    int i2 = pos < hi ? pos + n2 / 2 : (pos >= L - n2 / 2 ? pos - L + n2 / 2 : -1);
-    if (i2 < 0) return mk<T2>(0, 0);
-    const T2 bv = bet[r * n2 + i2];
-    if (bv.x == 0 && bv.y == 0) return mk<T2>(0, 0);
-    const int kp1 = job.start + r - n1 / 2, kp2 = i2 - n2 / 2;
-    const int z1 = kp1 + w.xc1, z2 = kp2 + w.xc2;
-    const int xi1 = w.Mi[0] * z1 + w.Mi[1] * z2, xi2 = w.Mi[2] * z1 + w.Mi[3] * z2;
-    return cmul(bv, fhat[(long long)imod(xi1, N) * N + imod(xi2, N)]);
+    const int i2 = pos < hi ? pos + h2 : pos - lo2;  // box column (valid iff pos < hi or pos >= L - n2/2)
+    T2 out = mk<T2>(0, 0);
+    if (pos < hi || pos >= lo2) {
+      const T2 bv = bet[r * n2 + i2];
+      if (bv.x != 0 || bv.y != 0) {
+        const int z1 = zb1 + r, z2 = zb2 + i2;
+        const int xi1 = m0 * z1 + m1 * z2, xi2 = m2 * z1 + m3 * z2;
+        const int r1 = pow2 ? (xi1 & (N - 1)) : imod(xi1, N), r2 = pow2 ? (xi2 & (N - 1)) : imod(xi2, N);
+        out = cmul(bv, fhat[r1 * N + r2]);
+      }
+    }
+    return out;
   };
   auto no_store = [](int, int, T2) {};
   T2* res = smem_fft_io<T2>(a, b, fl, tw + fl.tw_off, cnt, +1, load_h, no_store, true);
@@ -829,9 +837,12 @@ __global__ void __launch_bounds__(256) k_colpass(const WedgeDev* __restrict__ we
   const T2* src = p1 + w.p1_off + ((long long)job.t * w.n2f + c0) * n1;
   const int hi = n1 - n1 / 2;  // fine index pos = (i1 - n1/2) mod L
   // First stage reads the row-pass output directly; last stage writes the haloed fine-grid row.
+  const int h1 = n1 / 2, lo1 = L - h1;
   auto load_p = [&](int c, int pos) -> T2 {
-    int i1 = pos < hi ? pos + n1 / 2 : (pos >= L - n1 / 2 ? pos - L + n1 / 2 : -1);
-    return i1 < 0 ? mk<T2>(0, 0) : src[(long long)c * n1 + i1];
+    const int i1 = pos < hi ? pos + h1 : pos - lo1;  // valid iff pos < hi or pos >= L - n1/2
+    T2 out = mk<T2>(0, 0);
+    if (pos < hi || pos >= lo1) out = src[c * n1 + i1];
+    return out;
   };
   const int rowp = L + 2 * kHalo;
   T2* dst = g + w.g_off + ((long long)job.t * w.n2f + c0) * rowp + kHalo;
