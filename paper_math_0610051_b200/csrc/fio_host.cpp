@@ -341,9 +341,15 @@ void group_points(const double* u, long long NN, int taps, int P, int n1f, int n
 // columns (even), groups}; returns the largest rows*cols.
 // Tile rows have an even length (16-byte aligned complex64 window rows).  Padding the stride
 // against bank conflicts (odd / 2 mod 4 lengths) was measured: no gain (c128 K3 18.2 vs 17.6 ms).
+#ifndef FIO_TILE_ALIGN_C64
+#define FIO_TILE_ALIGN_C64 2
+#endif
+#ifndef FIO_TILE_ALIGN_C128
+#define FIO_TILE_ALIGN_C128 2
+#endif
 static inline int pad_tile_cols(int nc, int elem_bytes) {
-  (void)elem_bytes;
-  return nc + (nc & 1);
+  const int a = elem_bytes == 8 ? FIO_TILE_ALIGN_C64 : FIO_TILE_ALIGN_C128;
+  return (nc + a - 1) / a * a;
 }
 
 long long chunk_boxes(const std::vector<int>& anchor, int block, int win_rows, int win_cols, long long cap,
