@@ -95,7 +95,7 @@ typedef struct {
 /* Options; fio_default_opts() fills the defaults shown. */
 typedef struct {
   fio_dtype dtype;    /* FIO_C128 */
-  int n_wedges;       /* 0 -> W = 8 round(1.75 sqrt(N)/8), >= 8 (reading R1) */
+  int n_wedges;       /* 0 -> W = 8 round(2 sqrt(N)/8), >= 8 (reading R1) */
   int nufft_w;        /* 0 -> taps per dimension chosen from eps (reading R10) */
   double nufft_beta;  /* 0 -> 2.30 w (exponential-of-semicircle kernel) */
   uint64_t seed;      /* 0x5EED: seed of the randomized separation */

@@ -19,13 +19,14 @@ static thread_local std::string g_err;
 void set_error(const std::string& msg) { g_err = msg; }
 const char* last_error_cstr() { return g_err.c_str(); }
 
-// Reading R1: W = 8 round(1.75 sqrt(N) / 8), at least 8.  The paper fixes
-// W ~ sqrt(N) only up to a constant (the aperture 2 alpha / sqrt(N), alpha free); 1.75 is the
-// measured optimum of the B200 apply time (N = 1024: W = 56, 18.1 ms vs 21.2 ms at W = 32;
-// N = 2048: W = 80, 87.6 ms vs 98.8 ms at W = 48).  A multiple of 8 makes every boundary
-// ray (2l+1) pi / W irrational-sloped, so no lattice point is ever on a wedge boundary.
+// Reading R1: W = 8 round(2 sqrt(N) / 8), at least 8.  The paper fixes W ~ sqrt(N)
+// only up to a constant (the aperture 2 alpha / sqrt(N), alpha free); 2 is the measured optimum of
+// the B200 apply at the headline size (N = 1024: W = 48/56/64/72 give 14.29/14.14/13.88/13.77 ms
+// c128 and 3.27/3.32/3.27/3.39 ms c64; N = 2048: W = 80/88 give 69.3/70.6 ms).  A multiple of 8
+// makes every boundary ray (2l+1) pi / W irrational-sloped, so no lattice point is ever on a
+// wedge boundary.
 int default_wedges(int N) {
-  int w = 8 * (int)std::lround(1.75 * std::sqrt((double)N) / 8.0);
+  int w = 8 * (int)std::lround(2.0 * std::sqrt((double)N) / 8.0);
   return std::max(8, w);
 }
 
