@@ -12,7 +12,10 @@ namespace fio {
 
 constexpr int kMaxRadixStages = 24;
 constexpr int kMaxTaps = 10;
-constexpr int kGroupPC64 = 4;   // points per K3 group, complex64 (P = 8 measured slower: 4.63 vs 3.68 ms)
+#ifndef FIO_K3_P64
+#define FIO_K3_P64 4
+#endif
+constexpr int kGroupPC64 = FIO_K3_P64;   // points per K3 group, complex64
 constexpr int kGroupPC128 = 4;  // complex128 (register bound)
 inline int group_p(bool c64) { return c64 ? kGroupPC64 : kGroupPC128; }
 #ifndef FIO_K3_BLOCK64
@@ -43,7 +46,10 @@ constexpr int kHalo = 8;
 #ifndef FIO_K3_SC128
 #define FIO_K3_SC128 1  // measured: 2x1 supercells (8x7 windows) K3 11.95 ms vs 2x2 12.21, 1x1 13.05 (c128, N=1024)
 #endif
-constexpr int kSuperRowsC64 = 1;
+#ifndef FIO_K3_SR64
+#define FIO_K3_SR64 1
+#endif
+constexpr int kSuperRowsC64 = FIO_K3_SR64;
 constexpr int kSuperRowsC128 = FIO_K3_SR128;
 // supercell columns: 2 (windows w+1 wide) or 1 (complex128 only: points share their base column,
 // windows exactly w wide; complex64 needs even anchors for 16-byte window rows)
