@@ -536,6 +536,9 @@ __device__ __forceinline__ FastDiv make_fastdiv_dev(unsigned d) {
 template <typename T2> struct PadShift;
 template <> struct PadShift<float2> { static constexpr int value = 4; };
 template <> struct PadShift<double2> { static constexpr int value = 3; };
+#ifndef FIO_FFT_TWPOW
+#define FIO_FFT_TWPOW 1  // twiddles w^r = (w^1)^r: c128 K1+K2 2.68 -> 2.37 ms (N=1024)
+#endif
 #ifndef FIO_FFT_PAD
 #define FIO_FFT_PAD 0  // measured neutral-to-slower on B200 (K2 c128 3.38 vs 3.26 ms): off
 #endif
@@ -567,6 +570,26 @@ __device__ __forceinline__ void stockham_stage(const T2* __restrict__ a, T2* __r
     T2 v[R];
 #pragma unroll
     for (int r = 0; r < R; ++r) v[r] = in[pad_idx<T2, PAD>((j + r * nb) * si)];
+#if FIO_FFT_TWPOW
+    if constexpr (!(sizeof(T2) == 16 && FIO_FFT_TW2)) {
+      // w_r = w_1^r: one table / SFU twiddle per butterfly, the others by complex products
+      T2 w1;
+      if constexpr (sizeof(T2) == 8 && FIO_FFT_FAST_TWIDDLE) {
+        float sn, cs;
+        __sincosf(wscale * (float)(k * span), &sn, &cs);
+        w1 = mk<T2>(cs, sn);
+      } else {
+        w1 = tw[k * span];
+      }
+      if (sign < 0) w1.y = -w1.y;
+      T2 wr = w1;
+#pragma unroll
+      for (int r = 1; r < R; ++r) {
+        v[r] = cmul(v[r], wr);
+        if (r + 1 < R) wr = cmul(wr, w1);
+      }
+    } else
+#endif
 #pragma unroll
     for (int r = 1; r < R; ++r) {
       T2 w;
@@ -649,6 +672,24 @@ __device__ __forceinline__ void stockham_stage_io(int L, int Ns, const FastDiv& 
 #pragma unroll
     for (int r = 0; r < R; ++r) v[r] = load(sq, j + r * nb);
     if (Ns > 1) {
+#if FIO_FFT_TWPOW
+      // w_r = w_1^r: one table / SFU twiddle per butterfly, the others by complex products
+      T2 w1;
+      if constexpr (sizeof(T2) == 8 && FIO_FFT_FAST_TWIDDLE) {
+        float sn, cs;
+        __sincosf(wscale * (float)(k * span), &sn, &cs);
+        w1 = mk<T2>(cs, sn);
+      } else {
+        w1 = tw[k * span];
+      }
+      if (sign < 0) w1.y = -w1.y;
+      T2 wr = w1;
+#pragma unroll
+      for (int r = 1; r < R; ++r) {
+        v[r] = cmul(v[r], wr);
+        if (r + 1 < R) wr = cmul(wr, w1);
+      }
+#else
 #pragma unroll
       for (int r = 1; r < R; ++r) {
         T2 w;
@@ -662,6 +703,7 @@ __device__ __forceinline__ void stockham_stage_io(int L, int Ns, const FastDiv& 
         if (sign < 0) w.y = -w.y;
         v[r] = cmul(v[r], w);
       }
+#endif
     }
     dft_small<T2, R>(v, sign);
     const int base = jq * Ns * R + k;
