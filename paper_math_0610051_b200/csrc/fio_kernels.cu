@@ -1870,17 +1870,27 @@ __global__ void __launch_bounds__(128) k_spread_groups(InterpWedge iw, T2* __res
         T2 e[P];
 #pragma unroll
         for (int k = 0; k < P; ++k) e[k] = mk<T2>(p1[k][i] * c[k].x, p1[k][i] * c[k].y);
+        T2 v[WIN];
 #pragma unroll
         for (int j = 0; j < WIN; ++j) {
-          T2 v = mk<T2>(0, 0);
+          v[j] = mk<T2>(0, 0);
 #pragma unroll
-          for (int k = 0; k < P; ++k) v = cfma_real(p2[k][j], e[k], v);
-          // segmented sum toward the run head: after the steps d < maxrun, the head holds the run total
-          for (int d = 1; d < maxrun; d <<= 1) {
-            const T2 u = shfl_down_t2(v, d);
-            if (d < run) v = cadd(v, u);
+          for (int k = 0; k < P; ++k) v[j] = cfma_real(p2[k][j], e[k], v[j]);
+        }
+        // segmented sum toward the run head over the whole window row at once (WIN independent
+        // shuffle chains per step): after the steps d < maxrun the head holds the run total
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+          if (d >= maxrun) break;  // warp-uniform
+#pragma unroll
+          for (int j = 0; j < WIN; ++j) {
+            const T2 u = shfl_down_t2(v[j], d);
+            if (d < run) v[j] = cadd(v[j], u);
           }
-          if (head && valid) red_add(rp + j, v);
+        }
+        if (head && valid) {
+#pragma unroll
+          for (int j = 0; j < WIN; ++j) red_add(rp + j, v[j]);
         }
         rp += (r + 1 == n1f) ? -(long long)(n1f - 1) * n2p : (long long)n2p;
         r = (r + 1 == n1f) ? 0 : r + 1;
