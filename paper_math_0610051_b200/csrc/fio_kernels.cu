@@ -1856,12 +1856,28 @@ __global__ void __launch_bounds__(128) k_spread_groups(InterpWedge iw, T2* __res
       for (int i = 0; i < WINR; ++i) p1[k][i] = (Rt)w1[i];
       window_weights<Rt, TAPS, WIN>((Rt)o.y, inv_half_w, beta, poly, p2[k]);
     }
+    T2 anext[sizeof(T2) == 8 ? P : 1];  // c64: alpha'(t+1), loaded one term ahead
+    if constexpr (sizeof(T2) == 8) {
+#pragma unroll
+      for (int k = 0; k < P; ++k) anext[k] = (valid && q > 0) ? alpha[(long long)grp * P + k] : mk<T2>(0, 0);
+    }
     for (int t = 0; t < q; ++t) {
       T2 c[P];
 #pragma unroll
       for (int k = 0; k < P; ++k) {
-        const T2 av = valid ? alpha[t * nslots + (long long)grp * P + k] : mk<T2>(0, 0);  // conj(alpha') g
+        // conj(alpha') g; alpha' one term ahead for c64, at use for c128 (ahead: 52.7 vs 48.3 ms)
+        T2 av;
+        if constexpr (sizeof(T2) == 8)
+          av = anext[k];
+        else
+          av = valid ? alpha[t * nslots + (long long)grp * P + k] : mk<T2>(0, 0);
         c[k] = mk<T2>(av.x * gx[k].x + av.y * gx[k].y, av.x * gx[k].y - av.y * gx[k].x);
+      }
+      if constexpr (sizeof(T2) == 8) {
+        if (t + 1 < q && valid) {
+#pragma unroll
+          for (int k = 0; k < P; ++k) anext[k] = alpha[(t + 1) * nslots + (long long)grp * P + k];
+        }
       }
       T2* __restrict__ rp = G + t * gstride + (long long)r0 * n2p + a2;
       int r = r0;
