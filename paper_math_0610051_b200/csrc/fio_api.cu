@@ -770,16 +770,16 @@ fio_status build_plan(fio_plan_s& P, const fio_phase* phase, const fio_amplitude
     P.col_job_off.push_back((int)jc.size());
     for (int i = 0; i < w.n1; i += rows) {
       const int cnt = std::min(rows, w.n1 - i);
-      jra.push_back({(int)wi, 0, i, cnt});
+      jra.push_back({(int)wi, 0, i, cnt, w.fft2, {0, 0, 0}});
       smem_rowadj = std::max(smem_rowadj, sr * cnt + (size_t)cnt * w.n2 * (c64 ? sizeof(float2) : sizeof(double2)));
     }
     for (int t = 0; t < w.q; ++t) {
       for (int i = 0; i < w.n1; i += rows) {
-        jr.push_back({(int)wi, t, i, std::min(rows, w.n1 - i)});
+        jr.push_back({(int)wi, t, i, std::min(rows, w.n1 - i), w.fft2, {0, 0, 0}});
         smem_row = std::max(smem_row, sr * std::min(rows, w.n1 - i));
       }
       for (int c = 0; c < w.n2f; c += cols) {
-        jc.push_back({(int)wi, t, c, std::min(cols, w.n2f - c)});
+        jc.push_back({(int)wi, t, c, std::min(cols, w.n2f - c), w.fft1, {0, 0, 0}});
         smem_col = std::max(smem_col, sc * std::min(cols, w.n2f - c));
       }
     }

@@ -128,11 +128,13 @@ struct InterpWedge {
 
 // Work item of the batched FFT passes: one CTA processes `count` sequences of
 // the (wedge, t) pair starting at row/column `start`.
-struct FftJob {
+struct alignas(32) FftJob {
   int w;      // index into the owned-wedge table
   int t;
   int start;
   int count;
+  int fft;    // FftLen index of this pass (so the kernel's wedge and FFT-plan loads are independent)
+  int pad[3];
 };
 
 // Host-side geometry of one wedge.

@@ -824,7 +824,7 @@ __global__ void __launch_bounds__(256) k_rowpass(int N, const WedgeDev* __restri
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const FftJob job = jobs[blockIdx.x];
   const WedgeDev& w = wedges[job.w];
-  const FftLen& fl = ffts[w.fft2];
+  const FftLen& fl = ffts[job.fft];
   const int L = fl.L, n1 = w.n1, n2 = w.n2, cnt = job.count;
   T2* a = reinterpret_cast<T2*>(smem_raw);
   T2* b = a + cnt * L;
@@ -872,7 +872,7 @@ __global__ void __launch_bounds__(256) k_colpass(const WedgeDev* __restrict__ we
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const FftJob job = jobs[blockIdx.x];
   const WedgeDev& w = wedges[job.w];
-  const FftLen& fl = ffts[w.fft1];
+  const FftLen& fl = ffts[job.fft];
   const int L = fl.L, n1 = w.n1, C = job.count, c0 = job.start;
   T2* a = reinterpret_cast<T2*>(smem_raw);
   T2* b = a + C * L;
@@ -2044,7 +2044,7 @@ __global__ void __launch_bounds__(256) k_colpass_adj(const WedgeDev* __restrict_
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const FftJob job = jobs[blockIdx.x];
   const WedgeDev& w = wedges[job.w];
-  const FftLen& fl = ffts[w.fft1];
+  const FftLen& fl = ffts[job.fft];
   const int L = fl.L, n1 = w.n1, C = job.count, c0 = job.start;
   const int Lp = padded_len<T2, true>(L);
   T2* a = reinterpret_cast<T2*>(smem_raw);
@@ -2081,7 +2081,7 @@ __global__ void __launch_bounds__(256) k_rowpass_adj(int N, const WedgeDev* __re
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const FftJob job = jobs[blockIdx.x];
   const WedgeDev& w = wedges[job.w];
-  const FftLen& fl = ffts[w.fft2];
+  const FftLen& fl = ffts[job.fft];
   const int L = fl.L, n1 = w.n1, n2 = w.n2, cnt = job.count;
   const int Lp = padded_len<T2, true>(L);
   T2* a = reinterpret_cast<T2*>(smem_raw);
