@@ -1393,195 +1393,6 @@ __global__ void __launch_bounds__(K3Cfg<T2>::BLOCK, K3Cfg<T2>::MINB)
   }
 }
 
-// ------------------------------------------------------------------ K3, bulk-copy pipeline variant
-// Same arithmetic as k_interp_groups; the staging is a producer/consumer pipeline: thread 0 issues,
-// per term, one cp.async.bulk per tile row and one for the chunk's alpha' block, completing on the
-// slot's "full" mbarrier (expect_tx); every warp releases a slot through its "empty" mbarrier.  No
-// per-thread copies and no CTA-wide barrier per term: warps run decoupled.
-__device__ __forceinline__ unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
-__device__ __forceinline__ void mbar_init(unsigned long long* bar, int count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
-}
-__device__ __forceinline__ void mbar_expect_tx(unsigned long long* bar, unsigned bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
-}
-__device__ __forceinline__ void mbar_arrive(unsigned long long* bar) {
-  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
-}
-__device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned parity) {
-  asm volatile(
-      "{\n\t.reg .pred p;\n"
-      "FIO_WAIT_%=:\n\t"
-      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
-      "@!p bra FIO_WAIT_%=;\n\t}" ::"r"(smem_u32(bar)),
-      "r"(parity)
-      : "memory");
-}
-__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, unsigned long long* bar) {
-  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                   smem_u32(dst)),
-               "l"(src), "r"(bytes), "r"(smem_u32(bar))
-               : "memory");
-}
-
-template <typename T2, int TAPS, int P>
-__host__ __device__ constexpr size_t k3b_fixed_smem() {
-  return 2 * sizeof(unsigned long long) * kK3Stages + k3_fixed_smem<T2, TAPS, P>();
-}
-
-template <typename T2, int TAPS, int P>
-__global__ void __launch_bounds__(K3Cfg<T2>::BLOCK, K3Cfg<T2>::MINB)
-    k_interp_groups_bulk(InterpWedge iw, const T2* __restrict__ gbase, const double2* __restrict__ a0,
-                         const T2* __restrict__ fhat, int first, int add_dc, double es_beta, EsPoly poly,
-                         T2* __restrict__ Lf) {
-  using Rt = typename Real<T2>::type;
-  using O2 = typename OffT<T2>::type;
-  constexpr int WIN = k3_window_cols(TAPS, sizeof(T2) == 8);
-  constexpr int WINR = k3_window_rows(TAPS, sizeof(T2) == 8);
-  constexpr int BLOCK = K3Cfg<T2>::BLOCK;
-  constexpr int NWARP = BLOCK / 32;
-  constexpr int S = kK3Stages;
-  extern __shared__ __align__(16) unsigned char k3_smem[];
-  unsigned long long* full = reinterpret_cast<unsigned long long*>(k3_smem);
-  unsigned long long* empty = full + S;
-  T2* aring = reinterpret_cast<T2*>(k3_smem + 2 * sizeof(unsigned long long) * S);
-  float* p1s = reinterpret_cast<float*>(reinterpret_cast<unsigned char*>(aring) + sizeof(T2) * S * BLOCK * P);
-  T2* tring = reinterpret_cast<T2*>(k3_smem + k3b_fixed_smem<T2, TAPS, P>());
-  const int cap = iw.tile_cap;
-  const Rt inv_half_w = (Rt)(2.0 / TAPS);
-  const Rt beta = (Rt)es_beta;
-  const int n1f = iw.nrow, n2p = iw.ncolp, q = iw.q;
-  const long long gstride = (long long)n1f * n2p;
-  const long long nslots = (long long)iw.ngroups * P;
-  const T2* __restrict__ G = gbase + iw.g_off + kHalo;
-  const T2* __restrict__ alpha = reinterpret_cast<const T2*>(iw.alpha);
-  const O2* __restrict__ offs = reinterpret_cast<const O2*>(iw.slot_off);
-  const int lane = threadIdx.x & 31;
-  const int nck = blockIdx.x < iw.nchunks ? (iw.nchunks - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
-  const long long nterms = (long long)nck * q;
-  if (threadIdx.x == 0) {
-    for (int i = 0; i < S; ++i) {
-      mbar_init(&full[i], 1);
-      mbar_init(&empty[i], NWARP);
-    }
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  }
-  __syncthreads();
-  // producer (warp 0, all lanes): stage term n (chunk blockIdx.x + (n / q) gridDim.x, term n % q)
-  // into slot n % S; lane 0 waits for the slot and registers the byte count, then the lanes issue
-  // one bulk copy per tile row (and lane 0 the alpha' block)
-  auto produce = [&](long long n) {
-    const int slot = (int)(n % S);
-    const long long use = n / S;
-    const int ch = blockIdx.x + (int)(n / q) * gridDim.x;
-    const int t = (int)(n % q);
-    const int* cb = iw.box + 6 * ch;
-    const int g0 = cb[0], rlo = cb[1], clo = cb[2], nr = cb[3], nc = cb[4], cnt = cb[5];
-    const unsigned row_bytes = (unsigned)(nc * sizeof(T2));
-    const unsigned a_bytes = (unsigned)(cnt * P * sizeof(T2));
-    if (lane == 0) {
-      if (use > 0) mbar_wait(&empty[slot], (unsigned)((use - 1) & 1));
-      mbar_expect_tx(&full[slot], row_bytes * nr + a_bytes);
-    }
-    __syncwarp();
-    const T2* gt = G + t * gstride;
-    T2* tile = tring + (long long)slot * cap;
-    for (int rr = lane; rr < nr; rr += 32) {
-      int r = rlo + rr;
-      r = r < 0 ? r + n1f : (r >= n1f ? r - n1f : r);
-      bulk_g2s(tile + rr * nc, gt + (long long)r * n2p + clo, row_bytes, &full[slot]);
-    }
-    if (lane == 0)
-      bulk_g2s(aring + (long long)slot * BLOCK * P, alpha + t * nslots + (long long)g0 * P, a_bytes, &full[slot]);
-  };
-  if (threadIdx.x < 32)
-    for (long long n = 0; n < S - 1 && n < nterms; ++n) produce(n);
-  T2 f0 = mk<T2>(0, 0);
-  if (add_dc) f0 = fhat[0];
-  long long n = 0;
-  for (int k3c = 0; k3c < nck; ++k3c) {
-    const int ch = blockIdx.x + k3c * gridDim.x;
-    const int* cb = iw.box + 6 * ch;
-    const int g = cb[0] + threadIdx.x;
-    const bool valid = threadIdx.x < cb[5];
-    const int4 bx = make_int4(cb[1], cb[2], cb[3], cb[4]);
-    int a1 = 0, a2 = 0;
-    int xs[P];
-    Rt p2[P][WIN];
-    T2 base[P];
-    if (valid) {
-      a1 = iw.anchor[2 * g] - bx.x;
-      a2 = iw.anchor[2 * g + 1] - bx.y;
-    }
-#pragma unroll
-    for (int k = 0; k < P; ++k) {
-      O2 o;
-      o.x = (Rt)(0.5 * TAPS);
-      o.y = (Rt)(0.5 * TAPS);
-      xs[k] = -1;
-      if (valid) {
-        xs[k] = iw.slot_x[g * P + k];
-        o = offs[g * P + k];
-      }
-      float w1[WINR];
-      row_weights_f32<Rt, TAPS, WINR>(o.x, poly, w1);
-      window_weights<Rt, TAPS, WIN>(o.y, inv_half_w, beta, poly, p2[k]);
-#pragma unroll
-      for (int i = 0; i < WINR; ++i) p1s[(i * BLOCK + threadIdx.x) * P + k] = w1[i];
-      base[k] = mk<T2>(0, 0);
-      if (xs[k] >= 0 && !first) base[k] = Lf[xs[k]];
-    }
-    const int woff = a1 * bx.w + a2;
-    T2 acc[P];
-#pragma unroll
-    for (int k = 0; k < P; ++k) acc[k] = mk<T2>(0, 0);
-    for (int t = 0; t < q; ++t, ++n) {
-      if (threadIdx.x < 32 && n + S - 1 < nterms) produce(n + S - 1);
-      const int slot = (int)(n % S);
-      mbar_wait(&full[slot], (unsigned)((n / S) & 1));
-      const T2* __restrict__ win = tring + (long long)slot * cap + woff;
-      T2 F[P];
-#pragma unroll
-      for (int k = 0; k < P; ++k) F[k] = mk<T2>(0, 0);
-#pragma unroll
-      for (int i = 0; i < WINR; ++i) {
-        const T2* rowp = win + i * bx.w;
-        T2 v[WIN];
-        load_row<T2, WIN>(rowp, v);
-        Rt w1[P];
-        load_p1_f<Rt, P>(p1s + (i * BLOCK + threadIdx.x) * P, w1);
-#pragma unroll
-        for (int k = 0; k < P; ++k) {
-          T2 rr = mk<T2>(0, 0);
-#pragma unroll
-          for (int j = 0; j < WIN; ++j) rr = cfma_real(p2[k][j], v[j], rr);
-          F[k] = cfma_real(w1[k], rr, F[k]);
-        }
-      }
-      const T2* ring = aring + (long long)slot * BLOCK * P + threadIdx.x * P;
-#pragma unroll
-      for (int k = 0; k < P; ++k) {
-        T2 av = ring[k];
-        acc[k].x = fma(av.x, F[k].x, fma(-av.y, F[k].y, acc[k].x));
-        acc[k].y = fma(av.x, F[k].y, fma(av.y, F[k].x, acc[k].y));
-      }
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&empty[slot]);
-    }
-#pragma unroll
-    for (int k = 0; k < P; ++k) {
-      const int x = xs[k];
-      if (x < 0) continue;
-      T2 b0 = base[k];
-      if (first && add_dc) {
-        double2 d = a0[x];
-        b0 = mk<T2>((Rt)(d.x * (double)f0.x - d.y * (double)f0.y), (Rt)(d.x * (double)f0.y + d.y * (double)f0.x));
-      }
-      Lf[x] = mk<T2>(b0.x + acc[k].x, b0.y + acc[k].y);
-    }
-  }
-}
-
 // Lf = a(x,0) fhat(0) / N (rank 0) or 0: used only when this rank owns no wedge.
 template <typename T2>
 __global__ void k_dc_only(int N, const double2* __restrict__ a0, const T2* __restrict__ fhat, int add_dc,
@@ -1622,42 +1433,8 @@ __global__ void k_accum(T2* __restrict__ Lf, const T2* __restrict__ a0, const T2
   }
 }
 
-#ifndef FIO_K3_BULK
-#define FIO_K3_BULK 0  // bulk-copy + mbarrier pipeline: correct, measured no faster (c128 17.66 vs 17.56, c64 4.32 vs 3.64 ms)
-#endif
-
-template <typename T2, int TAPS, int P>
-static cudaError_t launch_groups_bulk_tp(const ApplyArgs& a, int wi, T2* Lf, int first, int add_dc,
-                                         cudaStream_t s) {
-  constexpr int BLOCK = K3Cfg<T2>::BLOCK;
-  const InterpWedge& iw = a.iw[wi];
-  const size_t smem = k3b_fixed_smem<T2, TAPS, P>() + sizeof(T2) * kK3Stages * (size_t)iw.tile_cap;
-  static int sms = 0;
-  static size_t configured = 0;
-  if (sms == 0) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  }
-  if (smem > configured) {
-    cudaError_t e = cudaFuncSetAttribute(k_interp_groups_bulk<T2, TAPS, P>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
-    configured = smem;
-  }
-  int per_sm = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_interp_groups_bulk<T2, TAPS, P>, BLOCK, smem);
-  per_sm = std::max(per_sm, 1);
-  int blocks = std::max(1, std::min(iw.nchunks, per_sm * sms));
-  k_interp_groups_bulk<T2, TAPS, P><<<blocks, BLOCK, smem, s>>>(iw, reinterpret_cast<const T2*>(a.g), a.a0,
-                                                               reinterpret_cast<const T2*>(a.fhat), first,
-                                                               add_dc, a.es_beta, *a.poly, Lf);
-  return cudaGetLastError();
-}
-
 template <typename T2, int TAPS, int P>
 static cudaError_t launch_groups_tp(const ApplyArgs& a, int wi, T2* Lf, int first, int add_dc, cudaStream_t s) {
-  if (FIO_K3_BULK) return launch_groups_bulk_tp<T2, TAPS, P>(a, wi, Lf, first, add_dc, s);
   constexpr int BLOCK = K3Cfg<T2>::BLOCK;
   const InterpWedge& iw = a.iw[wi];
   const size_t smem = k3_fixed_smem<T2, TAPS, P>() + sizeof(T2) * kK3Stages * (size_t)iw.tile_cap;
