@@ -14,6 +14,7 @@
 //                                 sums over t and l, + DC term.
 // No code here is shared with oracle/.
 #include <vector>
+#include <type_traits>
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -1102,6 +1103,7 @@ template <> struct K3Cfg<float2> {
 #define FIO_K3_AREG64 false
 #endif
   static constexpr bool AREG = FIO_K3_AREG64;
+  static constexpr bool P1D = false;
   static constexpr bool LEAN = false;   // lean-register variant measured slower (4.19 vs 3.68 ms)
   static constexpr int MAXC = kK3TileCapC64 / 2 / kK3BlockC64;  // 16-B tile-copy slots per thread
   static_assert(kK3TileCapC64 % (2 * kK3BlockC64) == 0, "tile cap must be a multiple of 2 BLOCK (copy slots)");
@@ -1111,6 +1113,10 @@ template <> struct K3Cfg<double2> {
   static constexpr bool P1REG = false;  // 64 more FP64 registers would not fit
   static constexpr bool LEAN = false;
   static constexpr bool AREG = false;
+#ifndef FIO_K3_P1D128
+#define FIO_K3_P1D128 false
+#endif
+  static constexpr bool P1D = FIO_K3_P1D128;  // row weights as FP64 in shared memory (no F2F per use)
   static constexpr int MAXC = kK3TileCapC128 / 1 / kK3BlockC128;
   static_assert(kK3TileCapC128 % kK3BlockC128 == 0, "tile cap must be a multiple of BLOCK (copy slots)");
 };
@@ -1130,7 +1136,9 @@ __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_gr
 // Dynamic shared memory of K3: alpha' ring [S][BLOCK][P], phi1 [P*WINR][BLOCK], tile ring [S][tile_cap].
 template <typename T2, int TAPS, int P>
 __host__ __device__ constexpr size_t k3_p1_smem() {
-  return K3Cfg<T2>::P1REG ? 0 : sizeof(float) * P * k3_window_rows(TAPS, sizeof(T2) == 8) * K3Cfg<T2>::BLOCK;
+  return K3Cfg<T2>::P1REG ? 0
+                          : (K3Cfg<T2>::P1D ? sizeof(T2) / 2 : sizeof(float)) * P * k3_window_rows(TAPS, sizeof(T2) == 8) *
+                                K3Cfg<T2>::BLOCK;
 }
 // prefetched per-chunk data: anchors (int2), slots (P ints), offsets (P x O2) per thread + 2 boxes
 template <typename T2, int P>
@@ -1169,7 +1177,8 @@ __global__ void __launch_bounds__(K3Cfg<T2>::BLOCK, K3Cfg<T2>::MINB)
   T2* aring = reinterpret_cast<T2*>(k3_smem);
   // row weights phi1 in shared memory as FP32 for both dtypes: they are used once per row and
   // point, and their own accuracy (ES polynomial, ~1.5 e^{-beta}) is below FP32 rounding anyway
-  float* p1s = reinterpret_cast<float*>(k3_smem + sizeof(T2) * S * BLOCK * P);
+  using P1T = typename std::conditional<K3Cfg<T2>::P1D, Rt, float>::type;  // row weights in shared memory
+  P1T* p1s = reinterpret_cast<P1T*>(k3_smem + sizeof(T2) * S * BLOCK * P);
   // per-chunk data of the NEXT chunk, prefetched with cp.async while the current chunk runs
   // (chunks are padded to BLOCK groups at plan time: chunk c's groups are [c BLOCK, (c+1) BLOCK))
   unsigned char* meta = k3_smem + sizeof(T2) * S * BLOCK * P + k3_p1_smem<T2, TAPS, P>();
@@ -1297,7 +1306,7 @@ __global__ void __launch_bounds__(K3Cfg<T2>::BLOCK, K3Cfg<T2>::MINB)
         for (int i = 0; i < WINR; ++i) p1r[k][i] = (Rt)w1[i];
       } else {
 #pragma unroll
-        for (int i = 0; i < WINR; ++i) p1s[(i * BLOCK + threadIdx.x) * P + k] = w1[i];
+        for (int i = 0; i < WINR; ++i) p1s[(i * BLOCK + threadIdx.x) * P + k] = (P1T)w1[i];
         // start the read of the running sum early (latency hidden by the term loop)
         base[k] = mk<T2>(0, 0);
         if constexpr (!K3Cfg<T2>::LEAN)
@@ -1340,7 +1349,16 @@ __global__ void __launch_bounds__(K3Cfg<T2>::BLOCK, K3Cfg<T2>::MINB)
 #pragma unroll
           for (int k = 0; k < P; ++k) w1[k] = p1r[k][i];
         } else {
-          load_p1_f<Rt, P>(p1s + (i * BLOCK + threadIdx.x) * P, w1);
+          if constexpr (K3Cfg<T2>::P1D) {
+#pragma unroll
+            for (int k = 0; k < P; k += 2) {
+              const double2 d = *reinterpret_cast<const double2*>(p1s + (i * BLOCK + threadIdx.x) * P + k);
+              w1[k] = (Rt)d.x;
+              w1[k + 1] = (Rt)d.y;
+            }
+          } else {
+            load_p1_f<Rt, P>(reinterpret_cast<const float*>(p1s) + (i * BLOCK + threadIdx.x) * P, w1);
+          }
         }
 #pragma unroll
         for (int k = 0; k < P; ++k) {
