@@ -205,6 +205,19 @@ fio_status fio_assign_wedges(int W, const double* cost, int nranks, int* owner);
 fio_status fio_profile_begin(fio_handle h, int max_applies);
 fio_status fio_profile_end(fio_handle h, double* stage_ms /* 5 */, int* n_applies);
 
+/* Plan save / load.  fio_plan_save writes the separation of every owned
+ * wedge in compact form -- skeleton columns C and Y = V S^{-1} (U = A(:, C) Y),
+ * skeleton rows R and Z = U_R^+ (beta = T = Z A(R, members)), the chosen r and
+ * the sampled error -- plus a header (N, W, dtype, taps, eps, beta, seed, rank, nranks and an FNV-1a
+ * hash of the phase / amplitude arrays).  fio_plan_load takes the same arguments as fio_plan plus
+ * the path; it validates the header against them (FIO_EINVAL on any mismatch or a malformed file)
+ * and rebuilds the plan with U and beta recomputed from the factors by the same kernels, skipping
+ * the randomized search: the loaded plan applies bit-identically to the saved one.  The file is
+ * host-endian binary; the caller owns path. */
+fio_status fio_plan_save(fio_handle h, const char* path);
+fio_status fio_plan_load(fio_handle* out, const char* path, int N, const fio_phase* phase,
+                         const fio_amplitude* amp, double eps, const fio_opts* opts);
+
 const char* fio_last_error(void); /* thread-local message of the last error */
 const char* fio_version(void);
 

@@ -32,7 +32,7 @@ FIO_C64, FIO_C128 = 1, 2
 FIO_OK, FIO_WNOTCERT = 0, 1
 
 # every entry point declared in include/fio.h
-SYMBOLS = ["fio_default_opts", "fio_plan", "fio_apply", "fio_apply_batch", "fio_apply_adjoint", "fio_apply_host", "fio_destroy", "fio_plan_info",
+SYMBOLS = ["fio_default_opts", "fio_plan", "fio_plan_save", "fio_plan_load", "fio_apply", "fio_apply_batch", "fio_apply_adjoint", "fio_apply_host", "fio_destroy", "fio_plan_info",
            "fio_plan_wedges", "fio_geometry", "fio_assign_wedges", "fio_profile_begin", "fio_profile_end",
            "fio_last_error", "fio_version"]
 STAGES = ["K0_rows", "K0_cols", "K1_rowpass", "K2_colpass", "K3_interp"]
@@ -93,6 +93,9 @@ def load_library():
     lib.fio_default_opts.restype = None
     lib.fio_plan.argtypes = [ctypes.POINTER(P), I, ctypes.POINTER(_Phase), ctypes.POINTER(_Amp), ctypes.c_double,
                              ctypes.POINTER(_Opts)]
+    lib.fio_plan_save.argtypes = [P, ctypes.c_char_p]
+    lib.fio_plan_load.argtypes = [ctypes.POINTER(P), ctypes.c_char_p, I, ctypes.POINTER(_Phase), ctypes.POINTER(_Amp),
+                                  ctypes.c_double, ctypes.POINTER(_Opts)]
     lib.fio_apply.argtypes = [P, P, P, P]
     lib.fio_apply_host.argtypes = [P, P, P, P]
     lib.fio_apply_adjoint.argtypes = [P, P, P, P]
@@ -185,7 +188,7 @@ class Plan:
                  dtype: str = "c128", n_wedges: int = 0, nufft_w: int = 0, nufft_beta: float = 0.0,
                  seed: int = 0x5EED, device: Optional[int] = None, rank: int = 0, nranks: int = 1,
                  r_init: int = 32, r_max: int = 512, certify: bool = True, rho_sign: int = 1,
-                 amplitude: str = "separable", skeleton: bool = False):
+                 amplitude: str = "separable", skeleton: bool = False, load: Optional[str] = None):
         import torch
         if not torch.cuda.is_available():
             raise FioError(-3, "no CUDA device: the FIO apply runs only on the GPU (no CPU fallback)")
@@ -216,12 +219,21 @@ class Plan:
         o.skeleton = int(bool(skeleton))
         h = ctypes.c_void_p()
         with torch.cuda.device(self.device):
-            self.status = _check(lib.fio_plan(ctypes.byref(h), self.N, ctypes.byref(ph), ctypes.byref(amp),
-                                              float(eps), ctypes.byref(o)))
+            if load is None:
+                self.status = _check(lib.fio_plan(ctypes.byref(h), self.N, ctypes.byref(ph), ctypes.byref(amp),
+                                                  float(eps), ctypes.byref(o)))
+            else:  # reuse a saved separation (fio_plan_load): same operator, N, eps and options required
+                self.status = _check(lib.fio_plan_load(ctypes.byref(h), os.fsencode(load), self.N, ctypes.byref(ph),
+                                                       ctypes.byref(amp), float(eps), ctypes.byref(o)))
         self._h = h
         self.eps = eps
         self.rank, self.nranks = int(rank), int(nranks)
         self.torch_dtype = torch.complex64 if self.c64 else torch.complex128
+
+    def save(self, path: str) -> None:
+        """fio_plan_save: write this plan's separation (per wedge C, V S^-1, R, U_R^+) to path;
+        Plan(..., load=path) rebuilds the identical plan without the randomized separation."""
+        _check(self._lib.fio_plan_save(self._h, os.fsencode(path)))
 
     # ------------------------------------------------------------ evaluation
     def apply(self, f, out=None, stream=None):

@@ -63,8 +63,20 @@ struct DevBuf {
 
 }  // namespace
 
+// The separation of one wedge in compact form (plan save/load): skeleton columns C, Y = V S^{-1}
+// (U = A(:, C) Y), skeleton rows R and Z = U_R^+ (beta = T = Z A(R, members)).
+struct WedgeFactors {
+  int l = 0, q = 0, r = 0;
+  double err = 0;
+  std::vector<int> C, R;
+  std::vector<cplx> Y, Z;
+};
+
 struct fio_plan_s {
   int N = 0, W = 0, taps = 0, c64 = 0, device = 0;
+  std::vector<WedgeFactors> factors;                 // per owned wedge, kept for fio_plan_save
+  const std::vector<WedgeFactors>* load = nullptr;   // fio_plan_load: factors read from a file
+  uint64_t input_hash = 0;                           // hash of the phase / amplitude arrays
   double eps = 0, es_beta = 0;
   fio_opts opts{};
   std::vector<WedgeGeom> geom;
@@ -210,7 +222,7 @@ namespace {
 // device, FP64), q, the final r and the sampled error.
 fio_status separate_wedge(fio_plan_s& P, const WedgeGeom& g, Rng& rng, cudaStream_t s, DevBuf& dU, DevBuf& dBeta,
                           int& q_out, int& r_out, double& err_out, std::vector<int>& C_out,
-                          std::vector<cplx>& Y_out) {
+                          std::vector<cplx>& Y_out, std::vector<int>& R_out, std::vector<cplx>& Z_out) {
   const int N = P.N;
   const int m = N * N;
   const int n = (int)g.members.size();
@@ -342,6 +354,8 @@ fio_status separate_wedge(fio_plan_s& P, const WedgeGeom& g, Rng& rng, cudaStrea
   FIO_CUDA(dAR.ensure(sizeof(double2) * (size_t)nR * n));
   FIO_CUDA(launch_eval_entries(P.op, g.u1, g.u2, dRows.as<int>(), nR, dMembers.as<int>(), n, dAR.as<double2>(), 1, nR,
                                s));
+  R_out = R;
+  Z_out = Z;
   FIO_CUDA(dZ.ensure(sizeof(double2) * Z.size()));
   FIO_CUDA(cudaMemcpy(dZ.p, Z.data(), sizeof(double2) * Z.size(), cudaMemcpyHostToDevice));
   FIO_CUDA(dBeta.ensure(sizeof(double2) * (size_t)q * n));
@@ -480,6 +494,44 @@ int fft_index(std::map<int, int>& lens, std::vector<FftLen>& tab, int L) {
   return idx;
 }
 
+// U = A(:, C) Y and beta = Z A(R, members) from saved factors: the same kernels and arguments as
+// separate_wedge, so a loaded plan reproduces the saved one bit for bit.
+fio_status expand_factors(fio_plan_s& P, const WedgeGeom& g, const WedgeFactors& F, cudaStream_t s, DevBuf& dU,
+                          DevBuf& dBeta) {
+  const int m = P.N * P.N;
+  const int n = (int)g.members.size();
+  const int q = F.q, rc = (int)F.C.size(), nR = (int)F.R.size();
+  if (q == 0) return FIO_OK;
+  if ((size_t)rc * q != F.Y.size() || (size_t)q * nR != F.Z.size()) {
+    set_error("fio_plan_load: inconsistent factors for wedge " + std::to_string(F.l));
+    return FIO_EINVAL;
+  }
+  DevBuf dMembers, dCols, dRows, dAC, dY, dAR, dZ;
+  FIO_CUDA(dMembers.ensure(sizeof(int) * n));
+  FIO_CUDA(cudaMemcpy(dMembers.p, g.members.data(), sizeof(int) * n, cudaMemcpyHostToDevice));
+  FIO_CUDA(dCols.ensure(sizeof(int) * rc));
+  FIO_CUDA(cudaMemcpy(dCols.p, F.C.data(), sizeof(int) * rc, cudaMemcpyHostToDevice));
+  FIO_CUDA(dAC.ensure(sizeof(double2) * (size_t)m * rc));
+  FIO_CUDA(launch_eval_entries(P.op, g.u1, g.u2, nullptr, m, dCols.as<int>(), rc, dAC.as<double2>(), 1, m, s));
+  FIO_CUDA(dY.ensure(sizeof(double2) * F.Y.size()));
+  FIO_CUDA(cudaMemcpy(dY.p, F.Y.data(), sizeof(double2) * F.Y.size(), cudaMemcpyHostToDevice));
+  FIO_CUDA(dU.ensure(sizeof(double2) * (size_t)m * q));
+  FIO_CUDA(launch_zgemm(m, q, rc, dAC.as<double2>(), 1, m, false, dY.as<double2>(), 1, rc, dU.as<double2>(), 1, m, 1,
+                        nullptr, s));
+  dAC.release();
+  FIO_CUDA(dRows.ensure(sizeof(int) * nR));
+  FIO_CUDA(cudaMemcpy(dRows.p, F.R.data(), sizeof(int) * nR, cudaMemcpyHostToDevice));
+  FIO_CUDA(dAR.ensure(sizeof(double2) * (size_t)nR * n));
+  FIO_CUDA(launch_eval_entries(P.op, g.u1, g.u2, dRows.as<int>(), nR, dMembers.as<int>(), n, dAR.as<double2>(), 1, nR,
+                               s));
+  FIO_CUDA(dZ.ensure(sizeof(double2) * F.Z.size()));
+  FIO_CUDA(cudaMemcpy(dZ.p, F.Z.data(), sizeof(double2) * F.Z.size(), cudaMemcpyHostToDevice));
+  FIO_CUDA(dBeta.ensure(sizeof(double2) * (size_t)q * n));
+  FIO_CUDA(launch_zgemm(q, n, nR, dZ.as<double2>(), 1, q, false, dAR.as<double2>(), 1, nR, dBeta.as<double2>(), 1, q,
+                        1, nullptr, s));
+  return FIO_OK;
+}
+
 fio_status build_plan(fio_plan_s& P, const fio_phase* phase, const fio_amplitude* amp) {
   const int N = P.N;
   const long long NN = (long long)N * N;
@@ -560,10 +612,29 @@ fio_status build_plan(fio_plan_s& P, const fio_phase* phase, const fio_amplitude
     DevBuf dU, dBeta;
     int q = 0, r = 0;
     double err = 0;
-    std::vector<int> Cs;
-    std::vector<cplx> Ys;
-    fio_status st = separate_wedge(P, g, rng, s, dU, dBeta, q, r, err, Cs, Ys);
+    WedgeFactors F;
+    fio_status st;
+    if (P.load) {  // fio_plan_load: the saved separation of this wedge
+      const WedgeFactors* src = nullptr;
+      for (const WedgeFactors& f : *P.load)
+        if (f.l == g.l) src = &f;
+      if (!src) {
+        set_error("fio_plan_load: the file has no factors for wedge " + std::to_string(g.l));
+        return FIO_EINVAL;
+      }
+      F = *src;
+      st = expand_factors(P, g, F, s, dU, dBeta);
+    } else {
+      F.l = g.l;
+      st = separate_wedge(P, g, rng, s, dU, dBeta, F.q, F.r, F.err, F.C, F.Y, F.R, F.Z);
+    }
     if (st != FIO_OK) return st;
+    q = F.q;
+    r = F.r;
+    err = F.err;
+    P.factors.push_back(std::move(F));
+    const std::vector<int>& Cs = P.factors.back().C;
+    const std::vector<cplx>& Ys = P.factors.back().Y;
     WedgeDev w{};
     w.l = g.l;
     w.q = q;
@@ -896,8 +967,139 @@ ApplyArgs make_args(const fio_plan_s& P) {
 
 extern "C" {
 
+// ------------------------------------------------------------------ plan save / load
+struct SaveHeader {
+  char magic[8];  // "FIOPLAN1"
+  int32_t version, N, W, dtype, taps, rank, nranks, skeleton, n_owned;
+  double eps, es_beta;
+  uint64_t seed, input_hash;
+};
+
+// FNV-1a over the operator inputs the plan depends on (phase and amplitude arrays, kinds).
+static uint64_t fnv1a(uint64_t h, const void* p, size_t n) {
+  const unsigned char* b = static_cast<const unsigned char*>(p);
+  for (size_t i = 0; i < n; ++i) {
+    h ^= b[i];
+    h *= 1099511628211ull;
+  }
+  return h;
+}
+static uint64_t input_hash(int N, const fio_phase* phase, const fio_amplitude* amp) {
+  const size_t NN = (size_t)N * N;
+  uint64_t h = 1469598103934665603ull;
+  h = fnv1a(h, phase->c1, sizeof(double) * NN);
+  h = fnv1a(h, phase->c2, sizeof(double) * NN);
+  const int flags[4] = {phase->b1 != nullptr, phase->b2 != nullptr, phase->rho_sign < 0 ? -1 : 1,
+                        amp ? amp->kind : FIO_AMP_SEPARABLE};
+  h = fnv1a(h, flags, sizeof(flags));
+  if (phase->b1) h = fnv1a(h, phase->b1, sizeof(double) * NN);
+  if (phase->b2) h = fnv1a(h, phase->b2, sizeof(double) * NN);
+  if (amp && amp->K > 0) {
+    h = fnv1a(h, &amp->K, sizeof(int));
+    h = fnv1a(h, amp->px, 2 * sizeof(double) * NN * amp->K);
+    h = fnv1a(h, amp->pxi, 2 * sizeof(double) * NN * amp->K);
+  }
+  return h;
+}
+
+static fio_status plan_impl(fio_handle* out, int N, const fio_phase* phase, const fio_amplitude* amp, double eps,
+                            const fio_opts* opts, const std::vector<WedgeFactors>* load, const SaveHeader* hdr);
+
 fio_status fio_plan(fio_handle* out, int N, const fio_phase* phase, const fio_amplitude* amp, double eps,
                     const fio_opts* opts) {
+  return plan_impl(out, N, phase, amp, eps, opts, nullptr, nullptr);
+}
+
+fio_status fio_plan_save(fio_handle h, const char* path) {
+  if (!h || !path) {
+    set_error("fio_plan_save: NULL argument");
+    return FIO_EINVAL;
+  }
+  FILE* fp = std::fopen(path, "wb");
+  if (!fp) {
+    set_error(std::string("fio_plan_save: cannot open ") + path);
+    return FIO_EINVAL;
+  }
+  SaveHeader hd{};
+  std::memcpy(hd.magic, "FIOPLAN1", 8);
+  hd.version = 1;
+  hd.N = h->N;
+  hd.W = h->W;
+  hd.dtype = h->opts.dtype;
+  hd.taps = h->taps;
+  hd.rank = h->opts.rank;
+  hd.nranks = h->opts.nranks;
+  hd.skeleton = h->opts.skeleton;
+  hd.n_owned = (int)h->factors.size();
+  hd.eps = h->eps;
+  hd.es_beta = h->es_beta;
+  hd.seed = h->opts.seed;
+  hd.input_hash = h->input_hash;
+  bool ok = std::fwrite(&hd, sizeof(hd), 1, fp) == 1;
+  for (const WedgeFactors& F : h->factors) {
+    const int32_t head[5] = {F.l, F.q, F.r, (int32_t)F.C.size(), (int32_t)F.R.size()};
+    ok = ok && std::fwrite(head, sizeof(head), 1, fp) == 1;
+    ok = ok && std::fwrite(&F.err, sizeof(double), 1, fp) == 1;
+    ok = ok && std::fwrite(F.C.data(), sizeof(int), F.C.size(), fp) == F.C.size();
+    ok = ok && std::fwrite(F.R.data(), sizeof(int), F.R.size(), fp) == F.R.size();
+    ok = ok && std::fwrite(F.Y.data(), sizeof(cplx), F.Y.size(), fp) == F.Y.size();
+    ok = ok && std::fwrite(F.Z.data(), sizeof(cplx), F.Z.size(), fp) == F.Z.size();
+  }
+  ok = (std::fclose(fp) == 0) && ok;
+  if (!ok) {
+    set_error(std::string("fio_plan_save: write failed: ") + path);
+    return FIO_EINVAL;
+  }
+  return FIO_OK;
+}
+
+fio_status fio_plan_load(fio_handle* out, const char* path, int N, const fio_phase* phase, const fio_amplitude* amp,
+                         double eps, const fio_opts* opts) {
+  if (!out || !path) {
+    set_error("fio_plan_load: NULL argument");
+    return FIO_EINVAL;
+  }
+  *out = nullptr;
+  FILE* fp = std::fopen(path, "rb");
+  if (!fp) {
+    set_error(std::string("fio_plan_load: cannot open ") + path);
+    return FIO_EINVAL;
+  }
+  SaveHeader hd{};
+  bool ok = std::fread(&hd, sizeof(hd), 1, fp) == 1 && std::memcmp(hd.magic, "FIOPLAN1", 8) == 0 && hd.version == 1 &&
+            hd.n_owned >= 0 && hd.n_owned <= 1 << 16;
+  std::vector<WedgeFactors> fs;
+  for (int i = 0; ok && i < hd.n_owned; ++i) {
+    WedgeFactors F;
+    int32_t head[5];
+    ok = std::fread(head, sizeof(head), 1, fp) == 1 && std::fread(&F.err, sizeof(double), 1, fp) == 1;
+    if (!ok) break;
+    F.l = head[0];
+    F.q = head[1];
+    F.r = head[2];
+    const long long nc = head[3], nr = head[4];
+    ok = F.q >= 0 && nc >= 0 && nr >= 0 && nc <= (1 << 20) && nr <= (1 << 22) && F.q <= (1 << 16);
+    if (!ok) break;
+    F.C.resize(nc);
+    F.R.resize(nr);
+    F.Y.resize((size_t)nc * F.q);
+    F.Z.resize((size_t)F.q * nr);
+    ok = std::fread(F.C.data(), sizeof(int), F.C.size(), fp) == F.C.size() &&
+         std::fread(F.R.data(), sizeof(int), F.R.size(), fp) == F.R.size() &&
+         std::fread(F.Y.data(), sizeof(cplx), F.Y.size(), fp) == F.Y.size() &&
+         std::fread(F.Z.data(), sizeof(cplx), F.Z.size(), fp) == F.Z.size();
+    fs.push_back(std::move(F));
+  }
+  std::fclose(fp);
+  if (!ok) {
+    set_error(std::string("fio_plan_load: not a valid plan file: ") + path);
+    return FIO_EINVAL;
+  }
+  return plan_impl(out, N, phase, amp, eps, opts, &fs, &hd);
+}
+
+static fio_status plan_impl(fio_handle* out, int N, const fio_phase* phase, const fio_amplitude* amp, double eps,
+                            const fio_opts* opts, const std::vector<WedgeFactors>* load, const SaveHeader* hdr) {
   if (!out) {
     set_error("fio_plan: out is NULL");
     return FIO_EINVAL;
@@ -975,7 +1177,20 @@ fio_status fio_plan(fio_handle* out, int N, const fio_phase* phase, const fio_am
   P->es_beta = o.nufft_beta > 0 ? o.nufft_beta : 2.30 * P->taps;
   // polynomial kernel for the c128 K3 weights: error ~1.5 e^{-beta}, the kernel's own edge value
   P->poly_err = es_poly_fit(P->taps, P->es_beta, 2.0 * std::exp(-P->es_beta), P->poly);
+  P->input_hash = input_hash(N, phase, amp);
+  if (load) {  // fio_plan_load: the file must describe exactly this plan
+    const bool same = hdr->N == N && hdr->W == P->W && hdr->dtype == o.dtype && hdr->taps == P->taps &&
+                      hdr->rank == o.rank && hdr->nranks == o.nranks && hdr->eps == eps &&
+                      hdr->es_beta == P->es_beta && hdr->seed == o.seed && hdr->input_hash == P->input_hash;
+    if (!same) {
+      delete P;
+      set_error("fio_plan_load: the file was saved for a different operator, size, eps or options");
+      return FIO_EINVAL;
+    }
+    P->load = load;
+  }
   fio_status st = build_plan(*P, phase, amp);
+  P->load = nullptr;
   if (st < 0) {
     delete P;
     return st;

@@ -429,3 +429,34 @@ def test_c64_storage_at_1e6():
     _, out = run(op, f, eps=1e-6, dtype="c64")
     err = oracle.rel_l2(out, oracle.fio(op, f))
     assert err <= 1e-5, err
+
+
+# ------------------------------------------------------------------ plan save / load (NEXT-3)
+@pytest.mark.parametrize("dtype,skeleton", [("c128", False), ("c64", False), ("c128", True)])
+def test_plan_save_load_roundtrip(tmp_path, dtype, skeleton):
+    N = 128
+    op = wl.grt_operator(N)
+    eps = 1e-6 if dtype == "c128" else 1e-4
+    tdt = torch.complex64 if dtype == "c64" else torch.complex128
+    p1 = make_plan(op, eps, dtype, skeleton=skeleton)
+    path = str(tmp_path / "plan.fio")
+    p1.save(path)
+    p2 = make_plan(op, eps, dtype, skeleton=skeleton, load=path)
+    assert p2.info["sum_q"] == p1.info["sum_q"] and p2.info["W"] == p1.info["W"]
+    f = torch.from_numpy(wl.white_noise(N, 5, dtype)).to(DEV, tdt)
+    a, b = p1.apply(f), p2.apply(f)
+    torch.cuda.synchronize()
+    assert torch.equal(a, b)  # same factors, same kernels: bit-identical
+    print("plan s", p1.info["plan_seconds"], "load s", p2.info["plan_seconds"])
+
+
+def test_plan_load_rejects_other_operator(tmp_path):
+    N = 64
+    op = wl.grt_operator(N)
+    p1 = make_plan(op)
+    path = str(tmp_path / "plan.fio")
+    p1.save(path)
+    with pytest.raises(fio.FioError):
+        make_plan(op, eps=1e-5, load=path)  # other eps
+    with pytest.raises(fio.FioError):
+        make_plan(wl.wave_operator(N), load=path)  # other phase (hash)

@@ -101,3 +101,21 @@ def test_no_cpu_fallback():
     op = wl.grt_operator(64)
     with pytest.raises(fio.FioError):
         fio.Plan(64, op.c1, op.c2)
+
+
+def test_plan_load_rejects_missing_and_malformed_files(tmp_path):
+    # fio_plan_load validates the file before touching the GPU (include/fio.h)
+    import ctypes
+    lib = fio.load_library()
+    N = 16
+    c = np.full(N * N, 0.5)
+    ph = fio._Phase(c.ctypes.data, c.ctypes.data, None, None, 1)
+    amp = fio._Amp(0, None, None, 0)
+    h = ctypes.c_void_p()
+    st = lib.fio_plan_load(ctypes.byref(h), str(tmp_path / "missing.fio").encode(), N, ctypes.byref(ph),
+                           ctypes.byref(amp), 1e-6, None)
+    assert st == -1 and b"cannot open" in lib.fio_last_error()
+    bad = tmp_path / "bad.fio"
+    bad.write_bytes(b"not a plan file at all" * 8)
+    st = lib.fio_plan_load(ctypes.byref(h), str(bad).encode(), N, ctypes.byref(ph), ctypes.byref(amp), 1e-6, None)
+    assert st == -1 and b"not a valid plan file" in lib.fio_last_error()
