@@ -606,9 +606,16 @@ fio_status build_plan(fio_plan_s& P, const fio_phase* phase, const fio_amplitude
   P.fft_N = fft_index(lens, ffts, N);
 
   // per owned wedge: separation, folding of alpha' and beta'
+  const bool prof = std::getenv("FIO_PLAN_PROFILE") != nullptr;  // per-phase plan timing to stderr
+  double t_sep = 0, t_group = 0, t_fold = 0, t_gp = 0, t_d2h = 0;
+  auto now = [] { return std::chrono::steady_clock::now(); };
+  auto secs = [](std::chrono::steady_clock::time_point a, std::chrono::steady_clock::time_point b) {
+    return std::chrono::duration<double>(b - a).count();
+  };
   for (size_t wi = 0; wi < P.owned.size(); ++wi) {
     const WedgeGeom& g = P.geom[P.owned[wi]];
     Rng rng(P.opts.seed ^ (0x9E3779B97F4A7C15ull * (uint64_t)(g.l + 1)));
+    auto tw0 = now();
     DevBuf dU, dBeta;
     int q = 0, r = 0;
     double err = 0;
@@ -633,6 +640,9 @@ fio_status build_plan(fio_plan_s& P, const fio_phase* phase, const fio_amplitude
     r = F.r;
     err = F.err;
     P.factors.push_back(std::move(F));
+    if (prof) cudaDeviceSynchronize();
+    auto tw1 = now();
+    t_sep += secs(tw0, tw1);
     const std::vector<int>& Cs = P.factors.back().C;
     const std::vector<cplx>& Ys = P.factors.back().Y;
     WedgeDev w{};
@@ -659,12 +669,17 @@ fio_status build_plan(fio_plan_s& P, const fio_phase* phase, const fio_amplitude
       std::vector<double> uh(2 * NN);
       FIO_CUDA(cudaMemcpyAsync(uh.data(), du.p, sizeof(double2) * NN, cudaMemcpyDeviceToHost, s));
       FIO_CUDA(cudaStreamSynchronize(s));
+      auto tg0 = now();
+#pragma omp parallel for schedule(static)
       for (long long x = 0; x < NN; ++x) std::swap(uh[2 * x], uh[2 * x + 1]);  // (K3 row, column) = (u2, u1)
       std::vector<int> anchor, slot_x;
       std::vector<double> off;
       group_points(uh.data(), NN, P.taps, group_p(c64), g.n2f, g.n1f, super_rows(c64), super_cols(c64), anchor, slot_x,
                    off);
       const int gp = group_p(c64);
+      auto tg1 = now();
+      t_gp += secs(tg0, tg1);
+      t_d2h += secs(tw1, tg0);
       real_groups = (long long)(anchor.size() / 2);
       std::vector<int> box;
       const int blk = c64 ? kK3BlockC64 : kK3BlockC128;
@@ -676,6 +691,7 @@ fio_status build_plan(fio_plan_s& P, const fio_phase* phase, const fio_amplitude
          // repeat the chunk's first anchor (inside the box), have no points (slot -1) and alpha' = 0.
         std::vector<int> pa((size_t)iw.nchunks * blk * 2), ps((size_t)iw.nchunks * blk * gp, -1);
         std::vector<double> po((size_t)iw.nchunks * blk * gp * 2, 0.5 * P.taps);
+#pragma omp parallel for schedule(static)
         for (int c = 0; c < iw.nchunks; ++c) {
           const long long g0 = box[6 * c], n = box[6 * c + 5];
           for (long long i = 0; i < blk; ++i) {
@@ -701,7 +717,9 @@ fio_status build_plan(fio_plan_s& P, const fio_phase* phase, const fio_amplitude
       FIO_CUDA(P.upload(&d_anchor, anchor.data(), anchor.size()));
       FIO_CUDA(P.upload(&d_slot, slot_x.data(), slot_x.size()));
       if (c64) {
-        std::vector<float> offf(off.begin(), off.end());
+        std::vector<float> offf(off.size());
+#pragma omp parallel for schedule(static)
+        for (long long i = 0; i < (long long)off.size(); ++i) offf[i] = (float)off[i];
         float* d_off = nullptr;
         FIO_CUDA(P.upload(&d_off, offf.data(), offf.size()));
         iw.slot_off = d_off;
@@ -720,6 +738,8 @@ fio_status build_plan(fio_plan_s& P, const fio_phase* phase, const fio_amplitude
       P.max_tile_cap = std::max(P.max_tile_cap, cap);
       P.meta_bytes += anchor.size() * 4 + slot_x.size() * 4 + off.size() * (c64 ? 4 : 8);
     }
+    auto tw2 = now();
+    t_group += secs(tw1, tw2);
     const long long nslots = (long long)iw.ngroups * group_p(c64);
     void* alpha = nullptr;
     void* betap = nullptr;
@@ -763,6 +783,8 @@ fio_status build_plan(fio_plan_s& P, const fio_phase* phase, const fio_amplitude
                                 dd2.as<double>(), betap, c64, s));
       FIO_CUDA(cudaStreamSynchronize(s));
     }
+    if (prof) cudaDeviceSynchronize();
+    t_fold += secs(tw2, now());
     if (!P.opts.skeleton) P.alpha_bytes += cs * (size_t)q * nslots;
     P.slots += real_groups * group_p(c64);  // point slots before the chunk padding
     P.slot_terms += nslots * (long long)q;
@@ -789,6 +811,11 @@ fio_status build_plan(fio_plan_s& P, const fio_phase* phase, const fio_amplitude
     if (err > 10.0 * P.eps) P.certified = 0;  // reading R7: certify at the 10 eps apply budget
   }
 
+  if (prof)
+    std::fprintf(stderr,
+                 "fio plan: separation %.2f s, K3 grouping %.2f s (coords+D2H %.2f, group_points %.2f), alpha'/beta' "
+                 "folding %.2f s (%zu wedges)\n",
+                 t_sep, t_group, t_d2h, t_gp, t_fold, P.owned.size());
   if (P.opts.skeleton) {  // one alpha' scratch shared by the wedges (rebuilt per wedge per apply)
     void* scratch = nullptr;
     FIO_CUDA(P.alloc(&scratch, cs * std::max<size_t>(P.scratch_elems, 1)));

@@ -284,54 +284,64 @@ void group_points(const double* u, long long NN, int taps, int P, int n1f, int n
   const long long n1s = kSuperRows == 1 ? n1f + 16 : n1f / 2 + 8, n2s = kSuperCols == 1 ? n2f + 16 : n2f / 2 + 8;
   const long long nkeys = n1s * n2s;
   std::vector<int> key(NN);
-  std::vector<long long> cnt(nkeys + 1, 0);
+#pragma omp parallel for schedule(static)
   for (long long x = 0; x < NN; ++x) {
     long long b1 = (long long)std::ceil(u[2 * x] - 0.5 * taps);
     long long b2 = (long long)std::ceil(u[2 * x + 1] - 0.5 * taps);
     long long s1 = (kSuperRows == 1 ? b1 : floor_div2(b1)) - lo1, s2 = (kSuperCols == 1 ? b2 : floor_div2(b2)) - lo2;
-    long long k = s1 * n2s + s2;
-    key[x] = (int)k;
-    cnt[k + 1]++;
+    key[x] = (int)(s1 * n2s + s2);
   }
+  std::vector<long long> cnt(nkeys + 1, 0);
+  for (long long x = 0; x < NN; ++x) cnt[key[x] + 1]++;
   for (long long k = 0; k < nkeys; ++k) cnt[k + 1] += cnt[k];
+  // points sorted by supercell (stable: by x within a supercell), carrying their coordinates
   std::vector<int> order(NN);
+  std::vector<double> us(2 * NN);
   {
     std::vector<long long> pos(cnt.begin(), cnt.end() - 1);
-    for (long long x = 0; x < NN; ++x) order[pos[key[x]]++] = (int)x;
+    for (long long x = 0; x < NN; ++x) {
+      const long long p = pos[key[x]]++;
+      order[p] = (int)x;
+      us[2 * p] = u[2 * x];
+      us[2 * p + 1] = u[2 * x + 1];
+    }
   }
-  anchor.clear();
-  slot_x.clear();
-  off.clear();
   // supercells in serpentine order of 8 x 8 blocks, so that any run of consecutive groups
   // (one K3 CTA chunk) has a compact footprint on the fine grid
   const long long BS = 8;
   const long long nb1 = (n1s + BS - 1) / BS, nb2 = (n2s + BS - 1) / BS;
-  for (long long bb1 = 0; bb1 < nb1; ++bb1) {
+  std::vector<long long> sc;  // non-empty supercell keys in traversal order
+  sc.reserve(nkeys);
+  for (long long bb1 = 0; bb1 < nb1; ++bb1)
     for (long long jb = 0; jb < nb2; ++jb) {
       const long long bb2 = (bb1 % 2 == 0) ? jb : nb2 - 1 - jb;
-      for (long long s1 = bb1 * BS; s1 < std::min(n1s, (bb1 + 1) * BS); ++s1) {
+      for (long long s1 = bb1 * BS; s1 < std::min(n1s, (bb1 + 1) * BS); ++s1)
         for (long long s2 = bb2 * BS; s2 < std::min(n2s, (bb2 + 1) * BS); ++s2) {
           const long long k = s1 * n2s + s2;
-          const long long b = cnt[k], e = cnt[k + 1];
-          if (b == e) continue;
-          const int a1 = (int)(kSuperRows * (s1 + lo1)), a2 = (int)(kSuperCols * (s2 + lo2));
-          for (long long i = b; i < e; i += P) {
-            anchor.push_back(a1);
-            anchor.push_back(a2);
-            for (int j = 0; j < P; ++j) {
-              if (i + j < e) {
-                const int x = order[i + j];
-                slot_x.push_back(x);
-                off.push_back(u[2 * (long long)x] - a1);
-                off.push_back(u[2 * (long long)x + 1] - a2);
-              } else {
-                slot_x.push_back(-1);
-                off.push_back(0.5 * taps);
-                off.push_back(0.5 * taps);
-              }
-            }
-          }
+          if (cnt[k + 1] > cnt[k]) sc.push_back(k);
         }
+    }
+  const long long nsc = (long long)sc.size();
+  std::vector<long long> goff(nsc + 1, 0);  // first group of each supercell
+  for (long long i = 0; i < nsc; ++i) goff[i + 1] = goff[i] + (cnt[sc[i] + 1] - cnt[sc[i]] + P - 1) / P;
+  const long long G = goff[nsc];
+  anchor.assign(2 * G, 0);
+  slot_x.assign((size_t)P * G, -1);
+  off.assign((size_t)2 * P * G, 0.5 * taps);
+#pragma omp parallel for schedule(dynamic, 512)
+  for (long long i = 0; i < nsc; ++i) {
+    const long long k = sc[i], s1 = k / n2s, s2 = k - s1 * n2s;
+    const int a1 = (int)(kSuperRows * (s1 + lo1)), a2 = (int)(kSuperCols * (s2 + lo2));
+    const long long b = cnt[k], e = cnt[k + 1];
+    long long g = goff[i];
+    for (long long p = b; p < e; p += P, ++g) {
+      anchor[2 * g] = a1;
+      anchor[2 * g + 1] = a2;
+      for (int j = 0; j < P && p + j < e; ++j) {
+        const long long sl = g * P + j;
+        slot_x[sl] = order[p + j];
+        off[2 * sl] = us[2 * (p + j)] - a1;
+        off[2 * sl + 1] = us[2 * (p + j) + 1] - a2;
       }
     }
   }
