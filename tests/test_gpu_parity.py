@@ -460,3 +460,26 @@ def test_plan_load_rejects_other_operator(tmp_path):
         make_plan(op, eps=1e-5, load=path)  # other eps
     with pytest.raises(fio.FioError):
         make_plan(wl.wave_operator(N), load=path)  # other phase (hash)
+
+
+def test_apply_captures_into_cuda_graph():
+    # the whole apply (K0..K3 on the caller's stream plus the plan's side stream, fork/join by events)
+    # is capturable: replaying the graph reproduces the eager result bit for bit
+    N = 128
+    op = wl.grt_operator(N)
+    plan = make_plan(op)
+    f = torch.from_numpy(wl.white_noise(N, 6)).to(DEV)
+    ref = plan.apply(f)
+    out = torch.empty_like(f)
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(s):
+        plan.apply(f, out=out)  # warm-up on the capture stream
+    torch.cuda.current_stream().wait_stream(s)
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        plan.apply(f, out=out)
+    out.zero_()
+    g.replay()
+    torch.cuda.synchronize()
+    assert torch.equal(out, ref)
