@@ -1710,126 +1710,6 @@ __global__ void __launch_bounds__(128) k_spread_groups(InterpWedge iw, T2* __res
   }
 }
 
-// K3* with shared-memory accumulation (FIO_SPREAD_TILES): a CTA takes a K3 chunk (BLOCK groups and
-// their footprint box, the same chunks as the forward K3).  Per term it spreads every group's
-// conj(alpha') g-weighted window into a shared tile of the footprint (lanes of a warp that share an
-// anchor are summed with the segmented shuffle first; the remaining conflicts are shared-memory
-// atomics), then flushes the tile to G*_lt with one coalesced global RED per non-zero cell and
-// zeroes it.  Global atomics drop from (window cells x groups) to (tile cells) per chunk-term.
-__device__ __forceinline__ void smem_add(float2* p, float2 v) {
-  unsigned long long* a = reinterpret_cast<unsigned long long*>(p);
-  unsigned long long old = *a, assumed;
-  do {
-    assumed = old;
-    float2 f = *reinterpret_cast<float2*>(&assumed);
-    f.x += v.x;
-    f.y += v.y;
-    old = atomicCAS(a, assumed, *reinterpret_cast<unsigned long long*>(&f));
-  } while (old != assumed);
-}
-__device__ __forceinline__ void smem_add(double2* p, double2 v) {
-  atomicAdd(&p->x, v.x);
-  atomicAdd(&p->y, v.y);
-}
-
-template <typename T2> struct SpreadCfg;
-template <> struct SpreadCfg<float2> { static constexpr int BLOCK = kK3BlockC64, CAP = kK3TileCapC64; };
-template <> struct SpreadCfg<double2> { static constexpr int BLOCK = kK3BlockC128, CAP = kK3TileCapC128; };
-
-template <typename T2, int TAPS, int P>
-__global__ void __launch_bounds__(SpreadCfg<T2>::BLOCK) k_spread_tiles(InterpWedge iw, T2* __restrict__ gstar,
-                                                                     const T2* __restrict__ g, EsPoly poly) {
-  using Rt = typename Real<T2>::type;
-  using O2 = typename OffT<T2>::type;
-  constexpr int WIN = k3_window_cols(TAPS, sizeof(T2) == 8);
-  constexpr int WINR = k3_window_rows(TAPS, sizeof(T2) == 8);
-  constexpr int BLOCK = SpreadCfg<T2>::BLOCK;
-  extern __shared__ __align__(16) unsigned char sp_smem[];
-  T2* tile = reinterpret_cast<T2*>(sp_smem);
-  const int n1f = iw.nrow, n2p = iw.ncolp, q = iw.q;
-  const long long gstride = (long long)n1f * n2p;
-  const long long nslots = (long long)iw.ngroups * P;
-  T2* __restrict__ G = gstar + iw.g_off + kHalo;
-  const T2* __restrict__ alpha = reinterpret_cast<const T2*>(iw.alpha);
-  const O2* __restrict__ offs = reinterpret_cast<const O2*>(iw.slot_off);
-  const int lane = threadIdx.x & 31;
-  for (int idx = threadIdx.x; idx < iw.tile_cap; idx += BLOCK) tile[idx] = mk<T2>(0, 0);
-  for (int ch = blockIdx.x; ch < iw.nchunks; ch += gridDim.x) {
-    const int* cb = iw.box + 6 * ch;  // first group, r_lo, c_lo, nr, nc, groups
-    const int grp = ch * BLOCK + threadIdx.x;  // chunks are padded to BLOCK groups
-    const int rlo = cb[1], clo = cb[2], nr = cb[3], nc = cb[4];
-    const int a1 = iw.anchor[2 * grp] - rlo, a2 = iw.anchor[2 * grp + 1] - clo;
-    const unsigned long long key = ((unsigned long long)(unsigned)a1 << 32) | (unsigned)a2;
-    const unsigned same = __match_any_sync(0xffffffffu, key);
-    const unsigned above = same >> lane;
-    const int run = above == 0xffffffffu ? 32 : __ffs(~above) - 1;  // a whole-warp run has ~above == 0
-    const bool head = lane == 0 || !((same >> (lane - 1)) & 1u);
-    int maxrun = run;
-#pragma unroll
-    for (int d = 16; d > 0; d >>= 1) maxrun = max(maxrun, __shfl_xor_sync(0xffffffffu, maxrun, d));
-    Rt p1[P][WINR], p2[P][WIN];
-    T2 gx[P];
-#pragma unroll
-    for (int k = 0; k < P; ++k) {
-      const int x = iw.slot_x[(long long)grp * P + k];
-      const O2 o = offs[(long long)grp * P + k];
-      gx[k] = x >= 0 ? g[x] : mk<T2>(0, 0);
-      float w1[WINR];
-      row_weights_f32<Rt, TAPS, WINR>((Rt)o.x, poly, w1);  // the forward K3's FP32 row weights
-#pragma unroll
-      for (int i = 0; i < WINR; ++i) p1[k][i] = (Rt)w1[i];
-      window_weights<Rt, TAPS, WIN>((Rt)o.y, (Rt)0, (Rt)0, poly, p2[k]);
-    }
-    T2 anext[P];
-#pragma unroll
-    for (int k = 0; k < P; ++k) anext[k] = q > 0 ? alpha[(long long)grp * P + k] : mk<T2>(0, 0);
-    for (int t = 0; t < q; ++t) {
-      T2 c[P];
-#pragma unroll
-      for (int k = 0; k < P; ++k) {
-        const T2 av = anext[k];  // conj(alpha') g
-        c[k] = mk<T2>(av.x * gx[k].x + av.y * gx[k].y, av.x * gx[k].y - av.y * gx[k].x);
-      }
-      if (t + 1 < q) {
-#pragma unroll
-        for (int k = 0; k < P; ++k) anext[k] = alpha[(t + 1) * nslots + (long long)grp * P + k];
-      }
-      T2* wp = tile + a1 * nc + a2;
-#pragma unroll 1
-      for (int i = 0; i < WINR; ++i) {
-        T2 e[P];
-#pragma unroll
-        for (int k = 0; k < P; ++k) e[k] = mk<T2>(p1[k][i] * c[k].x, p1[k][i] * c[k].y);
-#pragma unroll
-        for (int j = 0; j < WIN; ++j) {
-          T2 v = mk<T2>(0, 0);
-#pragma unroll
-          for (int k = 0; k < P; ++k) v = cfma_real(p2[k][j], e[k], v);
-          for (int d = 1; d < maxrun; d <<= 1) {
-            const T2 u = shfl_down_t2(v, d);
-            if (d < run) v = cadd(v, u);
-          }
-          if (head) smem_add(wp + j, v);
-        }
-        wp += nc;
-      }
-      __syncthreads();  // the tile holds term t's spread
-      const T2* __restrict__ gt = G + t * gstride;
-      for (int idx = threadIdx.x; idx < nr * nc; idx += BLOCK) {
-        const T2 v = tile[idx];
-        if (v.x != (Rt)0 || v.y != (Rt)0) {
-          const int rr = idx / nc, cc = idx - rr * nc;
-          int r = rlo + rr;
-          r = r < 0 ? r + n1f : (r >= n1f ? r - n1f : r);
-          red_add(const_cast<T2*>(gt) + (long long)r * n2p + clo + cc, v);
-          tile[idx] = mk<T2>(0, 0);
-        }
-      }
-      __syncthreads();  // the tile is zero again
-    }
-  }
-}
-
 // K2*: job (w, t, c0, C) over fine rows j2 in [c0, c0 + C) of G*_lt.
 template <typename T2>
 __global__ void __launch_bounds__(256) k_colpass_adj(const WedgeDev* __restrict__ wedges,
@@ -1943,9 +1823,6 @@ __global__ void __launch_bounds__(1024) k_dc_adj(long long NN, const double2* __
   if (threadIdx.x == 0) fhat[0] = mk<T2>((typename Real<T2>::type)sr[0], (typename Real<T2>::type)si[0]);
 }
 
-#ifndef FIO_SPREAD_TILES
-#define FIO_SPREAD_TILES 0  // shared-tile spread: correct, measured slower (N=1024: c128 107 vs 76 ms, c64 43.7 vs 15.9 ms)
-#endif
 template <typename T2, int TAPS, int P>
 static cudaError_t launch_spread_tp(const ApplyArgs& a, int wi, const T2* g, cudaStream_t s) {
   static int sms = 0;
@@ -1955,22 +1832,6 @@ static cudaError_t launch_spread_tp(const ApplyArgs& a, int wi, const T2* g, cud
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   }
   const InterpWedge& iw = a.iw[wi];
-  if (FIO_SPREAD_TILES) {
-    constexpr int BLOCK = SpreadCfg<T2>::BLOCK;
-    const size_t smem = sizeof(T2) * (size_t)SpreadCfg<T2>::CAP;
-    static bool configured = false;
-    if (!configured) {
-      cudaError_t e = cudaFuncSetAttribute(k_spread_tiles<T2, TAPS, P>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                           (int)smem);
-      if (e != cudaSuccess) return e;
-      configured = true;
-    }
-    int per_sm = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_spread_tiles<T2, TAPS, P>, BLOCK, smem);
-    int blocks = std::max(1, std::min(iw.nchunks, std::max(per_sm, 1) * sms));
-    k_spread_tiles<T2, TAPS, P><<<blocks, BLOCK, smem, s>>>(iw, reinterpret_cast<T2*>(a.g), g, *a.poly);
-    return cudaGetLastError();
-  }
   int blocks = std::max(1, std::min((iw.ngroups + 127) / 128, sms * 8));
   k_spread_groups<T2, TAPS, P><<<blocks, 128, 0, s>>>(iw, reinterpret_cast<T2*>(a.g), g, a.es_beta, *a.poly);
   return cudaGetLastError();
