@@ -6,6 +6,7 @@
 #include <chrono>
 #include <cmath>
 #include <cstdlib>
+#include <future>
 #include <math.h>
 #include <cstring>
 #include <map>
@@ -494,6 +495,73 @@ int fft_index(std::map<int, int>& lens, std::vector<FftLen>& tab, int L) {
   return idx;
 }
 
+// K3 tables of one wedge (plan time, host only): group the points by supercell, cut the groups into
+// chunks with bounded footprints and pad every chunk to BLOCK groups (see the K3 comment in
+// fio_kernels.cu).  uh: fine coordinates (u1, u2) per x, consumed.
+struct K3Tables {
+  std::vector<int> anchor, slot_x, box;
+  std::vector<double> off;   // c128 slot offsets
+  std::vector<float> offf;   // c64 slot offsets
+  long long cap = 0, real_groups = 0;
+  int nchunks = 0;
+};
+static K3Tables make_k3_tables(std::vector<double> uh, long long NN, int taps, bool c64, int n1f, int n2f) {
+  K3Tables T;
+#pragma omp parallel for schedule(static)
+  for (long long x = 0; x < NN; ++x) std::swap(uh[2 * x], uh[2 * x + 1]);  // (K3 row, column) = (u2, u1)
+  std::vector<int> anchor, slot_x;
+  std::vector<double> off;
+  group_points(uh.data(), NN, taps, group_p(c64), n2f, n1f, super_rows(c64), super_cols(c64), anchor, slot_x, off);
+  std::vector<double>().swap(uh);
+  const int gp = group_p(c64);
+  T.real_groups = (long long)(anchor.size() / 2);
+  const int blk = c64 ? kK3BlockC64 : kK3BlockC128;
+  T.cap = chunk_boxes(anchor, blk, k3_window_rows(taps, c64), k3_window_cols(taps, c64),
+                      c64 ? kK3TileCapC64 : kK3TileCapC128, T.box, c64 ? 8 : 16);
+  T.nchunks = (int)(T.box.size() / 6);
+  // pad every chunk to exactly blk groups, so that chunk c's groups are [c blk, (c+1) blk): K3 can then
+  // prefetch a chunk's per-thread data without reading its box first.  Padding groups repeat the
+  // chunk's first anchor (inside the box), have no points (slot -1) and alpha' = 0.
+  T.anchor.assign((size_t)T.nchunks * blk * 2, 0);
+  T.slot_x.assign((size_t)T.nchunks * blk * gp, -1);
+  T.off.assign((size_t)T.nchunks * blk * gp * 2, 0.5 * taps);
+  std::vector<int>& box = T.box;
+#pragma omp parallel for schedule(static)
+  for (int c = 0; c < T.nchunks; ++c) {
+    const long long g0 = box[6 * c], n = box[6 * c + 5];
+    for (long long i = 0; i < blk; ++i) {
+      const long long src = g0 + (i < n ? i : 0), dst = (long long)c * blk + i;
+      T.anchor[2 * dst] = anchor[2 * src];
+      T.anchor[2 * dst + 1] = anchor[2 * src + 1];
+      if (i < n)
+        for (int k = 0; k < gp; ++k) {
+          T.slot_x[dst * gp + k] = slot_x[src * gp + k];
+          T.off[2 * (dst * gp + k)] = off[2 * (src * gp + k)];
+          T.off[2 * (dst * gp + k) + 1] = off[2 * (src * gp + k) + 1];
+        }
+    }
+    box[6 * c] = c * blk;
+  }
+  if (c64) {
+    T.offf.resize(T.off.size());
+#pragma omp parallel for schedule(static)
+    for (long long i = 0; i < (long long)T.off.size(); ++i) T.offf[i] = (float)T.off[i];
+    std::vector<double>().swap(T.off);
+  }
+  return T;
+}
+
+static WedgeDev geometry_wedgedev(const WedgeGeom& g) {
+  WedgeDev w{};
+  w.l = g.l;
+  w.n1 = g.n1; w.n2 = g.n2; w.n1f = g.n1f; w.n2f = g.n2f;
+  std::memcpy(w.M, g.M, sizeof(w.M));
+  std::memcpy(w.Mi, g.Mi, sizeof(w.Mi));
+  w.xc1 = g.xc1; w.xc2 = g.xc2;
+  w.u1 = g.u1; w.u2 = g.u2;
+  return w;
+}
+
 // U = A(:, C) Y and beta = Z A(R, members) from saved factors: the same kernels and arguments as
 // separate_wedge, so a loaded plan reproduces the saved one bit for bit.
 fio_status expand_factors(fio_plan_s& P, const WedgeGeom& g, const WedgeFactors& F, cudaStream_t s, DevBuf& dU,
@@ -607,14 +675,39 @@ fio_status build_plan(fio_plan_s& P, const fio_phase* phase, const fio_amplitude
 
   // per owned wedge: separation, folding of alpha' and beta'
   const bool prof = std::getenv("FIO_PLAN_PROFILE") != nullptr;  // per-phase plan timing to stderr
-  double t_sep = 0, t_group = 0, t_fold = 0, t_gp = 0, t_d2h = 0;
+  double t_sep = 0, t_group = 0, t_fold = 0, t_gp = 0;
   auto now = [] { return std::chrono::steady_clock::now(); };
   auto secs = [](std::chrono::steady_clock::time_point a, std::chrono::steady_clock::time_point b) {
     return std::chrono::duration<double>(b - a).count();
   };
+  // The host-side K3 grouping of wedge i+1.. runs on worker threads while wedge i is separated and
+  // folded on the GPU (the grouping needs only the geometry and the fine coordinates).
+  const size_t nown = P.owned.size();
+  std::vector<std::future<K3Tables>> tables(nown);
+  size_t next_prefetch = 0;
+  auto prefetch = [&](size_t upto) -> fio_status {
+    for (; next_prefetch < std::min(upto, nown); ++next_prefetch) {
+      const WedgeGeom& gg = P.geom[P.owned[next_prefetch]];
+      const WedgeDev wg = geometry_wedgedev(gg);
+      DevBuf du;
+      FIO_CUDA(du.ensure(sizeof(double2) * NN));
+      FIO_CUDA(launch_fine_coords(P.op, wg, du.as<double2>(), s));
+      std::vector<double> uh(2 * NN);
+      FIO_CUDA(cudaMemcpyAsync(uh.data(), du.p, sizeof(double2) * NN, cudaMemcpyDeviceToHost, s));
+      FIO_CUDA(cudaStreamSynchronize(s));
+      tables[next_prefetch] = std::async(std::launch::async, make_k3_tables, std::move(uh), NN, P.taps, c64, gg.n1f,
+                                         gg.n2f);
+    }
+    return FIO_OK;
+  };
+  constexpr size_t kLookahead = 3;
   for (size_t wi = 0; wi < P.owned.size(); ++wi) {
     const WedgeGeom& g = P.geom[P.owned[wi]];
     Rng rng(P.opts.seed ^ (0x9E3779B97F4A7C15ull * (uint64_t)(g.l + 1)));
+    {
+      fio_status pst = prefetch(wi + kLookahead);
+      if (pst != FIO_OK) return pst;
+    }
     auto tw0 = now();
     DevBuf dU, dBeta;
     int q = 0, r = 0;
@@ -663,80 +756,41 @@ fio_status build_plan(fio_plan_s& P, const fio_phase* phase, const fio_amplitude
     iw.ncol = g.n1f;                 // K3 columns = j1 (haloed)
     iw.ncolp = g.n1f + 2 * kHalo;
     {
-      DevBuf du;
-      FIO_CUDA(du.ensure(sizeof(double2) * NN));
-      FIO_CUDA(launch_fine_coords(P.op, w, du.as<double2>(), s));
-      std::vector<double> uh(2 * NN);
-      FIO_CUDA(cudaMemcpyAsync(uh.data(), du.p, sizeof(double2) * NN, cudaMemcpyDeviceToHost, s));
-      FIO_CUDA(cudaStreamSynchronize(s));
       auto tg0 = now();
-#pragma omp parallel for schedule(static)
-      for (long long x = 0; x < NN; ++x) std::swap(uh[2 * x], uh[2 * x + 1]);  // (K3 row, column) = (u2, u1)
-      std::vector<int> anchor, slot_x;
-      std::vector<double> off;
-      group_points(uh.data(), NN, P.taps, group_p(c64), g.n2f, g.n1f, super_rows(c64), super_cols(c64), anchor, slot_x,
-                   off);
-      const int gp = group_p(c64);
-      auto tg1 = now();
-      t_gp += secs(tg0, tg1);
-      t_d2h += secs(tw1, tg0);
-      real_groups = (long long)(anchor.size() / 2);
-      std::vector<int> box;
-      const int blk = c64 ? kK3BlockC64 : kK3BlockC128;
-      const long long cap = chunk_boxes(anchor, blk, k3_window_rows(P.taps, c64), k3_window_cols(P.taps, c64),
-                                        c64 ? kK3TileCapC64 : kK3TileCapC128, box, c64 ? 8 : 16);
-      iw.nchunks = (int)(box.size() / 6);
-      {  // pad every chunk to exactly blk groups, so that chunk c's groups are [c blk, (c+1) blk): K3
-         // can then prefetch a chunk's per-thread data without reading its box first.  Padding groups
-         // repeat the chunk's first anchor (inside the box), have no points (slot -1) and alpha' = 0.
-        std::vector<int> pa((size_t)iw.nchunks * blk * 2), ps((size_t)iw.nchunks * blk * gp, -1);
-        std::vector<double> po((size_t)iw.nchunks * blk * gp * 2, 0.5 * P.taps);
-#pragma omp parallel for schedule(static)
-        for (int c = 0; c < iw.nchunks; ++c) {
-          const long long g0 = box[6 * c], n = box[6 * c + 5];
-          for (long long i = 0; i < blk; ++i) {
-            const long long src = g0 + (i < n ? i : 0), dst = (long long)c * blk + i;
-            pa[2 * dst] = anchor[2 * src];
-            pa[2 * dst + 1] = anchor[2 * src + 1];
-            if (i < n)
-              for (int k = 0; k < gp; ++k) {
-                ps[dst * gp + k] = slot_x[src * gp + k];
-                po[2 * (dst * gp + k)] = off[2 * (src * gp + k)];
-                po[2 * (dst * gp + k) + 1] = off[2 * (src * gp + k) + 1];
-              }
-          }
-          box[6 * c] = c * blk;
-        }
-        anchor.swap(pa);
-        slot_x.swap(ps);
-        off.swap(po);
+      K3Tables T;
+      try {
+        T = tables[wi].get();
+      } catch (const std::exception& ex) {
+        set_error(std::string("fio_plan: K3 grouping failed: ") + ex.what());
+        return FIO_ENOMEM;
       }
-      iw.ngroups = (int)(anchor.size() / 2);
+      t_gp += secs(tg0, now());
+      const int blk = c64 ? kK3BlockC64 : kK3BlockC128;
+      real_groups = T.real_groups;
+      iw.nchunks = T.nchunks;
+      iw.ngroups = (int)(T.anchor.size() / 2);
       int* d_anchor = nullptr;
       int* d_slot = nullptr;
-      FIO_CUDA(P.upload(&d_anchor, anchor.data(), anchor.size()));
-      FIO_CUDA(P.upload(&d_slot, slot_x.data(), slot_x.size()));
+      FIO_CUDA(P.upload(&d_anchor, T.anchor.data(), T.anchor.size()));
+      FIO_CUDA(P.upload(&d_slot, T.slot_x.data(), T.slot_x.size()));
       if (c64) {
-        std::vector<float> offf(off.size());
-#pragma omp parallel for schedule(static)
-        for (long long i = 0; i < (long long)off.size(); ++i) offf[i] = (float)off[i];
         float* d_off = nullptr;
-        FIO_CUDA(P.upload(&d_off, offf.data(), offf.size()));
+        FIO_CUDA(P.upload(&d_off, T.offf.data(), T.offf.size()));
         iw.slot_off = d_off;
       } else {
         double* d_off = nullptr;
-        FIO_CUDA(P.upload(&d_off, off.data(), off.size()));
+        FIO_CUDA(P.upload(&d_off, T.off.data(), T.off.size()));
         iw.slot_off = d_off;
       }
       iw.anchor = d_anchor;
       iw.slot_x = d_slot;
       P.chunk_threads += (long long)iw.nchunks * blk;
-      iw.tile_cap = (int)cap;
+      iw.tile_cap = (int)T.cap;
       int* d_box = nullptr;
-      FIO_CUDA(P.upload(&d_box, box.data(), std::max<size_t>(box.size(), 4)));
+      FIO_CUDA(P.upload(&d_box, T.box.data(), std::max<size_t>(T.box.size(), 4)));
       iw.box = d_box;
-      P.max_tile_cap = std::max(P.max_tile_cap, cap);
-      P.meta_bytes += anchor.size() * 4 + slot_x.size() * 4 + off.size() * (c64 ? 4 : 8);
+      P.max_tile_cap = std::max(P.max_tile_cap, T.cap);
+      P.meta_bytes += T.anchor.size() * 4 + T.slot_x.size() * 4 + (c64 ? T.offf.size() * 4 : T.off.size() * 8);
     }
     auto tw2 = now();
     t_group += secs(tw1, tw2);
@@ -813,9 +867,9 @@ fio_status build_plan(fio_plan_s& P, const fio_phase* phase, const fio_amplitude
 
   if (prof)
     std::fprintf(stderr,
-                 "fio plan: separation %.2f s, K3 grouping %.2f s (coords+D2H %.2f, group_points %.2f), alpha'/beta' "
-                 "folding %.2f s (%zu wedges)\n",
-                 t_sep, t_group, t_d2h, t_gp, t_fold, P.owned.size());
+                 "fio plan: separation %.2f s, K3 tables %.2f s (of which waiting for the grouping threads %.2f), "
+                 "alpha'/beta' folding %.2f s (%zu wedges)\n",
+                 t_sep, t_group, t_gp, t_fold, P.owned.size());
   if (P.opts.skeleton) {  // one alpha' scratch shared by the wedges (rebuilt per wedge per apply)
     void* scratch = nullptr;
     FIO_CUDA(P.alloc(&scratch, cs * std::max<size_t>(P.scratch_elems, 1)));
