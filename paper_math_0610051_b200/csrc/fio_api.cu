@@ -901,6 +901,10 @@ fio_status build_plan(fio_plan_s& P, const fio_phase* phase, const fio_amplitude
   // workspace offsets and FFT job lists
   size_t kSmemBudget = kSmemBudgetDefault;
   if (const char* e = std::getenv("FIO_FFT_SMEM_KB")) kSmemBudget = (size_t)std::max(8, std::atoi(e)) * 1024;
+  // K2 (column pass) budget: measured at N=1024, complex128 K2 48/64/80/96 KB = 1.49/1.36/1.59/1.53 ms,
+  // complex64 0.45/0.49/0.60/0.59 ms
+  size_t kSmemBudgetCol = std::getenv("FIO_FFT_SMEM_KB") ? kSmemBudget : (c64 ? 48 : 64) * 1024;
+  if (const char* e = std::getenv("FIO_FFT_SMEM_KB_COL")) kSmemBudgetCol = (size_t)std::max(8, std::atoi(e)) * 1024;
   int max_rows = 32, max_cols = 16;
   if (const char* e = std::getenv("FIO_FFT_MAXSEQ")) max_rows = max_cols = std::min(32, std::max(1, std::atoi(e)));
   long long p1_off = 0, g_off = 0;
@@ -915,7 +919,7 @@ fio_status build_plan(fio_plan_s& P, const fio_phase* phase, const fio_amplitude
     g_off += (long long)w.q * w.n2f * (w.n1f + 2 * kHalo);
     size_t sr = fft_seq_bytes(w.n2f, c64), sc = fft_seq_bytes(w.n1f, c64);
     int rows = (int)std::max<size_t>(1, std::min<size_t>(max_rows, kSmemBudget / sr));
-    int cols = (int)std::max<size_t>(1, std::min<size_t>(max_cols, kSmemBudget / sc));
+    int cols = (int)std::max<size_t>(1, std::min<size_t>(max_cols, kSmemBudgetCol / sc));
     cols = std::min(cols, w.n2f);
     rows = std::min(rows, w.n1);
     P.row_job_off.push_back((int)jr.size());
