@@ -537,6 +537,12 @@ __device__ __forceinline__ FastDiv make_fastdiv_dev(unsigned d) {
 template <typename T2> struct PadShift;
 template <> struct PadShift<float2> { static constexpr int value = 4; };
 template <> struct PadShift<double2> { static constexpr int value = 3; };
+#ifndef FIO_K1_THREADS
+#define FIO_K1_THREADS 256
+#endif
+#ifndef FIO_K2_THREADS
+#define FIO_K2_THREADS 256
+#endif
 #ifndef FIO_FFT_TWPOW
 #define FIO_FFT_TWPOW 1  // twiddles w^r = (w^1)^r: c128 K1+K2 2.68 -> 2.37 ms (N=1024)
 #endif
@@ -818,7 +824,7 @@ __device__ __forceinline__ int imod(int a, int n) {
 // placed at fine index k'_2 mod n2f, then H = FFT_{+}(h) along axis 2.  The result is
 // written TRANSPOSED, p1[t][j2][i1] (row length n1), so that K2 reads contiguous columns.
 template <typename T2>
-__global__ void __launch_bounds__(256) k_rowpass(int N, const WedgeDev* __restrict__ wedges,
+__global__ void __launch_bounds__(FIO_K1_THREADS) k_rowpass(int N, const WedgeDev* __restrict__ wedges,
                                                  const FftJob* __restrict__ jobs, const FftLen* __restrict__ ffts,
                                                  const T2* __restrict__ tw, const T2* const* __restrict__ betas,
                                                  const T2* __restrict__ fhat, T2* __restrict__ p1) {
@@ -867,7 +873,7 @@ __global__ void __launch_bounds__(256) k_rowpass(int N, const WedgeDev* __restri
 // its contiguous axis: G_lt[j2][kHalo + j1] (row length n1f + 2 kHalo), the layout K3
 // reads (K3's rows are j2, its columns j1).
 template <typename T2>
-__global__ void __launch_bounds__(256) k_colpass(const WedgeDev* __restrict__ wedges, const FftJob* __restrict__ jobs,
+__global__ void __launch_bounds__(FIO_K2_THREADS) k_colpass(const WedgeDev* __restrict__ wedges, const FftJob* __restrict__ jobs,
                                                  const FftLen* __restrict__ ffts, const T2* __restrict__ tw,
                                                  const T2* __restrict__ p1, T2* __restrict__ g) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -1991,12 +1997,12 @@ static cudaError_t enqueue_apply_t(const ApplyArgs* args, int nrhs, const T2* f0
         while (w1 < a.nw && wedge_batch[w1] == bt) ++w1;
         const int r0 = a.row_job_off[w0], r1 = a.row_job_off[w1], c0 = a.col_job_off[w0], c1 = a.col_job_off[w1];
         if (r1 > r0) {
-          k_rowpass<T2><<<r1 - r0, 256, a.smem_row, a.fft_stream>>>(a.N, a.wedges, a.jobs_row + r0, a.ffts, tw, betas,
+          k_rowpass<T2><<<r1 - r0, FIO_K1_THREADS, a.smem_row, a.fft_stream>>>(a.N, a.wedges, a.jobs_row + r0, a.ffts, tw, betas,
                                                                     fhat, reinterpret_cast<T2*>(a.p1));
           ++n;
         }
         if (c1 > c0) {
-          k_colpass<T2><<<c1 - c0, 256, a.smem_col, a.fft_stream>>>(a.wedges, a.jobs_col + c0, a.ffts, tw,
+          k_colpass<T2><<<c1 - c0, FIO_K2_THREADS, a.smem_col, a.fft_stream>>>(a.wedges, a.jobs_col + c0, a.ffts, tw,
                                                                     reinterpret_cast<const T2*>(a.p1),
                                                                     reinterpret_cast<T2*>(a.g));
           ++n;
@@ -2009,12 +2015,12 @@ static cudaError_t enqueue_apply_t(const ApplyArgs* args, int nrhs, const T2* f0
       mark();
     } else if (a.nw > 0) {
       const T2* const* betas = reinterpret_cast<const T2* const*>(a.beta);
-      k_rowpass<T2><<<a.njobs_row, 256, a.smem_row, s>>>(a.N, a.wedges, a.jobs_row, a.ffts, tw, betas, fhat,
+      k_rowpass<T2><<<a.njobs_row, FIO_K1_THREADS, a.smem_row, s>>>(a.N, a.wedges, a.jobs_row, a.ffts, tw, betas, fhat,
                                                          reinterpret_cast<T2*>(a.p1));
       if ((e = cudaGetLastError()) != cudaSuccess) return e;
       ++n;
       mark();
-      k_colpass<T2><<<a.njobs_col, 256, a.smem_col, s>>>(a.wedges, a.jobs_col, a.ffts, tw,
+      k_colpass<T2><<<a.njobs_col, FIO_K2_THREADS, a.smem_col, s>>>(a.wedges, a.jobs_col, a.ffts, tw,
                                                          reinterpret_cast<const T2*>(a.p1), reinterpret_cast<T2*>(a.g));
       if ((e = cudaGetLastError()) != cudaSuccess) return e;
       ++n;
