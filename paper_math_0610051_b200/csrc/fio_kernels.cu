@@ -1855,7 +1855,15 @@ static cudaError_t enqueue_adjoint_t(const ApplyArgs& a, const T2* g, T2* out, c
   if ((e = cudaMemsetAsync(fhat, 0, sizeof(T2) * NN, s)) != cudaSuccess) return e;
   if (a.nw > 0) {
     if ((e = cudaMemsetAsync(a.g, 0, sizeof(T2) * a.fine_elems, s)) != cudaSuccess) return e;
+    // the wedges' spreads write disjoint G*_l: they alternate between the caller's stream and the
+    // plan's side stream (not in skeleton mode, whose alpha' scratch is shared)
+    const bool two = a.skel == nullptr && a.side[0] != nullptr && a.nw >= 2 && a.k3_streams >= 2;
+    if (two) {
+      if ((e = cudaEventRecord(a.fork, s)) != cudaSuccess) return e;
+      if ((e = cudaStreamWaitEvent(a.side[0], a.fork, 0)) != cudaSuccess) return e;
+    }
     for (int wi = 0; wi < a.nw; ++wi) {
+      cudaStream_t sw = (two && (wi & 1)) ? a.side[0] : s;
       if (a.skel) {
         const InterpWedge& iw = a.iw[wi];
         e = launch_rebuild_alpha(a.op, a.wd_host[wi], a.skel[wi], iw.q, iw.slot_x,
@@ -1865,7 +1873,7 @@ static cudaError_t enqueue_adjoint_t(const ApplyArgs& a, const T2* g, T2* out, c
       }
 #define FIO_SPREAD_CASE(TP)                                   \
   case TP:                                                    \
-    e = launch_spread_tp<T2, TP, GroupP<T2>::value>(a, wi, g, s); \
+    e = launch_spread_tp<T2, TP, GroupP<T2>::value>(a, wi, g, sw); \
     break;
       switch (a.taps) {
         FIO_SPREAD_CASE(3)
@@ -1881,6 +1889,10 @@ static cudaError_t enqueue_adjoint_t(const ApplyArgs& a, const T2* g, T2* out, c
 #undef FIO_SPREAD_CASE
       if (e != cudaSuccess) return e;
       ++n;
+    }
+    if (two) {
+      if ((e = cudaEventRecord(a.join[0], a.side[0])) != cudaSuccess) return e;
+      if ((e = cudaStreamWaitEvent(s, a.join[0], 0)) != cudaSuccess) return e;
     }
     k_colpass_adj<T2><<<a.njobs_col, 256, a.smem_col, s>>>(a.wedges, a.jobs_col, a.ffts, tw,
                                                            reinterpret_cast<const T2*>(a.g),
