@@ -870,11 +870,12 @@ fio_status build_plan(fio_plan_s& P, const fio_phase* phase, const fio_amplitude
                  "fio plan: separation %.2f s, K3 tables %.2f s (of which waiting for the grouping threads %.2f), "
                  "alpha'/beta' folding %.2f s (%zu wedges)\n",
                  t_sep, t_group, t_gp, t_fold, P.owned.size());
-  if (P.opts.skeleton) {  // one alpha' scratch shared by the wedges (rebuilt per wedge per apply)
-    void* scratch = nullptr;
-    FIO_CUDA(P.alloc(&scratch, cs * std::max<size_t>(P.scratch_elems, 1)));
-    for (auto& iw : P.iw) iw.alpha = scratch;
-    P.alpha_bytes = cs * P.scratch_elems;
+  if (P.opts.skeleton) {  // two alpha' scratches, alternating over the wedges (rebuilt per wedge per apply):
+                          // wedge l's rebuild and K3 run on stream l mod 2, so they overlap the other's
+    void* scratch[2] = {nullptr, nullptr};
+    for (auto& sp : scratch) FIO_CUDA(P.alloc(&sp, cs * std::max<size_t>(P.scratch_elems, 1)));
+    for (size_t wi = 0; wi < P.iw.size(); ++wi) P.iw[wi].alpha = scratch[wi & 1];
+    P.alpha_bytes = 2 * cs * P.scratch_elems;
   }
 
   // twiddle tables

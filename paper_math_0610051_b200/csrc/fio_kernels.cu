@@ -1501,9 +1501,9 @@ static cudaError_t launch_interp(const ApplyArgs* args, int nrhs, T2* Lf0, cudaS
   }
   // K3 of wedge wi runs on stream wi % ns with its own accumulator (stream 0: the caller's, into
   // Lf), so one wedge's tail and prologue overlap other wedges' work; the partial sums are added at
-  // the end in a fixed order (deterministic).  Skeleton mode shares one alpha' scratch between
-  // wedges and stays on one stream.
-  const int ns = a.skel == nullptr ? std::max(1, std::min(a.k3_streams, a.nw)) : 1;
+  // the end in a fixed order (deterministic).  Skeleton mode: two alpha' scratches alternate over the
+  // wedges (fio_api.cu), so at most 2 streams, each rebuilding its wedge's alpha' before its K3.
+  const int ns = std::max(1, std::min(a.skel == nullptr ? a.k3_streams : std::min(a.k3_streams, 2), a.nw));
   if (ns > 1) {
     cudaError_t e = cudaEventRecord(a.fork, s);
     for (int j = 0; j + 1 < ns && e == cudaSuccess; ++j) e = cudaStreamWaitEvent(a.side[j], a.fork, 0);
@@ -1520,7 +1520,7 @@ static cudaError_t launch_interp(const ApplyArgs* args, int nrhs, T2* Lf0, cudaS
       if ((e = cudaStreamWaitEvent(sw, a.ev_batch[waited[sj]], 0)) != cudaSuccess) return e;
     }
     const int dc = (wi == 0 && a.add_dc) ? 1 : 0;
-    if (a.skel) {  // skeleton storage: regenerate this wedge's alpha' into the shared scratch
+    if (a.skel) {  // skeleton storage: regenerate this wedge's alpha' into its stream's scratch
       const InterpWedge& iw = a.iw[wi];
       e = launch_rebuild_alpha(a.op, a.wd_host[wi], a.skel[wi], iw.q, iw.slot_x,
                                (long long)iw.ngroups * GroupP<T2>::value, const_cast<void*>(iw.alpha),
@@ -1857,7 +1857,7 @@ static cudaError_t enqueue_adjoint_t(const ApplyArgs& a, const T2* g, T2* out, c
     if ((e = cudaMemsetAsync(a.g, 0, sizeof(T2) * a.fine_elems, s)) != cudaSuccess) return e;
     // the wedges' spreads write disjoint G*_l: they alternate between the caller's stream and the
     // plan's side stream (not in skeleton mode, whose alpha' scratch is shared)
-    const bool two = a.skel == nullptr && a.side[0] != nullptr && a.nw >= 2 && a.k3_streams >= 2;
+    const bool two = a.side[0] != nullptr && a.nw >= 2 && a.k3_streams >= 2;  // skeleton: 2 scratches
     if (two) {
       if ((e = cudaEventRecord(a.fork, s)) != cudaSuccess) return e;
       if ((e = cudaStreamWaitEvent(a.side[0], a.fork, 0)) != cudaSuccess) return e;
@@ -1867,7 +1867,7 @@ static cudaError_t enqueue_adjoint_t(const ApplyArgs& a, const T2* g, T2* out, c
       if (a.skel) {
         const InterpWedge& iw = a.iw[wi];
         e = launch_rebuild_alpha(a.op, a.wd_host[wi], a.skel[wi], iw.q, iw.slot_x,
-                                 (long long)iw.ngroups * GroupP<T2>::value, const_cast<void*>(iw.alpha), c64, s);
+                                 (long long)iw.ngroups * GroupP<T2>::value, const_cast<void*>(iw.alpha), c64, sw);
         if (e != cudaSuccess) return e;
         ++n;
       }
