@@ -531,12 +531,31 @@ __device__ __forceinline__ FastDiv make_fastdiv_dev(unsigned d) {
   return FastDiv{(unsigned)m, l, d};
 }
 
+// cp.async helpers (K2 input staging, K3 rings)
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+  unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
+  unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(s), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory"); }
+
 // Bank-conflict padding of the shared FFT buffers of the wedge passes: one empty slot after
 // every 128 bytes (8 complex128 / 16 complex64), so the stride-R writes of the early Stockham
 // stages hit distinct banks.  Sequence s, element e -> s * padded_len(L) + pad_idx(e).
 template <typename T2> struct PadShift;
 template <> struct PadShift<float2> { static constexpr int value = 4; };
 template <> struct PadShift<double2> { static constexpr int value = 3; };
+#ifndef FIO_K1_STAGE
+#define FIO_K1_STAGE 1  // measured: K1 c128 0.871 -> 0.813 ms, c64 0.297 -> 0.285 ms
+#endif
+#ifndef FIO_K2_STAGE
+#define FIO_K2_STAGE 1  // measured: K2 c128 1.355 -> 1.27 ms, c64 0.449 -> 0.427 ms
+#endif
 #ifndef FIO_K1_THREADS
 #define FIO_K1_THREADS 256
 #endif
@@ -836,6 +855,20 @@ __global__ void __launch_bounds__(FIO_K1_THREADS) k_rowpass(int N, const WedgeDe
   T2* a = reinterpret_cast<T2*>(smem_raw);
   T2* b = a + cnt * L;
   const T2* bet = betas[job.w] + ((long long)job.t * n1 + job.start) * n2;
+#if FIO_K1_STAGE
+  {  // the job's beta' rows are one contiguous block of cnt n2 elements: stage it in the first buffer
+    const int nel = cnt * n2;
+    if constexpr (sizeof(T2) == 16) {
+      for (int e = threadIdx.x; e < nel; e += blockDim.x) cp_async16(a + e, bet + e);
+    } else {
+      for (int e = threadIdx.x; e < nel; e += blockDim.x) cp_async8(a + e, bet + e);
+    }
+    cp_async_commit();
+    cp_async_wait<0>();
+    __syncthreads();
+    bet = a;
+  }
+#endif
   const int hi = n2 - n2 / 2;  // fine index pos = k'_2 mod L holds box column i2 = k'_2 + n2/2
   // The first Stockham stage reads h straight from beta' and fhat (no zero fill / placement pass).
   const int h2 = n2 / 2, lo2 = L - h2;
@@ -885,12 +918,31 @@ __global__ void __launch_bounds__(FIO_K2_THREADS) k_colpass(const WedgeDev* __re
   T2* b = a + C * L;
   const T2* src = p1 + w.p1_off + ((long long)job.t * w.n2f + c0) * n1;
   const int hi = n1 - n1 / 2;  // fine index pos = (i1 - n1/2) mod L
-  // First stage reads the row-pass output directly; last stage writes the haloed fine-grid row.
+#if FIO_K2_STAGE
+  // the job's input is one contiguous block of C n1 elements: copy it into the (not yet used) first
+  // ping-pong buffer with cp.async -- every thread keeps several copies in flight -- and let the
+  // first Stockham stage read it from shared memory
+  {
+    const int nel = C * n1;
+    if constexpr (sizeof(T2) == 16) {
+      for (int e = threadIdx.x; e < nel; e += blockDim.x) cp_async16(a + e, src + e);
+    } else {
+      for (int e = threadIdx.x; e < nel; e += blockDim.x) cp_async8(a + e, src + e);
+    }
+    cp_async_commit();
+    cp_async_wait<0>();
+    __syncthreads();
+  }
+  const T2* srcs = a;
+#else
+  const T2* srcs = src;
+#endif
+  // First stage reads the row-pass output; last stage writes the haloed fine-grid row.
   const int h1 = n1 / 2, lo1 = L - h1;
   auto load_p = [&](int c, int pos) -> T2 {
     const int i1 = pos < hi ? pos + h1 : pos - lo1;  // valid iff pos < hi or pos >= L - n1/2
     T2 out = mk<T2>(0, 0);
-    if (pos < hi || pos >= lo1) out = src[c * n1 + i1];
+    if (pos < hi || pos >= lo1) out = srcs[c * n1 + i1];
     return out;
   };
   const int rowp = L + 2 * kHalo;
@@ -1127,17 +1179,6 @@ template <> struct K3Cfg<double2> {
   static_assert(kK3TileCapC128 % kK3BlockC128 == 0, "tile cap must be a multiple of BLOCK (copy slots)");
 };
 
-__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
-  unsigned s = (unsigned)__cvta_generic_to_shared(smem);
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem) : "memory");
-}
-__device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
-  unsigned s = (unsigned)__cvta_generic_to_shared(smem);
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(s), "l"(gmem) : "memory");
-}
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
-template <int N>
-__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory"); }
 
 // Dynamic shared memory of K3: alpha' ring [S][BLOCK][P], phi1 [P*WINR][BLOCK], tile ring [S][tile_cap].
 template <typename T2, int TAPS, int P>
