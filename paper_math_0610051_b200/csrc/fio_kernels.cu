@@ -553,6 +553,9 @@ template <> struct PadShift<double2> { static constexpr int value = 3; };
 #ifndef FIO_K1_STAGE
 #define FIO_K1_STAGE 1  // measured: K1 c128 0.871 -> 0.813 ms, c64 0.297 -> 0.285 ms
 #endif
+#ifndef FIO_K1_GATHER
+#define FIO_K1_GATHER 0
+#endif
 #ifndef FIO_K2_STAGE
 #define FIO_K2_STAGE 1  // measured: K2 c128 1.355 -> 1.27 ms, c64 0.449 -> 0.427 ms
 #endif
@@ -875,17 +878,44 @@ __global__ void __launch_bounds__(FIO_K1_THREADS) k_rowpass(int N, const WedgeDe
   const int m0 = w.Mi[0], m1 = w.Mi[1], m2 = w.Mi[2], m3 = w.Mi[3];
   const int zb1 = job.start - n1 / 2 + w.xc1, zb2 = w.xc2 - h2;
   const bool pow2 = (N & (N - 1)) == 0;
+  auto fidx = [&](int r, int i2) {
+    const int z1 = zb1 + r, z2 = zb2 + i2;
+    const int xi1 = m0 * z1 + m1 * z2, xi2 = m2 * z1 + m3 * z2;
+    const int r1 = pow2 ? (xi1 & (N - 1)) : imod(xi1, N), r2 = pow2 ? (xi2 & (N - 1)) : imod(xi2, N);
+    return r1 * N + r2;
+  };
+#if FIO_K1_STAGE && FIO_K1_GATHER
+  // gather fhat for the member cells (beta' != 0) into the second half of the first buffer with
+  // cp.async, all in flight at once (the box is at most half of the fine row: 2 n2 <= L)
+  const T2* fg = nullptr;
+  if (2 * n2 <= L) {
+    T2* fs = a + cnt * n2;
+    const int nel = cnt * n2;
+    const FastDiv dn2 = make_fastdiv_dev((unsigned)n2);
+    for (int e = threadIdx.x; e < nel; e += blockDim.x) {
+      const T2 bv = bet[e];
+      if (bv.x != 0 || bv.y != 0) {
+        const int r = fdiv(e, dn2), i2 = e - r * n2;
+        if constexpr (sizeof(T2) == 16)
+          cp_async16(fs + e, fhat + fidx(r, i2));
+        else
+          cp_async8(fs + e, fhat + fidx(r, i2));
+      }
+    }
+    cp_async_commit();
+    cp_async_wait<0>();
+    __syncthreads();
+    fg = fs;
+  }
+#else
+  const T2* fg = nullptr;
+#endif
   auto load_h = [&](int r, int pos) -> T2 {
     const int i2 = pos < hi ? pos + h2 : pos - lo2;  // box column (valid iff pos < hi or pos >= L - n2/2)
     T2 out = mk<T2>(0, 0);
     if (pos < hi || pos >= lo2) {
       const T2 bv = bet[r * n2 + i2];
-      if (bv.x != 0 || bv.y != 0) {
-        const int z1 = zb1 + r, z2 = zb2 + i2;
-        const int xi1 = m0 * z1 + m1 * z2, xi2 = m2 * z1 + m3 * z2;
-        const int r1 = pow2 ? (xi1 & (N - 1)) : imod(xi1, N), r2 = pow2 ? (xi2 & (N - 1)) : imod(xi2, N);
-        out = cmul(bv, fhat[r1 * N + r2]);
-      }
+      if (bv.x != 0 || bv.y != 0) out = cmul(bv, fg ? fg[r * n2 + i2] : fhat[fidx(r, i2)]);
     }
     return out;
   };
