@@ -221,7 +221,8 @@ def test_adjoint_pairing_is_exact():
     assert abs(lhs - rhs) <= 1e-12 * np.linalg.norm(f) * np.linalg.norm(g) * N, (lhs, rhs)
 
 
-@pytest.mark.parametrize("N,W,dtype,tol", [(128, 32, "c128", 1e-12), (128, 32, "c64", 1e-5), (512, 0, "c128", 1e-12)])
+@pytest.mark.parametrize("N,W,dtype,tol", [(128, 32, "c128", 1e-12), (128, 32, "c64", 1e-5), (512, 0, "c128", 1e-12),
+                                           (1024, 0, "c128", 1e-12), (1024, 0, "c64", 1e-5)])
 def test_adjoint_pairing_dense_regions(N, W, dtype, tol):
     # the GRT map folds: at N >= 128 with W >= 32 whole warps of K3 groups share one anchor, the case
     # the segmented warp reduction of the spread must sum over all 32 lanes
