@@ -322,3 +322,87 @@ def test_bessel_dc_term_uses_clamped_radius():
     fh[0, 0] = 1.0
     s = oracle.fio(wl.bessel_grt_operator(N, +1), fhat=fh) + oracle.fio(wl.bessel_grt_operator(N, -1), fhat=fh)
     np.testing.assert_allclose(s, -circle_average_kernel(0.5) / N * np.ones((N, N)), rtol=1e-12)
+
+
+# ------------------------------------------------------------------ wedge-restricted mode
+def wedge_by_cross_products(W, xi1, xi2):
+    """The wedge of xi != 0 from the half-open arg interval [(2l-1) pi/W, (2l+1) pi/W),
+    decided by the signs of long-double cross products with the two boundary rays -- no atan2."""
+    pi = np.longdouble(np.pi)
+    A, B = np.longdouble(xi1), np.longdouble(xi2)
+    hits = [l for l in range(W)
+            if np.cos((2 * l - 1) * pi / W) * B - np.sin((2 * l - 1) * pi / W) * A >= 0
+            and np.cos((2 * l + 1) * pi / W) * B - np.sin((2 * l + 1) * pi / W) * A < 0]
+    assert len(hits) == 1, (xi1, xi2, hits)
+    return hits[0]
+
+
+@pytest.mark.parametrize("xi0", [(-13, 5), (7, -11), (-16, -16), (3, 0), (-1, 9), (0, -7)])
+def test_wedge_restricted_single_mode(xi0):
+    # fhat = delta_{xi0}: the partial operator of the wedge that owns xi0 reproduces the single-mode
+    # closed form (1/N) e^{2 pi i Phi(x, xi0)}; every other wedge gives exactly 0 (PAPER.md:236-241).
+    # catches: a selection that classifies the raw FFT index (k1, k2) instead of the signed frequency
+    # (xi1, xi2) -- every xi0 above has a negative component, whose raw index lies in another wedge --
+    # a swapped axis in the classification, or an off-by-one wedge
+    N, W = 32, 8
+    op = wl.grt_operator(N)
+    fh = np.zeros((N, N), complex)
+    fh[xi0[0] % N, xi0[1] % N] = 1.0
+    own = wedge_by_cross_products(W, *xi0)
+    raw = wedge_by_cross_products(W, xi0[0] % N if xi0[0] % N else 0, xi0[1] % N if xi0[1] % N else 0) \
+        if (xi0[0] % N, xi0[1] % N) != (0, 0) else None
+    x1, x2 = wl.grid(N)
+    phi = x1 * xi0[0] + x2 * xi0[1] + np.sqrt(op.c1 ** 2 * xi0[0] ** 2 + op.c2 ** 2 * xi0[1] ** 2)
+    mode = np.exp(2j * np.pi * phi) / N
+    for l in range(W):
+        out = oracle.fio(op, fhat=fh, wedges=[l], W=W, include_dc=False)
+        if l == own:
+            np.testing.assert_allclose(out, mode, atol=1e-13)
+        else:
+            assert np.array_equal(out, np.zeros_like(out)), (l, own)
+    if any(v < 0 for v in xi0):
+        assert raw != own  # the case is discriminating: the raw-index wedge differs
+    # the DC switch: xi = 0 is in no wedge and only include_dc brings it in
+    fdc = np.zeros((N, N), complex)
+    fdc[0, 0] = 2.0
+    assert np.array_equal(oracle.fio(op, fhat=fdc, wedges=list(range(W)), W=W, include_dc=False),
+                          np.zeros((N, N), complex))
+    np.testing.assert_allclose(oracle.fio(op, fhat=fdc, wedges=[], W=W, include_dc=True),
+                               np.full((N, N), 2.0 / N), atol=1e-15)
+
+
+# ------------------------------------------------------------------ adjoint branches (PAPER.md:1393-1396)
+def _pairing_ops(N):
+    x1, x2 = wl.grid(N)
+    grt = wl.grt_operator(N)
+    neg = wl.Operator(N, grt.c1, grt.c2, sign=-1, name="grt-")                       # rho_sign = -1
+    shifted = wl.Operator(N, grt.c1, grt.c2, b1=0.05 * np.sin(2 * np.pi * x2), b2=0.03 * np.cos(2 * np.pi * x1),
+                          sign=-1, name="grt-b")                                       # b != 0
+    wave = wl.wave_operator(N)
+    px = wave.px.copy()
+    px[1] = px[1] * np.exp(0.7j) * (1 + 0.3 * x2)                                     # complex spatial factor
+    pxi = wave.pxi.copy()
+    pxi[1] = pxi[1] * np.exp(-0.2j)                                                    # complex frequency factor
+    amp = wl.Operator(N, wave.c1, wave.c2, b1=shifted.b1, px=px, pxi=pxi, name="wave-amp-b")
+    return {"bessel+": wl.bessel_grt_operator(N, 1), "bessel-": wl.bessel_grt_operator(N, -1), "rho_sign-": neg,
+            "b": shifted, "amp+b": amp}
+
+
+@pytest.mark.parametrize("name", ["bessel+", "bessel-", "rho_sign-", "b", "amp+b"])
+def test_adjoint_pairing_all_branches(name):
+    # <L f, g>_X = <fhat, widehat(L* g)>_Omega for every branch of oracle_fio_adjoint_freq: the Bessel
+    # amplitude with both signs, rho_sign = -1, b(x) != 0 and a complex separable amplitude.  The forward
+    # branches are pinned by closed forms above (circle average, asymptotics, shifts, the wave amplitude),
+    # so this pins the adjoint's conj(a) and e^{-2 pi i Phi} in each branch.  Random complex fhat covers
+    # every frequency (DC included).
+    N = 12
+    op = _pairing_ops(N)[name]
+    f, g = crandn(N, N), crandn(N, N)
+    lhs = np.vdot(g, oracle.fio(op, f))
+    rhs = np.vdot(oracle.fio_adjoint_hat(op, g), oracle.dft2(f))
+    assert abs(lhs - rhs) < 1e-11 * abs(lhs), (lhs, rhs)
+    # and the adjoint is not trivially consistent: conjugating the amplitude's sign breaks the pairing
+    if name.startswith("bessel"):
+        other = wl.bessel_grt_operator(N, -op.sign)
+        bad = np.vdot(oracle.fio_adjoint_hat(other, g), oracle.dft2(f))
+        assert abs(lhs - bad) > 1e-3 * abs(lhs)
