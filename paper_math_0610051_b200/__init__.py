@@ -236,14 +236,31 @@ class Plan:
         _check(self._lib.fio_plan_save(self._h, os.fsencode(path)))
 
     # ------------------------------------------------------------ evaluation
+    def _dev_tensor(self, t, name, shape, writable=False):
+        """Check a device operand against the plan: CUDA, plan dtype, exact shape, the plan's device;
+        outputs must already be contiguous (the library writes through the raw pointer)."""
+        if not (t.is_cuda and t.dtype == self.torch_dtype and tuple(t.shape) == tuple(shape)
+                and t.device.index == self.device):
+            raise FioError(-1, f"{name} must be a {self.torch_dtype} tensor of shape {tuple(shape)} on "
+                               f"cuda:{self.device}")
+        if writable and not t.is_contiguous():
+            raise FioError(-1, f"{name} must be contiguous")
+        return t if writable else t.contiguous()
+
+    def _host_tensor(self, t, name):
+        """Check a host operand of apply_host: CPU, contiguous, plan dtype, exactly N*N elements."""
+        if t.is_cuda or t.dtype != self.torch_dtype or not t.is_contiguous() or t.numel() != self.N * self.N:
+            raise FioError(-1, f"{name} must be a contiguous CPU {self.torch_dtype} tensor of {self.N}x{self.N} "
+                               f"elements")
+        return t
+
     def apply(self, f, out=None, stream=None):
         """Lf for a device tensor f (N x N, complex64/complex128 matching the plan dtype)."""
         import torch
-        if not (f.is_cuda and f.dtype == self.torch_dtype and tuple(f.shape) == (self.N, self.N)):
-            raise FioError(-1, f"f must be a CUDA {self.torch_dtype} tensor of shape ({self.N}, {self.N})")
-        f = f.contiguous()
+        f = self._dev_tensor(f, "f", (self.N, self.N))
         if out is None:
             out = torch.empty_like(f)
+        out = self._dev_tensor(out, "out", (self.N, self.N), writable=True)
         if stream is None:
             stream = torch.cuda.current_stream(f.device)
         _check(self._lib.fio_apply(self._h, ctypes.c_void_p(f.data_ptr()), ctypes.c_void_p(out.data_ptr()),
@@ -253,11 +270,12 @@ class Plan:
     def apply_batch(self, f, out=None, stream=None):
         """L f_b for a device tensor f of shape (B, N, N) (plan dtype): one fio_apply_batch call."""
         import torch
-        if not (f.is_cuda and f.dtype == self.torch_dtype and f.dim() == 3 and tuple(f.shape[1:]) == (self.N, self.N)):
-            raise FioError(-1, f"f must be a CUDA {self.torch_dtype} tensor of shape (B, {self.N}, {self.N})")
-        f = f.contiguous()
+        if f.dim() != 3 or f.shape[0] < 1:
+            raise FioError(-1, f"f must have shape (B, {self.N}, {self.N})")
+        f = self._dev_tensor(f, "f", (f.shape[0], self.N, self.N))
         if out is None:
             out = torch.empty_like(f)
+        out = self._dev_tensor(out, "out", tuple(f.shape), writable=True)
         if stream is None:
             stream = torch.cuda.current_stream(f.device)
         _check(self._lib.fio_apply_batch(self._h, int(f.shape[0]), ctypes.c_void_p(f.data_ptr()),
@@ -267,11 +285,10 @@ class Plan:
     def apply_adjoint(self, g, out=None, stream=None):
         """L~* g for a device tensor g (N x N, plan dtype)."""
         import torch
-        if not (g.is_cuda and g.dtype == self.torch_dtype and tuple(g.shape) == (self.N, self.N)):
-            raise FioError(-1, f"g must be a CUDA {self.torch_dtype} tensor of shape ({self.N}, {self.N})")
-        g = g.contiguous()
+        g = self._dev_tensor(g, "g", (self.N, self.N))
         if out is None:
             out = torch.empty_like(g)
+        out = self._dev_tensor(out, "out", (self.N, self.N), writable=True)
         if stream is None:
             stream = torch.cuda.current_stream(g.device)
         _check(self._lib.fio_apply_adjoint(self._h, ctypes.c_void_p(g.data_ptr()), ctypes.c_void_p(out.data_ptr()),
@@ -281,6 +298,8 @@ class Plan:
     def apply_host(self, f_host, out_host, stream=None):
         """End-to-end apply from host (pinned) tensors; copies in both directions inside the call."""
         import torch
+        self._host_tensor(f_host, "f_host")
+        self._host_tensor(out_host, "out_host")
         if stream is None:
             stream = torch.cuda.current_stream(self.device)
         _check(self._lib.fio_apply_host(self._h, ctypes.c_void_p(f_host.data_ptr()),

@@ -62,6 +62,37 @@ struct DevBuf {
   }
 };
 
+// Selects `dev` for the lifetime of the guard and restores the caller's current device on every
+// return path (the library never leaves the calling thread on another device).
+struct DeviceGuard {
+  int prev = -1;
+  cudaError_t err = cudaSuccess;
+  explicit DeviceGuard(int dev) {
+    if (cudaGetDevice(&prev) != cudaSuccess) prev = -1;
+    if (dev >= 0 && dev != prev) err = cudaSetDevice(dev);
+  }
+  ~DeviceGuard() {
+    int cur = -1;
+    if (prev >= 0 && cudaGetDevice(&cur) == cudaSuccess && cur != prev) cudaSetDevice(prev);
+  }
+  DeviceGuard(const DeviceGuard&) = delete;
+  DeviceGuard& operator=(const DeviceGuard&) = delete;
+};
+
+#define FIO_GUARD(dev)                                                                      \
+  DeviceGuard guard_(dev);                                                                  \
+  if (guard_.err != cudaSuccess) {                                                          \
+    set_error(std::string("cudaSetDevice: ") + cudaGetErrorString(guard_.err));            \
+    return FIO_ECUDA;                                                                       \
+  }
+
+// [a, a + n) and [b, b + n) overlap
+static bool overlaps(const void* a, const void* b, size_t n) {
+  const char* x = static_cast<const char*>(a);
+  const char* y = static_cast<const char*>(b);
+  return x < y + n && y < x + n;
+}
+
 }  // namespace
 
 // The separation of one wedge in compact form (plan save/load): skeleton columns C, Y = V S^{-1}
@@ -74,7 +105,7 @@ struct WedgeFactors {
 };
 
 struct fio_plan_s {
-  int N = 0, W = 0, taps = 0, c64 = 0, device = 0;
+  int N = 0, W = 0, taps = 0, c64 = 0, device = 0, sms = 148;
   std::vector<WedgeFactors> factors;                 // per owned wedge, kept for fio_plan_save
   const std::vector<WedgeFactors>* load = nullptr;   // fio_plan_load: factors read from a file
   uint64_t input_hash = 0;                           // hash of the phase / amplitude arrays
@@ -129,6 +160,7 @@ struct fio_plan_s {
   std::vector<cudaEvent_t> prof_ev;  // (kStages + 1) per recorded apply
   int prof_cap = 0, prof_n = 0;
 
+  size_t elem_bytes() const { return c64 ? sizeof(float2) : sizeof(double2); }
   cudaError_t alloc(void** p, size_t bytes) {
     cudaError_t e = cudaMalloc(p, std::max<size_t>(bytes, 16));
     if (e == cudaSuccess) allocs.push_back(*p);
@@ -562,6 +594,38 @@ static WedgeDev geometry_wedgedev(const WedgeGeom& g) {
   return w;
 }
 
+// A loaded wedge's factors must index inside this plan: skeleton columns C are members of the
+// wedge (distinct), skeleton rows R are distinct output points in [0, N^2), and the factor shapes
+// match q.  Anything else is a corrupted or foreign file (FIO_EINVAL, never an out-of-bounds read).
+fio_status validate_factors(const WedgeFactors& F, const WedgeGeom& g, int N) {
+  const long long m = (long long)N * N;
+  const std::string w = " (wedge " + std::to_string(F.l) + ")";
+  if (F.q < 0 || F.q > (int)F.C.size() || F.q > (int)F.R.size() || (F.q > 0 && F.C.empty())) {
+    set_error("fio_plan_load: inconsistent rank q" + w);
+    return FIO_EINVAL;
+  }
+  std::vector<int> mem(g.members);
+  std::sort(mem.begin(), mem.end());
+  std::vector<int> c(F.C);
+  std::sort(c.begin(), c.end());
+  if (std::adjacent_find(c.begin(), c.end()) != c.end()) {
+    set_error("fio_plan_load: repeated skeleton column" + w);
+    return FIO_EINVAL;
+  }
+  for (int k : c)
+    if (!std::binary_search(mem.begin(), mem.end(), k)) {
+      set_error("fio_plan_load: skeleton column outside the wedge" + w);
+      return FIO_EINVAL;
+    }
+  std::vector<int> r(F.R);
+  std::sort(r.begin(), r.end());
+  if (std::adjacent_find(r.begin(), r.end()) != r.end() || (!r.empty() && (r.front() < 0 || r.back() >= m))) {
+    set_error("fio_plan_load: skeleton rows out of range or repeated" + w);
+    return FIO_EINVAL;
+  }
+  return FIO_OK;
+}
+
 // U = A(:, C) Y and beta = Z A(R, members) from saved factors: the same kernels and arguments as
 // separate_wedge, so a loaded plan reproduces the saved one bit for bit.
 fio_status expand_factors(fio_plan_s& P, const WedgeGeom& g, const WedgeFactors& F, cudaStream_t s, DevBuf& dU,
@@ -723,7 +787,8 @@ fio_status build_plan(fio_plan_s& P, const fio_phase* phase, const fio_amplitude
         return FIO_EINVAL;
       }
       F = *src;
-      st = expand_factors(P, g, F, s, dU, dBeta);
+      st = validate_factors(F, g, N);
+      if (st == FIO_OK) st = expand_factors(P, g, F, s, dU, dBeta);
     } else {
       F.l = g.l;
       st = separate_wedge(P, g, rng, s, dU, dBeta, F.q, F.r, F.err, F.C, F.Y, F.R, F.Z);
@@ -957,6 +1022,13 @@ fio_status build_plan(fio_plan_s& P, const fio_phase* phase, const fio_amplitude
   P.cols_per_cta_N = std::min(N, (int)std::max<size_t>(1, kSmemBudget / fft_seq_bytes(N, c64)));
   (void)kSmemBudgetDefault;
   FIO_CUDA(configure_kernels(kSmemMax));
+  if (!P.iw.empty()) FIO_CUDA(configure_interp(P.taps, c64, P.max_tile_cap));
+  if (P.opts.skeleton) {
+    size_t rb = 0;
+    for (size_t wi = 0; wi < P.skel.size(); ++wi) rb = std::max(rb, rebuild_smem_bytes(P.skel[wi].rc, P.wd[wi].q));
+    FIO_CUDA(configure_rebuild(c64, rb));
+  }
+  FIO_CUDA(cudaDeviceGetAttribute(&P.sms, cudaDevAttrMultiProcessorCount, P.device));
   if (!jr.empty()) FIO_CUDA(P.upload(&P.jobs_row, jr.data(), jr.size()));
   if (!jc.empty()) FIO_CUDA(P.upload(&P.jobs_col, jc.data(), jc.size()));
   if (!jra.empty()) FIO_CUDA(P.upload(&P.jobs_rowadj, jra.data(), jra.size()));
@@ -1046,6 +1118,7 @@ ApplyArgs make_args(const fio_plan_s& P) {
   a.masks = const_cast<const unsigned char* const*>(P.d_masks);
   a.fine_elems = P.fine_elems;
   a.cols_per_cta_N = P.cols_per_cta_N;
+  a.sms = P.sms;
   return a;
 }
 
@@ -1059,6 +1132,7 @@ struct SaveHeader {
   int32_t version, N, W, dtype, taps, rank, nranks, skeleton, n_owned;
   double eps, es_beta;
   uint64_t seed, input_hash;
+  uint64_t body_hash;  // FNV-1a over every byte after the header (version 2)
 };
 
 // FNV-1a over the operator inputs the plan depends on (phase and amplitude arrays, kinds).
@@ -1108,7 +1182,7 @@ fio_status fio_plan_save(fio_handle h, const char* path) {
   }
   SaveHeader hd{};
   std::memcpy(hd.magic, "FIOPLAN1", 8);
-  hd.version = 1;
+  hd.version = 2;
   hd.N = h->N;
   hd.W = h->W;
   hd.dtype = h->opts.dtype;
@@ -1121,16 +1195,20 @@ fio_status fio_plan_save(fio_handle h, const char* path) {
   hd.es_beta = h->es_beta;
   hd.seed = h->opts.seed;
   hd.input_hash = h->input_hash;
-  bool ok = std::fwrite(&hd, sizeof(hd), 1, fp) == 1;
+  std::string body;  // serialized factors; hashed into the header, then written after it
+  auto put = [&body](const void* p, size_t n) { body.append(static_cast<const char*>(p), n); };
   for (const WedgeFactors& F : h->factors) {
     const int32_t head[5] = {F.l, F.q, F.r, (int32_t)F.C.size(), (int32_t)F.R.size()};
-    ok = ok && std::fwrite(head, sizeof(head), 1, fp) == 1;
-    ok = ok && std::fwrite(&F.err, sizeof(double), 1, fp) == 1;
-    ok = ok && std::fwrite(F.C.data(), sizeof(int), F.C.size(), fp) == F.C.size();
-    ok = ok && std::fwrite(F.R.data(), sizeof(int), F.R.size(), fp) == F.R.size();
-    ok = ok && std::fwrite(F.Y.data(), sizeof(cplx), F.Y.size(), fp) == F.Y.size();
-    ok = ok && std::fwrite(F.Z.data(), sizeof(cplx), F.Z.size(), fp) == F.Z.size();
+    put(head, sizeof(head));
+    put(&F.err, sizeof(double));
+    put(F.C.data(), sizeof(int) * F.C.size());
+    put(F.R.data(), sizeof(int) * F.R.size());
+    put(F.Y.data(), sizeof(cplx) * F.Y.size());
+    put(F.Z.data(), sizeof(cplx) * F.Z.size());
   }
+  hd.body_hash = fnv1a(1469598103934665603ull, body.data(), body.size());
+  bool ok = std::fwrite(&hd, sizeof(hd), 1, fp) == 1;
+  ok = ok && std::fwrite(body.data(), 1, body.size(), fp) == body.size();
   ok = (std::fclose(fp) == 0) && ok;
   if (!ok) {
     set_error(std::string("fio_plan_save: write failed: ") + path);
@@ -1152,31 +1230,50 @@ fio_status fio_plan_load(fio_handle* out, const char* path, int N, const fio_pha
     return FIO_EINVAL;
   }
   SaveHeader hd{};
-  bool ok = std::fread(&hd, sizeof(hd), 1, fp) == 1 && std::memcmp(hd.magic, "FIOPLAN1", 8) == 0 && hd.version == 1 &&
+  bool ok = std::fread(&hd, sizeof(hd), 1, fp) == 1 && std::memcmp(hd.magic, "FIOPLAN1", 8) == 0 && hd.version == 2 &&
             hd.n_owned >= 0 && hd.n_owned <= 1 << 16;
+  std::string body;  // the rest of the file, checked against the header's hash before it is parsed
+  if (ok) {
+    std::vector<char> buf(1 << 16);
+    size_t got;
+    while ((got = std::fread(buf.data(), 1, buf.size(), fp)) > 0) body.append(buf.data(), got);
+    ok = fnv1a(1469598103934665603ull, body.data(), body.size()) == hd.body_hash;
+  }
+  std::fclose(fp);
+  size_t pos = 0;
+  auto take = [&](void* dst, size_t n) {
+    if (pos + n > body.size()) return false;
+    std::memcpy(dst, body.data() + pos, n);
+    pos += n;
+    return true;
+  };
   std::vector<WedgeFactors> fs;
+  std::vector<char> seen;
   for (int i = 0; ok && i < hd.n_owned; ++i) {
     WedgeFactors F;
     int32_t head[5];
-    ok = std::fread(head, sizeof(head), 1, fp) == 1 && std::fread(&F.err, sizeof(double), 1, fp) == 1;
+    ok = take(head, sizeof(head)) && take(&F.err, sizeof(double));
     if (!ok) break;
     F.l = head[0];
     F.q = head[1];
     F.r = head[2];
     const long long nc = head[3], nr = head[4];
-    ok = F.q >= 0 && nc >= 0 && nr >= 0 && nc <= (1 << 20) && nr <= (1 << 22) && F.q <= (1 << 16);
+    ok = F.q >= 0 && nc >= 0 && nr >= 0 && nc <= (1 << 20) && nr <= (1 << 22) && F.q <= (1 << 16) && F.l >= 0 &&
+         F.l < hd.W && F.l < (1 << 16);
+    if (!ok) break;
+    if ((int)seen.size() <= F.l) seen.resize(F.l + 1, 0);
+    ok = !seen[F.l];  // each wedge at most once
+    seen[F.l] = 1;
     if (!ok) break;
     F.C.resize(nc);
     F.R.resize(nr);
     F.Y.resize((size_t)nc * F.q);
     F.Z.resize((size_t)F.q * nr);
-    ok = std::fread(F.C.data(), sizeof(int), F.C.size(), fp) == F.C.size() &&
-         std::fread(F.R.data(), sizeof(int), F.R.size(), fp) == F.R.size() &&
-         std::fread(F.Y.data(), sizeof(cplx), F.Y.size(), fp) == F.Y.size() &&
-         std::fread(F.Z.data(), sizeof(cplx), F.Z.size(), fp) == F.Z.size();
+    ok = take(F.C.data(), sizeof(int) * F.C.size()) && take(F.R.data(), sizeof(int) * F.R.size()) &&
+         take(F.Y.data(), sizeof(cplx) * F.Y.size()) && take(F.Z.data(), sizeof(cplx) * F.Z.size());
     fs.push_back(std::move(F));
   }
-  std::fclose(fp);
+  ok = ok && pos == body.size();
   if (!ok) {
     set_error(std::string("fio_plan_load: not a valid plan file: ") + path);
     return FIO_EINVAL;
@@ -1240,13 +1337,7 @@ static fio_status plan_impl(fio_handle* out, int N, const fio_phase* phase, cons
   }
   if (o.r_init == 0) o.r_init = 32;
   if (o.r_max == 0) o.r_max = 512;
-  if (o.device >= 0) {
-    cudaError_t e = cudaSetDevice(o.device);
-    if (e != cudaSuccess) {
-      set_error(std::string("fio_plan: cudaSetDevice: ") + cudaGetErrorString(e));
-      return FIO_ECUDA;
-    }
-  }
+  FIO_GUARD(o.device)
   auto t0 = std::chrono::steady_clock::now();
   fio_plan_s* P = new (std::nothrow) fio_plan_s();
   if (!P) {
@@ -1292,13 +1383,11 @@ fio_status fio_apply(fio_handle h, const void* f_dev, void* Lf_dev, void* stream
     set_error("fio_apply: NULL argument");
     return FIO_EINVAL;
   }
-  if (f_dev == Lf_dev) {
-    set_error("fio_apply: f and Lf must not alias");
+  if (overlaps(f_dev, Lf_dev, h->elem_bytes() * (size_t)h->N * h->N)) {
+    set_error("fio_apply: f and Lf must not overlap");
     return FIO_EINVAL;
   }
-  int dev = -1;
-  cudaGetDevice(&dev);
-  if (dev != h->device) FIO_CUDA(cudaSetDevice(h->device));
+  FIO_GUARD(h->device)
   ApplyArgs a = make_args(*h);
   int launches = 0;
   cudaEvent_t* ev = nullptr;
@@ -1313,13 +1402,11 @@ fio_status fio_apply_batch(fio_handle h, int nrhs, const void* f_dev, void* Lf_d
     set_error("fio_apply_batch: bad arguments");
     return FIO_EINVAL;
   }
-  if (f_dev == Lf_dev) {
-    set_error("fio_apply_batch: f and Lf must not alias");
+  if (overlaps(f_dev, Lf_dev, h->elem_bytes() * (size_t)h->N * h->N * (size_t)nrhs)) {
+    set_error("fio_apply_batch: f and Lf must not overlap");
     return FIO_EINVAL;
   }
-  int dev = -1;
-  cudaGetDevice(&dev);
-  if (dev != h->device) FIO_CUDA(cudaSetDevice(h->device));
+  FIO_GUARD(h->device)
   const size_t cs = h->c64 ? sizeof(float2) : sizeof(double2);
   const size_t NN = (size_t)h->N * h->N;
   const size_t nacc = (size_t)std::max(0, h->k3_streams - 1);
@@ -1350,13 +1437,11 @@ fio_status fio_apply_adjoint(fio_handle h, const void* g_dev, void* out_dev, voi
     set_error("fio_apply_adjoint: NULL argument");
     return FIO_EINVAL;
   }
-  if (g_dev == out_dev) {
-    set_error("fio_apply_adjoint: g and out must not alias");
+  if (overlaps(g_dev, out_dev, h->elem_bytes() * (size_t)h->N * h->N)) {
+    set_error("fio_apply_adjoint: g and out must not overlap");
     return FIO_EINVAL;
   }
-  int dev = -1;
-  cudaGetDevice(&dev);
-  if (dev != h->device) FIO_CUDA(cudaSetDevice(h->device));
+  FIO_GUARD(h->device)
   ApplyArgs a = make_args(*h);
   int launches = 0;
   FIO_CUDA(enqueue_adjoint(a, h->c64, g_dev, out_dev, (cudaStream_t)stream, &launches));
@@ -1368,7 +1453,8 @@ fio_status fio_apply_host(fio_handle h, const void* f_host, void* Lf_host, void*
     set_error("fio_apply_host: NULL argument");
     return FIO_EINVAL;
   }
-  const size_t bytes = (size_t)h->N * h->N * (h->c64 ? sizeof(float2) : sizeof(double2));
+  const size_t bytes = (size_t)h->N * h->N * h->elem_bytes();
+  FIO_GUARD(h->device)  // the staging buffers live on the plan's device
   if (!h->e2e_in) {
     FIO_CUDA(h->alloc(&h->e2e_in, bytes));
     FIO_CUDA(h->alloc(&h->e2e_out, bytes));
@@ -1387,6 +1473,7 @@ fio_status fio_profile_begin(fio_handle h, int max_applies) {
     set_error("fio_profile_begin: bad arguments");
     return FIO_EINVAL;
   }
+  FIO_GUARD(h->device)
   h->free_events();
   h->prof_ev.resize((size_t)max_applies * (kStages + 1));
   for (auto& e : h->prof_ev) FIO_CUDA(cudaEventCreate(&e));
@@ -1400,6 +1487,7 @@ fio_status fio_profile_end(fio_handle h, double* stage_ms, int* n_applies) {
     set_error("fio_profile_end: NULL handle");
     return FIO_EINVAL;
   }
+  FIO_GUARD(h->device)
   std::vector<double> acc(kStages, 0.0);
   for (int i = 0; i < h->prof_n; ++i) {
     cudaEvent_t* ev = &h->prof_ev[(size_t)i * (kStages + 1)];
@@ -1419,6 +1507,7 @@ fio_status fio_profile_end(fio_handle h, double* stage_ms, int* n_applies) {
 
 fio_status fio_destroy(fio_handle h) {
   if (!h) return FIO_OK;
+  FIO_GUARD(h->device)  // streams, events and buffers are released on the plan's device
   delete h;
   return FIO_OK;
 }

@@ -19,10 +19,28 @@
 
 #include <algorithm>
 #include <cstdio>
+#include <map>
+#include <mutex>
 
 #include "fio_kernels.h"
 
 namespace fio {
+
+// cudaFuncSetAttribute(MaxDynamicSharedMemorySize) is per (kernel, device) and a later call with a
+// smaller value would lower it under an existing plan: raise-only, per device, under a mutex.
+static cudaError_t raise_smem_attr(const void* func, size_t smem) {
+  static std::mutex mu;
+  static std::map<std::pair<const void*, int>, size_t> done;
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  std::lock_guard<std::mutex> lk(mu);
+  size_t& cur = done[{func, dev}];
+  if (smem <= cur) return cudaSuccess;
+  e = cudaFuncSetAttribute(func, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e == cudaSuccess) cur = smem;
+  return e;
+}
 
 // ------------------------------------------------------------------ complex helpers
 __device__ __forceinline__ double2 cmul(double2 a, double2 b) {
@@ -335,17 +353,28 @@ __global__ void __launch_bounds__(128) k_rebuild_alpha(OperatorDev op, WedgeDev 
 template <typename T2, int QMAX>
 static cudaError_t launch_rebuild_q(const OperatorDev& op, const WedgeDev& w, const SkelWedge& sk, int q,
                                     const int* slot_x, long long nslots, T2* alpha, cudaStream_t s) {
-  const size_t smem = sizeof(double2) * (size_t)sk.rc * q + sizeof(int) * (size_t)sk.rc;
-  static size_t configured = 0;
-  if (smem > 48 * 1024 && smem > configured) {
-    cudaError_t e = cudaFuncSetAttribute(k_rebuild_alpha<T2, QMAX>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)smem);
-    if (e != cudaSuccess) return e;
-    configured = smem;
-  }
+  const size_t smem = rebuild_smem_bytes(sk.rc, q);  // attribute set at plan time (configure_rebuild)
   int blocks = (int)std::min<long long>((nslots + 127) / 128, 148LL * 8);
   k_rebuild_alpha<T2, QMAX><<<blocks, 128, smem, s>>>(op, w, sk, q, slot_x, nslots, alpha);
   return cudaGetLastError();
+}
+
+size_t rebuild_smem_bytes(int rc, int q) { return sizeof(double2) * (size_t)rc * q + sizeof(int) * (size_t)rc; }
+
+// Opt the rebuild kernels of this dtype into `smem` bytes of dynamic shared memory on the current
+// device (cudaFuncSetAttribute is per device: called by every plan for its own device).
+cudaError_t configure_rebuild(bool c64, size_t smem) {
+  if (smem <= 48 * 1024) return cudaSuccess;
+  cudaError_t e;
+#define FIO_RBA(QM)                                                                                             \
+  e = c64 ? raise_smem_attr((const void*)k_rebuild_alpha<float2, QM>, smem)                                   \
+          : raise_smem_attr((const void*)k_rebuild_alpha<double2, QM>, smem);                                   \
+  if (e != cudaSuccess) return e;
+  FIO_RBA(16)
+  FIO_RBA(32)
+  FIO_RBA(64)
+#undef FIO_RBA
+  return cudaSuccess;
 }
 
 cudaError_t launch_rebuild_alpha(const OperatorDev& op, const WedgeDev& w, const SkelWedge& sk, int q,
@@ -1532,28 +1561,41 @@ template <typename T2, int TAPS, int P>
 static cudaError_t launch_groups_tp(const ApplyArgs& a, int wi, T2* Lf, int first, int add_dc, cudaStream_t s) {
   constexpr int BLOCK = K3Cfg<T2>::BLOCK;
   const InterpWedge& iw = a.iw[wi];
+  // the plan opted this instance into its largest smem on its device (configure_interp)
   const size_t smem = k3_fixed_smem<T2, TAPS, P>() + sizeof(T2) * kK3Stages * (size_t)iw.tile_cap;
-  static int sms = 0;
-  static size_t configured = 0;
-  if (sms == 0) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  }
-  if (smem > configured) {
-    cudaError_t e = cudaFuncSetAttribute(k_interp_groups<T2, TAPS, P>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)smem);
-    if (e != cudaSuccess) return e;
-    configured = smem;
-  }
   int per_sm = 0;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_interp_groups<T2, TAPS, P>, BLOCK, smem);
   per_sm = std::max(per_sm, 1);
-  int blocks = std::max(1, std::min(iw.nchunks, per_sm * sms));
+  int blocks = std::max(1, std::min(iw.nchunks, per_sm * a.sms));
   k_interp_groups<T2, TAPS, P><<<blocks, BLOCK, smem, s>>>(iw, reinterpret_cast<const T2*>(a.g), a.a0,
                                                           reinterpret_cast<const T2*>(a.fhat), first,
                                                           add_dc, a.es_beta, *a.poly, Lf);
   return cudaGetLastError();
+}
+
+template <typename T2, int TAPS>
+static cudaError_t configure_interp_tp(long long tile_cap) {
+  constexpr int P = GroupP<T2>::value;
+  const size_t smem = k3_fixed_smem<T2, TAPS, P>() + sizeof(T2) * kK3Stages * (size_t)tile_cap;
+  return raise_smem_attr((const void*)k_interp_groups<T2, TAPS, P>, smem);
+}
+
+cudaError_t configure_interp(int taps, bool c64, long long max_tile_cap) {
+#define FIO_CFG_CASE(TP) \
+  case TP:               \
+    return c64 ? configure_interp_tp<float2, TP>(max_tile_cap) : configure_interp_tp<double2, TP>(max_tile_cap);
+  switch (taps) {
+    FIO_CFG_CASE(3)
+    FIO_CFG_CASE(4)
+    FIO_CFG_CASE(5)
+    FIO_CFG_CASE(6)
+    FIO_CFG_CASE(7)
+    FIO_CFG_CASE(8)
+    FIO_CFG_CASE(9)
+    FIO_CFG_CASE(10)
+    default: return cudaErrorInvalidValue;
+  }
+#undef FIO_CFG_CASE
 }
 
 template <typename T2>
@@ -1902,14 +1944,8 @@ __global__ void __launch_bounds__(1024) k_dc_adj(long long NN, const double2* __
 
 template <typename T2, int TAPS, int P>
 static cudaError_t launch_spread_tp(const ApplyArgs& a, int wi, const T2* g, cudaStream_t s) {
-  static int sms = 0;
-  if (sms == 0) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  }
   const InterpWedge& iw = a.iw[wi];
-  int blocks = std::max(1, std::min((iw.ngroups + 127) / 128, sms * 8));
+  int blocks = std::max(1, std::min((iw.ngroups + 127) / 128, a.sms * 8));
   k_spread_groups<T2, TAPS, P><<<blocks, 128, 0, s>>>(iw, reinterpret_cast<T2*>(a.g), g, a.es_beta, *a.poly);
   return cudaGetLastError();
 }
@@ -2008,7 +2044,7 @@ size_t fft_seq_bytes(int L, bool c64) {
 cudaError_t configure_kernels(size_t smem_bytes) {
   cudaError_t e;
 #define FIO_SMEM(K)                                                                          \
-  e = cudaFuncSetAttribute(K, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_bytes); \
+  e = raise_smem_attr((const void*)K, smem_bytes);                                           \
   if (e != cudaSuccess) return e;
   FIO_SMEM(k_fft_rows<double2>)
   FIO_SMEM(k_fft_rows<float2>)

@@ -61,6 +61,8 @@ struct SkelWedge {
 };
 
 // alpha'[t][s] = e^{2 pi i y(x_s).xi_c} / N * sum_c A(x_s, C_c) Y[c + t rc]  (slot order; 0 for padding)
+size_t rebuild_smem_bytes(int rc, int q);
+cudaError_t configure_rebuild(bool c64, size_t smem);  // per device, at plan time
 cudaError_t launch_rebuild_alpha(const OperatorDev& op, const WedgeDev& w, const SkelWedge& sk, int q,
                                  const int* slot_x, long long nslots, void* alpha, bool c64, cudaStream_t s);
 
@@ -110,6 +112,7 @@ struct ApplyArgs {
   const cudaEvent_t* ev_batch;     // kMaxPipeBatches
   const int* row_job_off;
   const int* col_job_off;
+  int sms;                  // multiprocessors of the plan's device (grid sizing)
   int rows_per_cta_N;       // K0 row pass
   int cols_per_cta_N;       // K0 column pass
 };
@@ -133,5 +136,8 @@ cudaError_t enqueue_adjoint(const ApplyArgs& a, bool c64, const void* g, void* o
 // Dynamic shared memory needed by the FFT passes for one sequence of length L.
 size_t fft_seq_bytes(int L, bool c64);
 cudaError_t configure_kernels(size_t smem_bytes);
+// Opt the K3 instance for (taps, dtype) into the dynamic shared memory of the plan's largest chunk
+// footprint, on the current device (per device: every plan configures its own device).
+cudaError_t configure_interp(int taps, bool c64, long long max_tile_cap);
 
 }  // namespace fio

@@ -484,3 +484,67 @@ def test_apply_captures_into_cuda_graph():
     g.replay()
     torch.cuda.synchronize()
     assert torch.equal(out, ref)
+
+
+# ------------------------------------------------------------------ argument checking of the binding and the file format
+def _fnv1a(b: bytes) -> int:
+    h = 1469598103934665603
+    for c in b:
+        h ^= c
+        h = (h * 1099511628211) & 0xFFFFFFFFFFFFFFFF
+    return h
+
+
+def test_plan_load_rejects_corrupted_body(tmp_path):
+    # a flipped byte fails the body checksum; a skeleton column rewritten to xi = 0 (in no wedge) with a
+    # recomputed checksum fails the index validation -- FIO_EINVAL, never an out-of-bounds device read
+    import struct
+    N = 64
+    op = wl.grt_operator(N)
+    p1 = make_plan(op)
+    path = str(tmp_path / "plan.fio")
+    p1.save(path)
+    raw = bytearray(open(path, "rb").read())
+    HDR = 88  # magic[8], 9 x int32, pad, eps, es_beta, seed, input_hash, body_hash
+    assert struct.unpack_from("<Q", raw, 80)[0] == _fnv1a(bytes(raw[HDR:]))
+    bad = bytearray(raw)
+    bad[HDR + 40] ^= 0x5A
+    open(path, "wb").write(bad)
+    with pytest.raises(fio.FioError):
+        make_plan(op, load=path)
+    bad = bytearray(raw)
+    l, q, r, nc, nr = struct.unpack_from("<5i", bad, HDR)
+    assert nc > 0
+    struct.pack_into("<i", bad, HDR + 20 + 8, 0)  # first skeleton column -> flat index 0 (xi = 0)
+    struct.pack_into("<Q", bad, 80, _fnv1a(bytes(bad[HDR:])))
+    open(path, "wb").write(bad)
+    with pytest.raises(fio.FioError):
+        make_plan(op, load=path)
+    open(path, "wb").write(raw)  # the untouched file still loads
+    make_plan(op, load=path)
+
+
+def test_binding_rejects_bad_operands():
+    N = 64
+    op = wl.grt_operator(N)
+    plan = make_plan(op)
+    f = torch.zeros((N, N), dtype=torch.complex128, device=DEV)
+    with pytest.raises(fio.FioError):
+        plan.apply(f, out=torch.empty((N, N), dtype=torch.complex64, device=DEV))      # out dtype
+    with pytest.raises(fio.FioError):
+        plan.apply(f, out=torch.empty((N, N // 2), dtype=torch.complex128, device=DEV))  # out shape
+    with pytest.raises(fio.FioError):
+        plan.apply(f, out=torch.empty((N, N), dtype=torch.complex128, device=DEV).t())   # non-contiguous out
+    with pytest.raises(fio.FioError):
+        plan.apply_adjoint(f, out=torch.empty((N, N), dtype=torch.complex64, device=DEV))
+    with pytest.raises(fio.FioError):
+        plan.apply_host(torch.zeros((N, N), dtype=torch.complex64), torch.zeros((N, N), dtype=torch.complex128))
+    with pytest.raises(fio.FioError):
+        plan.apply_host(torch.zeros((N, N - 1), dtype=torch.complex128), torch.zeros((N, N), dtype=torch.complex128))
+    with pytest.raises(fio.FioError):  # overlapping f / out inside the library (one buffer, shifted view)
+        buf = torch.zeros((2 * N, N), dtype=torch.complex128, device=DEV)
+        plan.apply(buf[N // 2:N // 2 + N], out=buf[:N])
+    # the caller's current device is left as it was
+    before = torch.cuda.current_device()
+    plan.apply(f)
+    assert torch.cuda.current_device() == before
