@@ -198,19 +198,19 @@ def time_config(name, args, rank, world, local, group):
     op = wl.make_operator(cfg)
     f_np = wl.make_input(cfg)
     dev = torch.device("cuda", local)
+    # N > 1: the plan owns an NCCL communicator (id broadcast over `group`); fio_apply then ends with
+    # the library's reduce-scatter and returns this rank's (N/R) x N row slab
     plan = fio.Plan(N, op.c1, op.c2, op.b1, op.b2, op.px, op.pxi, eps=cfg["eps"], dtype=cfg["dtype"],
-                    device=local, rank=rank, nranks=world)
+                    device=local, rank=rank, nranks=world, group=group if world > 1 else None)
     info = plan.info
     tdt = torch.complex64 if c64 else torch.complex128
     f = torch.from_numpy(f_np).to(dev, tdt)
     stream = torch.cuda.current_stream(dev)
 
     def step():
-        if world > 1:
-            return plan.apply_sharded(f, group=group)
         return plan.apply(f, out=out)
 
-    out = torch.empty_like(f)
+    out = torch.empty((plan.out_rows, N), dtype=tdt, device=dev)
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize(dev)
@@ -256,22 +256,11 @@ def time_config(name, args, rank, world, local, group):
     # device-timed with CUDA events on the launching stream (max over ranks)
     hin = torch.from_numpy(f_np.astype(np.complex64 if c64 else np.complex128)).pin_memory()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    if world == 1:
-        hout = torch.empty_like(hin).pin_memory()
+    hout = torch.empty((plan.out_rows, N), dtype=hin.dtype).pin_memory()
 
-        def e2e_step():
-            plan.apply_host(hin, hout)          # fio_apply_host: H2D, apply, D2H, stream sync
-        d2h = hout.numel() * hout.element_size()
-    else:
-        fdev = torch.empty_like(f)
-        rows = N // world
-        hout = torch.empty((rows, N), dtype=hin.dtype).pin_memory()
-
-        def e2e_step():
-            fdev.copy_(hin, non_blocking=True)
-            slab = plan.apply_sharded(fdev, group=group)
-            hout.copy_(slab, non_blocking=True)
-        d2h = hout.numel() * hout.element_size()
+    def e2e_step():
+        plan.apply_host(hin, hout)  # fio_apply_host: H2D, apply (+ reduce-scatter), D2H of the slab, sync
+    d2h = hout.numel() * hout.element_size()
     for _ in range(2):
         e2e_step()
     torch.cuda.synchronize(dev)

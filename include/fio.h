@@ -52,7 +52,7 @@ typedef enum {
   FIO_EINVAL = -1,    /* bad argument (message says which) */
   FIO_ENOMEM = -2,    /* device or host allocation failed */
   FIO_ECUDA = -3,     /* CUDA runtime error (launch or sync) */
-  FIO_ENCCL = -4,     /* reserved: collective failure */
+  FIO_ENCCL = -4,     /* NCCL failure (libnccl.so.2 missing, communicator setup or reduce-scatter) */
   FIO_ENOTHOMOG = -5, /* reserved: phase failed the degree-1 homogeneity check */
   FIO_EINTERNAL = -6  /* internal invariant violated (a bug) */
 } fio_status;
@@ -109,7 +109,18 @@ typedef struct {
                          keep only the skeleton columns C and V S^{-1} per wedge and rebuild
                          alpha' = A_[C] V S^{-1} (with the center phase) before each wedge's
                          interpolation; O(r q) storage per wedge, extra compute per apply */
+  const void* nccl_id; /* NULL.  Else FIO_NCCL_ID_BYTES bytes of an NCCL unique id
+                         (fio_nccl_unique_id on one rank, broadcast by the caller); fio_plan then
+                         creates this rank's communicator (a collective call: every rank must call
+                         fio_plan with the same id) and fio_apply ends with the cross-GPU sum.
+                         NULL with nranks > 1: fio_apply returns this rank's N x N partial sum. */
 } fio_opts;
+
+#define FIO_NCCL_ID_BYTES 128
+
+/* Write a fresh NCCL unique id (FIO_NCCL_ID_BYTES bytes) to id_out (host).  Host-only; loads
+ * libnccl.so.2 at run time (FIO_ENCCL if it cannot). */
+fio_status fio_nccl_unique_id(void* id_out);
 
 void fio_default_opts(fio_opts* opts);
 
@@ -123,25 +134,34 @@ fio_status fio_plan(fio_handle* out, int N, const fio_phase* phase, const fio_am
                     double eps, const fio_opts* opts);
 
 /* Evaluate L f.  f_dev: device N x N complex of the plan dtype (caller-owned,
- * read-only).  Lf_dev: device N x N complex of the plan dtype (caller-owned,
- * fully overwritten; must not alias f_dev).  With nranks > 1, Lf_dev receives
- * this rank's partial sum over its own wedges (the DC term is added on rank
- * 0 only); the caller sums the partials across ranks (reduce-scatter).
+ * read-only).  Lf_dev: device complex of the plan dtype (caller-owned, fully
+ * overwritten; must not overlap f_dev):
+ *  - nranks == 1: the N x N result;
+ *  - nranks > 1 with a communicator (opts.nccl_id): every rank passes the full
+ *    f and receives its row slab of L f, rows [rank N/R, (rank+1) N/R) -- an
+ *    (N/R) x N array -- after the wedge partials of all ranks are summed by an
+ *    NCCL reduce-scatter on `stream` (L = sum_l L_l; the
+ *    collective: every rank must call fio_apply);
+ *  - nranks > 1 without a communicator: this rank's N x N partial sum over its
+ *    own wedges (the DC term on rank 0 only), for the caller to sum.
  * stream: a cudaStream_t (NULL = legacy default stream).  Asynchronous on
- * `stream`; one apply in flight per handle (the workspace is per handle). */
+ * `stream`; one apply in flight per handle (the workspace is per handle).
+ * Errors: FIO_EINVAL (arguments), FIO_ECUDA (launch), FIO_ENCCL (collective). */
 fio_status fio_apply(fio_handle h, const void* f_dev, void* Lf_dev, void* stream);
 
 /* The adjoint: out = L~* g, the exact conjugate transpose of the fast
  * operator fio_apply evaluates (so <L~f, g> = <f, L~* g> to rounding), approximating
  * (L* g)(x) = (1/N) sum_xi e^{2 pi i x.xi} (1/N) sum_y conj(a(y,xi)) e^{-2 pi i Phi(y,xi)} g(y).
- * g_dev, out_dev: device N x N complex of the plan dtype (no aliasing).  With nranks > 1 the
- * result is this rank's partial (its wedges; the DC term on rank 0).  Asynchronous on stream;
+ * g_dev, out_dev: device N x N complex of the plan dtype (no overlap).  With nranks > 1 the
+ * result is this rank's row slab (with a communicator) or its partial over its wedges (without;
+ * the DC term on rank 0), exactly as for fio_apply.  Asynchronous on stream;
  * shares the handle's workspace with fio_apply (one call in flight per handle).  The type-1
  * spreading step accumulates with atomics: the last bits may vary between runs. */
 fio_status fio_apply_adjoint(fio_handle h, const void* g_dev, void* out_dev, void* stream);
 
-/* Multi-RHS apply (NEXT-2): Lf_b = L f_b for b < nrhs; f_dev and Lf_dev hold nrhs contiguous
- * N x N complex arrays of the plan dtype (device, no aliasing).  The FFT stages run per input;
+/* Multi-RHS apply (NEXT-2): Lf_b = L f_b for b < nrhs; f_dev holds nrhs contiguous N x N complex
+ * arrays of the plan dtype, Lf_dev nrhs contiguous outputs of fio_apply's shape (device, no
+ * overlap).  The FFT stages run per input;
  * per wedge the interpolation then serves every input from one alpha' (in skeleton storage mode
  * alpha' is rebuilt once per wedge for the whole batch).  The first call with a larger nrhs
  * allocates (nrhs - 1) extra spectra and fine-grid workspaces (synchronizing `stream`). */
@@ -149,7 +169,8 @@ fio_status fio_apply_batch(fio_handle h, int nrhs, const void* f_dev, void* Lf_d
 
 /* End-to-end variant: f_host / Lf_host are HOST buffers (pinned for overlap);
  * the host->device copy, the apply and the device->host copy are enqueued on
- * `stream`, which is synchronized before return. */
+ * `stream`, which is synchronized before return.  Lf_host has the shape
+ * fio_apply gives Lf_dev (the row slab with a communicator). */
 fio_status fio_apply_host(fio_handle h, const void* f_host, void* Lf_host, void* stream);
 
 fio_status fio_destroy(fio_handle h);
@@ -176,6 +197,8 @@ typedef struct {
                              alpha_bytes is then the size of the shared rebuild scratch */
   int k3_window_cols;     /* columns of the K3 interpolation window (w or w+1) */
   int k3_streams;         /* concurrent K3 streams of an apply (wedge l on stream l mod k3_streams) */
+  int has_comm;           /* 1 if the plan owns an NCCL communicator (fio_apply returns the row slab) */
+  int out_rows;           /* rows of the array fio_apply writes: N / nranks with a communicator, else N */
 } fio_info;
 
 fio_status fio_plan_info(fio_handle h, fio_info* info);

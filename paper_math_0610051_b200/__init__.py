@@ -9,7 +9,10 @@ CUDA device is missing, calls raise.
     Plan(N, c1, c2, ...)      fio_plan     (PAPER.md:981-1008, 1111-1250)
     Plan.apply(f)             fio_apply, device tensors
     Plan.apply_host(f, out)   fio_apply_host (host buffers, copies included)
-    Plan.apply_sharded(f, g)  per-rank partial + reduce-scatter over NCCL
+    Plan(..., nranks=R, group=g)  wedge-sharded plan; the library's NCCL communicator sums the
+                              ranks' partials (fio_apply returns this rank's row slab)
+    nccl_unique_id()          fio_nccl_unique_id (host only)
+    broadcast_nccl_id(group)  rank 0's id to every rank of a torch.distributed group
     geometry(N, W)            fio_geometry (host only)
     assign_wedges(cost, R)    fio_assign_wedges (host only)
 """
@@ -21,8 +24,8 @@ from typing import Optional
 
 import numpy as np
 
-__all__ = ["FioError", "Plan", "geometry", "assign_wedges", "reduce_scatter_rows", "library_path", "load_library",
-           "SYMBOLS", "STAGES"]
+__all__ = ["FioError", "Plan", "geometry", "assign_wedges", "nccl_unique_id", "broadcast_nccl_id", "row_slab",
+           "library_path", "load_library", "SYMBOLS", "STAGES"]
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 _LIB_PATH = os.path.join(_HERE, "libfio_b200.so")
@@ -34,7 +37,8 @@ FIO_OK, FIO_WNOTCERT = 0, 1
 # every entry point declared in include/fio.h
 SYMBOLS = ["fio_default_opts", "fio_plan", "fio_plan_save", "fio_plan_load", "fio_apply", "fio_apply_batch", "fio_apply_adjoint", "fio_apply_host", "fio_destroy", "fio_plan_info",
            "fio_plan_wedges", "fio_geometry", "fio_assign_wedges", "fio_profile_begin", "fio_profile_end",
-           "fio_last_error", "fio_version"]
+           "fio_last_error", "fio_version", "fio_nccl_unique_id"]
+NCCL_ID_BYTES = 128
 STAGES = ["K0_rows", "K0_cols", "K1_rowpass", "K2_colpass", "K3_interp"]
 
 
@@ -57,7 +61,8 @@ class _Opts(ctypes.Structure):
     _fields_ = [("dtype", ctypes.c_int), ("n_wedges", ctypes.c_int), ("nufft_w", ctypes.c_int),
                 ("nufft_beta", ctypes.c_double), ("seed", ctypes.c_uint64), ("device", ctypes.c_int),
                 ("rank", ctypes.c_int), ("nranks", ctypes.c_int), ("r_init", ctypes.c_int),
-                ("r_max", ctypes.c_int), ("certify", ctypes.c_int), ("skeleton", ctypes.c_int)]
+                ("r_max", ctypes.c_int), ("certify", ctypes.c_int), ("skeleton", ctypes.c_int),
+                ("nccl_id", ctypes.c_void_p)]
 
 
 class _Info(ctypes.Structure):
@@ -72,7 +77,8 @@ class _Info(ctypes.Structure):
                 ("max_tile_cap", ctypes.c_longlong), ("k3_thread_slots", ctypes.c_longlong),
                 ("rank_balance", ctypes.c_double), ("slot_terms", ctypes.c_longlong), ("group_p", ctypes.c_int),
                 ("k3_window_rows", ctypes.c_int), ("skeleton_bytes", ctypes.c_size_t),
-                ("k3_window_cols", ctypes.c_int), ("k3_streams", ctypes.c_int)]
+                ("k3_window_cols", ctypes.c_int), ("k3_streams", ctypes.c_int), ("has_comm", ctypes.c_int),
+                ("out_rows", ctypes.c_int)]
 
 
 def library_path() -> str:
@@ -107,10 +113,11 @@ def load_library():
     lib.fio_assign_wedges.argtypes = [I, P, I, P]
     lib.fio_profile_begin.argtypes = [P, I]
     lib.fio_profile_end.argtypes = [P, P, P]
+    lib.fio_nccl_unique_id.argtypes = [P]
     lib.fio_last_error.restype = ctypes.c_char_p
     lib.fio_version.restype = ctypes.c_char_p
     for name in ["fio_plan", "fio_apply", "fio_apply_batch", "fio_apply_adjoint", "fio_apply_host", "fio_destroy", "fio_plan_info", "fio_plan_wedges",
-                 "fio_geometry", "fio_assign_wedges", "fio_profile_begin", "fio_profile_end"]:
+                 "fio_geometry", "fio_assign_wedges", "fio_profile_begin", "fio_profile_end", "fio_nccl_unique_id"]:
         getattr(lib, name).restype = ctypes.c_int
     _lib = lib
     return lib
@@ -154,30 +161,31 @@ def assign_wedges(cost, nranks: int) -> np.ndarray:
     return owner
 
 
-def reduce_scatter_rows(part, nranks: int, group=None, out=None):
-    """Sum the N x N complex partials of all ranks and return this rank's row slab
-    [r N/R, (r+1) N/R).  NCCL: one reduce_scatter_tensor on the real view (NCCL has no complex
-    type).  Backends without reduce_scatter (gloo, used by the CPU tests): all_reduce + slice."""
-    import torch
+def nccl_unique_id() -> bytes:
+    """fio_nccl_unique_id: a fresh NCCL unique id (host only; the library loads libnccl.so.2)."""
+    buf = ctypes.create_string_buffer(NCCL_ID_BYTES)
+    _check(load_library().fio_nccl_unique_id(buf))
+    return buf.raw
+
+
+def broadcast_nccl_id(group=None) -> bytes:
+    """Rank 0 of the torch.distributed group draws the id, every rank returns the same bytes.  This
+    is the only collective the binding performs; the cross-GPU sum of the apply runs inside the
+    library (fio_apply's NCCL reduce-scatter)."""
     import torch.distributed as dist
-    N = part.shape[0]
+    obj = [nccl_unique_id() if dist.get_rank(group) == 0 else None]
+    dist.broadcast_object_list(obj, src=dist.get_global_rank(group, 0) if group is not None else 0, group=group)
+    if not isinstance(obj[0], (bytes, bytearray)) or len(obj[0]) != NCCL_ID_BYTES:
+        raise FioError(-4, "NCCL id broadcast failed")
+    return bytes(obj[0])
+
+
+def row_slab(N: int, nranks: int, rank: int):
+    """Rows [start, stop) of L f that rank `rank` receives from a communicator plan (include/fio.h)."""
     if N % nranks:
         raise FioError(-1, "nranks must divide N")
     rows = N // nranks
-    real = torch.view_as_real(part.contiguous()).reshape(-1)
-    if dist.get_backend(group) == "nccl":
-        slab = torch.empty(rows * N * 2, dtype=real.dtype, device=real.device) if out is None else \
-            torch.view_as_real(out).reshape(-1)
-        dist.reduce_scatter_tensor(slab, real, op=dist.ReduceOp.SUM, group=group)
-        return torch.view_as_complex(slab.reshape(rows, N, 2))
-    full = real.clone()
-    dist.all_reduce(full, op=dist.ReduceOp.SUM, group=group)
-    r = dist.get_rank(group)
-    slab = torch.view_as_complex(full.reshape(N, N, 2))[r * rows:(r + 1) * rows].clone()
-    if out is not None:
-        out.copy_(slab)
-        return out
-    return slab
+    return rank * rows, (rank + 1) * rows
 
 
 class Plan:
@@ -188,7 +196,8 @@ class Plan:
                  dtype: str = "c128", n_wedges: int = 0, nufft_w: int = 0, nufft_beta: float = 0.0,
                  seed: int = 0x5EED, device: Optional[int] = None, rank: int = 0, nranks: int = 1,
                  r_init: int = 32, r_max: int = 512, certify: bool = True, rho_sign: int = 1,
-                 amplitude: str = "separable", skeleton: bool = False, load: Optional[str] = None):
+                 amplitude: str = "separable", skeleton: bool = False, load: Optional[str] = None,
+                 group=None, nccl_id: Optional[bytes] = None):
         import torch
         if not torch.cuda.is_available():
             raise FioError(-3, "no CUDA device: the FIO apply runs only on the GPU (no CPU fallback)")
@@ -217,6 +226,15 @@ class Plan:
         o.device, o.rank, o.nranks = self.device, int(rank), int(nranks)
         o.r_init, o.r_max, o.certify = int(r_init), int(r_max), int(bool(certify))
         o.skeleton = int(bool(skeleton))
+        # wedge-sharded with a communicator: the id comes from rank 0 (broadcast over `group`, or given)
+        if nranks > 1 and nccl_id is None and group is not None:
+            nccl_id = broadcast_nccl_id(group)
+        idbuf = None
+        if nccl_id is not None:
+            if len(nccl_id) != NCCL_ID_BYTES:
+                raise FioError(-1, f"nccl_id must be {NCCL_ID_BYTES} bytes")
+            idbuf = ctypes.create_string_buffer(bytes(nccl_id), NCCL_ID_BYTES)
+            o.nccl_id = ctypes.cast(idbuf, ctypes.c_void_p)
         h = ctypes.c_void_p()
         with torch.cuda.device(self.device):
             if load is None:
@@ -229,6 +247,7 @@ class Plan:
         self.eps = eps
         self.rank, self.nranks = int(rank), int(nranks)
         self.torch_dtype = torch.complex64 if self.c64 else torch.complex128
+        self.out_rows = self.info["out_rows"]  # N, or N / nranks with a communicator (row slab)
 
     def save(self, path: str) -> None:
         """fio_plan_save: write this plan's separation (per wedge C, V S^-1, R, U_R^+) to path;
@@ -247,10 +266,11 @@ class Plan:
             raise FioError(-1, f"{name} must be contiguous")
         return t if writable else t.contiguous()
 
-    def _host_tensor(self, t, name):
-        """Check a host operand of apply_host: CPU, contiguous, plan dtype, exactly N*N elements."""
-        if t.is_cuda or t.dtype != self.torch_dtype or not t.is_contiguous() or t.numel() != self.N * self.N:
-            raise FioError(-1, f"{name} must be a contiguous CPU {self.torch_dtype} tensor of {self.N}x{self.N} "
+    def _host_tensor(self, t, name, rows=None):
+        """Check a host operand of apply_host: CPU, contiguous, plan dtype, exactly rows*N elements."""
+        rows = self.N if rows is None else rows
+        if t.is_cuda or t.dtype != self.torch_dtype or not t.is_contiguous() or t.numel() != rows * self.N:
+            raise FioError(-1, f"{name} must be a contiguous CPU {self.torch_dtype} tensor of {rows}x{self.N} "
                                f"elements")
         return t
 
@@ -259,8 +279,8 @@ class Plan:
         import torch
         f = self._dev_tensor(f, "f", (self.N, self.N))
         if out is None:
-            out = torch.empty_like(f)
-        out = self._dev_tensor(out, "out", (self.N, self.N), writable=True)
+            out = torch.empty((self.out_rows, self.N), dtype=f.dtype, device=f.device)
+        out = self._dev_tensor(out, "out", (self.out_rows, self.N), writable=True)
         if stream is None:
             stream = torch.cuda.current_stream(f.device)
         _check(self._lib.fio_apply(self._h, ctypes.c_void_p(f.data_ptr()), ctypes.c_void_p(out.data_ptr()),
@@ -274,8 +294,8 @@ class Plan:
             raise FioError(-1, f"f must have shape (B, {self.N}, {self.N})")
         f = self._dev_tensor(f, "f", (f.shape[0], self.N, self.N))
         if out is None:
-            out = torch.empty_like(f)
-        out = self._dev_tensor(out, "out", tuple(f.shape), writable=True)
+            out = torch.empty((f.shape[0], self.out_rows, self.N), dtype=f.dtype, device=f.device)
+        out = self._dev_tensor(out, "out", (f.shape[0], self.out_rows, self.N), writable=True)
         if stream is None:
             stream = torch.cuda.current_stream(f.device)
         _check(self._lib.fio_apply_batch(self._h, int(f.shape[0]), ctypes.c_void_p(f.data_ptr()),
@@ -287,8 +307,8 @@ class Plan:
         import torch
         g = self._dev_tensor(g, "g", (self.N, self.N))
         if out is None:
-            out = torch.empty_like(g)
-        out = self._dev_tensor(out, "out", (self.N, self.N), writable=True)
+            out = torch.empty((self.out_rows, self.N), dtype=g.dtype, device=g.device)
+        out = self._dev_tensor(out, "out", (self.out_rows, self.N), writable=True)
         if stream is None:
             stream = torch.cuda.current_stream(g.device)
         _check(self._lib.fio_apply_adjoint(self._h, ctypes.c_void_p(g.data_ptr()), ctypes.c_void_p(out.data_ptr()),
@@ -299,21 +319,13 @@ class Plan:
         """End-to-end apply from host (pinned) tensors; copies in both directions inside the call."""
         import torch
         self._host_tensor(f_host, "f_host")
-        self._host_tensor(out_host, "out_host")
+        self._host_tensor(out_host, "out_host", rows=self.out_rows)
         if stream is None:
             stream = torch.cuda.current_stream(self.device)
         _check(self._lib.fio_apply_host(self._h, ctypes.c_void_p(f_host.data_ptr()),
                                         ctypes.c_void_p(out_host.data_ptr()), ctypes.c_void_p(stream.cuda_stream)))
         return out_host
 
-    def apply_sharded(self, f, group=None, out=None):
-        """Wedge-sharded apply (BASELINE north_star (3)): this rank's partial sum over its own
-        wedges, then a sum-reduce-scatter over the process group.  Returns this rank's
-        (N/nranks) x N row slab of Lf."""
-        part = self.apply(f)
-        if self.nranks == 1:
-            return part
-        return reduce_scatter_rows(part, self.nranks, group=group, out=out)
 
     def profile_begin(self, max_applies: int):
         """Record per-stage CUDA events for the next max_applies applies (on their stream)."""

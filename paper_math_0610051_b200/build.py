@@ -18,8 +18,8 @@ INCLUDE = os.path.join(os.path.dirname(HERE), "include")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 CU_SOURCES = ["fio_kernels.cu", "fio_api.cu"]
-CPP_SOURCES = ["fio_host.cpp"]
-HEADERS = ["fio_internal.h", "fio_kernels.h"]
+CPP_SOURCES = ["fio_host.cpp", "fio_comm.cpp"]
+HEADERS = ["fio_internal.h", "fio_kernels.h", "fio_comm.h"]
 
 
 def _sources():
@@ -49,10 +49,11 @@ def build(force: bool = False, verbose: bool = False) -> str:
         objs.append(o)
     for s in CPP_SOURCES:
         o = os.path.join(objdir, s + ".o")
-        _run(["g++", *common, "-fPIC", "-fopenmp", "-Wall", "-c", os.path.join(CSRC, s), "-o", o], verbose)
+        _run(["g++", *common, "-I", os.path.join(os.path.dirname(os.path.dirname(NVCC)), "include"), "-fPIC",
+              "-fopenmp", "-Wall", "-c", os.path.join(CSRC, s), "-o", o], verbose)
         objs.append(o)
     tmp = LIB + ".tmp"
-    _run([NVCC, *ARCH, "-shared", "-cudart", "static", "-o", tmp, *objs, "-Xcompiler", "-fopenmp", "-lgomp"],
+    _run([NVCC, *ARCH, "-shared", "-cudart", "static", "-o", tmp, *objs, "-Xcompiler", "-fopenmp", "-lgomp", "-ldl"],
          verbose)
     os.replace(tmp, LIB)
     return LIB

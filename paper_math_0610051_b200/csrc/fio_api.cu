@@ -13,6 +13,7 @@
 #include <string>
 #include <vector>
 
+#include "fio_comm.h"
 #include "fio_internal.h"
 #include "fio_kernels.h"
 
@@ -86,11 +87,11 @@ struct DeviceGuard {
     return FIO_ECUDA;                                                                       \
   }
 
-// [a, a + n) and [b, b + n) overlap
-static bool overlaps(const void* a, const void* b, size_t n) {
+// [a, a + na) and [b, b + nb) overlap
+static bool overlaps(const void* a, size_t na, const void* b, size_t nb) {
   const char* x = static_cast<const char*>(a);
   const char* y = static_cast<const char*>(b);
-  return x < y + n && y < x + n;
+  return x < y + nb && y < x + na;
 }
 
 }  // namespace
@@ -157,10 +158,26 @@ struct fio_plan_s {
   double poly_err = 0;
   int certified = 1;
   int launches = 0;
+  void* comm = nullptr;        // NCCL communicator of the wedge-sharded apply (opts.nccl_id), or null
+  void* part = nullptr;        // comm: the N x N partial(s) this rank reduce-scatters (part_cap RHS)
+  int part_cap = 0;
   std::vector<cudaEvent_t> prof_ev;  // (kStages + 1) per recorded apply
   int prof_cap = 0, prof_n = 0;
 
   size_t elem_bytes() const { return c64 ? sizeof(float2) : sizeof(double2); }
+  int out_rows() const { return comm ? N / opts.nranks : N; }  // rows of what fio_apply writes
+  // comm: make room for nrhs N x N partials (synchronizes `s` before freeing a smaller buffer)
+  cudaError_t ensure_part(int nrhs, cudaStream_t s) {
+    if (nrhs <= part_cap) return cudaSuccess;
+    cudaError_t e = cudaStreamSynchronize(s);
+    if (e != cudaSuccess) return e;
+    if (part) cudaFree(part);
+    part = nullptr;
+    part_cap = 0;
+    e = cudaMalloc(&part, elem_bytes() * (size_t)N * N * nrhs);
+    if (e == cudaSuccess) part_cap = nrhs;
+    return e;
+  }
   cudaError_t alloc(void** p, size_t bytes) {
     cudaError_t e = cudaMalloc(p, std::max<size_t>(bytes, 16));
     if (e == cudaSuccess) allocs.push_back(*p);
@@ -190,6 +207,8 @@ struct fio_plan_s {
       if (side[j]) cudaStreamDestroy(side[j]);
     }
     if (batch_ws) cudaFree(batch_ws);
+    if (part) cudaFree(part);
+    comm_destroy(comm);
     for (void* p : allocs) cudaFree(p);
   }
 };
@@ -213,6 +232,14 @@ void fio_default_opts(fio_opts* o) {
   o->r_init = 32;
   o->r_max = 512;
   o->certify = 1;
+}
+
+fio_status fio_nccl_unique_id(void* id_out) {
+  if (!id_out) {
+    set_error("fio_nccl_unique_id: NULL argument");
+    return FIO_EINVAL;
+  }
+  return comm_unique_id(id_out);
 }
 
 fio_status fio_geometry(int N, int W, int* wedge_of_out, int* M, int* xc, int* box) {
@@ -1335,6 +1362,10 @@ static fio_status plan_impl(fio_handle* out, int N, const fio_phase* phase, cons
     set_error("fio_plan: negative option");
     return FIO_EINVAL;
   }
+  if (o.nranks > 1 && o.nccl_id && N % o.nranks != 0) {
+    set_error("fio_plan: with a communicator nranks must divide N (row slabs)");
+    return FIO_EINVAL;
+  }
   if (o.r_init == 0) o.r_init = 32;
   if (o.r_max == 0) o.r_max = 512;
   FIO_GUARD(o.device)
@@ -1366,7 +1397,17 @@ static fio_status plan_impl(fio_handle* out, int N, const fio_phase* phase, cons
     }
     P->load = load;
   }
-  fio_status st = build_plan(*P, phase, amp);
+  fio_status st = FIO_OK;
+  if (o.nccl_id) {  // (nranks == 1 is allowed: a one-rank communicator, the reduce-scatter is a copy)
+    // first, so that a rank whose plan fails later does not leave the others waiting in the init
+    st = comm_create(o.nccl_id, o.nranks, o.rank, &P->comm);
+    if (st != FIO_OK) {
+      delete P;
+      return st;
+    }
+  }
+  P->opts.nccl_id = nullptr;  // not retained (the caller owns the id bytes)
+  st = build_plan(*P, phase, amp);
   P->load = nullptr;
   if (st < 0) {
     delete P;
@@ -1383,7 +1424,7 @@ fio_status fio_apply(fio_handle h, const void* f_dev, void* Lf_dev, void* stream
     set_error("fio_apply: NULL argument");
     return FIO_EINVAL;
   }
-  if (overlaps(f_dev, Lf_dev, h->elem_bytes() * (size_t)h->N * h->N)) {
+  if (overlaps(f_dev, h->elem_bytes() * (size_t)h->N * h->N, Lf_dev, h->elem_bytes() * (size_t)h->out_rows() * h->N)) {
     set_error("fio_apply: f and Lf must not overlap");
     return FIO_EINVAL;
   }
@@ -1392,9 +1433,17 @@ fio_status fio_apply(fio_handle h, const void* f_dev, void* Lf_dev, void* stream
   int launches = 0;
   cudaEvent_t* ev = nullptr;
   if (h->prof_n < h->prof_cap) ev = &h->prof_ev[(size_t)h->prof_n++ * (kStages + 1)];
-  FIO_CUDA(enqueue_apply(a, h->c64, f_dev, Lf_dev, (cudaStream_t)stream, &launches, ev));
+  cudaStream_t s = (cudaStream_t)stream;
+  if (!h->comm) {
+    FIO_CUDA(enqueue_apply(a, h->c64, f_dev, Lf_dev, s, &launches, ev));
+    h->launches = launches;
+    return FIO_OK;
+  }
+  // A6: this rank's partial over its wedges, then the sum over ranks into its row slab
+  FIO_CUDA(h->ensure_part(1, s));
+  FIO_CUDA(enqueue_apply(a, h->c64, f_dev, h->part, s, &launches, ev));
   h->launches = launches;
-  return FIO_OK;
+  return comm_reduce_scatter(h->comm, h->part, Lf_dev, 2 * (size_t)h->out_rows() * h->N, h->c64, s);
 }
 
 fio_status fio_apply_batch(fio_handle h, int nrhs, const void* f_dev, void* Lf_dev, void* stream) {
@@ -1402,7 +1451,8 @@ fio_status fio_apply_batch(fio_handle h, int nrhs, const void* f_dev, void* Lf_d
     set_error("fio_apply_batch: bad arguments");
     return FIO_EINVAL;
   }
-  if (overlaps(f_dev, Lf_dev, h->elem_bytes() * (size_t)h->N * h->N * (size_t)nrhs)) {
+  if (overlaps(f_dev, h->elem_bytes() * (size_t)h->N * h->N * nrhs, Lf_dev,
+               h->elem_bytes() * (size_t)h->out_rows() * h->N * nrhs)) {
     set_error("fio_apply_batch: f and Lf must not overlap");
     return FIO_EINVAL;
   }
@@ -1428,7 +1478,19 @@ fio_status fio_apply_batch(fio_handle h, int nrhs, const void* f_dev, void* Lf_d
     for (size_t j = 0; j < nacc; ++j) args[b].acc[j] = base + cs * (NN + std::max<size_t>(h->fine_elems, 1) + j * NN);
   }
   int launches = 0;
-  FIO_CUDA(enqueue_apply_batch(args.data(), nrhs, h->c64, f_dev, Lf_dev, (cudaStream_t)stream, &launches));
+  cudaStream_t s = (cudaStream_t)stream;
+  if (!h->comm) {
+    FIO_CUDA(enqueue_apply_batch(args.data(), nrhs, h->c64, f_dev, Lf_dev, s, &launches));
+    return FIO_OK;
+  }
+  FIO_CUDA(h->ensure_part(nrhs, s));
+  FIO_CUDA(enqueue_apply_batch(args.data(), nrhs, h->c64, f_dev, h->part, s, &launches));
+  const size_t slab = (size_t)h->out_rows() * h->N;
+  for (int b = 0; b < nrhs; ++b) {
+    fio_status st = comm_reduce_scatter(h->comm, static_cast<char*>(h->part) + cs * NN * b,
+                                        static_cast<char*>(Lf_dev) + cs * slab * b, 2 * slab, h->c64, s);
+    if (st != FIO_OK) return st;
+  }
   return FIO_OK;
 }
 
@@ -1437,15 +1499,21 @@ fio_status fio_apply_adjoint(fio_handle h, const void* g_dev, void* out_dev, voi
     set_error("fio_apply_adjoint: NULL argument");
     return FIO_EINVAL;
   }
-  if (overlaps(g_dev, out_dev, h->elem_bytes() * (size_t)h->N * h->N)) {
+  if (overlaps(g_dev, h->elem_bytes() * (size_t)h->N * h->N, out_dev, h->elem_bytes() * (size_t)h->out_rows() * h->N)) {
     set_error("fio_apply_adjoint: g and out must not overlap");
     return FIO_EINVAL;
   }
   FIO_GUARD(h->device)
   ApplyArgs a = make_args(*h);
   int launches = 0;
-  FIO_CUDA(enqueue_adjoint(a, h->c64, g_dev, out_dev, (cudaStream_t)stream, &launches));
-  return FIO_OK;
+  cudaStream_t s = (cudaStream_t)stream;
+  if (!h->comm) {
+    FIO_CUDA(enqueue_adjoint(a, h->c64, g_dev, out_dev, s, &launches));
+    return FIO_OK;
+  }
+  FIO_CUDA(h->ensure_part(1, s));
+  FIO_CUDA(enqueue_adjoint(a, h->c64, g_dev, h->part, s, &launches));
+  return comm_reduce_scatter(h->comm, h->part, out_dev, 2 * (size_t)h->out_rows() * h->N, h->c64, s);
 }
 
 fio_status fio_apply_host(fio_handle h, const void* f_host, void* Lf_host, void* stream) {
@@ -1454,6 +1522,7 @@ fio_status fio_apply_host(fio_handle h, const void* f_host, void* Lf_host, void*
     return FIO_EINVAL;
   }
   const size_t bytes = (size_t)h->N * h->N * h->elem_bytes();
+  const size_t out_bytes = (size_t)h->out_rows() * h->N * h->elem_bytes();
   FIO_GUARD(h->device)  // the staging buffers live on the plan's device
   if (!h->e2e_in) {
     FIO_CUDA(h->alloc(&h->e2e_in, bytes));
@@ -1463,7 +1532,7 @@ fio_status fio_apply_host(fio_handle h, const void* f_host, void* Lf_host, void*
   FIO_CUDA(cudaMemcpyAsync(h->e2e_in, f_host, bytes, cudaMemcpyHostToDevice, s));
   fio_status st = fio_apply(h, h->e2e_in, h->e2e_out, stream);
   if (st != FIO_OK) return st;
-  FIO_CUDA(cudaMemcpyAsync(Lf_host, h->e2e_out, bytes, cudaMemcpyDeviceToHost, s));
+  FIO_CUDA(cudaMemcpyAsync(Lf_host, h->e2e_out, out_bytes, cudaMemcpyDeviceToHost, s));
   FIO_CUDA(cudaStreamSynchronize(s));
   return FIO_OK;
 }
@@ -1547,6 +1616,8 @@ fio_status fio_plan_info(fio_handle h, fio_info* info) {
   info->fine_elems = h->fine_elems;
   info->p1_elems = h->p1_elems;
   info->launches_per_apply = h->launches;
+  info->has_comm = h->comm ? 1 : 0;
+  info->out_rows = h->out_rows();
   return FIO_OK;
 }
 
