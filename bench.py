@@ -98,10 +98,11 @@ class Clocks:
 
 # ---------------------------------------------------------------- roofline model
 def k3_algorithmic_bytes(info, N, c64):
-    """Algorithmic HBM bytes of one K3 launch: alpha' (N^2 sum_q), every fine grid
-    read once, the phase data c1, c2 (8 B each per x), a(x,0)/N (16 B per x) and the Lf write."""
+    """Algorithmic HBM bytes of the K3 launches of one apply:
+    alpha' = N^2 sum_q s (every output point x each owned wedge's terms, no padding), one read of
+    every fine grid G_lt, and the Lf write."""
     cs = 8 if c64 else 16
-    return info["alpha_bytes"] + info["fine_elems"] * cs + N * N * (8 + 8 + 16 + cs)
+    return N * N * info["sum_q"] * cs + info["fine_elems"] * cs + N * N * cs
 
 
 def apply_algorithmic_bytes(info, N, c64):
@@ -114,24 +115,24 @@ def apply_algorithmic_bytes(info, N, c64):
 
 
 def k3_resource_model(info, c64, ms, sm_mhz):
-    """What binds K3: per group-term the thread reads its window (k3_window_rows
-    x k3_window_cols) and the P FP32 row weights from shared memory and alpha'(t) from the ring,
-    and issues 2 real FMAs per (point, window cell) plus 2 per (point, row) plus the alpha product.
-    Returns achieved fractions of the SM load datapath (128 B/clk/SM) and of the FMA pipe
-    (128 FP32 or 64 FP64 FMA/clk/SM) at the measured SM clock."""
-    w = info["nufft_w"]
+    """What binds K3 on chip: per group-term the thread reads its window
+    (k3_window_rows x k3_window_cols, plan dtype) and the P row weights (FP32 c64 / FP64 c128) from
+    shared memory and alpha'(t) from the ring, and issues 2 real FMAs per (point, window cell), 2 per
+    (point, row) and 4 for the alpha product.  Fractions of the shared -> register path
+    (128 B/clk/SM) and of the FMA pipe (measured: 126 FP32 / 63.3 FP64 FMA/clk/SM,
+    profiles/r02_microbench.json) at the sampled SM clock."""
     P = info["group_p"]
-    win, winr = info.get("k3_window_cols") or w + 1, info.get("k3_window_rows") or w
-    cs, rs = (8, 4) if c64 else (16, 4)
+    win, winr = info["k3_window_cols"], info["k3_window_rows"]
+    cs, rs = (8, 4) if c64 else (16, 8)
     gt = info["slot_terms"] / P
     lsu_bytes = gt * (winr * win * cs + winr * P * rs + P * cs)
-    fmas = gt * (winr * (P * win * 2 + P * 2) + 4 * P)
+    fmas = gt * P * (winr * (win * 2 + 2) + 4)
     clk = (sm_mhz or 1965.0) * 1e6
     t = ms * 1e-3
     sms = 148
     return {"lsu_bytes": lsu_bytes, "lsu_frac": lsu_bytes / t / (sms * 128 * clk),
-            "fma": fmas, "fma_frac": fmas / t / (sms * (128 if c64 else 64) * clk),
-            "sm_mhz": sm_mhz, "model": "DESIGN.md section 7"}
+            "fma": fmas, "fma_frac": fmas / t / (sms * (126.4 if c64 else 63.3) * clk),
+            "flops_per_s": 2 * fmas / t, "sm_mhz": sm_mhz, "model": "DESIGN.md section 7"}
 
 
 def peaks():
@@ -152,10 +153,11 @@ def cpu_oracle_rate(cfg, npts, seed=1):
     fh = oracle.dft2(f)
     pts = wl.sample_points(N, npts, seed)
     t0 = time.perf_counter()
-    oracle.fio(op, fhat=fh, pts=pts)
+    ref = oracle.fio(op, fhat=fh, pts=pts)
     dt = time.perf_counter() - t0
     pps = len(pts) / dt
-    return {"value": pps / (N * N), "unit": "applies/s", "points_per_s": pps, "cores": oracle.num_threads(),
+    return {"ref": ref, "pts": pts, "value": pps / (N * N), "unit": "applies/s", "points_per_s": pps,
+            "cores": oracle.num_threads(),
             "kind": "oracle",
             "sample": f"{len(pts)} seeded output points of the N={N} grid (direct sum over all N^2 frequencies, "
                       f"fhat precomputed), {dt:.1f} s; applies/s = points/s / N^2"}
@@ -171,6 +173,7 @@ def run_reference(args):
     npts = max(64, args.cpu_points // 4)
     for i in range(args.warmup + args.steps):
         r = cpu_oracle_rate(cfg, npts, seed=1 + i)
+        r.pop("ref"), r.pop("pts")
         if i >= args.warmup:
             times.append(r)
     pps = statistics.median([t["points_per_s"] for t in times])
@@ -284,9 +287,9 @@ def time_config(name, args, rank, world, local, group):
     k3_bytes = k3_algorithmic_bytes(info, N, c64)
     traffic = None  # DRAM bytes of all K3 launches of one apply, from the committed ncu capture
     try:
-        with open(os.path.join(ROOT, "profiles", "r01_k3_traffic.json")) as fh:
+        with open(os.path.join(ROOT, "profiles", "r02_k3_traffic.json")) as fh:
             tr = json.load(fh).get(name)
-        if tr and world == 1:
+        if tr and world == 1 and tr.get("sum_q") == info["sum_q"]:
             traffic = tr["dram_bytes"]
     except Exception:
         traffic = None
@@ -299,19 +302,22 @@ def time_config(name, args, rank, world, local, group):
         "k3_share": k3_ms / total_stage if total_stage > 0 else None,
         "roofline": {"bound": "hbm", "achieved": ach, "peak": hbm, "unit": "GB/s", "frac": ach / hbm,
                      "traffic": traffic, "kernel": "k_interp_groups (K3, all wedge launches of one apply)",
-                     "peak_source": src, "traffic_source": "profiles/r01_k3_traffic.json (ncu, cold cache)",
-                     "algorithmic_bytes": k3_bytes},
+                     "peak_source": src, "traffic_source": "profiles/r02_k3_traffic.json (ncu, cold cache)",
+                     "algorithmic_bytes": k3_bytes,
+                     "bytes_model": "N^2 sum_q s (alpha') + fine_elems s (G read once) + N^2 s (Lf write)"},
         "apply_hbm_gbs": apply_algorithmic_bytes(info, N, c64) / (ms_step * 1e-3) / 1e9,
         "k3_resources": k3_resource_model(info, c64, k3_ms, clk.summary().get("sm_mhz")),
         "plan": {"W": info["W"], "sum_q": info["sum_q"], "nufft_w": info["nufft_w"],
                  "plan_seconds": info["plan_seconds"], "max_sep_err": info["max_sep_err"],
                  "alpha_GB": info["alpha_bytes"] / 1e9, "fine_elems": info["fine_elems"],
                  "slots": info["slots"], "max_tile_cap": info["max_tile_cap"],
-                 "k3_thread_fill": info["slots"] / 4 / max(info["k3_thread_slots"], 1),
+                 "k3_group_fill": info["slots"] / max(info["slot_terms"] / max(info["sum_q"], 1), 1),
+                 "group_p": info["group_p"],
                  "rank_balance": info["rank_balance"]},
         "launches_per_step": info["launches_per_apply"],
         "adjoint_ms_per_step": adj_ms,
         "clocks": clk.summary(), "e2e": e2e,
+        "out": out.cpu().numpy().astype(np.complex128) if world == 1 else None,
     }
     plan.close()
     del f, out
@@ -339,8 +345,16 @@ def run_gpu(args):
                                                     "adjoint_ms_per_step", "k3_resources")}
     if rank == 0:
         cpu = None
+        check = None
         if world == 1 and not args.no_cpu_baseline:
             cpu = cpu_oracle_rate(wl.config(args.config), args.cpu_points)
+            # the TIMED output against the oracle values the cpu_baseline leg just computed
+            ref, pts = cpu.pop("ref"), cpu.pop("pts")
+            got = main["out"].ravel()[pts]
+            rms = float(np.sqrt(np.mean(np.abs(ref) ** 2)))
+            check = {"rel_l2": float(np.linalg.norm(got - ref) / np.linalg.norm(ref)),
+                     "max_abs_err_over_rms": float(np.abs(got - ref).max() / rms), "points": int(len(pts)),
+                     "bar": f"rel_l2 <= 10 eps = {10 * main['eps']:g}"}
         line = {
             "metric": "fio_applies_per_s", "value": main["applies_per_s"], "unit": "applies/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": main["ms_per_step"],
@@ -355,7 +369,7 @@ def run_gpu(args):
             "k3_share": main["k3_share"], "plan": main["plan"], "adjoint_ms_per_step": main["adjoint_ms_per_step"],
             "clocks": main["clocks"], "e2e": main["e2e"],
             "gpu_launches": main["launches_per_step"] * args.steps,
-            "cpu_baseline": cpu, "variants": variants,
+            "cpu_baseline": cpu, "check": check, "variants": variants,
         }
         print(json.dumps(line), flush=True)
     if world > 1:

@@ -96,7 +96,7 @@ typedef struct {
 typedef struct {
   fio_dtype dtype;    /* FIO_C128 */
   int n_wedges;       /* 0 -> W = 8 round(2 sqrt(N)/8), >= 8 (reading R1) */
-  int nufft_w;        /* 0 -> taps per dimension chosen from eps (reading R10) */
+  int nufft_w;        /* 0 -> taps per dimension chosen from eps (reading R10); 3..12 */
   double nufft_beta;  /* 0 -> 2.30 w (exponential-of-semicircle kernel) */
   uint64_t seed;      /* 0x5EED: seed of the randomized separation */
   int device;         /* CUDA device ordinal; -1 -> current device */
@@ -126,7 +126,8 @@ void fio_default_opts(fio_opts* opts);
 
 /* Build a plan for the N x N operator (N even, 5-smooth, 8 <= N <= 4096) at
  * separation accuracy eps in (0, 1) (the relative singular
- * value cutoff, reading R6).  opts may be NULL (defaults).  Runs on the device
+ * value cutoff, reading R6), eps >= 1e-6 for FIO_C64 and >= 1e-11 for FIO_C128
+ * (FIO_EINVAL below: the arithmetic could not deliver it, reading R24).  opts may be NULL (defaults).  Runs on the device
  * (kernel-entry evaluation, Gram products, factor expansion) and the host
  * (partition, pivoting, small Jacobi SVDs).  Synchronous.
  * Returns FIO_OK, FIO_WNOTCERT, or an error (*out is then NULL). */

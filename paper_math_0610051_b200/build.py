@@ -40,7 +40,9 @@ def build(force: bool = False, verbose: bool = False) -> str:
     objdir = os.path.join(HERE, "build")
     os.makedirs(objdir, exist_ok=True)
     objs = []
-    common = ["-O3", "-std=c++17", "-I", INCLUDE]
+    # FIO_NVCC_FLAGS: extra -D switches for measured variants (tools/k3_variants.py); empty for the product
+    extra = os.environ.get("FIO_NVCC_FLAGS", "").split()
+    common = ["-O3", "-std=c++17", "-I", INCLUDE, *extra]
     for s in CU_SOURCES:
         o = os.path.join(objdir, s + ".o")
         cmd = [NVCC, *ARCH, "-lineinfo", *common, "-Xptxas", "-v" if verbose else "-O3",

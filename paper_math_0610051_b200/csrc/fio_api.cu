@@ -28,6 +28,8 @@ namespace {
 constexpr size_t kSmemBudgetDefault = 48 * 1024;  // per-CTA FFT pass target (FIO_FFT_SMEM_KB overrides)
 constexpr size_t kSmemMax = 200 * 1024;     // opt-in maximum for one long sequence
 constexpr int kCertSamples = 200;           // s of PAPER.md:1464-1477
+constexpr double kEpsFloorC64 = 1e-6, kEpsFloorC128 = 1e-11;
+constexpr double kGramEpsFloor = 1e-7;      // below: shifted CholeskyQR3 instead of the Gram eigen-decomposition
 
 #define FIO_CUDA(expr)                                                                               \
   do {                                                                                               \
@@ -330,12 +332,63 @@ fio_status separate_wedge(fio_plan_s& P, const WedgeGeom& g, Rng& rng, cudaStrea
     int nsplit = std::max(1, std::min(256, m / 8192));
     FIO_CUDA(dWork.ensure(sizeof(double2) * (size_t)nsplit * rc * rc));
     FIO_CUDA(dGram.ensure(sizeof(double2) * (size_t)rc * rc));
-    FIO_CUDA(launch_zgemm(rc, rc, m, dAC.as<double2>(), m, 1, true, dAC.as<double2>(), 1, m, dGram.as<double2>(), 1,
-                          rc, nsplit, dWork.as<double2>(), s));
-    std::vector<cplx> G((size_t)rc * rc);
-    FIO_CUDA(cudaMemcpyAsync(G.data(), dGram.p, sizeof(cplx) * G.size(), cudaMemcpyDeviceToHost, s));
-    FIO_CUDA(cudaStreamSynchronize(s));
-    jacobi_svd(rc, rc, G, V, lam);  // G PSD: singular values = eigenvalues, V = eigenvectors
+    auto gram = [&](const double2* A, std::vector<cplx>& G) -> fio_status {  // G = A^H A (m x rc)
+      FIO_CUDA(launch_zgemm(rc, rc, m, A, m, 1, true, A, 1, m, dGram.as<double2>(), 1, rc, nsplit,
+                            dWork.as<double2>(), s));
+      G.resize((size_t)rc * rc);
+      FIO_CUDA(cudaMemcpyAsync(G.data(), dGram.p, sizeof(cplx) * G.size(), cudaMemcpyDeviceToHost, s));
+      FIO_CUDA(cudaStreamSynchronize(s));
+      return FIO_OK;
+    };
+    std::vector<cplx> G;
+    if (eps >= kGramEpsFloor) {
+      // singular values of A_C from the eigen-decomposition of its Gram matrix: sigma_k / sigma_1
+      // is resolved down to ~sqrt(machine eps), enough for eps >= kGramEpsFloor
+      fio_status st = gram(dAC.as<double2>(), G);
+      if (st != FIO_OK) return st;
+      jacobi_svd(rc, rc, G, V, lam);  // G PSD: singular values = eigenvalues, V = eigenvectors
+    } else {
+      // high accuracy (eps below ~1e-7): shifted CholeskyQR3 of A_C = Q R (Q orthonormal to machine
+      // precision even for numerically rank-deficient A_C), then the SVD of the small R, whose
+      // singular values carry A_C's to ~1e-15 sigma_1 (a Gram eigen-decomposition would square the
+      // condition number and lose everything below ~1e-8 sigma_1)
+      FIO_CUDA(dY.ensure(sizeof(double2) * (size_t)rc * rc));
+      DevBuf dQ[2];
+      FIO_CUDA(dQ[0].ensure(sizeof(double2) * (size_t)m * rc));
+      FIO_CUDA(dQ[1].ensure(sizeof(double2) * (size_t)m * rc));
+      FIO_CUDA(cudaMemcpyAsync(dQ[0].p, dAC.p, sizeof(double2) * (size_t)m * rc, cudaMemcpyDeviceToDevice, s));
+      std::vector<cplx> Rt((size_t)rc * rc, cplx{0, 0}), Rinv, tmp;
+      for (int i = 0; i < rc; ++i) Rt[i + (size_t)i * rc] = {1.0, 0.0};
+      int cur = 0;
+      for (int pass = 0; pass < 3; ++pass) {
+        fio_status st = gram(dQ[cur].as<double2>(), G);
+        if (st != FIO_OK) return st;
+        double shift = 0.0;
+        if (pass == 0) {  // Fukaya et al.'s shift 11 (m n + n (n+1)) u ||A||_F^2
+          double tr = 0;
+          for (int i = 0; i < rc; ++i) tr += G[i + (size_t)i * rc].re;
+          shift = 11.0 * ((double)m * rc + (double)rc * (rc + 1)) * 1.1102230246251565e-16 * tr;
+        }
+        std::vector<cplx> R = G;
+        for (int i = 0; i < rc; ++i) R[i + (size_t)i * rc].re += shift;
+        for (int tries = 0; !cholesky_upper(rc, R) && tries < 8; ++tries) {
+          shift = shift > 0 ? 10.0 * shift : 1e-15 * G[0].re;
+          R = G;
+          for (int i = 0; i < rc; ++i) R[i + (size_t)i * rc].re += shift;
+        }
+        upper_inverse(rc, R, Rinv);
+        FIO_CUDA(cudaMemcpy(dY.p, Rinv.data(), sizeof(cplx) * Rinv.size(), cudaMemcpyHostToDevice));
+        FIO_CUDA(launch_zgemm(m, rc, rc, dQ[cur].as<double2>(), 1, m, false, dY.as<double2>(), 1, rc,
+                              dQ[cur ^ 1].as<double2>(), 1, m, 1, nullptr, s));
+        cur ^= 1;
+        small_matmul(rc, R, Rt, tmp);  // R_total = R_pass R_total
+        Rt.swap(tmp);
+      }
+      std::vector<double> sg;
+      jacobi_svd(rc, rc, Rt, V, sg);  // R_total = U S V^H: A_C = (Q U) S V^H
+      lam.resize(rc);
+      for (int k = 0; k < rc; ++k) lam[k] = sg[k] * sg[k];
+    }
     const double s1 = std::sqrt(std::max(lam[0], 0.0));
     q = 0;
     for (int k = 0; k < rc; ++k)
@@ -570,9 +623,9 @@ static K3Tables make_k3_tables(std::vector<double> uh, long long NN, int taps, b
   for (long long x = 0; x < NN; ++x) std::swap(uh[2 * x], uh[2 * x + 1]);  // (K3 row, column) = (u2, u1)
   std::vector<int> anchor, slot_x;
   std::vector<double> off;
-  group_points(uh.data(), NN, taps, group_p(c64), n2f, n1f, super_rows(c64), super_cols(c64), anchor, slot_x, off);
+  group_points(uh.data(), NN, taps, group_p(c64, taps), n2f, n1f, super_rows(c64), super_cols(c64), anchor, slot_x, off);
   std::vector<double>().swap(uh);
-  const int gp = group_p(c64);
+  const int gp = group_p(c64, taps);
   T.real_groups = (long long)(anchor.size() / 2);
   const int blk = c64 ? kK3BlockC64 : kK3BlockC128;
   T.cap = chunk_boxes(anchor, blk, k3_window_rows(taps, c64), k3_window_cols(taps, c64),
@@ -886,7 +939,7 @@ fio_status build_plan(fio_plan_s& P, const fio_phase* phase, const fio_amplitude
     }
     auto tw2 = now();
     t_group += secs(tw1, tw2);
-    const long long nslots = (long long)iw.ngroups * group_p(c64);
+    const long long nslots = (long long)iw.ngroups * group_p(c64, P.taps);
     void* alpha = nullptr;
     void* betap = nullptr;
     SkelWedge sk{};
@@ -932,7 +985,7 @@ fio_status build_plan(fio_plan_s& P, const fio_phase* phase, const fio_amplitude
     if (prof) cudaDeviceSynchronize();
     t_fold += secs(tw2, now());
     if (!P.opts.skeleton) P.alpha_bytes += cs * (size_t)q * nslots;
-    P.slots += real_groups * group_p(c64);  // point slots before the chunk padding
+    P.slots += real_groups * group_p(c64, P.taps);  // point slots before the chunk padding
     P.slot_terms += nslots * (long long)q;
     P.iw.push_back(iw);
     P.beta_bytes += cs * (size_t)q * g.n1 * g.n2;
@@ -1350,12 +1403,21 @@ static fio_status plan_impl(fio_handle* out, int N, const fio_phase* phase, cons
     set_error("fio_plan: dtype must be FIO_C64 or FIO_C128");
     return FIO_EINVAL;
   }
+  // accuracy floors (reading R24): complex64 arithmetic cannot deliver 10 eps below ~1e-6;
+  // complex128 is limited by the largest NUFFT window (kMaxTaps taps, ~1e-11)
+  const double eps_floor = o.dtype == FIO_C64 ? kEpsFloorC64 : kEpsFloorC128;
+  if (eps < eps_floor) {
+    set_error("fio_plan: eps " + std::to_string(eps) + " is below the " +
+              (o.dtype == FIO_C64 ? std::string("complex64") : std::string("complex128")) + " floor " +
+              std::to_string(eps_floor));
+    return FIO_EINVAL;
+  }
   if (o.nranks < 1 || o.rank < 0 || o.rank >= o.nranks) {
     set_error("fio_plan: need 0 <= rank < nranks");
     return FIO_EINVAL;
   }
   if (o.nufft_w != 0 && (o.nufft_w < 3 || o.nufft_w > kMaxTaps)) {
-    set_error("fio_plan: nufft_w must be 0 or in [3, 10]");
+    set_error("fio_plan: nufft_w must be 0 or in [3, 12]");
     return FIO_EINVAL;
   }
   if (o.n_wedges < 0 || o.r_init < 0 || o.r_max < 0) {
@@ -1384,7 +1446,7 @@ static fio_status plan_impl(fio_handle* out, int N, const fio_phase* phase, cons
   P->taps = o.nufft_w > 0 ? o.nufft_w : taps_for_eps(eps);
   P->es_beta = o.nufft_beta > 0 ? o.nufft_beta : 2.30 * P->taps;
   // polynomial kernel for the c128 K3 weights: error ~1.5 e^{-beta}, the kernel's own edge value
-  P->poly_err = es_poly_fit(P->taps, P->es_beta, 2.0 * std::exp(-P->es_beta), P->poly);
+  P->poly_err = es_poly_fit(P->taps, P->es_beta, P->poly);
   P->input_hash = input_hash(N, phase, amp);
   if (load) {  // fio_plan_load: the file must describe exactly this plan
     const bool same = hdr->N == N && hdr->W == P->W && hdr->dtype == o.dtype && hdr->taps == P->taps &&
@@ -1606,7 +1668,7 @@ fio_status fio_plan_info(fio_handle h, fio_info* info) {
   info->k3_thread_slots = h->chunk_threads;
   info->rank_balance = h->balance;
   info->slot_terms = h->slot_terms;
-  info->group_p = group_p(h->c64);
+  info->group_p = group_p(h->c64, h->taps);
   info->skeleton_bytes = h->skel_bytes;
   info->k3_window_cols = k3_window_cols(h->taps, h->c64);
   info->k3_streams = h->k3_streams;

@@ -194,12 +194,13 @@ double es_fourier(double s, int w, double beta) {
 }
 
 // Chebyshev interpolation of phi(s - j) on s in (w/2 - 1, w/2] at deg+1 nodes, converted to
-// monomial coefficients in x = 2 (s - w/2) + 1; the degree grows until the error measured
-// on a fine grid is below tol.
-double es_poly_fit(int w, double beta, double tol, EsPoly& out) {
+// monomial coefficients in x = 2 (s - w/2) + 1, at the kernels' fixed degree k3_poly_deg(w); returns
+// the error measured on a fine grid (about 1.5 e^{-beta} at the default beta, the kernel's own edge
+// value: the polynomial is as accurate as the kernel it stands for).
+double es_poly_fit(int w, double beta, EsPoly& out) {
   const double pi = 3.14159265358979323846;
   double err = 1.0;
-  for (int deg = 6; deg <= kPolyMaxDeg; ++deg) {
+  for (int deg = k3_poly_deg(w); deg <= k3_poly_deg(w); ++deg) {
     std::memset(&out, 0, sizeof(out));
     out.deg = deg;
     const int n = deg + 1;
@@ -243,7 +244,6 @@ double es_poly_fit(int w, double beta, double tol, EsPoly& out) {
         err = std::max(err, std::fabs(p - es_kernel(sv - j, w, beta)));
       }
     }
-    if (err <= tol) break;
   }
   for (int m = 0; m <= out.deg; ++m)
     for (int j = 0; j < w; ++j) out.cf[m][j] = (float)out.c[j][m];
@@ -271,97 +271,119 @@ void lpt_assign(int W, const double* cost, int nranks, int* owner) {
   }
 }
 
-static inline long long floor_div2(long long b) { return b >= 0 ? b / 2 : -((-b + 1) / 2); }
-
-// K3 grouping: base cell b = ceil(u - w/2) per axis, supercell
-// s = (floor(b1 / super_rows), floor(b2 / 2)); points are counting-sorted by supercell (row-major,
-// then by x) and each supercell's list is cut into groups of P.  The k3_window_rows(w) x (w+1)
-// window anchored at (kSuperRows s1, 2 s2) covers the w x w taps of every point of the group.
+// K3 grouping: base cell b = ceil(u - w/2) per axis (the first of the point's w
+// taps).  The window of a group spans kSuperRows x kSuperCols base cells -- (w + kSuperRows - 1) x
+// (w + kSuperCols - 1) fine cells -- so a group may hold points whose base cells differ by at most
+// one along the "run" axis (columns when kSuperCols == 2, rows when kSuperRows == 2).  Points are
+// counting-sorted by (fixed axis, run axis, x) and cut greedily: a group takes the next points while
+// they share the fixed-axis base and lie within two run-axis bases of the group's first point (its
+// anchor), up to P points.  Sliding anchors (instead of a fixed supercell lattice) keep the groups
+// full: only a run's last group can be partly empty.  Groups are then ordered in serpentine
+// 16 x 16-cell blocks of their anchors, so a K3 chunk (consecutive groups) has a compact footprint.
 void group_points(const double* u, long long NN, int taps, int P, int n1f, int n2f, int kSuperRows, int kSuperCols,
                   std::vector<int>& anchor, std::vector<int>& slot_x, std::vector<double>& off) {
-  const long long lo = -((taps + 3) / 2) - 1;  // smallest possible supercell index (per axis, in units of 2)
-  const long long lo1 = kSuperRows == 1 ? 2 * lo : lo, lo2 = kSuperCols == 1 ? 2 * lo : lo;
-  const long long n1s = kSuperRows == 1 ? n1f + 16 : n1f / 2 + 8, n2s = kSuperCols == 1 ? n2f + 16 : n2f / 2 + 8;
-  const long long nkeys = n1s * n2s;
+  const bool run_cols = kSuperCols == 2;  // c64: runs along columns within a base row
+  const long long lo = -(taps / 2) - 2;    // smallest base index per axis (u >= 0)
+  const long long nb1 = n1f + taps + 4, nb2 = n2f + taps + 4;
+  std::vector<int> b1v(NN), b2v(NN);
   std::vector<int> key(NN);
+  const long long nmaj = run_cols ? nb1 : nb2, nmin = run_cols ? nb2 : nb1;
 #pragma omp parallel for schedule(static)
   for (long long x = 0; x < NN; ++x) {
-    long long b1 = (long long)std::ceil(u[2 * x] - 0.5 * taps);
-    long long b2 = (long long)std::ceil(u[2 * x + 1] - 0.5 * taps);
-    long long s1 = (kSuperRows == 1 ? b1 : floor_div2(b1)) - lo1, s2 = (kSuperCols == 1 ? b2 : floor_div2(b2)) - lo2;
-    key[x] = (int)(s1 * n2s + s2);
+    const long long b1 = (long long)std::ceil(u[2 * x] - 0.5 * taps);
+    const long long b2 = (long long)std::ceil(u[2 * x + 1] - 0.5 * taps);
+    b1v[x] = (int)b1;
+    b2v[x] = (int)b2;
+    const long long maj = (run_cols ? b1 : b2) - lo, mn = (run_cols ? b2 : b1) - lo;
+    key[x] = (int)(maj * nmin + mn);
   }
+  const long long nkeys = nmaj * nmin;
   std::vector<long long> cnt(nkeys + 1, 0);
   for (long long x = 0; x < NN; ++x) cnt[key[x] + 1]++;
   for (long long k = 0; k < nkeys; ++k) cnt[k + 1] += cnt[k];
-  // points sorted by supercell (stable: by x within a supercell), carrying their coordinates
   std::vector<int> order(NN);
-  std::vector<double> us(2 * NN);
   {
     std::vector<long long> pos(cnt.begin(), cnt.end() - 1);
-    for (long long x = 0; x < NN; ++x) {
-      const long long p = pos[key[x]]++;
-      order[p] = (int)x;
-      us[2 * p] = u[2 * x];
-      us[2 * p + 1] = u[2 * x + 1];
-    }
+    for (long long x = 0; x < NN; ++x) order[pos[key[x]]++] = (int)x;  // stable: by x within a cell
   }
-  // supercells in serpentine order of 8 x 8 blocks, so that any run of consecutive groups
-  // (one K3 CTA chunk) has a compact footprint on the fine grid
-  const long long BS = 8;
-  const long long nb1 = (n1s + BS - 1) / BS, nb2 = (n2s + BS - 1) / BS;
-  std::vector<long long> sc;  // non-empty supercell keys in traversal order
-  sc.reserve(nkeys);
-  for (long long bb1 = 0; bb1 < nb1; ++bb1)
-    for (long long jb = 0; jb < nb2; ++jb) {
-      const long long bb2 = (bb1 % 2 == 0) ? jb : nb2 - 1 - jb;
-      for (long long s1 = bb1 * BS; s1 < std::min(n1s, (bb1 + 1) * BS); ++s1)
-        for (long long s2 = bb2 * BS; s2 < std::min(n2s, (bb2 + 1) * BS); ++s2) {
-          const long long k = s1 * n2s + s2;
-          if (cnt[k + 1] > cnt[k]) sc.push_back(k);
-        }
+  // greedy runs -> groups (first point index into `order`, count)
+  std::vector<long long> gstart;
+  std::vector<int> gcount;
+  gstart.reserve(NN / P + 16);
+  gcount.reserve(NN / P + 16);
+  for (long long p = 0; p < NN;) {
+    const int x0 = order[p];
+    const int maj0 = run_cols ? b1v[x0] : b2v[x0], mn0 = run_cols ? b2v[x0] : b1v[x0];
+    long long e = p + 1;
+    while (e < NN && e - p < P) {
+      const int x = order[e];
+      const int maj = run_cols ? b1v[x] : b2v[x], mn = run_cols ? b2v[x] : b1v[x];
+      if (maj != maj0 || mn > mn0 + 1) break;
+      ++e;
     }
-  const long long nsc = (long long)sc.size();
-  std::vector<long long> goff(nsc + 1, 0);  // first group of each supercell
-  for (long long i = 0; i < nsc; ++i) goff[i + 1] = goff[i] + (cnt[sc[i] + 1] - cnt[sc[i]] + P - 1) / P;
-  const long long G = goff[nsc];
+    gstart.push_back(p);
+    gcount.push_back((int)(e - p));
+    p = e;
+  }
+  const long long G = (long long)gstart.size();
+  // serpentine 16 x 16-cell blocks of anchors
+  const long long BS = 16;
+  std::vector<std::pair<long long, long long>> gk(G);
+  const long long nbc = (std::max(nb1, nb2) + BS - 1) / BS + 2;
+#pragma omp parallel for schedule(static)
+  for (long long g = 0; g < G; ++g) {
+    const int x0 = order[gstart[g]];
+    const long long a1 = b1v[x0] - lo, a2 = b2v[x0] - lo;
+    const long long br = a1 / BS, bcr = a2 / BS;
+    const long long bc = (br % 2 == 0) ? bcr : nbc - 1 - bcr;
+    // row-major inside a block for both window shapes: consecutive groups (a warp's lanes) sit at
+    // consecutive anchor columns, so their window loads hit consecutive shared-memory words
+    const long long inner = (a1 % BS) * BS + (a2 % BS);
+    gk[g] = {(br * nbc + bc) * BS * BS + inner, g};
+  }
+  std::sort(gk.begin(), gk.end());
   anchor.assign(2 * G, 0);
   slot_x.assign((size_t)P * G, -1);
   off.assign((size_t)2 * P * G, 0.5 * taps);
-#pragma omp parallel for schedule(dynamic, 512)
-  for (long long i = 0; i < nsc; ++i) {
-    const long long k = sc[i], s1 = k / n2s, s2 = k - s1 * n2s;
-    const int a1 = (int)(kSuperRows * (s1 + lo1)), a2 = (int)(kSuperCols * (s2 + lo2));
-    const long long b = cnt[k], e = cnt[k + 1];
-    long long g = goff[i];
-    for (long long p = b; p < e; p += P, ++g) {
-      anchor[2 * g] = a1;
-      anchor[2 * g + 1] = a2;
-      for (int j = 0; j < P && p + j < e; ++j) {
-        const long long sl = g * P + j;
-        slot_x[sl] = order[p + j];
-        off[2 * sl] = us[2 * (p + j)] - a1;
-        off[2 * sl + 1] = us[2 * (p + j) + 1] - a2;
-      }
+#pragma omp parallel for schedule(static)
+  for (long long i = 0; i < G; ++i) {
+    const long long g = gk[i].second;
+    const long long p = gstart[g];
+    const int x0 = order[p];
+    const int a1 = b1v[x0], a2 = b2v[x0];
+    // anchor = the window's first fine cell: the smallest base on each axis among the members
+    int m1 = a1, m2 = a2;
+    for (int j = 0; j < gcount[g]; ++j) {
+      const int x = order[p + j];
+      m1 = std::min(m1, b1v[x]);
+      m2 = std::min(m2, b2v[x]);
+    }
+    anchor[2 * i] = m1;
+    anchor[2 * i + 1] = m2;
+    for (int j = 0; j < gcount[g]; ++j) {
+      const int x = order[p + j];
+      const long long sl = i * P + j;
+      slot_x[sl] = x;
+      off[2 * sl] = u[2 * x] - m1;
+      off[2 * sl + 1] = u[2 * x + 1] - m2;
     }
   }
 }
 
 // K3 chunks: runs of at most `block` consecutive groups whose windows' bounding box
 // has at most `cap` cells.  Per chunk: {first group, row origin, column origin, rows,
-// columns (even), groups}; returns the largest rows*cols.
-// Tile rows have an even length (16-byte aligned complex64 window rows).  Padding the stride
-// against bank conflicts (odd / 2 mod 4 lengths) was measured: no gain (c128 K3 18.2 vs 17.6 ms).
-#ifndef FIO_TILE_ALIGN_C64
-#define FIO_TILE_ALIGN_C64 2
-#endif
-#ifndef FIO_TILE_ALIGN_C128
-#define FIO_TILE_ALIGN_C128 2
-#endif
+// columns, groups}; returns the largest rows*cols.
+// Tile rows are an odd number of 16-byte units long (complex128: odd columns; complex64: columns
+// = 2 mod 4): lanes whose windows start on consecutive tile rows then hit distinct shared-memory
+// banks.
 static inline int pad_tile_cols(int nc, int elem_bytes) {
-  const int a = elem_bytes == 8 ? FIO_TILE_ALIGN_C64 : FIO_TILE_ALIGN_C128;
-  return (nc + a - 1) / a * a;
+  if (elem_bytes == 16) return nc | 1;
+  nc = (nc + 1) & ~1;                // even: 16-byte copy units
+  return (nc % 4 == 0) ? nc + 2 : nc;
 }
+
+// complex64 tile rows are copied in 16-byte units: the column origin is rounded down to even
+static inline int tile_col0(int clo, int elem_bytes) { return elem_bytes == 8 ? (clo & ~1) : clo; }
 
 long long chunk_boxes(const std::vector<int>& anchor, int block, int win_rows, int win_cols, long long cap,
                       std::vector<int>& box, int elem_bytes) {
@@ -376,11 +398,12 @@ long long chunk_boxes(const std::vector<int>& anchor, int block, int win_rows, i
       const int r = anchor[2 * c1], c = anchor[2 * c1 + 1];
       const int nrlo = std::min(rlo, r), nrhi = std::max(rhi, r), nclo = std::min(clo, c), nchi = std::max(chi, c);
       const long long nr = nrhi - nrlo + win_rows;
-      const long long nc = pad_tile_cols(nchi - nclo + win_cols, elem_bytes);
+      const long long nc = pad_tile_cols(nchi - tile_col0(nclo, elem_bytes) + win_cols, elem_bytes);
       if (nr * nc > cap) break;
       rlo = nrlo; rhi = nrhi; clo = nclo; chi = nchi;
       ++c1;
     }
+    clo = tile_col0(clo, elem_bytes);
     const int nr = rhi - rlo + win_rows;
     const int nc = pad_tile_cols(chi - clo + win_cols, elem_bytes);
     box.push_back((int)c0);
@@ -485,6 +508,62 @@ void jacobi_svd(int m, int n, std::vector<cplx>& A, std::vector<cplx>& V, std::v
     s2[k] = sigma[ord[k]];
   }
   A.swap(A2); V.swap(V2); sigma.swap(s2);
+}
+
+// Upper Cholesky factor of a Hermitian positive definite n x n column-major matrix: G = R^H R.
+// G is overwritten by R (lower part zeroed).  Returns false on a non-positive pivot.
+bool cholesky_upper(int n, std::vector<cplx>& G) {
+  for (int j = 0; j < n; ++j) {
+    double d = G[j + (size_t)j * n].re;
+    for (int k = 0; k < j; ++k) {
+      const cplx r = G[k + (size_t)j * n];
+      d -= r.re * r.re + r.im * r.im;
+    }
+    if (!(d > 0.0)) return false;
+    d = std::sqrt(d);
+    G[j + (size_t)j * n] = {d, 0.0};
+    for (int i = j + 1; i < n; ++i) {
+      cplx acc = G[j + (size_t)i * n];  // G(j, i)
+      for (int k = 0; k < j; ++k) {    // - sum_k conj(R(k, j)) R(k, i)
+        const cplx a = G[k + (size_t)j * n], b = G[k + (size_t)i * n];
+        acc.re -= a.re * b.re + a.im * b.im;
+        acc.im -= a.re * b.im - a.im * b.re;
+      }
+      G[j + (size_t)i * n] = {acc.re / d, acc.im / d};
+    }
+    for (int i = j + 1; i < n; ++i) G[i + (size_t)j * n] = {0.0, 0.0};
+  }
+  return true;
+}
+
+// X = R^{-1} for an upper triangular n x n column-major R (back substitution, column by column).
+void upper_inverse(int n, const std::vector<cplx>& R, std::vector<cplx>& X) {
+  X.assign((size_t)n * n, cplx{0, 0});
+  for (int c = 0; c < n; ++c) {
+    for (int i = c; i >= 0; --i) {
+      cplx acc = {i == c ? 1.0 : 0.0, 0.0};
+      for (int k = i + 1; k <= c; ++k) acc = {acc.re - cmul(R[i + (size_t)k * n], X[k + (size_t)c * n]).re,
+                                              acc.im - cmul(R[i + (size_t)k * n], X[k + (size_t)c * n]).im};
+      const cplx d = R[i + (size_t)i * n];
+      const double den = d.re * d.re + d.im * d.im;
+      X[i + (size_t)c * n] = {(acc.re * d.re + acc.im * d.im) / den, (acc.im * d.re - acc.re * d.im) / den};
+    }
+  }
+}
+
+// C = A B for n x n column-major matrices (small, host).
+void small_matmul(int n, const std::vector<cplx>& A, const std::vector<cplx>& B, std::vector<cplx>& C) {
+  C.assign((size_t)n * n, cplx{0, 0});
+  for (int j = 0; j < n; ++j)
+    for (int k = 0; k < n; ++k) {
+      const cplx b = B[k + (size_t)j * n];
+      if (b.re == 0.0 && b.im == 0.0) continue;
+      for (int i = 0; i < n; ++i) {
+        const cplx t = cmul(A[i + (size_t)k * n], b);
+        C[i + (size_t)j * n].re += t.re;
+        C[i + (size_t)j * n].im += t.im;
+      }
+    }
 }
 
 std::vector<int> pivoted_columns(int m, int n, std::vector<cplx>& B, int k) {

@@ -8,53 +8,58 @@
 
 #include "../../include/fio.h"
 
+#ifdef __CUDACC__
+#define FIO_HD_EARLY __host__ __device__
+#else
+#define FIO_HD_EARLY
+#endif
+
 namespace fio {
 
 constexpr int kMaxRadixStages = 24;
-constexpr int kMaxTaps = 10;
+constexpr int kMaxTaps = 12;  // up to eps ~ 1e-11 (reading R10)
+// K3 (interpolation + alpha epilogue).  One thread owns a group of up to P
+// points whose w x w tap windows all lie inside one window of the fine grid, loads each window value
+// once per term from shared memory and applies it to all P points (register reuse P: the shared ->
+// register path, 128 B/clk/SM, is K3's binding on-chip resource).
 #ifndef FIO_K3_P64
-#define FIO_K3_P64 4
+#define FIO_K3_P64 8
 #endif
-constexpr int kGroupPC64 = FIO_K3_P64;   // points per K3 group, complex64
-constexpr int kGroupPC128 = 4;  // complex128 (register bound)
-inline int group_p(bool c64) { return c64 ? kGroupPC64 : kGroupPC128; }
+#ifndef FIO_K3_P128
+#define FIO_K3_P128 8
+#endif
+#ifndef FIO_K3_BIGTAPS
+#define FIO_K3_BIGTAPS 8  // above this many taps the column weights of P points no longer fit: P = 4
+#endif
+constexpr int kGroupPC64 = FIO_K3_P64;    // points per K3 group, complex64
+constexpr int kGroupPC128 = FIO_K3_P128;  // complex128
+FIO_HD_EARLY constexpr int group_p(bool c64, int taps) {
+  return taps > FIO_K3_BIGTAPS ? 4 : (c64 ? kGroupPC64 : kGroupPC128);
+}
 #ifndef FIO_K3_BLOCK64
-#define FIO_K3_BLOCK64 64  // measured (N=1024, K3 ms): 256x2 CTAs/SM 2.655, 128x4 2.484, 64x8 2.441, 32x16 2.447
+#define FIO_K3_BLOCK64 64
 #endif
+#ifndef FIO_K3_BLOCK128
+#define FIO_K3_BLOCK128 64
+#endif
+constexpr int kK3BlockC64 = FIO_K3_BLOCK64;    // K3 threads per CTA (= groups per chunk), complex64
+constexpr int kK3BlockC128 = FIO_K3_BLOCK128;  // complex128
 #ifndef FIO_K3_CAP64
 #define FIO_K3_CAP64 512
 #endif
-constexpr int kK3BlockC64 = FIO_K3_BLOCK64;   // K3 threads per CTA (= groups per chunk), complex64
-#ifndef FIO_K3_BLOCK128
-#define FIO_K3_BLOCK128 64  // measured (N=1024, K3 ms): 128x2 CTAs/SM 11.95, 64x4 11.11, 32x8 11.42
-#endif
-constexpr int kK3BlockC128 = FIO_K3_BLOCK128;  // complex128
-constexpr int kK3Stages = 3;       // cp.async pipeline depth of K3 (fine-grid tiles + alpha')
-constexpr int kK3TileCapC64 = FIO_K3_CAP64;   // max cells of a K3 chunk footprint, complex64
 #ifndef FIO_K3_CAP128
 #define FIO_K3_CAP128 512
 #endif
-constexpr int kK3TileCapC128 = FIO_K3_CAP128;  // complex128
-constexpr int kHalo = 8;
-// K3 supercell shape: super_rows x 2 base cells.  1 groups points with the same base row (window
-// w rows x (w+1) columns); 2 gives (w+1) x (w+1) windows (rounded up to even rows).  Measured on
-// B200: 1 is slightly faster for complex64 (3.64 vs 3.68 ms), 2 clearly faster for complex128
-// (17.6 vs 20.0 ms) at N = 1024.
-#ifndef FIO_K3_SR128
-#define FIO_K3_SR128 2
-#endif
-#ifndef FIO_K3_SC128
-#define FIO_K3_SC128 1  // measured: 2x1 supercells (8x7 windows) K3 11.95 ms vs 2x2 12.21, 1x1 13.05 (c128, N=1024)
-#endif
-#ifndef FIO_K3_SR64
-#define FIO_K3_SR64 1
-#endif
-constexpr int kSuperRowsC64 = FIO_K3_SR64;
-constexpr int kSuperRowsC128 = FIO_K3_SR128;
-// supercell columns: 2 (windows w+1 wide) or 1 (complex128 only: points share their base column,
-// windows exactly w wide; complex64 needs even anchors for 16-byte window rows)
-constexpr int kSuperColsC64 = 2;
-constexpr int kSuperColsC128 = FIO_K3_SC128;
+constexpr int kK3Stages = 3;                    // cp.async pipeline depth of K3 (fine-grid tiles + alpha')
+constexpr int kK3TileCapC64 = FIO_K3_CAP64;     // max cells of a K3 chunk footprint, complex64
+constexpr int kK3TileCapC128 = FIO_K3_CAP128;   // complex128
+constexpr int kHalo = 8;  // periodic column halo on each side of a fine-grid row (K2 writes, K3 reads)
+// Window shape: a group's points share the base row and lie within two base columns (complex64:
+// w rows x (w+1) columns), or share the base column and lie within two base rows (complex128:
+// (w+1) rows x w columns).  Row weights are kept per point in shared memory, column weights in
+// registers, so the register cost per point is the column count.
+constexpr int kSuperRowsC64 = 1, kSuperColsC64 = 2;
+constexpr int kSuperRowsC128 = 2, kSuperColsC128 = 1;
 #ifdef __CUDACC__
 #define FIO_HD __host__ __device__
 #else
@@ -62,10 +67,8 @@ constexpr int kSuperColsC128 = FIO_K3_SC128;
 #endif
 FIO_HD constexpr int super_rows(bool c64) { return c64 ? kSuperRowsC64 : kSuperRowsC128; }
 FIO_HD constexpr int super_cols(bool c64) { return c64 ? kSuperColsC64 : kSuperColsC128; }
-FIO_HD constexpr int k3_window_rows(int taps, bool c64) {
-  return super_rows(c64) == 1 ? taps : ((taps + 2) & ~1);
-}
-FIO_HD constexpr int k3_window_cols(int taps, bool c64) { return super_cols(c64) == 1 ? taps : taps + 1; }    // periodic column halo on each side of a fine-grid row (K2 writes, K3 reads)
+FIO_HD constexpr int k3_window_rows(int taps, bool c64) { return taps + super_rows(c64) - 1; }
+FIO_HD constexpr int k3_window_cols(int taps, bool c64) { return taps + super_cols(c64) - 1; }
 
 // Division by a runtime constant d via multiply-high (Granlund-Montgomery), exact for
 // numerators n < 2^31: q = (umulhi(m, n) + n) >> l.
@@ -151,6 +154,12 @@ struct WedgeGeom {
 // cell is b and fractional offset s = u - b in (w/2 - 1, w/2] has weight
 // phi(s - j) = sum_m c[j][m] x^m, x = 2 (s - w/2) + 1 in (-1, 1].
 constexpr int kPolyMaxDeg = 20;
+// Degree of the K3 kernel polynomial for w taps (fixed at compile time: one unrolled Horner per
+// axis).  With the default beta = 2.3 w it meets the fit tolerance 2 e^{-beta}: w <= 5: 6, 6-7: 7,
+// 8-9: 8, 10: 9, 11: 10, 12: 11 (measured by es_poly_fit).
+FIO_HD_EARLY constexpr int k3_poly_deg(int taps) {
+  return taps <= 5 ? 6 : taps <= 7 ? 7 : taps <= 9 ? 8 : taps == 10 ? 9 : taps == 11 ? 10 : 11;
+}
 struct EsPoly {
   int deg;
   double c[kMaxTaps][kPolyMaxDeg + 1];
@@ -169,8 +178,8 @@ std::vector<int8_t> radix_plan(int L);
 double es_kernel(double z, int w, double beta);
 double es_fourier(double s, int w, double beta);  // psi(s) = int phi(v) cos(2 pi s v) dv
 int taps_for_eps(double eps);
-// Fit EsPoly for (w, beta) to absolute accuracy tol (degree chosen <= kPolyMaxDeg); returns max error.
-double es_poly_fit(int w, double beta, double tol, EsPoly& out);
+// Fit EsPoly for (w, beta) at degree k3_poly_deg(w) (Chebyshev interpolation); returns the max error.
+double es_poly_fit(int w, double beta, EsPoly& out);
 void lpt_assign(int W, const double* cost, int nranks, int* owner);
 
 // Group the output points of one wedge for K3 (see InterpWedge).  u: 2*NN doubles
@@ -190,6 +199,12 @@ struct cplx {
 // (m >= n): on return A holds U*Sigma (columns), V (n x n column-major) and
 // sigma (n), sorted descending.
 void jacobi_svd(int m, int n, std::vector<cplx>& A, std::vector<cplx>& V, std::vector<double>& sigma);
+
+// Small dense helpers of the high-accuracy separation (shifted CholeskyQR3, fio_api.cu):
+// G = R^H R (false if not positive definite; G overwritten by R), X = R^{-1}, C = A B.
+bool cholesky_upper(int n, std::vector<cplx>& G);
+void upper_inverse(int n, const std::vector<cplx>& R, std::vector<cplx>& X);
+void small_matmul(int n, const std::vector<cplx>& A, const std::vector<cplx>& B, std::vector<cplx>& C);
 
 // Column-pivoted modified Gram-Schmidt on the m x n column-major matrix B (destroyed);
 // returns up to k pivot column indices in order.

@@ -1016,20 +1016,6 @@ __global__ void __launch_bounds__(FIO_K2_THREADS) k_colpass(const WedgeDev* __re
 }
 
 // ------------------------------------------------------------------ K3: interpolation + alpha epilogue
-template <typename Rt>
-__device__ __forceinline__ Rt es_weight(Rt z, Rt inv_half_w, Rt beta) {
-  Rt t = z * inv_half_w;
-  Rt s = (Rt)1 - t * t;
-  return s > (Rt)0 ? exp(beta * (sqrt(s) - (Rt)1)) : (Rt)0;
-}
-template <>
-__device__ __forceinline__ float es_weight<float>(float z, float inv_half_w, float beta) {
-  float t = z * inv_half_w;
-  float s = 1.f - t * t;
-  // s * rsqrt(s) (MUFU.RSQ) and ex2.approx: ~1e-7 relative, far below the c64 NUFFT error
-  return s > 0.f ? __expf(beta * (s * rsqrtf(s) - 1.f)) : 0.f;
-}
-
 // c + a * (b.x, b.y) as one packed FFMA2 (sm_100 fma.rn.f32x2)
 __device__ __forceinline__ float2 ffma2(float a, float2 b, float2 c) {
   float2 r;
@@ -1047,140 +1033,89 @@ __device__ __forceinline__ double2 cfma_real(double a, double2 b, double2 c) {
   return make_double2(fma(a, b.x, c.x), fma(a, b.y, c.y));
 }
 
-// Weights of the window positions i = 0..NW-1 for a point at offset o = u - anchor
-// (o in (w/2 - 1, w/2 + 1]) from the plan's piecewise polynomials (EsPoly): the point's base
-// b = anchor + d, d = ceil(o - w/2) in {0, 1}, s = o - d, x = 2 (s - w/2) + 1, taps j = i - d.
-// float: FP32 coefficients, two taps per packed FFMA2 Horner step.  double: FP64 Horner.
-template <int TAPS, int NW>
-__device__ __forceinline__ void window_weights_f32(float o, const EsPoly& poly, float (&w)[NW]) {
+// Interpolation weights of P points along one axis: w[k][i] for the window
+// positions i < NW of the point at offset o_k = u_k - anchor.  The point's first tap sits at window
+// position d_k = [o_k > TAPS/2] (always 0 when NW == TAPS: the axis has no run), tap j at distance
+// s_k - j, s_k = o_k - d_k, with phi(s_k - j) = sum_{m <= DEG} c[j][m] x_k^m,
+// x_k = 2 (s_k - TAPS/2) + 1 (the plan's piecewise polynomial of the ES kernel, EsPoly, fitted at
+// exactly degree DEG = k3_poly_deg(TAPS)).  Coefficient-outer Horner: each coefficient is read once
+// per call (uniform) and applied to all P points.  FP32 (two taps per packed FFMA2) for complex64,
+// FP64 for complex128; the adjoint calls the same functions, so it stays the exact transpose.
+template <int TAPS, int NW, int P>
+__device__ __forceinline__ void axis_weights(const float (&o)[P], const EsPoly& poly, float (&w)[P][NW]) {
   constexpr int NP = (TAPS + 1) / 2;  // tap pairs
-  const int d = (o > 0.5f * TAPS) ? 1 : 0;
-  const float x = 2.f * (o - (float)d - 0.5f * TAPS) + 1.f;
-  float2 qv[NP];
-  constexpr int kDegF = 8;  // coefficients above the plan's degree are zero: fixed-length, unrolled Horner
-  if (poly.deg <= kDegF) {
+  constexpr int DEG = k3_poly_deg(TAPS);
+  float x[P];
+  bool d[P];
 #pragma unroll
-    for (int p = 0; p < NP; ++p) qv[p] = make_float2(poly.cf[kDegF][2 * p], poly.cf[kDegF][2 * p + 1]);
-#pragma unroll
-    for (int m = kDegF - 1; m >= 0; --m) {
-#pragma unroll
-      for (int p = 0; p < NP; ++p) qv[p] = ffma2_v(qv[p], x, make_float2(poly.cf[m][2 * p], poly.cf[m][2 * p + 1]));
-    }
-  } else {
-    const int deg = poly.deg;
-#pragma unroll
-    for (int p = 0; p < NP; ++p) qv[p] = make_float2(poly.cf[deg][2 * p], poly.cf[deg][2 * p + 1]);
-    for (int m = deg - 1; m >= 0; --m) {
-#pragma unroll
-      for (int p = 0; p < NP; ++p) qv[p] = ffma2_v(qv[p], x, make_float2(poly.cf[m][2 * p], poly.cf[m][2 * p + 1]));
-    }
+  for (int k = 0; k < P; ++k) {
+    d[k] = NW > TAPS && o[k] > 0.5f * TAPS;
+    x[k] = 2.f * (o[k] - (d[k] ? 1.f : 0.f) - 0.5f * TAPS) + 1.f;
   }
-  float q[2 * NP];
+  float2 qv[P][NP];
 #pragma unroll
   for (int p = 0; p < NP; ++p) {
-    q[2 * p] = qv[p].x;
-    q[2 * p + 1] = qv[p].y;
+    const float2 c = make_float2(poly.cf[DEG][2 * p], poly.cf[DEG][2 * p + 1]);
+#pragma unroll
+    for (int k = 0; k < P; ++k) qv[k][p] = c;
   }
 #pragma unroll
-  for (int i = 0; i < NW; ++i) {
-    const float a = (i < TAPS) ? q[i < TAPS ? i : 0] : 0.f;
-    const float b = (i >= 1 && i - 1 < TAPS) ? q[(i >= 1 && i - 1 < TAPS) ? i - 1 : 0] : 0.f;
-    w[i] = d ? b : a;
-  }
-}
-
-template <typename Rt, int TAPS, int NW>
-__device__ __forceinline__ void window_weights(Rt o, Rt inv_half_w, Rt beta, const EsPoly& poly, Rt (&w)[NW]) {
-  (void)inv_half_w;
-  (void)beta;
-  if constexpr (sizeof(Rt) == 4) {
-    window_weights_f32<TAPS, NW>(o, poly, w);
-  } else {
-    const int d = (o > (Rt)(0.5 * TAPS)) ? 1 : 0;
-    const Rt x = (Rt)2 * (o - (Rt)d - (Rt)(0.5 * TAPS)) + (Rt)1;
-    Rt qv[TAPS];
-    constexpr int kDegD = 8;  // as in window_weights_f32: zero coefficients above the plan's degree
-    if (poly.deg <= kDegD) {
+  for (int m = DEG - 1; m >= 0; --m) {
 #pragma unroll
-      for (int j = 0; j < TAPS; ++j) qv[j] = (Rt)poly.c[j][kDegD];
+    for (int p = 0; p < NP; ++p) {
+      const float2 c = make_float2(poly.cf[m][2 * p], poly.cf[m][2 * p + 1]);
 #pragma unroll
-      for (int m = kDegD - 1; m >= 0; --m) {
-#pragma unroll
-        for (int j = 0; j < TAPS; ++j) qv[j] = fma(qv[j], x, (Rt)poly.c[j][m]);
-      }
-    } else {
-#pragma unroll
-      for (int j = 0; j < TAPS; ++j) qv[j] = (Rt)poly.c[j][poly.deg];
-      for (int m = poly.deg - 1; m >= 0; --m) {
-#pragma unroll
-        for (int j = 0; j < TAPS; ++j) qv[j] = fma(qv[j], x, (Rt)poly.c[j][m]);
-      }
+      for (int k = 0; k < P; ++k) qv[k][p] = ffma2_v(qv[k][p], x[k], c);
     }
+  }
+#pragma unroll
+  for (int k = 0; k < P; ++k) {
 #pragma unroll
     for (int i = 0; i < NW; ++i) {
-      Rt a = (i < TAPS) ? qv[i < TAPS ? i : 0] : (Rt)0;
-      Rt b = (i >= 1 && i - 1 < TAPS) ? qv[(i >= 1 && i - 1 < TAPS) ? i - 1 : 0] : (Rt)0;
-      w[i] = d ? b : a;
+      const float a = i < TAPS ? (i % 2 ? qv[k][(i < TAPS ? i : 0) / 2].y : qv[k][(i < TAPS ? i : 0) / 2].x) : 0.f;
+      const int im = i >= 1 ? i - 1 : 0;
+      const float b = (i >= 1 && i - 1 < TAPS) ? (im % 2 ? qv[k][(i - 1 < TAPS ? im : 0) / 2].y
+                                                         : qv[k][(i - 1 < TAPS ? im : 0) / 2].x)
+                                               : 0.f;
+      w[k][i] = d[k] ? b : a;
     }
   }
 }
 
-// Row weights phi1 (kept in FP32 for both dtypes): FP32 polynomial, as float.
-template <typename Rt, int TAPS, int NW>
-__device__ __forceinline__ void row_weights_f32(Rt o, const EsPoly& poly, float (&w)[NW]) {
-  window_weights_f32<TAPS, NW>((float)o, poly, w);
-}
-
-// Window row of WIN elements from shared memory (float2 rows start 16-byte aligned:
-// anchors and tile origins are even) and the P row weights of one thread.
-template <typename T2, int WIN>
-__device__ __forceinline__ void load_row(const T2* p, T2 (&v)[WIN]) {
-  if constexpr (sizeof(T2) == 8) {
-    const float4* q = reinterpret_cast<const float4*>(p);
+template <int TAPS, int NW, int P>
+__device__ __forceinline__ void axis_weights(const double (&o)[P], const EsPoly& poly, double (&w)[P][NW]) {
+  constexpr int DEG = k3_poly_deg(TAPS);
+  double x[P];
+  bool d[P];
 #pragma unroll
-    for (int j = 0; j < WIN / 2; ++j) {
-      float4 a = q[j];
-      v[2 * j] = mk<T2>(a.x, a.y);
-      v[2 * j + 1] = mk<T2>(a.z, a.w);
-    }
-    if constexpr (WIN % 2) v[WIN - 1] = p[WIN - 1];
-  } else {
-#pragma unroll
-    for (int j = 0; j < WIN; ++j) v[j] = p[j];
+  for (int k = 0; k < P; ++k) {
+    d[k] = NW > TAPS && o[k] > 0.5 * TAPS;
+    x[k] = 2.0 * (o[k] - (d[k] ? 1.0 : 0.0) - 0.5 * TAPS) + 1.0;
   }
-}
-template <typename Rt, int P>
-__device__ __forceinline__ void load_p1(const Rt* p, Rt (&w)[P]) {
-  if constexpr (sizeof(Rt) == 4 && P % 4 == 0) {
+  double qv[P][TAPS];
 #pragma unroll
-    for (int k = 0; k < P; k += 4) {
-      float4 a = *reinterpret_cast<const float4*>(p + k);
-      w[k] = a.x; w[k + 1] = a.y; w[k + 2] = a.z; w[k + 3] = a.w;
-    }
-  } else if constexpr (sizeof(Rt) == 8 && P % 2 == 0) {
+  for (int j = 0; j < TAPS; ++j) {
+    const double c = poly.c[j][DEG];
 #pragma unroll
-    for (int k = 0; k < P; k += 2) {
-      double2 a = *reinterpret_cast<const double2*>(p + k);
-      w[k] = a.x; w[k + 1] = a.y;
-    }
-  } else {
-#pragma unroll
-    for (int k = 0; k < P; ++k) w[k] = p[k];
+    for (int k = 0; k < P; ++k) qv[k][j] = c;
   }
-}
-
-// P FP32 row weights (16-byte vector loads), widened to the compute type
-template <typename Rt, int P>
-__device__ __forceinline__ void load_p1_f(const float* p, Rt (&w)[P]) {
-  if constexpr (P % 4 == 0) {
 #pragma unroll
-    for (int k = 0; k < P; k += 4) {
-      float4 a = *reinterpret_cast<const float4*>(p + k);
-      w[k] = (Rt)a.x; w[k + 1] = (Rt)a.y; w[k + 2] = (Rt)a.z; w[k + 3] = (Rt)a.w;
+  for (int m = DEG - 1; m >= 0; --m) {
+#pragma unroll
+    for (int j = 0; j < TAPS; ++j) {
+      const double c = poly.c[j][m];
+#pragma unroll
+      for (int k = 0; k < P; ++k) qv[k][j] = fma(qv[k][j], x[k], c);
     }
-  } else {
+  }
 #pragma unroll
-    for (int k = 0; k < P; ++k) w[k] = (Rt)p[k];
+  for (int k = 0; k < P; ++k) {
+#pragma unroll
+    for (int i = 0; i < NW; ++i) {
+      const double a = i < TAPS ? qv[k][i < TAPS ? i : 0] : 0.0;
+      const double b = (i >= 1 && i - 1 < TAPS) ? qv[k][(i >= 1 && i - 1 < TAPS) ? i - 1 : 0] : 0.0;
+      w[k][i] = d[k] ? b : a;
+    }
   }
 }
 
@@ -1188,256 +1123,210 @@ template <typename T2> struct OffT;
 template <> struct OffT<float2> { using type = float2; };
 template <> struct OffT<double2> { using type = double2; };
 
-// One thread = one group of P points sharing a (TAPS+1)^2 window of each fine grid
-// G_lt.  For every term t: F_k = sum_i phi1_k[i] sum_j phi2_k[j] G_lt[a1+i][a2+j]
-// (PAPER.md:1305-1311, 1357-1363), acc_k += alpha'_lt(x_k) F_k.
-// The window is loaded once per (group, t) and reused by the P points.
-// Persistent grid-stride loop over the wedge's groups; Lf[x_k] is written (first
-// wedge, + the DC term of rank 0) or read-modify-written: each point occurs in
-// exactly one group per wedge, so one launch per wedge is race-free and the
-// summation order over wedges is fixed (deterministic).
-template <typename T2> struct GroupP;
-template <> struct GroupP<float2> { static constexpr int value = kGroupPC64; };
-template <> struct GroupP<double2> { static constexpr int value = kGroupPC128; };
+template <typename T2, int TAPS> struct GroupP { static constexpr int value = group_p(sizeof(T2) == 8, TAPS); };
 
-#ifndef FIO_K3_SPLIT
-#define FIO_K3_SPLIT 0
-#endif
-#ifndef FIO_K3_MINB128
-#define FIO_K3_MINB128 4
-#endif
+// K3 launch shape: threads per CTA (= groups per chunk) and the CTAs per SM the registers allow
 template <typename T2> struct K3Cfg;
 template <> struct K3Cfg<float2> {
 #ifndef FIO_K3_MINB64
-#define FIO_K3_MINB64 8
-#endif
-#ifndef FIO_K3_P1REG64
-#define FIO_K3_P1REG64 false
+#define FIO_K3_MINB64 5
 #endif
   static constexpr int BLOCK = kK3BlockC64, MINB = FIO_K3_MINB64;
-  static constexpr bool P1REG = FIO_K3_P1REG64;  // row weights in registers measured slower (4.28 vs 3.69 ms)
-#ifndef FIO_K3_AREG64
-#define FIO_K3_AREG64 false
-#endif
-  static constexpr bool AREG = FIO_K3_AREG64;
-  static constexpr bool P1D = false;
-  static constexpr bool LEAN = false;   // lean-register variant measured slower (4.19 vs 3.68 ms)
-  static constexpr int MAXC = kK3TileCapC64 / 2 / kK3BlockC64;  // 16-B tile-copy slots per thread
-  static_assert(kK3TileCapC64 % (2 * kK3BlockC64) == 0, "tile cap must be a multiple of 2 BLOCK (copy slots)");
 };
 template <> struct K3Cfg<double2> {
-  static constexpr int BLOCK = kK3BlockC128, MINB = FIO_K3_MINB128;
-  static constexpr bool P1REG = false;  // 64 more FP64 registers would not fit
-  static constexpr bool LEAN = false;
-  static constexpr bool AREG = false;
-#ifndef FIO_K3_P1D128
-#define FIO_K3_P1D128 false
+#ifndef FIO_K3_MINB128
+#define FIO_K3_MINB128 3
 #endif
-  static constexpr bool P1D = FIO_K3_P1D128;  // row weights as FP64 in shared memory (no F2F per use)
-  static constexpr int MAXC = kK3TileCapC128 / 1 / kK3BlockC128;
-  static_assert(kK3TileCapC128 % kK3BlockC128 == 0, "tile cap must be a multiple of BLOCK (copy slots)");
+  static constexpr int BLOCK = kK3BlockC128, MINB = FIO_K3_MINB128;
 };
 
-
-// Dynamic shared memory of K3: alpha' ring [S][BLOCK][P], phi1 [P*WINR][BLOCK], tile ring [S][tile_cap].
+// Shared memory of K3 (16-aligned sections).  Every per-thread array is stored in 16-byte units
+// with the thread index innermost -- [unit][thread][16 B] -- so a warp's vector loads hit 32
+// consecutive 16-byte units (no bank conflicts), and a thread's cp.async of its contiguous global
+// row (16-byte units in order) lands unit by unit:
+//   alpha' ring   [S][P/EPC][BLOCK] x 16 B   this thread's alpha'(t) for the S terms in flight
+//   row weights   [WINR][P/RPV][BLOCK] x 16 B  phi1 of every point (Rt: FP32 c64, FP64 c128)
+//   running sums  [P][BLOCK] T2                Lf(x_k) before this wedge (cp.async at chunk start)
+//   slots         [2][P/4][BLOCK] x 16 B       output index of every point (current, next chunk)
+//   offsets       [P/OPV][BLOCK] x 16 B        fine-grid offsets from the anchor (next chunk)
+//   anchors       [BLOCK] int2                 (next chunk)
+//   boxes         [2][8] int                   footprint box of the current and the next chunk
+//   tile ring     [S][cap] T2                  the chunk's footprint tile of G_lt per term in flight
 template <typename T2, int TAPS, int P>
-__host__ __device__ constexpr size_t k3_p1_smem() {
-  return K3Cfg<T2>::P1REG ? 0
-                          : (K3Cfg<T2>::P1D ? sizeof(T2) / 2 : sizeof(float)) * P * k3_window_rows(TAPS, sizeof(T2) == 8) *
-                                K3Cfg<T2>::BLOCK;
-}
-// prefetched per-chunk data: anchors (int2), slots (P ints), offsets (P x O2) per thread + 2 boxes
-template <typename T2, int P>
-__host__ __device__ constexpr size_t k3_meta_smem() {
-  return (size_t)K3Cfg<T2>::BLOCK * (8 + 4 * P + P * sizeof(T2)) + 64;
-}
-template <typename T2, int TAPS, int P>
-__host__ __device__ constexpr size_t k3_fixed_smem() {
-  return sizeof(T2) * kK3Stages * K3Cfg<T2>::BLOCK * P + k3_p1_smem<T2, TAPS, P>() + k3_meta_smem<T2, P>();
+struct K3Layout {
+  using Rt = typename Real<T2>::type;
+  static constexpr int BLOCK = K3Cfg<T2>::BLOCK;
+  static constexpr int WINR = k3_window_rows(TAPS, sizeof(T2) == 8);
+  static constexpr size_t al(size_t b) { return (b + 15) / 16 * 16; }
+  static constexpr size_t kRing = 0;
+  static constexpr size_t kP1 = kRing + al(sizeof(T2) * kK3Stages * BLOCK * P);
+  static constexpr size_t kLf = kP1 + al(sizeof(Rt) * WINR * BLOCK * P);
+  static constexpr size_t kSlot = kLf + al(sizeof(T2) * BLOCK * P);
+  static constexpr size_t kOff = kSlot + al(sizeof(int) * 2 * BLOCK * P);
+  static constexpr size_t kAnchor = kOff + al(sizeof(typename OffT<T2>::type) * BLOCK * P);
+  static constexpr size_t kBox = kAnchor + al(sizeof(int2) * BLOCK);
+  static constexpr size_t kFixed = kBox + al(sizeof(int) * 16);
+  static size_t bytes(long long cap) { return kFixed + sizeof(T2) * kK3Stages * (size_t)cap; }
+};
+
+// 16-byte unit u of thread t in a [unit][BLOCK] x 16 B array
+template <int BLOCK>
+__device__ __forceinline__ int unit16(int u, int t) {
+  return (u * BLOCK + t) * 16;
 }
 
-// K3: one CTA processes chunks of BLOCK consecutive groups (one group of P points per
-// thread).  For every term t the CTA stages, with cp.async, the footprint tile of the
-// chunk's windows on G_lt (rows wrap mod n1f; columns use the haloed row layout) and
-// each thread's alpha'(t) into a kK3Stages-deep ring, so global latency overlaps the
-// arithmetic of earlier terms.  Per group and term:
-//   F_k = sum_i phi1_k[i] sum_j phi2_k[j] G_lt[a1+i][a2+j]
-//   acc_k += alpha'_lt(x_k) F_k                                   (PAPER.md:1301-1302)
-// Lf[x_k] is written (first wedge, + the DC term of rank 0) or read-modify-written:
-// each point occurs in exactly one group per wedge, so one launch per wedge is
-// race-free and the summation order over wedges is fixed (deterministic).
+// K3: one CTA processes chunks of BLOCK consecutive groups (one group of up to P points per
+// thread; chunks are padded to BLOCK groups at plan time, so chunk c's groups are
+// [c BLOCK, (c+1) BLOCK)).  Per chunk the thread evaluates the interpolation weights of its points
+// once -- column weights phi2 into registers, row weights phi1 into shared memory -- and starts the
+// copy of its points' running sums Lf(x_k) into shared memory; then, for every term t, the CTA
+// stages with cp.async the chunk's footprint tile of G_lt (rows wrapped mod the fine grid, columns
+// from the haloed row layout) and each thread's alpha'(t) into a kK3Stages-deep ring, so global
+// latency overlaps the arithmetic of earlier terms.  Per group, term and window row i the thread
+// loads the row once and applies it to all P points:
+//   F_k += phi1_k[i] sum_j phi2_k[j] G_lt[a1 + i][a2 + j]
+//   acc_k += alpha'_lt(x_k) F_k                                     (PAPER.md:1301-1302)
+// The next chunk's tables (anchors, slots, offsets, box) are prefetched during the current one.
+// Lf[x_k] is written (first wedge of the stream, + the DC term of rank 0) or read-modify-written:
+// each point occurs in exactly one group per wedge, so one launch per wedge is race-free and the
+// summation order over wedges is fixed (deterministic).
 template <typename T2, int TAPS, int P>
 __global__ void __launch_bounds__(K3Cfg<T2>::BLOCK, K3Cfg<T2>::MINB)
     k_interp_groups(InterpWedge iw, const T2* __restrict__ gbase, const double2* __restrict__ a0,
-                    const T2* __restrict__ fhat, int first, int add_dc, double es_beta, EsPoly poly,
-                    T2* __restrict__ Lf) {
+                    const T2* __restrict__ fhat, int first, int add_dc, EsPoly poly, T2* __restrict__ Lf) {
   using Rt = typename Real<T2>::type;
   using O2 = typename OffT<T2>::type;
-  constexpr int WIN = k3_window_cols(TAPS, sizeof(T2) == 8);  // window columns
-  constexpr int WINR = k3_window_rows(TAPS, sizeof(T2) == 8);  // window rows (super_rows 2: even, extra row weight 0)
+  using L = K3Layout<T2, TAPS, P>;
+  constexpr bool C64 = sizeof(T2) == 8;
+  constexpr int WIN = k3_window_cols(TAPS, C64);
+  constexpr int WINR = k3_window_rows(TAPS, C64);
   constexpr int BLOCK = K3Cfg<T2>::BLOCK;
   constexpr int S = kK3Stages;
-  constexpr int ACH = P * (int)sizeof(T2) / 16;  // 16-byte alpha' chunks per (group, t)
-  constexpr int EPC = 16 / (int)sizeof(T2);      // elements per 16-byte chunk
+  constexpr int EPC = 16 / (int)sizeof(T2);  // complex elements per 16-byte unit
+  constexpr int RPV = 16 / (int)sizeof(Rt);  // row weights per 16-byte unit
+  constexpr int OPV = 16 / (int)sizeof(O2);  // offsets per 16-byte unit
+  static_assert(P % EPC == 0 && P % RPV == 0 && P % 4 == 0 && P % OPV == 0, "K3 group size");
   extern __shared__ __align__(16) unsigned char k3_smem[];
-  T2* aring = reinterpret_cast<T2*>(k3_smem);
-  // row weights phi1 in shared memory as FP32 for both dtypes: they are used once per row and
-  // point, and their own accuracy (ES polynomial, ~1.5 e^{-beta}) is below FP32 rounding anyway
-  using P1T = typename std::conditional<K3Cfg<T2>::P1D, Rt, float>::type;  // row weights in shared memory
-  P1T* p1s = reinterpret_cast<P1T*>(k3_smem + sizeof(T2) * S * BLOCK * P);
-  // per-chunk data of the NEXT chunk, prefetched with cp.async while the current chunk runs
-  // (chunks are padded to BLOCK groups at plan time: chunk c's groups are [c BLOCK, (c+1) BLOCK))
-  unsigned char* meta = k3_smem + sizeof(T2) * S * BLOCK * P + k3_p1_smem<T2, TAPS, P>();
-  int2* m_anchor = reinterpret_cast<int2*>(meta);
-  int* m_slot = reinterpret_cast<int*>(meta + 8 * BLOCK);
-  O2* m_off = reinterpret_cast<O2*>(meta + (8 + 4 * P) * BLOCK);
-  int* sbox = reinterpret_cast<int*>(meta + (8 + 4 * P + P * sizeof(T2)) * BLOCK);  // [2][8]
-  T2* tring = reinterpret_cast<T2*>(k3_smem + k3_fixed_smem<T2, TAPS, P>());
+  unsigned char* aring = k3_smem + L::kRing;
+  unsigned char* p1s = k3_smem + L::kP1;
+  T2* lfb = reinterpret_cast<T2*>(k3_smem + L::kLf);
+  unsigned char* m_slot = k3_smem + L::kSlot;
+  unsigned char* m_off = k3_smem + L::kOff;
+  int2* m_anchor = reinterpret_cast<int2*>(k3_smem + L::kAnchor);
+  int* sbox = reinterpret_cast<int*>(k3_smem + L::kBox);
+  T2* tring = reinterpret_cast<T2*>(k3_smem + L::kFixed);
+  const int tid = threadIdx.x;
   const int cap = iw.tile_cap;
-  const Rt inv_half_w = (Rt)(2.0 / TAPS);
-  const Rt beta = (Rt)es_beta;
-  const int n1f = iw.nrow, n2p = iw.ncolp, q = iw.q;  // K3 rows / haloed row length of G_lt
-  const long long gstride = (long long)n1f * n2p;
+  const int nrow = iw.nrow, n2p = iw.ncolp, q = iw.q;  // K3 rows / haloed row length of G_lt
+  const long long gstride = (long long)nrow * n2p;
   const long long nslots = (long long)iw.ngroups * P;
   const T2* __restrict__ G = gbase + iw.g_off + kHalo;
   const T2* __restrict__ alpha = reinterpret_cast<const T2*>(iw.alpha);
   const O2* __restrict__ offs = reinterpret_cast<const O2*>(iw.slot_off);
-  T2* myring = aring + threadIdx.x * P;
-  T2 f0 = mk<T2>(0, 0);
-  if (add_dc) f0 = fhat[0];
-  static_assert((4 * P) % 16 == 0 && (P * sizeof(T2)) % 16 == 0, "K3 metadata rows must be 16-byte multiples");
-  auto prefetch_meta = [&](int chn, int bslot) {
+  auto prefetch_meta = [&](int chn, int buf) {
     if (chn < iw.nchunks) {
-      const long long gn = (long long)chn * BLOCK + threadIdx.x;
-      cp_async8(m_anchor + threadIdx.x, iw.anchor + 2 * gn);
+      const long long gn = (long long)chn * BLOCK + tid;
+      cp_async8(m_anchor + tid, iw.anchor + 2 * gn);
 #pragma unroll
-      for (int c = 0; c < 4 * P / 16; ++c) cp_async16(m_slot + threadIdx.x * P + 4 * c, iw.slot_x + gn * P + 4 * c);
-      const char* so = reinterpret_cast<const char*>(offs + gn * P);
-      char* dofs = reinterpret_cast<char*>(m_off + threadIdx.x * P);
+      for (int c = 0; c < P / 4; ++c) cp_async16(m_slot + unit16<BLOCK>(buf * (P / 4) + c, tid), iw.slot_x + gn * P + 4 * c);
 #pragma unroll
-      for (int c = 0; c < (int)(P * sizeof(T2)) / 16; ++c) cp_async16(dofs + 16 * c, so + 16 * c);
-      if (threadIdx.x < 3) cp_async8(sbox + 8 * bslot + 2 * threadIdx.x, iw.box + 6 * (long long)chn + 2 * threadIdx.x);
+      for (int c = 0; c < P / OPV; ++c) cp_async16(m_off + unit16<BLOCK>(c, tid), offs + gn * P + OPV * c);
+      if (tid < 3) cp_async8(sbox + 8 * buf + 2 * tid, iw.box + 6 * (long long)chn + 2 * tid);
     }
   };
   prefetch_meta(blockIdx.x, 0);
   cp_async_commit();
   int it = 0;
   for (int ch = blockIdx.x; ch < iw.nchunks; ch += gridDim.x, ++it) {
+    const int buf = it & 1;
     cp_async_wait<0>();
-    __syncthreads();  // this chunk's prefetched data is visible; the previous chunk is done with every ring slot
-    const int* cb = sbox + 8 * (it & 1);  // first group, r_lo, c_lo, nr, nc, groups
-    const int g = ch * BLOCK + threadIdx.x;
-    const int4 bx = make_int4(cb[1], cb[2], cb[3], cb[4]);
-    const int tchunks = bx.z * (bx.w / EPC);                    // 16-byte chunks of one tile
-    const int cpr = bx.w / EPC;
-    const T2* __restrict__ al = alpha + (long long)g * P;
-    // this thread's share of a tile copy, fixed for the chunk: source offsets within G_lt
-    // (row wrapped mod n1f) and destination offsets within the tile
-    constexpr int MAXC = K3Cfg<T2>::MAXC;  // = tile_cap / EPC / BLOCK
-    constexpr bool LEAN = K3Cfg<T2>::LEAN;
-    int csrc[LEAN ? 1 : MAXC];
-    int cdst[LEAN ? 1 : MAXC];
-    int ncp = 0;
+    __syncthreads();  // this chunk's tables are visible; every thread is done with the previous chunk
+    const int* cb = sbox + 8 * buf;  // first group, row origin, column origin, rows, columns, groups
+    const int br = cb[1], bc = cb[2], bnr = cb[3], bnc = cb[4];
+    const int cpr = bnc / EPC;  // 16-byte copies per tile row
+    const int tchunks = bnr * cpr;
     const FastDiv dcpr = make_fastdiv_dev((unsigned)cpr);
-    if constexpr (!LEAN) {
+    const T2* __restrict__ al = alpha + ((long long)ch * BLOCK + tid) * P;
+    // the running sums Lf(x_k) of this thread's points, copied while the term loop runs
+    if (!first) {
 #pragma unroll
-      for (int u = 0; u < MAXC; ++u) {
-        const int idx = threadIdx.x + u * BLOCK;
-        csrc[u] = 0;
-        cdst[u] = 0;
-        if (idx < tchunks) {
-          const int rr = idx / cpr, cc = idx - rr * cpr;
-          int r = bx.x + rr;
-          r = r < 0 ? r + n1f : (r >= n1f ? r - n1f : r);
-          csrc[u] = r * n2p + bx.y + cc * EPC;
-          cdst[u] = rr * bx.w + cc * EPC;
-          ncp = u + 1;
-        }
+      for (int c = 0; c < P / 4; ++c) {
+        const int4 xv = *reinterpret_cast<const int4*>(m_slot + unit16<BLOCK>(buf * (P / 4) + c, tid));
+        const int xs4[4] = {xv.x, xv.y, xv.z, xv.w};
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+          if (xs4[u] >= 0) {
+            if constexpr (C64)
+              cp_async8(lfb + (4 * c + u) * BLOCK + tid, Lf + xs4[u]);
+            else
+              cp_async16(lfb + (4 * c + u) * BLOCK + tid, Lf + xs4[u]);
+          }
       }
     }
     // stage term t into ring slot t % S: this thread's alpha'(t) and its share of the tile
     auto issue = [&](int t, bool next_meta) {
       if (t < q) {
         const int st = t % S;
-        if constexpr (!K3Cfg<T2>::AREG) {
+        const T2* as = al + t * nslots;
 #pragma unroll
-          for (int c = 0; c < ACH; ++c)
-            cp_async16(reinterpret_cast<char*>(myring + st * BLOCK * P) + 16 * c,
-                       reinterpret_cast<const char*>(al + t * nslots) + 16 * c);
-        }
+        for (int c = 0; c < P / EPC; ++c) cp_async16(aring + unit16<BLOCK>(st * (P / EPC) + c, tid), as + EPC * c);
         const T2* __restrict__ gt = G + t * gstride;
         T2* tile = tring + st * cap;
-        if constexpr (LEAN) {
-          for (int idx = threadIdx.x; idx < tchunks; idx += BLOCK) {
-            const int rr = fdiv(idx, dcpr), cc = idx - rr * cpr;
-            int r = bx.x + rr;
-            r = r < 0 ? r + n1f : (r >= n1f ? r - n1f : r);
-            cp_async16(tile + rr * bx.w + cc * EPC, gt + (r * n2p + bx.y + cc * EPC));
-          }
-        } else {
-#pragma unroll
-          for (int u = 0; u < MAXC; ++u)
-            if (u < ncp) cp_async16(tile + cdst[u], gt + csrc[u]);
+        for (int idx = tid; idx < tchunks; idx += BLOCK) {
+          const int rr = fdiv(idx, dcpr), cc = idx - rr * cpr;
+          int r = br + rr;
+          r = r < 0 ? r + nrow : (r >= nrow ? r - nrow : r);
+          cp_async16(tile + rr * bnc + cc * EPC, gt + ((long long)r * n2p + bc + cc * EPC));
         }
       }
-      // the next chunk's data, issued once this thread has consumed its copy of the current one
-      if (next_meta) prefetch_meta(ch + gridDim.x, (it + 1) & 1);
+      // the next chunk's tables, issued once every thread has consumed the current offsets/anchors
+      if (next_meta) prefetch_meta(ch + gridDim.x, buf ^ 1);
       cp_async_commit();
     };
 #pragma unroll
     for (int st = 0; st < S - 1; ++st) issue(st, false);
-    int a1 = 0, a2 = 0;
-    int xs[P];
+    // weights of this thread's points: phi2 (columns) in registers, phi1 (rows) in shared memory
+    const int2 an = m_anchor[tid];
+    const int woff = (an.x - br) * bnc + (an.y - bc);
     Rt p2[P][WIN];
-    constexpr bool P1REG = K3Cfg<T2>::P1REG;
-    Rt p1r[P][P1REG ? WINR : 1];
-    T2 base[P];
     {
-      const int2 an = m_anchor[threadIdx.x];
-      a1 = an.x - bx.x;
-      a2 = an.y - bx.y;
-    }
+      Rt o1[P], o2[P];
 #pragma unroll
-    for (int k = 0; k < P; ++k) {
-      O2 o;
-      o.x = (Rt)(0.5 * TAPS);
-      o.y = (Rt)(0.5 * TAPS);
-      xs[k] = m_slot[threadIdx.x * P + k];
-      o = m_off[threadIdx.x * P + k];
-      float w1[WINR];
-      row_weights_f32<Rt, TAPS, WINR>(o.x, poly, w1);
-      window_weights<Rt, TAPS, WIN>(o.y, inv_half_w, beta, poly, p2[k]);
-      if constexpr (P1REG) {
-#pragma unroll
-        for (int i = 0; i < WINR; ++i) p1r[k][i] = (Rt)w1[i];
-      } else {
-#pragma unroll
-        for (int i = 0; i < WINR; ++i) p1s[(i * BLOCK + threadIdx.x) * P + k] = (P1T)w1[i];
-        // start the read of the running sum early (latency hidden by the term loop)
-        base[k] = mk<T2>(0, 0);
-        if constexpr (!K3Cfg<T2>::LEAN)
-          if (xs[k] >= 0 && !first) base[k] = Lf[xs[k]];
+      for (int c = 0; c < P / OPV; ++c) {
+        if constexpr (C64) {
+          const float4 v = *reinterpret_cast<const float4*>(m_off + unit16<BLOCK>(c, tid));
+          o1[2 * c] = v.x; o2[2 * c] = v.y; o1[2 * c + 1] = v.z; o2[2 * c + 1] = v.w;
+        } else {
+          const double2 v = *reinterpret_cast<const double2*>(m_off + unit16<BLOCK>(c, tid));
+          o1[c] = v.x; o2[c] = v.y;
+        }
       }
+      {
+        Rt w1[P][WINR];
+        axis_weights<TAPS, WINR, P>(o1, poly, w1);
+#pragma unroll
+        for (int i = 0; i < WINR; ++i)
+#pragma unroll
+          for (int c = 0; c < P / RPV; ++c) {
+            if constexpr (sizeof(Rt) == 4)
+              *reinterpret_cast<float4*>(p1s + unit16<BLOCK>(i * (P / RPV) + c, tid)) =
+                  make_float4(w1[4 * c][i], w1[4 * c + 1][i], w1[4 * c + 2][i], w1[4 * c + 3][i]);
+            else
+              *reinterpret_cast<double2*>(p1s + unit16<BLOCK>(i * (P / RPV) + c, tid)) =
+                  make_double2(w1[2 * c][i], w1[2 * c + 1][i]);
+          }
+      }
+      axis_weights<TAPS, WIN, P>(o2, poly, p2);
     }
-    if (q == 0) {  // no term loop: prefetch the next chunk's data here
-      prefetch_meta(ch + gridDim.x, (it + 1) & 1);
+    if (q == 0) {  // no term loop: fetch the next chunk's tables here
+      __syncthreads();
+      prefetch_meta(ch + gridDim.x, buf ^ 1);
       cp_async_commit();
     }
-    const int woff = a1 * bx.w + a2;
     T2 acc[P];
 #pragma unroll
     for (int k = 0; k < P; ++k) acc[k] = mk<T2>(0, 0);
-    // AREG: alpha'(t) read straight into registers one term ahead (no shared-memory ring)
-    T2 acur[K3Cfg<T2>::AREG ? P : 1], anx[K3Cfg<T2>::AREG ? P : 1];
-    if constexpr (K3Cfg<T2>::AREG) {
-#pragma unroll
-      for (int k = 0; k < P; ++k) acur[k] = q > 0 ? al[k] : mk<T2>(0, 0);
-    }
     for (int t = 0; t < q; ++t) {
-      if constexpr (K3Cfg<T2>::AREG) {
-#pragma unroll
-        for (int k = 0; k < P; ++k) anx[k] = (t + 1 < q) ? al[(t + 1) * nslots + k] : mk<T2>(0, 0);
-      }
       cp_async_wait<S - 2>();
       __syncthreads();  // term t staged by every thread; every thread is done with term t-1
       issue(t + S - 1, t == 0);
@@ -1447,72 +1336,56 @@ __global__ void __launch_bounds__(K3Cfg<T2>::BLOCK, K3Cfg<T2>::MINB)
       for (int k = 0; k < P; ++k) F[k] = mk<T2>(0, 0);
 #pragma unroll
       for (int i = 0; i < WINR; ++i) {
-        const T2* rowp = win + i * bx.w;
         T2 v[WIN];
-        load_row<T2, WIN>(rowp, v);
+#pragma unroll
+        for (int j = 0; j < WIN; ++j) v[j] = win[i * bnc + j];
         Rt w1[P];
-        if constexpr (P1REG) {
 #pragma unroll
-          for (int k = 0; k < P; ++k) w1[k] = p1r[k][i];
-        } else {
-          if constexpr (K3Cfg<T2>::P1D) {
-#pragma unroll
-            for (int k = 0; k < P; k += 2) {
-              const double2 d = *reinterpret_cast<const double2*>(p1s + (i * BLOCK + threadIdx.x) * P + k);
-              w1[k] = (Rt)d.x;
-              w1[k + 1] = (Rt)d.y;
-            }
+        for (int c = 0; c < P / RPV; ++c) {
+          if constexpr (sizeof(Rt) == 4) {
+            const float4 a = *reinterpret_cast<const float4*>(p1s + unit16<BLOCK>(i * (P / RPV) + c, tid));
+            w1[4 * c] = a.x; w1[4 * c + 1] = a.y; w1[4 * c + 2] = a.z; w1[4 * c + 3] = a.w;
           } else {
-            load_p1_f<Rt, P>(reinterpret_cast<const float*>(p1s) + (i * BLOCK + threadIdx.x) * P, w1);
+            const double2 a = *reinterpret_cast<const double2*>(p1s + unit16<BLOCK>(i * (P / RPV) + c, tid));
+            w1[2 * c] = a.x; w1[2 * c + 1] = a.y;
           }
         }
 #pragma unroll
         for (int k = 0; k < P; ++k) {
-#if FIO_K3_SPLIT
-          T2 r0 = mk<T2>(0, 0), r1 = mk<T2>(0, 0);
-#pragma unroll
-          for (int j = 0; j < WIN; j += 2) {
-            r0 = cfma_real(p2[k][j], v[j], r0);
-            if (j + 1 < WIN) r1 = cfma_real(p2[k][j + 1], v[j + 1], r1);
-          }
-          const T2 rr = mk<T2>(r0.x + r1.x, r0.y + r1.y);
-#else
           T2 rr = mk<T2>(0, 0);
 #pragma unroll
           for (int j = 0; j < WIN; ++j) rr = cfma_real(p2[k][j], v[j], rr);
-#endif
           F[k] = cfma_real(w1[k], rr, F[k]);
         }
       }
-      const T2* ring = myring + (t % S) * BLOCK * P;
+      const unsigned char* ring = aring + unit16<BLOCK>((t % S) * (P / EPC), tid);
 #pragma unroll
       for (int k = 0; k < P; ++k) {
-        T2 av;
-        if constexpr (K3Cfg<T2>::AREG) {
-          av = acur[k];
-          acur[k] = anx[k];
-        } else {
-          av = ring[k];
-        }
+        const T2 av = *reinterpret_cast<const T2*>(ring + (k / EPC) * BLOCK * 16 + (k % EPC) * sizeof(T2));
         acc[k].x = fma(av.x, F[k].x, fma(-av.y, F[k].y, acc[k].x));
         acc[k].y = fma(av.x, F[k].y, fma(av.y, F[k].x, acc[k].y));
       }
     }
+    cp_async_wait<0>();  // the running sums (in the first copy group) have landed
+    T2 f0 = mk<T2>(0, 0);
+    if (first && add_dc) f0 = fhat[0];
 #pragma unroll
-    for (int k = 0; k < P; ++k) {
-      const int x = xs[k];
-      if (x < 0) continue;
-      T2 b0;
-      if constexpr (P1REG || K3Cfg<T2>::LEAN) {
-        b0 = first ? mk<T2>(0, 0) : Lf[x];
-      } else {
-        b0 = base[k];
+    for (int c = 0; c < P / 4; ++c) {
+      const int4 xv = *reinterpret_cast<const int4*>(m_slot + unit16<BLOCK>(buf * (P / 4) + c, tid));
+      const int xs4[4] = {xv.x, xv.y, xv.z, xv.w};
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int k = 4 * c + u, x = xs4[u];
+        if (x < 0) continue;
+        T2 b0 = mk<T2>(0, 0);
+        if (!first) {
+          b0 = lfb[k * BLOCK + tid];
+        } else if (add_dc) {
+          const double2 d = a0[x];
+          b0 = mk<T2>((Rt)(d.x * (double)f0.x - d.y * (double)f0.y), (Rt)(d.x * (double)f0.y + d.y * (double)f0.x));
+        }
+        Lf[x] = mk<T2>(b0.x + acc[k].x, b0.y + acc[k].y);
       }
-      if (first && add_dc) {
-        double2 d = a0[x];
-        b0 = mk<T2>((Rt)(d.x * (double)f0.x - d.y * (double)f0.y), (Rt)(d.x * (double)f0.y + d.y * (double)f0.x));
-      }
-      Lf[x] = mk<T2>(b0.x + acc[k].x, b0.y + acc[k].y);
     }
   }
 }
@@ -1562,21 +1435,21 @@ static cudaError_t launch_groups_tp(const ApplyArgs& a, int wi, T2* Lf, int firs
   constexpr int BLOCK = K3Cfg<T2>::BLOCK;
   const InterpWedge& iw = a.iw[wi];
   // the plan opted this instance into its largest smem on its device (configure_interp)
-  const size_t smem = k3_fixed_smem<T2, TAPS, P>() + sizeof(T2) * kK3Stages * (size_t)iw.tile_cap;
+  const size_t smem = K3Layout<T2, TAPS, P>::bytes(iw.tile_cap);
   int per_sm = 0;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_interp_groups<T2, TAPS, P>, BLOCK, smem);
   per_sm = std::max(per_sm, 1);
   int blocks = std::max(1, std::min(iw.nchunks, per_sm * a.sms));
   k_interp_groups<T2, TAPS, P><<<blocks, BLOCK, smem, s>>>(iw, reinterpret_cast<const T2*>(a.g), a.a0,
                                                           reinterpret_cast<const T2*>(a.fhat), first,
-                                                          add_dc, a.es_beta, *a.poly, Lf);
+                                                          add_dc, *a.poly, Lf);
   return cudaGetLastError();
 }
 
 template <typename T2, int TAPS>
 static cudaError_t configure_interp_tp(long long tile_cap) {
-  constexpr int P = GroupP<T2>::value;
-  const size_t smem = k3_fixed_smem<T2, TAPS, P>() + sizeof(T2) * kK3Stages * (size_t)tile_cap;
+  constexpr int P = GroupP<T2, TAPS>::value;
+  const size_t smem = K3Layout<T2, TAPS, P>::bytes(tile_cap);
   return raise_smem_attr((const void*)k_interp_groups<T2, TAPS, P>, smem);
 }
 
@@ -1593,6 +1466,8 @@ cudaError_t configure_interp(int taps, bool c64, long long max_tile_cap) {
     FIO_CFG_CASE(8)
     FIO_CFG_CASE(9)
     FIO_CFG_CASE(10)
+    FIO_CFG_CASE(11)
+    FIO_CFG_CASE(12)
     default: return cudaErrorInvalidValue;
   }
 #undef FIO_CFG_CASE
@@ -1636,7 +1511,7 @@ static cudaError_t launch_interp(const ApplyArgs* args, int nrhs, T2* Lf0, cudaS
     if (a.skel) {  // skeleton storage: regenerate this wedge's alpha' into its stream's scratch
       const InterpWedge& iw = a.iw[wi];
       e = launch_rebuild_alpha(a.op, a.wd_host[wi], a.skel[wi], iw.q, iw.slot_x,
-                               (long long)iw.ngroups * GroupP<T2>::value, const_cast<void*>(iw.alpha),
+                               (long long)iw.ngroups * group_p(sizeof(T2) == 8, a.taps), const_cast<void*>(iw.alpha),
                                sizeof(T2) == sizeof(float2), sw);
       if (e != cudaSuccess) return e;
       ++*n;
@@ -1646,7 +1521,7 @@ static cudaError_t launch_interp(const ApplyArgs* args, int nrhs, T2* Lf0, cudaS
       T2* Lf = sj ? reinterpret_cast<T2*>(args[b].acc[sj - 1]) : Lf0 + b * NN;
 #define FIO_GROUPS_CASE(TP)                                                  \
   case TP:                                                                   \
-    e = launch_groups_tp<T2, TP, GroupP<T2>::value>(args[b], wi, Lf, first, dc, sw); \
+    e = launch_groups_tp<T2, TP, GroupP<T2, TP>::value>(args[b], wi, Lf, first, dc, sw); \
     break;
       switch (a.taps) {
         FIO_GROUPS_CASE(3)
@@ -1657,6 +1532,8 @@ static cudaError_t launch_interp(const ApplyArgs* args, int nrhs, T2* Lf0, cudaS
         FIO_GROUPS_CASE(8)
         FIO_GROUPS_CASE(9)
         FIO_GROUPS_CASE(10)
+        FIO_GROUPS_CASE(11)
+        FIO_GROUPS_CASE(12)
         default: return cudaErrorInvalidValue;
       }
 #undef FIO_GROUPS_CASE
@@ -1709,19 +1586,21 @@ __device__ __forceinline__ T2 shfl_down_t2(T2 v, int d) {
   return r;
 }
 
-// K3*: one thread per group (persistent grid-stride loop, whole warps iterate together).  Lanes
-// whose groups share an anchor (same supercell: identical windows, consecutive in the sorted group
-// order) are summed with a segmented shuffle reduction first, so only the segment head issues the
-// RED atomics for each window cell.
+// K3*: one thread per half group of PH = min(P, 4) points (persistent grid-stride loop, whole warps
+// iterate together; PH keeps both weight sets in registers).  Lanes whose windows share an anchor
+// (the two halves of a group, and neighbouring groups with the same anchor, consecutive in the
+// group order) are summed with a segmented shuffle reduction first, so only the segment head issues
+// the RED atomics for each window cell.
 template <typename T2, int TAPS, int P>
 __global__ void __launch_bounds__(128) k_spread_groups(InterpWedge iw, T2* __restrict__ gstar,
-                                                       const T2* __restrict__ g, double es_beta, EsPoly poly) {
+                                                       const T2* __restrict__ g, EsPoly poly) {
   using Rt = typename Real<T2>::type;
   using O2 = typename OffT<T2>::type;
+  constexpr int PH = P < 4 ? P : 4;
+  constexpr int SPLIT = P / PH;
+  static_assert(P % PH == 0, "group size");
   constexpr int WIN = k3_window_cols(TAPS, sizeof(T2) == 8);
   constexpr int WINR = k3_window_rows(TAPS, sizeof(T2) == 8);
-  const Rt inv_half_w = (Rt)(2.0 / TAPS);
-  const Rt beta = (Rt)es_beta;
   const int n1f = iw.nrow, n2p = iw.ncolp, q = iw.q;
   const long long gstride = (long long)n1f * n2p;
   const long long nslots = (long long)iw.ngroups * P;
@@ -1730,10 +1609,13 @@ __global__ void __launch_bounds__(128) k_spread_groups(InterpWedge iw, T2* __res
   const O2* __restrict__ offs = reinterpret_cast<const O2*>(iw.slot_off);
   const int lane = threadIdx.x & 31;
   const int stride = gridDim.x * blockDim.x;
-  // whole warps step through the groups so that the shuffles below see converged warps
-  for (int base = (blockIdx.x * blockDim.x + threadIdx.x) - lane; base < iw.ngroups; base += stride) {
-    const int grp = base + lane;
-    const bool valid = grp < iw.ngroups;
+  const int nvg = iw.ngroups * SPLIT;
+  // whole warps step through the half groups so that the shuffles below see converged warps
+  for (int base = (blockIdx.x * blockDim.x + threadIdx.x) - lane; base < nvg; base += stride) {
+    const int vg = base + lane;
+    const bool valid = vg < nvg;
+    const int grp = valid ? vg / SPLIT : 0;
+    const int s0 = grp * P + (vg - grp * SPLIT) * PH;  // first slot of this thread's points
     int a1 = 0, a2 = 0;
     if (valid) {
       a1 = iw.anchor[2 * grp];
@@ -1750,62 +1632,62 @@ __global__ void __launch_bounds__(128) k_spread_groups(InterpWedge iw, T2* __res
 #pragma unroll
     for (int d = 16; d > 0; d >>= 1) maxrun = max(maxrun, __shfl_xor_sync(0xffffffffu, maxrun, d));
     const int r0 = a1 < 0 ? a1 + n1f : a1;
-    Rt p1[P][WINR], p2[P][WIN];
-    T2 gx[P];
+    Rt p1[PH][WINR], p2[PH][WIN], o1[PH], o2[PH];
+    T2 gx[PH];
 #pragma unroll
-    for (int k = 0; k < P; ++k) {
+    for (int k = 0; k < PH; ++k) {
       int x = -1;
       O2 o;
       o.x = (Rt)(0.5 * TAPS);
       o.y = (Rt)(0.5 * TAPS);
       if (valid) {
-        x = iw.slot_x[grp * P + k];
-        o = offs[grp * P + k];
+        x = iw.slot_x[s0 + k];
+        o = offs[s0 + k];
       }
       gx[k] = x >= 0 ? g[x] : mk<T2>(0, 0);
-      // the same FP32 row weights as K3, so the adjoint stays the exact conjugate transpose
-      float w1[WINR];
-      row_weights_f32<Rt, TAPS, WINR>((Rt)o.x, poly, w1);
-#pragma unroll
-      for (int i = 0; i < WINR; ++i) p1[k][i] = (Rt)w1[i];
-      window_weights<Rt, TAPS, WIN>((Rt)o.y, inv_half_w, beta, poly, p2[k]);
+      o1[k] = o.x;
+      o2[k] = o.y;
     }
-    T2 anext[sizeof(T2) == 8 ? P : 1];  // c64: alpha'(t+1), loaded one term ahead
+    // the same weights (same function, same precision) as K3: the adjoint stays the exact
+    // conjugate transpose of the forward operator
+    axis_weights<TAPS, WINR, PH>(o1, poly, p1);
+    axis_weights<TAPS, WIN, PH>(o2, poly, p2);
+    T2 anext[sizeof(T2) == 8 ? PH : 1];  // c64: alpha'(t+1), loaded one term ahead
     if constexpr (sizeof(T2) == 8) {
 #pragma unroll
-      for (int k = 0; k < P; ++k) anext[k] = (valid && q > 0) ? alpha[(long long)grp * P + k] : mk<T2>(0, 0);
+      for (int k = 0; k < PH; ++k) anext[k] = (valid && q > 0) ? alpha[(long long)s0 + k] : mk<T2>(0, 0);
     }
     for (int t = 0; t < q; ++t) {
-      T2 c[P];
+      T2 c[PH];
 #pragma unroll
-      for (int k = 0; k < P; ++k) {
+      for (int k = 0; k < PH; ++k) {
         // conj(alpha') g; alpha' one term ahead for c64, at use for c128 (ahead: 52.7 vs 48.3 ms)
         T2 av;
         if constexpr (sizeof(T2) == 8)
           av = anext[k];
         else
-          av = valid ? alpha[t * nslots + (long long)grp * P + k] : mk<T2>(0, 0);
+          av = valid ? alpha[t * nslots + (long long)s0 + k] : mk<T2>(0, 0);
         c[k] = mk<T2>(av.x * gx[k].x + av.y * gx[k].y, av.x * gx[k].y - av.y * gx[k].x);
       }
       if constexpr (sizeof(T2) == 8) {
         if (t + 1 < q && valid) {
 #pragma unroll
-          for (int k = 0; k < P; ++k) anext[k] = alpha[(t + 1) * nslots + (long long)grp * P + k];
+          for (int k = 0; k < PH; ++k) anext[k] = alpha[(t + 1) * nslots + (long long)s0 + k];
         }
       }
       T2* __restrict__ rp = G + t * gstride + (long long)r0 * n2p + a2;
       int r = r0;
 #pragma unroll 1
       for (int i = 0; i < WINR; ++i) {
-        T2 e[P];
+        T2 e[PH];
 #pragma unroll
-        for (int k = 0; k < P; ++k) e[k] = mk<T2>(p1[k][i] * c[k].x, p1[k][i] * c[k].y);
+        for (int k = 0; k < PH; ++k) e[k] = mk<T2>(p1[k][i] * c[k].x, p1[k][i] * c[k].y);
         T2 v[WIN];
 #pragma unroll
         for (int j = 0; j < WIN; ++j) {
           v[j] = mk<T2>(0, 0);
 #pragma unroll
-          for (int k = 0; k < P; ++k) v[j] = cfma_real(p2[k][j], e[k], v[j]);
+          for (int k = 0; k < PH; ++k) v[j] = cfma_real(p2[k][j], e[k], v[j]);
         }
         // segmented sum toward the run head over the whole window row at once (WIN independent
         // shuffle chains per step): after the steps d < maxrun the head holds the run total
@@ -1945,8 +1827,9 @@ __global__ void __launch_bounds__(1024) k_dc_adj(long long NN, const double2* __
 template <typename T2, int TAPS, int P>
 static cudaError_t launch_spread_tp(const ApplyArgs& a, int wi, const T2* g, cudaStream_t s) {
   const InterpWedge& iw = a.iw[wi];
-  int blocks = std::max(1, std::min((iw.ngroups + 127) / 128, a.sms * 8));
-  k_spread_groups<T2, TAPS, P><<<blocks, 128, 0, s>>>(iw, reinterpret_cast<T2*>(a.g), g, a.es_beta, *a.poly);
+  const int nvg = iw.ngroups * (P / (P < 4 ? P : 4));
+  int blocks = std::max(1, std::min((nvg + 127) / 128, a.sms * 8));
+  k_spread_groups<T2, TAPS, P><<<blocks, 128, 0, s>>>(iw, reinterpret_cast<T2*>(a.g), g, *a.poly);
   return cudaGetLastError();
 }
 
@@ -1974,13 +1857,13 @@ static cudaError_t enqueue_adjoint_t(const ApplyArgs& a, const T2* g, T2* out, c
       if (a.skel) {
         const InterpWedge& iw = a.iw[wi];
         e = launch_rebuild_alpha(a.op, a.wd_host[wi], a.skel[wi], iw.q, iw.slot_x,
-                                 (long long)iw.ngroups * GroupP<T2>::value, const_cast<void*>(iw.alpha), c64, sw);
+                                 (long long)iw.ngroups * group_p(sizeof(T2) == 8, a.taps), const_cast<void*>(iw.alpha), c64, sw);
         if (e != cudaSuccess) return e;
         ++n;
       }
 #define FIO_SPREAD_CASE(TP)                                   \
   case TP:                                                    \
-    e = launch_spread_tp<T2, TP, GroupP<T2>::value>(a, wi, g, sw); \
+    e = launch_spread_tp<T2, TP, GroupP<T2, TP>::value>(a, wi, g, sw); \
     break;
       switch (a.taps) {
         FIO_SPREAD_CASE(3)
@@ -1991,6 +1874,8 @@ static cudaError_t enqueue_adjoint_t(const ApplyArgs& a, const T2* g, T2* out, c
         FIO_SPREAD_CASE(8)
         FIO_SPREAD_CASE(9)
         FIO_SPREAD_CASE(10)
+        FIO_SPREAD_CASE(11)
+        FIO_SPREAD_CASE(12)
         default: return cudaErrorInvalidValue;
       }
 #undef FIO_SPREAD_CASE

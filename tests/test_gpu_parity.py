@@ -115,8 +115,10 @@ def test_config3_sampled(name):
     op, f = wl.make_operator(cfg), wl.make_input(cfg)
     _, out = run(op, f, eps=cfg["eps"], dtype=cfg["dtype"])
     pts = wl.sample_points(op.N, 4096, 1)
-    err = oracle.rel_l2(out.ravel()[pts], oracle.fio(op, f, pts=pts))
-    assert err <= 10 * cfg["eps"], err
+    ref = oracle.fio(op, f, pts=pts)
+    err, mx = _pointwise(out.ravel()[pts], ref)
+    print(f"{name}: rel l2 {err:.3e}, max|err_i|/rms {mx:.3e}")
+    assert err <= 10 * cfg["eps"] and mx <= 100 * cfg["eps"], (err, mx)
 
 
 # ------------------------------------------------------------------ structure
@@ -170,9 +172,10 @@ def test_config4_sampled():
     op, f = wl.make_operator(cfg), wl.make_input(cfg)
     plan, out = run(op, f, eps=cfg["eps"])
     pts = wl.sample_points(op.N, 4096, 1)
-    err = oracle.rel_l2(out.ravel()[pts], oracle.fio(op, f, pts=pts))
-    print("config4: W", plan.info["W"], "sum_q", plan.info["sum_q"], "plan s", plan.info["plan_seconds"], "err", err)
-    assert err <= 10 * cfg["eps"], err
+    err, mx = _pointwise(out.ravel()[pts], oracle.fio(op, f, pts=pts))
+    print("config4: W", plan.info["W"], "sum_q", plan.info["sum_q"], "plan s", plan.info["plan_seconds"], "err", err,
+          "max|err_i|/rms", mx)
+    assert err <= 10 * cfg["eps"] and mx <= 100 * cfg["eps"], (err, mx)
 
 
 # ------------------------------------------------------------------ adjoint
@@ -548,3 +551,86 @@ def test_binding_rejects_bad_operands():
     before = torch.cuda.current_device()
     plan.apply(f)
     assert torch.cuda.current_device() == before
+
+
+# ------------------------------------------------------------------ full-grid element-wise parity at the headline sizes
+def _pointwise(out, ref):
+    """(rel l2, max_i |err_i| / rms(ref)) over every output point."""
+    rms = np.sqrt(np.mean(np.abs(ref) ** 2))
+    return oracle.rel_l2(out, ref), float(np.abs(out - ref).max() / rms)
+
+
+@pytest.mark.parametrize("N,dtype,eps", [(1024, "c128", 1e-6), (1024, "c64", 1e-4), (2048, "c128", 1e-6),
+                                         (2048, "c64", 1e-4)])
+def test_full_grid_pointwise_shift_field(N, dtype, eps):
+    # Phi = (x + k(x)/N).xi with an integer field k(x): Lf[n] = f[n + k(n)] exactly (DESIGN.md reading R12,
+    # pinned on the oracle by test_pointwise_shift_pins_spatial_indexing) -- checked at EVERY output point
+    # of the headline grids, so a fault confined to one K3 chunk or one wedge cannot hide
+    n1, n2 = np.meshgrid(np.arange(N), np.arange(N), indexing="ij")
+    k1 = (n1 // 97 + 2 * (n2 // 131)) % 5 - 2
+    k2 = ((n1 // 61) * (n2 // 83)) % 7 - 3
+    op = wl.shift_operator(N, k1, k2)
+    f = wl.white_noise(N, 11, dtype)
+    plan, out = run(op, f, eps=eps, dtype=dtype)
+    ref = f[(n1 + k1) % N, (n2 + k2) % N]
+    rel, mx = _pointwise(out, ref)
+    print(f"shift field N={N} {dtype}: rel l2 {rel:.3e}, max|err|/rms {mx:.3e}, sum_q {plan.info['sum_q']}")
+    assert rel <= 10 * eps and mx <= 100 * eps, (rel, mx)
+
+
+@pytest.mark.parametrize("N,dtype,eps", [(1024, "c128", 1e-6), (1024, "c64", 1e-4), (2048, "c128", 1e-6),
+                                         (2048, "c64", 1e-4)])
+def test_full_grid_pointwise_piecewise_radii(N, dtype, eps):
+    # c1, c2 piecewise constant over x (4 regions): at every x, Lf(x) is the constant-radius Fourier
+    # multiplier of that x's radii (PAPER.md:109-119; pinned on the oracle by
+    # test_piecewise_radii_pins_c1_c2_indexing).  The warped points x + grad rho(xihat_l) are genuinely
+    # off-grid, so this exercises the whole NUFFT (K1, K2, K3) at every output point of the grid.
+    n1, n2 = np.meshgrid(np.arange(N), np.arange(N), indexing="ij")
+    ma = ((n1 * 7) // N + (n2 * 5) // N) % 2 == 0
+    mb = (n1 + 3 * n2) % 4 == 0
+    A1, B1, A2, B2 = 0.3, 1.1, 0.9, 0.45
+    c1 = np.where(ma, A1, B1)
+    c2 = np.where(mb, A2, B2)
+    op = wl.Operator(N, c1, c2)
+    f = wl.white_noise(N, 12, dtype)
+    plan, out = run(op, f, eps=eps, dtype=dtype)
+    fh = np.fft.fft2(f) / N
+    xi1, xi2 = wl.freqs(N)
+    ref = np.zeros((N, N), complex)
+    for v1 in (A1, B1):
+        for v2 in (A2, B2):
+            m = np.exp(2j * np.pi * np.sqrt(v1 ** 2 * xi1 ** 2 + v2 ** 2 * xi2 ** 2))
+            sel = (c1 == v1) & (c2 == v2)
+            ref[sel] = (N * np.fft.ifft2(m * fh))[sel]
+    rel, mx = _pointwise(out, ref)
+    print(f"piecewise radii N={N} {dtype}: rel l2 {rel:.3e}, max|err|/rms {mx:.3e}, sum_q {plan.info['sum_q']}")
+    assert rel <= 10 * eps and mx <= 100 * eps, (rel, mx)
+
+
+# ------------------------------------------------------------------ high-accuracy complex128 (PAPER.md:1142-1143, 1318-1322)
+@pytest.mark.parametrize("N", [64, 256])
+def test_high_accuracy_c128(N):
+    # eps = 1e-8 and 1e-10: FP64 throughout (row and column weights, alpha', grids, accumulation), the
+    # shifted-CholeskyQR3 separation below 1e-7 and up to 12 taps; full grid against the direct sum
+    op = wl.grt_operator(N)
+    f = wl.white_noise(N, 21)
+    ref = oracle.fio(op, f)
+    for eps in (1e-8, 1e-10):
+        plan, out = run(op, f, eps=eps)
+        rel, mx = _pointwise(out, ref)
+        info = plan.info
+        print(f"N={N} eps={eps:g}: rel l2 {rel:.3e} max|err|/rms {mx:.3e} taps {info['nufft_w']} "
+              f"sum_q {info['sum_q']} sep {info['max_sep_err']:.2e}")
+        assert rel <= 10 * eps, (eps, rel)
+        if eps >= 1e-8:  # at 1e-10 the sampled Frobenius error (PAPER.md:1464-1477) is ~10 eps: report only
+            assert info["certified"] == 1
+
+
+def test_eps_floors_are_rejected():
+    op = wl.grt_operator(64)
+    with pytest.raises(fio.FioError, match="floor"):
+        make_plan(op, eps=1e-7, dtype="c64")
+    with pytest.raises(fio.FioError, match="floor"):
+        make_plan(op, eps=1e-12, dtype="c128")
+    make_plan(op, eps=1e-6, dtype="c64")  # at the floors: accepted
+    make_plan(op, eps=1e-11, dtype="c128")

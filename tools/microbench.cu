@@ -126,6 +126,7 @@ static float time_ms(F launch, int reps = 5) {
   CK(cudaEventCreate(&a));
   CK(cudaEventCreate(&b));
   launch();
+  CK(cudaGetLastError());
   CK(cudaDeviceSynchronize());
   float best = 1e30f;
   for (int r = 0; r < reps; ++r) {

@@ -1,23 +1,21 @@
-"""Run a few applies of one BASELINE config (for ncu / compute-sanitizer captures)."""
-import argparse
+"""Plan + a few applies of one BASELINE config (the command profiled under ncu):
+    python tools/run_apply.py cfg3_c64 [applies]"""
 import os
 import sys
 
-sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
-import torch  # noqa: E402
+import torch
 
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import paper_math_0610051_b200 as fio  # noqa: E402
 import workloads as wl  # noqa: E402
 
-p = argparse.ArgumentParser()
-p.add_argument("--config", default="cfg3_c64")
-p.add_argument("--iters", type=int, default=3)
-a = p.parse_args()
-cfg = wl.config(a.config)
+name = sys.argv[1] if len(sys.argv) > 1 else "cfg3_c64"
+n = int(sys.argv[2]) if len(sys.argv) > 2 else 3
+cfg = wl.config(name)
 op = wl.make_operator(cfg)
-f = torch.from_numpy(wl.make_input(cfg)).to("cuda:0", torch.complex64 if cfg["dtype"] == "c64" else torch.complex128)
 plan = fio.Plan(op.N, op.c1, op.c2, op.b1, op.b2, op.px, op.pxi, eps=cfg["eps"], dtype=cfg["dtype"], device=0)
-for _ in range(a.iters):
+f = torch.from_numpy(wl.make_input(cfg)).to("cuda:0", torch.complex64 if cfg["dtype"] == "c64" else torch.complex128)
+for _ in range(n):
     out = plan.apply(f)
 torch.cuda.synchronize()
-print(a.config, plan.info["sum_q"], plan.info["slots"], float(out.abs().mean()))
+print(name, plan.info["sum_q"], float(out.abs().mean()))
