@@ -114,6 +114,11 @@ typedef struct {
                          creates this rank's communicator (a collective call: every rank must call
                          fio_plan with the same id) and fio_apply ends with the cross-GPU sum.
                          NULL with nranks > 1: fio_apply returns this rank's N x N partial sum. */
+  double wedge_overlap; /* 0: the paper's indicator wedges chi_l.  In (0, 1]: the
+                         smooth polar-wedge partition of DESIGN.md reading R2 -- a C-infinity angular
+                         taper of half-width wedge_overlap pi / W around every boundary ray, sum_l
+                         chi_l = 1 exactly, so L is unchanged; each wedge's support,
+                         box and rank grow with the overlap. */
 } fio_opts;
 
 #define FIO_NCCL_ID_BYTES 128
@@ -200,6 +205,8 @@ typedef struct {
   int k3_streams;         /* concurrent K3 streams of an apply (wedge l on stream l mod k3_streams) */
   int has_comm;           /* 1 if the plan owns an NCCL communicator (fio_apply returns the row slab) */
   int out_rows;           /* rows of the array fio_apply writes: N / nranks with a communicator, else N */
+  double wedge_overlap;   /* 0: indicator wedges; > 0: smooth partition (opts.wedge_overlap) */
+  long long members;      /* sum over owned wedges of |supp chi_l| (frequencies carried) */
 } fio_info;
 
 fio_status fio_plan_info(fio_handle h, fio_info* info);
@@ -216,6 +223,10 @@ fio_status fio_plan_wedges(fio_handle h, int* l, int* q, int* box /* 4 per wedge
  * readings R3/R4); for each wedge: M (4 ints), xi_c (2), box n1,n2 and fine n1f,n2f
  * (4) as chosen by the plan (reading R5). */
 fio_status fio_geometry(int N, int W, int* wedge_of, int* M, int* xc, int* box);
+
+/* Partition weights chi_l(xi) of every wedge l < W at the frequency (xi1, xi2) (host only):
+ * the indicator for overlap 0, the smooth taper of reading R2 for overlap in (0, 1]. */
+fio_status fio_partition_weights(int W, double overlap, int xi1, int xi2, double* chi /* W */);
 
 /* Wedge -> rank assignment used for nranks > 1 (owner[l] in [0, nranks)), from
  * per-wedge costs (longest-processing-time greedy, deterministic). Host-only. */

@@ -13,6 +13,8 @@ Functions and the passages they restate:
                   phases Phi_+- (op.sign) and the Bessel amplitude of eq. ellipses_amp
                   (op.amp == "bessel", PAPER.md:1596-1603)
   wedge_of        wedges W_l PAPER.md:210-217 (W wedges, reading R1)
+  smooth_wedge_weights  the smooth polar-wedge partition chi_l of DESIGN.md reading R2 (numpy, from
+                  its definition); sum_l chi_l = 1, so L_l f = fio(op, fhat=chi_l fhat)
   nudft2          the Fourier series of evaluation step 3, PAPER.md:1299-1311
   fio_adjoint_hat widehat(L* g)(xi)
   rel_l2          the error estimator of PAPER.md:1549-1555
@@ -139,6 +141,43 @@ def fio_adjoint_hat(op, g: np.ndarray, fidx: Optional[np.ndarray] = None) -> np.
                                     _ptr(pxi), _ptr(g), fidx.shape[0], _ptr(fidx),
                                     int(getattr(op, "sign", 1)), _amp_kind(op), _ptr(out))
     return out.reshape(N, N) if full else out
+
+
+def _smooth_step(tau):
+    """S(tau) = g(u) / (g(u) + g(1 - u)), u = (1 + tau)/2, g(u) = exp(-1/u) for u > 0 (else 0):
+    0 for tau <= -1, 1 for tau >= 1, infinitely differentiable, S(tau) + S(-tau) = 1."""
+    tau = np.asarray(tau, dtype=np.float64)
+    u = np.clip(0.5 * (1.0 + tau), 0.0, 1.0)
+    with np.errstate(divide="ignore", over="ignore", invalid="ignore"):
+        gu = np.where(u > 0, np.exp(-1.0 / np.where(u > 0, u, 1.0)), 0.0)
+        gv = np.where(u < 1, np.exp(-1.0 / np.where(u < 1, 1.0 - u, 1.0)), 0.0)
+        out = gu / (gu + gv)
+    return np.where(tau <= -1, 0.0, np.where(tau >= 1, 1.0, out))
+
+
+def smooth_chi_angle(W: int, overlap: float, l: int, theta):
+    """chi_l at polar angle theta (reading R2): with D = 2 pi / W and the paper's boundary
+    rays b_l = (l - 1/2) D, h = overlap D / 2,
+        chi_l = S(((theta - b_l) mod 2 pi) / h) * (1 - S(((theta - b_{l+1}) mod 2 pi) / h)),
+    angle differences taken in (-pi, pi]."""
+    D = 2 * np.pi / W
+    h = 0.5 * overlap * D
+
+    def wrap(a):  # to (-pi, pi]
+        a = np.mod(np.asarray(a, dtype=np.float64), 2 * np.pi)
+        return np.where(a > np.pi, a - 2 * np.pi, a)
+    return _smooth_step(wrap(theta - (l - 0.5) * D) / h) * (1.0 - _smooth_step(wrap(theta - (l + 0.5) * D) / h))
+
+
+def smooth_wedge_weights(N: int, W: int, overlap: float) -> np.ndarray:
+    """chi_l(xi) on Omega in FFT-natural order, shape (W, N, N); chi_l(0) = 0 (xi = 0 is the DC term)."""
+    k = np.arange(N)
+    k = np.where(k >= N // 2, k - N, k)
+    xi1, xi2 = np.meshgrid(k, k, indexing="ij")
+    th = np.arctan2(xi2.astype(np.float64), xi1.astype(np.float64))
+    chi = np.stack([smooth_chi_angle(W, overlap, l, th) for l in range(W)])
+    chi[:, 0, 0] = 0.0
+    return chi
 
 
 def nudft2(coeffs: np.ndarray, y: np.ndarray) -> np.ndarray:

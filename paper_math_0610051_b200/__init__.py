@@ -24,7 +24,7 @@ from typing import Optional
 
 import numpy as np
 
-__all__ = ["FioError", "Plan", "geometry", "assign_wedges", "nccl_unique_id", "broadcast_nccl_id", "row_slab",
+__all__ = ["FioError", "Plan", "geometry", "assign_wedges", "partition_weights", "nccl_unique_id", "broadcast_nccl_id", "row_slab",
            "library_path", "load_library", "SYMBOLS", "STAGES"]
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
@@ -37,7 +37,7 @@ FIO_OK, FIO_WNOTCERT = 0, 1
 # every entry point declared in include/fio.h
 SYMBOLS = ["fio_default_opts", "fio_plan", "fio_plan_save", "fio_plan_load", "fio_apply", "fio_apply_batch", "fio_apply_adjoint", "fio_apply_host", "fio_destroy", "fio_plan_info",
            "fio_plan_wedges", "fio_geometry", "fio_assign_wedges", "fio_profile_begin", "fio_profile_end",
-           "fio_last_error", "fio_version", "fio_nccl_unique_id"]
+           "fio_last_error", "fio_version", "fio_nccl_unique_id", "fio_partition_weights"]
 NCCL_ID_BYTES = 128
 STAGES = ["K0_rows", "K0_cols", "K1_rowpass", "K2_colpass", "K3_interp"]
 
@@ -62,7 +62,7 @@ class _Opts(ctypes.Structure):
                 ("nufft_beta", ctypes.c_double), ("seed", ctypes.c_uint64), ("device", ctypes.c_int),
                 ("rank", ctypes.c_int), ("nranks", ctypes.c_int), ("r_init", ctypes.c_int),
                 ("r_max", ctypes.c_int), ("certify", ctypes.c_int), ("skeleton", ctypes.c_int),
-                ("nccl_id", ctypes.c_void_p)]
+                ("nccl_id", ctypes.c_void_p), ("wedge_overlap", ctypes.c_double)]
 
 
 class _Info(ctypes.Structure):
@@ -78,7 +78,7 @@ class _Info(ctypes.Structure):
                 ("rank_balance", ctypes.c_double), ("slot_terms", ctypes.c_longlong), ("group_p", ctypes.c_int),
                 ("k3_window_rows", ctypes.c_int), ("skeleton_bytes", ctypes.c_size_t),
                 ("k3_window_cols", ctypes.c_int), ("k3_streams", ctypes.c_int), ("has_comm", ctypes.c_int),
-                ("out_rows", ctypes.c_int)]
+                ("out_rows", ctypes.c_int), ("wedge_overlap", ctypes.c_double), ("members", ctypes.c_longlong)]
 
 
 def library_path() -> str:
@@ -114,10 +114,12 @@ def load_library():
     lib.fio_profile_begin.argtypes = [P, I]
     lib.fio_profile_end.argtypes = [P, P, P]
     lib.fio_nccl_unique_id.argtypes = [P]
+    lib.fio_partition_weights.argtypes = [I, ctypes.c_double, I, I, P]
     lib.fio_last_error.restype = ctypes.c_char_p
     lib.fio_version.restype = ctypes.c_char_p
     for name in ["fio_plan", "fio_apply", "fio_apply_batch", "fio_apply_adjoint", "fio_apply_host", "fio_destroy", "fio_plan_info", "fio_plan_wedges",
-                 "fio_geometry", "fio_assign_wedges", "fio_profile_begin", "fio_profile_end", "fio_nccl_unique_id"]:
+                 "fio_geometry", "fio_assign_wedges", "fio_profile_begin", "fio_profile_end", "fio_nccl_unique_id",
+                 "fio_partition_weights"]:
         getattr(lib, name).restype = ctypes.c_int
     _lib = lib
     return lib
@@ -151,6 +153,13 @@ def geometry(N: int, W: int) -> dict:
     _check(lib.fio_geometry(N, W, _ptr(wo), _ptr(M), _ptr(xc), _ptr(box)))
     return {"wedge_of": wo.reshape(N, N), "M": M.reshape(W, 2, 2), "xc": xc, "box": box[:, :2],
             "fine": box[:, 2:]}
+
+
+def partition_weights(W: int, overlap: float, xi1: int, xi2: int) -> np.ndarray:
+    """fio_partition_weights: chi_l(xi) for l < W (indicator for overlap 0, smooth taper otherwise)."""
+    out = np.empty(W, np.float64)
+    _check(load_library().fio_partition_weights(int(W), float(overlap), int(xi1), int(xi2), _ptr(out)))
+    return out
 
 
 def assign_wedges(cost, nranks: int) -> np.ndarray:
@@ -197,7 +206,7 @@ class Plan:
                  seed: int = 0x5EED, device: Optional[int] = None, rank: int = 0, nranks: int = 1,
                  r_init: int = 32, r_max: int = 512, certify: bool = True, rho_sign: int = 1,
                  amplitude: str = "separable", skeleton: bool = False, load: Optional[str] = None,
-                 group=None, nccl_id: Optional[bytes] = None):
+                 group=None, nccl_id: Optional[bytes] = None, wedge_overlap: float = 0.0):
         import torch
         if not torch.cuda.is_available():
             raise FioError(-3, "no CUDA device: the FIO apply runs only on the GPU (no CPU fallback)")
@@ -226,6 +235,7 @@ class Plan:
         o.device, o.rank, o.nranks = self.device, int(rank), int(nranks)
         o.r_init, o.r_max, o.certify = int(r_init), int(r_max), int(bool(certify))
         o.skeleton = int(bool(skeleton))
+        o.wedge_overlap = float(wedge_overlap)
         # wedge-sharded with a communicator: the id comes from rank 0 (broadcast over `group`, or given)
         if nranks > 1 and nccl_id is None and group is not None:
             nccl_id = broadcast_nccl_id(group)

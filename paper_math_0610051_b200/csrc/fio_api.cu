@@ -264,6 +264,15 @@ fio_status fio_geometry(int N, int W, int* wedge_of_out, int* M, int* xc, int* b
   return FIO_OK;
 }
 
+fio_status fio_partition_weights(int W, double overlap, int xi1, int xi2, double* chi) {
+  if (W < 1 || !chi || !(overlap >= 0.0 && overlap <= 1.0)) {
+    set_error("fio_partition_weights: need W >= 1, overlap in [0, 1] and an output array");
+    return FIO_EINVAL;
+  }
+  for (int l = 0; l < W; ++l) chi[l] = wedge_weight(W, overlap, l, xi1, xi2);
+  return FIO_OK;
+}
+
 fio_status fio_assign_wedges(int W, const double* cost, int nranks, int* owner) {
   if (W < 1 || nranks < 1 || !cost || !owner) {
     set_error("fio_assign_wedges: bad arguments");
@@ -630,14 +639,17 @@ static K3Tables make_k3_tables(std::vector<double> uh, long long NN, int taps, b
   const int blk = c64 ? kK3BlockC64 : kK3BlockC128;
   T.cap = chunk_boxes(anchor, blk, k3_window_rows(taps, c64), k3_window_cols(taps, c64),
                       c64 ? kK3TileCapC64 : kK3TileCapC128, T.box, c64 ? 8 : 16);
-  T.nchunks = (int)(T.box.size() / 6);
+  T.nchunks = (int)(T.box.size() / 6);  // (chunk_boxes: 6 ints per chunk, widened to kBoxInts below)
   // pad every chunk to exactly blk groups, so that chunk c's groups are [c blk, (c+1) blk): K3 can then
   // prefetch a chunk's per-thread data without reading its box first.  Padding groups repeat the
   // chunk's first anchor (inside the box), have no points (slot -1) and alpha' = 0.
+  // Slots are stored in K3's physical layout (k3_slot: element-major inside each chunk), so that one
+  // bulk copy moves a chunk's slot indices, offsets or alpha'(t) straight into its shared-memory image.
   T.anchor.assign((size_t)T.nchunks * blk * 2, 0);
   T.slot_x.assign((size_t)T.nchunks * blk * gp, -1);
   T.off.assign((size_t)T.nchunks * blk * gp * 2, 0.5 * taps);
-  std::vector<int>& box = T.box;
+  std::vector<int> box8((size_t)T.nchunks * kBoxInts, 0);  // per chunk: first group, r0, c0, rows, cols, groups, 0, 0
+  const std::vector<int>& box = T.box;
 #pragma omp parallel for schedule(static)
   for (int c = 0; c < T.nchunks; ++c) {
     const long long g0 = box[6 * c], n = box[6 * c + 5];
@@ -647,13 +659,16 @@ static K3Tables make_k3_tables(std::vector<double> uh, long long NN, int taps, b
       T.anchor[2 * dst + 1] = anchor[2 * src + 1];
       if (i < n)
         for (int k = 0; k < gp; ++k) {
-          T.slot_x[dst * gp + k] = slot_x[src * gp + k];
-          T.off[2 * (dst * gp + k)] = off[2 * (src * gp + k)];
-          T.off[2 * (dst * gp + k) + 1] = off[2 * (src * gp + k) + 1];
+          const long long ph = k3_slot(dst, k, gp, blk);
+          T.slot_x[ph] = slot_x[src * gp + k];
+          T.off[2 * ph] = off[2 * (src * gp + k)];
+          T.off[2 * ph + 1] = off[2 * (src * gp + k) + 1];
         }
     }
-    box[6 * c] = c * blk;
+    for (int e = 0; e < 6; ++e) box8[(size_t)kBoxInts * c + e] = box[6 * c + e];
+    box8[(size_t)kBoxInts * c] = c * blk;
   }
+  T.box.swap(box8);
   if (c64) {
     T.offf.resize(T.off.size());
 #pragma omp parallel for schedule(static)
@@ -786,7 +801,7 @@ fio_status build_plan(fio_plan_s& P, const fio_phase* phase, const fio_amplitude
   FIO_CUDA(P.upload(&P.a0, a0.data(), NN));
 
   // geometry and ownership
-  build_geometry(N, P.W, P.geom);
+  build_geometry(N, P.W, P.geom, P.opts.wedge_overlap);
   std::vector<int> owner(P.W, 0);
   if (P.opts.nranks > 1) {
     // per-wedge cost = q_l (estimated, identical on every rank) x (interpolation N^2 w^2 + FFT volume)
@@ -971,15 +986,19 @@ fio_status build_plan(fio_plan_s& P, const fio_phase* phase, const fio_amplitude
       std::vector<double> d1(g.n1), d2(g.n2);
       for (int i = 0; i < g.n1; ++i) d1[i] = 1.0 / es_fourier((double)(i - g.n1 / 2) / g.n1f, P.taps, P.es_beta);
       for (int i = 0; i < g.n2; ++i) d2[i] = 1.0 / es_fourier((double)(i - g.n2 / 2) / g.n2f, P.taps, P.es_beta);
-      DevBuf dd1, dd2, dMem;
+      DevBuf dd1, dd2, dMem, dChi;
       FIO_CUDA(dd1.ensure(sizeof(double) * g.n1));
       FIO_CUDA(dd2.ensure(sizeof(double) * g.n2));
       FIO_CUDA(dMem.ensure(sizeof(int) * g.members.size()));
       FIO_CUDA(cudaMemcpy(dd1.p, d1.data(), sizeof(double) * g.n1, cudaMemcpyHostToDevice));
       FIO_CUDA(cudaMemcpy(dd2.p, d2.data(), sizeof(double) * g.n2, cudaMemcpyHostToDevice));
       FIO_CUDA(cudaMemcpy(dMem.p, g.members.data(), sizeof(int) * g.members.size(), cudaMemcpyHostToDevice));
+      if (!g.chi.empty()) {  // smooth partition: chi_l folded into beta' with the deconvolution
+        FIO_CUDA(dChi.ensure(sizeof(double) * g.chi.size()));
+        FIO_CUDA(cudaMemcpy(dChi.p, g.chi.data(), sizeof(double) * g.chi.size(), cudaMemcpyHostToDevice));
+      }
       FIO_CUDA(launch_fold_beta(N, w, dMem.as<int>(), (int)g.members.size(), dBeta.as<double2>(), q, dd1.as<double>(),
-                                dd2.as<double>(), betap, c64, s));
+                                dd2.as<double>(), g.chi.empty() ? nullptr : dChi.as<double>(), betap, c64, s));
       FIO_CUDA(cudaStreamSynchronize(s));
     }
     if (prof) cudaDeviceSynchronize();
@@ -1199,6 +1218,7 @@ ApplyArgs make_args(const fio_plan_s& P) {
   a.fine_elems = P.fine_elems;
   a.cols_per_cta_N = P.cols_per_cta_N;
   a.sms = P.sms;
+  a.overlap = P.opts.wedge_overlap > 0.0 ? 1 : 0;
   return a;
 }
 
@@ -1420,6 +1440,10 @@ static fio_status plan_impl(fio_handle* out, int N, const fio_phase* phase, cons
     set_error("fio_plan: nufft_w must be 0 or in [3, 12]");
     return FIO_EINVAL;
   }
+  if (!(o.wedge_overlap >= 0.0 && o.wedge_overlap <= 1.0)) {
+    set_error("fio_plan: wedge_overlap must lie in [0, 1]");
+    return FIO_EINVAL;
+  }
   if (o.n_wedges < 0 || o.r_init < 0 || o.r_max < 0) {
     set_error("fio_plan: negative option");
     return FIO_EINVAL;
@@ -1448,6 +1472,7 @@ static fio_status plan_impl(fio_handle* out, int N, const fio_phase* phase, cons
   // polynomial kernel for the c128 K3 weights: error ~1.5 e^{-beta}, the kernel's own edge value
   P->poly_err = es_poly_fit(P->taps, P->es_beta, P->poly);
   P->input_hash = input_hash(N, phase, amp);
+  if (o.wedge_overlap > 0.0) P->input_hash = fnv1a(P->input_hash, &o.wedge_overlap, sizeof(double));
   if (load) {  // fio_plan_load: the file must describe exactly this plan
     const bool same = hdr->N == N && hdr->W == P->W && hdr->dtype == o.dtype && hdr->taps == P->taps &&
                       hdr->rank == o.rank && hdr->nranks == o.nranks && hdr->eps == eps &&
@@ -1679,6 +1704,8 @@ fio_status fio_plan_info(fio_handle h, fio_info* info) {
   info->p1_elems = h->p1_elems;
   info->launches_per_apply = h->launches;
   info->has_comm = h->comm ? 1 : 0;
+  info->wedge_overlap = h->opts.wedge_overlap;
+  for (int l : h->owned) info->members += (long long)h->geom[l].members.size();
   info->out_rows = h->out_rows();
   return FIO_OK;
 }

@@ -58,6 +58,41 @@ int wedge_of(int W, int xi1, int xi2) {
   return std::min(std::max(l, 0), W - 1);
 }
 
+// Smooth partition of unity over the angle (reading R2; BASELINE north_star "smooth
+// polar-wedge partition"): with D = 2 pi / W, the paper's boundary rays b_l = (l - 1/2) D
+// and a taper half-width h = overlap D / 2,
+//   chi_l(xi) = S((theta - b_l) / h) (1 - S((theta - b_{l+1}) / h)),
+// angles differences taken in (-pi, pi], where S is the C-infinity step S(tau) = g(u) / (g(u) + g(1-u)),
+// u = (1 + tau) / 2, g(u) = e^{-1/u} (u > 0), S = 0 for tau <= -1 and 1 for tau >= 1.  S(tau) +
+// S(-tau) = 1, so at every angle the two wedges sharing a boundary carry 1 - S and S (sum 1),
+// chi_l = 1/2 on the paper's boundary rays and chi_l is the indicator outside the tapers.
+// overlap <= 0: the paper's indicator wedges (wedge_of).
+static double smooth_step(double tau) {
+  if (tau <= -1.0) return 0.0;
+  if (tau >= 1.0) return 1.0;
+  const double u = 0.5 * (1.0 + tau), v = 1.0 - u;
+  const double gu = std::exp(-1.0 / u), gv = std::exp(-1.0 / v);
+  return gu / (gu + gv);
+}
+
+static double angle_diff(double a) {  // a wrapped to (-pi, pi]
+  const double pi = 3.14159265358979323846, twopi = 2.0 * pi;
+  a = std::fmod(a, twopi);
+  if (a <= -pi) a += twopi;
+  if (a > pi) a -= twopi;
+  return a;
+}
+
+double wedge_weight(int W, double overlap, int l, int xi1, int xi2) {
+  if (xi1 == 0 && xi2 == 0) return 0.0;
+  if (!(overlap > 0.0)) return wedge_of(W, xi1, xi2) == l ? 1.0 : 0.0;
+  const double pi = 3.14159265358979323846;
+  const double D = 2.0 * pi / W, h = 0.5 * overlap * D;
+  const double th = std::atan2((double)xi2, (double)xi1);
+  const double lo = angle_diff(th - (l - 0.5) * D), hi = angle_diff(th - (l + 0.5) * D);
+  return smooth_step(lo / h) * (1.0 - smooth_step(hi / h));
+}
+
 static void all_sl2z(std::vector<std::array<int, 4>>& out) {
   out.clear();
   // identity first so that ties keep the plain relabeling of PAPER.md:1331-1336
@@ -74,7 +109,7 @@ static void all_sl2z(std::vector<std::array<int, 4>>& out) {
 // oversampled volume (PAPER.md:1327-1347 uses the identity or a 45-degree
 // shear; reading R5 generalizes to any small unimodular M -- still an exact
 // relabeling).  xi_c places the box's k' range at [-floor(n/2), n - floor(n/2)).
-void build_geometry(int N, int W, std::vector<WedgeGeom>& wedges) {
+void build_geometry(int N, int W, std::vector<WedgeGeom>& wedges, double overlap) {
   wedges.assign(W, WedgeGeom());
   const double pi = 3.14159265358979323846;
   for (int l = 0; l < W; ++l) {
@@ -86,8 +121,22 @@ void build_geometry(int N, int W, std::vector<WedgeGeom>& wedges) {
     int x1 = k1 >= N / 2 ? k1 - N : k1;
     for (int k2 = 0; k2 < N; ++k2) {
       int x2 = k2 >= N / 2 ? k2 - N : k2;
-      int l = wedge_of(W, x1, x2);
-      if (l >= 0) wedges[l].members.push_back(k1 * N + k2);
+      if (!(overlap > 0.0)) {
+        int l = wedge_of(W, x1, x2);
+        if (l >= 0) wedges[l].members.push_back(k1 * N + k2);
+        continue;
+      }
+      // smooth partition: the (at most two) wedges with chi_l(xi) > 0 around the indicator's wedge
+      const int l0 = wedge_of(W, x1, x2);
+      if (l0 < 0) continue;
+      for (int dl = -1; dl <= 1; ++dl) {
+        const int l = (l0 + dl + W) % W;
+        const double c = wedge_weight(W, overlap, l, x1, x2);
+        if (c > 0.0) {
+          wedges[l].members.push_back(k1 * N + k2);
+          wedges[l].chi.push_back(c);
+        }
+      }
     }
   }
   std::vector<std::array<int, 4>> mats;
@@ -123,15 +172,11 @@ void build_geometry(int N, int W, std::vector<WedgeGeom>& wedges) {
   }
 }
 
-// Stockham radix sequence: 4s, then 2, 3s, 5s (all sizes 5-smooth).  Radix-8/16 butterflies
-// exist in the kernels but measured slower on B200 for these lengths (fewer butterflies per
-// stage than threads, higher register use); FIO_FFT_RADIX16=1 selects them.
+// Stockham radix sequence: 4s, then 2, 3s, 5s (all sizes 5-smooth).  (Radix-8/16 stages were
+// measured slower on B200 for these lengths -- fewer butterflies per stage than threads, more
+// registers -- and removed.)
 std::vector<int8_t> radix_plan(int L) {
   std::vector<int8_t> r;
-  if (const char* e = std::getenv("FIO_FFT_RADIX16"); e && std::atoi(e) == 1) {  // needs FIO_FFT_BIG_RADIX=1 build
-    while (L % 16 == 0) { r.push_back(16); L /= 16; }
-    while (L % 8 == 0) { r.push_back(8); L /= 8; }
-  }
   while (L % 4 == 0) { r.push_back(4); L /= 4; }
   while (L % 2 == 0) { r.push_back(2); L /= 2; }
   while (L % 3 == 0) { r.push_back(3); L /= 3; }

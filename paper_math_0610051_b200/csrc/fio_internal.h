@@ -26,7 +26,7 @@ constexpr int kMaxTaps = 12;  // up to eps ~ 1e-11 (reading R10)
 #define FIO_K3_P64 8
 #endif
 #ifndef FIO_K3_P128
-#define FIO_K3_P128 8
+#define FIO_K3_P128 4
 #endif
 #ifndef FIO_K3_BIGTAPS
 #define FIO_K3_BIGTAPS 8  // above this many taps the column weights of P points no longer fit: P = 4
@@ -50,7 +50,10 @@ constexpr int kK3BlockC128 = FIO_K3_BLOCK128;  // complex128
 #ifndef FIO_K3_CAP128
 #define FIO_K3_CAP128 512
 #endif
-constexpr int kK3Stages = 3;                    // cp.async pipeline depth of K3 (fine-grid tiles + alpha')
+#ifndef FIO_K3_STAGES
+#define FIO_K3_STAGES 3
+#endif
+constexpr int kK3Stages = FIO_K3_STAGES;        // pipeline depth of K3 (fine-grid tiles + alpha')
 constexpr int kK3TileCapC64 = FIO_K3_CAP64;     // max cells of a K3 chunk footprint, complex64
 constexpr int kK3TileCapC128 = FIO_K3_CAP128;   // complex128
 constexpr int kHalo = 8;  // periodic column halo on each side of a fine-grid row (K2 writes, K3 reads)
@@ -116,17 +119,24 @@ struct WedgeDev {
 // of the fine grid anchored at `anchor` covers all their taps.
 // The fine grid is stored [j2][kHalo + j1]: K3's "rows" are j2 (nrow = n2f, wrapped) and
 // its "columns" are j1 (ncol = n1f, haloed row stride ncolp = n1f + 2 kHalo).
+constexpr int kBoxInts = 8;  // one 32-byte box record per K3 chunk (a bulk-copy unit)
+// Physical position of slot k of group g: element-major inside each chunk of `block` groups,
+// [chunk][k][g mod block] -- the shared-memory image K3 reads conflict-free (lane = group).
+FIO_HD_EARLY inline long long k3_slot(long long g, int k, int P, int block) {
+  return (g / block) * block * P + (long long)k * block + g % block;
+}
+
 struct InterpWedge {
   int q, nrow, ncol, ngroups;
   int ncolp;
   long long g_off;          // element offset of this wedge's fine grids
   const int* anchor;        // 2 ints per group (a1, a2), may be negative (wrapped in K3)
-  const int* slot_x;        // P per group: flat output index, -1 = padding
-  const void* slot_off;     // P per group: (u1 - a1, u2 - a2) as float2 (c64) / double2 (c128)
-  const void* alpha;        // alpha'[t][group*P + k], plan dtype
+  const int* slot_x;        // per slot (k3_slot layout): flat output index, -1 = padding
+  const void* slot_off;     // per slot: (u1 - a1, u2 - a2) as float2 (c64) / double2 (c128)
+  const void* alpha;        // alpha'[t][slot] (k3_slot layout), plan dtype
   int nchunks;              // chunks of K3 BLOCK consecutive groups
   int tile_cap;             // max rows*cols of a chunk's window footprint (elements)
-  const int* box;           // 6 per chunk: first group, row origin, column origin, rows, columns, groups
+  const int* box;           // kBoxInts per chunk: first group, row origin, column origin, rows, columns, groups
 };
 
 // Work item of the batched FFT passes: one CTA processes `count` sequences of
@@ -144,6 +154,7 @@ struct alignas(32) FftJob {
 struct WedgeGeom {
   int l;
   std::vector<int> members;  // flat FFT-order frequency indices k1*N+k2
+  std::vector<double> chi;   // smooth partition: chi_l of every member (empty: the indicator, chi = 1)
   int M[4], Mi[4];
   int xc1, xc2;
   int n1, n2, n1f, n2f;
@@ -173,7 +184,8 @@ int default_wedges(int N);
 bool is_smooth5(int n);
 int next_fine_size(int extent);
 int wedge_of(int W, int xi1, int xi2);
-void build_geometry(int N, int W, std::vector<WedgeGeom>& wedges);
+void build_geometry(int N, int W, std::vector<WedgeGeom>& wedges, double overlap = 0.0);
+double wedge_weight(int W, double overlap, int l, int xi1, int xi2);  // chi_l(xi), reading R2
 std::vector<int8_t> radix_plan(int L);
 double es_kernel(double z, int w, double beta);
 double es_fourier(double s, int w, double beta);  // psi(s) = int phi(v) cos(2 pi s v) dv

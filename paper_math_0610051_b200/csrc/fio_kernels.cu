@@ -413,7 +413,7 @@ cudaError_t launch_fine_coords(const OperatorDev& op, const WedgeDev& w, double2
 template <typename T2>
 __global__ void k_fold_beta(int N, WedgeDev w, const int* __restrict__ members, int n,
                             const double2* __restrict__ beta, int q, const double* __restrict__ d1,
-                            const double* __restrict__ d2, T2* __restrict__ betap) {
+                            const double* __restrict__ d2, const double* __restrict__ chi, T2* __restrict__ betap) {
   long long total = (long long)n * q;
   const long long box = (long long)w.n1 * w.n2;
   for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < total;
@@ -426,19 +426,21 @@ __global__ void k_fold_beta(int N, WedgeDev w, const int* __restrict__ members, 
     int i2 = w.M[2] * xi1 + w.M[3] * xi2 - w.xc2 + w.n2 / 2;
     double2 b = beta[t + (long long)j * q];
     double d = d1[i1] * d2[i2];
+    if (chi) d *= chi[j];  // smooth partition weight chi_l(xi) (reading R2)
     betap[t * box + (long long)i1 * w.n2 + i2] = to_t2<T2>(make_double2(b.x * d, b.y * d));
   }
 }
 
 cudaError_t launch_fold_beta(int N, const WedgeDev& w, const int* members, int n, const double2* beta, int q,
-                             const double* d1, const double* d2, void* betap, bool c64, cudaStream_t s) {
+                             const double* d1, const double* d2, const double* chi, void* betap, bool c64,
+                             cudaStream_t s) {
   long long total = (long long)n * q;
   if (total == 0) return cudaSuccess;
   int blocks = (int)std::min<long long>((total + 255) / 256, 148LL * 16);
   if (c64)
-    k_fold_beta<float2><<<blocks, 256, 0, s>>>(N, w, members, n, beta, q, d1, d2, (float2*)betap);
+    k_fold_beta<float2><<<blocks, 256, 0, s>>>(N, w, members, n, beta, q, d1, d2, chi, (float2*)betap);
   else
-    k_fold_beta<double2><<<blocks, 256, 0, s>>>(N, w, members, n, beta, q, d1, d2, (double2*)betap);
+    k_fold_beta<double2><<<blocks, 256, 0, s>>>(N, w, members, n, beta, q, d1, d2, chi, (double2*)betap);
   return cudaGetLastError();
 }
 
@@ -487,68 +489,8 @@ __device__ __forceinline__ void dft_small(T2 (&v)[R], int sign) {
     v[4] = csub(m1, r1);
     v[2] = cadd(m2, r2);
     v[3] = csub(m2, r2);
-  } else if constexpr (R == 8) {
-    const Rt r2 = (Rt)0.70710678118654752440;
-    const Rt sg = (Rt)sign;
-    T2 a[4] = {v[0], v[2], v[4], v[6]};
-    T2 b[4] = {v[1], v[3], v[5], v[7]};
-    dft_small<T2, 4>(a, sign);
-    dft_small<T2, 4>(b, sign);
-    // b_k *= e^{sign 2 pi i k / 8}
-    b[1] = mk<T2>((b[1].x - sg * b[1].y) * r2, (b[1].y + sg * b[1].x) * r2);
-    b[2] = mul_i(b[2], sign);
-    b[3] = mk<T2>((-b[3].x - sg * b[3].y) * r2, (-b[3].y + sg * b[3].x) * r2);
-#pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      v[k] = cadd(a[k], b[k]);
-      v[k + 4] = csub(a[k], b[k]);
-    }
-  } else if constexpr (R == 16) {
-    // 16 = 4 x 4: inner DFT-4 over r1 (stride 4), twiddle w16^{r2 o1}, outer DFT-4 over r2
-    T2 y[4][4];
-#pragma unroll
-    for (int r2 = 0; r2 < 4; ++r2) {
-      T2 t[4] = {v[r2], v[4 + r2], v[8 + r2], v[12 + r2]};
-      dft_small<T2, 4>(t, sign);
-#pragma unroll
-      for (int o1 = 0; o1 < 4; ++o1) y[r2][o1] = t[o1];
-    }
-    const Rt C[10] = {(Rt)1, (Rt)0.92387953251128675613, (Rt)0.70710678118654752440, (Rt)0.38268343236508977173,
-                      (Rt)0, (Rt)-0.38268343236508977173, (Rt)-0.70710678118654752440,
-                      (Rt)-0.92387953251128675613, (Rt)-1, (Rt)-0.92387953251128675613};
-    const Rt S[10] = {(Rt)0, (Rt)0.38268343236508977173, (Rt)0.70710678118654752440, (Rt)0.92387953251128675613,
-                      (Rt)1, (Rt)0.92387953251128675613, (Rt)0.70710678118654752440, (Rt)0.38268343236508977173,
-                      (Rt)0, (Rt)-0.38268343236508977173};
-#pragma unroll
-    for (int r2 = 1; r2 < 4; ++r2)
-#pragma unroll
-      for (int o1 = 1; o1 < 4; ++o1) {
-        const int m = r2 * o1;
-        const Rt c = C[m], sn = (Rt)sign * S[m];
-        T2 u = y[r2][o1];
-        y[r2][o1] = mk<T2>(u.x * c - u.y * sn, u.x * sn + u.y * c);
-      }
-#pragma unroll
-    for (int o1 = 0; o1 < 4; ++o1) {
-      T2 t[4] = {y[0][o1], y[1][o1], y[2][o1], y[3][o1]};
-      dft_small<T2, 4>(t, sign);
-#pragma unroll
-      for (int o2 = 0; o2 < 4; ++o2) v[o1 + 4 * o2] = t[o2];
-    }
   }
 }
-
-// Radix-8/16 stages (compiled in with -DFIO_FFT_BIG_RADIX=1 and selected by FIO_FFT_RADIX16=1):
-// measured slower on B200 and their register footprint slows every FFT kernel, so off by default.
-#ifndef FIO_FFT_BIG_RADIX
-#define FIO_FFT_BIG_RADIX 0
-#endif
-#ifndef FIO_FFT_FAST_TWIDDLE
-#define FIO_FFT_FAST_TWIDDLE 1
-#endif
-#ifndef FIO_FFT_TW2
-#define FIO_FFT_TW2 0  // two-level shared twiddles for c128: measured no gain
-#endif
 
 __device__ __forceinline__ int fdiv(int n, const FastDiv& f) {
   return (int)((__umulhi(f.m, (unsigned)n) + (unsigned)n) >> f.l);
@@ -573,47 +515,20 @@ __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commi
 template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory"); }
 
-// Bank-conflict padding of the shared FFT buffers of the wedge passes: one empty slot after
-// every 128 bytes (8 complex128 / 16 complex64), so the stride-R writes of the early Stockham
-// stages hit distinct banks.  Sequence s, element e -> s * padded_len(L) + pad_idx(e).
-template <typename T2> struct PadShift;
-template <> struct PadShift<float2> { static constexpr int value = 4; };
-template <> struct PadShift<double2> { static constexpr int value = 3; };
-#ifndef FIO_K1_STAGE
-#define FIO_K1_STAGE 1  // measured: K1 c128 0.871 -> 0.813 ms, c64 0.297 -> 0.285 ms
-#endif
-#ifndef FIO_K1_GATHER
-#define FIO_K1_GATHER 0
-#endif
-#ifndef FIO_K2_STAGE
-#define FIO_K2_STAGE 1  // measured: K2 c128 1.355 -> 1.27 ms, c64 0.449 -> 0.427 ms
-#endif
 #ifndef FIO_K1_THREADS
 #define FIO_K1_THREADS 256
 #endif
 #ifndef FIO_K2_THREADS
 #define FIO_K2_THREADS 256
 #endif
-#ifndef FIO_FFT_TWPOW
-#define FIO_FFT_TWPOW 1  // twiddles w^r = (w^1)^r: c128 K1+K2 2.68 -> 2.37 ms (N=1024)
-#endif
-#ifndef FIO_FFT_PAD
-#define FIO_FFT_PAD 0  // measured neutral-to-slower on B200 (K2 c128 3.38 vs 3.26 ms): off
-#endif
-template <typename T2, bool PAD>
-__host__ __device__ __forceinline__ int pad_idx(int i) {
-  return (PAD && FIO_FFT_PAD) ? i + (i >> PadShift<T2>::value) : i;
-}
-template <typename T2, bool PAD>
-__host__ __device__ __forceinline__ int padded_len(int L) {
-  return (PAD && FIO_FFT_PAD) ? L + (L >> PadShift<T2>::value) + 1 : L;
-}
 
-template <typename T2, int R, bool PAD>
+// One radix-R Stockham stage over nseq sequences (element e of sequence q at q sb + e si).
+// Twiddles w_r = w_1^r: one table (complex128) or SFU (complex64, |error| ~ 1e-6, far below its
+// budget) twiddle per butterfly, the others by complex products (c128 K1+K2 2.68 -> 2.37 ms).
+template <typename T2, int R>
 __device__ __forceinline__ void stockham_stage(const T2* __restrict__ a, T2* __restrict__ b, int L, int Ns,
-                                               const FastDiv& dnb, const FastDiv& dns,
-                                               const T2* __restrict__ tw, const T2* __restrict__ tlo,
-                                               const T2* __restrict__ thi, int nseq, int si, int sb, int sign) {
+                                               const FastDiv& dnb, const FastDiv& dns, const T2* __restrict__ tw,
+                                               int nseq, int si, int sb, int sign) {
   const int nb = L / R;
   const int span = L / (Ns * R);
   const int total = nseq * nb;
@@ -627,78 +542,42 @@ __device__ __forceinline__ void stockham_stage(const T2* __restrict__ a, T2* __r
     T2* out = b + sq * sb;
     T2 v[R];
 #pragma unroll
-    for (int r = 0; r < R; ++r) v[r] = in[pad_idx<T2, PAD>((j + r * nb) * si)];
-#if FIO_FFT_TWPOW
-    if constexpr (!(sizeof(T2) == 16 && FIO_FFT_TW2)) {
-      // w_r = w_1^r: one table / SFU twiddle per butterfly, the others by complex products
-      T2 w1;
-      if constexpr (sizeof(T2) == 8 && FIO_FFT_FAST_TWIDDLE) {
-        float sn, cs;
-        __sincosf(wscale * (float)(k * span), &sn, &cs);
-        w1 = mk<T2>(cs, sn);
-      } else {
-        w1 = tw[k * span];
-      }
-      if (sign < 0) w1.y = -w1.y;
-      T2 wr = w1;
-#pragma unroll
-      for (int r = 1; r < R; ++r) {
-        v[r] = cmul(v[r], wr);
-        if (r + 1 < R) wr = cmul(wr, w1);
-      }
-    } else
-#endif
+    for (int r = 0; r < R; ++r) v[r] = in[(j + r * nb) * si];
+    T2 w1;
+    if constexpr (sizeof(T2) == 8) {
+      float sn, cs;
+      __sincosf(wscale * (float)(k * span), &sn, &cs);
+      w1 = mk<T2>(cs, sn);
+    } else {
+      w1 = tw[k * span];
+    }
+    if (sign < 0) w1.y = -w1.y;
+    T2 wr = w1;
 #pragma unroll
     for (int r = 1; r < R; ++r) {
-      T2 w;
-      if constexpr (sizeof(T2) == 8 && FIO_FFT_FAST_TWIDDLE) {
-        // complex64: e^{2 pi i m / L} from the SFU (|error| ~ 1e-6, far below the c64 budget)
-        float sn, cs;
-        __sincosf(wscale * (float)(r * k * span), &sn, &cs);
-        w = mk<T2>(cs, sn);
-      } else if constexpr (sizeof(T2) == 16 && FIO_FFT_TW2) {
-        // complex128: e^{2 pi i m/L} = lo[m mod 64] * hi[m / 64] from a shared two-level table
-        const int m = r * k * span;
-        w = cmul(tlo[m & 63], thi[m >> 6]);
-      } else {
-        w = tw[r * k * span];
-      }
-      if (sign < 0) w.y = -w.y;
-      v[r] = cmul(v[r], w);
+      v[r] = cmul(v[r], wr);
+      if (r + 1 < R) wr = cmul(wr, w1);
     }
     dft_small<T2, R>(v, sign);
     int base = jq * Ns * R + k;
 #pragma unroll
-    for (int r = 0; r < R; ++r) out[pad_idx<T2, PAD>((base + r * Ns) * si)] = v[r];
+    for (int r = 0; r < R; ++r) out[(base + r * Ns) * si] = v[r];
   }
 }
 
 // Returns the buffer holding the result (a or b).  Ends with __syncthreads().
-template <typename T2, bool PAD = false>
+template <typename T2>
 __device__ T2* smem_fft(T2* a, T2* b, const FftLen& fl, const T2* tw, int nseq, int si, int sb, int sign) {
-  // two-level twiddle tables (complex128): lo[j] = e^{2 pi i j/L}, hi[h] = e^{2 pi i 64 h/L}, L <= 4096
-  __shared__ T2 tw_lo[64], tw_hi[64];
-  if constexpr (sizeof(T2) == 16 && FIO_FFT_TW2) {
-    for (int j = threadIdx.x; j < 64; j += blockDim.x) {
-      if (j < fl.L) tw_lo[j] = tw[j];
-      if (64 * j < fl.L) tw_hi[j] = tw[64 * j];
-    }
-    __syncthreads();
-  }
   int Ns = 1;
   for (int st = 0; st < fl.nst; ++st) {
     const int R = fl.radix[st];
     const FastDiv& dnb = fl.div_nb[st];
     const FastDiv& dns = fl.div_ns[st];
     switch (R) {
-#if FIO_FFT_BIG_RADIX
-      case 16: stockham_stage<T2, 16, PAD>(a, b, fl.L, Ns, dnb, dns, tw, tw_lo, tw_hi, nseq, si, sb, sign); break;
-      case 8: stockham_stage<T2, 8, PAD>(a, b, fl.L, Ns, dnb, dns, tw, tw_lo, tw_hi, nseq, si, sb, sign); break;
-#endif
-      case 4: stockham_stage<T2, 4, PAD>(a, b, fl.L, Ns, dnb, dns, tw, tw_lo, tw_hi, nseq, si, sb, sign); break;
-      case 2: stockham_stage<T2, 2, PAD>(a, b, fl.L, Ns, dnb, dns, tw, tw_lo, tw_hi, nseq, si, sb, sign); break;
-      case 3: stockham_stage<T2, 3, PAD>(a, b, fl.L, Ns, dnb, dns, tw, tw_lo, tw_hi, nseq, si, sb, sign); break;
-      default: stockham_stage<T2, 5, PAD>(a, b, fl.L, Ns, dnb, dns, tw, tw_lo, tw_hi, nseq, si, sb, sign); break;
+      case 4: stockham_stage<T2, 4>(a, b, fl.L, Ns, dnb, dns, tw, nseq, si, sb, sign); break;
+      case 2: stockham_stage<T2, 2>(a, b, fl.L, Ns, dnb, dns, tw, nseq, si, sb, sign); break;
+      case 3: stockham_stage<T2, 3>(a, b, fl.L, Ns, dnb, dns, tw, nseq, si, sb, sign); break;
+      default: stockham_stage<T2, 5>(a, b, fl.L, Ns, dnb, dns, tw, nseq, si, sb, sign); break;
     }
     __syncthreads();
     T2* t = a;
@@ -729,11 +608,9 @@ __device__ __forceinline__ void stockham_stage_io(int L, int Ns, const FastDiv& 
     T2 v[R];
 #pragma unroll
     for (int r = 0; r < R; ++r) v[r] = load(sq, j + r * nb);
-    if (Ns > 1) {
-#if FIO_FFT_TWPOW
-      // w_r = w_1^r: one table / SFU twiddle per butterfly, the others by complex products
+    if (Ns > 1) {  // twiddles w_r = w_1^r (as in stockham_stage)
       T2 w1;
-      if constexpr (sizeof(T2) == 8 && FIO_FFT_FAST_TWIDDLE) {
+      if constexpr (sizeof(T2) == 8) {
         float sn, cs;
         __sincosf(wscale * (float)(k * span), &sn, &cs);
         w1 = mk<T2>(cs, sn);
@@ -747,21 +624,6 @@ __device__ __forceinline__ void stockham_stage_io(int L, int Ns, const FastDiv& 
         v[r] = cmul(v[r], wr);
         if (r + 1 < R) wr = cmul(wr, w1);
       }
-#else
-#pragma unroll
-      for (int r = 1; r < R; ++r) {
-        T2 w;
-        if constexpr (sizeof(T2) == 8 && FIO_FFT_FAST_TWIDDLE) {
-          float sn, cs;
-          __sincosf(wscale * (float)(r * k * span), &sn, &cs);
-          w = mk<T2>(cs, sn);
-        } else {
-          w = tw[r * k * span];
-        }
-        if (sign < 0) w.y = -w.y;
-        v[r] = cmul(v[r], w);
-      }
-#endif
     }
     dft_small<T2, R>(v, sign);
     const int base = jq * Ns * R + k;
@@ -887,7 +749,6 @@ __global__ void __launch_bounds__(FIO_K1_THREADS) k_rowpass(int N, const WedgeDe
   T2* a = reinterpret_cast<T2*>(smem_raw);
   T2* b = a + cnt * L;
   const T2* bet = betas[job.w] + ((long long)job.t * n1 + job.start) * n2;
-#if FIO_K1_STAGE
   {  // the job's beta' rows are one contiguous block of cnt n2 elements: stage it in the first buffer
     const int nel = cnt * n2;
     if constexpr (sizeof(T2) == 16) {
@@ -900,7 +761,6 @@ __global__ void __launch_bounds__(FIO_K1_THREADS) k_rowpass(int N, const WedgeDe
     __syncthreads();
     bet = a;
   }
-#endif
   const int hi = n2 - n2 / 2;  // fine index pos = k'_2 mod L holds box column i2 = k'_2 + n2/2
   // The first Stockham stage reads h straight from beta' and fhat (no zero fill / placement pass).
   const int h2 = n2 / 2, lo2 = L - h2;
@@ -913,38 +773,12 @@ __global__ void __launch_bounds__(FIO_K1_THREADS) k_rowpass(int N, const WedgeDe
     const int r1 = pow2 ? (xi1 & (N - 1)) : imod(xi1, N), r2 = pow2 ? (xi2 & (N - 1)) : imod(xi2, N);
     return r1 * N + r2;
   };
-#if FIO_K1_STAGE && FIO_K1_GATHER
-  // gather fhat for the member cells (beta' != 0) into the second half of the first buffer with
-  // cp.async, all in flight at once (the box is at most half of the fine row: 2 n2 <= L)
-  const T2* fg = nullptr;
-  if (2 * n2 <= L) {
-    T2* fs = a + cnt * n2;
-    const int nel = cnt * n2;
-    const FastDiv dn2 = make_fastdiv_dev((unsigned)n2);
-    for (int e = threadIdx.x; e < nel; e += blockDim.x) {
-      const T2 bv = bet[e];
-      if (bv.x != 0 || bv.y != 0) {
-        const int r = fdiv(e, dn2), i2 = e - r * n2;
-        if constexpr (sizeof(T2) == 16)
-          cp_async16(fs + e, fhat + fidx(r, i2));
-        else
-          cp_async8(fs + e, fhat + fidx(r, i2));
-      }
-    }
-    cp_async_commit();
-    cp_async_wait<0>();
-    __syncthreads();
-    fg = fs;
-  }
-#else
-  const T2* fg = nullptr;
-#endif
   auto load_h = [&](int r, int pos) -> T2 {
     const int i2 = pos < hi ? pos + h2 : pos - lo2;  // box column (valid iff pos < hi or pos >= L - n2/2)
     T2 out = mk<T2>(0, 0);
     if (pos < hi || pos >= lo2) {
       const T2 bv = bet[r * n2 + i2];
-      if (bv.x != 0 || bv.y != 0) out = cmul(bv, fg ? fg[r * n2 + i2] : fhat[fidx(r, i2)]);
+      if (bv.x != 0 || bv.y != 0) out = cmul(bv, fhat[fidx(r, i2)]);
     }
     return out;
   };
@@ -977,7 +811,6 @@ __global__ void __launch_bounds__(FIO_K2_THREADS) k_colpass(const WedgeDev* __re
   T2* b = a + C * L;
   const T2* src = p1 + w.p1_off + ((long long)job.t * w.n2f + c0) * n1;
   const int hi = n1 - n1 / 2;  // fine index pos = (i1 - n1/2) mod L
-#if FIO_K2_STAGE
   // the job's input is one contiguous block of C n1 elements: copy it into the (not yet used) first
   // ping-pong buffer with cp.async -- every thread keeps several copies in flight -- and let the
   // first Stockham stage read it from shared memory
@@ -993,9 +826,6 @@ __global__ void __launch_bounds__(FIO_K2_THREADS) k_colpass(const WedgeDev* __re
     __syncthreads();
   }
   const T2* srcs = a;
-#else
-  const T2* srcs = src;
-#endif
   // First stage reads the row-pass output; last stage writes the haloed fine-grid row.
   const int h1 = n1 / 2, lo1 = L - h1;
   auto load_p = [&](int c, int pos) -> T2 {
@@ -1135,23 +965,50 @@ template <> struct K3Cfg<float2> {
 };
 template <> struct K3Cfg<double2> {
 #ifndef FIO_K3_MINB128
-#define FIO_K3_MINB128 3
+#define FIO_K3_MINB128 4
 #endif
   static constexpr int BLOCK = kK3BlockC128, MINB = FIO_K3_MINB128;
 };
 
-// Shared memory of K3 (16-aligned sections).  Every per-thread array is stored in 16-byte units
-// with the thread index innermost -- [unit][thread][16 B] -- so a warp's vector loads hit 32
-// consecutive 16-byte units (no bank conflicts), and a thread's cp.async of its contiguous global
-// row (16-byte units in order) lands unit by unit:
-//   alpha' ring   [S][P/EPC][BLOCK] x 16 B   this thread's alpha'(t) for the S terms in flight
-//   row weights   [WINR][P/RPV][BLOCK] x 16 B  phi1 of every point (Rt: FP32 c64, FP64 c128)
-//   running sums  [P][BLOCK] T2                Lf(x_k) before this wedge (cp.async at chunk start)
-//   slots         [2][P/4][BLOCK] x 16 B       output index of every point (current, next chunk)
-//   offsets       [P/OPV][BLOCK] x 16 B        fine-grid offsets from the anchor (next chunk)
-//   anchors       [BLOCK] int2                 (next chunk)
-//   boxes         [2][8] int                   footprint box of the current and the next chunk
-//   tile ring     [S][cap] T2                  the chunk's footprint tile of G_lt per term in flight
+// ---- bulk copies (the TMA engine, cp.async.bulk) completing on shared-memory mbarriers
+__device__ __forceinline__ unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(unsigned long long* bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(unsigned long long* bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra WAIT_%=;\n}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+// global -> shared, `bytes` (multiple of 16, both addresses 16-byte aligned), completing on `bar`
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, unsigned long long* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+                   smem_u32(dst)),
+               "l"(src), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
+}
+
+// Shared memory of K3 (16-aligned sections).  Per-point arrays are element-major with the thread
+// index innermost -- [k][thread] -- the same order the plan stores them in global memory inside
+// each chunk (k3_slot), so one bulk copy per array fills them and a warp's loads of element k hit 32
+// consecutive words (no bank conflicts):
+//   alpha' ring   [S][P][BLOCK] T2        this chunk's alpha'(t) for the S terms in flight
+//   row weights   [WINR][P/RPV][BLOCK]x16B phi1 of every point (FP32 c64, FP64 c128), thread-written
+//   running sums  [P][BLOCK] T2           Lf(x_k) before this wedge (cp.async gathers at chunk start)
+//   slots         [2][P][BLOCK] int       output index of every point (current, next chunk)
+//   offsets       [P][BLOCK] O2           fine-grid offsets from the anchor (next chunk, bulk)
+//   anchors       [BLOCK] int2            (next chunk, bulk)
+//   boxes         [2][kBoxInts] int       footprint box of the current and the next chunk
+//   mbarriers     [S] tile+alpha' stages, [2] chunk tables
+//   tile ring     [S][cap] T2             the chunk's footprint tile of G_lt per term in flight
 template <typename T2, int TAPS, int P>
 struct K3Layout {
   using Rt = typename Real<T2>::type;
@@ -1165,31 +1022,26 @@ struct K3Layout {
   static constexpr size_t kOff = kSlot + al(sizeof(int) * 2 * BLOCK * P);
   static constexpr size_t kAnchor = kOff + al(sizeof(typename OffT<T2>::type) * BLOCK * P);
   static constexpr size_t kBox = kAnchor + al(sizeof(int2) * BLOCK);
-  static constexpr size_t kFixed = kBox + al(sizeof(int) * 16);
+  static constexpr size_t kBar = kBox + al(sizeof(int) * 2 * kBoxInts);
+  static constexpr size_t kFixed = kBar + al(8 * (kK3Stages + 2));
   static size_t bytes(long long cap) { return kFixed + sizeof(T2) * kK3Stages * (size_t)cap; }
 };
 
-// 16-byte unit u of thread t in a [unit][BLOCK] x 16 B array
-template <int BLOCK>
-__device__ __forceinline__ int unit16(int u, int t) {
-  return (u * BLOCK + t) * 16;
-}
-
 // K3: one CTA processes chunks of BLOCK consecutive groups (one group of up to P points per
 // thread; chunks are padded to BLOCK groups at plan time, so chunk c's groups are
-// [c BLOCK, (c+1) BLOCK)).  Per chunk the thread evaluates the interpolation weights of its points
+// [c BLOCK, (c+1) BLOCK)).  Per chunk every thread evaluates the interpolation weights of its points
 // once -- column weights phi2 into registers, row weights phi1 into shared memory -- and starts the
-// copy of its points' running sums Lf(x_k) into shared memory; then, for every term t, the CTA
-// stages with cp.async the chunk's footprint tile of G_lt (rows wrapped mod the fine grid, columns
-// from the haloed row layout) and each thread's alpha'(t) into a kK3Stages-deep ring, so global
-// latency overlaps the arithmetic of earlier terms.  Per group, term and window row i the thread
-// loads the row once and applies it to all P points:
+// copy of its points' running sums Lf(x_k); for every term t, warp 0 stages the chunk's footprint
+// tile of G_lt (one bulk copy per tile row, rows wrapped mod the fine grid, columns from the haloed
+// row layout) and the chunk's alpha'(t) (one bulk copy) into a kK3Stages-deep ring on an mbarrier,
+// so HBM/L2 latency overlaps the arithmetic of earlier terms.  Per group, term and window row i the
+// thread loads the row once and applies it to all P points:
 //   F_k += phi1_k[i] sum_j phi2_k[j] G_lt[a1 + i][a2 + j]
 //   acc_k += alpha'_lt(x_k) F_k
-// The next chunk's tables (anchors, slots, offsets, box) are prefetched during the current one.
-// Lf[x_k] is written (first wedge of the stream, + the DC term of rank 0) or read-modify-written:
-// each point occurs in exactly one group per wedge, so one launch per wedge is race-free and the
-// summation order over wedges is fixed (deterministic).
+// The next chunk's tables (anchors, box, slots, offsets: four bulk copies) are prefetched during the
+// current one.  Lf[x_k] is written (first wedge of the stream, + the DC term of rank 0) or
+// read-modify-written: each point occurs in exactly one group per wedge, so one launch per wedge is
+// race-free and the summation order over wedges is fixed (deterministic).
 template <typename T2, int TAPS, int P>
 __global__ void __launch_bounds__(K3Cfg<T2>::BLOCK, K3Cfg<T2>::MINB)
     k_interp_groups(InterpWedge iw, const T2* __restrict__ gbase, const double2* __restrict__ a0,
@@ -1202,20 +1054,21 @@ __global__ void __launch_bounds__(K3Cfg<T2>::BLOCK, K3Cfg<T2>::MINB)
   constexpr int WINR = k3_window_rows(TAPS, C64);
   constexpr int BLOCK = K3Cfg<T2>::BLOCK;
   constexpr int S = kK3Stages;
-  constexpr int EPC = 16 / (int)sizeof(T2);  // complex elements per 16-byte unit
   constexpr int RPV = 16 / (int)sizeof(Rt);  // row weights per 16-byte unit
-  constexpr int OPV = 16 / (int)sizeof(O2);  // offsets per 16-byte unit
-  static_assert(P % EPC == 0 && P % RPV == 0 && P % 4 == 0 && P % OPV == 0, "K3 group size");
+  static_assert(P % RPV == 0 && BLOCK % 32 == 0, "K3 group size");
   extern __shared__ __align__(16) unsigned char k3_smem[];
-  unsigned char* aring = k3_smem + L::kRing;
+  T2* aring = reinterpret_cast<T2*>(k3_smem + L::kRing);
   unsigned char* p1s = k3_smem + L::kP1;
   T2* lfb = reinterpret_cast<T2*>(k3_smem + L::kLf);
-  unsigned char* m_slot = k3_smem + L::kSlot;
-  unsigned char* m_off = k3_smem + L::kOff;
+  int* m_slot = reinterpret_cast<int*>(k3_smem + L::kSlot);
+  O2* m_off = reinterpret_cast<O2*>(k3_smem + L::kOff);
   int2* m_anchor = reinterpret_cast<int2*>(k3_smem + L::kAnchor);
   int* sbox = reinterpret_cast<int*>(k3_smem + L::kBox);
+  unsigned long long* bar_full = reinterpret_cast<unsigned long long*>(k3_smem + L::kBar);  // [S]
+  unsigned long long* bar_meta = bar_full + S;                                              // [2]
   T2* tring = reinterpret_cast<T2*>(k3_smem + L::kFixed);
-  const int tid = threadIdx.x;
+  const int tid = threadIdx.x, lane = tid & 31;
+  const bool producer = tid < 32;  // warp 0 issues the bulk copies
   const int cap = iw.tile_cap;
   const int nrow = iw.nrow, n2p = iw.ncolp, q = iw.q;  // K3 rows / haloed row length of G_lt
   const long long gstride = (long long)nrow * n2p;
@@ -1223,68 +1076,67 @@ __global__ void __launch_bounds__(K3Cfg<T2>::BLOCK, K3Cfg<T2>::MINB)
   const T2* __restrict__ G = gbase + iw.g_off + kHalo;
   const T2* __restrict__ alpha = reinterpret_cast<const T2*>(iw.alpha);
   const O2* __restrict__ offs = reinterpret_cast<const O2*>(iw.slot_off);
+  if (tid == 0) {
+    for (int s = 0; s < S + 2; ++s) mbar_init(bar_full + s, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  __syncthreads();
+  // chunk tables of chunk chn into buffer buf (warp 0; lane 0 arms the barrier first)
   auto prefetch_meta = [&](int chn, int buf) {
-    if (chn < iw.nchunks) {
-      const long long gn = (long long)chn * BLOCK + tid;
-      cp_async8(m_anchor + tid, iw.anchor + 2 * gn);
-#pragma unroll
-      for (int c = 0; c < P / 4; ++c) cp_async16(m_slot + unit16<BLOCK>(buf * (P / 4) + c, tid), iw.slot_x + gn * P + 4 * c);
-#pragma unroll
-      for (int c = 0; c < P / OPV; ++c) cp_async16(m_off + unit16<BLOCK>(c, tid), offs + gn * P + OPV * c);
-      if (tid < 3) cp_async8(sbox + 8 * buf + 2 * tid, iw.box + 6 * (long long)chn + 2 * tid);
-    }
+    if (chn >= iw.nchunks || !producer) return;
+    const long long c0 = (long long)chn * BLOCK * P;  // first physical slot of the chunk
+    constexpr unsigned kA = sizeof(int2) * BLOCK, kB = sizeof(int) * kBoxInts, kS = sizeof(int) * BLOCK * P,
+                       kO = sizeof(O2) * BLOCK * P;
+    if (lane == 0) mbar_expect_tx(bar_meta + buf, kA + kB + kS + kO);
+    __syncwarp();
+    if (lane == 0) bulk_g2s(m_anchor, iw.anchor + 2 * (long long)chn * BLOCK, kA, bar_meta + buf);
+    if (lane == 1) bulk_g2s(sbox + kBoxInts * buf, iw.box + (long long)kBoxInts * chn, kB, bar_meta + buf);
+    if (lane == 2) bulk_g2s(m_slot + buf * BLOCK * P, iw.slot_x + c0, kS, bar_meta + buf);
+    if (lane == 3) bulk_g2s(m_off, offs + c0, kO, bar_meta + buf);
   };
   prefetch_meta(blockIdx.x, 0);
-  cp_async_commit();
+  unsigned gterm = 0;  // terms staged by this CTA so far (stage = gterm % S, parity = (gterm / S) & 1)
   int it = 0;
   for (int ch = blockIdx.x; ch < iw.nchunks; ch += gridDim.x, ++it) {
     const int buf = it & 1;
-    cp_async_wait<0>();
-    __syncthreads();  // this chunk's tables are visible; every thread is done with the previous chunk
-    const int* cb = sbox + 8 * buf;  // first group, row origin, column origin, rows, columns, groups
+    mbar_wait(bar_meta + buf, (unsigned)(it >> 1) & 1u);
+    __syncthreads();  // every thread is done with the previous chunk (its ring slots may be refilled)
+    const int* cb = sbox + kBoxInts * buf;  // first group, row origin, column origin, rows, columns, groups
     const int br = cb[1], bc = cb[2], bnr = cb[3], bnc = cb[4];
-    const int cpr = bnc / EPC;  // 16-byte copies per tile row
-    const int tchunks = bnr * cpr;
-    const FastDiv dcpr = make_fastdiv_dev((unsigned)cpr);
-    const T2* __restrict__ al = alpha + ((long long)ch * BLOCK + tid) * P;
-    // the running sums Lf(x_k) of this thread's points, copied while the term loop runs
+    const unsigned tbytes = (unsigned)(bnr * bnc) * sizeof(T2);
+    const T2* __restrict__ al = alpha + (long long)ch * BLOCK * P;
+    const unsigned t0 = gterm;
+    // the running sums Lf(x_k) of this thread's points, gathered while the term loop runs
     if (!first) {
 #pragma unroll
-      for (int c = 0; c < P / 4; ++c) {
-        const int4 xv = *reinterpret_cast<const int4*>(m_slot + unit16<BLOCK>(buf * (P / 4) + c, tid));
-        const int xs4[4] = {xv.x, xv.y, xv.z, xv.w};
-#pragma unroll
-        for (int u = 0; u < 4; ++u)
-          if (xs4[u] >= 0) {
-            if constexpr (C64)
-              cp_async8(lfb + (4 * c + u) * BLOCK + tid, Lf + xs4[u]);
-            else
-              cp_async16(lfb + (4 * c + u) * BLOCK + tid, Lf + xs4[u]);
-          }
-      }
-    }
-    // stage term t into ring slot t % S: this thread's alpha'(t) and its share of the tile
-    auto issue = [&](int t, bool next_meta) {
-      if (t < q) {
-        const int st = t % S;
-        const T2* as = al + t * nslots;
-#pragma unroll
-        for (int c = 0; c < P / EPC; ++c) cp_async16(aring + unit16<BLOCK>(st * (P / EPC) + c, tid), as + EPC * c);
-        const T2* __restrict__ gt = G + t * gstride;
-        T2* tile = tring + st * cap;
-        for (int idx = tid; idx < tchunks; idx += BLOCK) {
-          const int rr = fdiv(idx, dcpr), cc = idx - rr * cpr;
-          int r = br + rr;
-          r = r < 0 ? r + nrow : (r >= nrow ? r - nrow : r);
-          cp_async16(tile + rr * bnc + cc * EPC, gt + ((long long)r * n2p + bc + cc * EPC));
+      for (int k = 0; k < P; ++k) {
+        const int x = m_slot[(buf * P + k) * BLOCK + tid];
+        if (x >= 0) {
+          if constexpr (C64)
+            cp_async8(lfb + k * BLOCK + tid, Lf + x);
+          else
+            cp_async16(lfb + k * BLOCK + tid, Lf + x);
         }
       }
-      // the next chunk's tables, issued once every thread has consumed the current offsets/anchors
-      if (next_meta) prefetch_meta(ch + gridDim.x, buf ^ 1);
       cp_async_commit();
+    }
+    // stage term t of this chunk (warp 0): alpha'(t) block and the tile rows, on bar_full[stage]
+    auto issue = [&](int t) {
+      if (t >= q || !producer) return;
+      const unsigned st = (t0 + t) % S;
+      if (lane == 0) mbar_expect_tx(bar_full + st, (unsigned)(sizeof(T2) * BLOCK * P) + tbytes);
+      __syncwarp();
+      if (lane == 0) bulk_g2s(aring + st * BLOCK * P, al + t * nslots, sizeof(T2) * BLOCK * P, bar_full + st);
+      const T2* __restrict__ gt = G + t * gstride;
+      T2* tile = tring + st * cap;
+      for (int rr = lane; rr < bnr; rr += 32) {
+        int r = br + rr;
+        r = r < 0 ? r + nrow : (r >= nrow ? r - nrow : r);
+        bulk_g2s(tile + rr * bnc, gt + ((long long)r * n2p + bc), (unsigned)bnc * sizeof(T2), bar_full + st);
+      }
     };
 #pragma unroll
-    for (int st = 0; st < S - 1; ++st) issue(st, false);
+    for (int s = 0; s < S - 1; ++s) issue(s);
     // weights of this thread's points: phi2 (columns) in registers, phi1 (rows) in shared memory
     const int2 an = m_anchor[tid];
     const int woff = (an.x - br) * bnc + (an.y - bc);
@@ -1292,14 +1144,10 @@ __global__ void __launch_bounds__(K3Cfg<T2>::BLOCK, K3Cfg<T2>::MINB)
     {
       Rt o1[P], o2[P];
 #pragma unroll
-      for (int c = 0; c < P / OPV; ++c) {
-        if constexpr (C64) {
-          const float4 v = *reinterpret_cast<const float4*>(m_off + unit16<BLOCK>(c, tid));
-          o1[2 * c] = v.x; o2[2 * c] = v.y; o1[2 * c + 1] = v.z; o2[2 * c + 1] = v.w;
-        } else {
-          const double2 v = *reinterpret_cast<const double2*>(m_off + unit16<BLOCK>(c, tid));
-          o1[c] = v.x; o2[c] = v.y;
-        }
+      for (int k = 0; k < P; ++k) {
+        const O2 o = m_off[k * BLOCK + tid];
+        o1[k] = o.x;
+        o2[k] = o.y;
       }
       {
         Rt w1[P][WINR];
@@ -1309,28 +1157,26 @@ __global__ void __launch_bounds__(K3Cfg<T2>::BLOCK, K3Cfg<T2>::MINB)
 #pragma unroll
           for (int c = 0; c < P / RPV; ++c) {
             if constexpr (sizeof(Rt) == 4)
-              *reinterpret_cast<float4*>(p1s + unit16<BLOCK>(i * (P / RPV) + c, tid)) =
+              *reinterpret_cast<float4*>(p1s + ((i * (P / RPV) + c) * BLOCK + tid) * 16) =
                   make_float4(w1[4 * c][i], w1[4 * c + 1][i], w1[4 * c + 2][i], w1[4 * c + 3][i]);
             else
-              *reinterpret_cast<double2*>(p1s + unit16<BLOCK>(i * (P / RPV) + c, tid)) =
+              *reinterpret_cast<double2*>(p1s + ((i * (P / RPV) + c) * BLOCK + tid) * 16) =
                   make_double2(w1[2 * c][i], w1[2 * c + 1][i]);
           }
       }
       axis_weights<TAPS, WIN, P>(o2, poly, p2);
     }
-    if (q == 0) {  // no term loop: fetch the next chunk's tables here
-      __syncthreads();
-      prefetch_meta(ch + gridDim.x, buf ^ 1);
-      cp_async_commit();
-    }
+    __syncthreads();  // every thread has read this chunk's anchors and offsets: the next chunk's may land
+    prefetch_meta(ch + gridDim.x, buf ^ 1);
     T2 acc[P];
 #pragma unroll
     for (int k = 0; k < P; ++k) acc[k] = mk<T2>(0, 0);
     for (int t = 0; t < q; ++t) {
-      cp_async_wait<S - 2>();
-      __syncthreads();  // term t staged by every thread; every thread is done with term t-1
-      issue(t + S - 1, t == 0);
-      const T2* __restrict__ win = tring + (t % S) * cap + woff;
+      if (t > 0) __syncthreads();  // every thread is done with term t-1: its stage may be refilled
+      issue(t + S - 1);
+      const unsigned st = (t0 + t) % S;
+      mbar_wait(bar_full + st, ((t0 + t) / S) & 1u);
+      const T2* __restrict__ win = tring + st * cap + woff;
       T2 F[P];
 #pragma unroll
       for (int k = 0; k < P; ++k) F[k] = mk<T2>(0, 0);
@@ -1343,10 +1189,10 @@ __global__ void __launch_bounds__(K3Cfg<T2>::BLOCK, K3Cfg<T2>::MINB)
 #pragma unroll
         for (int c = 0; c < P / RPV; ++c) {
           if constexpr (sizeof(Rt) == 4) {
-            const float4 a = *reinterpret_cast<const float4*>(p1s + unit16<BLOCK>(i * (P / RPV) + c, tid));
+            const float4 a = *reinterpret_cast<const float4*>(p1s + ((i * (P / RPV) + c) * BLOCK + tid) * 16);
             w1[4 * c] = a.x; w1[4 * c + 1] = a.y; w1[4 * c + 2] = a.z; w1[4 * c + 3] = a.w;
           } else {
-            const double2 a = *reinterpret_cast<const double2*>(p1s + unit16<BLOCK>(i * (P / RPV) + c, tid));
+            const double2 a = *reinterpret_cast<const double2*>(p1s + ((i * (P / RPV) + c) * BLOCK + tid) * 16);
             w1[2 * c] = a.x; w1[2 * c + 1] = a.y;
           }
         }
@@ -1358,34 +1204,30 @@ __global__ void __launch_bounds__(K3Cfg<T2>::BLOCK, K3Cfg<T2>::MINB)
           F[k] = cfma_real(w1[k], rr, F[k]);
         }
       }
-      const unsigned char* ring = aring + unit16<BLOCK>((t % S) * (P / EPC), tid);
+      const T2* ring = aring + st * BLOCK * P + tid;
 #pragma unroll
       for (int k = 0; k < P; ++k) {
-        const T2 av = *reinterpret_cast<const T2*>(ring + (k / EPC) * BLOCK * 16 + (k % EPC) * sizeof(T2));
+        const T2 av = ring[k * BLOCK];
         acc[k].x = fma(av.x, F[k].x, fma(-av.y, F[k].y, acc[k].x));
         acc[k].y = fma(av.x, F[k].y, fma(av.y, F[k].x, acc[k].y));
       }
     }
-    cp_async_wait<0>();  // the running sums (in the first copy group) have landed
+    gterm += q;
+    if (!first) cp_async_wait<0>();  // the running sums have landed
     T2 f0 = mk<T2>(0, 0);
     if (first && add_dc) f0 = fhat[0];
 #pragma unroll
-    for (int c = 0; c < P / 4; ++c) {
-      const int4 xv = *reinterpret_cast<const int4*>(m_slot + unit16<BLOCK>(buf * (P / 4) + c, tid));
-      const int xs4[4] = {xv.x, xv.y, xv.z, xv.w};
-#pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        const int k = 4 * c + u, x = xs4[u];
-        if (x < 0) continue;
-        T2 b0 = mk<T2>(0, 0);
-        if (!first) {
-          b0 = lfb[k * BLOCK + tid];
-        } else if (add_dc) {
-          const double2 d = a0[x];
-          b0 = mk<T2>((Rt)(d.x * (double)f0.x - d.y * (double)f0.y), (Rt)(d.x * (double)f0.y + d.y * (double)f0.x));
-        }
-        Lf[x] = mk<T2>(b0.x + acc[k].x, b0.y + acc[k].y);
+    for (int k = 0; k < P; ++k) {
+      const int x = m_slot[(buf * P + k) * BLOCK + tid];
+      if (x < 0) continue;
+      T2 b0 = mk<T2>(0, 0);
+      if (!first) {
+        b0 = lfb[k * BLOCK + tid];
+      } else if (add_dc) {
+        const double2 d = a0[x];
+        b0 = mk<T2>((Rt)(d.x * (double)f0.x - d.y * (double)f0.y), (Rt)(d.x * (double)f0.y + d.y * (double)f0.x));
       }
+      Lf[x] = mk<T2>(b0.x + acc[k].x, b0.y + acc[k].y);
     }
   }
 }
@@ -1615,7 +1457,8 @@ __global__ void __launch_bounds__(128) k_spread_groups(InterpWedge iw, T2* __res
     const int vg = base + lane;
     const bool valid = vg < nvg;
     const int grp = valid ? vg / SPLIT : 0;
-    const int s0 = grp * P + (vg - grp * SPLIT) * PH;  // first slot of this thread's points
+    const int k0 = (vg - grp * SPLIT) * PH;  // this thread's points: k0 .. k0 + PH - 1 of the group
+    constexpr int BLK = K3Cfg<T2>::BLOCK;    // slots in K3's physical layout (k3_slot)
     int a1 = 0, a2 = 0;
     if (valid) {
       a1 = iw.anchor[2 * grp];
@@ -1641,8 +1484,9 @@ __global__ void __launch_bounds__(128) k_spread_groups(InterpWedge iw, T2* __res
       o.x = (Rt)(0.5 * TAPS);
       o.y = (Rt)(0.5 * TAPS);
       if (valid) {
-        x = iw.slot_x[s0 + k];
-        o = offs[s0 + k];
+        const long long sl = k3_slot(grp, k0 + k, P, BLK);
+        x = iw.slot_x[sl];
+        o = offs[sl];
       }
       gx[k] = x >= 0 ? g[x] : mk<T2>(0, 0);
       o1[k] = o.x;
@@ -1655,7 +1499,7 @@ __global__ void __launch_bounds__(128) k_spread_groups(InterpWedge iw, T2* __res
     T2 anext[sizeof(T2) == 8 ? PH : 1];  // c64: alpha'(t+1), loaded one term ahead
     if constexpr (sizeof(T2) == 8) {
 #pragma unroll
-      for (int k = 0; k < PH; ++k) anext[k] = (valid && q > 0) ? alpha[(long long)s0 + k] : mk<T2>(0, 0);
+      for (int k = 0; k < PH; ++k) anext[k] = (valid && q > 0) ? alpha[k3_slot(grp, k0 + k, P, BLK)] : mk<T2>(0, 0);
     }
     for (int t = 0; t < q; ++t) {
       T2 c[PH];
@@ -1666,13 +1510,13 @@ __global__ void __launch_bounds__(128) k_spread_groups(InterpWedge iw, T2* __res
         if constexpr (sizeof(T2) == 8)
           av = anext[k];
         else
-          av = valid ? alpha[t * nslots + (long long)s0 + k] : mk<T2>(0, 0);
+          av = valid ? alpha[t * nslots + k3_slot(grp, k0 + k, P, BLK)] : mk<T2>(0, 0);
         c[k] = mk<T2>(av.x * gx[k].x + av.y * gx[k].y, av.x * gx[k].y - av.y * gx[k].x);
       }
       if constexpr (sizeof(T2) == 8) {
         if (t + 1 < q && valid) {
 #pragma unroll
-          for (int k = 0; k < PH; ++k) anext[k] = alpha[(t + 1) * nslots + (long long)s0 + k];
+          for (int k = 0; k < PH; ++k) anext[k] = alpha[(t + 1) * nslots + k3_slot(grp, k0 + k, P, BLK)];
         }
       }
       T2* __restrict__ rp = G + t * gstride + (long long)r0 * n2p + a2;
@@ -1722,7 +1566,7 @@ __global__ void __launch_bounds__(256) k_colpass_adj(const WedgeDev* __restrict_
   const WedgeDev& w = wedges[job.w];
   const FftLen& fl = ffts[job.fft];
   const int L = fl.L, n1 = w.n1, C = job.count, c0 = job.start;
-  const int Lp = padded_len<T2, true>(L);
+  const int Lp = L;
   T2* a = reinterpret_cast<T2*>(smem_raw);
   T2* b = a + C * Lp;
   const int rowp = L + 2 * kHalo;
@@ -1733,17 +1577,17 @@ __global__ void __launch_bounds__(256) k_colpass_adj(const WedgeDev* __restrict_
       T2 v = rp[j1];
       if (j1 < kHalo) v = cadd(v, rp[L + j1]);        // right halo holds columns 0..kHalo-1
       if (j1 >= L - kHalo) v = cadd(v, rp[j1 - L]);   // left halo holds columns L-kHalo..L-1
-      a[c * Lp + pad_idx<T2, true>(j1)] = v;
+      a[c * Lp + j1] = v;
     }
   }
   __syncthreads();
-  T2* res = smem_fft<T2, true>(a, b, fl, tw + fl.tw_off, C, 1, Lp, -1);
+  T2* res = smem_fft<T2>(a, b, fl, tw + fl.tw_off, C, 1, Lp, -1);
   T2* dst = p1 + w.p1_off + ((long long)job.t * w.n2f + c0) * n1;
   for (int c = 0; c < C; ++c)
     for (int i1 = threadIdx.x; i1 < n1; i1 += blockDim.x) {
       int pos = i1 - n1 / 2;
       pos = pos < 0 ? pos + L : pos;
-      dst[(long long)c * n1 + i1] = res[c * Lp + pad_idx<T2, true>(pos)];
+      dst[(long long)c * n1 + i1] = res[c * Lp + pos];
     }
 }
 
@@ -1753,13 +1597,14 @@ __global__ void __launch_bounds__(256) k_rowpass_adj(int N, const WedgeDev* __re
                                                      const FftJob* __restrict__ jobs, const FftLen* __restrict__ ffts,
                                                      const T2* __restrict__ tw, const T2* const* __restrict__ betas,
                                                      const unsigned char* const* __restrict__ masks,
-                                                     const T2* __restrict__ p1, T2* __restrict__ fhat) {
+                                                     const T2* __restrict__ p1, T2* __restrict__ fhat,
+                                                     int accumulate) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const FftJob job = jobs[blockIdx.x];
   const WedgeDev& w = wedges[job.w];
   const FftLen& fl = ffts[job.fft];
   const int L = fl.L, n1 = w.n1, n2 = w.n2, cnt = job.count;
-  const int Lp = padded_len<T2, true>(L);
+  const int Lp = L;
   T2* a = reinterpret_cast<T2*>(smem_raw);
   T2* b = a + cnt * Lp;
   T2* acc = b + cnt * Lp;
@@ -1770,17 +1615,17 @@ __global__ void __launch_bounds__(256) k_rowpass_adj(int N, const WedgeDev* __re
     __syncthreads();
     for (int idx = threadIdx.x; idx < cnt * L; idx += blockDim.x) {
       const int j2 = fdiv(idx, dc), r = idx - j2 * cnt;
-      a[r * Lp + pad_idx<T2, true>(j2)] = src[(long long)j2 * n1 + r];
+      a[r * Lp + j2] = src[(long long)j2 * n1 + r];
     }
     __syncthreads();
-    T2* res = smem_fft<T2, true>(a, b, fl, tw + fl.tw_off, cnt, 1, Lp, -1);
+    T2* res = smem_fft<T2>(a, b, fl, tw + fl.tw_off, cnt, 1, Lp, -1);
     const T2* bet = betas[job.w] + ((long long)t * n1 + job.start) * n2;
     for (int r = 0; r < cnt; ++r)
       for (int i2 = threadIdx.x; i2 < n2; i2 += blockDim.x) {
         const T2 bv = bet[r * n2 + i2];
         int pos = i2 - n2 / 2;
         pos = pos < 0 ? pos + L : pos;
-        const T2 h = res[r * Lp + pad_idx<T2, true>(pos)];
+        const T2 h = res[r * Lp + pos];
         T2 v = acc[r * n2 + i2];
         v.x += bv.x * h.x + bv.y * h.y;  // conj(beta') h
         v.y += bv.x * h.y - bv.y * h.x;
@@ -1795,7 +1640,11 @@ __global__ void __launch_bounds__(256) k_rowpass_adj(int N, const WedgeDev* __re
       const int kp1 = job.start + r - n1 / 2, kp2 = i2 - n2 / 2;
       const int z1 = kp1 + w.xc1, z2 = kp2 + w.xc2;
       const int xi1 = w.Mi[0] * z1 + w.Mi[1] * z2, xi2 = w.Mi[2] * z1 + w.Mi[3] * z2;
-      fhat[(long long)imod(xi1, N) * N + imod(xi2, N)] = acc[r * n2 + i2];
+      T2* dst = fhat + (long long)imod(xi1, N) * N + imod(xi2, N);
+      if (accumulate)  // smooth partition: up to two wedges carry this xi (fhat* zeroed first)
+        red_add(dst, acc[r * n2 + i2]);
+      else
+        *dst = acc[r * n2 + i2];  // indicator wedges: each xi belongs to exactly one wedge
     }
 }
 
@@ -1893,7 +1742,8 @@ static cudaError_t enqueue_adjoint_t(const ApplyArgs& a, const T2* g, T2* out, c
     ++n;
     const T2* const* betas = reinterpret_cast<const T2* const*>(a.beta);
     k_rowpass_adj<T2><<<a.njobs_rowadj, 256, a.smem_rowadj, s>>>(a.N, a.wedges, a.jobs_rowadj, a.ffts, tw, betas,
-                                                                a.masks, reinterpret_cast<const T2*>(a.p1), fhat);
+                                                                a.masks, reinterpret_cast<const T2*>(a.p1), fhat,
+                                                                a.overlap);
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
     ++n;
   }
@@ -1922,8 +1772,8 @@ cudaError_t enqueue_adjoint(const ApplyArgs& a, bool c64, const void* g, void* o
 }
 
 size_t fft_seq_bytes(int L, bool c64) {
-  return c64 ? 2 * (size_t)padded_len<float2, true>(L) * sizeof(float2)
-             : 2 * (size_t)padded_len<double2, true>(L) * sizeof(double2);
+  return c64 ? 2 * (size_t)L * sizeof(float2)
+             : 2 * (size_t)L * sizeof(double2);
 }
 
 cudaError_t configure_kernels(size_t smem_bytes) {

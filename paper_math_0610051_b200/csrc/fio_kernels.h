@@ -50,7 +50,8 @@ cudaError_t launch_fine_coords(const OperatorDev& op, const WedgeDev& w, double2
 // (zero elsewhere; chi_l, the relabeling xi' = M xi - xi_c and the NUFFT
 // deconvolution folded).
 cudaError_t launch_fold_beta(int N, const WedgeDev& w, const int* members, int n, const double2* beta, int q,
-                             const double* d1, const double* d2, void* betap, bool c64, cudaStream_t s);
+                             const double* d1, const double* d2, const double* chi, void* betap, bool c64,
+                             cudaStream_t s);
 
 // Skeleton storage: per owned wedge the skeleton columns C (member
 // frequency indices) and Y = V S^{-1} (rc x q, column-major, FP64).
@@ -113,6 +114,7 @@ struct ApplyArgs {
   const int* row_job_off;
   const int* col_job_off;
   int sms;                  // multiprocessors of the plan's device (grid sizing)
+  int overlap;              // smooth partition: wedges overlap, K1* accumulates fhat* atomically
   int rows_per_cta_N;       // K0 row pass
   int cols_per_cta_N;       // K0 column pass
 };

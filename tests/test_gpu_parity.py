@@ -634,3 +634,66 @@ def test_eps_floors_are_rejected():
         make_plan(op, eps=1e-12, dtype="c128")
     make_plan(op, eps=1e-6, dtype="c64")  # at the floors: accepted
     make_plan(op, eps=1e-11, dtype="c128")
+
+
+# ------------------------------------------------------------------ smooth polar-wedge partition (reading R2)
+@pytest.mark.parametrize("name,full", [("cfg0", True), ("cfg1", True), ("cfg2", False), ("cfg3_c64", False),
+                                       ("cfg3_c128", False)])
+def test_smooth_partition_configs(name, full):
+    # sum_l chi_l = 1: the smooth taper changes the wedges, not L
+    cfg = wl.config(name)
+    op, f = wl.make_operator(cfg), wl.make_input(cfg)
+    plan, out = run(op, f, eps=cfg["eps"], dtype=cfg["dtype"], wedge_overlap=0.25)
+    assert plan.info["wedge_overlap"] == 0.25 and plan.info["members"] > op.N ** 2 - 1
+    if full:
+        ref, got = oracle.fio(op, f), out
+    else:
+        pts = wl.sample_points(op.N, 4096, 1)
+        ref, got = oracle.fio(op, f, pts=pts), out.ravel()[pts]
+    err, mx = _pointwise(got, ref)
+    print(f"smooth {name}: rel l2 {err:.3e} max/rms {mx:.3e} sum_q {plan.info['sum_q']} "
+          f"members {plan.info['members']} fine {plan.info['fine_elems']}")
+    assert err <= 10 * cfg["eps"] and mx <= 100 * cfg["eps"], (err, mx)
+
+
+def test_smooth_partition_partials_and_adjoint():
+    # rank r's partial is L applied to (sum of its chi_l) fhat -- the oracle with its own chi -- and the
+    # adjoint (whose K1* now accumulates the two wedges sharing a frequency) stays the exact transpose
+    N, ov = 64, 0.5
+    op = wl.grt_operator(N)
+    f = wl.white_noise(N, 0)
+    fh = oracle.dft2(f)
+    chi = oracle.smooth_wedge_weights(N, 16, ov)
+    plan, part = run(op, f, rank=1, nranks=3, n_wedges=16, wedge_overlap=ov)
+    ws = plan.wedges()["l"]
+    ref = oracle.fio(op, fhat=fh * chi[list(ws)].sum(0))
+    assert oracle.rel_l2(part, ref) <= 1e-5
+    full = make_plan(op, n_wedges=16, wedge_overlap=ov)
+    a, b = crandn(N, 71), crandn(N, 72)
+    La = full.apply(torch.from_numpy(a).to(DEV)).cpu().numpy()
+    Lsb = full.apply_adjoint(torch.from_numpy(b).to(DEV)).cpu().numpy()
+    assert abs(np.vdot(b, La) - np.vdot(Lsb, a)) <= 1e-12 * np.linalg.norm(a) * np.linalg.norm(b) * N
+    assert oracle.rel_l2(Lsb, adjoint_ref(op, b)) <= 1e-5
+
+
+# ------------------------------------------------------------------ the paper's own experiment (Table tbl:result_a)
+@pytest.mark.parametrize("N", [64, 128])
+def test_paper_table_result_a_replay(N):
+    # PAPER.md:1440-1458 (eq. nrphase: ellipse radii r1, r2), white noise, eps = 10 N^-2, error measured on
+    # the full grid against the direct sum; the paper prints (Table tbl:result_a) the
+    # errors 2.08e-3 (N = 64) and 8.02e-4 (N = 128) for its own Matlab run -- a loose pin: ours must be
+    # of the same order and inside the 10 eps bar
+    import json
+    import os
+    rows = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "spec_examples.json")))[
+        "paper_table_result_a"]["rows"]
+    paper = {int(r[0]): (r[1], r[2]) for r in rows}
+    eps, printed = paper[N]
+    assert abs(eps - 10.0 / N ** 2) < 1e-3 * eps
+    op = wl.paper_ellipse_operator(N)
+    f = wl.white_noise(N, 0)
+    plan, out = run(op, f, eps=eps)
+    err = oracle.rel_l2(out, oracle.fio(op, f))
+    print(f"Table tbl:result_a replay N={N}: eps {eps:.3g}, error {err:.3g} (paper {printed:.3g}), "
+          f"W {plan.info['W']} sum_q {plan.info['sum_q']}")
+    assert err <= 10 * eps and printed / 20 <= err <= 5 * printed, (err, printed)

@@ -119,3 +119,23 @@ def test_plan_load_rejects_missing_and_malformed_files(tmp_path):
     bad.write_bytes(b"not a plan file at all" * 8)
     st = lib.fio_plan_load(ctypes.byref(h), str(bad).encode(), N, ctypes.byref(ph), ctypes.byref(amp), 1e-6, None)
     assert st == -1 and b"not a valid plan file" in lib.fio_last_error()
+
+
+@pytest.mark.parametrize("W,ov", [(16, 0.25), (8, 1.0), (24, 0.6), (16, 0.0)])
+def test_product_partition_weights_match_oracle(W, ov):
+    # the product's chi_l (C++, fio_partition_weights) against the oracle's independent numpy version
+    # of the same definition (reading R2); overlap 0 is the paper's indicator
+    N = 48
+    xi1, xi2 = wl.freqs(N)
+    ref = oracle.smooth_wedge_weights(N, W, ov) if ov > 0 else None
+    for a in range(N):
+        for b in range(N):
+            got = fio.partition_weights(W, ov, int(xi1[a, b]), int(xi2[a, b]))
+            if ov > 0:
+                np.testing.assert_allclose(got, ref[:, a, b], atol=1e-13)
+            else:
+                exp_ = np.zeros(W)
+                l = oracle.wedge_of(W, int(xi1[a, b]), int(xi2[a, b]))
+                if l >= 0:
+                    exp_[l] = 1.0
+                assert np.array_equal(got, exp_)

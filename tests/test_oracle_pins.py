@@ -406,3 +406,52 @@ def test_adjoint_pairing_all_branches(name):
         other = wl.bessel_grt_operator(N, -op.sign)
         bad = np.vdot(oracle.fio_adjoint_hat(other, g), oracle.dft2(f))
         assert abs(lhs - bad) > 1e-3 * abs(lhs)
+
+
+# ------------------------------------------------------------------ smooth polar-wedge partition (reading R2)
+@pytest.mark.parametrize("N,W,ov", [(64, 8, 0.25), (64, 16, 1.0), (40, 12, 0.5)])
+def test_smooth_partition_of_unity(N, W, ov):
+    # sum_l chi_l = 1 on Omega \ {0} (PAPER.md:236-238 needs only this), 0 <= chi <= 1, at most two
+    # wedges overlap, and away from the tapers chi_l is the paper's indicator wedge
+    chi = oracle.smooth_wedge_weights(N, W, ov)
+    tot = chi.sum(0)
+    tot[0, 0] = 1.0
+    assert np.abs(tot - 1).max() < 1e-13  # rounding of the wrapped angle at the 0 / 2 pi seam
+    assert chi.min() >= 0 and chi.max() <= 1
+    assert (chi > 0).sum(0).max() <= 2
+    xi1, xi2 = wl.freqs(N)
+    th = np.arctan2(xi2, xi1)
+    D = 2 * np.pi / W
+    d = np.mod(th + D / 2, D)                  # angle above the last boundary ray
+    far = (np.minimum(d, D - d) > 0.5 * ov * D + 1e-9)
+    far[0, 0] = False
+    for a, b in zip(*np.nonzero(far)):
+        l = wedge_by_cross_products(W, int(xi1[a, b]), int(xi2[a, b]))
+        assert chi[l, a, b] == 1.0 and chi[:, a, b].sum() == 1.0, (a, b, l)
+
+
+def test_smooth_partition_boundary_center_and_rotation():
+    # chi_l = 1/2 on the paper's boundary rays (2l +- 1) pi / W, 1 at the wedge centre, and
+    # chi_l(theta) = chi_0(theta - 2 pi l / W) (rotation covariance)
+    W, ov = 16, 0.3
+    D = 2 * np.pi / W
+    for l in range(W):
+        assert abs(oracle.smooth_chi_angle(W, ov, l, (l - 0.5) * D) - 0.5) < 1e-15
+        assert abs(oracle.smooth_chi_angle(W, ov, l, (l + 0.5) * D) - 0.5) < 1e-15
+        assert oracle.smooth_chi_angle(W, ov, l, l * D) == 1.0
+    th = np.linspace(-np.pi, np.pi, 2001)
+    for l in (1, 5, 11):
+        np.testing.assert_allclose(oracle.smooth_chi_angle(W, ov, l, th), oracle.smooth_chi_angle(W, ov, 0, th - l * D),
+                                   atol=1e-14)
+
+
+def test_smooth_step_is_smooth():
+    # S is C-infinity: finite differences of S and S' are continuous across the taper edges and S'
+    # vanishes at tau = +-1 (no kink where the taper meets the indicator)
+    t = np.linspace(-1.5, 1.5, 30001)
+    s = oracle._smooth_step(t)
+    d1 = np.gradient(s, t)
+    d2 = np.gradient(d1, t)
+    assert np.abs(np.diff(d1)).max() < 1e-2 and np.abs(np.diff(d2)).max() < 0.5
+    assert abs(d1[np.searchsorted(t, -1.0)]) < 1e-12 and abs(d1[np.searchsorted(t, 1.0)]) < 1e-12
+    np.testing.assert_allclose(s + oracle._smooth_step(-t), 1.0, atol=1e-15)

@@ -68,10 +68,17 @@ def main():
         if os.path.exists(d):
             shutil.rmtree(d)
         shutil.copytree(ROOT, d, ignore=shutil.ignore_patterns(".git", "gpurun_out", "profiles", "*.ncu-rep"))
+        if spec.split("=", 1)[-1].split("@")[0] == "" :
+            pass  # product build: the in-tree .so is rebuilt below with no extra flags
+        runenv = {}
+        if "@" in flags:  # NAME=FLAGS@ENV=V,ENV2=V2: run-time environment of the variant
+            flags, e = flags.split("@", 1)
+            runenv = dict(kv.split("=", 1) for kv in e.split(",") if kv)
         env = dict(os.environ, FIO_NVCC_FLAGS=flags)
         subprocess.check_call([sys.executable, "-c", "from paper_math_0610051_b200 import build; build.build(force=True)"],
                               cwd=d, env=env)
-        r = subprocess.run([sys.executable, "-c", CHILD, d, configs, steps], cwd=d, capture_output=True, text=True)
+        r = subprocess.run([sys.executable, "-c", CHILD, d, configs, steps], cwd=d, capture_output=True, text=True,
+                           env=dict(os.environ, **runenv))
         line = [l for l in r.stdout.splitlines() if l.startswith("RESULT ")]
         out[name] = {"flags": flags, **(json.loads(line[0][7:]) if line else {"error": r.stderr[-2000:]})}
         print(name, json.dumps(out[name]), flush=True)
