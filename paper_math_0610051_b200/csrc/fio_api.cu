@@ -137,15 +137,8 @@ struct fio_plan_s {
   int rows_per_cta_N = 1, cols_per_cta_N = 1, fft_N = 0;
   void *e2e_in = nullptr, *e2e_out = nullptr;
   void* batch_ws = nullptr;  // (nrhs - 1) x (fhat + fine grids + K3 accumulator) for fio_apply_batch
-  int k3_streams = 1;  // concurrent K3 streams (wedge wi on stream wi % k3_streams)
-  cudaStream_t side[kMaxK3Streams - 1] = {};
-  cudaEvent_t ev_fork = nullptr, ev_join[kMaxK3Streams - 1] = {};
-  void* acc_extra = nullptr;  // (k3_streams - 2) x N*N accumulators beyond tmp
-  int pipe_batches = 0;       // pipelined K1/K2 || K3 (0: off)
-  cudaStream_t fft_stream = nullptr;
-  cudaEvent_t ev_k0 = nullptr;
-  cudaEvent_t ev_batch[kMaxPipeBatches] = {};
-  std::vector<int> row_job_off, col_job_off;  // per owned wedge: first job in jobs_row / jobs_col
+  cudaStream_t side = nullptr;  // plan-owned side stream (skeleton-mode K3, adjoint spreads)
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   int batch_cap = 1;
   size_t alpha_bytes = 0, beta_bytes = 0, ws_bytes = 0, fine_elems = 0, p1_elems = 0, meta_bytes = 0;
   long long slots = 0;
@@ -200,14 +193,8 @@ struct fio_plan_s {
   ~fio_plan_s() {
     free_events();
     if (ev_fork) cudaEventDestroy(ev_fork);
-    if (ev_k0) cudaEventDestroy(ev_k0);
-    for (cudaEvent_t e : ev_batch)
-      if (e) cudaEventDestroy(e);
-    if (fft_stream) cudaStreamDestroy(fft_stream);
-    for (int j = 0; j + 1 < kMaxK3Streams; ++j) {
-      if (ev_join[j]) cudaEventDestroy(ev_join[j]);
-      if (side[j]) cudaStreamDestroy(side[j]);
-    }
+    if (ev_join) cudaEventDestroy(ev_join);
+    if (side) cudaStreamDestroy(side);
     if (batch_ws) cudaFree(batch_ws);
     if (part) cudaFree(part);
     comm_destroy(comm);
@@ -1087,8 +1074,6 @@ fio_status build_plan(fio_plan_s& P, const fio_phase* phase, const fio_amplitude
     int cols = (int)std::max<size_t>(1, std::min<size_t>(max_cols, kSmemBudgetCol / sc));
     cols = std::min(cols, w.n2f);
     rows = std::min(rows, w.n1);
-    P.row_job_off.push_back((int)jr.size());
-    P.col_job_off.push_back((int)jc.size());
     for (int i = 0; i < w.n1; i += rows) {
       const int cnt = std::min(rows, w.n1 - i);
       jra.push_back({(int)wi, 0, i, cnt, w.fft2, {0, 0, 0}});
@@ -1109,8 +1094,6 @@ fio_status build_plan(fio_plan_s& P, const fio_phase* phase, const fio_amplitude
     set_error("fine grid too large for the shared-memory FFT (N too large for this dtype)");
     return FIO_EINVAL;
   }
-  P.row_job_off.push_back((int)jr.size());
-  P.col_job_off.push_back((int)jc.size());
   P.smem_row = (int)smem_row;
   P.smem_col = (int)smem_col;
   P.njobs_row = (int)jr.size();
@@ -1138,29 +1121,13 @@ fio_status build_plan(fio_plan_s& P, const fio_phase* phase, const fio_amplitude
   FIO_CUDA(P.upload(&P.d_wedges, P.wd.data(), std::max<size_t>(P.wd.size(), 1)));
   FIO_CUDA(P.upload(&P.d_beta, P.beta_ptrs.data(), std::max<size_t>(P.beta_ptrs.size(), 1)));
   FIO_CUDA(P.alloc(&P.fhat, cs * NN));
-  FIO_CUDA(P.alloc(&P.tmp, cs * NN));
-  {  // concurrent K3 streams (measured on B200, N = 1024: 1 -> 2 streams c128 18.1 -> 16.2 ms)
-    int ns = kDefaultK3Streams;
-    if (const char* env = std::getenv("FIO_K3_STREAMS")) ns = std::atoi(env);
-    P.k3_streams = std::max(1, std::min(ns, kMaxK3Streams));
-    FIO_CUDA(cudaEventCreateWithFlags(&P.ev_fork, cudaEventDisableTiming));
-    for (int j = 0; j + 1 < P.k3_streams; ++j) {
-      FIO_CUDA(cudaStreamCreateWithFlags(&P.side[j], cudaStreamNonBlocking));
-      FIO_CUDA(cudaEventCreateWithFlags(&P.ev_join[j], cudaEventDisableTiming));
-    }
-    if (P.k3_streams > 2) FIO_CUDA(P.alloc(&P.acc_extra, cs * NN * (P.k3_streams - 2)));
-    int nb = kDefaultPipeBatches;
-    if (const char* env = std::getenv("FIO_PIPE_BATCHES")) nb = std::atoi(env);
-    P.pipe_batches = std::max(0, std::min(nb, kMaxPipeBatches));
-    if (P.pipe_batches > 1) {
-      FIO_CUDA(cudaStreamCreateWithFlags(&P.fft_stream, cudaStreamNonBlocking));
-      FIO_CUDA(cudaEventCreateWithFlags(&P.ev_k0, cudaEventDisableTiming));
-      for (int b = 0; b < P.pipe_batches; ++b) FIO_CUDA(cudaEventCreateWithFlags(&P.ev_batch[b], cudaEventDisableTiming));
-    }
-  }
+  FIO_CUDA(P.alloc(&P.tmp, cs * NN));  // K0's scratch, then K3's second accumulator
+  FIO_CUDA(cudaEventCreateWithFlags(&P.ev_fork, cudaEventDisableTiming));
+  FIO_CUDA(cudaEventCreateWithFlags(&P.ev_join, cudaEventDisableTiming));
+  FIO_CUDA(cudaStreamCreateWithFlags(&P.side, cudaStreamNonBlocking));
   FIO_CUDA(P.alloc(&P.p1, cs * std::max<size_t>(P.p1_elems, 1)));
   FIO_CUDA(P.alloc(&P.g, cs * std::max<size_t>(P.fine_elems, 1)));
-  P.ws_bytes = cs * (2 * NN + P.p1_elems + P.fine_elems + NN * (size_t)std::max(0, P.k3_streams - 2));
+  P.ws_bytes = cs * (2 * NN + P.p1_elems + P.fine_elems);
   FIO_CUDA(cudaDeviceSynchronize());
   return FIO_OK;
 }
@@ -1185,23 +1152,10 @@ ApplyArgs make_args(const fio_plan_s& P) {
   a.poly = &P.poly;
   a.fhat = P.fhat;
   a.tmp = P.tmp;
-  a.k3_streams = P.k3_streams;
-  for (int j = 0; j + 1 < kMaxK3Streams; ++j) {
-    // accumulator 0 is K0's scratch (free once K3 starts), the others are acc_extra
-    a.acc[j] = j == 0 ? P.tmp
-                      : (j + 1 < P.k3_streams ? static_cast<char*>(P.acc_extra) + (j - 1) * a.N * (size_t)a.N *
-                                                                                     (P.c64 ? 8 : 16)
-                                              : nullptr);
-    a.side[j] = P.side[j];
-    a.join[j] = P.ev_join[j];
-  }
+  a.acc[0] = P.tmp;  // the second K3 accumulator is K0's scratch (free once K3 starts)
+  a.side[0] = P.side;
+  a.join[0] = P.ev_join;
   a.fork = P.ev_fork;
-  a.pipe_batches = P.pipe_batches;
-  a.fft_stream = P.fft_stream;
-  a.ev_k0 = P.ev_k0;
-  a.ev_batch = P.ev_batch;
-  a.row_job_off = P.row_job_off.empty() ? nullptr : P.row_job_off.data();
-  a.col_job_off = P.col_job_off.empty() ? nullptr : P.col_job_off.data();
   a.p1 = P.p1;
   a.g = P.g;
   a.jobs_row = P.jobs_row;
@@ -1546,7 +1500,7 @@ fio_status fio_apply_batch(fio_handle h, int nrhs, const void* f_dev, void* Lf_d
   FIO_GUARD(h->device)
   const size_t cs = h->c64 ? sizeof(float2) : sizeof(double2);
   const size_t NN = (size_t)h->N * h->N;
-  const size_t nacc = (size_t)std::max(0, h->k3_streams - 1);
+  const size_t nacc = 1;  // K3's second accumulator
   const size_t per = NN + std::max<size_t>(h->fine_elems, 1) + nacc * NN;
   if (nrhs > h->batch_cap) {
     FIO_CUDA(cudaStreamSynchronize((cudaStream_t)stream));
@@ -1562,7 +1516,7 @@ fio_status fio_apply_batch(fio_handle h, int nrhs, const void* f_dev, void* Lf_d
     char* base = static_cast<char*>(h->batch_ws) + cs * per * (size_t)(b - 1);
     args[b].fhat = base;
     args[b].g = base + cs * NN;
-    for (size_t j = 0; j < nacc; ++j) args[b].acc[j] = base + cs * (NN + std::max<size_t>(h->fine_elems, 1) + j * NN);
+    args[b].acc[0] = base + cs * (NN + std::max<size_t>(h->fine_elems, 1));
   }
   int launches = 0;
   cudaStream_t s = (cudaStream_t)stream;
@@ -1696,7 +1650,7 @@ fio_status fio_plan_info(fio_handle h, fio_info* info) {
   info->group_p = group_p(h->c64, h->taps);
   info->skeleton_bytes = h->skel_bytes;
   info->k3_window_cols = k3_window_cols(h->taps, h->c64);
-  info->k3_streams = h->k3_streams;
+  info->k3_streams = 2;  // K3 launches alternate between the caller's stream and the side stream
   info->k3_window_rows = k3_window_rows(h->taps, h->c64);
   info->beta_bytes = h->beta_bytes;
   info->workspace_bytes = h->ws_bytes;

@@ -322,9 +322,12 @@ void lpt_assign(int W, const double* cost, int nranks, int* owner) {
 // one along the "run" axis (columns when kSuperCols == 2, rows when kSuperRows == 2).  Points are
 // counting-sorted by (fixed axis, run axis, x) and cut greedily: a group takes the next points while
 // they share the fixed-axis base and lie within two run-axis bases of the group's first point (its
-// anchor), up to P points.  Sliding anchors (instead of a fixed supercell lattice) keep the groups
-// full: only a run's last group can be partly empty.  Groups are then ordered in serpentine
+// anchor), up to P points.  complex128 slides the anchor (only a run's last group can be partly
+// empty); complex64 keeps a fixed lattice of two-column supercells, whose even anchors make every
+// window row a run of 16-byte aligned pairs (vector loads).  Groups are then ordered in serpentine
 // 16 x 16-cell blocks of their anchors, so a K3 chunk (consecutive groups) has a compact footprint.
+static inline long long floor_div2(long long b) { return b >= 0 ? b / 2 : -((-b + 1) / 2); }
+
 void group_points(const double* u, long long NN, int taps, int P, int n1f, int n2f, int kSuperRows, int kSuperCols,
                   std::vector<int>& anchor, std::vector<int>& slot_x, std::vector<double>& off) {
   const bool run_cols = kSuperCols == 2;  // c64: runs along columns within a base row
@@ -363,7 +366,9 @@ void group_points(const double* u, long long NN, int taps, int P, int n1f, int n
     while (e < NN && e - p < P) {
       const int x = order[e];
       const int maj = run_cols ? b1v[x] : b2v[x], mn = run_cols ? b2v[x] : b1v[x];
-      if (maj != maj0 || mn > mn0 + 1) break;
+      // complex64 (runs along columns): fixed two-column supercells, so every anchor column is even
+      // (16-byte aligned window rows); complex128: sliding pairs of base rows
+      if (maj != maj0 || (run_cols ? (floor_div2(mn) != floor_div2(mn0)) : (mn > mn0 + 1))) break;
       ++e;
     }
     gstart.push_back(p);
@@ -397,12 +402,14 @@ void group_points(const double* u, long long NN, int taps, int P, int n1f, int n
     const int x0 = order[p];
     const int a1 = b1v[x0], a2 = b2v[x0];
     // anchor = the window's first fine cell: the smallest base on each axis among the members
+    // (complex64: the supercell's even column)
     int m1 = a1, m2 = a2;
     for (int j = 0; j < gcount[g]; ++j) {
       const int x = order[p + j];
       m1 = std::min(m1, b1v[x]);
       m2 = std::min(m2, b2v[x]);
     }
+    if (run_cols) m2 = (int)(2 * floor_div2(a2));
     anchor[2 * i] = m1;
     anchor[2 * i + 1] = m2;
     for (int j = 0; j < gcount[g]; ++j) {

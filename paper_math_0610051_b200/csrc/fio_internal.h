@@ -23,7 +23,7 @@ constexpr int kMaxTaps = 12;  // up to eps ~ 1e-11 (reading R10)
 // once per term from shared memory and applies it to all P points (register reuse P: the shared ->
 // register path, 128 B/clk/SM, is K3's binding on-chip resource).
 #ifndef FIO_K3_P64
-#define FIO_K3_P64 8
+#define FIO_K3_P64 4
 #endif
 #ifndef FIO_K3_P128
 #define FIO_K3_P128 4

@@ -959,7 +959,7 @@ template <typename T2, int TAPS> struct GroupP { static constexpr int value = gr
 template <typename T2> struct K3Cfg;
 template <> struct K3Cfg<float2> {
 #ifndef FIO_K3_MINB64
-#define FIO_K3_MINB64 5
+#define FIO_K3_MINB64 8
 #endif
   static constexpr int BLOCK = kK3BlockC64, MINB = FIO_K3_MINB64;
 };
@@ -970,45 +970,18 @@ template <> struct K3Cfg<double2> {
   static constexpr int BLOCK = kK3BlockC128, MINB = FIO_K3_MINB128;
 };
 
-// ---- bulk copies (the TMA engine, cp.async.bulk) completing on shared-memory mbarriers
-__device__ __forceinline__ unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
-__device__ __forceinline__ void mbar_init(unsigned long long* bar, unsigned count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count) : "memory");
-}
-__device__ __forceinline__ void mbar_expect_tx(unsigned long long* bar, unsigned bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(bytes)
-               : "memory");
-}
-__device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned parity) {
-  asm volatile(
-      "{\n\t.reg .pred p;\n"
-      "WAIT_%=:\n\t"
-      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
-      "@!p bra WAIT_%=;\n}\n" ::"r"(smem_u32(bar)),
-      "r"(parity)
-      : "memory");
-}
-// global -> shared, `bytes` (multiple of 16, both addresses 16-byte aligned), completing on `bar`
-__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, unsigned long long* bar) {
-  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
-                   smem_u32(dst)),
-               "l"(src), "r"(bytes), "r"(smem_u32(bar))
-               : "memory");
-}
-
 // Shared memory of K3 (16-aligned sections).  Per-point arrays are element-major with the thread
-// index innermost -- [k][thread] -- the same order the plan stores them in global memory inside
-// each chunk (k3_slot), so one bulk copy per array fills them and a warp's loads of element k hit 32
-// consecutive words (no bank conflicts):
-//   alpha' ring   [S][P][BLOCK] T2        this chunk's alpha'(t) for the S terms in flight
-//   row weights   [WINR][P/RPV][BLOCK]x16B phi1 of every point (FP32 c64, FP64 c128), thread-written
-//   running sums  [P][BLOCK] T2           Lf(x_k) before this wedge (cp.async gathers at chunk start)
-//   slots         [2][P][BLOCK] int       output index of every point (current, next chunk)
-//   offsets       [P][BLOCK] O2           fine-grid offsets from the anchor (next chunk, bulk)
-//   anchors       [BLOCK] int2            (next chunk, bulk)
-//   boxes         [2][kBoxInts] int       footprint box of the current and the next chunk
-//   mbarriers     [S] tile+alpha' stages, [2] chunk tables
-//   tile ring     [S][cap] T2             the chunk's footprint tile of G_lt per term in flight
+// index innermost -- [k][thread] -- the same order the plan stores them in global memory inside each
+// chunk (k3_slot): the CTA copies a chunk's block with coalesced 16-byte cp.async units and a warp's
+// loads of element k hit 32 consecutive words (no bank conflicts):
+//   alpha' ring   [S][P][BLOCK] T2          the chunk's alpha'(t) for the S terms in flight
+//   row weights   [WINR][P/RPV][BLOCK]x16B  phi1 of every point (FP32 c64, FP64 c128), thread-written
+//   running sums  [P][BLOCK] T2             Lf(x_k) before this wedge (cp.async gathers)
+//   slots         [2][P][BLOCK] int         output index of every point (current, next chunk)
+//   offsets       [P][BLOCK] O2             fine-grid offsets from the anchor (next chunk)
+//   anchors       [BLOCK] int2              (next chunk)
+//   boxes         [2][kBoxInts] int         footprint box of the current and the next chunk
+//   tile ring     [S][cap] T2               the chunk's footprint tile of G_lt per term in flight
 template <typename T2, int TAPS, int P>
 struct K3Layout {
   using Rt = typename Real<T2>::type;
@@ -1022,26 +995,33 @@ struct K3Layout {
   static constexpr size_t kOff = kSlot + al(sizeof(int) * 2 * BLOCK * P);
   static constexpr size_t kAnchor = kOff + al(sizeof(typename OffT<T2>::type) * BLOCK * P);
   static constexpr size_t kBox = kAnchor + al(sizeof(int2) * BLOCK);
-  static constexpr size_t kBar = kBox + al(sizeof(int) * 2 * kBoxInts);
-  static constexpr size_t kFixed = kBar + al(8 * (kK3Stages + 2));
+  static constexpr size_t kFixed = kBox + al(sizeof(int) * 2 * kBoxInts);
   static size_t bytes(long long cap) { return kFixed + sizeof(T2) * kK3Stages * (size_t)cap; }
 };
 
-// K3: one CTA processes chunks of BLOCK consecutive groups (one group of up to P points per
-// thread; chunks are padded to BLOCK groups at plan time, so chunk c's groups are
-// [c BLOCK, (c+1) BLOCK)).  Per chunk every thread evaluates the interpolation weights of its points
-// once -- column weights phi2 into registers, row weights phi1 into shared memory -- and starts the
-// copy of its points' running sums Lf(x_k); for every term t, warp 0 stages the chunk's footprint
-// tile of G_lt (one bulk copy per tile row, rows wrapped mod the fine grid, columns from the haloed
-// row layout) and the chunk's alpha'(t) (one bulk copy) into a kK3Stages-deep ring on an mbarrier,
-// so HBM/L2 latency overlaps the arithmetic of earlier terms.  Per group, term and window row i the
-// thread loads the row once and applies it to all P points:
+// `bytes` (a multiple of 16) from global to shared memory by the whole CTA, 16-byte cp.async units
+template <int BLOCK>
+__device__ __forceinline__ void cta_copy16(void* dst, const void* src, int bytes) {
+  char* d = static_cast<char*>(dst);
+  const char* s = static_cast<const char*>(src);
+  for (int u = threadIdx.x; u < bytes / 16; u += BLOCK) cp_async16(d + 16 * u, s + 16 * u);
+}
+
+// K3: one CTA processes chunks of BLOCK consecutive groups (one group of up to P points per thread;
+// chunks are padded to BLOCK groups at plan time, so chunk c's groups are [c BLOCK, (c+1) BLOCK)).
+// Per chunk every thread evaluates the interpolation weights of its points once -- column weights
+// phi2 in registers, row weights phi1 in shared memory -- and starts the copy of its points' running
+// sums Lf(x_k); then, for every term t, the CTA stages with cp.async the chunk's footprint tile of
+// G_lt (rows wrapped mod the fine grid, columns from the haloed row layout; every thread copies a
+// fixed set of 16-byte units whose addresses it computes once per chunk) and the chunk's alpha'(t)
+// block into a kK3Stages-deep ring, so global latency overlaps the arithmetic of earlier terms.
+// Per group, term and window row i the thread loads the row once and applies it to all P points:
 //   F_k += phi1_k[i] sum_j phi2_k[j] G_lt[a1 + i][a2 + j]
 //   acc_k += alpha'_lt(x_k) F_k
-// The next chunk's tables (anchors, box, slots, offsets: four bulk copies) are prefetched during the
-// current one.  Lf[x_k] is written (first wedge of the stream, + the DC term of rank 0) or
-// read-modify-written: each point occurs in exactly one group per wedge, so one launch per wedge is
-// race-free and the summation order over wedges is fixed (deterministic).
+// The next chunk's tables (anchors, box, slots, offsets) are prefetched during the current one.
+// Lf[x_k] is written (first wedge of the stream, + the DC term of rank 0) or read-modify-written:
+// each point occurs in exactly one group per wedge, so one launch per wedge is race-free and the
+// summation order over wedges is fixed (deterministic).
 template <typename T2, int TAPS, int P>
 __global__ void __launch_bounds__(K3Cfg<T2>::BLOCK, K3Cfg<T2>::MINB)
     k_interp_groups(InterpWedge iw, const T2* __restrict__ gbase, const double2* __restrict__ a0,
@@ -1054,8 +1034,10 @@ __global__ void __launch_bounds__(K3Cfg<T2>::BLOCK, K3Cfg<T2>::MINB)
   constexpr int WINR = k3_window_rows(TAPS, C64);
   constexpr int BLOCK = K3Cfg<T2>::BLOCK;
   constexpr int S = kK3Stages;
+  constexpr int EPC = 16 / (int)sizeof(T2);  // complex elements per 16-byte unit
   constexpr int RPV = 16 / (int)sizeof(Rt);  // row weights per 16-byte unit
-  static_assert(P % RPV == 0 && BLOCK % 32 == 0, "K3 group size");
+  constexpr int MAXC = C64 ? kK3TileCapC64 / 2 / BLOCK : kK3TileCapC128 / BLOCK;  // tile units per thread
+  static_assert(P % RPV == 0, "K3 group size");
   extern __shared__ __align__(16) unsigned char k3_smem[];
   T2* aring = reinterpret_cast<T2*>(k3_smem + L::kRing);
   unsigned char* p1s = k3_smem + L::kP1;
@@ -1064,11 +1046,8 @@ __global__ void __launch_bounds__(K3Cfg<T2>::BLOCK, K3Cfg<T2>::MINB)
   O2* m_off = reinterpret_cast<O2*>(k3_smem + L::kOff);
   int2* m_anchor = reinterpret_cast<int2*>(k3_smem + L::kAnchor);
   int* sbox = reinterpret_cast<int*>(k3_smem + L::kBox);
-  unsigned long long* bar_full = reinterpret_cast<unsigned long long*>(k3_smem + L::kBar);  // [S]
-  unsigned long long* bar_meta = bar_full + S;                                              // [2]
   T2* tring = reinterpret_cast<T2*>(k3_smem + L::kFixed);
-  const int tid = threadIdx.x, lane = tid & 31;
-  const bool producer = tid < 32;  // warp 0 issues the bulk copies
+  const int tid = threadIdx.x;
   const int cap = iw.tile_cap;
   const int nrow = iw.nrow, n2p = iw.ncolp, q = iw.q;  // K3 rows / haloed row length of G_lt
   const long long gstride = (long long)nrow * n2p;
@@ -1076,36 +1055,47 @@ __global__ void __launch_bounds__(K3Cfg<T2>::BLOCK, K3Cfg<T2>::MINB)
   const T2* __restrict__ G = gbase + iw.g_off + kHalo;
   const T2* __restrict__ alpha = reinterpret_cast<const T2*>(iw.alpha);
   const O2* __restrict__ offs = reinterpret_cast<const O2*>(iw.slot_off);
-  if (tid == 0) {
-    for (int s = 0; s < S + 2; ++s) mbar_init(bar_full + s, 1);
-    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
-  }
-  __syncthreads();
-  // chunk tables of chunk chn into buffer buf (warp 0; lane 0 arms the barrier first)
+  constexpr int kA = sizeof(int2) * BLOCK, kB = sizeof(int) * kBoxInts, kS = sizeof(int) * BLOCK * P,
+                kO = sizeof(O2) * BLOCK * P, kAl = sizeof(T2) * BLOCK * P;
   auto prefetch_meta = [&](int chn, int buf) {
-    if (chn >= iw.nchunks || !producer) return;
-    const long long c0 = (long long)chn * BLOCK * P;  // first physical slot of the chunk
-    constexpr unsigned kA = sizeof(int2) * BLOCK, kB = sizeof(int) * kBoxInts, kS = sizeof(int) * BLOCK * P,
-                       kO = sizeof(O2) * BLOCK * P;
-    if (lane == 0) mbar_expect_tx(bar_meta + buf, kA + kB + kS + kO);
-    __syncwarp();
-    if (lane == 0) bulk_g2s(m_anchor, iw.anchor + 2 * (long long)chn * BLOCK, kA, bar_meta + buf);
-    if (lane == 1) bulk_g2s(sbox + kBoxInts * buf, iw.box + (long long)kBoxInts * chn, kB, bar_meta + buf);
-    if (lane == 2) bulk_g2s(m_slot + buf * BLOCK * P, iw.slot_x + c0, kS, bar_meta + buf);
-    if (lane == 3) bulk_g2s(m_off, offs + c0, kO, bar_meta + buf);
+    if (chn < iw.nchunks) {
+      const long long c0 = (long long)chn * BLOCK * P;  // first physical slot of the chunk
+      cta_copy16<BLOCK>(m_anchor, iw.anchor + 2 * (long long)chn * BLOCK, kA);
+      cta_copy16<BLOCK>(sbox + kBoxInts * buf, iw.box + (long long)kBoxInts * chn, kB);
+      cta_copy16<BLOCK>(m_slot + buf * BLOCK * P, iw.slot_x + c0, kS);
+      cta_copy16<BLOCK>(m_off, offs + c0, kO);
+    }
   };
   prefetch_meta(blockIdx.x, 0);
-  unsigned gterm = 0;  // terms staged by this CTA so far (stage = gterm % S, parity = (gterm / S) & 1)
+  cp_async_commit();
   int it = 0;
   for (int ch = blockIdx.x; ch < iw.nchunks; ch += gridDim.x, ++it) {
     const int buf = it & 1;
-    mbar_wait(bar_meta + buf, (unsigned)(it >> 1) & 1u);
-    __syncthreads();  // every thread is done with the previous chunk (its ring slots may be refilled)
+    cp_async_wait<0>();
+    __syncthreads();  // this chunk's tables are visible; every thread is done with the previous chunk
     const int* cb = sbox + kBoxInts * buf;  // first group, row origin, column origin, rows, columns, groups
     const int br = cb[1], bc = cb[2], bnr = cb[3], bnc = cb[4];
-    const unsigned tbytes = (unsigned)(bnr * bnc) * sizeof(T2);
+    const int cpr = bnc / EPC;  // 16-byte units per tile row
+    const int tchunks = bnr * cpr;
     const T2* __restrict__ al = alpha + (long long)ch * BLOCK * P;
-    const unsigned t0 = gterm;
+    // this thread's share of every tile copy, fixed for the chunk: source offsets within G_lt (row
+    // wrapped mod the fine grid) and destination offsets within the tile
+    int csrc[MAXC], cdst[MAXC];
+    int ncp = 0;
+#pragma unroll
+    for (int u = 0; u < MAXC; ++u) {
+      const int idx = tid + u * BLOCK;
+      csrc[u] = 0;
+      cdst[u] = 0;
+      if (idx < tchunks) {
+        const int rr = idx / cpr, cc = idx - rr * cpr;
+        int r = br + rr;
+        r = r < 0 ? r + nrow : (r >= nrow ? r - nrow : r);
+        csrc[u] = r * n2p + bc + cc * EPC;
+        cdst[u] = rr * bnc + cc * EPC;
+        ncp = u + 1;
+      }
+    }
     // the running sums Lf(x_k) of this thread's points, gathered while the term loop runs
     if (!first) {
 #pragma unroll
@@ -1118,25 +1108,24 @@ __global__ void __launch_bounds__(K3Cfg<T2>::BLOCK, K3Cfg<T2>::MINB)
             cp_async16(lfb + k * BLOCK + tid, Lf + x);
         }
       }
-      cp_async_commit();
     }
-    // stage term t of this chunk (warp 0): alpha'(t) block and the tile rows, on bar_full[stage]
-    auto issue = [&](int t) {
-      if (t >= q || !producer) return;
-      const unsigned st = (t0 + t) % S;
-      if (lane == 0) mbar_expect_tx(bar_full + st, (unsigned)(sizeof(T2) * BLOCK * P) + tbytes);
-      __syncwarp();
-      if (lane == 0) bulk_g2s(aring + st * BLOCK * P, al + t * nslots, sizeof(T2) * BLOCK * P, bar_full + st);
-      const T2* __restrict__ gt = G + t * gstride;
-      T2* tile = tring + st * cap;
-      for (int rr = lane; rr < bnr; rr += 32) {
-        int r = br + rr;
-        r = r < 0 ? r + nrow : (r >= nrow ? r - nrow : r);
-        bulk_g2s(tile + rr * bnc, gt + ((long long)r * n2p + bc), (unsigned)bnc * sizeof(T2), bar_full + st);
+    // stage term t into ring slot t % S: the chunk's alpha'(t) block and the tile
+    auto issue = [&](int t, bool next_meta) {
+      if (t < q) {
+        const int st = t % S;
+        cta_copy16<BLOCK>(aring + st * BLOCK * P, al + t * nslots, kAl);
+        const T2* __restrict__ gt = G + t * gstride;
+        T2* tile = tring + st * cap;
+#pragma unroll
+        for (int u = 0; u < MAXC; ++u)
+          if (u < ncp) cp_async16(tile + cdst[u], gt + csrc[u]);
       }
+      // the next chunk's tables, issued once every thread has consumed the current offsets/anchors
+      if (next_meta) prefetch_meta(ch + gridDim.x, buf ^ 1);
+      cp_async_commit();
     };
 #pragma unroll
-    for (int s = 0; s < S - 1; ++s) issue(s);
+    for (int s = 0; s < S - 1; ++s) issue(s, false);
     // weights of this thread's points: phi2 (columns) in registers, phi1 (rows) in shared memory
     const int2 an = m_anchor[tid];
     const int woff = (an.x - br) * bnc + (an.y - bc);
@@ -1155,56 +1144,68 @@ __global__ void __launch_bounds__(K3Cfg<T2>::BLOCK, K3Cfg<T2>::MINB)
 #pragma unroll
         for (int i = 0; i < WINR; ++i)
 #pragma unroll
-          for (int c = 0; c < P / RPV; ++c) {
+          for (int cc = 0; cc < P / RPV; ++cc) {
             if constexpr (sizeof(Rt) == 4)
-              *reinterpret_cast<float4*>(p1s + ((i * (P / RPV) + c) * BLOCK + tid) * 16) =
-                  make_float4(w1[4 * c][i], w1[4 * c + 1][i], w1[4 * c + 2][i], w1[4 * c + 3][i]);
+              *reinterpret_cast<float4*>(p1s + ((i * (P / RPV) + cc) * BLOCK + tid) * 16) =
+                  make_float4(w1[4 * cc][i], w1[4 * cc + 1][i], w1[4 * cc + 2][i], w1[4 * cc + 3][i]);
             else
-              *reinterpret_cast<double2*>(p1s + ((i * (P / RPV) + c) * BLOCK + tid) * 16) =
-                  make_double2(w1[2 * c][i], w1[2 * c + 1][i]);
+              *reinterpret_cast<double2*>(p1s + ((i * (P / RPV) + cc) * BLOCK + tid) * 16) =
+                  make_double2(w1[2 * cc][i], w1[2 * cc + 1][i]);
           }
       }
       axis_weights<TAPS, WIN, P>(o2, poly, p2);
     }
-    __syncthreads();  // every thread has read this chunk's anchors and offsets: the next chunk's may land
-    prefetch_meta(ch + gridDim.x, buf ^ 1);
+    if (q == 0) {  // no term loop: fetch the next chunk's tables here
+      __syncthreads();
+      prefetch_meta(ch + gridDim.x, buf ^ 1);
+      cp_async_commit();
+    }
     T2 acc[P];
 #pragma unroll
     for (int k = 0; k < P; ++k) acc[k] = mk<T2>(0, 0);
     for (int t = 0; t < q; ++t) {
-      if (t > 0) __syncthreads();  // every thread is done with term t-1: its stage may be refilled
-      issue(t + S - 1);
-      const unsigned st = (t0 + t) % S;
-      mbar_wait(bar_full + st, ((t0 + t) / S) & 1u);
-      const T2* __restrict__ win = tring + st * cap + woff;
+      cp_async_wait<S - 2>();
+      __syncthreads();  // term t staged by every thread; every thread is done with term t-1
+      issue(t + S - 1, t == 0);
+      const T2* __restrict__ win = tring + (t % S) * cap + woff;
       T2 F[P];
 #pragma unroll
       for (int k = 0; k < P; ++k) F[k] = mk<T2>(0, 0);
 #pragma unroll
       for (int i = 0; i < WINR; ++i) {
         T2 v[WIN];
+        if constexpr (C64 && WIN % 2 == 0) {  // complex64: even anchors -> 16-byte aligned pairs
+          const float4* wp = reinterpret_cast<const float4*>(win + i * bnc);
 #pragma unroll
-        for (int j = 0; j < WIN; ++j) v[j] = win[i * bnc + j];
+          for (int jj = 0; jj < WIN / 2; ++jj) {
+            const float4 a = wp[jj];
+            v[2 * jj] = mk<T2>(a.x, a.y);
+            v[2 * jj + 1] = mk<T2>(a.z, a.w);
+          }
+        } else {
+#pragma unroll
+          for (int jj = 0; jj < WIN; ++jj) v[jj] = win[i * bnc + jj];
+        }
         Rt w1[P];
 #pragma unroll
-        for (int c = 0; c < P / RPV; ++c) {
+        for (int cc = 0; cc < P / RPV; ++cc) {
           if constexpr (sizeof(Rt) == 4) {
-            const float4 a = *reinterpret_cast<const float4*>(p1s + ((i * (P / RPV) + c) * BLOCK + tid) * 16);
-            w1[4 * c] = a.x; w1[4 * c + 1] = a.y; w1[4 * c + 2] = a.z; w1[4 * c + 3] = a.w;
+            const float4 a = *reinterpret_cast<const float4*>(p1s + ((i * (P / RPV) + cc) * BLOCK + tid) * 16);
+            w1[4 * cc] = a.x; w1[4 * cc + 1] = a.y; w1[4 * cc + 2] = a.z; w1[4 * cc + 3] = a.w;
           } else {
-            const double2 a = *reinterpret_cast<const double2*>(p1s + ((i * (P / RPV) + c) * BLOCK + tid) * 16);
-            w1[2 * c] = a.x; w1[2 * c + 1] = a.y;
+            const double2 a = *reinterpret_cast<const double2*>(p1s + ((i * (P / RPV) + cc) * BLOCK + tid) * 16);
+            w1[2 * cc] = a.x; w1[2 * cc + 1] = a.y;
           }
         }
 #pragma unroll
         for (int k = 0; k < P; ++k) {
           T2 rr = mk<T2>(0, 0);
 #pragma unroll
-          for (int j = 0; j < WIN; ++j) rr = cfma_real(p2[k][j], v[j], rr);
+          for (int jj = 0; jj < WIN; ++jj) rr = cfma_real(p2[k][jj], v[jj], rr);
           F[k] = cfma_real(w1[k], rr, F[k]);
         }
       }
-      const T2* ring = aring + st * BLOCK * P + tid;
+      const T2* ring = aring + (t % S) * BLOCK * P + tid;
 #pragma unroll
       for (int k = 0; k < P; ++k) {
         const T2 av = ring[k * BLOCK];
@@ -1212,8 +1213,7 @@ __global__ void __launch_bounds__(K3Cfg<T2>::BLOCK, K3Cfg<T2>::MINB)
         acc[k].y = fma(av.x, F[k].y, fma(av.y, F[k].x, acc[k].y));
       }
     }
-    gterm += q;
-    if (!first) cp_async_wait<0>();  // the running sums have landed
+    cp_async_wait<0>();  // the running sums (in the first copy group) have landed
     T2 f0 = mk<T2>(0, 0);
     if (first && add_dc) f0 = fhat[0];
 #pragma unroll
@@ -1273,18 +1273,16 @@ __global__ void k_accum(T2* __restrict__ Lf, const T2* __restrict__ a0, const T2
 }
 
 template <typename T2, int TAPS, int P>
-static cudaError_t launch_groups_tp(const ApplyArgs& a, int wi, T2* Lf, int first, int add_dc, cudaStream_t s) {
+static cudaError_t launch_groups_tp(const ApplyArgs& a, const InterpWedge& iw, const T2* g, const T2* fhat, T2* Lf,
+                                    int first, int add_dc, cudaStream_t s) {
   constexpr int BLOCK = K3Cfg<T2>::BLOCK;
-  const InterpWedge& iw = a.iw[wi];
-  // the plan opted this instance into its largest smem on its device (configure_interp)
+  // the plan opted this instance into its largest footprint's smem on its device (configure_interp)
   const size_t smem = K3Layout<T2, TAPS, P>::bytes(iw.tile_cap);
   int per_sm = 0;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_interp_groups<T2, TAPS, P>, BLOCK, smem);
   per_sm = std::max(per_sm, 1);
-  int blocks = std::max(1, std::min(iw.nchunks, per_sm * a.sms));
-  k_interp_groups<T2, TAPS, P><<<blocks, BLOCK, smem, s>>>(iw, reinterpret_cast<const T2*>(a.g), a.a0,
-                                                          reinterpret_cast<const T2*>(a.fhat), first,
-                                                          add_dc, *a.poly, Lf);
+  const int blocks = std::max(1, std::min(iw.nchunks, per_sm * a.sms));
+  k_interp_groups<T2, TAPS, P><<<blocks, BLOCK, smem, s>>>(iw, g, a.a0, fhat, first, add_dc, *a.poly, Lf);
   return cudaGetLastError();
 }
 
@@ -1316,10 +1314,36 @@ cudaError_t configure_interp(int taps, bool c64, long long max_tile_cap) {
 }
 
 template <typename T2>
-static cudaError_t launch_interp(const ApplyArgs* args, int nrhs, T2* Lf0, cudaStream_t s, int* n,
-                                 const int* wedge_batch = nullptr) {
+static cudaError_t launch_groups(const ApplyArgs& a, const InterpWedge& iw, const T2* g, const T2* fhat, T2* Lf,
+                                 int first, int add_dc, cudaStream_t s) {
+#define FIO_GROUPS_CASE(TP) \
+  case TP:                  \
+    return launch_groups_tp<T2, TP, GroupP<T2, TP>::value>(a, iw, g, fhat, Lf, first, add_dc, s);
+  switch (a.taps) {
+    FIO_GROUPS_CASE(3)
+    FIO_GROUPS_CASE(4)
+    FIO_GROUPS_CASE(5)
+    FIO_GROUPS_CASE(6)
+    FIO_GROUPS_CASE(7)
+    FIO_GROUPS_CASE(8)
+    FIO_GROUPS_CASE(9)
+    FIO_GROUPS_CASE(10)
+    FIO_GROUPS_CASE(11)
+    FIO_GROUPS_CASE(12)
+    default: return cudaErrorInvalidValue;
+  }
+#undef FIO_GROUPS_CASE
+}
+
+// K3 of the whole apply: one launch per owned wedge, alternating between the caller's stream (into Lf)
+// and the plan's side stream (into the second accumulator), so one wedge's tail and the next one's
+// start overlap; the two partial sums are added in a fixed order (deterministic).  Skeleton storage:
+// alpha' is first regenerated into the stream's scratch.  One alpha' serves every right-hand side.
+template <typename T2>
+static cudaError_t launch_interp(const ApplyArgs* args, int nrhs, T2* Lf0, cudaStream_t s, int* n) {
   const ApplyArgs& a = args[0];
   const long long NN = (long long)a.N * a.N;
+  cudaError_t e;
   if (a.nw == 0) {
     int blocks = (int)std::min<long long>((NN + 255) / 256, 148LL * 8);
     for (int b = 0; b < nrhs; ++b) {
@@ -1329,77 +1353,42 @@ static cudaError_t launch_interp(const ApplyArgs* args, int nrhs, T2* Lf0, cudaS
     }
     return cudaGetLastError();
   }
-  // K3 of wedge wi runs on stream wi % ns with its own accumulator (stream 0: the caller's, into
-  // Lf), so one wedge's tail and prologue overlap other wedges' work; the partial sums are added at
-  // the end in a fixed order (deterministic).  Skeleton mode: two alpha' scratches alternate over the
-  // wedges (fio_api.cu), so at most 2 streams, each rebuilding its wedge's alpha' before its K3.
-  const int ns = std::max(1, std::min(a.skel == nullptr ? a.k3_streams : std::min(a.k3_streams, 2), a.nw));
+  const int ns = a.nw > 1 && a.side[0] ? 2 : 1;
   if (ns > 1) {
-    cudaError_t e = cudaEventRecord(a.fork, s);
-    for (int j = 0; j + 1 < ns && e == cudaSuccess; ++j) e = cudaStreamWaitEvent(a.side[j], a.fork, 0);
-    if (e != cudaSuccess) return e;
+    if ((e = cudaEventRecord(a.fork, s)) != cudaSuccess) return e;
+    if ((e = cudaStreamWaitEvent(a.side[0], a.fork, 0)) != cudaSuccess) return e;
   }
-  int waited[kMaxK3Streams] = {-1, -1, -1, -1};  // pipelined: last batch each K3 stream waited for
   for (int wi = 0; wi < a.nw; ++wi) {
-    cudaError_t e;
     const int sj = wi % ns;
-    cudaStream_t sw = sj ? a.side[sj - 1] : s;
-    const int first = wi < ns;
-    if (wedge_batch && wedge_batch[wi] != waited[sj]) {  // this wedge's fine grids come from fft_stream
-      waited[sj] = wedge_batch[wi];
-      if ((e = cudaStreamWaitEvent(sw, a.ev_batch[waited[sj]], 0)) != cudaSuccess) return e;
-    }
-    const int dc = (wi == 0 && a.add_dc) ? 1 : 0;
-    if (a.skel) {  // skeleton storage: regenerate this wedge's alpha' into its stream's scratch
-      const InterpWedge& iw = a.iw[wi];
+    cudaStream_t sw = sj ? a.side[0] : s;
+    const InterpWedge& iw = a.iw[wi];
+    if (a.skel) {
       e = launch_rebuild_alpha(a.op, a.wd_host[wi], a.skel[wi], iw.q, iw.slot_x,
                                (long long)iw.ngroups * group_p(sizeof(T2) == 8, a.taps), const_cast<void*>(iw.alpha),
                                sizeof(T2) == sizeof(float2), sw);
       if (e != cudaSuccess) return e;
       ++*n;
     }
-    // one alpha' (rebuilt once in skeleton mode) serves every right-hand side (NEXT-2)
     for (int b = 0; b < nrhs; ++b) {
-      T2* Lf = sj ? reinterpret_cast<T2*>(args[b].acc[sj - 1]) : Lf0 + b * NN;
-#define FIO_GROUPS_CASE(TP)                                                  \
-  case TP:                                                                   \
-    e = launch_groups_tp<T2, TP, GroupP<T2, TP>::value>(args[b], wi, Lf, first, dc, sw); \
-    break;
-      switch (a.taps) {
-        FIO_GROUPS_CASE(3)
-        FIO_GROUPS_CASE(4)
-        FIO_GROUPS_CASE(5)
-        FIO_GROUPS_CASE(6)
-        FIO_GROUPS_CASE(7)
-        FIO_GROUPS_CASE(8)
-        FIO_GROUPS_CASE(9)
-        FIO_GROUPS_CASE(10)
-        FIO_GROUPS_CASE(11)
-        FIO_GROUPS_CASE(12)
-        default: return cudaErrorInvalidValue;
-      }
-#undef FIO_GROUPS_CASE
-      if (e != cudaSuccess) return e;
+      T2* acc = sj ? reinterpret_cast<T2*>(args[b].acc[0]) : Lf0 + b * NN;
+      if ((e = launch_groups<T2>(a, iw, reinterpret_cast<const T2*>(args[b].g),
+                                 reinterpret_cast<const T2*>(args[b].fhat), acc, wi < ns,
+                                 (wi == 0 && a.add_dc) ? 1 : 0, sw)) != cudaSuccess)
+        return e;
       ++*n;
     }
   }
   if (ns > 1) {
-    cudaError_t e = cudaSuccess;
-    for (int j = 0; j + 1 < ns && e == cudaSuccess; ++j) {
-      e = cudaEventRecord(a.join[j], a.side[j]);
-      if (e == cudaSuccess) e = cudaStreamWaitEvent(s, a.join[j], 0);
-    }
-    if (e != cudaSuccess) return e;
-    const int blocks = (int)std::min<long long>((NN + 255) / 256, 148LL * 8);
+    if ((e = cudaEventRecord(a.join[0], a.side[0])) != cudaSuccess) return e;
+    if ((e = cudaStreamWaitEvent(s, a.join[0], 0)) != cudaSuccess) return e;
+    const int accb = (int)std::min<long long>((NN + 255) / 256, 148LL * 8);
     for (int b = 0; b < nrhs; ++b) {
-      const T2* const* acc = reinterpret_cast<const T2* const*>(args[b].acc);
-      k_accum<T2><<<blocks, 256, 0, s>>>(Lf0 + b * NN, acc[0], ns > 2 ? acc[1] : acc[0], ns > 3 ? acc[2] : acc[0],
-                                          ns - 1, NN);
+      const T2* acc1 = reinterpret_cast<const T2*>(args[b].acc[0]);
+      k_accum<T2><<<accb, 256, 0, s>>>(Lf0 + b * NN, acc1, acc1, acc1, 1, NN);
       ++*n;
     }
-    return cudaGetLastError();
   }
-  return cudaSuccess;
+  return cudaGetLastError();
 }
 
 // ================================================================== adjoint
@@ -1696,7 +1685,7 @@ static cudaError_t enqueue_adjoint_t(const ApplyArgs& a, const T2* g, T2* out, c
     if ((e = cudaMemsetAsync(a.g, 0, sizeof(T2) * a.fine_elems, s)) != cudaSuccess) return e;
     // the wedges' spreads write disjoint G*_l: they alternate between the caller's stream and the
     // plan's side stream (not in skeleton mode, whose alpha' scratch is shared)
-    const bool two = a.side[0] != nullptr && a.nw >= 2 && a.k3_streams >= 2;  // skeleton: 2 scratches
+    const bool two = a.side[0] != nullptr && a.nw >= 2;  // skeleton: 2 scratches
     if (two) {
       if ((e = cudaEventRecord(a.fork, s)) != cudaSuccess) return e;
       if ((e = cudaStreamWaitEvent(a.side[0], a.fork, 0)) != cudaSuccess) return e;
@@ -1812,19 +1801,6 @@ static cudaError_t enqueue_apply_t(const ApplyArgs* args, int nrhs, const T2* f0
   const T2* tw = reinterpret_cast<const T2*>(a0.tw);
   const size_t seq = fft_seq_bytes(a0.N, sizeof(T2) == sizeof(float2));
   const long long NN = (long long)a0.N * a0.N;
-  // pipelined K1/K2 || K3 (not with the per-stage profile, whose events need the stages in sequence)
-  const int nbat = std::min(a0.pipe_batches, kMaxPipeBatches);
-  const bool pipe = nbat > 1 && nrhs == 1 && ev == nullptr && a0.skel == nullptr && a0.nw >= 2 &&
-                    a0.fft_stream != nullptr && a0.row_job_off != nullptr;
-  std::vector<int> wedge_batch;
-  if (pipe) {
-    // the first batch is one wedge per K3 stream (only it is exposed), the rest split evenly
-    const int ns = std::max(1, std::min(a0.k3_streams, a0.nw));
-    wedge_batch.resize(a0.nw);
-    const int first = std::min(ns, a0.nw), rest = a0.nw - first, nb = std::max(1, std::min(nbat - 1, rest));
-    for (int wi = 0; wi < a0.nw; ++wi)
-      wedge_batch[wi] = wi < first ? 0 : 1 + (int)((long long)(wi - first) * nb / std::max(rest, 1));
-  }
   for (int b = 0; b < nrhs; ++b) {
     const ApplyArgs& a = args[b];
     const T2* f = f0 + b * NN;
@@ -1842,32 +1818,7 @@ static cudaError_t enqueue_apply_t(const ApplyArgs* args, int nrhs, const T2* f0
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
     ++n;
     mark();
-    if (pipe) {  // K1/K2 per wedge batch on fft_stream; K3 waits per batch (launch_interp)
-      const T2* const* betas = reinterpret_cast<const T2* const*>(a.beta);
-      if ((e = cudaEventRecord(a.ev_k0, s)) != cudaSuccess) return e;
-      if ((e = cudaStreamWaitEvent(a.fft_stream, a.ev_k0, 0)) != cudaSuccess) return e;
-      for (int bt = 0, w0 = 0; w0 < a.nw; ++bt) {
-        int w1 = w0;
-        while (w1 < a.nw && wedge_batch[w1] == bt) ++w1;
-        const int r0 = a.row_job_off[w0], r1 = a.row_job_off[w1], c0 = a.col_job_off[w0], c1 = a.col_job_off[w1];
-        if (r1 > r0) {
-          k_rowpass<T2><<<r1 - r0, FIO_K1_THREADS, a.smem_row, a.fft_stream>>>(a.N, a.wedges, a.jobs_row + r0, a.ffts, tw, betas,
-                                                                    fhat, reinterpret_cast<T2*>(a.p1));
-          ++n;
-        }
-        if (c1 > c0) {
-          k_colpass<T2><<<c1 - c0, FIO_K2_THREADS, a.smem_col, a.fft_stream>>>(a.wedges, a.jobs_col + c0, a.ffts, tw,
-                                                                    reinterpret_cast<const T2*>(a.p1),
-                                                                    reinterpret_cast<T2*>(a.g));
-          ++n;
-        }
-        if ((e = cudaGetLastError()) != cudaSuccess) return e;
-        if ((e = cudaEventRecord(a.ev_batch[bt], a.fft_stream)) != cudaSuccess) return e;
-        w0 = w1;
-      }
-      mark();
-      mark();
-    } else if (a.nw > 0) {
+    if (a.nw > 0) {
       const T2* const* betas = reinterpret_cast<const T2* const*>(a.beta);
       k_rowpass<T2><<<a.njobs_row, FIO_K1_THREADS, a.smem_row, s>>>(a.N, a.wedges, a.jobs_row, a.ffts, tw, betas, fhat,
                                                          reinterpret_cast<T2*>(a.p1));
@@ -1884,10 +1835,7 @@ static cudaError_t enqueue_apply_t(const ApplyArgs* args, int nrhs, const T2* f0
       mark();
     }
   }
-  if ((e = launch_interp<T2>(args, nrhs, Lf, s, &n, pipe ? wedge_batch.data() : nullptr)) != cudaSuccess) return e;
-  if (pipe) {  // join fft_stream (its last batch) back into s
-    if ((e = cudaStreamWaitEvent(s, a0.ev_batch[wedge_batch.back()], 0)) != cudaSuccess) return e;
-  }
+  if ((e = launch_interp<T2>(args, nrhs, Lf, s, &n)) != cudaSuccess) return e;
   mark();
   if (launches) *launches = n;
   return cudaSuccess;

@@ -68,10 +68,7 @@ cudaError_t launch_rebuild_alpha(const OperatorDev& op, const WedgeDev& w, const
                                  const int* slot_x, long long nslots, void* alpha, bool c64, cudaStream_t s);
 
 // ---- apply-time kernels (the hot path) ----
-constexpr int kMaxK3Streams = 4;
-constexpr int kDefaultK3Streams = 2;  // env FIO_K3_STREAMS overrides (1..4)
-constexpr int kMaxPipeBatches = 16;
-constexpr int kDefaultPipeBatches = 0;  // env FIO_PIPE_BATCHES overrides; measured: 4/8/16 batches 14.46/14.51/14.56 ms vs 14.18 off (c128): K3 already fills the GPU
+
 struct ApplyArgs {
   int N;
   int nw;                   // owned wedges
@@ -98,25 +95,15 @@ struct ApplyArgs {
   const FftJob* jobs_rowadj; int njobs_rowadj; int smem_rowadj;  // K1* (all t per job)
   const unsigned char* const* masks;  // per owned wedge: n1 x n2 box mask (cell is a member)
   size_t fine_elems;        // elements of the fine-grid workspace (G, reused as G* by the adjoint)
-  // K3 runs wedge wi on stream wi % k3_streams: stream 0 is the caller's and accumulates into Lf,
-  // stream j > 0 is plan-owned (side[j-1]) and accumulates into acc[j-1] (N*N each, per RHS)
-  int k3_streams;
-  void* acc[kMaxK3Streams - 1];
-  cudaStream_t side[kMaxK3Streams - 1];
-  cudaEvent_t fork, join[kMaxK3Streams - 1];
-  // pipelined apply (nrhs == 1, not skeleton): K1/K2 of wedge batch b run on fft_stream while K3 of
-  // batch b-1 runs; ev_batch[b] marks batch b's fine grids ready.  row/col_job_off: per owned wedge,
-  // its first job in jobs_row / jobs_col (nw + 1 entries, host).
-  int pipe_batches;                // 0/1: off
-  cudaStream_t fft_stream;
-  cudaEvent_t ev_k0;
-  const cudaEvent_t* ev_batch;     // kMaxPipeBatches
-  const int* row_job_off;
-  const int* col_job_off;
-  int sms;                  // multiprocessors of the plan's device (grid sizing)
-  int overlap;              // smooth partition: wedges overlap, K1* accumulates fhat* atomically
+  // second K3 accumulator (the side stream's wedges), N*N per RHS, the plan-owned side stream of K3
+  // and of the adjoint's spreads, and the events that fork / join it
+  void* acc[1];
+  cudaStream_t side[1];
+  cudaEvent_t fork, join[1];
   int rows_per_cta_N;       // K0 row pass
   int cols_per_cta_N;       // K0 column pass
+  int sms;                  // multiprocessors of the plan's device (grid sizing)
+  int overlap;              // smooth partition: wedges overlap, K1* accumulates fhat* atomically
 };
 
 // Enqueue the whole apply (K0 row/column FFT, K1 window x beta + row FFT,

@@ -405,23 +405,22 @@ def test_more_invalid_arguments():
         plan.apply(torch.zeros((32, 32), dtype=torch.complex128, device=DEV))  # wrong shape
 
 
-# ------------------------------------------------------------------ stream / pipeline schedules
-@pytest.mark.parametrize("env,exact", [({"FIO_PIPE_BATCHES": "4"}, True), ({"FIO_K3_STREAMS": "1"}, False),
-                                       ({"FIO_K3_STREAMS": "3"}, False)])
-def test_apply_schedules_agree(env, exact, monkeypatch):
-    # the K3 stream count and the optional K1/K2 || K3 pipeline change only the schedule (and, for the
-    # stream count, the grouping of the per-wedge partial sums)
+# ------------------------------------------------------------------ determinism of the two-stream K3 schedule
+@pytest.mark.parametrize("dtype,eps", [("c128", 1e-6), ("c64", 1e-4)])
+def test_apply_is_deterministic(dtype, eps):
+    # K3's wedges alternate between two streams with their own accumulators, each point is written by
+    # one thread per wedge and the accumulators are added in a fixed order: repeated applies (and a
+    # re-planned operator with the same seed) agree bit for bit (reading R20)
     N = 256
     op = wl.grt_operator(N)
-    f = wl.white_noise(N, 9)
-    _, ref = run(op, f)
-    for k, v in env.items():
-        monkeypatch.setenv(k, v)
-    _, out = run(op, f)
-    if exact:
-        assert np.array_equal(out, ref)
-    else:
-        assert oracle.rel_l2(out, ref) <= 1e-13
+    f = wl.white_noise(N, 9, dtype)
+    plan, ref = run(op, f, eps=eps, dtype=dtype)
+    tdt = torch.complex64 if dtype == "c64" else torch.complex128
+    t = torch.from_numpy(f).to(DEV, tdt)
+    for _ in range(3):
+        assert np.array_equal(plan.apply(t).cpu().numpy().astype(np.complex128), ref)
+    _, again = run(op, f, eps=eps, dtype=dtype)
+    assert np.array_equal(again, ref)
 
 
 def test_c64_storage_at_1e6():
