@@ -135,6 +135,19 @@ def k3_resource_model(info, c64, ms, sm_mhz):
             "flops_per_s": 2 * fmas / t, "sm_mhz": sm_mhz, "model": "DESIGN.md section 7"}
 
 
+def alu_roofline(info, c64, k3_ms):
+    """K3 against its arithmetic roofline: the FMAs it issues per apply (k3_resource_model, padding
+    slots included) as FLOP/s over the measured FMA peak of its precision (FP64 pipe for complex128,
+    FP32 packed FFMA2 for complex64)."""
+    fp64, fp32, src = alu_peaks()
+    m = k3_resource_model(info, c64, k3_ms, None)
+    ach = m["flops_per_s"] / 1e12
+    peak = fp32 if c64 else fp64
+    return {"bound": "alu", "pipe": "fp32 (FFMA2)" if c64 else "fp64 (DFMA)", "achieved": ach, "peak": peak,
+            "unit": "TFLOP/s", "frac": ach / peak, "peak_source": src,
+            "flops": 2 * m["fma"], "flops_model": "2 x slot_terms x (rows (2 cols + 2) + 4)"}
+
+
 def peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
@@ -142,6 +155,18 @@ def peaks():
         return float(mp["hbm_gbs"]), "measured"
     except Exception:
         return 6650.0, "fallback"
+
+
+def alu_peaks():
+    """FP64 / FP32 FMA peaks of this pool's B200s, measured by tools/microbench.cu (profiles/
+    r02_microbench.json): DFMA and packed FFMA2 over all 148 SMs; fallback = the guide's unit counts
+    (64 DFMA / 128 FFMA per clk per SM at 1965 MHz)."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "r02_microbench.json")) as fh:
+            mb = json.load(fh)
+        return float(mb["dfma_tflops"]), float(mb["ffma2_tflops"]), "measured (profiles/r02_microbench.json)"
+    except Exception:
+        return 2 * 64 * 148 * 1.965e9 / 1e12, 2 * 128 * 148 * 1.965e9 / 1e12, "unit counts x 1965 MHz"
 
 
 # ---------------------------------------------------------------- CPU oracle baseline
@@ -305,6 +330,8 @@ def time_config(name, args, rank, world, local, group):
                      "peak_source": src, "traffic_source": "profiles/r02_k3_traffic.json (ncu, cold cache)",
                      "algorithmic_bytes": k3_bytes,
                      "bytes_model": "N^2 sum_q s (alpha') + fine_elems s (G read once) + N^2 s (Lf write)"},
+        "alu_roofline": dict(alu_roofline(info, c64, k3_ms), traffic=traffic,
+                             kernel="k_interp_groups (K3, all wedge launches of one apply)"),
         "apply_hbm_gbs": apply_algorithmic_bytes(info, N, c64) / (ms_step * 1e-3) / 1e9,
         "k3_resources": k3_resource_model(info, c64, k3_ms, clk.summary().get("sm_mhz")),
         "plan": {"W": info["W"], "sum_q": info["sum_q"], "nufft_w": info["nufft_w"],
@@ -342,7 +369,7 @@ def run_gpu(args):
         v = time_config(args.variant, args, rank, world, local, group)
         variants[args.variant] = {k: v[k] for k in ("dtype", "eps", "applies_per_s", "points_per_s", "ms_per_step",
                                                     "roofline", "stage_ms", "k3_share", "plan", "e2e",
-                                                    "adjoint_ms_per_step", "k3_resources")}
+                                                    "adjoint_ms_per_step", "k3_resources", "alu_roofline")}
     if rank == 0:
         cpu = None
         check = None
@@ -364,7 +391,11 @@ def run_gpu(args):
                        "parallelism": f"wedge-sharded x{world}" if world > 1 else "single GPU",
                        "l2": "inputs larger than L2 (alpha' streams %.1f GB per step)" % main["plan"]["alpha_GB"]},
             "points_per_s": main["points_per_s"],
-            "roofline": main["roofline"], "apply_hbm_gbs": main["apply_hbm_gbs"], "stage_ms": main["stage_ms"],
+            # the roofline that binds the dominant kernel: FP64 pipe for complex128 K3,
+            # HBM for complex64; the other one is reported beside it
+            "roofline": main["alu_roofline"] if main["dtype"] == "c128" else main["roofline"],
+            "hbm_roofline": main["roofline"], "alu_roofline": main["alu_roofline"],
+            "apply_hbm_gbs": main["apply_hbm_gbs"], "stage_ms": main["stage_ms"],
             "k3_resources": main["k3_resources"],
             "k3_share": main["k3_share"], "plan": main["plan"], "adjoint_ms_per_step": main["adjoint_ms_per_step"],
             "clocks": main["clocks"], "e2e": main["e2e"],

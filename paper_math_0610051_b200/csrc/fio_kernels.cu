@@ -961,13 +961,15 @@ template <> struct K3Cfg<float2> {
 #ifndef FIO_K3_MINB64
 #define FIO_K3_MINB64 8
 #endif
-  static constexpr int BLOCK = kK3BlockC64, MINB = FIO_K3_MINB64;
+  static constexpr int BLOCK = kK3BlockC64, MINB = FIO_K3_MINB64, STAGES = FIO_K3_STAGES64;
+  static_assert(kK3TileCapC64 % (2 * BLOCK) == 0, "tile cap: a whole number of 16-byte units per thread");
 };
 template <> struct K3Cfg<double2> {
 #ifndef FIO_K3_MINB128
 #define FIO_K3_MINB128 4
 #endif
-  static constexpr int BLOCK = kK3BlockC128, MINB = FIO_K3_MINB128;
+  static constexpr int BLOCK = kK3BlockC128, MINB = FIO_K3_MINB128, STAGES = FIO_K3_STAGES128;
+  static_assert(kK3TileCapC128 % BLOCK == 0, "tile cap: a whole number of 16-byte units per thread");
 };
 
 // Shared memory of K3 (16-aligned sections).  Per-point arrays are element-major with the thread
@@ -989,14 +991,14 @@ struct K3Layout {
   static constexpr int WINR = k3_window_rows(TAPS, sizeof(T2) == 8);
   static constexpr size_t al(size_t b) { return (b + 15) / 16 * 16; }
   static constexpr size_t kRing = 0;
-  static constexpr size_t kP1 = kRing + al(sizeof(T2) * kK3Stages * BLOCK * P);
+  static constexpr size_t kP1 = kRing + al(sizeof(T2) * K3Cfg<T2>::STAGES * BLOCK * P);
   static constexpr size_t kLf = kP1 + al(sizeof(Rt) * WINR * BLOCK * P);
   static constexpr size_t kSlot = kLf + al(sizeof(T2) * BLOCK * P);
   static constexpr size_t kOff = kSlot + al(sizeof(int) * 2 * BLOCK * P);
   static constexpr size_t kAnchor = kOff + al(sizeof(typename OffT<T2>::type) * BLOCK * P);
   static constexpr size_t kBox = kAnchor + al(sizeof(int2) * BLOCK);
   static constexpr size_t kFixed = kBox + al(sizeof(int) * 2 * kBoxInts);
-  static size_t bytes(long long cap) { return kFixed + sizeof(T2) * kK3Stages * (size_t)cap; }
+  static size_t bytes(long long cap) { return kFixed + sizeof(T2) * K3Cfg<T2>::STAGES * (size_t)cap; }
 };
 
 // `bytes` (a multiple of 16) from global to shared memory by the whole CTA, 16-byte cp.async units
@@ -1014,7 +1016,7 @@ __device__ __forceinline__ void cta_copy16(void* dst, const void* src, int bytes
 // sums Lf(x_k); then, for every term t, the CTA stages with cp.async the chunk's footprint tile of
 // G_lt (rows wrapped mod the fine grid, columns from the haloed row layout; every thread copies a
 // fixed set of 16-byte units whose addresses it computes once per chunk) and the chunk's alpha'(t)
-// block into a kK3Stages-deep ring, so global latency overlaps the arithmetic of earlier terms.
+// block into a K3Cfg::STAGES-deep ring, so global latency overlaps the arithmetic of earlier terms.
 // Per group, term and window row i the thread loads the row once and applies it to all P points:
 //   F_k += phi1_k[i] sum_j phi2_k[j] G_lt[a1 + i][a2 + j]
 //   acc_k += alpha'_lt(x_k) F_k
@@ -1033,7 +1035,7 @@ __global__ void __launch_bounds__(K3Cfg<T2>::BLOCK, K3Cfg<T2>::MINB)
   constexpr int WIN = k3_window_cols(TAPS, C64);
   constexpr int WINR = k3_window_rows(TAPS, C64);
   constexpr int BLOCK = K3Cfg<T2>::BLOCK;
-  constexpr int S = kK3Stages;
+  constexpr int S = K3Cfg<T2>::STAGES;
   constexpr int EPC = 16 / (int)sizeof(T2);  // complex elements per 16-byte unit
   constexpr int RPV = 16 / (int)sizeof(Rt);  // row weights per 16-byte unit
   constexpr int MAXC = C64 ? kK3TileCapC64 / 2 / BLOCK : kK3TileCapC128 / BLOCK;  // tile units per thread
