@@ -280,7 +280,8 @@ namespace {
 // device, FP64), q, the final r and the sampled error.
 fio_status separate_wedge(fio_plan_s& P, const WedgeGeom& g, Rng& rng, cudaStream_t s, DevBuf& dU, DevBuf& dBeta,
                           int& q_out, int& r_out, double& err_out, std::vector<int>& C_out,
-                          std::vector<cplx>& Y_out, std::vector<int>& R_out, std::vector<cplx>& Z_out) {
+                          std::vector<cplx>& Y_out, std::vector<int>& R_out, std::vector<cplx>& Z_out,
+                          int r_start) {
   const int N = P.N;
   const int m = N * N;
   const int n = (int)g.members.size();
@@ -289,7 +290,7 @@ fio_status separate_wedge(fio_plan_s& P, const WedgeGeom& g, Rng& rng, cudaStrea
   FIO_CUDA(dMembers.ensure(sizeof(int) * n));
   FIO_CUDA(cudaMemcpy(dMembers.p, g.members.data(), sizeof(int) * n, cudaMemcpyHostToDevice));
 
-  int r = std::min(std::max(P.opts.r_init, 4), n);
+  int r = std::min(std::max(r_start, 4), n);
   std::vector<int> C;
   std::vector<cplx> V;
   std::vector<double> lam;
@@ -873,7 +874,25 @@ fio_status build_plan(fio_plan_s& P, const fio_phase* phase, const fio_amplitude
       if (st == FIO_OK) st = expand_factors(P, g, F, s, dU, dBeta);
     } else {
       F.l = g.l;
-      st = separate_wedge(P, g, rng, s, dU, dBeta, F.q, F.r, F.err, F.C, F.Y, F.R, F.Z);
+      st = separate_wedge(P, g, rng, s, dU, dBeta, F.q, F.r, F.err, F.C, F.Y, F.R, F.Z, P.opts.r_init);
+      // Certification-driven retry (reading R8): a random row sample can miss a rare kind
+      // of output point (e.g. one region of a piecewise-smooth phase), so the skeleton -- and q --
+      // miss a direction; the s = 200 sampled check sees it.  Redraw with a
+      // doubled r (fresh draws from the wedge's stream) until certified or r_max.
+      for (int r0 = 2 * P.opts.r_init; st == FIO_OK && P.opts.certify && F.err > 10.0 * P.eps && r0 <= P.opts.r_max;
+           r0 *= 2) {
+        WedgeFactors G2;
+        G2.l = g.l;
+        DevBuf dU2, dB2;
+        st = separate_wedge(P, g, rng, s, dU2, dB2, G2.q, G2.r, G2.err, G2.C, G2.Y, G2.R, G2.Z, r0);
+        if (st == FIO_OK && G2.err < F.err) {
+          F = std::move(G2);
+          std::swap(dU.p, dU2.p);
+          std::swap(dU.bytes, dU2.bytes);
+          std::swap(dBeta.p, dB2.p);
+          std::swap(dBeta.bytes, dB2.bytes);
+        }
+      }
     }
     if (st != FIO_OK) return st;
     q = F.q;

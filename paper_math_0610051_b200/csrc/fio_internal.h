@@ -48,7 +48,7 @@ constexpr int kK3BlockC128 = FIO_K3_BLOCK128;  // complex128
 #define FIO_K3_CAP64 512
 #endif
 #ifndef FIO_K3_CAP128
-#define FIO_K3_CAP128 512
+#define FIO_K3_CAP128 384
 #endif
 // K3 pipeline depth (terms in flight: fine-grid tiles + alpha').  Measured at N = 1024 (K3 ms):
 // complex64 2 / 3 / 4 stages 2.59 / 2.62 / 2.72, complex128 11.16 / 12.47 / 12.52 -- shallower rings

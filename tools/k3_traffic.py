@@ -1,10 +1,11 @@
 """Sum the DRAM bytes of all K3 launches of one apply from ncu --csv metric dumps.
 
-usage: python tools/k3_traffic.py OUT.json cfg=path.csv [cfg=path.csv ...]
+usage: python tools/k3_traffic.py OUT.json cfg=path.csv:SUM_Q [cfg=path.csv:SUM_Q ...]
 Each csv comes from
   ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum --clock-control none \
-      -k regex:k_interp_groups --csv python tools/run_apply.py --config CFG --iters 1
-(every K3 launch of one apply, cold cache per launch).
+      -k regex:k_interp_groups --csv python tools/run_apply.py CFG 1
+(every K3 launch of one apply, cold cache per launch); SUM_Q is the plan's sum of separation ranks
+(printed by run_apply.py), so bench.py uses the capture only for the plan it was taken on.
 """
 import csv
 import json
@@ -30,14 +31,16 @@ def parse(path):
 def main():
     out = {}
     for arg in sys.argv[2:]:
-        cfg, path = arg.split("=", 1)
+        cfg, rest = arg.split("=", 1)
+        path, sum_q = rest.rsplit(":", 1)
         n, acc = parse(path)
         rd, wr = acc.get("dram__bytes_read.sum", 0.0), acc.get("dram__bytes_write.sum", 0.0)
-        out[cfg] = {"launches": n, "dram_read_bytes": rd, "dram_write_bytes": wr, "dram_bytes": rd + wr,
+        out[cfg] = {"launches": n, "sum_q": int(sum_q), "dram_read_bytes": rd, "dram_write_bytes": wr,
+                    "dram_bytes": rd + wr,
                     "ncu_time_s": acc.get("gpu__time_duration.sum", 0.0),
                     "how": "ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum "
-                           "--clock-control none -k regex:k_interp_groups, python tools/run_apply.py --config "
-                           f"{cfg} --iters 1 (all K3 launches of one apply; cold cache per launch)"}
+                           f"--clock-control none -k regex:k_interp_groups, python tools/run_apply.py {cfg} 1 "
+                           "(all K3 launches of one apply; cold cache per launch)"}
     json.dump(out, open(sys.argv[1], "w"), indent=1)
     print(json.dumps(out, indent=1))
 
