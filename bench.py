@@ -338,7 +338,7 @@ def time_config(name, args, rank, world, local, group):
                  "plan_seconds": info["plan_seconds"], "max_sep_err": info["max_sep_err"],
                  "alpha_GB": info["alpha_bytes"] / 1e9, "fine_elems": info["fine_elems"],
                  "slots": info["slots"], "max_tile_cap": info["max_tile_cap"],
-                 "k3_group_fill": info["slots"] / max(info["slot_terms"] / max(info["sum_q"], 1), 1),
+                 "k3_group_fill": N * N * info["n_owned"] / max(info["slots"], 1),
                  "group_p": info["group_p"],
                  "rank_balance": info["rank_balance"]},
         "launches_per_step": info["launches_per_apply"],

@@ -1,6 +1,7 @@
 """Build K3 variants (compile-time switches) in scratch copies of the repo and time them on the GPU.
 
-    python tools/k3_variants.py NAME=FLAGS [NAME=FLAGS ...] [--configs cfg3_c64,cfg3_c128] [--steps 10]
+    python tools/k3_variants.py NAME=FLAGS[@ENV=V,...] [NAME=FLAGS ...] [--configs=cfg3_c64,cfg3_c128] [--steps=10]
+                                [--overlap=0.25]
 
 Each variant: copy the repo to /tmp/fio_var_NAME, build libfio_b200.so with FIO_NVCC_FLAGS=FLAGS,
 then (in a fresh process) plan + apply the configs, report per-stage ms (CUDA events, library
@@ -22,7 +23,8 @@ res = {}
 for name in sys.argv[2].split(","):
     cfg = wl.config(name); op = wl.make_operator(cfg); f = wl.make_input(cfg)
     c64 = cfg["dtype"] == "c64"
-    plan = fio.Plan(op.N, op.c1, op.c2, eps=cfg["eps"], dtype=cfg["dtype"], device=0)
+    plan = fio.Plan(op.N, op.c1, op.c2, eps=cfg["eps"], dtype=cfg["dtype"], device=0,
+                    wedge_overlap=float(sys.argv[4]) if len(sys.argv) > 4 else 0.0)
     t = torch.from_numpy(f).to("cuda:0", torch.complex64 if c64 else torch.complex128)
     out = torch.empty_like(t)
     for _ in range(3): plan.apply(t, out=out)
@@ -50,7 +52,8 @@ for name in sys.argv[2].split(","):
                  "maxerr_rms": float(np.abs(got - ref).max() / np.sqrt(np.mean(np.abs(ref) ** 2))),
                  "sum_q": info["sum_q"], "slots": info["slots"], "slot_terms": info["slot_terms"],
                  "alpha_GB": info["alpha_bytes"] / 1e9, "group_p": info["group_p"],
-                 "k3_thread_slots": info["k3_thread_slots"], "max_tile_cap": info["max_tile_cap"]}
+                 "k3_thread_slots": info["k3_thread_slots"], "max_tile_cap": info["max_tile_cap"],
+                 "fine_elems": info["fine_elems"], "wedge_overlap": info["wedge_overlap"]}
     plan.close()
 print("RESULT " + json.dumps(res))
 '''
@@ -77,7 +80,8 @@ def main():
         env = dict(os.environ, FIO_NVCC_FLAGS=flags)
         subprocess.check_call([sys.executable, "-c", "from paper_math_0610051_b200 import build; build.build(force=True)"],
                               cwd=d, env=env)
-        r = subprocess.run([sys.executable, "-c", CHILD, d, configs, steps], cwd=d, capture_output=True, text=True,
+        r = subprocess.run([sys.executable, "-c", CHILD, d, configs, steps, opts.get("overlap", "0")], cwd=d,
+                           capture_output=True, text=True,
                            env=dict(os.environ, **runenv))
         line = [l for l in r.stdout.splitlines() if l.startswith("RESULT ")]
         out[name] = {"flags": flags, **(json.loads(line[0][7:]) if line else {"error": r.stderr[-2000:]})}
