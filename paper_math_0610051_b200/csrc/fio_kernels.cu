@@ -997,9 +997,36 @@ struct K3Layout {
   static constexpr size_t kOff = kSlot + al(sizeof(int) * 2 * BLOCK * P);
   static constexpr size_t kAnchor = kOff + al(sizeof(typename OffT<T2>::type) * BLOCK * P);
   static constexpr size_t kBox = kAnchor + al(sizeof(int2) * BLOCK);
-  static constexpr size_t kFixed = kBox + al(sizeof(int) * 2 * kBoxInts);
+  static constexpr size_t kBar = kBox + al(sizeof(int) * 2 * kBoxInts);
+  static constexpr size_t kFixed = kBar + al(8 * (K3Cfg<T2>::STAGES + 2));
   static size_t bytes(long long cap) { return kFixed + sizeof(T2) * K3Cfg<T2>::STAGES * (size_t)cap; }
 };
+
+// ---- the TMA engine (cp.async.bulk) for K3's contiguous alpha' blocks, completing on mbarriers
+__device__ __forceinline__ unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(unsigned long long* bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(unsigned long long* bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra WAIT_%=;\n}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+// global -> shared, `bytes` (multiple of 16, both addresses 16-byte aligned), completing on `bar`
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, unsigned long long* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+                   smem_u32(dst)),
+               "l"(src), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
+}
 
 // `bytes` (a multiple of 16) from global to shared memory by the whole CTA, 16-byte cp.async units
 template <int BLOCK>
@@ -1048,6 +1075,7 @@ __global__ void __launch_bounds__(K3Cfg<T2>::BLOCK, K3Cfg<T2>::MINB)
   O2* m_off = reinterpret_cast<O2*>(k3_smem + L::kOff);
   int2* m_anchor = reinterpret_cast<int2*>(k3_smem + L::kAnchor);
   int* sbox = reinterpret_cast<int*>(k3_smem + L::kBox);
+  unsigned long long* bar_a = reinterpret_cast<unsigned long long*>(k3_smem + L::kBar);  // [S] alpha' blocks
   T2* tring = reinterpret_cast<T2*>(k3_smem + L::kFixed);
   const int tid = threadIdx.x;
   const int cap = iw.tile_cap;
@@ -1059,21 +1087,29 @@ __global__ void __launch_bounds__(K3Cfg<T2>::BLOCK, K3Cfg<T2>::MINB)
   const O2* __restrict__ offs = reinterpret_cast<const O2*>(iw.slot_off);
   constexpr int kA = sizeof(int2) * BLOCK, kB = sizeof(int) * kBoxInts, kS = sizeof(int) * BLOCK * P,
                 kO = sizeof(O2) * BLOCK * P, kAl = sizeof(T2) * BLOCK * P;
+  unsigned long long* bar_m = bar_a + S;  // [2] chunk tables
+  // the chunk's tables are four contiguous blocks: four bulk copies (TMA engine) by thread 0
   auto prefetch_meta = [&](int chn, int buf) {
-    if (chn < iw.nchunks) {
+    if (chn < iw.nchunks && tid == 0) {
       const long long c0 = (long long)chn * BLOCK * P;  // first physical slot of the chunk
-      cta_copy16<BLOCK>(m_anchor, iw.anchor + 2 * (long long)chn * BLOCK, kA);
-      cta_copy16<BLOCK>(sbox + kBoxInts * buf, iw.box + (long long)kBoxInts * chn, kB);
-      cta_copy16<BLOCK>(m_slot + buf * BLOCK * P, iw.slot_x + c0, kS);
-      cta_copy16<BLOCK>(m_off, offs + c0, kO);
+      mbar_expect_tx(bar_m + buf, (unsigned)(kA + kB + kS + kO));
+      bulk_g2s(m_anchor, iw.anchor + 2 * (long long)chn * BLOCK, kA, bar_m + buf);
+      bulk_g2s(sbox + kBoxInts * buf, iw.box + (long long)kBoxInts * chn, kB, bar_m + buf);
+      bulk_g2s(m_slot + buf * BLOCK * P, iw.slot_x + c0, kS, bar_m + buf);
+      bulk_g2s(m_off, offs + c0, kO, bar_m + buf);
     }
   };
+  if (tid == 0) {
+    for (int st = 0; st < S + 2; ++st) mbar_init(bar_a + st, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  __syncthreads();
+  unsigned gterm = 0;  // terms this CTA has staged before the current chunk (ring slot / mbarrier phase)
   prefetch_meta(blockIdx.x, 0);
-  cp_async_commit();
   int it = 0;
   for (int ch = blockIdx.x; ch < iw.nchunks; ch += gridDim.x, ++it) {
     const int buf = it & 1;
-    cp_async_wait<0>();
+    mbar_wait(bar_m + buf, (unsigned)(it >> 1) & 1u);
     __syncthreads();  // this chunk's tables are visible; every thread is done with the previous chunk
     const int* cb = sbox + kBoxInts * buf;  // first group, row origin, column origin, rows, columns, groups
     const int br = cb[1], bc = cb[2], bnr = cb[3], bnc = cb[4];
@@ -1112,10 +1148,15 @@ __global__ void __launch_bounds__(K3Cfg<T2>::BLOCK, K3Cfg<T2>::MINB)
       }
     }
     // stage term t into ring slot t % S: the chunk's alpha'(t) block and the tile
+    // the chunk's alpha'(t) block is contiguous: one bulk copy (TMA engine) on the stage's mbarrier;
+    // the tile (short scattered rows) by cp.async from every thread
     auto issue = [&](int t, bool next_meta) {
       if (t < q) {
-        const int st = t % S;
-        cta_copy16<BLOCK>(aring + st * BLOCK * P, al + t * nslots, kAl);
+        const int st = (int)((gterm + t) % S);
+        if (tid == 0) {
+          mbar_expect_tx(bar_a + st, (unsigned)kAl);
+          bulk_g2s(aring + st * BLOCK * P, al + t * nslots, (unsigned)kAl, bar_a + st);
+        }
         const T2* __restrict__ gt = G + t * gstride;
         T2* tile = tring + st * cap;
 #pragma unroll
@@ -1160,16 +1201,17 @@ __global__ void __launch_bounds__(K3Cfg<T2>::BLOCK, K3Cfg<T2>::MINB)
     if (q == 0) {  // no term loop: fetch the next chunk's tables here
       __syncthreads();
       prefetch_meta(ch + gridDim.x, buf ^ 1);
-      cp_async_commit();
     }
     T2 acc[P];
 #pragma unroll
     for (int k = 0; k < P; ++k) acc[k] = mk<T2>(0, 0);
     for (int t = 0; t < q; ++t) {
+      const int st = (int)((gterm + t) % S);
       cp_async_wait<S - 2>();
+      mbar_wait(bar_a + st, (unsigned)((gterm + t) / S) & 1u);
       __syncthreads();  // term t staged by every thread; every thread is done with term t-1
       issue(t + S - 1, t == 0);
-      const T2* __restrict__ win = tring + (t % S) * cap + woff;
+      const T2* __restrict__ win = tring + st * cap + woff;
       T2 F[P];
 #pragma unroll
       for (int k = 0; k < P; ++k) F[k] = mk<T2>(0, 0);
@@ -1207,7 +1249,7 @@ __global__ void __launch_bounds__(K3Cfg<T2>::BLOCK, K3Cfg<T2>::MINB)
           F[k] = cfma_real(w1[k], rr, F[k]);
         }
       }
-      const T2* ring = aring + (t % S) * BLOCK * P + tid;
+      const T2* ring = aring + st * BLOCK * P + tid;
 #pragma unroll
       for (int k = 0; k < P; ++k) {
         const T2 av = ring[k * BLOCK];
@@ -1215,6 +1257,7 @@ __global__ void __launch_bounds__(K3Cfg<T2>::BLOCK, K3Cfg<T2>::MINB)
         acc[k].y = fma(av.x, F[k].y, fma(av.y, F[k].x, acc[k].y));
       }
     }
+    gterm += q;
     cp_async_wait<0>();  // the running sums (in the first copy group) have landed
     T2 f0 = mk<T2>(0, 0);
     if (first && add_dc) f0 = fhat[0];
