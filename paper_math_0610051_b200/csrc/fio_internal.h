@@ -50,15 +50,10 @@ constexpr int kK3BlockC128 = FIO_K3_BLOCK128;  // complex128
 #ifndef FIO_K3_CAP128
 #define FIO_K3_CAP128 384
 #endif
-// K3 pipeline depth (terms in flight: fine-grid tiles + alpha').  Measured at N = 1024 (K3 ms):
-// complex64 2 / 3 / 4 stages 2.59 / 2.62 / 2.72, complex128 11.16 / 12.47 / 12.52 -- shallower rings
-// leave room for more CTAs per SM, which hide the latency better than a deeper ring.
-#ifndef FIO_K3_STAGES64
-#define FIO_K3_STAGES64 2
-#endif
-#ifndef FIO_K3_STAGES128
-#define FIO_K3_STAGES128 2
-#endif
+// K3 pipeline: the term loop advances TT terms per step and stages the next step while computing
+// (a ring of 2 TT terms; fio_kernels.cu K3Cfg).  Measured at N = 1024 (K3 ms, TT = 1): complex64 ring
+// of 2 / 3 / 4 terms 2.59 / 2.62 / 2.72, complex128 11.16 / 12.47 / 12.52 -- shallow rings leave room
+// for more CTAs per SM, which hide latency better than a deeper ring.
 constexpr int kK3TileCapC64 = FIO_K3_CAP64;     // max cells of a K3 chunk footprint, complex64
 constexpr int kK3TileCapC128 = FIO_K3_CAP128;   // complex128
 constexpr int kHalo = 8;  // periodic column halo on each side of a fine-grid row (K2 writes, K3 reads)

@@ -961,14 +961,22 @@ template <> struct K3Cfg<float2> {
 #ifndef FIO_K3_MINB64
 #define FIO_K3_MINB64 8
 #endif
-  static constexpr int BLOCK = kK3BlockC64, MINB = FIO_K3_MINB64, STAGES = FIO_K3_STAGES64;
+#ifndef FIO_K3_TT64
+#define FIO_K3_TT64 1
+#endif
+  // TT terms per step of the term loop (interleaved: more independent FMA chains per row); the ring
+  // holds two steps (the one computed and the one in flight)
+  static constexpr int BLOCK = kK3BlockC64, MINB = FIO_K3_MINB64, TT = FIO_K3_TT64, STAGES = 2 * TT;
   static_assert(kK3TileCapC64 % (2 * BLOCK) == 0, "tile cap: a whole number of 16-byte units per thread");
 };
 template <> struct K3Cfg<double2> {
 #ifndef FIO_K3_MINB128
 #define FIO_K3_MINB128 4
 #endif
-  static constexpr int BLOCK = kK3BlockC128, MINB = FIO_K3_MINB128, STAGES = FIO_K3_STAGES128;
+#ifndef FIO_K3_TT128
+#define FIO_K3_TT128 1
+#endif
+  static constexpr int BLOCK = kK3BlockC128, MINB = FIO_K3_MINB128, TT = FIO_K3_TT128, STAGES = 2 * TT;
   static_assert(kK3TileCapC128 % BLOCK == 0, "tile cap: a whole number of 16-byte units per thread");
 };
 
@@ -1063,6 +1071,7 @@ __global__ void __launch_bounds__(K3Cfg<T2>::BLOCK, K3Cfg<T2>::MINB)
   constexpr int WINR = k3_window_rows(TAPS, C64);
   constexpr int BLOCK = K3Cfg<T2>::BLOCK;
   constexpr int S = K3Cfg<T2>::STAGES;
+  constexpr int TT = K3Cfg<T2>::TT;
   constexpr int EPC = 16 / (int)sizeof(T2);  // complex elements per 16-byte unit
   constexpr int RPV = 16 / (int)sizeof(Rt);  // row weights per 16-byte unit
   constexpr int MAXC = C64 ? kK3TileCapC64 / 2 / BLOCK : kK3TileCapC128 / BLOCK;  // tile units per thread
@@ -1168,7 +1177,7 @@ __global__ void __launch_bounds__(K3Cfg<T2>::BLOCK, K3Cfg<T2>::MINB)
       cp_async_commit();
     };
 #pragma unroll
-    for (int s = 0; s < S - 1; ++s) issue(s, false);
+    for (int u = 0; u < TT; ++u) issue(u, false);
     // weights of this thread's points: phi2 (columns) in registers, phi1 (rows) in shared memory
     const int2 an = m_anchor[tid];
     const int woff = (an.x - br) * bnc + (an.y - bc);
@@ -1205,31 +1214,25 @@ __global__ void __launch_bounds__(K3Cfg<T2>::BLOCK, K3Cfg<T2>::MINB)
     T2 acc[P];
 #pragma unroll
     for (int k = 0; k < P; ++k) acc[k] = mk<T2>(0, 0);
-    for (int t = 0; t < q; ++t) {
-      const int st = (int)((gterm + t) % S);
-      cp_async_wait<S - 2>();
-      mbar_wait(bar_a + st, (unsigned)((gterm + t) / S) & 1u);
-      __syncthreads();  // term t staged by every thread; every thread is done with term t-1
-      issue(t + S - 1, t == 0);
-      const T2* __restrict__ win = tring + st * cap + woff;
-      T2 F[P];
+    for (int t0 = 0; t0 < q; t0 += TT) {
+      // step: terms t0 .. t0 + TT - 1 (those < q); their tiles are the only copies in flight
+      cp_async_wait<0>();
 #pragma unroll
-      for (int k = 0; k < P; ++k) F[k] = mk<T2>(0, 0);
+      for (int u = 0; u < TT; ++u)
+        if (t0 + u < q) mbar_wait(bar_a + (gterm + t0 + u) % S, (unsigned)((gterm + t0 + u) / S) & 1u);
+      __syncthreads();  // this step staged by every thread; every thread is done with the previous step
+#pragma unroll
+      for (int u = 0; u < TT; ++u) issue(t0 + TT + u, t0 == 0 && u == 0);
+      const T2* __restrict__ win[TT];
+#pragma unroll
+      for (int u = 0; u < TT; ++u) win[u] = tring + (int)((gterm + t0 + u) % S) * cap + woff;
+      T2 F[TT][P];
+#pragma unroll
+      for (int u = 0; u < TT; ++u)
+#pragma unroll
+        for (int k = 0; k < P; ++k) F[u][k] = mk<T2>(0, 0);
 #pragma unroll
       for (int i = 0; i < WINR; ++i) {
-        T2 v[WIN];
-        if constexpr (C64 && WIN % 2 == 0) {  // complex64: even anchors -> 16-byte aligned pairs
-          const float4* wp = reinterpret_cast<const float4*>(win + i * bnc);
-#pragma unroll
-          for (int jj = 0; jj < WIN / 2; ++jj) {
-            const float4 a = wp[jj];
-            v[2 * jj] = mk<T2>(a.x, a.y);
-            v[2 * jj + 1] = mk<T2>(a.z, a.w);
-          }
-        } else {
-#pragma unroll
-          for (int jj = 0; jj < WIN; ++jj) v[jj] = win[i * bnc + jj];
-        }
         Rt w1[P];
 #pragma unroll
         for (int cc = 0; cc < P / RPV; ++cc) {
@@ -1242,19 +1245,40 @@ __global__ void __launch_bounds__(K3Cfg<T2>::BLOCK, K3Cfg<T2>::MINB)
           }
         }
 #pragma unroll
-        for (int k = 0; k < P; ++k) {
-          T2 rr = mk<T2>(0, 0);
+        for (int u = 0; u < TT; ++u) {
+          if (TT > 1 && t0 + u >= q) continue;  // uniform: the last step may be partial
+          T2 v[WIN];
+          if constexpr (C64 && WIN % 2 == 0) {  // complex64: even anchors -> 16-byte aligned pairs
+            const float4* wp = reinterpret_cast<const float4*>(win[u] + i * bnc);
 #pragma unroll
-          for (int jj = 0; jj < WIN; ++jj) rr = cfma_real(p2[k][jj], v[jj], rr);
-          F[k] = cfma_real(w1[k], rr, F[k]);
+            for (int jj = 0; jj < WIN / 2; ++jj) {
+              const float4 a = wp[jj];
+              v[2 * jj] = mk<T2>(a.x, a.y);
+              v[2 * jj + 1] = mk<T2>(a.z, a.w);
+            }
+          } else {
+#pragma unroll
+            for (int jj = 0; jj < WIN; ++jj) v[jj] = win[u][i * bnc + jj];
+          }
+#pragma unroll
+          for (int k = 0; k < P; ++k) {
+            T2 rr = mk<T2>(0, 0);
+#pragma unroll
+            for (int jj = 0; jj < WIN; ++jj) rr = cfma_real(p2[k][jj], v[jj], rr);
+            F[u][k] = cfma_real(w1[k], rr, F[u][k]);
+          }
         }
       }
-      const T2* ring = aring + st * BLOCK * P + tid;
 #pragma unroll
-      for (int k = 0; k < P; ++k) {
-        const T2 av = ring[k * BLOCK];
-        acc[k].x = fma(av.x, F[k].x, fma(-av.y, F[k].y, acc[k].x));
-        acc[k].y = fma(av.x, F[k].y, fma(av.y, F[k].x, acc[k].y));
+      for (int u = 0; u < TT; ++u) {
+        if (TT > 1 && t0 + u >= q) continue;
+        const T2* ring = aring + (int)((gterm + t0 + u) % S) * BLOCK * P + tid;
+#pragma unroll
+        for (int k = 0; k < P; ++k) {
+          const T2 av = ring[k * BLOCK];
+          acc[k].x = fma(av.x, F[u][k].x, fma(-av.y, F[u][k].y, acc[k].x));
+          acc[k].y = fma(av.x, F[u][k].y, fma(av.y, F[u][k].x, acc[k].y));
+        }
       }
     }
     gterm += q;
