@@ -45,7 +45,7 @@ FIO_HD_EARLY constexpr int group_p(bool c64, int taps) {
 constexpr int kK3BlockC64 = FIO_K3_BLOCK64;    // K3 threads per CTA (= groups per chunk), complex64
 constexpr int kK3BlockC128 = FIO_K3_BLOCK128;  // complex128
 #ifndef FIO_K3_CAP64
-#define FIO_K3_CAP64 512
+#define FIO_K3_CAP64 384
 #endif
 #ifndef FIO_K3_CAP128
 #define FIO_K3_CAP128 384

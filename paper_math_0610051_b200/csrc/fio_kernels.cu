@@ -959,14 +959,17 @@ template <typename T2, int TAPS> struct GroupP { static constexpr int value = gr
 template <typename T2> struct K3Cfg;
 template <> struct K3Cfg<float2> {
 #ifndef FIO_K3_MINB64
-#define FIO_K3_MINB64 8
+#define FIO_K3_MINB64 10
 #endif
 #ifndef FIO_K3_TT64
 #define FIO_K3_TT64 1
 #endif
   // TT terms per step of the term loop (interleaved: more independent FMA chains per row); the ring
   // holds two steps (the one computed and the one in flight)
-  static constexpr int BLOCK = kK3BlockC64, MINB = FIO_K3_MINB64, TT = FIO_K3_TT64, STAGES = 2 * TT;
+  // 10 CTAs per SM (102 registers) measured 5 % faster than 8 at N = 1024 for w <= 8 (the c64 range
+  // the eps floor allows); wider windows take 8 or 6, which they need to stay free of spills
+  static constexpr int BLOCK = kK3BlockC64, TT = FIO_K3_TT64, STAGES = 2 * TT;
+  static constexpr int minb(int taps) { return taps <= 8 ? FIO_K3_MINB64 : (taps <= 10 ? 8 : 6); }
   static_assert(kK3TileCapC64 % (2 * BLOCK) == 0, "tile cap: a whole number of 16-byte units per thread");
 };
 template <> struct K3Cfg<double2> {
@@ -976,7 +979,8 @@ template <> struct K3Cfg<double2> {
 #ifndef FIO_K3_TT128
 #define FIO_K3_TT128 1
 #endif
-  static constexpr int BLOCK = kK3BlockC128, MINB = FIO_K3_MINB128, TT = FIO_K3_TT128, STAGES = 2 * TT;
+  static constexpr int BLOCK = kK3BlockC128, TT = FIO_K3_TT128, STAGES = 2 * TT;
+  static constexpr int minb(int) { return FIO_K3_MINB128; }
   static_assert(kK3TileCapC128 % BLOCK == 0, "tile cap: a whole number of 16-byte units per thread");
 };
 
@@ -1060,7 +1064,7 @@ __device__ __forceinline__ void cta_copy16(void* dst, const void* src, int bytes
 // each point occurs in exactly one group per wedge, so one launch per wedge is race-free and the
 // summation order over wedges is fixed (deterministic).
 template <typename T2, int TAPS, int P>
-__global__ void __launch_bounds__(K3Cfg<T2>::BLOCK, K3Cfg<T2>::MINB)
+__global__ void __launch_bounds__(K3Cfg<T2>::BLOCK, K3Cfg<T2>::minb(TAPS))
     k_interp_groups(InterpWedge iw, const T2* __restrict__ gbase, const double2* __restrict__ a0,
                     const T2* __restrict__ fhat, int first, int add_dc, EsPoly poly, T2* __restrict__ Lf) {
   using Rt = typename Real<T2>::type;
