@@ -179,6 +179,16 @@ fio_status fio_apply_batch(fio_handle h, int nrhs, const void* f_dev, void* Lf_d
  * fio_apply gives Lf_dev (the row slab with a communicator). */
 fio_status fio_apply_host(fio_handle h, const void* f_host, void* Lf_host, void* stream);
 
+/* Streaming end-to-end variant (serving loop): Lf_i = L f_i for i < count, f_host holding `count`
+ * contiguous N x N HOST inputs and Lf_host `count` contiguous HOST outputs of fio_apply's shape
+ * (both pinned for overlap; no overlap between them).  Every input is copied to the device and
+ * every result back inside the call, pipelined: the copy of input i+1 and the read-back of result
+ * i-1 run on two plan-owned copy streams while apply i runs on `stream` (double-buffered device
+ * staging, allocated on first use).  The results equal fio_apply's bit for bit (a communicator
+ * plan: every rank calls it with the same count).  `stream` is synchronized before return.
+ * Errors: FIO_EINVAL (arguments, count < 0), FIO_ECUDA, FIO_ENCCL. */
+fio_status fio_apply_host_stream(fio_handle h, int count, const void* f_host, void* Lf_host, void* stream);
+
 fio_status fio_destroy(fio_handle h);
 
 typedef struct {

@@ -9,6 +9,7 @@ CUDA device is missing, calls raise.
     Plan(N, c1, c2, ...)      fio_plan     (PAPER.md:981-1008, 1111-1250)
     Plan.apply(f)             fio_apply, device tensors
     Plan.apply_host(f, out)   fio_apply_host (host buffers, copies included)
+    Plan.apply_host_stream(fs, outs)  fio_apply_host_stream (a stream of host inputs, copies pipelined)
     Plan(..., nranks=R, group=g)  wedge-sharded plan; the library's NCCL communicator sums the
                               ranks' partials (fio_apply returns this rank's row slab)
     nccl_unique_id()          fio_nccl_unique_id (host only)
@@ -35,7 +36,7 @@ FIO_C64, FIO_C128 = 1, 2
 FIO_OK, FIO_WNOTCERT = 0, 1
 
 # every entry point declared in include/fio.h
-SYMBOLS = ["fio_default_opts", "fio_plan", "fio_plan_save", "fio_plan_load", "fio_apply", "fio_apply_batch", "fio_apply_adjoint", "fio_apply_host", "fio_destroy", "fio_plan_info",
+SYMBOLS = ["fio_default_opts", "fio_plan", "fio_plan_save", "fio_plan_load", "fio_apply", "fio_apply_batch", "fio_apply_adjoint", "fio_apply_host", "fio_apply_host_stream", "fio_destroy", "fio_plan_info",
            "fio_plan_wedges", "fio_geometry", "fio_assign_wedges", "fio_profile_begin", "fio_profile_end",
            "fio_last_error", "fio_version", "fio_nccl_unique_id", "fio_partition_weights"]
 NCCL_ID_BYTES = 128
@@ -104,6 +105,7 @@ def load_library():
                                   ctypes.c_double, ctypes.POINTER(_Opts)]
     lib.fio_apply.argtypes = [P, P, P, P]
     lib.fio_apply_host.argtypes = [P, P, P, P]
+    lib.fio_apply_host_stream.argtypes = [P, I, P, P, P]
     lib.fio_apply_adjoint.argtypes = [P, P, P, P]
     lib.fio_apply_batch.argtypes = [P, I, P, P, P]
     lib.fio_destroy.argtypes = [P]
@@ -117,7 +119,8 @@ def load_library():
     lib.fio_partition_weights.argtypes = [I, ctypes.c_double, I, I, P]
     lib.fio_last_error.restype = ctypes.c_char_p
     lib.fio_version.restype = ctypes.c_char_p
-    for name in ["fio_plan", "fio_apply", "fio_apply_batch", "fio_apply_adjoint", "fio_apply_host", "fio_destroy", "fio_plan_info", "fio_plan_wedges",
+    for name in ["fio_plan", "fio_apply", "fio_apply_batch", "fio_apply_adjoint", "fio_apply_host",
+                 "fio_apply_host_stream", "fio_destroy", "fio_plan_info", "fio_plan_wedges",
                  "fio_geometry", "fio_assign_wedges", "fio_profile_begin", "fio_profile_end", "fio_nccl_unique_id",
                  "fio_partition_weights"]:
         getattr(lib, name).restype = ctypes.c_int
@@ -336,6 +339,27 @@ class Plan:
                                         ctypes.c_void_p(out_host.data_ptr()), ctypes.c_void_p(stream.cuda_stream)))
         return out_host
 
+
+    def apply_host_stream(self, f_host, out_host, stream=None):
+        """L f_i for a stream of host (pinned) inputs f_host (count, N, N) into out_host (count, out_rows, N):
+        one fio_apply_host_stream call; every copy happens inside it, pipelined with the applies."""
+        import torch
+        count = int(f_host.shape[0]) if f_host.dim() == 3 else -1
+        if count < 0 or out_host.dim() != 3 or out_host.shape[0] != count:
+            raise FioError(-1, "apply_host_stream: f_host (count, N, N) and out_host (count, out_rows, N)")
+        if count and (f_host.is_cuda or f_host.dtype != self.torch_dtype or not f_host.is_contiguous()
+                      or tuple(f_host.shape[1:]) != (self.N, self.N)):
+            raise FioError(-1, f"f_host must be a contiguous CPU {self.torch_dtype} tensor (count, {self.N}, {self.N})")
+        if count and (out_host.is_cuda or out_host.dtype != self.torch_dtype or not out_host.is_contiguous()
+                      or tuple(out_host.shape[1:]) != (self.out_rows, self.N)):
+            raise FioError(-1, f"out_host must be a contiguous CPU {self.torch_dtype} tensor "
+                               f"(count, {self.out_rows}, {self.N})")
+        if stream is None:
+            stream = torch.cuda.current_stream(self.device)
+        _check(self._lib.fio_apply_host_stream(self._h, count, ctypes.c_void_p(f_host.data_ptr()),
+                                               ctypes.c_void_p(out_host.data_ptr()),
+                                               ctypes.c_void_p(stream.cuda_stream)))
+        return out_host
 
     def profile_begin(self, max_applies: int):
         """Record per-stage CUDA events for the next max_applies applies (on their stream)."""

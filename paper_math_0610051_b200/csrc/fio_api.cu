@@ -136,6 +136,10 @@ struct fio_plan_s {
   int njobs_row = 0, njobs_col = 0, smem_row = 0, smem_col = 0;
   int rows_per_cta_N = 1, cols_per_cta_N = 1, fft_N = 0;
   void *e2e_in = nullptr, *e2e_out = nullptr;
+  // fio_apply_host_stream: double-buffered staging, its two copy streams and the pipeline's events
+  void *hs_in[2] = {nullptr, nullptr}, *hs_out[2] = {nullptr, nullptr};
+  cudaStream_t hs_h2d = nullptr, hs_d2h = nullptr;
+  cudaEvent_t hs_fork = nullptr, hs_join = nullptr, hs_in_ready[2] = {}, hs_done[2] = {}, hs_out_free[2] = {};
   void* batch_ws = nullptr;  // (nrhs - 1) x (fhat + fine grids + K3 accumulator) for fio_apply_batch
   cudaStream_t side = nullptr;  // plan-owned side stream (skeleton-mode K3, adjoint spreads)
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
@@ -195,6 +199,11 @@ struct fio_plan_s {
     if (ev_fork) cudaEventDestroy(ev_fork);
     if (ev_join) cudaEventDestroy(ev_join);
     if (side) cudaStreamDestroy(side);
+    for (cudaEvent_t e : {hs_fork, hs_join, hs_in_ready[0], hs_in_ready[1], hs_done[0], hs_done[1], hs_out_free[0],
+                          hs_out_free[1]})
+      if (e) cudaEventDestroy(e);
+    if (hs_h2d) cudaStreamDestroy(hs_h2d);
+    if (hs_d2h) cudaStreamDestroy(hs_d2h);
     if (batch_ws) cudaFree(batch_ws);
     if (part) cudaFree(part);
     comm_destroy(comm);
@@ -1593,6 +1602,58 @@ fio_status fio_apply_host(fio_handle h, const void* f_host, void* Lf_host, void*
   fio_status st = fio_apply(h, h->e2e_in, h->e2e_out, stream);
   if (st != FIO_OK) return st;
   FIO_CUDA(cudaMemcpyAsync(Lf_host, h->e2e_out, out_bytes, cudaMemcpyDeviceToHost, s));
+  FIO_CUDA(cudaStreamSynchronize(s));
+  return FIO_OK;
+}
+
+fio_status fio_apply_host_stream(fio_handle h, int count, const void* f_host, void* Lf_host, void* stream) {
+  if (!h || count < 0 || (count > 0 && (!f_host || !Lf_host))) {
+    set_error("fio_apply_host_stream: bad arguments");
+    return FIO_EINVAL;
+  }
+  if (count == 0) return FIO_OK;
+  const size_t bytes = (size_t)h->N * h->N * h->elem_bytes();
+  const size_t out_bytes = (size_t)h->out_rows() * h->N * h->elem_bytes();
+  FIO_GUARD(h->device)
+  if (!h->hs_in[0]) {
+    for (int b = 0; b < 2; ++b) {
+      FIO_CUDA(h->alloc(&h->hs_in[b], bytes));
+      FIO_CUDA(h->alloc(&h->hs_out[b], bytes));
+      FIO_CUDA(cudaEventCreateWithFlags(&h->hs_in_ready[b], cudaEventDisableTiming));
+      FIO_CUDA(cudaEventCreateWithFlags(&h->hs_done[b], cudaEventDisableTiming));
+      FIO_CUDA(cudaEventCreateWithFlags(&h->hs_out_free[b], cudaEventDisableTiming));
+    }
+    FIO_CUDA(cudaEventCreateWithFlags(&h->hs_fork, cudaEventDisableTiming));
+    FIO_CUDA(cudaEventCreateWithFlags(&h->hs_join, cudaEventDisableTiming));
+    FIO_CUDA(cudaStreamCreateWithFlags(&h->hs_h2d, cudaStreamNonBlocking));
+    FIO_CUDA(cudaStreamCreateWithFlags(&h->hs_d2h, cudaStreamNonBlocking));
+  }
+  cudaStream_t s = (cudaStream_t)stream;
+  // the copy streams start behind everything already enqueued on `stream`
+  FIO_CUDA(cudaEventRecord(h->hs_fork, s));
+  FIO_CUDA(cudaStreamWaitEvent(h->hs_h2d, h->hs_fork, 0));
+  FIO_CUDA(cudaStreamWaitEvent(h->hs_d2h, h->hs_fork, 0));
+  for (int i = 0; i < count; ++i) {
+    const int b = i & 1;
+    const char* in = static_cast<const char*>(f_host) + (size_t)i * bytes;
+    char* out = static_cast<char*>(Lf_host) + (size_t)i * out_bytes;
+    // input i into staging b once apply i-2 has consumed it
+    if (i >= 2) FIO_CUDA(cudaStreamWaitEvent(h->hs_h2d, h->hs_done[b], 0));
+    FIO_CUDA(cudaMemcpyAsync(h->hs_in[b], in, bytes, cudaMemcpyHostToDevice, h->hs_h2d));
+    FIO_CUDA(cudaEventRecord(h->hs_in_ready[b], h->hs_h2d));
+    // apply i once its input has landed and the read-back of output i-2 has left staging b
+    FIO_CUDA(cudaStreamWaitEvent(s, h->hs_in_ready[b], 0));
+    if (i >= 2) FIO_CUDA(cudaStreamWaitEvent(s, h->hs_out_free[b], 0));
+    fio_status st = fio_apply(h, h->hs_in[b], h->hs_out[b], stream);
+    if (st != FIO_OK) return st;
+    FIO_CUDA(cudaEventRecord(h->hs_done[b], s));
+    // read-back of output i on the second copy stream (both copy directions overlap the applies)
+    FIO_CUDA(cudaStreamWaitEvent(h->hs_d2h, h->hs_done[b], 0));
+    FIO_CUDA(cudaMemcpyAsync(out, h->hs_out[b], out_bytes, cudaMemcpyDeviceToHost, h->hs_d2h));
+    FIO_CUDA(cudaEventRecord(h->hs_out_free[b], h->hs_d2h));
+  }
+  FIO_CUDA(cudaEventRecord(h->hs_join, h->hs_d2h));
+  FIO_CUDA(cudaStreamWaitEvent(s, h->hs_join, 0));
   FIO_CUDA(cudaStreamSynchronize(s));
   return FIO_OK;
 }

@@ -47,6 +47,10 @@ def test_one_rank_communicator_matches_plain_apply(dtype, eps):
     hout = torch.empty_like(hin).pin_memory()
     comm.apply_host(hin, hout)
     assert torch.equal(hout, a.cpu())
+    hs = torch.stack([f.cpu(), (2 * f).cpu(), f.cpu()]).pin_memory()
+    ho = torch.empty_like(hs).pin_memory()
+    comm.apply_host_stream(hs, ho)
+    assert torch.equal(ho[0], a.cpu()) and torch.equal(ho[2], a.cpu())
     ga, gb = plain.apply_adjoint(f), comm.apply_adjoint(f)
     assert oracle.rel_l2(gb.cpu().numpy(), ga.cpu().numpy()) <= 1e-5  # atomics: last bits may differ
 

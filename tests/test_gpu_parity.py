@@ -155,6 +155,27 @@ def test_linearity_and_apply_host():
     assert np.array_equal(hout.numpy(), Lf)
 
 
+@pytest.mark.parametrize("dtype,eps", [("c128", 1e-6), ("c64", 1e-4)])
+def test_apply_host_stream_equals_apply(dtype, eps):
+    # fio_apply_host_stream (pipelined copies, double-buffered staging): every result is fio_apply's,
+    # bit for bit, for distinct inputs -- odd count so both staging buffers are reused and one is
+    # left half-used; count 0 is a no-op
+    N, count = 96, 5
+    op = wl.grt_operator(N)
+    plan = fio.Plan(N, op.c1, op.c2, eps=eps, dtype=dtype, device=0)
+    tdt = torch.complex64 if dtype == "c64" else torch.complex128
+    fs = torch.stack([torch.from_numpy(crandn(N, 10 + i)).to(tdt) for i in range(count)]).pin_memory()
+    outs = torch.full((count, N, N), float("nan"), dtype=tdt).pin_memory()
+    plan.apply_host_stream(fs, outs)
+    for i in range(count):
+        assert torch.equal(outs[i], plan.apply(fs[i].to(DEV)).cpu()), i
+    plan.apply_host_stream(fs[:0], outs[:0])
+    with pytest.raises(fio.FioError):
+        plan.apply_host_stream(fs, outs[:2])
+    with pytest.raises(fio.FioError):
+        plan.apply_host_stream(fs.to(torch.complex64 if dtype == "c128" else torch.complex128), outs)
+
+
 def test_invalid_arguments():
     op = wl.grt_operator(64)
     with pytest.raises(fio.FioError):
