@@ -320,7 +320,8 @@ def time_config(name, args, rank, world, local, group):
     try:
         with open(os.path.join(ROOT, "profiles", "r02_k3_traffic.json")) as fh:
             tr = json.load(fh).get(name)
-        if tr and world == 1 and tr.get("sum_q") == info["sum_q"]:
+        if (tr and world == 1 and tr.get("sum_q") == info["sum_q"]
+                and tr.get("max_tile_cap") == info["max_tile_cap"]):
             traffic = tr["dram_bytes"]
     except Exception:
         traffic = None

@@ -1,11 +1,12 @@
 """Sum the DRAM bytes of all K3 launches of one apply from ncu --csv metric dumps.
 
-usage: python tools/k3_traffic.py OUT.json cfg=path.csv:SUM_Q [cfg=path.csv:SUM_Q ...]
+usage: python tools/k3_traffic.py OUT.json cfg=path.csv:SUM_Q:MAX_TILE_CAP [...]
 Each csv comes from
   ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum --clock-control none \
       -k regex:k_interp_groups --csv python tools/run_apply.py CFG 1
-(every K3 launch of one apply, cold cache per launch); SUM_Q is the plan's sum of separation ranks
-(printed by run_apply.py), so bench.py uses the capture only for the plan it was taken on.
+(every K3 launch of one apply, cold cache per launch); SUM_Q and MAX_TILE_CAP are the plan's sum of
+separation ranks and largest K3 chunk footprint (printed by run_apply.py), so bench.py uses the capture
+only for the plan (and K3 chunking) it was taken on.
 """
 import csv
 import json
@@ -32,10 +33,10 @@ def main():
     out = {}
     for arg in sys.argv[2:]:
         cfg, rest = arg.split("=", 1)
-        path, sum_q = rest.rsplit(":", 1)
+        path, sum_q, cap = rest.rsplit(":", 2)
         n, acc = parse(path)
         rd, wr = acc.get("dram__bytes_read.sum", 0.0), acc.get("dram__bytes_write.sum", 0.0)
-        out[cfg] = {"launches": n, "sum_q": int(sum_q), "dram_read_bytes": rd, "dram_write_bytes": wr,
+        out[cfg] = {"launches": n, "sum_q": int(sum_q), "max_tile_cap": int(cap), "dram_read_bytes": rd, "dram_write_bytes": wr,
                     "dram_bytes": rd + wr,
                     "ncu_time_s": acc.get("gpu__time_duration.sum", 0.0),
                     "how": "ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum "

@@ -18,4 +18,4 @@ f = torch.from_numpy(wl.make_input(cfg)).to("cuda:0", torch.complex64 if cfg["dt
 for _ in range(n):
     out = plan.apply(f)
 torch.cuda.synchronize()
-print(name, plan.info["sum_q"], float(out.abs().mean()))
+print(name, plan.info["sum_q"], plan.info["max_tile_cap"], float(out.abs().mean()))
