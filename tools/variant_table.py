@@ -22,7 +22,8 @@ def rows(path, with_k12=False):
             st = r["stages"]
             k12 = f"K1 {st['K1_rowpass']:6.3f} K2 {st['K2_colpass']:6.3f}  " if with_k12 else ""
             out.append(f"  {name:8s} {d['flags'][:70]:70s} {cfg:10s} {k12}K3 {st['K3_interp']:7.3f}  apply "
-                       f"{r['ms']:7.3f}  err {r['err']:.2e}  P {r.get('group_p')}")
+                       f"{r['ms']:7.3f}  " + (f"err {r['err']:.2e}" if "err" in r else f"dev {r['dev']:.1e}") +
+                       f"  P {r.get('group_p')}")
     return out
 
 
