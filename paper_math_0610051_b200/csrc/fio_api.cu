@@ -4,6 +4,7 @@
 
 #include <algorithm>
 #include <chrono>
+#include <climits>
 #include <cmath>
 #include <cstdlib>
 #include <future>
@@ -623,6 +624,58 @@ struct K3Tables {
   long long cap = 0, real_groups = 0;
   int nchunks = 0;
 };
+// Bank-conflict-free lane order inside one K3 chunk.  K3 reads every window row with 16-byte shared
+// loads at (16-byte unit) offset u_g + const, u_g = ((a1 - r0) cols + (a2 - c0)) / epc for the group g
+// a lane holds; a quarter-warp (8 lanes) is served in one wavefront iff its lanes' u_g are distinct mod 8
+// or equal (same anchor: a broadcast).  Place the n groups on the blk lanes so that every quarter-warp
+// holds at most one distinct u per residue (greedy: largest same-anchor runs first, kept together);
+// padding lanes copy the anchor of a group of their quarter-warp.  lane_src[i] = group (0..n-1) on lane
+// i, or -1 - g for a padding lane repeating group g's anchor.  Pure reordering: the arithmetic of every
+// point is unchanged (K3 results are identical; the adjoint's spread sums in another order).
+static void chunk_lane_order(const int* anc, int n, int blk, int r0, int c0, int cols, int epc, int* lane_src) {
+  constexpr int kQ = 8;  // lanes per quarter-warp (16-byte loads)
+  const int nq = blk / kQ;
+  std::vector<long long> u(n);
+  for (int g = 0; g < n; ++g) u[g] = ((long long)(anc[2 * g] - r0) * cols + (anc[2 * g + 1] - c0)) / epc;
+  // runs of groups with the same u (same anchor), in their original order
+  std::vector<std::pair<int, int>> runs;  // (first group, length)
+  for (int g = 0; g < n;) {
+    int e = g + 1;
+    while (e < n && u[e] == u[g]) ++e;
+    runs.push_back({g, e - g});
+    g = e;
+  }
+  std::stable_sort(runs.begin(), runs.end(), [](const auto& a, const auto& b) { return a.second > b.second; });
+  std::vector<int> fill(nq, 0);
+  std::vector<long long> res_u((size_t)nq * kQ, -1);  // per quarter-warp and residue: the u it holds
+  std::vector<int> lanes((size_t)nq * kQ, INT_MIN);
+  for (const auto& run : runs) {
+    const long long ur = u[run.first];
+    const int r = (int)(((ur % kQ) + kQ) % kQ);
+    int left = run.second, g = run.first;
+    while (left > 0) {
+      int best = -1;
+      for (int qw = 0; qw < nq && best < 0; ++qw)  // a quarter-warp already holding this u
+        if (fill[qw] < kQ && res_u[(size_t)qw * kQ + r] == ur) best = qw;
+      for (int qw = 0; qw < nq && best < 0; ++qw)  // else one where the residue is free
+        if (fill[qw] < kQ && res_u[(size_t)qw * kQ + r] < 0) best = qw;
+      for (int qw = 0; qw < nq && best < 0; ++qw)  // else any room (a conflict the chunk cannot avoid)
+        if (fill[qw] < kQ) best = qw;
+      if (res_u[(size_t)best * kQ + r] < 0) res_u[(size_t)best * kQ + r] = ur;
+      const int take = std::min(left, kQ - fill[best]);
+      for (int k = 0; k < take; ++k) lanes[(size_t)best * kQ + fill[best]++] = g++;
+      left -= take;
+    }
+  }
+  for (int qw = 0; qw < nq; ++qw) {
+    const int rep = fill[qw] > 0 ? lanes[(size_t)qw * kQ] : 0;  // padding: a group of this quarter-warp
+    for (int k = 0; k < kQ; ++k) {
+      const int v = k < fill[qw] ? lanes[(size_t)qw * kQ + k] : -1 - rep;
+      lane_src[qw * kQ + k] = v;
+    }
+  }
+}
+
 static K3Tables make_k3_tables(std::vector<double> uh, long long NN, int taps, bool c64, int n1f, int n2f) {
   K3Tables T;
 #pragma omp parallel for schedule(static)
@@ -650,11 +703,15 @@ static K3Tables make_k3_tables(std::vector<double> uh, long long NN, int taps, b
 #pragma omp parallel for schedule(static)
   for (int c = 0; c < T.nchunks; ++c) {
     const long long g0 = box[6 * c], n = box[6 * c + 5];
+    std::vector<int> lane_src(blk);
+    chunk_lane_order(&anchor[2 * g0], (int)n, blk, box[6 * c + 1], box[6 * c + 2], box[6 * c + 4], c64 ? 2 : 1,
+                     lane_src.data());
     for (long long i = 0; i < blk; ++i) {
-      const long long src = g0 + (i < n ? i : 0), dst = (long long)c * blk + i;
+      const bool real = lane_src[i] >= 0;
+      const long long src = g0 + (real ? lane_src[i] : -1 - lane_src[i]), dst = (long long)c * blk + i;
       T.anchor[2 * dst] = anchor[2 * src];
       T.anchor[2 * dst + 1] = anchor[2 * src + 1];
-      if (i < n)
+      if (real)
         for (int k = 0; k < gp; ++k) {
           const long long ph = k3_slot(dst, k, gp, blk);
           T.slot_x[ph] = slot_x[src * gp + k];
