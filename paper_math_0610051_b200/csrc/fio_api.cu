@@ -624,56 +624,69 @@ struct K3Tables {
   long long cap = 0, real_groups = 0;
   int nchunks = 0;
 };
-// Bank-conflict-free lane order inside one K3 chunk.  K3 reads every window row with 16-byte shared
-// loads at (16-byte unit) offset u_g + const, u_g = ((a1 - r0) cols + (a2 - c0)) / epc for the group g
-// a lane holds; a quarter-warp (8 lanes) is served in one wavefront iff its lanes' u_g are distinct mod 8
-// or equal (same anchor: a broadcast).  Place the n groups on the blk lanes so that every quarter-warp
-// holds at most one distinct u per residue (greedy: largest same-anchor runs first, kept together);
-// padding lanes copy the anchor of a group of their quarter-warp.  lane_src[i] = group (0..n-1) on lane
-// i, or -1 - g for a padding lane repeating group g's anchor.  Pure reordering: the arithmetic of every
-// point is unchanged (K3 results are identical; the adjoint's spread sums in another order).
-static void chunk_lane_order(const int* anc, int n, int blk, int r0, int c0, int cols, int epc, int* lane_src) {
+// Bank-conflict-aware lane order inside one K3 chunk.  K3 reads every window row with 16-byte shared
+// loads at (16-byte unit) offset u_g + const, u_g = ((a1 - r0) stride + (a2 - c0)) / epc for the group
+// g a lane holds; a quarter-warp (8 lanes) takes one wavefront per distinct u among lanes with the
+// same u mod 8 (equal u, i.e. the same anchor, is a broadcast).  Place the n groups on the blk lanes so
+// that each quarter-warp holds at most one distinct u per residue where possible (greedy: largest
+// same-anchor runs first, kept together); padding lanes repeat the anchor of a group of their
+// quarter-warp.  lane_src[i] = group (0..n-1) on lane i, or -1 - g for a padding lane repeating group
+// g's anchor.  Returns the extra wavefronts per window-row load summed over the quarter-warps.
+// Pure reordering: every point's arithmetic is unchanged (K3 results are bit-identical).
+static long long chunk_lane_order(const int* anc, int n, int blk, int r0, int c0, int stride, int epc,
+                                  int* lane_src) {
   constexpr int kQ = 8;  // lanes per quarter-warp (16-byte loads)
   const int nq = blk / kQ;
   std::vector<long long> u(n);
-  for (int g = 0; g < n; ++g) u[g] = ((long long)(anc[2 * g] - r0) * cols + (anc[2 * g + 1] - c0)) / epc;
-  // runs of groups with the same u (same anchor), in their original order
-  std::vector<std::pair<int, int>> runs;  // (first group, length)
+  for (int g = 0; g < n; ++g) u[g] = ((long long)(anc[2 * g] - r0) * stride + (anc[2 * g + 1] - c0)) / epc;
+  std::vector<std::pair<int, int>> runs;  // (first group, length) of equal-u runs, in group order
   for (int g = 0; g < n;) {
     int e = g + 1;
     while (e < n && u[e] == u[g]) ++e;
     runs.push_back({g, e - g});
     g = e;
   }
-  std::stable_sort(runs.begin(), runs.end(), [](const auto& a, const auto& b) { return a.second > b.second; });
+  std::stable_sort(runs.begin(), runs.end(), [](const auto& x, const auto& y) { return x.second > y.second; });
   std::vector<int> fill(nq, 0);
-  std::vector<long long> res_u((size_t)nq * kQ, -1);  // per quarter-warp and residue: the u it holds
-  std::vector<int> lanes((size_t)nq * kQ, INT_MIN);
+  std::vector<int> lanes((size_t)nq * kQ, 0);
+  std::vector<std::vector<long long>> held((size_t)nq * kQ);  // per quarter-warp and residue: distinct u
   for (const auto& run : runs) {
     const long long ur = u[run.first];
     const int r = (int)(((ur % kQ) + kQ) % kQ);
     int left = run.second, g = run.first;
     while (left > 0) {
+      auto holds = [&](int qw) {
+        const auto& h = held[(size_t)qw * kQ + r];
+        return std::find(h.begin(), h.end(), ur) != h.end();
+      };
       int best = -1;
       for (int qw = 0; qw < nq && best < 0; ++qw)  // a quarter-warp already holding this u
-        if (fill[qw] < kQ && res_u[(size_t)qw * kQ + r] == ur) best = qw;
+        if (fill[qw] < kQ && holds(qw)) best = qw;
       for (int qw = 0; qw < nq && best < 0; ++qw)  // else one where the residue is free
-        if (fill[qw] < kQ && res_u[(size_t)qw * kQ + r] < 0) best = qw;
-      for (int qw = 0; qw < nq && best < 0; ++qw)  // else any room (a conflict the chunk cannot avoid)
-        if (fill[qw] < kQ) best = qw;
-      if (res_u[(size_t)best * kQ + r] < 0) res_u[(size_t)best * kQ + r] = ur;
+        if (fill[qw] < kQ && held[(size_t)qw * kQ + r].empty()) best = qw;
+      if (best < 0) {  // else the one with room whose residue holds the fewest (an unavoidable conflict)
+        size_t fewest = SIZE_MAX;
+        for (int qw = 0; qw < nq; ++qw)
+          if (fill[qw] < kQ && held[(size_t)qw * kQ + r].size() < fewest) {
+            fewest = held[(size_t)qw * kQ + r].size();
+            best = qw;
+          }
+      }
+      if (!holds(best)) held[(size_t)best * kQ + r].push_back(ur);
       const int take = std::min(left, kQ - fill[best]);
       for (int k = 0; k < take; ++k) lanes[(size_t)best * kQ + fill[best]++] = g++;
       left -= take;
     }
   }
+  long long extra = 0;
   for (int qw = 0; qw < nq; ++qw) {
+    size_t mx = 1;
+    for (int r = 0; r < kQ; ++r) mx = std::max(mx, held[(size_t)qw * kQ + r].size());
+    extra += (long long)mx - 1;
     const int rep = fill[qw] > 0 ? lanes[(size_t)qw * kQ] : 0;  // padding: a group of this quarter-warp
-    for (int k = 0; k < kQ; ++k) {
-      const int v = k < fill[qw] ? lanes[(size_t)qw * kQ + k] : -1 - rep;
-      lane_src[qw * kQ + k] = v;
-    }
+    for (int k = 0; k < kQ; ++k) lane_src[qw * kQ + k] = k < fill[qw] ? lanes[(size_t)qw * kQ + k] : -1 - rep;
   }
+  return extra;
 }
 
 static K3Tables make_k3_tables(std::vector<double> uh, long long NN, int taps, bool c64, int n1f, int n2f) {
@@ -692,20 +705,40 @@ static K3Tables make_k3_tables(std::vector<double> uh, long long NN, int taps, b
   T.nchunks = (int)(T.box.size() / 6);  // (chunk_boxes: 6 ints per chunk, widened to kBoxInts below)
   // pad every chunk to exactly blk groups, so that chunk c's groups are [c blk, (c+1) blk): K3 can then
   // prefetch a chunk's per-thread data without reading its box first.  Padding groups repeat the
-  // chunk's first anchor (inside the box), have no points (slot -1) and alpha' = 0.
+  // anchor of a group of their quarter-warp (inside the box), have no points (slot -1) and alpha' = 0;
+  // the groups' lane order and the tile's shared-memory row stride avoid bank conflicts
+  // (chunk_lane_order).
   // Slots are stored in K3's physical layout (k3_slot: element-major inside each chunk), so that one
   // bulk copy moves a chunk's slot indices, offsets or alpha'(t) straight into its shared-memory image.
   T.anchor.assign((size_t)T.nchunks * blk * 2, 0);
   T.slot_x.assign((size_t)T.nchunks * blk * gp, -1);
   T.off.assign((size_t)T.nchunks * blk * gp * 2, 0.5 * taps);
-  std::vector<int> box8((size_t)T.nchunks * kBoxInts, 0);  // per chunk: first group, r0, c0, rows, cols, groups, 0, 0
+  std::vector<int> box8((size_t)T.nchunks * kBoxInts, 0);  // per chunk: first group, r0, c0, rows, cols, groups,
+                                                           // shared-memory row stride, 0
+  std::vector<int> strides(T.nchunks);
   const std::vector<int>& box = T.box;
 #pragma omp parallel for schedule(static)
   for (int c = 0; c < T.nchunks; ++c) {
     const long long g0 = box[6 * c], n = box[6 * c + 5];
-    std::vector<int> lane_src(blk);
-    chunk_lane_order(&anchor[2 * g0], (int)n, blk, box[6 * c + 1], box[6 * c + 2], box[6 * c + 4], c64 ? 2 : 1,
-                     lane_src.data());
+    // the tile's shared-memory row stride: the copied width or up to 7 (16-byte units) more, the one
+    // whose best lane order leaves the fewest bank conflicts, inside the tile cap
+    const int epc = c64 ? 2 : 1, rows = box[6 * c + 3], cols = box[6 * c + 4];
+    const long long cap_c = c64 ? kK3TileCapC64 : kK3TileCapC128;
+    std::vector<int> lane_src(blk), trial(blk);
+    long long best = LLONG_MAX;
+    int stride = cols;
+    for (int st = cols; st <= cols + 7 * epc; st += epc) {
+      if (st > cols && (long long)rows * st > cap_c) break;
+      const long long ex = chunk_lane_order(&anchor[2 * g0], (int)n, blk, box[6 * c + 1], box[6 * c + 2], st, epc,
+                                            trial.data());
+      if (ex < best) {
+        best = ex;
+        stride = st;
+        lane_src.swap(trial);
+        if (ex == 0) break;
+      }
+    }
+    strides[c] = stride;
     for (long long i = 0; i < blk; ++i) {
       const bool real = lane_src[i] >= 0;
       const long long src = g0 + (real ? lane_src[i] : -1 - lane_src[i]), dst = (long long)c * blk + i;
@@ -721,8 +754,11 @@ static K3Tables make_k3_tables(std::vector<double> uh, long long NN, int taps, b
     }
     for (int e = 0; e < 6; ++e) box8[(size_t)kBoxInts * c + e] = box[6 * c + e];
     box8[(size_t)kBoxInts * c] = c * blk;
+    box8[(size_t)kBoxInts * c + 6] = stride;
   }
   T.box.swap(box8);
+  for (int c = 0; c < T.nchunks; ++c)  // ring slot: the largest tile image (rows x stride)
+    T.cap = std::max(T.cap, (long long)T.box[(size_t)kBoxInts * c + 3] * strides[c]);
   if (c64) {
     T.offf.resize(T.off.size());
 #pragma omp parallel for schedule(static)

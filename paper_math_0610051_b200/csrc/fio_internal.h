@@ -136,7 +136,8 @@ struct InterpWedge {
   const void* alpha;        // alpha'[t][slot] (k3_slot layout), plan dtype
   int nchunks;              // chunks of K3 BLOCK consecutive groups
   int tile_cap;             // max rows*cols of a chunk's window footprint (elements)
-  const int* box;           // kBoxInts per chunk: first group, row origin, column origin, rows, columns, groups
+  const int* box;           // kBoxInts per chunk: first group, row origin, column origin, rows, columns, groups,
+                            // shared-memory row stride of the tile (>= columns), 0
 };
 
 // Work item of the batched FFT passes: one CTA processes `count` sequences of

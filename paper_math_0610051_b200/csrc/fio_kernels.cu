@@ -1126,6 +1126,7 @@ __global__ void __launch_bounds__(K3Cfg<T2>::BLOCK, K3Cfg<T2>::minb(TAPS))
     __syncthreads();  // this chunk's tables are visible; every thread is done with the previous chunk
     const int* cb = sbox + kBoxInts * buf;  // first group, row origin, column origin, rows, columns, groups
     const int br = cb[1], bc = cb[2], bnr = cb[3], bnc = cb[4];
+    const int sst = cb[6];      // row stride of the tile in shared memory (>= bnc, chosen at plan time)
     const int cpr = bnc / EPC;  // 16-byte units per tile row
     const int tchunks = bnr * cpr;
     const T2* __restrict__ al = alpha + (long long)ch * BLOCK * P;
@@ -1143,7 +1144,7 @@ __global__ void __launch_bounds__(K3Cfg<T2>::BLOCK, K3Cfg<T2>::minb(TAPS))
         int r = br + rr;
         r = r < 0 ? r + nrow : (r >= nrow ? r - nrow : r);
         csrc[u] = r * n2p + bc + cc * EPC;
-        cdst[u] = rr * bnc + cc * EPC;
+        cdst[u] = rr * sst + cc * EPC;
         ncp = u + 1;
       }
     }
@@ -1184,7 +1185,7 @@ __global__ void __launch_bounds__(K3Cfg<T2>::BLOCK, K3Cfg<T2>::minb(TAPS))
     for (int u = 0; u < TT; ++u) issue(u, false);
     // weights of this thread's points: phi2 (columns) in registers, phi1 (rows) in shared memory
     const int2 an = m_anchor[tid];
-    const int woff = (an.x - br) * bnc + (an.y - bc);
+    const int woff = (an.x - br) * sst + (an.y - bc);
     Rt p2[P][WIN];
     {
       Rt o1[P], o2[P];
@@ -1253,7 +1254,7 @@ __global__ void __launch_bounds__(K3Cfg<T2>::BLOCK, K3Cfg<T2>::minb(TAPS))
           if (TT > 1 && t0 + u >= q) continue;  // uniform: the last step may be partial
           T2 v[WIN];
           if constexpr (C64 && WIN % 2 == 0) {  // complex64: even anchors -> 16-byte aligned pairs
-            const float4* wp = reinterpret_cast<const float4*>(win[u] + i * bnc);
+            const float4* wp = reinterpret_cast<const float4*>(win[u] + i * sst);
 #pragma unroll
             for (int jj = 0; jj < WIN / 2; ++jj) {
               const float4 a = wp[jj];
@@ -1262,7 +1263,7 @@ __global__ void __launch_bounds__(K3Cfg<T2>::BLOCK, K3Cfg<T2>::minb(TAPS))
             }
           } else {
 #pragma unroll
-            for (int jj = 0; jj < WIN; ++jj) v[jj] = win[u][i * bnc + jj];
+            for (int jj = 0; jj < WIN; ++jj) v[jj] = win[u][i * sst + jj];
           }
 #pragma unroll
           for (int k = 0; k < P; ++k) {
