@@ -968,7 +968,10 @@ template <> struct K3Cfg<float2> {
   // holds two steps (the one computed and the one in flight)
   // 10 CTAs per SM (102 registers) measured 5 % faster than 8 at N = 1024 for w <= 8 (the c64 range
   // the eps floor allows); wider windows take 8 or 6, which they need to stay free of spills
-  static constexpr int BLOCK = kK3BlockC64, TT = FIO_K3_TT64, STAGES = 2 * TT;
+#ifndef FIO_K3_ST64
+#define FIO_K3_ST64 (2 * FIO_K3_TT64)
+#endif
+  static constexpr int BLOCK = kK3BlockC64, TT = FIO_K3_TT64, STAGES = FIO_K3_ST64;
   static constexpr int minb(int taps) { return taps <= 8 ? FIO_K3_MINB64 : (taps <= 10 ? 8 : 6); }
   static_assert(kK3TileCapC64 % (2 * BLOCK) == 0, "tile cap: a whole number of 16-byte units per thread");
 };
@@ -979,7 +982,10 @@ template <> struct K3Cfg<double2> {
 #ifndef FIO_K3_TT128
 #define FIO_K3_TT128 1
 #endif
-  static constexpr int BLOCK = kK3BlockC128, TT = FIO_K3_TT128, STAGES = 2 * TT;
+#ifndef FIO_K3_ST128
+#define FIO_K3_ST128 (2 * FIO_K3_TT128)
+#endif
+  static constexpr int BLOCK = kK3BlockC128, TT = FIO_K3_TT128, STAGES = FIO_K3_ST128;
   static constexpr int minb(int) { return FIO_K3_MINB128; }
   static_assert(kK3TileCapC128 % BLOCK == 0, "tile cap: a whole number of 16-byte units per thread");
 };
@@ -1076,6 +1082,8 @@ __global__ void __launch_bounds__(K3Cfg<T2>::BLOCK, K3Cfg<T2>::minb(TAPS))
   constexpr int BLOCK = K3Cfg<T2>::BLOCK;
   constexpr int S = K3Cfg<T2>::STAGES;
   constexpr int TT = K3Cfg<T2>::TT;
+  constexpr int LA = S - TT;  // terms staged ahead of the step being computed
+  static_assert(LA >= TT, "K3 ring: at least one step in flight");
   constexpr int EPC = 16 / (int)sizeof(T2);  // complex elements per 16-byte unit
   constexpr int RPV = 16 / (int)sizeof(Rt);  // row weights per 16-byte unit
   constexpr int MAXC = C64 ? kK3TileCapC64 / 2 / BLOCK : kK3TileCapC128 / BLOCK;  // tile units per thread
@@ -1182,7 +1190,7 @@ __global__ void __launch_bounds__(K3Cfg<T2>::BLOCK, K3Cfg<T2>::minb(TAPS))
       cp_async_commit();
     };
 #pragma unroll
-    for (int u = 0; u < TT; ++u) issue(u, false);
+    for (int u = 0; u < LA; ++u) issue(u, false);
     // weights of this thread's points: phi2 (columns) in registers, phi1 (rows) in shared memory
     const int2 an = m_anchor[tid];
     const int woff = (an.x - br) * sst + (an.y - bc);
@@ -1221,13 +1229,13 @@ __global__ void __launch_bounds__(K3Cfg<T2>::BLOCK, K3Cfg<T2>::minb(TAPS))
     for (int k = 0; k < P; ++k) acc[k] = mk<T2>(0, 0);
     for (int t0 = 0; t0 < q; t0 += TT) {
       // step: terms t0 .. t0 + TT - 1 (those < q); their tiles are the only copies in flight
-      cp_async_wait<0>();
+      cp_async_wait<LA - TT>();  // this step's tiles (the newer LA - TT terms may stay in flight)
 #pragma unroll
       for (int u = 0; u < TT; ++u)
         if (t0 + u < q) mbar_wait(bar_a + (gterm + t0 + u) % S, (unsigned)((gterm + t0 + u) / S) & 1u);
       __syncthreads();  // this step staged by every thread; every thread is done with the previous step
 #pragma unroll
-      for (int u = 0; u < TT; ++u) issue(t0 + TT + u, t0 == 0 && u == 0);
+      for (int u = 0; u < TT; ++u) issue(t0 + LA + u, t0 == 0 && u == 0);
       const T2* __restrict__ win[TT];
 #pragma unroll
       for (int u = 0; u < TT; ++u) win[u] = tring + (int)((gterm + t0 + u) % S) * cap + woff;
