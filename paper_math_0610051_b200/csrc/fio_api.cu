@@ -624,7 +624,7 @@ struct K3Tables {
   long long cap = 0, real_groups = 0;
   int nchunks = 0;
 };
-// Bank-conflict-aware lane order inside one K3 chunk.  K3 reads every window row with 16-byte shared
+// Bank-conflict-aware lane order inside one warp's share of a K3 chunk (blk lanes).  K3 reads every window row with 16-byte shared
 // loads at (16-byte unit) offset u_g + const, u_g = ((a1 - r0) stride + (a2 - c0)) / epc for the group
 // g a lane holds; a quarter-warp (8 lanes) takes one wavefront per distinct u among lanes with the
 // same u mod 8 (equal u, i.e. the same anchor, is a broadcast).  Place the n groups on the blk lanes so
@@ -729,8 +729,18 @@ static K3Tables make_k3_tables(std::vector<double> uh, long long NN, int taps, b
     int stride = cols;
     for (int st = cols; st <= cols + 7 * epc; st += epc) {
       if (st > cols && (long long)rows * st > cap_c) break;
-      const long long ex = chunk_lane_order(&anchor[2 * g0], (int)n, blk, box[6 * c + 1], box[6 * c + 2], st, epc,
-                                            trial.data());
+      // per warp: the lane order only permutes a warp's own groups, so every warp still covers the
+      // same (serpentine-contiguous) groups -- the adjoint's spread keeps its atomics' locality
+      long long ex = 0;
+      for (int w0 = 0; w0 < blk; w0 += 32) {
+        const int nw = (int)std::max<long long>(0, std::min<long long>(32, n - w0));
+        if (nw == 0) {
+          for (int i = 0; i < 32; ++i) trial[w0 + i] = -1;  // all padding: group 0's anchor
+          continue;
+        }
+        ex += chunk_lane_order(&anchor[2 * (g0 + w0)], nw, 32, box[6 * c + 1], box[6 * c + 2], st, epc, &trial[w0]);
+        for (int i = 0; i < 32; ++i) trial[w0 + i] += trial[w0 + i] >= 0 ? w0 : -w0;
+      }
       if (ex < best) {
         best = ex;
         stride = st;
