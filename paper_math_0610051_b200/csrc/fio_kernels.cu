@@ -971,7 +971,10 @@ template <> struct K3Cfg<float2> {
 #ifndef FIO_K3_ST64
 #define FIO_K3_ST64 (2 * FIO_K3_TT64)
 #endif
-  static constexpr int BLOCK = kK3BlockC64, TT = FIO_K3_TT64, STAGES = FIO_K3_ST64;
+#ifndef FIO_K3_RP64
+#define FIO_K3_RP64 2
+#endif
+  static constexpr int BLOCK = kK3BlockC64, TT = FIO_K3_TT64, STAGES = FIO_K3_ST64, RP = FIO_K3_RP64;
   static constexpr int minb(int taps) { return taps <= 8 ? FIO_K3_MINB64 : (taps <= 10 ? 8 : 6); }
   static_assert(kK3TileCapC64 % (2 * BLOCK) == 0, "tile cap: a whole number of 16-byte units per thread");
 };
@@ -985,7 +988,10 @@ template <> struct K3Cfg<double2> {
 #ifndef FIO_K3_ST128
 #define FIO_K3_ST128 (2 * FIO_K3_TT128)
 #endif
-  static constexpr int BLOCK = kK3BlockC128, TT = FIO_K3_TT128, STAGES = FIO_K3_ST128;
+#ifndef FIO_K3_RP128
+#define FIO_K3_RP128 2
+#endif
+  static constexpr int BLOCK = kK3BlockC128, TT = FIO_K3_TT128, STAGES = FIO_K3_ST128, RP = FIO_K3_RP128;
   static constexpr int minb(int) { return FIO_K3_MINB128; }
   static_assert(kK3TileCapC128 % BLOCK == 0, "tile cap: a whole number of 16-byte units per thread");
 };
@@ -1082,6 +1088,7 @@ __global__ void __launch_bounds__(K3Cfg<T2>::BLOCK, K3Cfg<T2>::minb(TAPS))
   constexpr int BLOCK = K3Cfg<T2>::BLOCK;
   constexpr int S = K3Cfg<T2>::STAGES;
   constexpr int TT = K3Cfg<T2>::TT;
+  constexpr int RP = K3Cfg<T2>::RP;
   constexpr int LA = S - TT;  // terms staged ahead of the step being computed
   static_assert(LA >= TT, "K3 ring: at least one step in flight");
   constexpr int EPC = 16 / (int)sizeof(T2);  // complex elements per 16-byte unit
@@ -1245,40 +1252,60 @@ __global__ void __launch_bounds__(K3Cfg<T2>::BLOCK, K3Cfg<T2>::minb(TAPS))
 #pragma unroll
         for (int k = 0; k < P; ++k) F[u][k] = mk<T2>(0, 0);
 #pragma unroll
-      for (int i = 0; i < WINR; ++i) {
-        Rt w1[P];
+      // RP window rows per iteration: RP independent column sums per point in flight (latency hiding;
+      // the same operations in the same order, so the results do not depend on RP)
 #pragma unroll
-        for (int cc = 0; cc < P / RPV; ++cc) {
-          if constexpr (sizeof(Rt) == 4) {
-            const float4 a = *reinterpret_cast<const float4*>(p1s + ((i * (P / RPV) + cc) * BLOCK + tid) * 16);
-            w1[4 * cc] = a.x; w1[4 * cc + 1] = a.y; w1[4 * cc + 2] = a.z; w1[4 * cc + 3] = a.w;
-          } else {
-            const double2 a = *reinterpret_cast<const double2*>(p1s + ((i * (P / RPV) + cc) * BLOCK + tid) * 16);
-            w1[2 * cc] = a.x; w1[2 * cc + 1] = a.y;
+      for (int i0 = 0; i0 < WINR; i0 += RP) {
+        Rt w1[RP][P];
+#pragma unroll
+        for (int r = 0; r < RP; ++r) {
+          if (i0 + r >= WINR) continue;
+          const int i = i0 + r;
+#pragma unroll
+          for (int cc = 0; cc < P / RPV; ++cc) {
+            if constexpr (sizeof(Rt) == 4) {
+              const float4 a = *reinterpret_cast<const float4*>(p1s + ((i * (P / RPV) + cc) * BLOCK + tid) * 16);
+              w1[r][4 * cc] = a.x; w1[r][4 * cc + 1] = a.y; w1[r][4 * cc + 2] = a.z; w1[r][4 * cc + 3] = a.w;
+            } else {
+              const double2 a = *reinterpret_cast<const double2*>(p1s + ((i * (P / RPV) + cc) * BLOCK + tid) * 16);
+              w1[r][2 * cc] = a.x; w1[r][2 * cc + 1] = a.y;
+            }
           }
         }
 #pragma unroll
         for (int u = 0; u < TT; ++u) {
           if (TT > 1 && t0 + u >= q) continue;  // uniform: the last step may be partial
-          T2 v[WIN];
-          if constexpr (C64 && WIN % 2 == 0) {  // complex64: even anchors -> 16-byte aligned pairs
-            const float4* wp = reinterpret_cast<const float4*>(win[u] + i * sst);
+          T2 v[RP][WIN];
 #pragma unroll
-            for (int jj = 0; jj < WIN / 2; ++jj) {
-              const float4 a = wp[jj];
-              v[2 * jj] = mk<T2>(a.x, a.y);
-              v[2 * jj + 1] = mk<T2>(a.z, a.w);
+          for (int r = 0; r < RP; ++r) {
+            if (i0 + r >= WINR) continue;
+            const int i = i0 + r;
+            if constexpr (C64 && WIN % 2 == 0) {  // complex64: even anchors -> 16-byte aligned pairs
+              const float4* wp = reinterpret_cast<const float4*>(win[u] + i * sst);
+#pragma unroll
+              for (int jj = 0; jj < WIN / 2; ++jj) {
+                const float4 a = wp[jj];
+                v[r][2 * jj] = mk<T2>(a.x, a.y);
+                v[r][2 * jj + 1] = mk<T2>(a.z, a.w);
+              }
+            } else {
+#pragma unroll
+              for (int jj = 0; jj < WIN; ++jj) v[r][jj] = win[u][i * sst + jj];
             }
-          } else {
-#pragma unroll
-            for (int jj = 0; jj < WIN; ++jj) v[jj] = win[u][i * sst + jj];
           }
 #pragma unroll
           for (int k = 0; k < P; ++k) {
-            T2 rr = mk<T2>(0, 0);
+            T2 rr[RP];
 #pragma unroll
-            for (int jj = 0; jj < WIN; ++jj) rr = cfma_real(p2[k][jj], v[jj], rr);
-            F[u][k] = cfma_real(w1[k], rr, F[u][k]);
+            for (int r = 0; r < RP; ++r) rr[r] = mk<T2>(0, 0);
+#pragma unroll
+            for (int jj = 0; jj < WIN; ++jj)
+#pragma unroll
+              for (int r = 0; r < RP; ++r)
+                if (i0 + r < WINR) rr[r] = cfma_real(p2[k][jj], v[r][jj], rr[r]);
+#pragma unroll
+            for (int r = 0; r < RP; ++r)
+              if (i0 + r < WINR) F[u][k] = cfma_real(w1[r][k], rr[r], F[u][k]);
           }
         }
       }
