@@ -1287,6 +1287,7 @@ ApplyArgs make_args(const fio_plan_s& P) {
   a.side[0] = P.side;
   a.join[0] = P.ev_join;
   a.fork = P.ev_fork;
+  a.k3_rhs = std::getenv("FIO_K3_RHS") ? std::max(1, std::atoi(std::getenv("FIO_K3_RHS"))) : 2;
   a.p1 = P.p1;
   a.g = P.g;
   a.jobs_row = P.jobs_row;

@@ -1008,8 +1008,8 @@ template <> struct K3Cfg<double2> {
 //   anchors       [BLOCK] int2              (next chunk)
 //   boxes         [2][kBoxInts] int         footprint box of the current and the next chunk
 //   tile ring     [S][cap] T2               the chunk's footprint tile of G_lt per term in flight
-template <typename T2, int TAPS, int P>
-struct K3Layout {
+template <typename T2, int TAPS, int P, int NR = 1>
+struct K3Layout {  // NR right-hand sides: NR running-sum buffers, NR tiles per ring stage
   using Rt = typename Real<T2>::type;
   static constexpr int BLOCK = K3Cfg<T2>::BLOCK;
   static constexpr int WINR = k3_window_rows(TAPS, sizeof(T2) == 8);
@@ -1017,13 +1017,13 @@ struct K3Layout {
   static constexpr size_t kRing = 0;
   static constexpr size_t kP1 = kRing + al(sizeof(T2) * K3Cfg<T2>::STAGES * BLOCK * P);
   static constexpr size_t kLf = kP1 + al(sizeof(Rt) * WINR * BLOCK * P);
-  static constexpr size_t kSlot = kLf + al(sizeof(T2) * BLOCK * P);
+  static constexpr size_t kSlot = kLf + al(sizeof(T2) * BLOCK * P * NR);
   static constexpr size_t kOff = kSlot + al(sizeof(int) * 2 * BLOCK * P);
   static constexpr size_t kAnchor = kOff + al(sizeof(typename OffT<T2>::type) * BLOCK * P);
   static constexpr size_t kBox = kAnchor + al(sizeof(int2) * BLOCK);
   static constexpr size_t kBar = kBox + al(sizeof(int) * 2 * kBoxInts);
   static constexpr size_t kFixed = kBar + al(8 * (K3Cfg<T2>::STAGES + 2));
-  static size_t bytes(long long cap) { return kFixed + sizeof(T2) * K3Cfg<T2>::STAGES * (size_t)cap; }
+  static size_t bytes(long long cap) { return kFixed + sizeof(T2) * K3Cfg<T2>::STAGES * NR * (size_t)cap; }
 };
 
 // ---- the TMA engine (cp.async.bulk) for K3's contiguous alpha' blocks, completing on mbarriers
@@ -1060,6 +1060,16 @@ __device__ __forceinline__ void cta_copy16(void* dst, const void* src, int bytes
   for (int u = threadIdx.x; u < bytes / 16; u += BLOCK) cp_async16(d + 16 * u, s + 16 * u);
 }
 
+// The right-hand sides one K3 launch serves (NEXT-2: one alpha' pass for NR inputs): per RHS its fine
+// grids, its spectrum (DC term) and its output / running sum.
+constexpr int kK3MaxRhs = 2;
+template <typename T2>
+struct K3Rhs {
+  const T2* g[kK3MaxRhs];
+  const T2* fhat[kK3MaxRhs];
+  T2* Lf[kK3MaxRhs];
+};
+
 // K3: one CTA processes chunks of BLOCK consecutive groups (one group of up to P points per thread;
 // chunks are padded to BLOCK groups at plan time, so chunk c's groups are [c BLOCK, (c+1) BLOCK)).
 // Per chunk every thread evaluates the interpolation weights of its points once -- column weights
@@ -1074,14 +1084,18 @@ __device__ __forceinline__ void cta_copy16(void* dst, const void* src, int bytes
 // The next chunk's tables (anchors, box, slots, offsets) are prefetched during the current one.
 // Lf[x_k] is written (first wedge of the stream, + the DC term of rank 0) or read-modify-written:
 // each point occurs in exactly one group per wedge, so one launch per wedge is race-free and the
-// summation order over wedges is fixed (deterministic).
-template <typename T2, int TAPS, int P>
-__global__ void __launch_bounds__(K3Cfg<T2>::BLOCK, K3Cfg<T2>::minb(TAPS))
-    k_interp_groups(InterpWedge iw, const T2* __restrict__ gbase, const double2* __restrict__ a0,
-                    const T2* __restrict__ fhat, int first, int add_dc, EsPoly poly, T2* __restrict__ Lf) {
+// summation order over wedges is fixed (deterministic).  With NR > 1 right-hand sides (fio_apply_batch)
+// the weights, tables and alpha'(t) blocks of a chunk serve all of them: per term the CTA stages NR
+// tiles and every RHS runs the same arithmetic as a single apply (bit-identical results).
+template <typename T2, int TAPS, int P, int NR>
+__global__ void __launch_bounds__(K3Cfg<T2>::BLOCK, NR == 1 ? K3Cfg<T2>::minb(TAPS)
+                                                          : K3Cfg<T2>::minb(TAPS) - (sizeof(T2) == 8 ? 2 : 1))
+    k_interp_groups(InterpWedge iw, K3Rhs<T2> rhs, const double2* __restrict__ a0, int first, int add_dc,
+                    EsPoly poly) {
+  static_assert(NR >= 1 && NR <= kK3MaxRhs, "K3 right-hand sides");
   using Rt = typename Real<T2>::type;
   using O2 = typename OffT<T2>::type;
-  using L = K3Layout<T2, TAPS, P>;
+  using L = K3Layout<T2, TAPS, P, NR>;
   constexpr bool C64 = sizeof(T2) == 8;
   constexpr int WIN = k3_window_cols(TAPS, C64);
   constexpr int WINR = k3_window_rows(TAPS, C64);
@@ -1110,7 +1124,9 @@ __global__ void __launch_bounds__(K3Cfg<T2>::BLOCK, K3Cfg<T2>::minb(TAPS))
   const int nrow = iw.nrow, n2p = iw.ncolp, q = iw.q;  // K3 rows / haloed row length of G_lt
   const long long gstride = (long long)nrow * n2p;
   const long long nslots = (long long)iw.ngroups * P;
-  const T2* __restrict__ G = gbase + iw.g_off + kHalo;
+  const T2* G[NR];
+#pragma unroll
+  for (int r = 0; r < NR; ++r) G[r] = rhs.g[r] + iw.g_off + kHalo;
   const T2* __restrict__ alpha = reinterpret_cast<const T2*>(iw.alpha);
   const O2* __restrict__ offs = reinterpret_cast<const O2*>(iw.slot_off);
   constexpr int kA = sizeof(int2) * BLOCK, kB = sizeof(int) * kBoxInts, kS = sizeof(int) * BLOCK * P,
@@ -1169,10 +1185,13 @@ __global__ void __launch_bounds__(K3Cfg<T2>::BLOCK, K3Cfg<T2>::minb(TAPS))
       for (int k = 0; k < P; ++k) {
         const int x = m_slot[(buf * P + k) * BLOCK + tid];
         if (x >= 0) {
-          if constexpr (C64)
-            cp_async8(lfb + k * BLOCK + tid, Lf + x);
-          else
-            cp_async16(lfb + k * BLOCK + tid, Lf + x);
+#pragma unroll
+          for (int r = 0; r < NR; ++r) {
+            if constexpr (C64)
+              cp_async8(lfb + (r * P + k) * BLOCK + tid, rhs.Lf[r] + x);
+            else
+              cp_async16(lfb + (r * P + k) * BLOCK + tid, rhs.Lf[r] + x);
+          }
         }
       }
     }
@@ -1186,11 +1205,14 @@ __global__ void __launch_bounds__(K3Cfg<T2>::BLOCK, K3Cfg<T2>::minb(TAPS))
           mbar_expect_tx(bar_a + st, (unsigned)kAl);
           bulk_g2s(aring + st * BLOCK * P, al + t * nslots, (unsigned)kAl, bar_a + st);
         }
-        const T2* __restrict__ gt = G + t * gstride;
-        T2* tile = tring + st * cap;
 #pragma unroll
-        for (int u = 0; u < MAXC; ++u)
-          if (u < ncp) cp_async16(tile + cdst[u], gt + csrc[u]);
+        for (int r = 0; r < NR; ++r) {
+          const T2* __restrict__ gt = G[r] + t * gstride;
+          T2* tile = tring + (st * NR + r) * cap;
+#pragma unroll
+          for (int u = 0; u < MAXC; ++u)
+            if (u < ncp) cp_async16(tile + cdst[u], gt + csrc[u]);
+        }
       }
       // the next chunk's tables, issued once every thread has consumed the current offsets/anchors
       if (next_meta) prefetch_meta(ch + gridDim.x, buf ^ 1);
@@ -1231,9 +1253,11 @@ __global__ void __launch_bounds__(K3Cfg<T2>::BLOCK, K3Cfg<T2>::minb(TAPS))
       __syncthreads();
       prefetch_meta(ch + gridDim.x, buf ^ 1);
     }
-    T2 acc[P];
+    T2 acc[NR][P];
 #pragma unroll
-    for (int k = 0; k < P; ++k) acc[k] = mk<T2>(0, 0);
+    for (int r = 0; r < NR; ++r)
+#pragma unroll
+      for (int k = 0; k < P; ++k) acc[r][k] = mk<T2>(0, 0);
     for (int t0 = 0; t0 < q; t0 += TT) {
       // step: terms t0 .. t0 + TT - 1 (those < q); their tiles are the only copies in flight
       cp_async_wait<LA - TT>();  // this step's tiles (the newer LA - TT terms may stay in flight)
@@ -1243,9 +1267,11 @@ __global__ void __launch_bounds__(K3Cfg<T2>::BLOCK, K3Cfg<T2>::minb(TAPS))
       __syncthreads();  // this step staged by every thread; every thread is done with the previous step
 #pragma unroll
       for (int u = 0; u < TT; ++u) issue(t0 + LA + u, t0 == 0 && u == 0);
+#pragma unroll
+      for (int rh = 0; rh < NR; ++rh) {  // right-hand side rh: its tiles, the shared weights and alpha'
       const T2* __restrict__ win[TT];
 #pragma unroll
-      for (int u = 0; u < TT; ++u) win[u] = tring + (int)((gterm + t0 + u) % S) * cap + woff;
+      for (int u = 0; u < TT; ++u) win[u] = tring + ((int)((gterm + t0 + u) % S) * NR + rh) * cap + woff;
       T2 F[TT][P];
 #pragma unroll
       for (int u = 0; u < TT; ++u)
@@ -1316,27 +1342,31 @@ __global__ void __launch_bounds__(K3Cfg<T2>::BLOCK, K3Cfg<T2>::minb(TAPS))
 #pragma unroll
         for (int k = 0; k < P; ++k) {
           const T2 av = ring[k * BLOCK];
-          acc[k].x = fma(av.x, F[u][k].x, fma(-av.y, F[u][k].y, acc[k].x));
-          acc[k].y = fma(av.x, F[u][k].y, fma(av.y, F[u][k].x, acc[k].y));
+          acc[rh][k].x = fma(av.x, F[u][k].x, fma(-av.y, F[u][k].y, acc[rh][k].x));
+          acc[rh][k].y = fma(av.x, F[u][k].y, fma(av.y, F[u][k].x, acc[rh][k].y));
         }
       }
+      }  // right-hand sides
     }
     gterm += q;
     cp_async_wait<0>();  // the running sums (in the first copy group) have landed
-    T2 f0 = mk<T2>(0, 0);
-    if (first && add_dc) f0 = fhat[0];
 #pragma unroll
-    for (int k = 0; k < P; ++k) {
-      const int x = m_slot[(buf * P + k) * BLOCK + tid];
-      if (x < 0) continue;
-      T2 b0 = mk<T2>(0, 0);
-      if (!first) {
-        b0 = lfb[k * BLOCK + tid];
-      } else if (add_dc) {
-        const double2 d = a0[x];
-        b0 = mk<T2>((Rt)(d.x * (double)f0.x - d.y * (double)f0.y), (Rt)(d.x * (double)f0.y + d.y * (double)f0.x));
+    for (int rh = 0; rh < NR; ++rh) {
+      T2 f0 = mk<T2>(0, 0);
+      if (first && add_dc) f0 = rhs.fhat[rh][0];
+#pragma unroll
+      for (int k = 0; k < P; ++k) {
+        const int x = m_slot[(buf * P + k) * BLOCK + tid];
+        if (x < 0) continue;
+        T2 b0 = mk<T2>(0, 0);
+        if (!first) {
+          b0 = lfb[(rh * P + k) * BLOCK + tid];
+        } else if (add_dc) {
+          const double2 d = a0[x];
+          b0 = mk<T2>((Rt)(d.x * (double)f0.x - d.y * (double)f0.y), (Rt)(d.x * (double)f0.y + d.y * (double)f0.x));
+        }
+        rhs.Lf[rh][x] = mk<T2>(b0.x + acc[rh][k].x, b0.y + acc[rh][k].y);
       }
-      Lf[x] = mk<T2>(b0.x + acc[k].x, b0.y + acc[k].y);
     }
   }
 }
@@ -1381,25 +1411,33 @@ __global__ void k_accum(T2* __restrict__ Lf, const T2* __restrict__ a0, const T2
   }
 }
 
-template <typename T2, int TAPS, int P>
-static cudaError_t launch_groups_tp(const ApplyArgs& a, const InterpWedge& iw, const T2* g, const T2* fhat, T2* Lf,
-                                    int first, int add_dc, cudaStream_t s) {
+template <typename T2, int TAPS, int P, int NR>
+static cudaError_t launch_groups_tpr(const ApplyArgs& a, const InterpWedge& iw, const K3Rhs<T2>& rhs, int first,
+                                     int add_dc, cudaStream_t s) {
   constexpr int BLOCK = K3Cfg<T2>::BLOCK;
   // the plan opted this instance into its largest footprint's smem on its device (configure_interp)
-  const size_t smem = K3Layout<T2, TAPS, P>::bytes(iw.tile_cap);
+  const size_t smem = K3Layout<T2, TAPS, P, NR>::bytes(iw.tile_cap);
   int per_sm = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_interp_groups<T2, TAPS, P>, BLOCK, smem);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_interp_groups<T2, TAPS, P, NR>, BLOCK, smem);
   per_sm = std::max(per_sm, 1);
   const int blocks = std::max(1, std::min(iw.nchunks, per_sm * a.sms));
-  k_interp_groups<T2, TAPS, P><<<blocks, BLOCK, smem, s>>>(iw, g, a.a0, fhat, first, add_dc, *a.poly, Lf);
+  k_interp_groups<T2, TAPS, P, NR><<<blocks, BLOCK, smem, s>>>(iw, rhs, a.a0, first, add_dc, *a.poly);
   return cudaGetLastError();
+}
+
+template <typename T2, int TAPS, int P>
+static cudaError_t launch_groups_tp(const ApplyArgs& a, const InterpWedge& iw, const K3Rhs<T2>& rhs, int nr,
+                                    int first, int add_dc, cudaStream_t s) {
+  return nr == 2 ? launch_groups_tpr<T2, TAPS, P, 2>(a, iw, rhs, first, add_dc, s)
+                 : launch_groups_tpr<T2, TAPS, P, 1>(a, iw, rhs, first, add_dc, s);
 }
 
 template <typename T2, int TAPS>
 static cudaError_t configure_interp_tp(long long tile_cap) {
   constexpr int P = GroupP<T2, TAPS>::value;
-  const size_t smem = K3Layout<T2, TAPS, P>::bytes(tile_cap);
-  return raise_smem_attr((const void*)k_interp_groups<T2, TAPS, P>, smem);
+  cudaError_t e = raise_smem_attr((const void*)k_interp_groups<T2, TAPS, P, 1>, K3Layout<T2, TAPS, P, 1>::bytes(tile_cap));
+  if (e != cudaSuccess) return e;
+  return raise_smem_attr((const void*)k_interp_groups<T2, TAPS, P, 2>, K3Layout<T2, TAPS, P, 2>::bytes(tile_cap));
 }
 
 cudaError_t configure_interp(int taps, bool c64, long long max_tile_cap) {
@@ -1423,11 +1461,11 @@ cudaError_t configure_interp(int taps, bool c64, long long max_tile_cap) {
 }
 
 template <typename T2>
-static cudaError_t launch_groups(const ApplyArgs& a, const InterpWedge& iw, const T2* g, const T2* fhat, T2* Lf,
-                                 int first, int add_dc, cudaStream_t s) {
+static cudaError_t launch_groups(const ApplyArgs& a, const InterpWedge& iw, const K3Rhs<T2>& rhs, int nr, int first,
+                                 int add_dc, cudaStream_t s) {
 #define FIO_GROUPS_CASE(TP) \
   case TP:                  \
-    return launch_groups_tp<T2, TP, GroupP<T2, TP>::value>(a, iw, g, fhat, Lf, first, add_dc, s);
+    return launch_groups_tp<T2, TP, GroupP<T2, TP>::value>(a, iw, rhs, nr, first, add_dc, s);
   switch (a.taps) {
     FIO_GROUPS_CASE(3)
     FIO_GROUPS_CASE(4)
@@ -1478,13 +1516,20 @@ static cudaError_t launch_interp(const ApplyArgs* args, int nrhs, T2* Lf0, cudaS
       if (e != cudaSuccess) return e;
       ++*n;
     }
-    for (int b = 0; b < nrhs; ++b) {
-      T2* acc = sj ? reinterpret_cast<T2*>(args[b].acc[0]) : Lf0 + b * NN;
-      if ((e = launch_groups<T2>(a, iw, reinterpret_cast<const T2*>(args[b].g),
-                                 reinterpret_cast<const T2*>(args[b].fhat), acc, wi < ns,
-                                 (wi == 0 && a.add_dc) ? 1 : 0, sw)) != cudaSuccess)
+    // up to k3_rhs right-hand sides per launch: one pass over the wedge's alpha' serves them all
+    for (int b = 0; b < nrhs;) {
+      // (w > 7 would spill with two right-hand sides' accumulators: one at a time there)
+      const int nr = a.taps > 7 ? 1 : std::max(1, std::min({a.k3_rhs, kK3MaxRhs, nrhs - b}));
+      K3Rhs<T2> rhs{};
+      for (int r = 0; r < nr; ++r) {
+        rhs.g[r] = reinterpret_cast<const T2*>(args[b + r].g);
+        rhs.fhat[r] = reinterpret_cast<const T2*>(args[b + r].fhat);
+        rhs.Lf[r] = sj ? reinterpret_cast<T2*>(args[b + r].acc[0]) : Lf0 + (b + r) * NN;
+      }
+      if ((e = launch_groups<T2>(a, iw, rhs, nr, wi < ns, (wi == 0 && a.add_dc) ? 1 : 0, sw)) != cudaSuccess)
         return e;
       ++*n;
+      b += nr;
     }
   }
   if (ns > 1) {

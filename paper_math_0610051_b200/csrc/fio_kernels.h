@@ -104,6 +104,7 @@ struct ApplyArgs {
   int cols_per_cta_N;       // K0 column pass
   int sms;                  // multiprocessors of the plan's device (grid sizing)
   int overlap;              // smooth partition: wedges overlap, K1* accumulates fhat* atomically
+  int k3_rhs;               // fio_apply_batch: right-hand sides per K3 launch (1 or 2; FIO_K3_RHS)
 };
 
 // Enqueue the whole apply (K0 row/column FFT, K1 window x beta + row FFT,
