@@ -53,7 +53,9 @@ typedef enum {
   FIO_ENOMEM = -2,    /* device or host allocation failed */
   FIO_ECUDA = -3,     /* CUDA runtime error (launch or sync) */
   FIO_ENCCL = -4,     /* NCCL failure (libnccl.so.2 missing, communicator setup or reduce-scatter) */
-  FIO_ENOTHOMOG = -5, /* reserved: phase failed the degree-1 homogeneity check */
+  FIO_ENOTHOMOG = -5, /* reserved, never returned: the phase interface (fio_phase: the elliptic family
+                         x.xi + b(x).xi +- sqrt(c1^2 xi1^2 + c2^2 xi2^2) given by its coefficient grids) is
+                         homogeneous of degree 1 in xi by construction, so there is nothing to check */
   FIO_EINTERNAL = -6  /* internal invariant violated (a bug) */
 } fio_status;
 
