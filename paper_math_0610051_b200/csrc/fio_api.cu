@@ -1,5 +1,7 @@
 // fio_api.cu -- the C ABI (include/fio.h): plan construction (PAPER.md:981-1008,
 // 1111-1250) and the apply orchestration.
+#include <cuda.h>
+#include <cudaTypedefs.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -130,6 +132,8 @@ struct fio_plan_s {
   void* d_tw = nullptr;
   void** d_beta = nullptr;
   void *fhat = nullptr, *tmp = nullptr, *p1 = nullptr, *g = nullptr;
+  std::vector<CUtensorMap> tmaps;  // per owned wedge: TMA map of its fine grids (K3 tiles)
+  PFN_cuTensorMapEncodeTiled_v12000 encode_tmap = nullptr;  // driver entry point (null: no TMA tiles)
   FftJob *jobs_row = nullptr, *jobs_col = nullptr, *jobs_rowadj = nullptr;
   int njobs_rowadj = 0, smem_rowadj = 0;
   std::vector<void*> mask_ptrs;
@@ -715,20 +719,26 @@ static K3Tables make_k3_tables(std::vector<double> uh, long long NN, int taps, b
   T.off.assign((size_t)T.nchunks * blk * gp * 2, 0.5 * taps);
   std::vector<int> box8((size_t)T.nchunks * kBoxInts, 0);  // per chunk: first group, r0, c0, rows, cols, groups,
                                                            // shared-memory row stride, 0
-  std::vector<int> strides(T.nchunks);
+  std::vector<int> strides(T.nchunks), tmas(T.nchunks);
   const std::vector<int>& box = T.box;
 #pragma omp parallel for schedule(static)
   for (int c = 0; c < T.nchunks; ++c) {
     const long long g0 = box[6 * c], n = box[6 * c + 5];
     // the tile's shared-memory row stride: the copied width or up to 7 (16-byte units) more, the one
-    // whose best lane order leaves the fewest bank conflicts, inside the tile cap
+    // whose best lane order leaves the fewest bank conflicts, inside the tile cap -- or, for a chunk
+    // whose footprint fits the TMA box without wrapping, the box width (the TMA image is dense)
     const int epc = c64 ? 2 : 1, rows = box[6 * c + 3], cols = box[6 * c + 4];
+    const int r0 = box[6 * c + 1], c0 = box[6 * c + 2];
+    const int bxr = c64 ? kK3BoxRows64 : kK3BoxRows128, bxc = c64 ? kK3BoxCols64 : kK3BoxCols128;
+    const bool tma = FIO_K3_TMA && rows <= bxr && cols <= bxc && r0 >= 0 && r0 + rows <= n2f && c0 + kHalo >= 0 &&
+                     c0 + kHalo + bxc <= n1f + 2 * kHalo;
+    tmas[c] = tma ? 1 : 0;
     const long long cap_c = c64 ? kK3TileCapC64 : kK3TileCapC128;
     std::vector<int> lane_src(blk), trial(blk);
     long long best = LLONG_MAX;
     int stride = cols;
-    for (int st = cols; st <= cols + 7 * epc; st += epc) {
-      if (st > cols && (long long)rows * st > cap_c) break;
+    for (int st = tma ? bxc : cols; st <= (tma ? bxc : cols + 7 * epc); st += epc) {
+      if (!tma && st > cols && (long long)rows * st > cap_c) break;
       // per warp: the lane order only permutes a warp's own groups, so every warp still covers the
       // same (serpentine-contiguous) groups -- the adjoint's spread keeps its atomics' locality
       long long ex = 0;
@@ -748,7 +758,7 @@ static K3Tables make_k3_tables(std::vector<double> uh, long long NN, int taps, b
         if (ex == 0) break;
       }
     }
-    strides[c] = stride;
+    strides[c] = tma ? bxc : stride;
     for (long long i = 0; i < blk; ++i) {
       const bool real = lane_src[i] >= 0;
       const long long src = g0 + (real ? lane_src[i] : -1 - lane_src[i]), dst = (long long)c * blk + i;
@@ -764,11 +774,14 @@ static K3Tables make_k3_tables(std::vector<double> uh, long long NN, int taps, b
     }
     for (int e = 0; e < 6; ++e) box8[(size_t)kBoxInts * c + e] = box[6 * c + e];
     box8[(size_t)kBoxInts * c] = c * blk;
-    box8[(size_t)kBoxInts * c + 6] = stride;
+    box8[(size_t)kBoxInts * c + 6] = strides[c];
+    box8[(size_t)kBoxInts * c + 7] = tmas[c];
   }
   T.box.swap(box8);
-  for (int c = 0; c < T.nchunks; ++c)  // ring slot: the largest tile image (rows x stride)
-    T.cap = std::max(T.cap, (long long)T.box[(size_t)kBoxInts * c + 3] * strides[c]);
+  for (int c = 0; c < T.nchunks; ++c)  // ring slot: the largest tile image (rows x stride, or the TMA box)
+    T.cap = std::max(T.cap, tmas[c] ? (long long)(c64 ? kK3BoxRows64 * kK3BoxCols64 : kK3BoxRows128 * kK3BoxCols128)
+                                    : (long long)T.box[(size_t)kBoxInts * c + 3] * strides[c]);
+  T.cap = (T.cap + (c64 ? 15 : 7)) / (c64 ? 16 : 8) * (c64 ? 16 : 8);  // 128-byte slots (TMA destinations)
   if (c64) {
     T.offf.resize(T.off.size());
 #pragma omp parallel for schedule(static)
@@ -1259,6 +1272,33 @@ fio_status build_plan(fio_plan_s& P, const fio_phase* phase, const fio_amplitude
   FIO_CUDA(P.alloc(&P.p1, cs * std::max<size_t>(P.p1_elems, 1)));
   FIO_CUDA(P.alloc(&P.g, cs * std::max<size_t>(P.fine_elems, 1)));
   P.ws_bytes = cs * (2 * NN + P.p1_elems + P.fine_elems);
+  // one TMA tensor map per owned wedge over its fine grids G_lt: 3-D [t][row][haloed column] in 8-byte
+  // units (complex64: one element, complex128: two), box = the K3 TMA box (kK3BoxRows x kK3BoxCols)
+  if (!P.encode_tmap) {  // the driver's encoder, through the runtime (no libcuda link dependency)
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult qr{};
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &qr) == cudaSuccess &&
+        qr == cudaDriverEntryPointSuccess)
+      P.encode_tmap = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+    cudaGetLastError();
+  }
+  P.tmaps.assign(P.iw.size(), CUtensorMap{});
+  for (size_t wi = 0; wi < P.iw.size(); ++wi) {
+    InterpWedge& iw = P.iw[wi];
+    iw.tma = 0;
+    if (!FIO_K3_TMA || iw.q == 0 || !P.encode_tmap) continue;
+    const cuuint64_t U = c64 ? 1 : 2;
+    const cuuint64_t dims[3] = {U * (cuuint64_t)iw.ncolp, (cuuint64_t)iw.nrow, (cuuint64_t)iw.q};
+    const cuuint64_t strides[2] = {(cuuint64_t)iw.ncolp * cs, (cuuint64_t)iw.nrow * iw.ncolp * cs};
+    const cuuint32_t boxd[3] = {(cuuint32_t)(U * (c64 ? kK3BoxCols64 : kK3BoxCols128)),
+                                (cuuint32_t)(c64 ? kK3BoxRows64 : kK3BoxRows128), 1};
+    const cuuint32_t estr[3] = {1, 1, 1};
+    void* base = static_cast<char*>(P.g) + (size_t)iw.g_off * cs;
+    CUresult r = P.encode_tmap(&P.tmaps[wi], CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, base, dims, strides, boxd, estr,
+                               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                               CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    iw.tma = r == CUDA_SUCCESS ? 1 : 0;  // else this wedge keeps the cp.async tiles
+  }
   FIO_CUDA(cudaDeviceSynchronize());
   return FIO_OK;
 }
@@ -1287,6 +1327,7 @@ ApplyArgs make_args(const fio_plan_s& P) {
   a.side[0] = P.side;
   a.join[0] = P.ev_join;
   a.fork = P.ev_fork;
+  a.tmaps = P.tmaps.empty() ? nullptr : P.tmaps.data();
   a.k3_rhs = std::getenv("FIO_K3_RHS") ? std::max(1, std::atoi(std::getenv("FIO_K3_RHS"))) : 2;
   a.p1 = P.p1;
   a.g = P.g;

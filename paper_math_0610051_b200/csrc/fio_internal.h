@@ -137,8 +137,18 @@ struct InterpWedge {
   int nchunks;              // chunks of K3 BLOCK consecutive groups
   int tile_cap;             // max rows*cols of a chunk's window footprint (elements)
   const int* box;           // kBoxInts per chunk: first group, row origin, column origin, rows, columns, groups,
-                            // shared-memory row stride of the tile (>= columns), 0
+                            // shared-memory row stride of the tile (>= columns), 1 = tile by TMA (tensor map)
+  int tma;                  // this launch may stage tiles by TMA (the plan's tensor map of this wedge's G)
 };
+
+// K3 tiles by TMA (cp.async.bulk.tensor.3d, one request per chunk and term): the fixed box (rows x
+// columns of the fine grid) a chunk's footprint must fit, unwrapped, to use it; other chunks keep the
+// per-thread cp.async copies.  Box widths are an odd number of 16-byte units (bank-conflict-free rows).
+#ifndef FIO_K3_TMA
+#define FIO_K3_TMA 1
+#endif
+constexpr int kK3BoxRows64 = 12, kK3BoxCols64 = 22;
+constexpr int kK3BoxRows128 = 16, kK3BoxCols128 = 23;
 
 // Work item of the batched FFT passes: one CTA processes `count` sequences of
 // the (wedge, t) pair starting at row/column `start`.

@@ -15,6 +15,7 @@
 // No code here is shared with oracle/.
 #include <vector>
 #include <type_traits>
+#include <cuda.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -1022,7 +1023,9 @@ struct K3Layout {  // NR right-hand sides: NR running-sum buffers, NR tiles per 
   static constexpr size_t kAnchor = kOff + al(sizeof(typename OffT<T2>::type) * BLOCK * P);
   static constexpr size_t kBox = kAnchor + al(sizeof(int2) * BLOCK);
   static constexpr size_t kBar = kBox + al(sizeof(int) * 2 * kBoxInts);
-  static constexpr size_t kFixed = kBar + al(8 * (K3Cfg<T2>::STAGES + 2));
+  // the tile ring: 128-byte aligned (TMA destination); the plan rounds the slot size (tile_cap) to
+  // a multiple of 128 bytes
+  static constexpr size_t kFixed = (kBar + al(8 * (K3Cfg<T2>::STAGES + 2)) + 127) / 128 * 128;
   static size_t bytes(long long cap) { return kFixed + sizeof(T2) * K3Cfg<T2>::STAGES * NR * (size_t)cap; }
 };
 
@@ -1050,6 +1053,15 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned by
                    smem_u32(dst)),
                "l"(src), "r"(bytes), "r"(smem_u32(bar))
                : "memory");
+}
+// TMA tensor copy: the box at (x, y, z) of a 3-D tensor map into shared memory, completing on `bar`
+__device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, int x, int y, int z,
+                                            unsigned long long* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], "
+      "[%5];\n" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<unsigned long long>(map)), "r"(x), "r"(y), "r"(z), "r"(smem_u32(bar))
+      : "memory");
 }
 
 // `bytes` (a multiple of 16) from global to shared memory by the whole CTA, 16-byte cp.async units
@@ -1091,7 +1103,7 @@ template <typename T2, int TAPS, int P, int NR>
 __global__ void __launch_bounds__(K3Cfg<T2>::BLOCK, NR == 1 ? K3Cfg<T2>::minb(TAPS)
                                                           : K3Cfg<T2>::minb(TAPS) - (sizeof(T2) == 8 ? 2 : 1))
     k_interp_groups(InterpWedge iw, K3Rhs<T2> rhs, const double2* __restrict__ a0, int first, int add_dc,
-                    EsPoly poly) {
+                    EsPoly poly, const __grid_constant__ CUtensorMap tmap) {
   static_assert(NR >= 1 && NR <= kK3MaxRhs, "K3 right-hand sides");
   using Rt = typename Real<T2>::type;
   using O2 = typename OffT<T2>::type;
@@ -1109,7 +1121,7 @@ __global__ void __launch_bounds__(K3Cfg<T2>::BLOCK, NR == 1 ? K3Cfg<T2>::minb(TA
   constexpr int RPV = 16 / (int)sizeof(Rt);  // row weights per 16-byte unit
   constexpr int MAXC = C64 ? kK3TileCapC64 / 2 / BLOCK : kK3TileCapC128 / BLOCK;  // tile units per thread
   static_assert(P % RPV == 0, "K3 group size");
-  extern __shared__ __align__(16) unsigned char k3_smem[];
+  extern __shared__ __align__(128) unsigned char k3_smem[];
   T2* aring = reinterpret_cast<T2*>(k3_smem + L::kRing);
   unsigned char* p1s = k3_smem + L::kP1;
   T2* lfb = reinterpret_cast<T2*>(k3_smem + L::kLf);
@@ -1158,6 +1170,7 @@ __global__ void __launch_bounds__(K3Cfg<T2>::BLOCK, NR == 1 ? K3Cfg<T2>::minb(TA
     const int* cb = sbox + kBoxInts * buf;  // first group, row origin, column origin, rows, columns, groups
     const int br = cb[1], bc = cb[2], bnr = cb[3], bnc = cb[4];
     const int sst = cb[6];      // row stride of the tile in shared memory (>= bnc, chosen at plan time)
+    const bool tma = NR == 1 && iw.tma && cb[7];  // the tile by one TMA request per term (plan-time choice)
     const int cpr = bnc / EPC;  // 16-byte units per tile row
     const int tchunks = bnr * cpr;
     const T2* __restrict__ al = alpha + (long long)ch * BLOCK * P;
@@ -1201,6 +1214,14 @@ __global__ void __launch_bounds__(K3Cfg<T2>::BLOCK, NR == 1 ? K3Cfg<T2>::minb(TA
     auto issue = [&](int t, bool next_meta) {
       if (t < q) {
         const int st = (int)((gterm + t) % S);
+        if (tma) {  // alpha'(t) and the tile (the fixed TMA box at the chunk's origin) on one mbarrier
+          if (tid == 0) {
+            constexpr int kTile = (C64 ? kK3BoxRows64 * kK3BoxCols64 : kK3BoxRows128 * kK3BoxCols128) * sizeof(T2);
+            mbar_expect_tx(bar_a + st, (unsigned)(kAl + kTile));
+            bulk_g2s(aring + st * BLOCK * P, al + t * nslots, (unsigned)kAl, bar_a + st);
+            tma_load_3d(tring + st * NR * cap, &tmap, (bc + kHalo) * (int)(sizeof(T2) / 8), br, t, bar_a + st);
+          }
+        } else {
         if (tid == 0) {
           mbar_expect_tx(bar_a + st, (unsigned)kAl);
           bulk_g2s(aring + st * BLOCK * P, al + t * nslots, (unsigned)kAl, bar_a + st);
@@ -1212,6 +1233,7 @@ __global__ void __launch_bounds__(K3Cfg<T2>::BLOCK, NR == 1 ? K3Cfg<T2>::minb(TA
 #pragma unroll
           for (int u = 0; u < MAXC; ++u)
             if (u < ncp) cp_async16(tile + cdst[u], gt + csrc[u]);
+        }
         }
       }
       // the next chunk's tables, issued once every thread has consumed the current offsets/anchors
@@ -1413,7 +1435,7 @@ __global__ void k_accum(T2* __restrict__ Lf, const T2* __restrict__ a0, const T2
 
 template <typename T2, int TAPS, int P, int NR>
 static cudaError_t launch_groups_tpr(const ApplyArgs& a, const InterpWedge& iw, const K3Rhs<T2>& rhs, int first,
-                                     int add_dc, cudaStream_t s) {
+                                     int add_dc, const CUtensorMap& tmap, cudaStream_t s) {
   constexpr int BLOCK = K3Cfg<T2>::BLOCK;
   // the plan opted this instance into its largest footprint's smem on its device (configure_interp)
   const size_t smem = K3Layout<T2, TAPS, P, NR>::bytes(iw.tile_cap);
@@ -1421,15 +1443,15 @@ static cudaError_t launch_groups_tpr(const ApplyArgs& a, const InterpWedge& iw, 
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_interp_groups<T2, TAPS, P, NR>, BLOCK, smem);
   per_sm = std::max(per_sm, 1);
   const int blocks = std::max(1, std::min(iw.nchunks, per_sm * a.sms));
-  k_interp_groups<T2, TAPS, P, NR><<<blocks, BLOCK, smem, s>>>(iw, rhs, a.a0, first, add_dc, *a.poly);
+  k_interp_groups<T2, TAPS, P, NR><<<blocks, BLOCK, smem, s>>>(iw, rhs, a.a0, first, add_dc, *a.poly, tmap);
   return cudaGetLastError();
 }
 
 template <typename T2, int TAPS, int P>
 static cudaError_t launch_groups_tp(const ApplyArgs& a, const InterpWedge& iw, const K3Rhs<T2>& rhs, int nr,
-                                    int first, int add_dc, cudaStream_t s) {
-  return nr == 2 ? launch_groups_tpr<T2, TAPS, P, 2>(a, iw, rhs, first, add_dc, s)
-                 : launch_groups_tpr<T2, TAPS, P, 1>(a, iw, rhs, first, add_dc, s);
+                                    int first, int add_dc, const CUtensorMap& tmap, cudaStream_t s) {
+  return nr == 2 ? launch_groups_tpr<T2, TAPS, P, 2>(a, iw, rhs, first, add_dc, tmap, s)
+                 : launch_groups_tpr<T2, TAPS, P, 1>(a, iw, rhs, first, add_dc, tmap, s);
 }
 
 template <typename T2, int TAPS>
@@ -1462,10 +1484,10 @@ cudaError_t configure_interp(int taps, bool c64, long long max_tile_cap) {
 
 template <typename T2>
 static cudaError_t launch_groups(const ApplyArgs& a, const InterpWedge& iw, const K3Rhs<T2>& rhs, int nr, int first,
-                                 int add_dc, cudaStream_t s) {
+                                 int add_dc, const CUtensorMap& tmap, cudaStream_t s) {
 #define FIO_GROUPS_CASE(TP) \
   case TP:                  \
-    return launch_groups_tp<T2, TP, GroupP<T2, TP>::value>(a, iw, rhs, nr, first, add_dc, s);
+    return launch_groups_tp<T2, TP, GroupP<T2, TP>::value>(a, iw, rhs, nr, first, add_dc, tmap, s);
   switch (a.taps) {
     FIO_GROUPS_CASE(3)
     FIO_GROUPS_CASE(4)
@@ -1526,7 +1548,11 @@ static cudaError_t launch_interp(const ApplyArgs* args, int nrhs, T2* Lf0, cudaS
         rhs.fhat[r] = reinterpret_cast<const T2*>(args[b + r].fhat);
         rhs.Lf[r] = sj ? reinterpret_cast<T2*>(args[b + r].acc[0]) : Lf0 + (b + r) * NN;
       }
-      if ((e = launch_groups<T2>(a, iw, rhs, nr, wi < ns, (wi == 0 && a.add_dc) ? 1 : 0, sw)) != cudaSuccess)
+      // TMA tiles read the plan's own fine grids: the first right-hand side of a single apply only
+      InterpWedge iwl = iw;
+      iwl.tma = (a.tmaps && nr == 1 && rhs.g[0] == reinterpret_cast<const T2*>(a.g)) ? iw.tma : 0;
+      const CUtensorMap tm = iwl.tma ? a.tmaps[wi] : CUtensorMap{};
+      if ((e = launch_groups<T2>(a, iwl, rhs, nr, wi < ns, (wi == 0 && a.add_dc) ? 1 : 0, tm, sw)) != cudaSuccess)
         return e;
       ++*n;
       b += nr;

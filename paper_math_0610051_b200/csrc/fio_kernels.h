@@ -1,5 +1,6 @@
 // fio_kernels.h -- launchers of the sm_100a kernels (fio_kernels.cu).
 #pragma once
+#include <cuda.h>
 #include <cuda_runtime.h>
 
 #include "fio_internal.h"
@@ -105,6 +106,7 @@ struct ApplyArgs {
   int sms;                  // multiprocessors of the plan's device (grid sizing)
   int overlap;              // smooth partition: wedges overlap, K1* accumulates fhat* atomically
   int k3_rhs;               // fio_apply_batch: right-hand sides per K3 launch (1 or 2; FIO_K3_RHS)
+  const CUtensorMap* tmaps; // host array, per owned wedge: TMA map of its fine grids (iw.tma), or null
 };
 
 // Enqueue the whole apply (K0 row/column FFT, K1 window x beta + row FFT,
