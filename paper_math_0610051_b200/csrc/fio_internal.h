@@ -147,8 +147,14 @@ struct InterpWedge {
 #ifndef FIO_K3_TMA
 #define FIO_K3_TMA 1
 #endif
-constexpr int kK3BoxRows64 = 12, kK3BoxCols64 = 22;
-constexpr int kK3BoxRows128 = 16, kK3BoxCols128 = 23;
+#ifndef FIO_K3_BOXR64
+#define FIO_K3_BOXR64 12
+#endif
+#ifndef FIO_K3_BOXR128
+#define FIO_K3_BOXR128 12
+#endif
+constexpr int kK3BoxRows64 = FIO_K3_BOXR64, kK3BoxCols64 = 22;
+constexpr int kK3BoxRows128 = FIO_K3_BOXR128, kK3BoxCols128 = 23;
 
 // Work item of the batched FFT passes: one CTA processes `count` sequences of
 // the (wedge, t) pair starting at row/column `start`.
