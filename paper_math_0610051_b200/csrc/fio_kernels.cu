@@ -1183,7 +1183,7 @@ __global__ void __launch_bounds__(K3Cfg<T2>::BLOCK, NR == 1 ? K3Cfg<T2>::minb(TA
       const int idx = tid + u * BLOCK;
       csrc[u] = 0;
       cdst[u] = 0;
-      if (idx < tchunks) {
+      if (!tma && idx < tchunks) {  // (TMA chunks copy their tile without per-thread addresses)
         const int rr = idx / cpr, cc = idx - rr * cpr;
         int r = br + rr;
         r = r < 0 ? r + nrow : (r >= nrow ? r - nrow : r);
