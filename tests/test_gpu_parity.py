@@ -717,3 +717,33 @@ def test_paper_table_result_a_replay(N):
     print(f"Table tbl:result_a replay N={N}: eps {eps:.3g}, error {err:.3g} (paper {printed:.3g}), "
           f"W {plan.info['W']} sum_q {plan.info['sum_q']}")
     assert err <= 10 * eps and printed / 20 <= err <= 5 * printed, (err, printed)
+
+
+# ------------------------------------------------------------------ the NUFFT alone (K1 -> K2 -> K3) against the direct NUDFT
+@pytest.mark.parametrize("N,dtype,eps,npts", [(128, "c128", 1e-6, None), (128, "c64", 1e-4, None),
+                                              (1024, "c128", 1e-6, 2048), (1024, "c64", 1e-4, 2048)])
+def test_nufft_component_vs_direct_nudft(N, dtype, eps, npts):
+    # "The only step that requires attention" (section 3.4): the nonuniform Fourier
+    # series of evaluation step 3 at the warped points.  A phase linear in xi, Phi = (x + b(x)).xi with a
+    # real, non-integer displacement b, has a residual identically 1 (separation rank 1 in every wedge,
+    # PAPER.md:1283-1302), so the apply IS the wedge-split NUFFT: Lf(x) = (1/N) sum_xi fhat(xi)
+    # e^{2 pi i (x + b(x)).xi}, compared here with oracle.nudft2 (direct sum, pinned in
+    # test_oracle_pins.py) at arbitrary off-grid targets y = x + b(x) -- every tap of K3's window, the
+    # box maps M and the deconvolution folded into beta' are exercised without the separation.
+    n1, n2 = np.meshgrid(np.arange(N), np.arange(N), indexing="ij")
+    r = np.random.default_rng(5)
+    b1 = 0.2 * np.sin(2 * np.pi * n2 / N) + r.uniform(-2.5, 2.5, (N, N)) / N
+    b2 = 0.15 * np.cos(2 * np.pi * n1 / N) + r.uniform(-2.5, 2.5, (N, N)) / N
+    z = np.zeros((N, N))
+    op = wl.Operator(N, z, z.copy(), b1, b2, name="warp-only")
+    f = wl.white_noise(N, 13, dtype)
+    plan, out = run(op, f, eps=eps, dtype=dtype)
+    assert np.all(plan.wedges()["q"] == 1)
+    idx = np.arange(N * N) if npts is None else wl.sample_points(N, npts, seed=3)
+    p1, p2 = idx // N, idx % N
+    y = np.stack([p1 / N + b1[p1, p2], p2 / N + b2[p1, p2]], axis=1)
+    fh = np.fft.fftshift(oracle.dft2(f))   # box [-N/2, N/2)^2 in nudft2's centred layout
+    ref = oracle.nudft2(fh, y) / N
+    rel, mx = _pointwise(out.ravel()[idx], ref)
+    print(f"NUFFT component N={N} {dtype}: rel l2 {rel:.3e}, max|err|/rms {mx:.3e}, w {plan.info['nufft_w']}")
+    assert rel <= 10 * eps and mx <= 100 * eps, (rel, mx)
