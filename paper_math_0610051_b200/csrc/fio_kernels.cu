@@ -1009,6 +1009,11 @@ template <> struct K3Cfg<double2> {
 //   anchors       [BLOCK] int2              (next chunk)
 //   boxes         [2][kBoxInts] int         footprint box of the current and the next chunk
 //   tile ring     [S][cap] T2               the chunk's footprint tile of G_lt per term in flight
+// FIO_K3_OFFG: the points' fine-grid offsets are read from global memory (L2) when a chunk starts instead
+// of being prefetched into shared memory (saves BLOCK P sizeof(O2) bytes per CTA: one more CTA per SM)
+#ifndef FIO_K3_OFFG
+#define FIO_K3_OFFG 0
+#endif
 template <typename T2, int TAPS, int P, int NR = 1>
 struct K3Layout {  // NR right-hand sides: NR running-sum buffers, NR tiles per ring stage
   using Rt = typename Real<T2>::type;
@@ -1020,7 +1025,7 @@ struct K3Layout {  // NR right-hand sides: NR running-sum buffers, NR tiles per 
   static constexpr size_t kLf = kP1 + al(sizeof(Rt) * WINR * BLOCK * P);
   static constexpr size_t kSlot = kLf + al(sizeof(T2) * BLOCK * P * NR);
   static constexpr size_t kOff = kSlot + al(sizeof(int) * 2 * BLOCK * P);
-  static constexpr size_t kAnchor = kOff + al(sizeof(typename OffT<T2>::type) * BLOCK * P);
+  static constexpr size_t kAnchor = kOff + (FIO_K3_OFFG ? 0 : al(sizeof(typename OffT<T2>::type) * BLOCK * P));
   static constexpr size_t kBox = kAnchor + al(sizeof(int2) * BLOCK);
   static constexpr size_t kBar = kBox + al(sizeof(int) * 2 * kBoxInts);
   // the tile ring: 128-byte aligned (TMA destination); the plan rounds the slot size (tile_cap) to
@@ -1148,11 +1153,11 @@ __global__ void __launch_bounds__(K3Cfg<T2>::BLOCK, NR == 1 ? K3Cfg<T2>::minb(TA
   auto prefetch_meta = [&](int chn, int buf) {
     if (chn < iw.nchunks && tid == 0) {
       const long long c0 = (long long)chn * BLOCK * P;  // first physical slot of the chunk
-      mbar_expect_tx(bar_m + buf, (unsigned)(kA + kB + kS + kO));
+      mbar_expect_tx(bar_m + buf, (unsigned)(kA + kB + kS + (FIO_K3_OFFG ? 0 : kO)));
       bulk_g2s(m_anchor, iw.anchor + 2 * (long long)chn * BLOCK, kA, bar_m + buf);
       bulk_g2s(sbox + kBoxInts * buf, iw.box + (long long)kBoxInts * chn, kB, bar_m + buf);
       bulk_g2s(m_slot + buf * BLOCK * P, iw.slot_x + c0, kS, bar_m + buf);
-      bulk_g2s(m_off, offs + c0, kO, bar_m + buf);
+      if (!FIO_K3_OFFG) bulk_g2s(m_off, offs + c0, kO, bar_m + buf);
     }
   };
   if (tid == 0) {
@@ -1174,6 +1179,11 @@ __global__ void __launch_bounds__(K3Cfg<T2>::BLOCK, NR == 1 ? K3Cfg<T2>::minb(TA
     const int cpr = bnc / EPC;  // 16-byte units per tile row
     const int tchunks = bnr * cpr;
     const T2* __restrict__ al = alpha + (long long)ch * BLOCK * P;
+    O2 goff[P];  // FIO_K3_OFFG: this thread's offsets, loaded from global memory early in the chunk
+    if (FIO_K3_OFFG) {
+#pragma unroll
+      for (int k = 0; k < P; ++k) goff[k] = offs[(long long)ch * BLOCK * P + k * BLOCK + tid];
+    }
     // this thread's share of every tile copy, fixed for the chunk: source offsets within G_lt (row
     // wrapped mod the fine grid) and destination offsets within the tile
     int csrc[MAXC], cdst[MAXC];
@@ -1250,7 +1260,7 @@ __global__ void __launch_bounds__(K3Cfg<T2>::BLOCK, NR == 1 ? K3Cfg<T2>::minb(TA
       Rt o1[P], o2[P];
 #pragma unroll
       for (int k = 0; k < P; ++k) {
-        const O2 o = m_off[k * BLOCK + tid];
+        const O2 o = FIO_K3_OFFG ? goff[k] : m_off[k * BLOCK + tid];
         o1[k] = o.x;
         o2[k] = o.y;
       }
