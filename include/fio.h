@@ -121,6 +121,10 @@ typedef struct {
                          taper of half-width wedge_overlap pi / W around every boundary ray, sum_l
                          chi_l = 1 exactly, so L is unchanged; each wedge's support,
                          box and rank grow with the overlap. */
+  int paper_accept;   /* 0: accept the skeleton when q <= 3r/4 (reading R8, the pivoted
+                         skeletons need less oversampling; backed by the certification).  1: the paper's
+                         rule q <= r/3, i.e. keep doubling r until the numerical
+                         rank is at most a third of the sample -- more plan time, same operator. */
 } fio_opts;
 
 #define FIO_NCCL_ID_BYTES 128

@@ -63,7 +63,7 @@ class _Opts(ctypes.Structure):
                 ("nufft_beta", ctypes.c_double), ("seed", ctypes.c_uint64), ("device", ctypes.c_int),
                 ("rank", ctypes.c_int), ("nranks", ctypes.c_int), ("r_init", ctypes.c_int),
                 ("r_max", ctypes.c_int), ("certify", ctypes.c_int), ("skeleton", ctypes.c_int),
-                ("nccl_id", ctypes.c_void_p), ("wedge_overlap", ctypes.c_double)]
+                ("nccl_id", ctypes.c_void_p), ("wedge_overlap", ctypes.c_double), ("paper_accept", ctypes.c_int)]
 
 
 class _Info(ctypes.Structure):
@@ -209,7 +209,8 @@ class Plan:
                  seed: int = 0x5EED, device: Optional[int] = None, rank: int = 0, nranks: int = 1,
                  r_init: int = 32, r_max: int = 512, certify: bool = True, rho_sign: int = 1,
                  amplitude: str = "separable", skeleton: bool = False, load: Optional[str] = None,
-                 group=None, nccl_id: Optional[bytes] = None, wedge_overlap: float = 0.0):
+                 group=None, nccl_id: Optional[bytes] = None, wedge_overlap: float = 0.0,
+                 paper_accept: bool = False):
         import torch
         if not torch.cuda.is_available():
             raise FioError(-3, "no CUDA device: the FIO apply runs only on the GPU (no CPU fallback)")
@@ -239,6 +240,7 @@ class Plan:
         o.r_init, o.r_max, o.certify = int(r_init), int(r_max), int(bool(certify))
         o.skeleton = int(bool(skeleton))
         o.wedge_overlap = float(wedge_overlap)
+        o.paper_accept = int(bool(paper_accept))
         # wedge-sharded with a communicator: the id comes from rank 0 (broadcast over `group`, or given)
         if nranks > 1 and nccl_id is None and group is not None:
             nccl_id = broadcast_nccl_id(group)

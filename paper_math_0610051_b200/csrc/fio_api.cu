@@ -405,7 +405,8 @@ fio_status separate_wedge(fio_plan_s& P, const WedgeGeom& g, Rng& rng, cudaStrea
     for (int k = 0; k < rc; ++k)
       if (std::sqrt(std::max(lam[k], 0.0)) > eps * s1) ++q;
     // accept when q is small against r, else double r and resample
-    if (4 * q <= 3 * rc || rc < r || r >= n || r >= P.opts.r_max) break;
+    const bool accepted = P.opts.paper_accept ? 3 * q <= rc : 4 * q <= 3 * rc;
+    if (accepted || rc < r || r >= n || r >= P.opts.r_max) break;
     r = std::min(std::min(2 * r, n), P.opts.r_max);
   }
   r_out = r;
@@ -1567,6 +1568,10 @@ static fio_status plan_impl(fio_handle* out, int N, const fio_phase* phase, cons
     set_error("fio_plan: nufft_w must be 0 or in [3, 12]");
     return FIO_EINVAL;
   }
+  if (o.paper_accept != 0 && o.paper_accept != 1) {
+    set_error("fio_plan: paper_accept must be 0 or 1");
+    return FIO_EINVAL;
+  }
   if (!(o.wedge_overlap >= 0.0 && o.wedge_overlap <= 1.0)) {
     set_error("fio_plan: wedge_overlap must lie in [0, 1]");
     return FIO_EINVAL;
@@ -1600,6 +1605,7 @@ static fio_status plan_impl(fio_handle* out, int N, const fio_phase* phase, cons
   P->poly_err = es_poly_fit(P->taps, P->es_beta, P->poly);
   P->input_hash = input_hash(N, phase, amp);
   if (o.wedge_overlap > 0.0) P->input_hash = fnv1a(P->input_hash, &o.wedge_overlap, sizeof(double));
+  if (o.paper_accept) P->input_hash = fnv1a(P->input_hash, &o.paper_accept, sizeof(int));
   if (load) {  // fio_plan_load: the file must describe exactly this plan
     const bool same = hdr->N == N && hdr->W == P->W && hdr->dtype == o.dtype && hdr->taps == P->taps &&
                       hdr->rank == o.rank && hdr->nranks == o.nranks && hdr->eps == eps &&

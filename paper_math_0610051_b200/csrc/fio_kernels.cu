@@ -1059,6 +1059,35 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned by
                "l"(src), "r"(bytes), "r"(smem_u32(bar))
                : "memory");
 }
+// FIO_K3_L2HINT: L2 eviction priorities for K3's streams -- alpha' blocks and chunk tables are read
+// exactly once (evict_first), the fine-grid tiles are re-read by neighbouring chunks (evict_last), so the
+// 14 GB alpha' stream does not push a wedge's ~31 MB of G out of the 126 MB L2
+#ifndef FIO_K3_L2HINT
+#define FIO_K3_L2HINT 1
+#endif
+__device__ __forceinline__ unsigned long long l2_policy_first() {
+  unsigned long long p;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;\n" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ unsigned long long l2_policy_last() {
+  unsigned long long p;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;\n" : "=l"(p));
+  return p;
+}
+// bulk_g2s with an L2 cache policy
+__device__ __forceinline__ void bulk_g2s_hint(void* dst, const void* src, unsigned bytes, unsigned long long* bar,
+                                              unsigned long long pol) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;\n" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(pol)
+      : "memory");
+}
+__device__ __forceinline__ void cp_async16_hint(void* smem, const void* gmem, unsigned long long pol) {
+  unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.cg.shared.global.L2::cache_hint [%0], [%1], 16, %2;\n" ::"r"(s), "l"(gmem), "l"(pol) : "memory");
+}
 // TMA tensor copy: the box at (x, y, z) of a 3-D tensor map into shared memory, completing on `bar`
 __device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, int x, int y, int z,
                                             unsigned long long* bar) {
@@ -1066,6 +1095,15 @@ __device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, i
       "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], "
       "[%5];\n" ::"r"(smem_u32(dst)),
       "l"(reinterpret_cast<unsigned long long>(map)), "r"(x), "r"(y), "r"(z), "r"(smem_u32(bar))
+      : "memory");
+}
+
+__device__ __forceinline__ void tma_load_3d_hint(void* dst, const CUtensorMap* map, int x, int y, int z,
+                                                 unsigned long long* bar, unsigned long long pol) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1, {%2, "
+      "%3, %4}], [%5], %6;\n" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<unsigned long long>(map)), "r"(x), "r"(y), "r"(z), "r"(smem_u32(bar)), "l"(pol)
       : "memory");
 }
 
@@ -1154,10 +1192,18 @@ __global__ void __launch_bounds__(K3Cfg<T2>::BLOCK, NR == 1 ? K3Cfg<T2>::minb(TA
     if (chn < iw.nchunks && tid == 0) {
       const long long c0 = (long long)chn * BLOCK * P;  // first physical slot of the chunk
       mbar_expect_tx(bar_m + buf, (unsigned)(kA + kB + kS + (FIO_K3_OFFG ? 0 : kO)));
+      if (FIO_K3_L2HINT) {
+        const unsigned long long pf = l2_policy_first();
+        bulk_g2s_hint(m_anchor, iw.anchor + 2 * (long long)chn * BLOCK, kA, bar_m + buf, pf);
+        bulk_g2s_hint(sbox + kBoxInts * buf, iw.box + (long long)kBoxInts * chn, kB, bar_m + buf, pf);
+        bulk_g2s_hint(m_slot + buf * BLOCK * P, iw.slot_x + c0, kS, bar_m + buf, pf);
+        if (!FIO_K3_OFFG) bulk_g2s_hint(m_off, offs + c0, kO, bar_m + buf, pf);
+      } else {
       bulk_g2s(m_anchor, iw.anchor + 2 * (long long)chn * BLOCK, kA, bar_m + buf);
       bulk_g2s(sbox + kBoxInts * buf, iw.box + (long long)kBoxInts * chn, kB, bar_m + buf);
       bulk_g2s(m_slot + buf * BLOCK * P, iw.slot_x + c0, kS, bar_m + buf);
       if (!FIO_K3_OFFG) bulk_g2s(m_off, offs + c0, kO, bar_m + buf);
+      }
     }
   };
   if (tid == 0) {
@@ -1228,21 +1274,36 @@ __global__ void __launch_bounds__(K3Cfg<T2>::BLOCK, NR == 1 ? K3Cfg<T2>::minb(TA
           if (tid == 0) {
             constexpr int kTile = (C64 ? kK3BoxRows64 * kK3BoxCols64 : kK3BoxRows128 * kK3BoxCols128) * sizeof(T2);
             mbar_expect_tx(bar_a + st, (unsigned)(kAl + kTile));
+            if (FIO_K3_L2HINT) {
+              bulk_g2s_hint(aring + st * BLOCK * P, al + t * nslots, (unsigned)kAl, bar_a + st, l2_policy_first());
+              tma_load_3d_hint(tring + st * NR * cap, &tmap, (bc + kHalo) * (int)(sizeof(T2) / 8), br, t, bar_a + st,
+                               l2_policy_last());
+            } else {
             bulk_g2s(aring + st * BLOCK * P, al + t * nslots, (unsigned)kAl, bar_a + st);
             tma_load_3d(tring + st * NR * cap, &tmap, (bc + kHalo) * (int)(sizeof(T2) / 8), br, t, bar_a + st);
+            }
           }
         } else {
         if (tid == 0) {
           mbar_expect_tx(bar_a + st, (unsigned)kAl);
-          bulk_g2s(aring + st * BLOCK * P, al + t * nslots, (unsigned)kAl, bar_a + st);
+          if (FIO_K3_L2HINT)
+            bulk_g2s_hint(aring + st * BLOCK * P, al + t * nslots, (unsigned)kAl, bar_a + st, l2_policy_first());
+          else
+            bulk_g2s(aring + st * BLOCK * P, al + t * nslots, (unsigned)kAl, bar_a + st);
         }
+        const unsigned long long pl = FIO_K3_L2HINT ? l2_policy_last() : 0ull;
 #pragma unroll
         for (int r = 0; r < NR; ++r) {
           const T2* __restrict__ gt = G[r] + t * gstride;
           T2* tile = tring + (st * NR + r) * cap;
 #pragma unroll
           for (int u = 0; u < MAXC; ++u)
-            if (u < ncp) cp_async16(tile + cdst[u], gt + csrc[u]);
+            if (u < ncp) {
+              if (FIO_K3_L2HINT)
+                cp_async16_hint(tile + cdst[u], gt + csrc[u], pl);
+              else
+                cp_async16(tile + cdst[u], gt + csrc[u]);
+            }
         }
         }
       }

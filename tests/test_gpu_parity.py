@@ -747,3 +747,27 @@ def test_nufft_component_vs_direct_nudft(N, dtype, eps, npts):
     rel, mx = _pointwise(out.ravel()[idx], ref)
     print(f"NUFFT component N={N} {dtype}: rel l2 {rel:.3e}, max|err|/rms {mx:.3e}, w {plan.info['nufft_w']}")
     assert rel <= 10 * eps and mx <= 100 * eps, (rel, mx)
+
+
+# ------------------------------------------------------------------ the paper's acceptance rule
+@pytest.mark.parametrize("name", ["cfg0", "cfg1", "cfg3_c128"])
+def test_paper_acceptance_rule(name):
+    # opts.paper_accept = 1: r doubles until q <= r/3 (the paper's test) instead of the default q <= 3r/4
+    # (reading R8).  Same operator, same eps-rank per wedge (within the sampling's +-2), parity kept.
+    cfg = wl.config(name)
+    op, f = wl.make_operator(cfg), wl.make_input(cfg)
+    base = make_plan(op, cfg["eps"])
+    plan, out = run(op, f, eps=cfg["eps"], paper_accept=True)
+    wd, wb = plan.wedges(), base.wedges()
+    assert np.all((3 * wd["q"] <= wd["r"]) | (wd["r"] >= 512)), (wd["q"], wd["r"])
+    assert np.all(np.abs(wd["q"] - wb["q"]) <= 2), (wd["q"], wb["q"])
+    if op.N <= 256:
+        err = oracle.rel_l2(out, oracle.fio(op, f))
+    else:
+        pts = wl.sample_points(op.N, 4096, 1)
+        err = oracle.rel_l2(out.ravel()[pts], oracle.fio(op, f, pts=pts))
+    print(f"{name} paper rule: sum_q {plan.info['sum_q']} (default {base.info['sum_q']}), mean r "
+          f"{wd['r'].mean():.1f} (default {wb['r'].mean():.1f}), plan {plan.info['plan_seconds']:.2f} s "
+          f"(default {base.info['plan_seconds']:.2f} s), rel l2 {err:.3e}, max sep err {wd['sep_err'].max():.2e}")
+    assert err <= 10 * cfg["eps"], err
+    assert plan.info["certified"] == 1
