@@ -327,9 +327,13 @@ fio_status separate_wedge(fio_plan_s& P, const WedgeGeom& g, Rng& rng, cudaStrea
     FIO_CUDA(cudaMemcpyAsync(B.data(), dTmp.p, sizeof(cplx) * B.size(), cudaMemcpyDeviceToHost, s));
     FIO_CUDA(cudaStreamSynchronize(s));
     // (2) column pivoting -> skeleton columns C
-    std::vector<int> piv = pivoted_columns(nr0, nc0, B, r);
     C.clear();
-    for (int p : piv) C.push_back(candCols[p]);
+    if (P.opts.paper_accept) {  // the paper's step: r columns drawn uniformly
+      for (int j = 0; j < std::min(r, nc0); ++j) C.push_back(candCols[j]);
+    } else {
+      std::vector<int> piv = pivoted_columns(nr0, nc0, B, r);
+      for (int p : piv) C.push_back(candCols[p]);
+    }
     const int rc = (int)C.size();
     if (rc == 0) {
       q = 0;
@@ -405,8 +409,10 @@ fio_status separate_wedge(fio_plan_s& P, const WedgeGeom& g, Rng& rng, cudaStrea
     for (int k = 0; k < rc; ++k)
       if (std::sqrt(std::max(lam[k], 0.0)) > eps * s1) ++q;
     // accept when q is small against r, else double r and resample
-    const bool accepted = P.opts.paper_accept ? 3 * q <= rc : 4 * q <= 3 * rc;
-    if (accepted || rc < r || r >= n || r >= P.opts.r_max) break;
+    // paper_accept: uniform columns, accepted when q <= r/3; default: pivoted
+    // columns, accepted when q <= 3r/4 or when the pivoting ran out of numerical rank (rc < r)
+    const bool accepted = P.opts.paper_accept ? 3 * q <= rc : (4 * q <= 3 * rc || rc < r);
+    if (accepted || r >= n || r >= P.opts.r_max) break;
     r = std::min(std::min(2 * r, n), P.opts.r_max);
   }
   r_out = r;

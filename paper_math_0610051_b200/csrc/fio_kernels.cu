@@ -1062,6 +1062,10 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned by
 // FIO_K3_L2HINT: L2 eviction priorities for K3's streams -- alpha' blocks and chunk tables are read
 // exactly once (evict_first), the fine-grid tiles are re-read by neighbouring chunks (evict_last), so the
 // 14 GB alpha' stream does not push a wedge's ~31 MB of G out of the 126 MB L2
+// FIO_K3_KINNER: K3's per-row column sums with the points innermost (more independent FMA chains)
+#ifndef FIO_K3_KINNER
+#define FIO_K3_KINNER 0
+#endif
 #ifndef FIO_K3_L2HINT
 #define FIO_K3_L2HINT 1
 #endif
@@ -1412,6 +1416,25 @@ __global__ void __launch_bounds__(K3Cfg<T2>::BLOCK, NR == 1 ? K3Cfg<T2>::minb(TA
               for (int jj = 0; jj < WIN; ++jj) v[r][jj] = win[u][i * sst + jj];
             }
           }
+          if (FIO_K3_KINNER) {  // points innermost: P RP independent column-sum chains per tap
+            T2 rr[P][RP];
+#pragma unroll
+            for (int k = 0; k < P; ++k)
+#pragma unroll
+              for (int r = 0; r < RP; ++r) rr[k][r] = mk<T2>(0, 0);
+#pragma unroll
+            for (int jj = 0; jj < WIN; ++jj)
+#pragma unroll
+              for (int k = 0; k < P; ++k)
+#pragma unroll
+                for (int r = 0; r < RP; ++r)
+                  if (i0 + r < WINR) rr[k][r] = cfma_real(p2[k][jj], v[r][jj], rr[k][r]);
+#pragma unroll
+            for (int k = 0; k < P; ++k)
+#pragma unroll
+              for (int r = 0; r < RP; ++r)
+                if (i0 + r < WINR) F[u][k] = cfma_real(w1[r][k], rr[k][r], F[u][k]);
+          } else {
 #pragma unroll
           for (int k = 0; k < P; ++k) {
             T2 rr[RP];
@@ -1425,6 +1448,7 @@ __global__ void __launch_bounds__(K3Cfg<T2>::BLOCK, NR == 1 ? K3Cfg<T2>::minb(TA
 #pragma unroll
             for (int r = 0; r < RP; ++r)
               if (i0 + r < WINR) F[u][k] = cfma_real(w1[r][k], rr[r], F[u][k]);
+          }
           }
         }
       }
