@@ -1092,6 +1092,15 @@ __device__ __forceinline__ void cp_async16_hint(void* smem, const void* gmem, un
   unsigned s = (unsigned)__cvta_generic_to_shared(smem);
   asm volatile("cp.async.cg.shared.global.L2::cache_hint [%0], [%1], 16, %2;\n" ::"r"(s), "l"(gmem), "l"(pol) : "memory");
 }
+// FIO_K3_L2PF: thread 0 asks the TMA engine to prefetch into L2 the alpha'(t) block FIO_K3_L2PF terms
+// beyond the one it stages (across the chunk boundary into the CTA's next chunk), so the staging copy
+// finds it in L2 -- a deeper pipeline that costs no shared memory
+#ifndef FIO_K3_L2PF
+#define FIO_K3_L2PF 0
+#endif
+__device__ __forceinline__ void bulk_prefetch_l2(const void* src, unsigned bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;\n" ::"l"(src), "r"(bytes) : "memory");
+}
 // TMA tensor copy: the box at (x, y, z) of a 3-D tensor map into shared memory, completing on `bar`
 __device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, int x, int y, int z,
                                             unsigned long long* bar) {
@@ -1272,6 +1281,13 @@ __global__ void __launch_bounds__(K3Cfg<T2>::BLOCK, NR == 1 ? K3Cfg<T2>::minb(TA
     // the chunk's alpha'(t) block is contiguous: one bulk copy (TMA engine) on the stage's mbarrier;
     // the tile (short scattered rows) by cp.async from every thread
     auto issue = [&](int t, bool next_meta) {
+      if (FIO_K3_L2PF > 0 && tid == 0) {  // L2 prefetch of the alpha' block FIO_K3_L2PF terms ahead
+        const int tp = t + FIO_K3_L2PF;
+        if (tp < q)
+          bulk_prefetch_l2(al + tp * nslots, (unsigned)kAl);
+        else if (ch + (int)gridDim.x < iw.nchunks && tp - q < q)
+          bulk_prefetch_l2(alpha + (long long)(ch + gridDim.x) * BLOCK * P + (tp - q) * nslots, (unsigned)kAl);
+      }
       if (t < q) {
         const int st = (int)((gterm + t) % S);
         if (tma) {  // alpha'(t) and the tile (the fixed TMA box at the chunk's origin) on one mbarrier
