@@ -772,3 +772,38 @@ def test_paper_acceptance_rule(name):
     nmem = np.bincount(fio.geometry(op.N, plan.info["W"])["wedge_of"].ravel() + 1,
                        minlength=plan.info["W"] + 1)[1:][wd["l"]]
     assert np.all((3 * wd["q"] <= wd["r"]) | (wd["r"] >= np.minimum(512, nmem))), (wd["q"], wd["r"])
+
+
+# ------------------------------------------------------------------ the maximum size (reading R21: N <= 4096)
+@pytest.mark.parametrize("dtype,eps", [("c64", 1e-4), ("c128", 1e-6)])
+def test_max_size_shift_field_pointwise(dtype, eps):
+    # N = 4096, the largest grid the library accepts: the pointwise integer-shift field (exact reference
+    # Lf[n] = f[n + k(n)], reading R12) compared at all 16.8 M output points, W = 128 wedges
+    N = 4096
+    n1, n2 = np.meshgrid(np.arange(N, dtype=np.int64), np.arange(N, dtype=np.int64), indexing="ij")
+    k1 = (n1 // 389 + 2 * (n2 // 523)) % 5 - 2
+    k2 = ((n1 // 241) * (n2 // 331)) % 7 - 3
+    op = wl.shift_operator(N, k1, k2)
+    f = wl.white_noise(N, 17, dtype)
+    plan, out = run(op, f, eps=eps, dtype=dtype)
+    ref = f[(n1 + k1) % N, (n2 + k2) % N]
+    rel, mx = _pointwise(out, ref)
+    print(f"max size N={N} {dtype}: W {plan.info['W']}, rel l2 {rel:.3e}, max|err|/rms {mx:.3e}")
+    assert rel <= 10 * eps and mx <= 100 * eps, (rel, mx)
+
+
+@pytest.mark.slow
+def test_max_size_grt_c64_sampled():
+    # N = 4096 generalized-Radon phase (BASELINE configs[0] family), complex64 at eps = 1e-4: the largest
+    # plan that fits one B200 (alpha' ~123 GB resident), checked against the direct sum at 256 seeded points
+    N, eps = 4096, 1e-4
+    op = wl.grt_operator(N)
+    f = wl.white_noise(N, 0, "c64")
+    plan, out = run(op, f, eps=eps, dtype="c64")
+    pts = wl.sample_points(N, 256, 1)
+    ref = oracle.fio(op, f, pts=pts)
+    rel, mx = _pointwise(out.ravel()[pts], ref)
+    print(f"max size GRT N={N} c64: W {plan.info['W']}, sum_q {plan.info['sum_q']}, alpha "
+          f"{plan.info['alpha_bytes'] / 1e9:.1f} GB, plan {plan.info['plan_seconds']:.1f} s, rel l2 {rel:.3e}, "
+          f"max|err|/rms {mx:.3e}")
+    assert rel <= 10 * eps and mx <= 100 * eps, (rel, mx)
