@@ -807,3 +807,44 @@ def test_max_size_grt_c64_sampled():
           f"{plan.info['alpha_bytes'] / 1e9:.1f} GB, plan {plan.info['plan_seconds']:.1f} s, rel l2 {rel:.3e}, "
           f"max|err|/rms {mx:.3e}")
     assert rel <= 10 * eps and mx <= 100 * eps, (rel, mx)
+
+
+# ------------------------------------------------------------------ distinct handles are independent (include/fio.h)
+def test_concurrent_handles_on_threads():
+    # two plans (different operators and dtypes) applied concurrently from two host threads, each on its
+    # own CUDA stream: every result equals the same plan's serial apply bit for bit (no process-wide
+    # launch state, per-handle workspaces; DESIGN.md section 2 "Device state")
+    import threading
+    N = 256
+    jobs = [(wl.grt_operator(N), wl.white_noise(N, 21, "c128"), "c128", 1e-6),
+            (wl.wave_operator(N), wl.white_noise(N, 22, "c64"), "c64", 1e-4)]
+    plans, refs, ins = [], [], []
+    for op, f, dt, eps in jobs:
+        p, r = run(op, f, eps=eps, dtype=dt)
+        plans.append(p)
+        refs.append(r)
+        ins.append(torch.from_numpy(f).to(DEV, torch.complex64 if dt == "c64" else torch.complex128))
+    results = [[], []]
+    errors = []
+
+    def worker(i):
+        try:
+            s = torch.cuda.Stream(device=DEV)
+            with torch.cuda.stream(s):
+                for _ in range(8):
+                    out = plans[i].apply(ins[i], stream=s)
+                    s.synchronize()
+                    results[i].append(out.cpu().numpy().astype(np.complex128))
+        except Exception as e:  # pragma: no cover - reported below
+            errors.append(repr(e))
+
+    th = [threading.Thread(target=worker, args=(i,)) for i in range(2)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
+    assert not errors, errors
+    for i in range(2):
+        assert len(results[i]) == 8
+        for r in results[i]:
+            assert np.array_equal(r, refs[i])
