@@ -188,6 +188,14 @@ def cpu_oracle_rate(cfg, npts, seed=1):
                       f"fhat precomputed), {dt:.1f} s; applies/s = points/s / N^2"}
 
 
+def bench_config(name, world):
+    """The `config` object of the JSON line -- identical for the CUDA arm and the oracle arm."""
+    cfg = wl.config(name)
+    return {"workload": name, "N": cfg["N"], "eps": cfg["eps"],
+            "parallelism": f"wedge-sharded x{world}" if world > 1 else "single GPU",
+            "l2": "inputs larger than L2 (the separated factors alpha' are streamed from HBM every step)"}
+
+
 def run_reference(args):
     rank, world, _ = dist_env()
     if rank != 0:
@@ -205,8 +213,8 @@ def run_reference(args):
     val = pps / (N * N)
     line = {"metric": "fio_applies_per_s", "value": val, "unit": "applies/s", "n_gpus": 0, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": 1e3 / val, "higher_is_better": True, "scaling": "strong",
-            "vs_baseline": None, "dtype": "f64", "data": "synthetic", "impl": "reference",
-            "config": {"workload": args.config, "N": N, "eps": cfg["eps"]},
+            "vs_baseline": None, "dtype": "c128", "data": "synthetic", "impl": "reference",
+            "config": bench_config(args.config, world),
             "points_per_s": pps,
             "cpu_baseline": {"value": val, "unit": "applies/s", "cores": times[0]["cores"], "kind": "oracle",
                              "sample": f"each step: {npts} seeded output points (direct sum), median over steps"},
@@ -394,9 +402,8 @@ def run_gpu(args):
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": main["ms_per_step"],
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
             "dtype": main["dtype"], "data": "synthetic",
-            "config": {"workload": args.config, "N": main["N"], "eps": main["eps"],
-                       "parallelism": f"wedge-sharded x{world}" if world > 1 else "single GPU",
-                       "l2": "inputs larger than L2 (alpha' streams %.1f GB per step)" % main["plan"]["alpha_GB"]},
+            "config": bench_config(args.config, world),
+            "alpha_GB_per_step": main["plan"]["alpha_GB"],
             "points_per_s": main["points_per_s"],
             # the roofline that binds the dominant kernel: FP64 pipe for complex128 K3,
             # HBM for complex64; the other one is reported beside it
