@@ -119,8 +119,8 @@ def k3_resource_model(info, c64, ms, sm_mhz):
     (k3_window_rows x k3_window_cols, plan dtype) and the P row weights (FP32 c64 / FP64 c128) from
     shared memory and alpha'(t) from the ring, and issues 2 real FMAs per (point, window cell), 2 per
     (point, row) and 4 for the alpha product.  Fractions of the shared -> register path
-    (128 B/clk/SM) and of the FMA pipe (measured: 126 FP32 / 63.3 FP64 FMA/clk/SM,
-    profiles/r02_microbench.json) at the sampled SM clock."""
+    (measured: 126 B/clk/SM for conflict-free 16-byte loads) and of the FMA pipe (measured: 126 FP32 /
+    63 FP64 FMA/clk/SM), profiles/r02_microbench.json, at the sampled SM clock."""
     P = info["group_p"]
     win, winr = info["k3_window_cols"], info["k3_window_rows"]
     cs, rs = (8, 4) if c64 else (16, 8)
@@ -130,8 +130,16 @@ def k3_resource_model(info, c64, ms, sm_mhz):
     clk = (sm_mhz or 1965.0) * 1e6
     t = ms * 1e-3
     sms = 148
-    return {"lsu_bytes": lsu_bytes, "lsu_frac": lsu_bytes / t / (sms * 128 * clk),
-            "fma": fmas, "fma_frac": fmas / t / (sms * (126.4 if c64 else 63.3) * clk),
+    lds, f32, f64 = 128.0, 126.4, 63.3  # fallback: the guide's shared-memory path, measured FMA rates
+    try:
+        with open(os.path.join(ROOT, "profiles", "r02_microbench.json")) as fh:
+            mb = json.load(fh)
+        lds, f32, f64 = (float(mb["lds128_contiguous_B_per_clk_sm"]), float(mb["ffma2_fma_per_clk_sm"]),
+                         float(mb["dfma_per_clk_sm"]))
+    except Exception:
+        pass
+    return {"lsu_bytes": lsu_bytes, "lsu_frac": lsu_bytes / t / (sms * lds * clk),
+            "fma": fmas, "fma_frac": fmas / t / (sms * (f32 if c64 else f64) * clk),
             "flops_per_s": 2 * fmas / t, "sm_mhz": sm_mhz, "model": "DESIGN.md section 7"}
 
 

@@ -86,8 +86,8 @@ __global__ void k_lds(float* out, int mode, int seed) {
   constexpr int W = BYTES / 4;
   unsigned h = (threadIdx.x * 2654435761u) ^ (seed * 40503u);
   int base;
-  if (mode == 0)
-    base = (threadIdx.x * W) & (8192 - 256);
+  if (mode == 0)  // lane l of a warp reads bytes [BYTES l, BYTES (l + 1)) of the warp's block
+    base = (threadIdx.x * W) % 4096;
   else if (mode == 1)
     base = ((h >> 7) % (8192 / W - 128)) * W;
   else
@@ -100,11 +100,11 @@ __global__ void k_lds(float* out, int mode, int seed) {
     const unsigned addr = sbase + 4u * (unsigned)(base + ((i * 8 * W) & 255));
     if constexpr (W == 4) {
       float a, b, c, d;
-      asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(a), "=f"(b), "=f"(c), "=f"(d) : "r"(addr));
+      asm volatile("ld.volatile.shared.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(a), "=f"(b), "=f"(c), "=f"(d) : "r"(addr));
       acc += a + b + c + d;
     } else {
       float a, b;
-      asm volatile("ld.shared.v2.f32 {%0, %1}, [%2];" : "=f"(a), "=f"(b) : "r"(addr));
+      asm volatile("ld.volatile.shared.v2.f32 {%0, %1}, [%2];" : "=f"(a), "=f"(b) : "r"(addr));
       acc += a + b;
     }
   }
