@@ -1009,6 +1009,16 @@ template <> struct K3Cfg<double2> {
 //   anchors       [BLOCK] int2              (next chunk)
 //   boxes         [2][kBoxInts] int         footprint box of the current and the next chunk
 //   tile ring     [S][cap] T2               the chunk's footprint tile of G_lt per term in flight
+// FIO_K3_P1REG: the row weights stay in registers for the chunk (no shared-memory reloads per term;
+// c64 K3 2.08 -> 1.93 ms, c128 10.04 -> 9.87 ms at N = 1024) wherever they fit without spills
+// (ptxas -v, all instantiations): otherwise they stay in shared memory
+#ifndef FIO_K3_P1REG
+#define FIO_K3_P1REG 1
+#endif
+constexpr bool k3_p1reg(bool c64, int taps, int nr) {
+  return FIO_K3_P1REG && (c64 ? (nr == 1 ? (taps <= 5 || (taps >= 9 && taps <= 11)) : (taps <= 7 || taps >= 9))
+                              : (nr == 1 ? taps <= 9 : taps <= 7));
+}
 // FIO_K3_OFFG: the points' fine-grid offsets are read from global memory (L2) when a chunk starts instead
 // of being prefetched into shared memory (saves BLOCK P sizeof(O2) bytes per CTA: one more CTA per SM)
 #ifndef FIO_K3_OFFG
@@ -1022,7 +1032,8 @@ struct K3Layout {  // NR right-hand sides: NR running-sum buffers, NR tiles per 
   static constexpr size_t al(size_t b) { return (b + 15) / 16 * 16; }
   static constexpr size_t kRing = 0;
   static constexpr size_t kP1 = kRing + al(sizeof(T2) * K3Cfg<T2>::STAGES * BLOCK * P);
-  static constexpr size_t kLf = kP1 + al(sizeof(Rt) * WINR * BLOCK * P);
+  static constexpr bool PREG = k3_p1reg(sizeof(T2) == 8, TAPS, NR);  // row weights in registers
+  static constexpr size_t kLf = kP1 + (PREG ? 0 : al(sizeof(Rt) * WINR * BLOCK * P));
   static constexpr size_t kSlot = kLf + al(sizeof(T2) * BLOCK * P * NR);
   static constexpr size_t kOff = kSlot + al(sizeof(int) * 2 * BLOCK * P);
   static constexpr size_t kAnchor = kOff + (FIO_K3_OFFG ? 0 : al(sizeof(typename OffT<T2>::type) * BLOCK * P));
@@ -1337,6 +1348,8 @@ __global__ void __launch_bounds__(K3Cfg<T2>::BLOCK, NR == 1 ? K3Cfg<T2>::minb(TA
     const int2 an = m_anchor[tid];
     const int woff = (an.x - br) * sst + (an.y - bc);
     Rt p2[P][WIN];
+    constexpr bool PREG = L::PREG;
+    Rt p1r[P][PREG ? WINR : 1];  // row weights kept in registers (k3_p1reg)
     {
       Rt o1[P], o2[P];
 #pragma unroll
@@ -1348,6 +1361,12 @@ __global__ void __launch_bounds__(K3Cfg<T2>::BLOCK, NR == 1 ? K3Cfg<T2>::minb(TA
       {
         Rt w1[P][WINR];
         axis_weights<TAPS, WINR, P>(o1, poly, w1);
+        if constexpr (PREG) {
+#pragma unroll
+          for (int k = 0; k < P; ++k)
+#pragma unroll
+            for (int i = 0; i < WINR; ++i) p1r[k][i] = w1[k][i];
+        } else
 #pragma unroll
         for (int i = 0; i < WINR; ++i)
 #pragma unroll
@@ -1400,6 +1419,11 @@ __global__ void __launch_bounds__(K3Cfg<T2>::BLOCK, NR == 1 ? K3Cfg<T2>::minb(TA
         for (int r = 0; r < RP; ++r) {
           if (i0 + r >= WINR) continue;
           const int i = i0 + r;
+          if constexpr (PREG) {
+#pragma unroll
+            for (int k = 0; k < P; ++k) w1[r][k] = p1r[k][i];
+            continue;
+          }
 #pragma unroll
           for (int cc = 0; cc < P / RPV; ++cc) {
             if constexpr (sizeof(Rt) == 4) {
