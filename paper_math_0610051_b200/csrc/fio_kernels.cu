@@ -1019,6 +1019,10 @@ constexpr bool k3_p1reg(bool c64, int taps, int nr) {
   return FIO_K3_P1REG && (c64 ? (nr == 1 ? (taps <= 5 || (taps >= 9 && taps <= 11)) : (taps <= 7 || taps >= 9))
                               : (nr == 1 ? taps <= 9 : taps <= 7));
 }
+// FIO_K3_XCHUNK: stage the next chunk's first term during the current chunk's last term
+#ifndef FIO_K3_XCHUNK
+#define FIO_K3_XCHUNK 0
+#endif
 // FIO_K3_OFFG: the points' fine-grid offsets are read from global memory (L2) when a chunk starts instead
 // of being prefetched into shared memory (saves BLOCK P sizeof(O2) bytes per CTA: one more CTA per SM)
 #ifndef FIO_K3_OFFG
@@ -1183,6 +1187,7 @@ __global__ void __launch_bounds__(K3Cfg<T2>::BLOCK, NR == 1 ? K3Cfg<T2>::minb(TA
   constexpr int TT = K3Cfg<T2>::TT;
   constexpr int RP = K3Cfg<T2>::RP;
   constexpr int LA = S - TT;  // terms staged ahead of the step being computed
+  constexpr bool kXChunk = FIO_K3_XCHUNK && LA == 1 && TT == 1 && NR == 1;
   static_assert(LA >= TT, "K3 ring: at least one step in flight");
   constexpr int EPC = 16 / (int)sizeof(T2);  // complex elements per 16-byte unit
   constexpr int RPV = 16 / (int)sizeof(Rt);  // row weights per 16-byte unit
@@ -1340,10 +1345,32 @@ __global__ void __launch_bounds__(K3Cfg<T2>::BLOCK, NR == 1 ? K3Cfg<T2>::minb(TA
       }
       // the next chunk's tables, issued once every thread has consumed the current offsets/anchors
       if (next_meta) prefetch_meta(ch + gridDim.x, buf ^ 1);
+      // FIO_K3_XCHUNK: during the last term, thread 0 stages term 0 of the CTA's next chunk (alpha'
+      // block and TMA tile, from the next chunk's prefetched box) into the free ring slot, so a chunk
+      // boundary does not expose a full memory latency
+      if constexpr (kXChunk) {
+        if (t == q && tid == 0 && ch + (int)gridDim.x < iw.nchunks && iw.tma) {
+          const int nb = buf ^ 1;
+          mbar_wait(bar_m + nb, (unsigned)((it + 1) >> 1) & 1u);
+          const int* nbx = sbox + kBoxInts * nb;
+          if (nbx[7]) {
+            const int st = (int)((gterm + q) % S);
+            constexpr int kTile = (C64 ? kK3BoxRows64 * kK3BoxCols64 : kK3BoxRows128 * kK3BoxCols128) * sizeof(T2);
+            mbar_expect_tx(bar_a + st, (unsigned)(kAl + kTile));
+            bulk_g2s_hint(aring + st * BLOCK * P, alpha + (long long)(ch + gridDim.x) * BLOCK * P, (unsigned)kAl,
+                          bar_a + st, l2_policy_first());
+            tma_load_3d_hint(tring + st * NR * cap, &tmap, (nbx[2] + kHalo) * (int)(sizeof(T2) / 8), nbx[1], 0,
+                             bar_a + st, l2_policy_last());
+          }
+        }
+      }
       cp_async_commit();
     };
+    if (kXChunk && it > 0 && tma && q > 0)
+      cp_async_commit();  // term 0 was staged during the previous chunk (the running sums' copy group)
+    else
 #pragma unroll
-    for (int u = 0; u < LA; ++u) issue(u, false);
+      for (int u = 0; u < LA; ++u) issue(u, false);
     // weights of this thread's points: phi2 (columns) in registers, phi1 (rows) in shared memory
     const int2 an = m_anchor[tid];
     const int woff = (an.x - br) * sst + (an.y - bc);
