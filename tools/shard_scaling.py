@@ -1,6 +1,8 @@
 """Estimate wedge-sharded strong scaling on ONE GPU: time rank r's partial apply (its wedges only:
 the compute every rank does at R GPUs) for r = 0..R-1 and report T1 / (R * max_r T_r).  The NCCL
-reduce-scatter (N*N complex, over NVLink) is not included."""
+reduce-scatter is not measured (one GPU): `rs_ms_model` is its modelled time, (R-1)/R N^2 s bytes per rank at
+the guide's measured 8-rank NCCL bus bandwidth (725 GB/s, B200_PROFILING.md) plus 20 us, and
+`est_efficiency_with_rs` = T1 / (R (max_r T_r + rs_ms_model)) -- an estimate, not a multi-GPU measurement."""
 import json
 import os
 import sys
@@ -44,6 +46,11 @@ for name in sys.argv[1:] or ["cfg3_c128"]:
         if R == 1:
             t1 = tmax
         eff = t1 / (R * tmax)
-        res[f"{name}_R{R}"] = {"max_rank_ms": tmax, "min_rank_ms": min(ts), "est_efficiency": eff}
-        print(f"{name} R={R}: per-rank ms max {tmax:.3f} min {min(ts):.3f} -> est. efficiency {eff:.3f}", flush=True)
+        cs = 8 if cfg["dtype"] == "c64" else 16
+        rs = 0.0 if R == 1 else ((R - 1) / R * op.N * op.N * cs / 725e9 + 20e-6) * 1e3
+        eff_rs = t1 / (R * (tmax + rs))
+        res[f"{name}_R{R}"] = {"max_rank_ms": tmax, "min_rank_ms": min(ts), "est_efficiency": eff,
+                               "rs_ms_model": rs, "est_efficiency_with_rs": eff_rs}
+        print(f"{name} R={R}: per-rank ms max {tmax:.3f} min {min(ts):.3f} -> est. efficiency {eff:.3f}, "
+              f"with the modelled reduce-scatter ({rs:.3f} ms) {eff_rs:.3f}", flush=True)
 print(json.dumps(res))
