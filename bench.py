@@ -116,8 +116,8 @@ def apply_algorithmic_bytes(info, N, c64):
 
 def k3_resource_model(info, c64, ms, sm_mhz):
     """What binds K3 on chip: per group-term the thread reads its window
-    (k3_window_rows x k3_window_cols, plan dtype) and the P row weights (FP32 c64 / FP64 c128) from
-    shared memory and alpha'(t) from the ring, and issues 2 real FMAs per (point, window cell), 2 per
+    (k3_window_rows x k3_window_cols, plan dtype) -- plus the P row weights (FP32 c64 / FP64 c128) where
+    they do not stay in registers -- from shared memory and alpha'(t) from the ring, and issues 2 real FMAs per (point, window cell), 2 per
     (point, row) and 4 for the alpha product.  Fractions of the shared -> register path
     (measured: 126 B/clk/SM for conflict-free 16-byte loads) and of the FMA pipe (measured: 126 FP32 /
     63 FP64 FMA/clk/SM), profiles/r02_microbench.json, at the sampled SM clock."""
@@ -125,7 +125,11 @@ def k3_resource_model(info, c64, ms, sm_mhz):
     win, winr = info["k3_window_cols"], info["k3_window_rows"]
     cs, rs = (8, 4) if c64 else (16, 8)
     gt = info["slot_terms"] / P
-    lsu_bytes = gt * (winr * win * cs + winr * P * rs + P * cs)
+    # row weights come from shared memory only where K3 keeps them out of registers (fio_kernels.cu
+    # k3_p1reg: complex64 w <= 5 or 9..11, complex128 w <= 9 keep them in registers)
+    taps = info["nufft_w"]
+    preg = (taps <= 5 or 9 <= taps <= 11) if c64 else taps <= 9
+    lsu_bytes = gt * (winr * win * cs + (0 if preg else winr * P * rs) + P * cs)
     fmas = gt * P * (winr * (win * 2 + 2) + 4)
     clk = (sm_mhz or 1965.0) * 1e6
     t = ms * 1e-3
