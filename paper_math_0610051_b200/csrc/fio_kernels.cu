@@ -1019,15 +1019,6 @@ constexpr bool k3_p1reg(bool c64, int taps, int nr) {
   return FIO_K3_P1REG && (c64 ? (nr == 1 ? (taps <= 5 || (taps >= 9 && taps <= 11)) : (taps <= 7 || taps >= 9))
                               : (nr == 1 ? taps <= 9 : taps <= 7));
 }
-// FIO_K3_XCHUNK: stage the next chunk's first term during the current chunk's last term
-#ifndef FIO_K3_XCHUNK
-#define FIO_K3_XCHUNK 0
-#endif
-// FIO_K3_OFFG: the points' fine-grid offsets are read from global memory (L2) when a chunk starts instead
-// of being prefetched into shared memory (saves BLOCK P sizeof(O2) bytes per CTA: one more CTA per SM)
-#ifndef FIO_K3_OFFG
-#define FIO_K3_OFFG 0
-#endif
 template <typename T2, int TAPS, int P, int NR = 1>
 struct K3Layout {  // NR right-hand sides: NR running-sum buffers, NR tiles per ring stage
   using Rt = typename Real<T2>::type;
@@ -1040,7 +1031,7 @@ struct K3Layout {  // NR right-hand sides: NR running-sum buffers, NR tiles per 
   static constexpr size_t kLf = kP1 + (PREG ? 0 : al(sizeof(Rt) * WINR * BLOCK * P));
   static constexpr size_t kSlot = kLf + al(sizeof(T2) * BLOCK * P * NR);
   static constexpr size_t kOff = kSlot + al(sizeof(int) * 2 * BLOCK * P);
-  static constexpr size_t kAnchor = kOff + (FIO_K3_OFFG ? 0 : al(sizeof(typename OffT<T2>::type) * BLOCK * P));
+  static constexpr size_t kAnchor = kOff + al(sizeof(typename OffT<T2>::type) * BLOCK * P);
   static constexpr size_t kBox = kAnchor + al(sizeof(int2) * BLOCK);
   static constexpr size_t kBar = kBox + al(sizeof(int) * 2 * kBoxInts);
   // the tile ring: 128-byte aligned (TMA destination); the plan rounds the slot size (tile_cap) to
@@ -1077,10 +1068,6 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned by
 // FIO_K3_L2HINT: L2 eviction priorities for K3's streams -- alpha' blocks and chunk tables are read
 // exactly once (evict_first), the fine-grid tiles are re-read by neighbouring chunks (evict_last), so the
 // 14 GB alpha' stream does not push a wedge's ~31 MB of G out of the 126 MB L2
-// FIO_K3_KINNER: K3's per-row column sums with the points innermost (more independent FMA chains)
-#ifndef FIO_K3_KINNER
-#define FIO_K3_KINNER 0
-#endif
 #ifndef FIO_K3_L2HINT
 #define FIO_K3_L2HINT 1
 #endif
@@ -1106,15 +1093,6 @@ __device__ __forceinline__ void bulk_g2s_hint(void* dst, const void* src, unsign
 __device__ __forceinline__ void cp_async16_hint(void* smem, const void* gmem, unsigned long long pol) {
   unsigned s = (unsigned)__cvta_generic_to_shared(smem);
   asm volatile("cp.async.cg.shared.global.L2::cache_hint [%0], [%1], 16, %2;\n" ::"r"(s), "l"(gmem), "l"(pol) : "memory");
-}
-// FIO_K3_L2PF: thread 0 asks the TMA engine to prefetch into L2 the alpha'(t) block FIO_K3_L2PF terms
-// beyond the one it stages (across the chunk boundary into the CTA's next chunk), so the staging copy
-// finds it in L2 -- a deeper pipeline that costs no shared memory
-#ifndef FIO_K3_L2PF
-#define FIO_K3_L2PF 0
-#endif
-__device__ __forceinline__ void bulk_prefetch_l2(const void* src, unsigned bytes) {
-  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;\n" ::"l"(src), "r"(bytes) : "memory");
 }
 // TMA tensor copy: the box at (x, y, z) of a 3-D tensor map into shared memory, completing on `bar`
 __device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, int x, int y, int z,
@@ -1187,7 +1165,6 @@ __global__ void __launch_bounds__(K3Cfg<T2>::BLOCK, NR == 1 ? K3Cfg<T2>::minb(TA
   constexpr int TT = K3Cfg<T2>::TT;
   constexpr int RP = K3Cfg<T2>::RP;
   constexpr int LA = S - TT;  // terms staged ahead of the step being computed
-  constexpr bool kXChunk = FIO_K3_XCHUNK && LA == 1 && TT == 1 && NR == 1;
   static_assert(LA >= TT, "K3 ring: at least one step in flight");
   constexpr int EPC = 16 / (int)sizeof(T2);  // complex elements per 16-byte unit
   constexpr int RPV = 16 / (int)sizeof(Rt);  // row weights per 16-byte unit
@@ -1220,18 +1197,18 @@ __global__ void __launch_bounds__(K3Cfg<T2>::BLOCK, NR == 1 ? K3Cfg<T2>::minb(TA
   auto prefetch_meta = [&](int chn, int buf) {
     if (chn < iw.nchunks && tid == 0) {
       const long long c0 = (long long)chn * BLOCK * P;  // first physical slot of the chunk
-      mbar_expect_tx(bar_m + buf, (unsigned)(kA + kB + kS + (FIO_K3_OFFG ? 0 : kO)));
+      mbar_expect_tx(bar_m + buf, (unsigned)(kA + kB + kS + kO));
       if (FIO_K3_L2HINT) {
         const unsigned long long pf = l2_policy_first();
         bulk_g2s_hint(m_anchor, iw.anchor + 2 * (long long)chn * BLOCK, kA, bar_m + buf, pf);
         bulk_g2s_hint(sbox + kBoxInts * buf, iw.box + (long long)kBoxInts * chn, kB, bar_m + buf, pf);
         bulk_g2s_hint(m_slot + buf * BLOCK * P, iw.slot_x + c0, kS, bar_m + buf, pf);
-        if (!FIO_K3_OFFG) bulk_g2s_hint(m_off, offs + c0, kO, bar_m + buf, pf);
+        bulk_g2s_hint(m_off, offs + c0, kO, bar_m + buf, pf);
       } else {
       bulk_g2s(m_anchor, iw.anchor + 2 * (long long)chn * BLOCK, kA, bar_m + buf);
       bulk_g2s(sbox + kBoxInts * buf, iw.box + (long long)kBoxInts * chn, kB, bar_m + buf);
       bulk_g2s(m_slot + buf * BLOCK * P, iw.slot_x + c0, kS, bar_m + buf);
-      if (!FIO_K3_OFFG) bulk_g2s(m_off, offs + c0, kO, bar_m + buf);
+      bulk_g2s(m_off, offs + c0, kO, bar_m + buf);
       }
     }
   };
@@ -1254,11 +1231,6 @@ __global__ void __launch_bounds__(K3Cfg<T2>::BLOCK, NR == 1 ? K3Cfg<T2>::minb(TA
     const int cpr = bnc / EPC;  // 16-byte units per tile row
     const int tchunks = bnr * cpr;
     const T2* __restrict__ al = alpha + (long long)ch * BLOCK * P;
-    O2 goff[P];  // FIO_K3_OFFG: this thread's offsets, loaded from global memory early in the chunk
-    if (FIO_K3_OFFG) {
-#pragma unroll
-      for (int k = 0; k < P; ++k) goff[k] = offs[(long long)ch * BLOCK * P + k * BLOCK + tid];
-    }
     // this thread's share of every tile copy, fixed for the chunk: source offsets within G_lt (row
     // wrapped mod the fine grid) and destination offsets within the tile
     int csrc[MAXC], cdst[MAXC];
@@ -1297,13 +1269,6 @@ __global__ void __launch_bounds__(K3Cfg<T2>::BLOCK, NR == 1 ? K3Cfg<T2>::minb(TA
     // the chunk's alpha'(t) block is contiguous: one bulk copy (TMA engine) on the stage's mbarrier;
     // the tile (short scattered rows) by cp.async from every thread
     auto issue = [&](int t, bool next_meta) {
-      if (FIO_K3_L2PF > 0 && tid == 0) {  // L2 prefetch of the alpha' block FIO_K3_L2PF terms ahead
-        const int tp = t + FIO_K3_L2PF;
-        if (tp < q)
-          bulk_prefetch_l2(al + tp * nslots, (unsigned)kAl);
-        else if (ch + (int)gridDim.x < iw.nchunks && tp - q < q)
-          bulk_prefetch_l2(alpha + (long long)(ch + gridDim.x) * BLOCK * P + (tp - q) * nslots, (unsigned)kAl);
-      }
       if (t < q) {
         const int st = (int)((gterm + t) % S);
         if (tma) {  // alpha'(t) and the tile (the fixed TMA box at the chunk's origin) on one mbarrier
@@ -1345,32 +1310,10 @@ __global__ void __launch_bounds__(K3Cfg<T2>::BLOCK, NR == 1 ? K3Cfg<T2>::minb(TA
       }
       // the next chunk's tables, issued once every thread has consumed the current offsets/anchors
       if (next_meta) prefetch_meta(ch + gridDim.x, buf ^ 1);
-      // FIO_K3_XCHUNK: during the last term, thread 0 stages term 0 of the CTA's next chunk (alpha'
-      // block and TMA tile, from the next chunk's prefetched box) into the free ring slot, so a chunk
-      // boundary does not expose a full memory latency
-      if constexpr (kXChunk) {
-        if (t == q && tid == 0 && ch + (int)gridDim.x < iw.nchunks && iw.tma) {
-          const int nb = buf ^ 1;
-          mbar_wait(bar_m + nb, (unsigned)((it + 1) >> 1) & 1u);
-          const int* nbx = sbox + kBoxInts * nb;
-          if (nbx[7]) {
-            const int st = (int)((gterm + q) % S);
-            constexpr int kTile = (C64 ? kK3BoxRows64 * kK3BoxCols64 : kK3BoxRows128 * kK3BoxCols128) * sizeof(T2);
-            mbar_expect_tx(bar_a + st, (unsigned)(kAl + kTile));
-            bulk_g2s_hint(aring + st * BLOCK * P, alpha + (long long)(ch + gridDim.x) * BLOCK * P, (unsigned)kAl,
-                          bar_a + st, l2_policy_first());
-            tma_load_3d_hint(tring + st * NR * cap, &tmap, (nbx[2] + kHalo) * (int)(sizeof(T2) / 8), nbx[1], 0,
-                             bar_a + st, l2_policy_last());
-          }
-        }
-      }
       cp_async_commit();
     };
-    if (kXChunk && it > 0 && tma && q > 0)
-      cp_async_commit();  // term 0 was staged during the previous chunk (the running sums' copy group)
-    else
 #pragma unroll
-      for (int u = 0; u < LA; ++u) issue(u, false);
+    for (int u = 0; u < LA; ++u) issue(u, false);
     // weights of this thread's points: phi2 (columns) in registers, phi1 (rows) in shared memory
     const int2 an = m_anchor[tid];
     const int woff = (an.x - br) * sst + (an.y - bc);
@@ -1381,7 +1324,7 @@ __global__ void __launch_bounds__(K3Cfg<T2>::BLOCK, NR == 1 ? K3Cfg<T2>::minb(TA
       Rt o1[P], o2[P];
 #pragma unroll
       for (int k = 0; k < P; ++k) {
-        const O2 o = FIO_K3_OFFG ? goff[k] : m_off[k * BLOCK + tid];
+        const O2 o = m_off[k * BLOCK + tid];
         o1[k] = o.x;
         o2[k] = o.y;
       }
@@ -1483,25 +1426,6 @@ __global__ void __launch_bounds__(K3Cfg<T2>::BLOCK, NR == 1 ? K3Cfg<T2>::minb(TA
               for (int jj = 0; jj < WIN; ++jj) v[r][jj] = win[u][i * sst + jj];
             }
           }
-          if (FIO_K3_KINNER) {  // points innermost: P RP independent column-sum chains per tap
-            T2 rr[P][RP];
-#pragma unroll
-            for (int k = 0; k < P; ++k)
-#pragma unroll
-              for (int r = 0; r < RP; ++r) rr[k][r] = mk<T2>(0, 0);
-#pragma unroll
-            for (int jj = 0; jj < WIN; ++jj)
-#pragma unroll
-              for (int k = 0; k < P; ++k)
-#pragma unroll
-                for (int r = 0; r < RP; ++r)
-                  if (i0 + r < WINR) rr[k][r] = cfma_real(p2[k][jj], v[r][jj], rr[k][r]);
-#pragma unroll
-            for (int k = 0; k < P; ++k)
-#pragma unroll
-              for (int r = 0; r < RP; ++r)
-                if (i0 + r < WINR) F[u][k] = cfma_real(w1[r][k], rr[k][r], F[u][k]);
-          } else {
 #pragma unroll
           for (int k = 0; k < P; ++k) {
             T2 rr[RP];
@@ -1515,7 +1439,6 @@ __global__ void __launch_bounds__(K3Cfg<T2>::BLOCK, NR == 1 ? K3Cfg<T2>::minb(TA
 #pragma unroll
             for (int r = 0; r < RP; ++r)
               if (i0 + r < WINR) F[u][k] = cfma_real(w1[r][k], rr[r], F[u][k]);
-          }
           }
         }
       }
