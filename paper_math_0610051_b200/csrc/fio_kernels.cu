@@ -1379,7 +1379,6 @@ __global__ void __launch_bounds__(K3Cfg<T2>::BLOCK, NR == 1 ? K3Cfg<T2>::minb(TA
       for (int u = 0; u < TT; ++u)
 #pragma unroll
         for (int k = 0; k < P; ++k) F[u][k] = mk<T2>(0, 0);
-#pragma unroll
       // RP window rows per iteration: RP independent column sums per point in flight (latency hiding;
       // the same operations in the same order, so the results do not depend on RP)
 #pragma unroll
@@ -1392,16 +1391,16 @@ __global__ void __launch_bounds__(K3Cfg<T2>::BLOCK, NR == 1 ? K3Cfg<T2>::minb(TA
           if constexpr (PREG) {
 #pragma unroll
             for (int k = 0; k < P; ++k) w1[r][k] = p1r[k][i];
-            continue;
-          }
+          } else {
 #pragma unroll
-          for (int cc = 0; cc < P / RPV; ++cc) {
-            if constexpr (sizeof(Rt) == 4) {
-              const float4 a = *reinterpret_cast<const float4*>(p1s + ((i * (P / RPV) + cc) * BLOCK + tid) * 16);
-              w1[r][4 * cc] = a.x; w1[r][4 * cc + 1] = a.y; w1[r][4 * cc + 2] = a.z; w1[r][4 * cc + 3] = a.w;
-            } else {
-              const double2 a = *reinterpret_cast<const double2*>(p1s + ((i * (P / RPV) + cc) * BLOCK + tid) * 16);
-              w1[r][2 * cc] = a.x; w1[r][2 * cc + 1] = a.y;
+            for (int cc = 0; cc < P / RPV; ++cc) {
+              if constexpr (sizeof(Rt) == 4) {
+                const float4 a = *reinterpret_cast<const float4*>(p1s + ((i * (P / RPV) + cc) * BLOCK + tid) * 16);
+                w1[r][4 * cc] = a.x; w1[r][4 * cc + 1] = a.y; w1[r][4 * cc + 2] = a.z; w1[r][4 * cc + 3] = a.w;
+              } else {
+                const double2 a = *reinterpret_cast<const double2*>(p1s + ((i * (P / RPV) + cc) * BLOCK + tid) * 16);
+                w1[r][2 * cc] = a.x; w1[r][2 * cc + 1] = a.y;
+              }
             }
           }
         }
