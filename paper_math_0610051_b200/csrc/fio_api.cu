@@ -292,6 +292,16 @@ namespace {
 // row sample, rows by pivoting on U; the paper's doubling of r and relative
 // threshold eps are kept).  Produces U (m x q, device, FP64), beta (q x n,
 // device, FP64), q, the final r and the sampled error.
+// Rows sampled for the column pivoting of the separation, per skeleton column (reading R8): a wider row
+// sample lets the pivoting see point classes a small sample misses.  FIO_SEP_ROWS overrides (experiments).
+static int sep_row_oversample() {
+  static const int v = [] {
+    const char* e = std::getenv("FIO_SEP_ROWS");
+    return e ? std::max(1, std::atoi(e)) : kSepRowOversample;
+  }();
+  return v;
+}
+
 fio_status separate_wedge(fio_plan_s& P, const WedgeGeom& g, Rng& rng, cudaStream_t s, DevBuf& dU, DevBuf& dBeta,
                           int& q_out, int& r_out, double& err_out, std::vector<int>& C_out,
                           std::vector<cplx>& Y_out, std::vector<int>& R_out, std::vector<cplx>& Z_out,
@@ -311,7 +321,7 @@ fio_status separate_wedge(fio_plan_s& P, const WedgeGeom& g, Rng& rng, cudaStrea
   int q = 0;
   for (;;) {
     // (1) random row sample R0, candidate columns, A(R0, cand) -> host
-    std::vector<int> R0 = sample_distinct(rng, m, r);
+    std::vector<int> R0 = sample_distinct(rng, m, std::min(m, std::max(r, std::min(sep_row_oversample() * r, kSepRowCap))));
     std::vector<int> candIdx = sample_distinct(rng, n, std::min(n, 64 * r));
     std::vector<int> candCols(candIdx.size());
     for (size_t j = 0; j < candIdx.size(); ++j) candCols[j] = g.members[candIdx[j]];

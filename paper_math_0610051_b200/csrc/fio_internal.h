@@ -54,6 +54,11 @@ constexpr int kK3BlockC128 = FIO_K3_BLOCK128;  // complex128
 // (a ring of 2 TT terms; fio_kernels.cu K3Cfg).  Measured at N = 1024 (K3 ms, TT = 1): complex64 ring
 // of 2 / 3 / 4 terms 2.59 / 2.62 / 2.72, complex128 11.16 / 12.47 / 12.52 -- shallow rings leave room
 // for more CTAs per SM, which hide latency better than a deeper ring.
+// Separation (reading R8): rows sampled for the column pivoting = min(8 r, 512) (at least r).  Measured over
+// the seeded random operators of tests/test_gpu_parity.py (profiles/r02_sep_rows.txt): r rows leave a worst
+// pointwise error of 136 eps (a point class the small sample misses), 8 r rows 22 eps; sum_q, plan time and
+// the apply at N = 1024 are unchanged.
+constexpr int kSepRowOversample = 8, kSepRowCap = 512;
 constexpr int kK3TileCapC64 = FIO_K3_CAP64;     // max cells of a K3 chunk footprint, complex64
 constexpr int kK3TileCapC128 = FIO_K3_CAP128;   // complex128
 constexpr int kHalo = 8;  // periodic column halo on each side of a fine-grid row (K2 writes, K3 reads)

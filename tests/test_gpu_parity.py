@@ -848,3 +848,61 @@ def test_concurrent_handles_on_threads():
         assert len(results[i]) == 8
         for r in results[i]:
             assert np.array_equal(r, refs[i])
+
+
+# ------------------------------------------------------------------ randomized operators (seeded fuzz over the plan's parameter space)
+def _random_operator(seed):
+    """A seeded random member of the phase/amplitude family of include/fio.h: smooth random radii fields
+    c1, c2 (trigonometric polynomials of degree <= 2, values in [0.15, 1.4]), a smooth displacement b,
+    the sign of rho, and a random separable amplitude of rank 0-2 (pxi_k: 1, xi1/|xi| or xi2/|xi|)."""
+    r = np.random.default_rng(1000 + seed)
+    N = int(r.choice([8, 10, 12, 16, 18, 20, 24, 30, 32, 40, 48, 50, 60, 64, 72, 80, 90, 96, 100, 120, 128]))
+    x1, x2 = wl.grid(N)
+
+    def smooth(lo, hi):
+        v = np.zeros((N, N))
+        for m in range(3):
+            for n in range(3):
+                v += r.normal() * np.cos(2 * np.pi * (m * x1 + n * x2) + r.uniform(0, 2 * np.pi)) / (1 + m + n)
+        v = (v - v.min()) / max(v.max() - v.min(), 1e-12)
+        return lo + (hi - lo) * v
+
+    c1 = smooth(r.uniform(0.15, 0.6), r.uniform(0.7, 1.4))
+    c2 = smooth(r.uniform(0.15, 0.6), r.uniform(0.7, 1.4))
+    b1 = b2 = None
+    if r.random() < 0.5:
+        b1, b2 = smooth(-0.05, 0.05), smooth(-0.05, 0.05)
+    K = int(r.integers(0, 3))
+    px = pxi = None
+    if K:
+        xi1, xi2 = wl.freqs(N)
+        rad = np.sqrt(xi1.astype(float) ** 2 + xi2.astype(float) ** 2)
+        choices = [np.ones((N, N)), np.where(rad > 0, xi1 / np.where(rad > 0, rad, 1), 0.0),
+                   np.where(rad > 0, xi2 / np.where(rad > 0, rad, 1), 0.0)]
+        px = np.stack([smooth(0.2, 1.0) * np.exp(1j * smooth(0, 1)) for _ in range(K)]).astype(np.complex128)
+        pxi = np.stack([choices[int(r.integers(0, 3))] for _ in range(K)]).astype(np.complex128)
+    sign = int(r.choice([1, -1]))
+    op = wl.Operator(N, c1, c2, b1, b2, px, pxi, name=f"random{seed}", sign=sign)
+    dtype = "c64" if r.random() < 0.35 else "c128"
+    eps = float(r.choice([1e-4, 1e-5])) if dtype == "c64" else float(r.choice([1e-5, 1e-6, 1e-7, 1e-8]))
+    kw = {}
+    if r.random() < 0.4:
+        kw["n_wedges"] = int(8 * r.integers(1, 5))
+    if r.random() < 0.3:
+        kw["wedge_overlap"] = 0.25
+    return op, dtype, eps, kw, int(r.integers(0, 1 << 30))
+
+
+@pytest.mark.parametrize("seed", range(16))
+def test_randomized_operators_full_grid(seed):
+    # every output point against the direct sum (eq. dfio) for a seeded random operator: grid size (even,
+    # 5-smooth, 8..128), radii fields, displacement, rho sign, separable amplitude rank, dtype, eps,
+    # wedge count and partition all drawn from the seed -- parity must not depend on a lucky configuration
+    op, dtype, eps, kw, fseed = _random_operator(seed)
+    f = wl.white_noise(op.N, fseed % 997, dtype)
+    plan, out = run(op, f, eps=eps, dtype=dtype, **kw)
+    ref = oracle.fio(op, f)
+    rel, mx = _pointwise(out, ref)
+    print(f"random{seed}: N={op.N} {dtype} eps={eps:g} sign={op.sign} K={op.K} b={'yes' if op.b1 is not None else 'no'} "
+          f"{kw} W={plan.info['W']} sum_q={plan.info['sum_q']}: rel l2 {rel:.3e}, max|err|/rms {mx:.3e}")
+    assert rel <= 10 * eps and mx <= 100 * eps, (rel, mx)
