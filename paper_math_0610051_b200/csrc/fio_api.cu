@@ -116,6 +116,7 @@ struct fio_plan_s {
   const std::vector<WedgeFactors>* load = nullptr;   // fio_plan_load: factors read from a file
   uint64_t input_hash = 0;                           // hash of the phase / amplitude arrays
   double eps = 0, es_beta = 0;
+  int low_r2 = 0;  // reading R27: wedge members with |xi|^2 <= low_r2 are always skeleton columns
   fio_opts opts{};
   std::vector<WedgeGeom> geom;
   std::vector<int> owned;
@@ -315,6 +316,16 @@ fio_status separate_wedge(fio_plan_s& P, const WedgeGeom& g, Rng& rng, cudaStrea
   FIO_CUDA(cudaMemcpy(dMembers.p, g.members.data(), sizeof(int) * n, cudaMemcpyHostToDevice));
 
   int r = std::min(std::max(r_start, 4), n);
+  // reading R27: the members of the low-frequency disk |xi|^2 <= low_r2 (where the Bessel amplitude's
+  // regularisation rho_e = max(rho, 1/2) makes the kernel non-smooth) are always skeleton columns and
+  // always certified: a random column sample rarely contains these few frequencies
+  std::vector<int> forced;  // member indices
+  if (P.low_r2 > 0)
+    for (int i = 0; i < n; ++i) {
+      const int k = g.members[i], k1 = k / N, k2 = k - k1 * N;
+      const long long x1 = k1 - (k1 >= N / 2 ? N : 0), x2 = k2 - (k2 >= N / 2 ? N : 0);
+      if (x1 * x1 + x2 * x2 <= P.low_r2) forced.push_back(i);
+    }
   std::vector<int> C;
   std::vector<cplx> V;
   std::vector<double> lam;
@@ -344,6 +355,8 @@ fio_status separate_wedge(fio_plan_s& P, const WedgeGeom& g, Rng& rng, cudaStrea
       std::vector<int> piv = pivoted_columns(nr0, nc0, B, r);
       for (int p : piv) C.push_back(candCols[p]);
     }
+    for (int i : forced)
+      if (std::find(C.begin(), C.end(), g.members[i]) == C.end()) C.push_back(g.members[i]);
     const int rc = (int)C.size();
     if (rc == 0) {
       q = 0;
@@ -508,6 +521,8 @@ fio_status separate_wedge(fio_plan_s& P, const WedgeGeom& g, Rng& rng, cudaStrea
   if (P.opts.certify) {
     std::vector<int> Gam = sample_distinct(rng, m, kCertSamples);
     std::vector<int> Del = sample_distinct(rng, n, kCertSamples);
+    for (int i : forced)
+      if (std::find(Del.begin(), Del.end(), i) == Del.end()) Del.push_back(i);
     const int ng = (int)Gam.size(), nd = (int)Del.size();
     std::vector<int> delCols(nd);
     for (int j = 0; j < nd; ++j) delCols[j] = g.members[Del[j]];
@@ -905,6 +920,13 @@ fio_status build_plan(fio_plan_s& P, const fio_phase* phase, const fio_amplitude
   P.op.sign = phase->rho_sign < 0 ? -1 : 1;
   P.op.amp_kind = amp ? amp->kind : FIO_AMP_SEPARABLE;
   std::vector<double2> a0(NN);
+  if (P.op.amp_kind == FIO_AMP_BESSEL_GRT) {
+    // reading R27: the disk where rho_e = max(rho, 1/2) clamps, |xi| <= 1 / (2 min_x min(c1, c2)), plus one
+    double cmin = 1e300;
+    for (long long x = 0; x < NN; ++x) cmin = std::min(cmin, std::min(std::fabs(phase->c1[x]), std::fabs(phase->c2[x])));
+    const int R = cmin > 1.0 / 30.0 ? (int)std::ceil(0.5 / cmin) + 1 : 16;
+    P.low_r2 = std::min(R, 16) * std::min(R, 16);
+  }
   if (P.op.amp_kind == FIO_AMP_BESSEL_GRT) {
     // a(x, 0) at rho_e = 1/2 (reading R22): (J0(pi) + s i Y0(pi)) e^{-s i pi} / (4 pi), x-independent
     const double PI = 3.14159265358979323846;
