@@ -947,3 +947,24 @@ def test_randomized_operators_large_sampled(seed):
     print(f"random_large{seed}: N={N} {dtype} eps={eps:g} sign={opL.sign} amp={amp} {kw} W={plan.info['W']} "
           f"sum_q={plan.info['sum_q']}: rel l2 {rel:.3e}, max|err|/rms {mx:.3e}")
     assert rel <= 10 * eps and mx <= _pointwise_bar(N, eps, kw), (rel, mx)
+
+
+@pytest.mark.parametrize("seed", range(16))
+def test_randomized_operators_adjoint(seed):
+    # NEXT-1 on the seeded random family: the GPU adjoint against the oracle's L* on
+    # the full grid, and exact pairing <L~f, g> = <f, L~* g> with the GPU forward of the same plan
+    op, dtype, eps, kw, fseed = _random_operator(seed)
+    N = op.N
+    tdt = torch.complex64 if dtype == "c64" else torch.complex128
+    g = wl.white_noise(N, (fseed + 1) % 997, dtype)
+    f = wl.white_noise(N, (fseed + 2) % 997, dtype)
+    plan = make_plan(op, eps, dtype, **kw)
+    Lsg = plan.apply_adjoint(torch.from_numpy(g).to(DEV, tdt)).cpu().numpy().astype(np.complex128)
+    Lf = plan.apply(torch.from_numpy(f).to(DEV, tdt)).cpu().numpy().astype(np.complex128)
+    rel = oracle.rel_l2(Lsg, adjoint_ref(op, g))
+    lhs, rhs = np.vdot(g, Lf), np.vdot(Lsg, f)
+    pair = abs(lhs - rhs) / (np.linalg.norm(f) * np.linalg.norm(g))
+    ptol = 1e-5 if dtype == "c64" else 1e-12
+    print(f"random adjoint {seed}: N={N} {dtype} eps={eps:g} {kw}: rel l2 vs oracle {rel:.3e}, pairing {pair:.2e}")
+    assert rel <= 10 * eps, rel
+    assert pair <= ptol * N, pair
