@@ -968,3 +968,33 @@ def test_randomized_operators_adjoint(seed):
     print(f"random adjoint {seed}: N={N} {dtype} eps={eps:g} {kw}: rel l2 vs oracle {rel:.3e}, pairing {pair:.2e}")
     assert rel <= 10 * eps, rel
     assert pair <= ptol * N, pair
+
+
+@pytest.mark.parametrize("seed", range(8))
+def test_randomized_operators_api_consistency(seed, tmp_path):
+    # every entry point of include/fio.h on the seeded random family agrees with fio_apply: fio_apply_batch
+    # (3 inputs) and fio_apply_host_stream bit for bit, a saved-and-loaded plan bit for bit, and a 3-way
+    # wedge sharding (per-rank N x N partials, no communicator) summing to the 1-rank result (L = sum_l L_l,
+    # PAPER.md:236-241) to rounding
+    op, dtype, eps, kw, fseed = _random_operator(seed)
+    N = op.N
+    tdt = torch.complex64 if dtype == "c64" else torch.complex128
+    fs = torch.stack([torch.from_numpy(wl.white_noise(N, (fseed + i) % 997, dtype)).to(tdt) for i in range(3)])
+    plan = make_plan(op, eps, dtype, **kw)
+    single = [plan.apply(fs[i].to(DEV)).cpu() for i in range(3)]
+    batch = plan.apply_batch(fs.to(DEV)).cpu()
+    hin, hout = fs.clone().pin_memory(), torch.empty_like(fs).pin_memory()
+    plan.apply_host_stream(hin, hout)
+    for i in range(3):
+        assert torch.equal(batch[i], single[i]), ("batch", i)
+        assert torch.equal(hout[i], single[i]), ("host_stream", i)
+    path = str(tmp_path / "plan.fio")
+    plan.save(path)
+    loaded = make_plan(op, eps, dtype, load=path, **kw)
+    assert torch.equal(loaded.apply(fs[0].to(DEV)).cpu(), single[0])
+    acc = torch.zeros_like(single[0], dtype=torch.complex128)
+    for r in range(3):
+        acc += make_plan(op, eps, dtype, rank=r, nranks=3, **kw).apply(fs[0].to(DEV)).cpu().to(torch.complex128)
+    rel = oracle.rel_l2(acc.numpy(), single[0].numpy())
+    print(f"random api {seed}: N={N} {dtype} eps={eps:g} {kw}: sharded-sum vs 1 rank {rel:.2e}")
+    assert rel <= (1e-5 if dtype == "c64" else 1e-12), rel
