@@ -998,3 +998,17 @@ def test_randomized_operators_api_consistency(seed, tmp_path):
     rel = oracle.rel_l2(acc.numpy(), single[0].numpy())
     print(f"random api {seed}: N={N} {dtype} eps={eps:g} {kw}: sharded-sum vs 1 rank {rel:.2e}")
     assert rel <= (1e-5 if dtype == "c64" else 1e-12), rel
+
+
+@pytest.mark.parametrize("N,dtype,eps", [(1000, "c128", 1e-6), (1080, "c64", 1e-4), (1250, "c128", 1e-6),
+                                         (1536, "c64", 1e-5)])
+def test_non_power_of_two_headline_sizes(N, dtype, eps):
+    # 5-smooth, non-power-of-two grids near the headline size (K0's mixed radices 3 and 5, K1's general
+    # f-hat index wrap instead of the power-of-two mask): GRT phase, 1024 sampled points vs the direct sum
+    op = wl.grt_operator(N)
+    f = wl.white_noise(N, 31, dtype)
+    plan, out = run(op, f, eps=eps, dtype=dtype)
+    pts = wl.sample_points(N, 1024, 5)
+    rel, mx = _pointwise(out.ravel()[pts], oracle.fio(op, f, pts=pts))
+    print(f"N={N} {dtype} eps={eps:g}: W {plan.info['W']} sum_q {plan.info['sum_q']}: rel l2 {rel:.3e}, max {mx:.3e}")
+    assert rel <= 10 * eps and mx <= 100 * eps, (rel, mx)
