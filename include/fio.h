@@ -126,6 +126,10 @@ typedef struct {
                          column step -- r columns drawn uniformly, r doubled until
                          q <= r/3; rows as in the default.  Same operator; more
                          plan time. */
+  int allgather;      /* 0: with a communicator every rank receives its (N/R) x N row slab.  1: every rank
+                         receives the full N x N result -- the reduce-scatter into the rank's rows of
+                         Lf_dev is followed by an in-place NCCL all-gather on the same stream (SURVEY.md
+                         8(b) ownership).  Requires nccl_id (FIO_EINVAL without it). */
 } fio_opts;
 
 #define FIO_NCCL_ID_BYTES 128
@@ -155,6 +159,8 @@ fio_status fio_plan(fio_handle* out, int N, const fio_phase* phase, const fio_am
  *    (N/R) x N array -- after the wedge partials of all ranks are summed by an
  *    NCCL reduce-scatter on `stream` (L = sum_l L_l; the
  *    collective: every rank must call fio_apply);
+ *  - the same with opts.allgather = 1: the full N x N L f on every rank (the
+ *    reduce-scatter writes this rank's rows, an in-place all-gather the rest);
  *  - nranks > 1 without a communicator: this rank's N x N partial sum over its
  *    own wedges (the DC term on rank 0 only), for the caller to sum.
  * stream: a cudaStream_t (NULL = legacy default stream).  Asynchronous on

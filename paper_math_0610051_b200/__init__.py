@@ -63,7 +63,8 @@ class _Opts(ctypes.Structure):
                 ("nufft_beta", ctypes.c_double), ("seed", ctypes.c_uint64), ("device", ctypes.c_int),
                 ("rank", ctypes.c_int), ("nranks", ctypes.c_int), ("r_init", ctypes.c_int),
                 ("r_max", ctypes.c_int), ("certify", ctypes.c_int), ("skeleton", ctypes.c_int),
-                ("nccl_id", ctypes.c_void_p), ("wedge_overlap", ctypes.c_double), ("paper_accept", ctypes.c_int)]
+                ("nccl_id", ctypes.c_void_p), ("wedge_overlap", ctypes.c_double), ("paper_accept", ctypes.c_int),
+                ("allgather", ctypes.c_int)]
 
 
 class _Info(ctypes.Structure):
@@ -210,7 +211,7 @@ class Plan:
                  r_init: int = 32, r_max: int = 512, certify: bool = True, rho_sign: int = 1,
                  amplitude: str = "separable", skeleton: bool = False, load: Optional[str] = None,
                  group=None, nccl_id: Optional[bytes] = None, wedge_overlap: float = 0.0,
-                 paper_accept: bool = False):
+                 paper_accept: bool = False, allgather: bool = False):
         import torch
         if not torch.cuda.is_available():
             raise FioError(-3, "no CUDA device: the FIO apply runs only on the GPU (no CPU fallback)")
@@ -241,6 +242,7 @@ class Plan:
         o.skeleton = int(bool(skeleton))
         o.wedge_overlap = float(wedge_overlap)
         o.paper_accept = int(bool(paper_accept))
+        o.allgather = int(bool(allgather))  # with a communicator: the full N x N on every rank
         # wedge-sharded with a communicator: the id comes from rank 0 (broadcast over `group`, or given)
         if nranks > 1 and nccl_id is None and group is not None:
             nccl_id = broadcast_nccl_id(group)
@@ -262,7 +264,7 @@ class Plan:
         self.eps = eps
         self.rank, self.nranks = int(rank), int(nranks)
         self.torch_dtype = torch.complex64 if self.c64 else torch.complex128
-        self.out_rows = self.info["out_rows"]  # N, or N / nranks with a communicator (row slab)
+        self.out_rows = self.info["out_rows"]  # N, or N / nranks with a communicator (row slab, no allgather)
 
     def save(self, path: str) -> None:
         """fio_plan_save: write this plan's separation (per wedge C, V S^-1, R, U_R^+) to path;

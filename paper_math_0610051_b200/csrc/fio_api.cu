@@ -170,7 +170,17 @@ struct fio_plan_s {
   int prof_cap = 0, prof_n = 0;
 
   size_t elem_bytes() const { return c64 ? sizeof(float2) : sizeof(double2); }
-  int out_rows() const { return comm ? N / opts.nranks : N; }  // rows of what fio_apply writes
+  int out_rows() const { return comm && !opts.allgather ? N / opts.nranks : N; }  // rows fio_apply writes
+  // A6: the sum over ranks of this rank's N x N partial into `out` -- its row slab (reduce-scatter),
+  // or with opts.allgather the full N x N (reduce-scatter into this rank's rows of `out`, then an
+  // in-place all-gather), both on stream s
+  fio_status sum_ranks(const void* part_b, void* out, cudaStream_t s) const {
+    const size_t slab = 2 * (size_t)(N / opts.nranks) * N;  // reals per rank
+    if (!opts.allgather) return comm_reduce_scatter(comm, part_b, out, slab, c64, s);
+    void* mine = static_cast<char*>(out) + (c64 ? sizeof(float) : sizeof(double)) * slab * (size_t)opts.rank;
+    fio_status st = comm_reduce_scatter(comm, part_b, mine, slab, c64, s);
+    return st != FIO_OK ? st : comm_all_gather(comm, out, opts.rank, slab, c64, s);
+  }
   // comm: make room for nrhs N x N partials (synchronizes `s` before freeing a smaller buffer)
   cudaError_t ensure_part(int nrhs, cudaStream_t s) {
     if (nrhs <= part_cap) return cudaSuccess;
@@ -1622,6 +1632,14 @@ static fio_status plan_impl(fio_handle* out, int N, const fio_phase* phase, cons
     set_error("fio_plan: with a communicator nranks must divide N (row slabs)");
     return FIO_EINVAL;
   }
+  if (o.allgather != 0 && o.allgather != 1) {
+    set_error("fio_plan: allgather must be 0 or 1");
+    return FIO_EINVAL;
+  }
+  if (o.allgather && !o.nccl_id) {
+    set_error("fio_plan: allgather needs a communicator (nccl_id)");
+    return FIO_EINVAL;
+  }
   if (o.r_init == 0) o.r_init = 32;
   if (o.r_max == 0) o.r_max = 512;
   FIO_GUARD(o.device)
@@ -1701,7 +1719,7 @@ fio_status fio_apply(fio_handle h, const void* f_dev, void* Lf_dev, void* stream
   FIO_CUDA(h->ensure_part(1, s));
   FIO_CUDA(enqueue_apply(a, h->c64, f_dev, h->part, s, &launches, ev));
   h->launches = launches;
-  return comm_reduce_scatter(h->comm, h->part, Lf_dev, 2 * (size_t)h->out_rows() * h->N, h->c64, s);
+  return h->sum_ranks(h->part, Lf_dev, s);
 }
 
 fio_status fio_apply_batch(fio_handle h, int nrhs, const void* f_dev, void* Lf_dev, void* stream) {
@@ -1745,8 +1763,7 @@ fio_status fio_apply_batch(fio_handle h, int nrhs, const void* f_dev, void* Lf_d
   FIO_CUDA(enqueue_apply_batch(args.data(), nrhs, h->c64, f_dev, h->part, s, &launches));
   const size_t slab = (size_t)h->out_rows() * h->N;
   for (int b = 0; b < nrhs; ++b) {
-    fio_status st = comm_reduce_scatter(h->comm, static_cast<char*>(h->part) + cs * NN * b,
-                                        static_cast<char*>(Lf_dev) + cs * slab * b, 2 * slab, h->c64, s);
+    fio_status st = h->sum_ranks(static_cast<char*>(h->part) + cs * NN * b, static_cast<char*>(Lf_dev) + cs * slab * b, s);
     if (st != FIO_OK) return st;
   }
   return FIO_OK;
@@ -1771,7 +1788,7 @@ fio_status fio_apply_adjoint(fio_handle h, const void* g_dev, void* out_dev, voi
   }
   FIO_CUDA(h->ensure_part(1, s));
   FIO_CUDA(enqueue_adjoint(a, h->c64, g_dev, h->part, s, &launches));
-  return comm_reduce_scatter(h->comm, h->part, out_dev, 2 * (size_t)h->out_rows() * h->N, h->c64, s);
+  return h->sum_ranks(h->part, out_dev, s);
 }
 
 fio_status fio_apply_host(fio_handle h, const void* f_host, void* Lf_host, void* stream) {

@@ -24,6 +24,7 @@ struct NcclApi {
   ncclResult_t (*comm_destroy)(ncclComm_t) = nullptr;
   ncclResult_t (*reduce_scatter)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
                                  cudaStream_t) = nullptr;
+  ncclResult_t (*all_gather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t, cudaStream_t) = nullptr;
   const char* (*error_string)(ncclResult_t) = nullptr;
 };
 
@@ -42,8 +43,9 @@ const NcclApi& api() {
     a.comm_init_rank = reinterpret_cast<decltype(a.comm_init_rank)>(dlsym(h, "ncclCommInitRank"));
     a.comm_destroy = reinterpret_cast<decltype(a.comm_destroy)>(dlsym(h, "ncclCommDestroy"));
     a.reduce_scatter = reinterpret_cast<decltype(a.reduce_scatter)>(dlsym(h, "ncclReduceScatter"));
+    a.all_gather = reinterpret_cast<decltype(a.all_gather)>(dlsym(h, "ncclAllGather"));
     a.error_string = reinterpret_cast<decltype(a.error_string)>(dlsym(h, "ncclGetErrorString"));
-    a.ok = a.get_unique_id && a.comm_init_rank && a.comm_destroy && a.reduce_scatter && a.error_string;
+    a.ok = a.get_unique_id && a.comm_init_rank && a.comm_destroy && a.reduce_scatter && a.all_gather && a.error_string;
     if (!a.ok) a.why = "libnccl.so.2 lacks a required symbol";
   });
   return a;
@@ -93,6 +95,15 @@ fio_status comm_reduce_scatter(void* comm, const void* part, void* slab, size_t 
   ncclResult_t r = api().reduce_scatter(part, slab, slab_reals, c64 ? ncclFloat32 : ncclFloat64, ncclSum,
                                         static_cast<ncclComm_t>(comm), s);
   if (r != ncclSuccess) return nccl_fail("ncclReduceScatter", r);
+  return FIO_OK;
+}
+
+fio_status comm_all_gather(void* comm, void* full, int rank, size_t slab_reals, bool c64, cudaStream_t s) {
+  const size_t rb = c64 ? sizeof(float) : sizeof(double);
+  const void* mine = static_cast<const char*>(full) + rb * slab_reals * (size_t)rank;  // in place (NCCL)
+  ncclResult_t r = api().all_gather(mine, full, slab_reals, c64 ? ncclFloat32 : ncclFloat64,
+                                    static_cast<ncclComm_t>(comm), s);
+  if (r != ncclSuccess) return nccl_fail("ncclAllGather", r);
   return FIO_OK;
 }
 

@@ -16,5 +16,7 @@ void comm_destroy(void* comm);
 // sum over ranks of `part` (nranks * slab_reals reals), rank r keeps reals [r slab_reals, (r+1) slab_reals)
 fio_status comm_reduce_scatter(void* comm, const void* part, void* slab, size_t slab_reals, bool c64,
                                cudaStream_t s);
+// in-place all-gather: rank r's slab_reals reals at full + r slab_reals are copied to every rank
+fio_status comm_all_gather(void* comm, void* full, int rank, size_t slab_reals, bool c64, cudaStream_t s);
 
 }  // namespace fio

@@ -55,6 +55,34 @@ def test_one_rank_communicator_matches_plain_apply(dtype, eps):
     assert oracle.rel_l2(gb.cpu().numpy(), ga.cpu().numpy()) <= 1e-5  # atomics: last bits may differ
 
 
+@pytest.mark.parametrize("dtype,eps", [("c128", 1e-6), ("c64", 1e-4)])
+def test_one_rank_communicator_allgather_matches_plain_apply(dtype, eps):
+    # opts.allgather (include/fio.h): reduce-scatter into this rank's rows, then an in-place NCCL
+    # all-gather; with one rank both collectives are copies and the result is the plain apply's
+    N = 96
+    op = wl.grt_operator(N)
+    tdt = torch.complex64 if dtype == "c64" else torch.complex128
+    plain = _plan(op, eps, dtype, device=0)
+    comm = _plan(op, eps, dtype, device=0, nccl_id=fio.nccl_unique_id(), allgather=True)
+    assert comm.info["has_comm"] == 1 and comm.out_rows == N
+    f = torch.from_numpy(wl.white_noise(N, 4, dtype)).to("cuda:0", tdt)
+    a = plain.apply(f)
+    b = torch.full_like(a, float("nan"))
+    comm.apply(f, out=b)
+    torch.cuda.synchronize()
+    assert torch.equal(a, b)
+    assert oracle.rel_l2(b.cpu().numpy(), oracle.fio(op, f.cpu().numpy().astype(np.complex128))) <= 10 * eps
+    fb = torch.stack([f, 2 * f, f])
+    ob = comm.apply_batch(fb)
+    assert torch.equal(ob[0], a) and torch.equal(ob[1], plain.apply(2 * f)) and torch.equal(ob[2], a)
+    hin = f.cpu().pin_memory()
+    hout = torch.empty_like(hin).pin_memory()
+    comm.apply_host(hin, hout)
+    assert torch.equal(hout, a.cpu())
+    ga, gb = plain.apply_adjoint(f), comm.apply_adjoint(f)
+    assert oracle.rel_l2(gb.cpu().numpy(), ga.cpu().numpy()) <= 1e-5
+
+
 # ---------------------------------------------------------------- >= 2 GPUs
 def _check_slab(op, f, slab, rank, world, pts_all):
     N = op.N
@@ -81,6 +109,12 @@ def _proc(rank, world, port, N, q):
         plan = _plan(op, device=rank, rank=rank, nranks=world, group=dist.group.WORLD)
         slab = plan.apply(torch.from_numpy(f).to(f"cuda:{rank}")).cpu().numpy()
         err = _check_slab(op, f, slab, rank, world, wl.sample_points(N, 4096, 1))
+        if N <= 256:  # the all-gather option: every rank holds the full Lf
+            full = _plan(op, device=rank, rank=rank, nranks=world, group=dist.group.WORLD, allgather=True)
+            Lf = full.apply(torch.from_numpy(f).to(f"cuda:{rank}")).cpu().numpy()
+            r0, r1 = fio.row_slab(N, world, rank)
+            assert Lf.shape == (N, N) and np.array_equal(Lf[r0:r1], slab)
+            err = max(err, oracle.rel_l2(Lf, oracle.fio(op, f)))
         q.put((rank, err, plan.info["n_owned"]))
     except Exception as e:  # pragma: no cover - reported to the parent
         q.put((rank, repr(e), -1))

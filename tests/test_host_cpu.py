@@ -139,3 +139,45 @@ def test_product_partition_weights_match_oracle(W, ov):
                 if l >= 0:
                     exp_[l] = 1.0
                 assert np.array_equal(got, exp_)
+
+
+def test_ctypes_structs_match_the_c_abi(tmp_path):
+    # the binding's ctypes mirrors of fio_opts / fio_phase / fio_amplitude / fio_info must have the C
+    # layout (fio_plan copies the whole fio_opts: a missing trailing field would be read as garbage)
+    import ctypes
+    structs = {"fio_opts": fio._Opts, "fio_phase": fio._Phase, "fio_amplitude": fio._Amp,
+               "fio_info": fio._Info}
+    lines = ['#include <stdio.h>', '#include <stddef.h>', '#include "fio.h"', "int main(void) {"]
+    for cname, py in structs.items():
+        lines.append(f'  printf("{cname} %zu\\n", sizeof({cname}));')
+        for fname, _ in py._fields_:
+            lines.append(f'  printf("{cname}.{fname} %zu\\n", offsetof({cname}, {fname}));')
+    lines += ["  return 0;", "}"]
+    src = tmp_path / "abi.c"
+    src.write_text("\n".join(lines))
+    exe = tmp_path / "abi"
+    subprocess.run(["gcc", "-std=c11", "-I", os.path.join(ROOT, "include"), str(src), "-o", str(exe)], check=True)
+    got = dict(l.rsplit(" ", 1) for l in subprocess.run([str(exe)], capture_output=True, text=True,
+                                                          check=True).stdout.splitlines())
+    for cname, py in structs.items():
+        assert int(got[cname]) == ctypes.sizeof(py), cname
+        for fname, _ in py._fields_:
+            assert int(got[f"{cname}.{fname}"]) == getattr(py, fname).offset, (cname, fname)
+
+
+def test_allgather_option_is_validated_before_any_device_work():
+    # fio_opts.allgather (include/fio.h): only with a communicator, only 0 or 1 -- FIO_EINVAL otherwise
+    import ctypes
+    lib = fio.load_library()
+    N = 16
+    c = np.full(N * N, 0.5)
+    ph = fio._Phase(c.ctypes.data, c.ctypes.data, None, None, 1)
+    amp = fio._Amp(0, None, None, 0)
+    for val, msg in [(1, b"needs a communicator"), (2, b"must be 0 or 1")]:
+        o = fio._Opts()
+        lib.fio_default_opts(ctypes.byref(o))
+        assert o.allgather == 0
+        o.allgather = val
+        h = ctypes.c_void_p()
+        st = lib.fio_plan(ctypes.byref(h), N, ctypes.byref(ph), ctypes.byref(amp), 1e-6, ctypes.byref(o))
+        assert st == -1 and msg in lib.fio_last_error() and not h.value
