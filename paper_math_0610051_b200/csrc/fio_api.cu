@@ -1275,7 +1275,7 @@ fio_status build_plan(fio_plan_s& P, const fio_phase* phase, const fio_amplitude
     for (int t = 0; t < w.q; ++t) {
       for (int i = 0; i < w.n1; i += rows) {
         jr.push_back({(int)wi, t, i, std::min(rows, w.n1 - i), w.fft2, {0, 0, 0}});
-        smem_row = std::max(smem_row, sr * std::min(rows, w.n1 - i));
+        smem_row = std::max(smem_row, k1_row_bytes(w.n2f, c64) * std::min(rows, w.n1 - i));
       }
       for (int c = 0; c < w.n2f; c += cols) {
         jc.push_back({(int)wi, t, c, std::min(cols, w.n2f - c), w.fft1, {0, 0, 0}});

@@ -519,6 +519,11 @@ __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_gr
 #ifndef FIO_K1_THREADS
 #define FIO_K1_THREADS 256
 #endif
+// K1's smem row stride of the last FFT stage (odd: conflict-free transposed read-out; the plan sizes
+// K1's shared memory for L + 1 per row, k1_row_bytes)
+#ifndef FIO_K1_LD
+#define FIO_K1_LD(L) ((L) | 1)
+#endif
 #ifndef FIO_K2_THREADS
 #define FIO_K2_THREADS 256
 #endif
@@ -645,11 +650,13 @@ __device__ __forceinline__ void stage_dispatch(int R, int L, int Ns, const FastD
 }
 
 // Returns the shared buffer holding the result when the last stage writes to shared memory
-// (store_last_to_smem), else nullptr.  Ends with __syncthreads().
+// (store_last_to_smem; sequence stride last_ld >= L there, 0 = L), else nullptr.  Ends with
+// __syncthreads().
 template <typename T2, class LoadFirst, class StoreLast>
 __device__ T2* smem_fft_io(T2* a, T2* b, const FftLen& fl, const T2* tw, int nseq, int sign, LoadFirst load_first,
-                           StoreLast store_last, bool store_last_to_smem) {
+                           StoreLast store_last, bool store_last_to_smem, int last_ld = 0) {
   const int L = fl.L;
+  const int ldl = last_ld > 0 ? last_ld : L;
   int Ns = 1;
   T2* in = a;   // unused by stage 0 (reads through load_first)
   T2* out = b;
@@ -658,12 +665,17 @@ __device__ T2* smem_fft_io(T2* a, T2* b, const FftLen& fl, const T2* tw, int nse
     const bool first = st == 0, last = st == fl.nst - 1;
     auto sload = [&](int sq, int e) { return in[sq * L + e]; };
     auto sstore = [&](int sq, int e, T2 v) { out[sq * L + e] = v; };
+    auto sstore_ld = [&](int sq, int e, T2 v) { out[sq * ldl + e] = v; };  // the last stage, in smem
     if (first && last && !store_last_to_smem)
       stage_dispatch<T2>(R, L, Ns, fl.div_nb[st], fl.div_ns[st], tw, nseq, sign, load_first, store_last);
+    else if (first && last)
+      stage_dispatch<T2>(R, L, Ns, fl.div_nb[st], fl.div_ns[st], tw, nseq, sign, load_first, sstore_ld);
     else if (first)
       stage_dispatch<T2>(R, L, Ns, fl.div_nb[st], fl.div_ns[st], tw, nseq, sign, load_first, sstore);
     else if (last && !store_last_to_smem)
       stage_dispatch<T2>(R, L, Ns, fl.div_nb[st], fl.div_ns[st], tw, nseq, sign, sload, store_last);
+    else if (last)
+      stage_dispatch<T2>(R, L, Ns, fl.div_nb[st], fl.div_ns[st], tw, nseq, sign, sload, sstore_ld);
     else
       stage_dispatch<T2>(R, L, Ns, fl.div_nb[st], fl.div_ns[st], tw, nseq, sign, sload, sstore);
     __syncthreads();
@@ -747,8 +759,11 @@ __global__ void __launch_bounds__(FIO_K1_THREADS) k_rowpass(int N, const WedgeDe
   const WedgeDev& w = wedges[job.w];
   const FftLen& fl = ffts[job.fft];
   const int L = fl.L, n1 = w.n1, n2 = w.n2, cnt = job.count;
+  // the last stage writes its rows with an odd stride: the transposed read-out below (consecutive
+  // threads: consecutive rows, same column) is then free of shared-memory bank conflicts
+  const int ld = FIO_K1_LD(L);
   T2* a = reinterpret_cast<T2*>(smem_raw);
-  T2* b = a + cnt * L;
+  T2* b = a + cnt * ld;
   const T2* bet = betas[job.w] + ((long long)job.t * n1 + job.start) * n2;
   {  // the job's beta' rows are one contiguous block of cnt n2 elements: stage it in the first buffer
     const int nel = cnt * n2;
@@ -784,12 +799,12 @@ __global__ void __launch_bounds__(FIO_K1_THREADS) k_rowpass(int N, const WedgeDe
     return out;
   };
   auto no_store = [](int, int, T2) {};
-  T2* res = smem_fft_io<T2>(a, b, fl, tw + fl.tw_off, cnt, +1, load_h, no_store, true);
+  T2* res = smem_fft_io<T2>(a, b, fl, tw + fl.tw_off, cnt, +1, load_h, no_store, true, ld);
   T2* dst = p1 + w.p1_off + (long long)job.t * L * n1 + job.start;
   const FastDiv dc = make_fastdiv_dev((unsigned)cnt);
   for (int idx = threadIdx.x; idx < cnt * L; idx += blockDim.x) {  // consecutive threads: consecutive i1
     const int j2 = fdiv(idx, dc), r = idx - j2 * cnt;
-    dst[(long long)j2 * n1 + r] = res[r * L + j2];
+    dst[(long long)j2 * n1 + r] = res[r * ld + j2];
   }
 }
 
@@ -2023,6 +2038,8 @@ cudaError_t enqueue_adjoint(const ApplyArgs& a, bool c64, const void* g, void* o
   if (c64) return enqueue_adjoint_t<float2>(a, (const float2*)g, (float2*)out, s, launches);
   return enqueue_adjoint_t<double2>(a, (const double2*)g, (double2*)out, s, launches);
 }
+
+size_t k1_row_bytes(int L, bool c64) { return fft_seq_bytes(L + 1, c64); }
 
 size_t fft_seq_bytes(int L, bool c64) {
   return c64 ? 2 * (size_t)L * sizeof(float2)

@@ -127,6 +127,7 @@ cudaError_t enqueue_adjoint(const ApplyArgs& a, bool c64, const void* g, void* o
 
 // Dynamic shared memory needed by the FFT passes for one sequence of length L.
 size_t fft_seq_bytes(int L, bool c64);
+size_t k1_row_bytes(int L, bool c64);  // K1 shared memory per row (two buffers of stride L + 1)
 cudaError_t configure_kernels(size_t smem_bytes);
 // Opt the K3 instance for (taps, dtype) into the dynamic shared memory of the plan's largest chunk
 // footprint, on the current device (per device: every plan configures its own device).
